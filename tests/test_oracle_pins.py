@@ -1,0 +1,407 @@
+"""Pins of the CPU oracle (oracle/oracle.c) to things other than itself.
+
+Each test names what fixes the expected value: a worked example printed in the
+reference (tests/golden), an independent algorithm from the paper (Eq. 1-2 by
+path enumeration, the minimax Floyd-Warshall variant, the MST-path property),
+a library special case (scipy single linkage + cophenet), exact rational
+arithmetic, or an invariant of the mathematics.  CPU only.
+"""
+import itertools
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import generators as G
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def assert_bit_equal(a, b):
+    a = np.asarray(a, np.float32)
+    b = np.asarray(b, np.float32)
+    assert a.shape == b.shape
+    # canonical +0 everywhere on both sides (reading Q5): compare bits exactly
+    diff = np.nonzero(bits(a) != bits(b))
+    assert diff[0].size == 0, f"{diff[0].size} mismatches, first at {diff[0][0]},{diff[1][0] if len(diff) > 1 else ''}: {a[tuple(x[0] for x in diff)]} vs {b[tuple(x[0] for x in diff)]}"
+
+
+REGIMES = ["uniform", "ties", "ints255", "negative", "signed_zero"]
+
+
+# --------------------------------------------------------------------------
+# worked examples printed in the reference
+# --------------------------------------------------------------------------
+def test_worked_examples_weights():
+    g = json.load(open(GOLD))
+    for c in g["cases"]:
+        W = np.array(c["W"], np.float32)
+        M = oracle.appd_weights(W, c["sense"])
+        assert_bit_equal(M, np.array(c["M"], np.float32))
+        assert_bit_equal(oracle.floyd(W, c["sense"]), np.array(c["M"], np.float32))
+        if W.shape[0] <= 9:
+            assert_bit_equal(oracle.brute(W, c["sense"]), np.array(c["M"], np.float32))
+        if "mst" in c:
+            eu, ev, ew = oracle.prim_weights(W, 1)
+            got = sorted((min(u, v), max(u, v), float(w)) for u, v, w in zip(eu, ev, ew))
+            assert got == sorted((a, b, float(w)) for a, b, w in c["mst"])
+
+
+def test_worked_examples_points():
+    g = json.load(open(GOLD))
+    for c in g["points"]:
+        X = np.array(c["X"], np.float32)
+        assert_bit_equal(oracle.points_weights(X), np.array(c["W"], np.float32))
+        assert_bit_equal(oracle.appd_points(X), np.array(c["M"], np.float32))
+
+
+def test_write_counts_printed():
+    g = json.load(open(GOLD))
+    for c in g["write_counts"]:
+        W = G.random_weights(c["n"], 3, "uniform")
+        _, st = oracle.appd_weights(W, 1, with_stats=True)
+        assert st["writes"] == c["writes"]
+
+
+# --------------------------------------------------------------------------
+# Eq. 1-2 by path enumeration (the definition itself)
+# --------------------------------------------------------------------------
+def _py_brute(W, sense):
+    """Eq. 1-2 transcribed in Python over itertools.permutations (n <= 6)."""
+    n = W.shape[0]
+    M = np.zeros((n, n), np.float32)
+    for i in range(n):
+        for j in range(n):
+            if i == j:
+                continue
+            others = [k for k in range(n) if k not in (i, j)]
+            phi = []
+            for r in range(len(others) + 1):
+                for mid in itertools.permutations(others, r):
+                    p = (i, *mid, j)
+                    ws = [W[p[t], p[t + 1]] + np.float32(0) for t in range(len(p) - 1)]
+                    phi.append(max(ws) if sense > 0 else min(ws))
+            M[i, j] = min(phi) if sense > 0 else max(phi)
+    return M
+
+
+def test_c_brute_equals_python_brute():
+    """The C path enumerator is itself checked against an itertools transcription of Eq. 1-2."""
+    for n in range(1, 7):
+        for seed in range(4):
+            for kind in REGIMES:
+                W = G.random_weights(n, seed, kind)
+                for sense in (1, -1):
+                    assert_bit_equal(oracle.brute(W, sense), _py_brute(W, sense))
+
+
+@pytest.mark.parametrize("kind", REGIMES + ["huge"])
+def test_algo4_equals_brute_force(kind):
+    """Algorithm 4 == Eq. 2 on every n <= 8 (50 seeds at n = 8)."""
+    for n in range(1, 9):
+        seeds = range(50) if n == 8 else range(8)
+        for seed in seeds:
+            W = G.random_weights(n, seed, kind)
+            for sense in (1, -1):
+                want = oracle.brute(W, sense)
+                assert_bit_equal(oracle.appd_weights(W, sense), want)
+                assert_bit_equal(oracle.floyd(W, sense), want)
+
+
+# --------------------------------------------------------------------------
+# the paper's O(n^3) Floyd-Warshall variant and the MST-path property
+# --------------------------------------------------------------------------
+def test_algo4_equals_floyd_and_mst_path_200_seeds():
+    """>= 200 seeded graphs, n in 2..64, both senses, bit-exact."""
+    rs = np.random.default_rng(7)
+    for seed in range(200):
+        n = int(rs.integers(2, 65))
+        kind = REGIMES[seed % len(REGIMES)]
+        W = G.random_weights(n, seed, kind)
+        for sense in (1, -1):
+            assert_bit_equal(oracle.appd_weights(W, sense), oracle.floyd(W, sense))
+        assert_bit_equal(oracle.appd_weights(W, 1), oracle.mst_path(W))
+
+
+def test_c1_equals_floyd():
+    W = G.config("C1")
+    assert_bit_equal(oracle.appd_weights(W), oracle.floyd(W))
+
+
+def test_mst_path_large():
+    for n, kind in [(300, "uniform"), (700, "ties"), (1024, "negative")]:
+        W = G.random_weights(n, 11, kind)
+        assert_bit_equal(oracle.appd_weights(W), oracle.mst_path(W))
+
+
+# --------------------------------------------------------------------------
+# library special case: single linkage dendrogram read-off
+# --------------------------------------------------------------------------
+def _scipy_appd(W):
+    from scipy.cluster.hierarchy import cophenet, linkage
+    from scipy.spatial.distance import squareform
+
+    Wd = np.asarray(W, np.float64).copy()
+    np.fill_diagonal(Wd, 0.0)
+    Z = linkage(squareform(Wd, checks=False), method="single")
+    return squareform(cophenet(Z)).astype(np.float32)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties", "ints255"])
+def test_scipy_single_linkage_cophenet(kind):
+    for seed, n in [(0, 50), (1, 200), (2, 513)]:
+        W = G.random_weights(n, seed, kind)
+        assert_bit_equal(oracle.appd_weights(W), _scipy_appd(W))
+
+
+def test_scipy_on_configs_c1_c2():
+    W = G.config("C1")
+    assert_bit_equal(oracle.appd_weights(W), _scipy_appd(W))
+    X = G.config("C2")
+    assert_bit_equal(oracle.appd_points(X), _scipy_appd(oracle.points_weights(X)))
+
+
+# --------------------------------------------------------------------------
+# invariants of the mathematics
+# --------------------------------------------------------------------------
+def check_invariants(W, M, sense=1, triples=None):
+    n = W.shape[0]
+    Wc = np.where(W == 0, np.float32(0), W).astype(np.float32)
+    assert (bits(M) == bits(M.T)).all(), "symmetry"
+    assert (bits(np.diag(M)) == 0).all(), "+0 diagonal"
+    off = ~np.eye(n, dtype=bool)
+    if sense > 0:
+        assert (M[off] <= Wc[off]).all(), "M <= W"
+    else:
+        assert (M[off] >= Wc[off]).all(), "M >= W (widest)"
+    eu, ev, ew = oracle.prim_weights(W, sense)
+    vals = np.unique(M[off]) if n > 1 else np.array([], np.float32)
+    assert len(vals) <= max(n - 1, 0)
+    assert np.isin(vals, ew).all(), "every value is an MST edge weight"
+    if n <= 128:
+        # all triples: ultrametric M[i][j] <= max(M[i][k], M[k][j])  (dual for widest)
+        # the diagonal is the empty path (-inf for minimax, +inf for widest); exclude it
+        Mx = M.copy()
+        np.fill_diagonal(Mx, -np.inf if sense > 0 else np.inf)
+        for i in range(n):
+            if sense > 0:
+                bound = np.maximum(Mx[i][:, None], Mx)  # [k, j]: max(M[i][k], M[k][j])
+                assert (Mx[i][None, :] <= bound).all()
+            else:
+                bound = np.minimum(Mx[i][:, None], Mx)
+                assert (Mx[i][None, :] >= bound).all()
+    else:
+        rs = np.random.default_rng(0)
+        t = triples or 200000
+        i, j, k = rs.integers(0, n, (3, t))
+        ok = (i != j) & (j != k) & (i != k)
+        i, j, k = i[ok], j[ok], k[ok]
+        if sense > 0:
+            assert (M[i, j] <= np.maximum(M[i, k], M[k, j])).all()
+        else:
+            assert (M[i, j] >= np.minimum(M[i, k], M[k, j])).all()
+
+
+@pytest.mark.parametrize("kind", REGIMES)
+def test_invariants_and_write_once(kind):
+    for n in (2, 3, 10, 100, 1000):
+        W = G.random_weights(n, n + 1, kind)
+        for sense in (1, -1):
+            M, st = oracle.appd_weights(W, sense, with_stats=True)
+            check_invariants(W, M, sense)
+            assert st["writes"] == n * (n - 1) // 2
+            assert st["traversed"] <= n * (n - 1) // 2 + n - 1
+
+
+def test_mst_weight_is_minimal_by_enumeration():
+    """Prim (R2) against all spanning trees for n <= 6: same total weight, both senses."""
+    for n in range(2, 7):
+        for seed in range(6):
+            W = G.random_weights(n, seed, "ties" if seed % 2 else "uniform")
+            edges = [(i, j) for i in range(n) for j in range(i + 1, n)]
+            best_min, best_max = np.inf, -np.inf
+            for sub in itertools.combinations(range(len(edges)), n - 1):
+                parent = list(range(n))
+
+                def find(x):
+                    while parent[x] != x:
+                        x = parent[x]
+                    return x
+
+                ok = True
+                for e in sub:
+                    a, b = find(edges[e][0]), find(edges[e][1])
+                    if a == b:
+                        ok = False
+                        break
+                    parent[a] = b
+                if ok:
+                    tot = sum(float(W[edges[e]]) for e in sub)
+                    best_min = min(best_min, tot)
+                    best_max = max(best_max, tot)
+            _, _, ew = oracle.prim_weights(W, 1)
+            assert abs(float(np.sum(ew.astype(np.float64))) - best_min) < 1e-9
+            _, _, ew = oracle.prim_weights(W, -1)
+            assert abs(float(np.sum(ew.astype(np.float64))) - best_max) < 1e-9
+
+
+# --------------------------------------------------------------------------
+# metamorphic identities
+# --------------------------------------------------------------------------
+def test_permutation_equivariance_with_ties():
+    """relabelling invariance under ties, 50 seeds, n <= 32 (+ larger)."""
+    for seed in range(50):
+        n = 2 + seed % 31
+        W = G.random_weights(n, seed, "ties")
+        p = np.random.default_rng(seed).permutation(n)
+        M = oracle.appd_weights(W)
+        Mp = oracle.appd_weights(W[np.ix_(p, p)])
+        assert_bit_equal(Mp, M[np.ix_(p, p)])
+    X = G.random_points(300, 3, 1, "grid")
+    p = np.random.default_rng(1).permutation(300)
+    assert_bit_equal(oracle.appd_points(X[p]), oracle.appd_points(X)[np.ix_(p, p)])
+
+
+def test_idempotence_and_monotone_commutation():
+    for seed in range(30):
+        n = 5 + seed * 3
+        W = G.random_weights(n, seed, REGIMES[seed % len(REGIMES)])
+        M = oracle.appd_weights(W)
+        assert_bit_equal(oracle.appd_weights(M), M)  # APPD of an ultrametric is itself
+        for f in (lambda a: np.floor(a), lambda a: a * np.float32(2), lambda a: np.minimum(a, np.float32(1))):
+            fW = f(W).astype(np.float32)
+            np.fill_diagonal(fW, 0)
+            fM = f(M).astype(np.float32)
+            np.fill_diagonal(fM, 0)
+            assert_bit_equal(oracle.appd_weights(fW), fM + np.float32(0))
+
+
+def test_widest_duality():
+    """minimax(G) == -widest(-G) exactly (100 seeds, n <= 64); -0 canonicalised."""
+    rs = np.random.default_rng(3)
+    for seed in range(100):
+        n = int(rs.integers(2, 65))
+        W = G.random_weights(n, seed, REGIMES[seed % len(REGIMES)])
+        a = oracle.appd_weights(W, 1)
+        b = -oracle.appd_weights(-W, -1) + np.float32(0)
+        assert_bit_equal(a, b)
+
+
+def test_points_mode_equals_weights_mode_on_r1_weights():
+    for kind in ("uniform", "blobs", "dups", "grid", "wide"):
+        X = G.random_points(257, 5, 2, kind)
+        assert_bit_equal(oracle.appd_points(X), oracle.appd_weights(oracle.points_weights(X)))
+
+
+def test_sqrt_commutation_points():
+    """Monotone commutation with f = sqrtf (App. A.4): APPD(sqrt(d2)) == sqrt(APPD(d2))."""
+    for kind in ("uniform", "grid", "dups"):
+        X = G.random_points(200, 4, 5, kind)
+        W = oracle.points_weights(X)
+        D2 = np.empty_like(W)
+        for i in range(200):
+            for j in range(200):
+                D2[i, j] = oracle.r1_dist2(X[i], X[j]) if i != j else 0
+        assert_bit_equal(np.sqrt(oracle.appd_weights(D2)), oracle.appd_weights(W))
+
+
+def test_row_window_r5_equals_full():
+    X = G.random_points(500, 3, 9, "dups")
+    M = oracle.appd_points(X)
+    for r0, R in [(0, 1), (0, 500), (123, 77), (499, 1)]:
+        assert_bit_equal(oracle.appd_points_rows(X, r0, R), M[r0:r0 + R])
+    W = G.random_weights(300, 4, "negative")
+    Mw = oracle.appd_weights(W)
+    assert_bit_equal(oracle.appd_weights_rows(W, 100, 50), Mw[100:150])
+
+
+# --------------------------------------------------------------------------
+# R1 weights: exact rational emulation of the pinned fmaf chain, fp64 bound
+# --------------------------------------------------------------------------
+def round_f32(q: Fraction) -> np.float32:
+    """Round an exact rational to the nearest fp32, ties to even (IEEE-754 RN)."""
+    if q == 0:
+        return np.float32(0.0)
+    s = -1 if q < 0 else 1
+    a = abs(q)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= a:
+        e += 1
+    e = max(e, -126)
+    ulp = Fraction(2) ** (e - 23)
+    k = a / ulp
+    fl = k.numerator // k.denominator
+    rem = k - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return np.float32(s * float(fl * ulp))
+
+
+def r1_exact(xi, xj):
+    acc = Fraction(0)
+    for a, b in zip(xi, xj):
+        t = round_f32(Fraction(float(a)) - Fraction(float(b)))
+        acc = Fraction(float(round_f32(Fraction(float(t)) * Fraction(float(t)) + acc)))
+    return np.float32(float(acc))
+
+
+def test_r1_matches_exact_rational_fma_chain():
+    rs = np.random.default_rng(5)
+    for trial in range(300):
+        d = int(rs.integers(1, 9))
+        scale = 10.0 ** rs.integers(-6, 6)
+        xi = (rs.standard_normal(d) * scale).astype(np.float32)
+        xj = (rs.standard_normal(d) * scale).astype(np.float32)
+        assert bits(oracle.r1_dist2(xi, xj)) == bits(r1_exact(xi, xj))
+
+
+def test_r1_double_rounding_case():
+    """The fmaf step must round once.  Constructed case (search in DESIGN.md notes):
+    t0 = 2047 * 2^-27 (t0^2 exact in fp32), t = 0x1.000ff8p+0: t^2 + t0^2 lies 2^-54
+    above an fp32 midpoint whose lower neighbour is even.  A single rounding goes up;
+    an fp64 emulation fl32(fl64(t*t + acc)) lands on the midpoint and goes down."""
+    t0 = float.fromhex("0x1.ffcp-17")
+    t = float.fromhex("0x1.000ff8p+0")
+    exact = round_f32(Fraction(t) ** 2 + Fraction(t0) ** 2)
+    emulated = np.float32(np.float64(t) * np.float64(t) + np.float64(np.float32(t0 * t0)))
+    assert bits(exact) != bits(emulated)
+    xi = np.array([t0, t], np.float32)
+    xj = np.zeros(2, np.float32)
+    assert bits(oracle.r1_dist2(xi, xj)) == bits(exact)
+    assert bits(oracle.r1_dist2(xj, xi)) == bits(exact)
+
+
+def test_r1_symmetry_zero_and_fp64_bound():
+    for name, X in [("C2", G.config("C2")), ("C4s", G.config("C4", n=512)), ("C5s", G.config("C5", n=2048))]:
+        n, d = X.shape
+        rs = np.random.default_rng(1)
+        rows = rs.integers(0, n, 64)
+        Wb = oracle.points_weights(X, 0, n)[rows] if n <= 4096 else np.stack(
+            [oracle.points_weights(X, int(r), 1)[0] for r in rows])
+        bound = (d / 2 + 2) * 2.0 ** -24
+        worst = 0.0
+        for t, r in enumerate(rows):
+            ref = np.sqrt(((X[r].astype(np.float64) - X.astype(np.float64)) ** 2).sum(1))
+            got = Wb[t].astype(np.float64)
+            nz = ref > 0
+            assert (got[~nz] == 0).all()
+            rel = np.abs(got[nz] - ref[nz]) / ref[nz]
+            worst = max(worst, rel.max(initial=0))
+            # symmetry, bitwise
+            for c in rs.integers(0, n, 16):
+                assert bits(oracle.r1_weight(X[r], X[c])) == bits(oracle.r1_weight(X[c], X[r]))
+        assert worst <= bound and worst <= 1e-5, (name, worst, bound)
+
+
+def test_dist_f64_exact_small():
+    assert oracle.dist_f64(np.array([0, 0], np.float32), np.array([3, 4], np.float32)) == 5.0
+    assert oracle.r1_weight(np.array([1, 2, 2], np.float32), np.zeros(3, np.float32)) == 3.0
