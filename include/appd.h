@@ -1,0 +1,163 @@
+/*
+ * appd.h -- C ABI of libappd, the B200 (sm_100a) all-points minimax path
+ * distance (APPD) library.
+ *
+ * The operation (arxiv 2407.07058, PAPER.md):
+ *   Eq. 1-2: for vertices i, j of an undirected weighted graph G,
+ *     M(i,j | G) = min over all paths p from i to j of max_weight(p).
+ *   the APPD is the n x n matrix of M(i,j); "a dataset X can be
+ *     straightforwardly converted to a complete graph" (points mode; the edge
+ *     weight is the Euclidean distance, reading Q6, computed by the
+ *     pinned fp32 formula R1: acc=+0; for k<d: t=fl(x_ik-x_jk); acc=fmaf(t,t,acc);
+ *     w=sqrtf(acc)).
+ *   P:L93-98 (Algorithm 4): the APPD follows from a minimum spanning tree: its
+ *     edges removed from large to small split the vertex set, and every pair
+ *     across a split gets the removed edge's weight.  libappd computes the same
+ *     matrix with an MST stage (Boruvka), an edge sort and a dendrogram
+ *     (leaf order pi, merge heights h) and a fill that writes
+ *     M[pi_a][pi_b] = max(h[a..b-1]).
+ *   P:L50, P:L119 (widest path): sense = -1 computes the widest-path APPD
+ *     (maximum spanning tree, minimum over the path) -- weights mode only.
+ *
+ * Conventions for every call:
+ *   - Matrices are fp32, row-major, contiguous, leading dimension n (W, M) or
+ *     d (X).  Indices are 0-based.
+ *   - M[i][i] = +0.0 (the empty path, reading Q3).  Every other entry
+ *     is bit-identical to one input weight (weights mode) or one R1 weight
+ *     (points mode).  -0.0 input weights are read as +0.0 (reading Q5).
+ *   - Unless a name ends in _host, pointers are CUDA device pointers on the
+ *     context's device; host pointers are rejected with
+ *     APPD_ERR_INVALID_ARGUMENT.  The caller owns every buffer it passes.
+ *   - Calls enqueue work on the context's stream and return after it has
+ *     completed (so data-dependent validation errors can be reported).
+ *   - Every call returns a status; nothing throws across the ABI.  After a
+ *     CUDA or NCCL failure the context is poisoned: later calls return
+ *     APPD_ERR_POISONED and only appd_destroy is valid.
+ *   - A context is not thread-safe: use one host thread per context.
+ *   - Multi-GPU (world > 1): one process per GPU, every rank calls the solve
+ *     with the same n (and d).  Rank r owns the rows [row0, row0+rows) of M
+ *     returned by appd_row_range, and M points to that rows x n block.  Points
+ *     mode: X is replicated on every rank.  Weights mode: W points to the
+ *     rank's rows x n row block; symmetry is checked inside the rank's diagonal
+ *     block only.
+ *   - Validation reports one offender: the first non-finite value in row-major
+ *     order if there is any, else the first nonzero diagonal entry, else the
+ *     first asymmetric pair (i, j) with i < j in row-major order.
+ */
+#ifndef APPD_H
+#define APPD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct appd_ctx appd_ctx; /* opaque: device, stream, workspace, optional NCCL communicator */
+
+typedef enum {
+  APPD_OK = 0,
+  APPD_ERR_INVALID_ARGUMENT = 1, /* n < 1, d < 1, NULL or host pointer, bad option */
+  APPD_ERR_NONFINITE = 2,        /* NaN or +-Inf in W or X; appd_error_index gives (i, j) */
+  APPD_ERR_NOT_SYMMETRIC = 3,    /* W[i][j] != W[j][i] bitwise (after -0 -> +0); first (i, j), i < j */
+  APPD_ERR_BAD_DIAGONAL = 4,     /* W[i][i] is not +-0; (i, i) */
+  APPD_ERR_UNSUPPORTED = 5,      /* size beyond the supported index widths, or option not built */
+  APPD_ERR_OUT_OF_MEMORY = 6,    /* device or pinned host allocation failed */
+  APPD_ERR_CUDA = 7,             /* CUDA runtime error (context poisoned) */
+  APPD_ERR_NCCL = 8,             /* NCCL error (context poisoned) */
+  APPD_ERR_POISONED = 9          /* an earlier call failed with CUDA/NCCL error */
+} appd_status;
+
+/* MST variant (appd_options.variant) */
+#define APPD_VARIANT_AUTO 0
+#define APPD_VARIANT_PRIM 1    /* single-CTA Prim, emits the leaf order directly (n <= 4096, world == 1) */
+#define APPD_VARIANT_BORUVKA 2 /* row-parallel Boruvka rounds (any n, shards over ranks) */
+
+typedef struct {
+  uint32_t struct_size;          /* = sizeof(appd_options); set by appd_options_init */
+  int32_t device;                /* CUDA device ordinal (default 0) */
+  void* cuda_stream;             /* cudaStream_t to run on; NULL = library-owned stream */
+  int32_t rank, world;           /* process rank / count (default 0 / 1) */
+  const uint8_t* nccl_unique_id; /* world > 1: 128-byte ncclUniqueId from appd_get_nccl_unique_id on rank 0 */
+  int32_t variant;               /* APPD_VARIANT_* (default AUTO) */
+  int32_t validate;              /* 1 = check W/X (default), 0 = trust the input */
+  int32_t sense;                 /* +1 minimax (default), -1 widest path (weights mode only) */
+  int32_t timing;                /* 1 = record per-stage CUDA events (appd_get_stats), default 0 */
+  int32_t dendrogram;            /* 0 auto, 1 host union-find, 2 GPU */
+  int32_t reserved[8];
+} appd_options;
+
+typedef struct {
+  uint32_t struct_size; /* = sizeof(appd_stats) */
+  int32_t variant;      /* variant used by the last solve */
+  int32_t rounds;       /* Boruvka rounds (0 for Prim) */
+  int32_t dendrogram;   /* 1 host, 2 GPU, 0 none (Prim) */
+  int64_t n, d, row0, rows;
+  /* per-stage device time of the last solve in ms (timing = 1), else 0 */
+  double ms_validate, ms_mst, ms_sort, ms_dendrogram, ms_prep, ms_fill, ms_total;
+  int64_t kernel_launches; /* kernels launched by the last solve */
+  int64_t fill_launches;   /* launches of the fill kernel in the last solve */
+  int64_t fill_bytes;      /* bytes the fill wrote (algorithmic: rows * n * 4) */
+} appd_stats;
+
+/* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */
+void appd_options_init(appd_options* opt);
+
+/* Create a context.  opt may be NULL (defaults).  world > 1 initialises NCCL
+ * (collective over the ranks).  On failure *out is NULL. */
+appd_status appd_create(appd_ctx** out, const appd_options* opt);
+
+/* Set the stream later calls run on (NULL = library-owned stream). */
+appd_status appd_set_stream(appd_ctx* ctx, void* cuda_stream);
+
+/* Weights mode.  W: n x n (world 1) or this rank's rows x n block; M: rows x n.
+ * Validation (validate = 1): finite, W[i][i] == +-0, W[i][j] == W[j][i]. */
+appd_status appd_solve_weights(appd_ctx* ctx, const float* W, int64_t n, float* M);
+
+/* Points mode.  X: n x d (replicated on every rank); M: rows x n.  W is never
+ * materialised; n <= 131072 (the packed 64-bit edge key). */
+appd_status appd_solve_points(appd_ctx* ctx, const float* X, int64_t n, int64_t d, float* M);
+
+/* The same with HOST buffers (pinned or pageable): copies X/W in and M out on
+ * the context stream, inside the call. */
+appd_status appd_solve_points_host(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host);
+appd_status appd_solve_weights_host(appd_ctx* ctx, const float* W_host, int64_t n, float* M_host);
+
+void appd_destroy(appd_ctx* ctx); /* NULL-safe; frees the workspace and the NCCL communicator */
+
+/* ---- support ---- */
+
+/* Rows of M this rank owns: [row0, row0 + rows) (host-only; no device needed). */
+appd_status appd_row_range(const appd_ctx* ctx, int64_t n, int64_t* row0, int64_t* rows);
+/* Same without a context: the row split rank r of world uses. */
+appd_status appd_row_range_of(int64_t n, int32_t rank, int32_t world, int64_t* row0, int64_t* rows);
+
+/* R1 weights for rows [row0, row0+rows) of the complete graph of X (device, rows x n). */
+appd_status appd_points_weights(appd_ctx* ctx, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,
+                                float* Wblock);
+
+/* 128-byte ncclUniqueId for appd_options.nccl_unique_id (call on rank 0 only). */
+appd_status appd_get_nccl_unique_id(uint8_t out[128]);
+
+/* Statistics of the last solve; stats->struct_size must be sizeof(appd_stats). */
+appd_status appd_get_stats(const appd_ctx* ctx, appd_stats* stats);
+
+/* Test hook: leaf order pi (int32[n]) and merge heights h (float[n-1]) of the last
+ * solve, to host memory.  Either pointer may be NULL. */
+appd_status appd_last_dendrogram(const appd_ctx* ctx, int32_t* pi_host, float* h_host, int64_t n);
+
+/* Offending indices of the last NONFINITE / NOT_SYMMETRIC / BAD_DIAGONAL status. */
+appd_status appd_error_index(const appd_ctx* ctx, int64_t* i, int64_t* j);
+
+const char* appd_last_error(const appd_ctx* ctx); /* message of the last failure ("" if none) */
+const char* appd_status_string(appd_status s);
+
+/* Library build identification: "libappd <version> sm_100a". */
+const char* appd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APPD_H */

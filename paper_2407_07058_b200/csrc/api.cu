@@ -1,0 +1,513 @@
+// api.cu -- the C ABI of libappd (include/appd.h) and the stage pipeline:
+//   validate (a1) -> MST by Boruvka rounds (a2, a3; a8 exchange when world > 1)
+//   -> sort the MST edge keys (a4) -> dendrogram: leaf order pi + heights h (a5)
+//   -> fill prep: positions + sparse table (a6) -> fill (a7).
+// Every step runs in this library's kernels on the context stream; the host
+// only sequences them (and, in v1, runs the O(n) union-find dendrogram).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace appd;
+
+namespace appd {
+
+void* ws(appd_ctx* c, int slot, size_t bytes) {
+  DevBuf& b = c->buf[slot];
+  if (b.bytes >= bytes && b.p) return b.p;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  size_t want = bytes < 256 ? 256 : bytes;
+  want = (want + 4095) & ~(size_t)4095;
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return nullptr;
+  }
+  b.bytes = want;
+  return b.p;
+}
+
+appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...) {
+  char msg[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(msg, sizeof msg, fmt, ap);
+  va_end(ap);
+  if (c) c->last_error = msg;
+  return s;
+}
+
+appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where) {
+  if (c) c->poisoned = true;
+  return fail(c, APPD_ERR_CUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+}
+
+}  // namespace appd
+
+static const char* kStatusNames[] = {"APPD_OK",
+                                     "APPD_ERR_INVALID_ARGUMENT",
+                                     "APPD_ERR_NONFINITE",
+                                     "APPD_ERR_NOT_SYMMETRIC",
+                                     "APPD_ERR_BAD_DIAGONAL",
+                                     "APPD_ERR_UNSUPPORTED",
+                                     "APPD_ERR_OUT_OF_MEMORY",
+                                     "APPD_ERR_CUDA",
+                                     "APPD_ERR_NCCL",
+                                     "APPD_ERR_POISONED"};
+
+extern "C" const char* appd_status_string(appd_status s) {
+  if ((int)s < 0 || (int)s > 9) return "APPD_ERR_UNKNOWN";
+  return kStatusNames[(int)s];
+}
+
+extern "C" const char* appd_version(void) { return "libappd 0.1 sm_100a"; }
+
+extern "C" void appd_options_init(appd_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->struct_size = sizeof(appd_options);
+  o->device = 0;
+  o->rank = 0;
+  o->world = 1;
+  o->variant = APPD_VARIANT_AUTO;
+  o->validate = 1;
+  o->sense = 1;
+  o->timing = 0;
+  o->dendrogram = 0;
+}
+
+extern "C" appd_status appd_row_range_of(int64_t n, int32_t rank, int32_t world, int64_t* row0, int64_t* rows) {
+  if (n < 1 || world < 1 || rank < 0 || rank >= world || !row0 || !rows) return APPD_ERR_INVALID_ARGUMENT;
+  // blocks of 128 rows (the MST scan tile), split as evenly as possible
+  int64_t blocks = (n + 127) / 128;
+  int64_t b0 = blocks * rank / world, b1 = blocks * (rank + 1) / world;
+  int64_t r0 = std::min(n, b0 * 128), r1 = std::min(n, b1 * 128);
+  *row0 = r0;
+  *rows = r1 - r0;
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_row_range(const appd_ctx* c, int64_t n, int64_t* row0, int64_t* rows) {
+  if (!c) return APPD_ERR_INVALID_ARGUMENT;
+  return appd_row_range_of(n, c->opt.rank, c->opt.world, row0, rows);
+}
+
+extern "C" appd_status appd_get_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return APPD_ERR_INVALID_ARGUMENT;
+  std::string err;
+  return nccl_unique_id(out, &err);
+}
+
+extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
+  if (!out) return APPD_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  appd_options o;
+  appd_options_init(&o);
+  if (opt) {
+    if (opt->struct_size != sizeof(appd_options)) return APPD_ERR_INVALID_ARGUMENT;
+    o = *opt;
+  }
+  if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.sense != 1 && o.sense != -1) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.world > 1 && !o.nccl_unique_id) return APPD_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return APPD_ERR_CUDA;
+  }
+  if (o.device < 0 || o.device >= ndev) return APPD_ERR_INVALID_ARGUMENT;
+  appd_ctx* c = new appd_ctx();
+  c->opt = o;
+  c->device = o.device;
+  std::memset(&c->stats, 0, sizeof c->stats);
+  c->stats.struct_size = sizeof(appd_stats);
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    delete c;
+    return APPD_ERR_CUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) == cudaSuccess) c->sm_count = prop.multiProcessorCount;
+  if (prop.major < 10) {
+    delete c;
+    return APPD_ERR_UNSUPPORTED;  // built for sm_100a only
+  }
+  if (o.cuda_stream) {
+    c->stream = (cudaStream_t)o.cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return APPD_ERR_CUDA;
+    }
+    c->own_stream = true;
+  }
+  for (int i = 0; i < 16; i++) cudaEventCreate(&c->ev[i]);
+  c->ev_ready = true;
+  if (o.world > 1) {
+    appd_status s = nccl_init(c, o.nccl_unique_id, o.rank, o.world);
+    if (s != APPD_OK) {
+      appd_destroy(c);
+      return s;
+    }
+  }
+  *out = c;
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_set_stream(appd_ctx* c, void* stream) {
+  if (!c) return APPD_ERR_INVALID_ARGUMENT;
+  if (c->poisoned) return APPD_ERR_POISONED;
+  cudaSetDevice(c->device);
+  if (stream) {
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    c->own_stream = false;
+    c->stream = (cudaStream_t)stream;
+  } else if (!c->own_stream) {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return APPD_ERR_CUDA;
+    c->own_stream = true;
+  }
+  return APPD_OK;
+}
+
+extern "C" void appd_destroy(appd_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  nccl_destroy(c);
+  for (auto& b : c->buf)
+    if (b.p) cudaFree(b.p);
+  if (c->ev_ready)
+    for (int i = 0; i < 16; i++) cudaEventDestroy(c->ev[i]);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  cudaGetLastError();
+  delete c;
+}
+
+extern "C" const char* appd_last_error(const appd_ctx* c) { return c ? c->last_error.c_str() : ""; }
+
+extern "C" appd_status appd_error_index(const appd_ctx* c, int64_t* i, int64_t* j) {
+  if (!c || !i || !j) return APPD_ERR_INVALID_ARGUMENT;
+  *i = c->err_i;
+  *j = c->err_j;
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_get_stats(const appd_ctx* c, appd_stats* s) {
+  if (!c || !s || s->struct_size != sizeof(appd_stats)) return APPD_ERR_INVALID_ARGUMENT;
+  *s = c->stats;
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_last_dendrogram(const appd_ctx* c, int32_t* pi, float* h, int64_t n) {
+  if (!c || !c->have_dendrogram || (int64_t)c->last_pi.size() != n) return APPD_ERR_INVALID_ARGUMENT;
+  if (pi) std::memcpy(pi, c->last_pi.data(), sizeof(int32_t) * n);
+  if (h && n > 1) std::memcpy(h, c->last_h.data(), sizeof(float) * (n - 1));
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+static appd_status check_device_ptr(appd_ctx* c, const void* p, const char* name) {
+  if (!p) return fail(c, APPD_ERR_INVALID_ARGUMENT, "%s is NULL", name);
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, APPD_ERR_INVALID_ARGUMENT, "%s is not a CUDA pointer", name);
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    return fail(c, APPD_ERR_INVALID_ARGUMENT, "%s is not device memory", name);
+  if (a.device != c->device) return fail(c, APPD_ERR_INVALID_ARGUMENT, "%s is on another device", name);
+  return APPD_OK;
+}
+
+static inline void stage_event(appd_ctx* c, int idx) {
+  if (c->opt.timing) cudaEventRecord(c->ev[idx], c->stream);
+}
+
+static float ev_ms(appd_ctx* c, int a, int b) {
+  float ms = 0.0f;
+  if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.0f;
+  }
+  return ms;
+}
+
+// map the three first-offender indices to a status.  Priority: any non-finite
+// value first (its first occurrence in row-major order), then the first bad
+// diagonal entry, then the first asymmetric pair (i < j).
+static appd_status report_validation(appd_ctx* c, const u64 bad[3], int64_t n, bool points, int64_t d) {
+  int which = -1;
+  for (int t = 0; t < 3 && which < 0; t++)
+    if (bad[t] != KEY_NONE) which = t;
+  if (which < 0) return APPD_OK;
+  u64 best = bad[which];
+  int64_t w = points ? d : n;
+  c->err_i = (int64_t)(best / (u64)w);
+  c->err_j = (int64_t)(best % (u64)w);
+  if (which == 0)
+    return fail(c, APPD_ERR_NONFINITE, "non-finite %s at (%lld, %lld)", points ? "coordinate" : "weight",
+                (long long)c->err_i, (long long)c->err_j);
+  if (which == 1)
+    return fail(c, APPD_ERR_BAD_DIAGONAL, "nonzero diagonal W[%lld][%lld]", (long long)c->err_i, (long long)c->err_j);
+  return fail(c, APPD_ERR_NOT_SYMMETRIC, "W[%lld][%lld] != W[%lld][%lld]", (long long)c->err_i,
+              (long long)c->err_j, (long long)c->err_j, (long long)c->err_i);
+}
+
+// The whole pipeline.  X (points) or W (weights) is a device pointer.
+static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
+  const bool points = X != nullptr;
+  const int sense = points ? 1 : c->opt.sense;
+  int64_t row0, rows;
+  appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
+  std::memset(&c->stats, 0, sizeof c->stats);
+  c->stats.struct_size = sizeof(appd_stats);
+  c->stats.n = n;
+  c->stats.d = points ? d : 0;
+  c->stats.row0 = row0;
+  c->stats.rows = rows;
+  c->stats.variant = APPD_VARIANT_BORUVKA;
+  c->launches = 0;
+  c->have_dendrogram = false;
+  c->err_i = c->err_j = -1;
+  c->last_error.clear();
+  stage_event(c, 0);
+
+  // ---- a1: validation ----
+  if (c->opt.validate) {
+    u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
+    if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
+    APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
+    appd_status s = points ? launch_validate_points(c, X, n, d, bad) : launch_validate_weights(c, W, n, row0, rows, bad);
+    if (s) return s;
+    u64 hb[3];
+    APPD_CUDA(c, cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->opt.world > 1) {
+      // every rank must agree on the verdict (else the others would hang in the next collective)
+      u64* agree = (u64*)ws(c, S_TMP, sizeof(u64) * 3);
+      if (!agree) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
+      APPD_CUDA(c, cudaMemcpyAsync(agree, hb, sizeof hb, cudaMemcpyHostToDevice, c->stream));
+      if ((s = nccl_allreduce_min_u64(c, agree, 3))) return s;
+      APPD_CUDA(c, cudaMemcpyAsync(hb, agree, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
+      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if ((s = report_validation(c, hb, n, points, d))) return s;
+  }
+  stage_event(c, 1);
+
+  if (n == 1) {
+    if (rows > 0) {
+      appd_status s = launch_set_diag_zero_single(c, M);
+      if (s) return s;
+    }
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->last_pi.assign(1, 0);
+    c->last_h.clear();
+    c->have_dendrogram = true;
+    c->stats.kernel_launches = c->launches;
+    return APPD_OK;
+  }
+
+  // ---- a2/a3: MST by Boruvka rounds ----
+  KeySpec ks;
+  ks.points = points;
+  ks.shift = points ? 33 : 32;
+  ks.sense = sense;
+  int* comp = (int*)ws(c, S_COMP, sizeof(int) * n);
+  u64* compbest = (u64*)ws(c, S_COMPBEST, sizeof(u64) * n);
+  int* link = (int*)ws(c, S_LINK, sizeof(int) * n);
+  int* parent = (int*)ws(c, S_PARENT, sizeof(int) * n);
+  int* newid = (int*)ws(c, S_NEWID, sizeof(int) * (n + 1));
+  int* flags = (int*)ws(c, S_FLAGS, sizeof(int) * (n + 1));
+  u64* mstkeys = (u64*)ws(c, S_MSTKEYS, sizeof(u64) * n);
+  u64* sorted = (u64*)ws(c, S_MSTKEYS_SORTED, sizeof(u64) * n);
+  int* counters = (int*)ws(c, S_COUNTERS, sizeof(int) * 16);
+  if (!comp || !compbest || !link || !parent || !newid || !flags || !mstkeys || !sorted || !counters)
+    return fail(c, APPD_ERR_OUT_OF_MEMORY, "MST workspace (n = %lld)", (long long)n);
+  float* XT = nullptr;
+  int64_t npad = 0, dpad = 0;
+  appd_status s;
+  if (points) {
+    npad = (n + 127) / 128 * 128;
+    dpad = (d + 31) / 32 * 32;
+    XT = (float*)ws(c, S_XT, sizeof(float) * npad * dpad);
+    if (!XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "XT workspace");
+    if ((s = launch_transpose_points(c, X, n, d, XT, npad, dpad))) return s;
+  }
+  if ((s = launch_iota(c, comp, n))) return s;
+  APPD_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(int) * 16, c->stream));
+  int64_t k = n;
+  int rounds = 0;
+  int* hostk = nullptr;
+  int hk[2];
+  hostk = hk;
+  while (k > 1) {
+    if ((s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
+    const int* cmp = rounds == 0 ? nullptr : comp;
+    if (points) s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
+    else s = launch_scan_weights(c, W, n, row0, rows, cmp, compbest, sense);
+    if (s) return s;
+    if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
+    if ((s = launch_hook(c, compbest, k, comp, ks.shift, link))) return s;
+    if ((s = launch_mutual(c, compbest, k, link, parent, mstkeys, counters))) return s;
+    if ((s = launch_jump(c, parent, k, flags))) return s;
+    if ((s = exclusive_scan_i32(c, flags, newid, k))) return s;
+    if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    int64_t knew = (int64_t)hostk[0] + hostk[1];
+    rounds++;
+    if (knew >= k || knew < 1) return fail(c, APPD_ERR_CUDA, "Boruvka made no progress (k = %lld)", (long long)k);
+    k = knew;
+  }
+  c->stats.rounds = rounds;
+  {
+    int cnt = 0;
+    APPD_CUDA(c, cudaMemcpyAsync(&cnt, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (cnt != n - 1) return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", cnt, (long long)(n - 1));
+  }
+  stage_event(c, 2);
+
+  // ---- a4: sort the MST edge keys ascending (Kruskal order = P:L98's descending removal reversed) ----
+  if ((s = sort_keys_u64(c, mstkeys, sorted, n - 1))) return s;
+  stage_event(c, 3);
+
+  // ---- a5: dendrogram (v1: host union-find with list concatenation) ----
+  std::vector<u64> hkeys(n - 1);
+  APPD_CUDA(c, cudaMemcpyAsync(hkeys.data(), sorted, sizeof(u64) * (n - 1), cudaMemcpyDeviceToHost, c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->last_pi.resize(n);
+  c->last_h.resize(n - 1);
+  host_dendrogram(hkeys.data(), n, ks, c->last_pi.data(), c->last_h.data());
+  c->have_dendrogram = true;
+  c->stats.dendrogram = 1;
+  const int64_t m = n - 1;
+  int levels = 1;
+  while ((1ll << levels) <= m) levels++;
+  const int64_t stride = m;
+  int* pi = (int*)ws(c, S_PI, sizeof(int) * n);
+  int* pos = (int*)ws(c, S_POS, sizeof(int) * n);
+  float* ST = (float*)ws(c, S_ST, sizeof(float) * stride * levels);
+  if (!pi || !pos || !ST) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
+  APPD_CUDA(c, cudaMemcpyAsync(pi, c->last_pi.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaMemcpyAsync(ST, c->last_h.data(), sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
+  stage_event(c, 4);
+
+  // ---- a6: fill prep ----
+  if ((s = launch_positions(c, pi, n, pos))) return s;
+  if ((s = launch_sparse_table(c, ST, m, levels, stride, sense < 0))) return s;
+  const int* rows_sorted = pi;
+  int* rowpos = (int*)ws(c, S_ROWPOS, sizeof(int) * n);
+  if (!rowpos) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
+  if (c->opt.world == 1) {
+    if ((s = launch_iota(c, rowpos, n))) return s;
+  } else {
+    int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (rows + 1));
+    int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (rows + 1));
+    if (!keys || !rs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
+    if ((s = launch_gather_rowpos(c, pos, row0, rows, keys, keys + rows + 1))) return s;
+    if ((s = sort_pairs_i32(c, keys, rowpos, keys + rows + 1, rs, rows))) return s;
+    rows_sorted = rs;
+  }
+  stage_event(c, 5);
+
+  // ---- a7: fill ----
+  if ((s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, stride, n, M, row0, sense < 0))) return s;
+  stage_event(c, 6);
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->stats.fill_bytes = rows * n * 4;
+  c->stats.kernel_launches = c->launches;
+  if (c->opt.timing) {
+    c->stats.ms_validate = ev_ms(c, 0, 1);
+    c->stats.ms_mst = ev_ms(c, 1, 2);
+    c->stats.ms_sort = ev_ms(c, 2, 3);
+    c->stats.ms_dendrogram = ev_ms(c, 3, 4);
+    c->stats.ms_prep = ev_ms(c, 4, 5);
+    c->stats.ms_fill = ev_ms(c, 5, 6);
+    c->stats.ms_total = ev_ms(c, 0, 6);
+  }
+  return APPD_OK;
+}
+
+static appd_status enter(appd_ctx* c) {
+  if (!c) return APPD_ERR_INVALID_ARGUMENT;
+  if (c->poisoned) return APPD_ERR_POISONED;
+  if (cudaSetDevice(c->device) != cudaSuccess) return cuda_fail(c, cudaGetLastError(), "cudaSetDevice");
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_solve_weights(appd_ctx* c, const float* W, int64_t n, float* M) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
+  if (n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682 (32-bit pair index)");
+  if ((s = check_device_ptr(c, W, "W"))) return s;
+  if ((s = check_device_ptr(c, M, "M"))) return s;
+  return solve(c, W, nullptr, n, 0, M);
+}
+
+extern "C" appd_status appd_solve_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1 || d < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld, d = %lld", (long long)n, (long long)d);
+  if (n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072 (33-bit pair index)");
+  if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
+  if ((s = check_device_ptr(c, X, "X"))) return s;
+  if ((s = check_device_ptr(c, M, "M"))) return s;
+  return solve(c, nullptr, X, n, d, M);
+}
+
+// host-buffer variants (end to end: H2D of the input and D2H of M inside the call)
+static appd_status solve_host(appd_ctx* c, const float* Wh, const float* Xh, int64_t n, int64_t d, float* Mh) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (!Mh || (!Wh && !Xh)) return fail(c, APPD_ERR_INVALID_ARGUMENT, "NULL host buffer");
+  if (n < 1 || (Xh && d < 1)) return APPD_ERR_INVALID_ARGUMENT;
+  int64_t row0, rows;
+  appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
+  size_t in_bytes = Xh ? sizeof(float) * n * d : sizeof(float) * rows * n;
+  size_t out_bytes = sizeof(float) * rows * n;
+  float* din = (float*)ws(c, S_HOST_IN, in_bytes);
+  float* dout = (float*)ws(c, S_HOST_OUT, out_bytes);
+  if (!din || !dout) return fail(c, APPD_ERR_OUT_OF_MEMORY, "device staging for host buffers");
+  APPD_CUDA(c, cudaMemcpyAsync(din, Xh ? Xh : Wh, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  s = Xh ? solve(c, nullptr, din, n, d, dout) : solve(c, din, nullptr, n, 0, dout);
+  if (s) return s;
+  APPD_CUDA(c, cudaMemcpyAsync(Mh, dout, out_bytes, cudaMemcpyDeviceToHost, c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  return APPD_OK;
+}
+
+extern "C" appd_status appd_solve_points_host(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M) {
+  if (c && n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072");
+  return solve_host(c, nullptr, X, n, d, M);
+}
+
+extern "C" appd_status appd_solve_weights_host(appd_ctx* c, const float* W, int64_t n, float* M) {
+  if (c && n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682");
+  return solve_host(c, W, nullptr, n, 0, M);
+}
+
+extern "C" appd_status appd_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0,
+                                           int64_t rows, float* Wb) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1 || d < 1 || row0 < 0 || rows < 0 || row0 + rows > n) return APPD_ERR_INVALID_ARGUMENT;
+  if ((s = check_device_ptr(c, X, "X"))) return s;
+  if ((s = check_device_ptr(c, Wb, "Wblock"))) return s;
+  if ((s = launch_points_weights(c, X, n, d, row0, rows, Wb))) return s;
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  return APPD_OK;
+}

@@ -1,0 +1,189 @@
+// internal.cuh -- shared declarations of libappd (B200 / sm_100a).
+// Nothing here is shared with oracle/ (the CPU oracle is independent).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/appd.h"
+
+namespace appd {
+
+typedef unsigned long long u64;
+
+constexpr u64 KEY_NONE = ~0ULL;
+
+// ---------------------------------------------------------------------------
+// Edge keys.  A strict total order on edges is required so that Boruvka never
+// forms a cycle under ties: an edge {u, v},
+// u < v, is ordered by (weight, v, u).  The pair index tri(u, v) = v(v-1)/2 + u
+// is monotone in (v, u), so key = wkey << shift | tri(u, v).
+//   weights mode: wkey = orderable(w) (32 bits), shift 32, n <= 92682
+//   points mode:  wkey = bits(d^2) (31 bits, d^2 >= +0), shift 33, n <= 131072
+// Restricted to one row i, the order is "smaller weight, then smaller j", so a
+// row argmin over (w, j) is consistent with the component minimum over keys.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline uint32_t orderable(float f) {
+#ifdef __CUDA_ARCH__
+  uint32_t b = __float_as_uint(f);
+#else
+  uint32_t b;
+  memcpy(&b, &f, 4);
+#endif
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__host__ __device__ inline float from_orderable(uint32_t u) {
+  uint32_t b = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(b);
+#else
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+#endif
+}
+
+__host__ __device__ inline u64 tri_index(int64_t a, int64_t b) {
+  int64_t u = a < b ? a : b, v = a < b ? b : a;
+  return (u64)(v * (v - 1) / 2 + u);
+}
+
+// inverse of tri_index; t < 2^33
+__host__ __device__ inline void tri_decode(u64 t, int64_t* u, int64_t* v) {
+  double s = sqrt(1.0 + 8.0 * (double)t);
+  int64_t vv = (int64_t)((1.0 + s) * 0.5);
+  while (vv * (vv - 1) / 2 > (int64_t)t) vv--;
+  while ((vv + 1) * vv / 2 <= (int64_t)t) vv++;
+  *v = vv;
+  *u = (int64_t)t - vv * (vv - 1) / 2;
+}
+
+struct KeySpec {
+  int shift;     // 32 (weights) or 33 (points)
+  bool points;   // key weight is bits(d^2)
+  int sense;     // +1 minimax, -1 widest (weights only)
+};
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct NcclApi;  // nccl_shim.cpp
+
+}  // namespace appd
+
+struct appd_ctx {
+  appd_options opt;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool poisoned = false;
+  std::string last_error;
+  int64_t err_i = -1, err_j = -1;
+  appd_stats stats;
+  int64_t launches = 0;  // kernels launched in the current solve
+  void* nccl_comm = nullptr;
+  int sm_count = 148;
+  // workspace (grown on demand)
+  appd::DevBuf buf[32];
+  // host-side copies of the last dendrogram
+  std::vector<int32_t> last_pi;
+  std::vector<float> last_h;
+  bool have_dendrogram = false;
+  // events for stage timing
+  cudaEvent_t ev[16];
+  bool ev_ready = false;
+  // pinned host staging for host-buffer calls
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+namespace appd {
+
+// workspace slots
+enum Slot {
+  S_COMP = 0, S_COMPBEST, S_LINK, S_PARENT, S_NEWID, S_FLAGS, S_MSTKEYS, S_MSTKEYS_SORTED, S_COUNTERS,
+  S_XT, S_PI, S_POS, S_H, S_ST, S_ROWS_SORTED, S_ROWPOS, S_TMP, S_TMP2, S_VALID, S_KEYS_TMP, S_PRIM,
+  S_HOST_IN, S_HOST_OUT, S_NSLOTS
+};
+
+void* ws(appd_ctx* c, int slot, size_t bytes);  // grows; returns nullptr on OOM
+appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...);
+appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
+
+#define APPD_CUDA(c, expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
+  } while (0)
+
+#define APPD_LAUNCHED(c)                                                     \
+  do {                                                                       \
+    (c)->launches++;                                                         \
+    cudaError_t _e = cudaGetLastError();                                     \
+    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, "kernel launch");  \
+  } while (0)
+
+// ---- kernels (k_*.cu) ----
+// validation
+appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
+                                    u64* out3 /*device, 3 minima*/);
+appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64_t d, u64* out3);
+
+// Boruvka
+appd_status launch_scan_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
+                                const int* comp, u64* compbest, int sense);
+appd_status launch_transpose_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* XT, int64_t npad,
+                                    int64_t dpad);
+appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
+                               int64_t rows, const int* comp, u64* compbest);
+appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v);
+appd_status launch_iota(appd_ctx* c, int* p, int64_t count);
+appd_status launch_hook(appd_ctx* c, const u64* compbest, int64_t k, const int* comp, int shift, int* link);
+appd_status launch_mutual(appd_ctx* c, const u64* compbest, int64_t k, const int* link, int* parent,
+                          u64* mstkeys, int* counters /*[0]=mst count*/);
+appd_status launch_jump(appd_ctx* c, int* parent, int64_t k, int* flags);
+appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent, const int* newid);
+
+// fill
+appd_status launch_positions(appd_ctx* c, const int* pi, int64_t n, int* pos);
+appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, int64_t stride, int widest);
+appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
+                        const float* ST, int64_t stride, int64_t n, float* M, int64_t row0, int widest);
+appd_status launch_sqrt_inplace(appd_ctx* c, float* h, int64_t m);
+appd_status launch_set_diag_zero_single(appd_ctx* c, float* M);
+appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,
+                                  float* Wb);
+appd_status launch_gather_rowpos(appd_ctx* c, const int* pos, int64_t row0, int64_t rows, int* keys, int* vals);
+
+// Prim (single CTA)
+appd_status launch_prim_points(appd_ctx* c, const float* X, int64_t n, int64_t d, int* pi, float* h, void* scratch);
+appd_status launch_prim_weights(appd_ctx* c, const float* W, int64_t n, int sense, int* pi, float* h, void* scratch);
+int prim_max_n();
+
+// sorting (CUB)
+appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count);
+appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count);
+appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t count);
+
+// host dendrogram (dendrogram_host.cpp)
+void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32_t* pi, float* h);
+
+// NCCL (nccl_shim.cpp)
+appd_status nccl_unique_id(uint8_t out[128], std::string* err);
+appd_status nccl_init(appd_ctx* c, const uint8_t* id, int rank, int world);
+appd_status nccl_allreduce_min_u64(appd_ctx* c, u64* buf, int64_t count);
+appd_status nccl_allreduce_max_u64(appd_ctx* c, u64* buf, int64_t count);
+void nccl_destroy(appd_ctx* c);
+
+}  // namespace appd

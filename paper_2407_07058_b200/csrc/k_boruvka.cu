@@ -1,0 +1,436 @@
+// k_boruvka.cu -- the MST stage: Boruvka rounds.
+//
+// P:L98 (§3) builds the MST with Prim; any MST gives the same APPD (P:L79,
+// "the path between any two nodes in a minimum spanning tree (MST) is a minimax
+// path", and DESIGN.md reading Q2), so the GPU uses Boruvka: each round every
+// row finds its lightest edge leaving its component (a row-parallel, coalesced
+// component-filtered argmin), components take the minimum over their rows, and
+// the chosen edges merge components.  At most ceil(log2 n) rounds.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "internal.cuh"
+
+namespace appd {
+
+// ---------------------------------------------------------------------------
+// weights mode: one CTA per row (grid-stride), float4 loads of W's row, the
+// component labels of the columns come from L2 (n x 4 B, resident).
+// Per thread: best (w, j) with strict "<" so the smallest j wins ties (columns
+// are visited in increasing order per thread); then a (key) min over the CTA.
+// ---------------------------------------------------------------------------
+template <bool ROUND0, int SENSE>
+__global__ void __launch_bounds__(256) k_scan_weights(const float* __restrict__ W, int64_t n, int64_t row0,
+                                                      int64_t rows, const int* __restrict__ comp,
+                                                      u64* __restrict__ compbest) {
+  __shared__ u64 red[8];
+  const bool vec = (n & 3) == 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t i = row0 + r;
+    const float* Wr = W + r * n;
+    const int ci = ROUND0 ? (int)i : comp[i];
+    float bw = SENSE > 0 ? INFINITY : -INFINITY;
+    int64_t bj = -1;
+    if (vec) {
+      const float4* W4 = reinterpret_cast<const float4*>(Wr);
+      const int4* C4 = reinterpret_cast<const int4*>(comp);
+      const int64_t n4 = n >> 2;
+#pragma unroll 4
+      for (int64_t q = threadIdx.x; q < n4; q += 256) {
+        float4 w = __ldcs(W4 + q);  // streamed once per round: evict-first
+        int4 cc;
+        if (!ROUND0) cc = __ldg(C4 + q);
+        const int64_t j = q * 4;
+        float ws[4] = {w.x, w.y, w.z, w.w};
+        int cs[4];
+        if (!ROUND0) { cs[0] = cc.x; cs[1] = cc.y; cs[2] = cc.z; cs[3] = cc.w; }
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          bool elig = ROUND0 ? (j + t != i) : (cs[t] != ci);
+          bool better = SENSE > 0 ? (ws[t] < bw) : (ws[t] > bw);
+          if (elig && better) { bw = ws[t]; bj = j + t; }
+        }
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < n; j += 256) {
+        float w = __ldcs(Wr + j);
+        bool elig = ROUND0 ? (j != i) : (__ldg(comp + j) != ci);
+        bool better = SENSE > 0 ? (w < bw) : (w > bw);
+        if (elig && better) { bw = w; bj = j; }
+      }
+    }
+    // row key (weight, j): weight mapped to the orderable u32 of the minimised quantity
+    u64 key = KEY_NONE;
+    if (bj >= 0) {
+      float m = SENSE > 0 ? bw : -bw;
+      m = m + 0.0f;  // -0 -> +0 (reading Q5)
+      key = ((u64)orderable(m) << 32) | (u64)bj;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      u64 other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other < key ? other : key;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 k = red[0];
+#pragma unroll
+      for (int t = 1; t < 8; t++) k = red[t] < k ? red[t] : k;
+      if (k != KEY_NONE) {
+        int64_t j = (int64_t)(k & 0xFFFFFFFFull);
+        u64 gkey = (k & 0xFFFFFFFF00000000ull) | tri_index(i, j);
+        atomicMin(compbest + ci, gkey);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+appd_status launch_scan_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
+                                const int* comp, u64* compbest, int sense) {
+  int grid = (int)(rows < (int64_t)c->sm_count * 8 ? rows : (int64_t)c->sm_count * 8);
+  if (grid < 1) grid = 1;
+  if (comp == nullptr) {
+    if (sense > 0) k_scan_weights<true, 1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, comp, compbest);
+    else k_scan_weights<true, -1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, comp, compbest);
+  } else {
+    if (sense > 0) k_scan_weights<false, 1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, comp, compbest);
+    else k_scan_weights<false, -1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, comp, compbest);
+  }
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// points mode: X is first transposed to XT[dpad][npad] (zero padded: a zero
+// coordinate adds fmaf(0,0,acc) = acc exactly, so padding d changes nothing).
+// A CTA owns 128 rows and sweeps a range of 128-column tiles; each thread owns
+// an 8x8 micro-tile of squared distances, accumulated over k = 0..d-1 in order
+// with the pinned R1 chain  t = x_ik - x_jk (RN), acc = fma(t, t, acc) (RN),
+// written with __fsub_rn/__fmaf_rn so no contraction can change it.
+// ---------------------------------------------------------------------------
+__global__ void k_transpose_points(const float* __restrict__ X, int64_t n, int64_t d, float* __restrict__ XT,
+                                   int64_t npad, int64_t dpad) {
+  __shared__ float tile[32][33];
+  int64_t i0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int64_t i = i0 + r, k = k0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < n && k < d) ? X[i * d + k] : 0.0f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    int64_t k = k0 + r, i = i0 + threadIdx.x;
+    if (k < dpad && i < npad) XT[k * npad + i] = tile[threadIdx.x][r];
+  }
+}
+
+appd_status launch_transpose_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* XT, int64_t npad,
+                                    int64_t dpad) {
+  dim3 grid((unsigned)(npad / 32), (unsigned)(dpad / 32));
+  k_transpose_points<<<grid, dim3(32, 8), 0, c->stream>>>(X, n, d, XT, npad, dpad);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+constexpr int PT_BM = 128, PT_BN = 128, PT_KC = 32;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <bool ROUND0>
+__global__ void __launch_bounds__(256, 2)
+    k_scan_points(const float* __restrict__ XT, int64_t n, int64_t npad, int dpad, int64_t row0, int64_t rows,
+                  int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest) {
+  extern __shared__ __align__(16) float smem[];
+  float* As = smem;                           // [2][KC][BM]
+  float* Bs = smem + 2 * PT_KC * PT_BM;       // [2][KC][BN]
+  int* ccol = (int*)(Bs + 2 * PT_KC * PT_BN); // [BN] component labels of the current column tile
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t rbase = row0 + (int64_t)blockIdx.x * PT_BM;
+  const int64_t total_col_tiles = npad / PT_BN;
+  const int64_t ct0 = (int64_t)blockIdx.y * col_tiles_per_cta;
+  int64_t ct1 = ct0 + col_tiles_per_cta;
+  if (ct1 > total_col_tiles) ct1 = total_col_tiles;
+  if (ct0 >= ct1) return;
+  const int nk = dpad / PT_KC;
+
+  int64_t ri[8];
+  int cr[8];
+  float bd[8];
+  int64_t bj[8];
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    ri[a] = rbase + ty * 8 + a;
+    cr[a] = ROUND0 ? (int)ri[a] : ((ri[a] < n) ? comp[ri[a]] : -1);
+    bd[a] = INFINITY;
+    bj[a] = -1;
+  }
+
+  // stage loader: chunk index s = tile_local * nk + kc
+  auto load_stage = [&](int64_t s, int buf) {
+    int64_t ct = ct0 + s / nk;
+    int kc = (int)(s % nk);
+    const float* ga = XT + (int64_t)(kc * PT_KC) * npad + rbase;
+    const float* gb = XT + (int64_t)(kc * PT_KC) * npad + ct * PT_BN;
+    float* sa = As + buf * PT_KC * PT_BM;
+    float* sb = Bs + buf * PT_KC * PT_BN;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      int e = threadIdx.x + q * 256;  // 1024 float4 per operand
+      int k = e >> 5, c4 = (e & 31) * 4;
+      cp_async16(sa + k * PT_BM + c4, ga + (int64_t)k * npad + c4);
+      cp_async16(sb + k * PT_BN + c4, gb + (int64_t)k * npad + c4);
+    }
+  };
+
+  const int64_t nstages = (ct1 - ct0) * nk;
+  load_stage(0, 0);
+  cp_async_commit();
+  float acc[8][8];
+  for (int64_t s = 0; s < nstages; s++) {
+    const int buf = (int)(s & 1);
+    const int kc = (int)(s % nk);
+    const int64_t ct = ct0 + s / nk;
+    if (kc == 0) {
+#pragma unroll
+      for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 8; b++) acc[a][b] = 0.0f;
+    }
+    if (s + 1 < nstages) load_stage(s + 1, buf ^ 1);
+    cp_async_commit();
+    if (kc == 0 && !ROUND0) {
+      // labels of this column tile (previous readers finished at the last __syncthreads)
+      int64_t j = ct * PT_BN + (threadIdx.x & 127);
+      if (threadIdx.x < 128) ccol[threadIdx.x] = (j < n) ? comp[j] : -2;
+    }
+    cp_async_wait<1>();
+    __syncthreads();
+    const float* sa = As + buf * PT_KC * PT_BM;
+    const float* sb = Bs + buf * PT_KC * PT_BN;
+#pragma unroll 4
+    for (int k = 0; k < PT_KC; k++) {
+      float4 a0 = *reinterpret_cast<const float4*>(sa + k * PT_BM + ty * 8);
+      float4 a1 = *reinterpret_cast<const float4*>(sa + k * PT_BM + ty * 8 + 4);
+      float4 b0 = *reinterpret_cast<const float4*>(sb + k * PT_BN + tx * 8);
+      float4 b1 = *reinterpret_cast<const float4*>(sb + k * PT_BN + tx * 8 + 4);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          float t = __fsub_rn(av[a], bv[b]);
+          acc[a][b] = __fmaf_rn(t, t, acc[a][b]);
+        }
+    }
+    if (kc == nk - 1) {
+      // epilogue of this column tile: component-filtered running argmin per row.
+      // Columns are visited in increasing j per thread, so strict '<' keeps the
+      // smallest j among equal distances.
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        int64_t j = ct * PT_BN + tx * 8 + b;
+        int cj = ROUND0 ? 0 : ccol[tx * 8 + b];
+#pragma unroll
+        for (int a = 0; a < 8; a++) {
+          bool elig = ROUND0 ? (j < n && j != ri[a]) : (cj != cr[a] && cj >= 0);
+          if (elig && acc[a][b] < bd[a]) { bd[a] = acc[a][b]; bj[a] = j; }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  // reduce (d2, j) over the 16 threads sharing each row (lanes differing in tx)
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    u64 key = bj[a] >= 0 ? (((u64)__float_as_uint(bd[a]) << 32) | (u64)bj[a]) : KEY_NONE;
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      u64 other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other < key ? other : key;
+    }
+    if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) {
+      int64_t j = (int64_t)(key & 0xFFFFFFFFull);
+      u64 d2bits = (key >> 32) & 0x7FFFFFFFull;
+      u64 gkey = (d2bits << 33) | tri_index(ri[a], j);
+      atomicMin(compbest + cr[a], gkey);
+    }
+  }
+}
+
+appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
+                               int64_t rows, const int* comp, u64* compbest) {
+  const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_scan_points<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
+  int64_t col_tiles = npad / PT_BN;
+  // enough CTAs for ~4 waves of 2 CTAs/SM; split the column range accordingly
+  int64_t want = (int64_t)c->sm_count * 2 * 4;
+  int64_t splits = (want + row_blocks - 1) / row_blocks;
+  if (splits > col_tiles) splits = col_tiles;
+  if (splits < 1) splits = 1;
+  int64_t per = (col_tiles + splits - 1) / splits;
+  splits = (col_tiles + per - 1) / per;
+  dim3 grid((unsigned)row_blocks, (unsigned)splits);
+  if (comp == nullptr)
+    k_scan_points<true><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp,
+                                                       compbest);
+  else
+    k_scan_points<false><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp,
+                                                        compbest);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// component step: hook, break mutual pairs, pointer-jump, compact, relabel
+// ---------------------------------------------------------------------------
+__global__ void k_fill_u64(u64* p, int64_t count, u64 v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v) {
+  int grid = (int)((count + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  if (grid < 1) grid = 1;
+  k_fill_u64<<<grid, 256, 0, c->stream>>>(p, count, v);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+__global__ void k_iota(int* p, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int)i;
+}
+appd_status launch_iota(appd_ctx* c, int* p, int64_t count) {
+  int grid = (int)((count + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  if (grid < 1) grid = 1;
+  k_iota<<<grid, 256, 0, c->stream>>>(p, count);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// link[c] = the component at the other end of c's chosen edge
+__global__ void k_hook(const u64* __restrict__ compbest, int64_t k, const int* __restrict__ comp, int shift,
+                       int* __restrict__ link) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  u64 key = compbest[c];
+  if (key == KEY_NONE) { link[c] = (int)c; return; }
+  int64_t u, v;
+  tri_decode(key & ((1ull << shift) - 1), &u, &v);
+  int cu = comp[u], cv = comp[v];
+  link[c] = (cu == (int)c) ? cv : cu;
+}
+appd_status launch_hook(appd_ctx* c, const u64* compbest, int64_t k, const int* comp, int shift, int* link) {
+  k_hook<<<(unsigned)((k + 255) / 256), 256, 0, c->stream>>>(compbest, k, comp, shift, link);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// Under a strict edge order, the only cycles among chosen edges are 2-cycles
+// (c -> o -> c, the same edge).  The smaller id becomes the root; the edge is
+// recorded once (by the smaller id).  Every other chosen edge is a new MST edge.
+__global__ void k_mutual(const u64* __restrict__ compbest, int64_t k, const int* __restrict__ link,
+                         int* __restrict__ parent, u64* __restrict__ mstkeys, int* __restrict__ counters) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  int o = link[c];
+  if (o == (int)c) { parent[c] = (int)c; return; }
+  bool mutual = link[o] == (int)c;
+  if (mutual && (int)c < o) {
+    parent[c] = (int)c;
+  } else {
+    parent[c] = o;
+  }
+  if (!(mutual && (int)c > o)) {
+    int slot = atomicAdd(counters, 1);
+    mstkeys[slot] = compbest[c];
+  }
+}
+appd_status launch_mutual(appd_ctx* c, const u64* compbest, int64_t k, const int* link, int* parent, u64* mstkeys,
+                          int* counters) {
+  k_mutual<<<(unsigned)((k + 255) / 256), 256, 0, c->stream>>>(compbest, k, link, parent, mstkeys, counters);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// pointer jumping to the root; flags[c] = (c is a root)
+__global__ void k_jump(int* parent, int64_t k, int* flags) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  int p = parent[c];
+  while (true) {
+    int pp = parent[p];
+    if (pp == p) break;
+    p = pp;
+  }
+  parent[c] = p;  // concurrent readers see either the old ancestor or the root
+  flags[c] = (p == (int)c) ? 1 : 0;
+}
+appd_status launch_jump(appd_ctx* c, int* parent, int64_t k, int* flags) {
+  k_jump<<<(unsigned)((k + 255) / 256), 256, 0, c->stream>>>(parent, k, flags);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+__global__ void k_relabel(int* comp, int64_t n, const int* __restrict__ parent, const int* __restrict__ newid) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    comp[i] = newid[parent[comp[i]]];
+}
+appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent, const int* newid) {
+  int grid = (int)((n + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  k_relabel<<<grid, 256, 0, c->stream>>>(comp, n, parent, newid);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CUB wrappers
+// ---------------------------------------------------------------------------
+appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, (int)count, 0, 64, c->stream);
+  void* t = ws(c, S_KEYS_TMP, tmp + 16);
+  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
+  APPD_CUDA(c, cub::DeviceRadixSort::SortKeys(t, tmp, in, out, (int)count, 0, 64, c->stream));
+  c->launches += 4;
+  return APPD_OK;
+}
+
+appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)count, 0, 32, c->stream);
+  void* t = ws(c, S_KEYS_TMP, tmp + 16);
+  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
+  APPD_CUDA(c, cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)count, 0, 32, c->stream));
+  c->launches += 4;
+  return APPD_OK;
+}
+
+appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t count) {
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)count, c->stream);
+  void* t = ws(c, S_TMP2, tmp + 16);
+  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "scan workspace");
+  APPD_CUDA(c, cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int)count, c->stream));
+  c->launches += 2;
+  return APPD_OK;
+}
+
+}  // namespace appd

@@ -1,0 +1,222 @@
+// k_fill.cu -- the APPD fill.
+//
+// Algorithm 4 writes, for each removed MST edge, its weight into every cell of
+// tree1 x tree2, each cell exactly once.  Equivalently (DESIGN.md
+// "leaf order"), with a leaf order pi of the single-linkage dendrogram and
+// h[a] = M[pi_a][pi_{a+1}]:   M[pi_a][pi_b] = max(h[min(a,b) .. max(a,b)-1]).
+//
+// The fill processes a tile of rows that are consecutive in leaf order
+// (positions a_0 < ... < a_{R-1}) against a block of columns in ORIGINAL order
+// (so every store is a coalesced 128-bit row segment).  For a column j at
+// position b:
+//   b >  a_{R-1}:  M[row t][j] = max( S[t], RMQ(a_{R-1}, b) ),  S[t] = RMQ(a_t, a_{R-1})
+//   b <  a_0:      M[row t][j] = max( P[t], RMQ(b, a_0) ),      P[t] = RMQ(a_0, a_t)
+//   otherwise:     M = RMQ(min(a_t,b), max(a_t,b)), 0 on the diagonal (b == a_t)
+// so the inner loop is one select + one max per element: the kernel is bound by
+// HBM write bandwidth (n^2 * 4 bytes).  RMQ is a sparse table over h
+// (ST[k][i] = max h[i .. i+2^k-1]).  Widest sense: min instead of max.
+#include "internal.cuh"
+
+namespace appd {
+
+__global__ void k_positions(const int* __restrict__ pi, int64_t n, int* __restrict__ pos) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+    pos[pi[a]] = (int)a;
+}
+appd_status launch_positions(appd_ctx* c, const int* pi, int64_t n, int* pos) {
+  int grid = (int)((n + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  k_positions<<<grid, 256, 0, c->stream>>>(pi, n, pos);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+__global__ void k_sqrt_inplace(float* h, int64_t m) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < m; a += (int64_t)gridDim.x * blockDim.x)
+    h[a] = __fsqrt_rn(h[a]);
+}
+appd_status launch_sqrt_inplace(appd_ctx* c, float* h, int64_t m) {
+  if (m <= 0) return APPD_OK;
+  int grid = (int)((m + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  k_sqrt_inplace<<<grid, 256, 0, c->stream>>>(h, m);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// level k from level k-1 (level 0 = h, already in place)
+template <bool WIDEST>
+__global__ void k_st_level(float* ST, int64_t m, int64_t stride, int k) {
+  const int64_t half = 1ll << (k - 1);
+  const float* prev = ST + (int64_t)(k - 1) * stride;
+  float* cur = ST + (int64_t)k * stride;
+  const int64_t cnt = m - (1ll << k) + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    float a = prev[i], b = prev[i + half];
+    cur[i] = WIDEST ? fminf(a, b) : fmaxf(a, b);
+  }
+}
+appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, int64_t stride, int widest) {
+  for (int k = 1; k < levels; k++) {
+    int64_t cnt = m - (1ll << k) + 1;
+    int grid = (int)((cnt + 255) / 256);
+    if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+    if (grid < 1) grid = 1;
+    if (widest) k_st_level<true><<<grid, 256, 0, c->stream>>>(ST, m, stride, k);
+    else k_st_level<false><<<grid, 256, 0, c->stream>>>(ST, m, stride, k);
+    APPD_LAUNCHED(c);
+  }
+  return APPD_OK;
+}
+
+template <bool WIDEST>
+__device__ __forceinline__ float comb(float a, float b) {
+  return WIDEST ? fminf(a, b) : fmaxf(a, b);
+}
+
+// RMQ over h[l .. r-1], l < r
+template <bool WIDEST>
+__device__ __forceinline__ float rmq(const float* __restrict__ ST, int64_t stride, int l, int r) {
+  int len = r - l;
+  int k = 31 - __clz(len);
+  float a = __ldg(ST + (int64_t)k * stride + l);
+  float b = __ldg(ST + (int64_t)k * stride + r - (1 << k));
+  return comb<WIDEST>(a, b);
+}
+
+constexpr int FILL_THREADS = 256;
+constexpr int FILL_R = 128;  // rows per tile (consecutive in leaf order)
+
+template <int VEC, bool WIDEST>
+__global__ void __launch_bounds__(FILL_THREADS)
+    k_fill(const int* __restrict__ rows_sorted, const int* __restrict__ rowpos, int64_t nrows,
+           const int* __restrict__ pos, const float* __restrict__ ST, int64_t stride, int64_t n,
+           float* __restrict__ M, int64_t row0) {
+  __shared__ float sS[FILL_R], sP[FILL_R];
+  __shared__ int64_t sOff[FILL_R];
+  __shared__ int sA[FILL_R];
+  const float ID = WIDEST ? INFINITY : -INFINITY;
+  const int64_t t0 = (int64_t)blockIdx.y * FILL_R;
+  int R = (int)((nrows - t0) < FILL_R ? (nrows - t0) : FILL_R);
+  const int aL = rowpos[t0], aR = rowpos[t0 + R - 1];
+  if (threadIdx.x < R) {
+    int t = threadIdx.x;
+    int at = rowpos[t0 + t];
+    sA[t] = at;
+    sOff[t] = ((int64_t)rows_sorted[t0 + t] - row0) * n;
+    sS[t] = (at < aR) ? rmq<WIDEST>(ST, stride, at, aR) : ID;
+    sP[t] = (at > aL) ? rmq<WIDEST>(ST, stride, aL, at) : ID;
+  }
+  // this thread's VEC columns
+  const int64_t jbase = (int64_t)blockIdx.x * (FILL_THREADS * VEC) + (int64_t)threadIdx.x * VEC;
+  int b[VEC];
+  float base[VEC];
+  int side[VEC];  // 0 right (use S), 1 left (use P), 2 inside
+  bool any_inside = false;
+#pragma unroll
+  for (int q = 0; q < VEC; q++) {
+    int64_t j = jbase + q;
+    int bb = (j < n) ? __ldg(pos + j) : aL;
+    b[q] = bb;
+    if (bb > aR) { side[q] = 0; base[q] = rmq<WIDEST>(ST, stride, aR, bb); }
+    else if (bb < aL) { side[q] = 1; base[q] = rmq<WIDEST>(ST, stride, bb, aL); }
+    else { side[q] = 2; base[q] = ID; any_inside = true; }
+  }
+  const bool warp_inside = __any_sync(0xffffffffu, any_inside);
+  const bool in_range = jbase < n;
+  __syncthreads();
+#pragma unroll 4
+  for (int t = 0; t < R; t++) {
+    const float S = sS[t], P = sP[t];
+    float v[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; q++) v[q] = comb<WIDEST>(side[q] == 0 ? S : P, base[q]);
+    if (warp_inside) {
+      const int at = sA[t];
+#pragma unroll
+      for (int q = 0; q < VEC; q++) {
+        if (side[q] == 2) {
+          int bb = b[q];
+          v[q] = (bb == at) ? 0.0f : (bb < at ? rmq<WIDEST>(ST, stride, bb, at) : rmq<WIDEST>(ST, stride, at, bb));
+        }
+      }
+    }
+    float* dst = M + sOff[t] + jbase;
+    if (VEC == 4) {
+      if (in_range) __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; q++)
+        if (jbase + q < n) __stcs(dst + q, v[q]);
+    }
+  }
+}
+
+appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
+                        const float* ST, int64_t stride, int64_t n, float* M, int64_t row0, int widest) {
+  if (nrows <= 0) return APPD_OK;
+  const bool vec4 = (n % 4) == 0 && ((uintptr_t)M % 16) == 0;
+  const int cols_per_cta = FILL_THREADS * (vec4 ? 4 : 1);
+  dim3 grid((unsigned)((n + cols_per_cta - 1) / cols_per_cta), (unsigned)((nrows + FILL_R - 1) / FILL_R));
+  if (grid.y > 65535u) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
+  if (vec4) {
+    if (widest) k_fill<4, true><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<4, false><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  } else {
+    if (widest) k_fill<1, true><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<1, false><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  }
+  APPD_LAUNCHED(c);
+  c->stats.fill_launches++;
+  return APPD_OK;
+}
+
+// rows [row0, row0+rows) of this rank: keys = positions, vals = row ids (sorted later)
+__global__ void k_gather_rowpos(const int* __restrict__ pos, int64_t row0, int64_t rows, int* keys, int* vals) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    keys[r] = pos[row0 + r];
+    vals[r] = (int)(row0 + r);
+  }
+}
+appd_status launch_gather_rowpos(appd_ctx* c, const int* pos, int64_t row0, int64_t rows, int* keys, int* vals) {
+  int grid = (int)((rows + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  if (grid < 1) grid = 1;
+  k_gather_rowpos<<<grid, 256, 0, c->stream>>>(pos, row0, rows, keys, vals);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+__global__ void k_zero1(float* M) { M[0] = 0.0f; }
+appd_status launch_set_diag_zero_single(appd_ctx* c, float* M) {
+  k_zero1<<<1, 1, 0, c->stream>>>(M);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// K11 test hook: R1 weights of a row block, the same pinned chain as the MST scan
+__global__ void k_points_weights(const float* __restrict__ X, int64_t n, int64_t d, int64_t row0, int64_t rows,
+                                 float* __restrict__ Wb) {
+  int64_t total = rows * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / n, j = e % n, i = row0 + r;
+    float acc = 0.0f;
+    for (int64_t k = 0; k < d; k++) {
+      float t = __fsub_rn(X[i * d + k], X[j * d + k]);
+      acc = __fmaf_rn(t, t, acc);
+    }
+    Wb[e] = (i == j) ? 0.0f : __fsqrt_rn(acc);
+  }
+}
+appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,
+                                  float* Wb) {
+  int64_t total = rows * n;
+  int grid = (int)((total + 255) / 256);
+  if (grid > c->sm_count * 16) grid = c->sm_count * 16;
+  if (grid < 1) grid = 1;
+  k_points_weights<<<grid, 256, 0, c->stream>>>(X, n, d, row0, rows, Wb);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd

@@ -1,0 +1,101 @@
+// k_validate.cu -- ingest checks.
+// A valid weight matrix is finite, has a +-0 diagonal and is bitwise symmetric
+// after -0 -> +0 (reading Q5).  Each kernel records the first offender of each
+// kind in row-major order as a 64-bit linear index (atomicMin); the host picks
+// the earliest (ties: NONFINITE first).
+#include "internal.cuh"
+
+namespace appd {
+
+__device__ __forceinline__ uint32_t canon_bits(float w) { return __float_as_uint(w + 0.0f); }
+
+// 32x32 tile pairs (I,J) and (J,I), I <= J, inside the square [row0, row0+rows)^2
+// of global indices; W is the rank's row block (rows x n, first row = row0).
+__global__ void k_validate_square(const float* __restrict__ W, int64_t n, int64_t row0, int64_t rows,
+                                  int64_t tiles, u64* __restrict__ out3) {
+  __shared__ float a[32][33];
+  __shared__ float b[32][33];
+  // map blockIdx.x to (I, J) with I <= J over a T x T upper triangle
+  const int64_t p = blockIdx.x, T = tiles;
+  // pairs before row I: f(I) = I*T - I*(I-1)/2; largest I with f(I) <= p
+  double q = (double)(2 * T + 1);
+  int64_t I = (int64_t)((q - sqrt(q * q - 8.0 * (double)p)) * 0.5);
+  if (I < 0) I = 0;
+  while (I > 0 && I * T - I * (I - 1) / 2 > p) I--;
+  while ((I + 1) * T - (I + 1) * I / 2 <= p) I++;
+  int64_t J = I + (p - (I * T - I * (I - 1) / 2));
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    int64_t li = I * 32 + r, lj = J * 32 + tx;  // local square coords
+    a[r][tx] = (li < rows && lj < rows) ? W[li * n + row0 + lj] : 0.0f;
+    int64_t mi = J * 32 + r, mj = I * 32 + tx;
+    b[r][tx] = (mi < rows && mj < rows) ? W[mi * n + row0 + mj] : 0.0f;
+  }
+  __syncthreads();
+  u64 bad_nf = KEY_NONE, bad_diag = KEY_NONE, bad_sym = KEY_NONE;
+  for (int r = ty; r < 32; r += 8) {
+    int64_t li = I * 32 + r, lj = J * 32 + tx;
+    if (li < rows && lj < rows) {
+      int64_t gi = row0 + li, gj = row0 + lj;
+      float x = a[r][tx];           // W[gi][gj]
+      float y = b[tx][r];           // W[gj][gi]
+      u64 idx = (u64)(gi * n + gj);
+      u64 idxT = (u64)(gj * n + gi);
+      if (!isfinite(x)) bad_nf = min(bad_nf, idx);
+      if (!isfinite(y)) bad_nf = min(bad_nf, idxT);
+      if (gi == gj) {
+        if (x != 0.0f) bad_diag = min(bad_diag, idx);
+      } else if (canon_bits(x) != canon_bits(y)) {
+        bad_sym = min(bad_sym, gi < gj ? idx : idxT);
+      }
+    }
+  }
+  if (bad_nf != KEY_NONE) atomicMin(out3 + 0, bad_nf);
+  if (bad_diag != KEY_NONE) atomicMin(out3 + 1, bad_diag);
+  if (bad_sym != KEY_NONE) atomicMin(out3 + 2, bad_sym);
+}
+
+// finiteness of the columns outside the diagonal square (world > 1)
+__global__ void k_validate_finite_rest(const float* __restrict__ W, int64_t n, int64_t row0, int64_t rows,
+                                       u64* __restrict__ out3) {
+  int64_t total = rows * n;
+  u64 bad = KEY_NONE;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / n, j = e % n;
+    if (j >= row0 && j < row0 + rows) continue;
+    if (!isfinite(W[e])) bad = min(bad, (u64)((row0 + r) * n + j));
+  }
+  if (bad != KEY_NONE) atomicMin(out3 + 0, bad);
+}
+
+appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows, u64* out3) {
+  int64_t T = (rows + 31) / 32;
+  int64_t pairs = T * (T + 1) / 2;
+  if (pairs > 0x7FFFFFFFll) return fail(c, APPD_ERR_UNSUPPORTED, "validation grid too large");
+  k_validate_square<<<(unsigned)pairs, dim3(32, 8), 0, c->stream>>>(W, n, row0, rows, T, out3);
+  APPD_LAUNCHED(c);
+  if (rows < n) {
+    k_validate_finite_rest<<<c->sm_count * 8, 256, 0, c->stream>>>(W, n, row0, rows, out3);
+    APPD_LAUNCHED(c);
+  }
+  return APPD_OK;
+}
+
+__global__ void k_validate_points(const float* __restrict__ X, int64_t total, u64* __restrict__ out3) {
+  u64 bad = KEY_NONE;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(X[e])) bad = min(bad, (u64)e);
+  if (bad != KEY_NONE) atomicMin(out3, bad);
+}
+
+appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64_t d, u64* out3) {
+  int64_t total = n * d;
+  int grid = (int)((total + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  if (grid < 1) grid = 1;
+  k_validate_points<<<grid, 256, 0, c->stream>>>(X, total, out3);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd

@@ -1,0 +1,291 @@
+"""GPU parity: libappd (through its C ABI) against the CPU oracle, bit-exact.
+
+The APPD is a function of W (unique, bit-unique after -0 -> +0; reading Q9), so
+every comparison is exact.  Points mode: the GPU's R1 weights (appd_points_weights)
+must equal the oracle's R1 bit-exactly and fp64 within 1e-5 relative, and the
+APPD is compared bit-exactly.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import generators as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def assert_bit_equal(got, want, what=""):
+    got = np.asarray(got, np.float32)
+    want = np.asarray(want, np.float32)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    bad = np.nonzero(bits(got) != bits(want))
+    if bad[0].size:
+        idx = tuple(b[0] for b in bad)
+        raise AssertionError(f"{what}: {bad[0].size} mismatching entries, first {idx}: gpu {got[idx]!r} oracle {want[idx]!r}")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2407_07058_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    c = P.Context(timing=True)
+    yield c
+    c.close()
+
+
+def gpu_weights(ctx, W, sense=1, c=None):
+    c = c or ctx
+    Wt = torch.from_numpy(np.ascontiguousarray(W, np.float32)).cuda()
+    return c.solve_weights(Wt).cpu().numpy()
+
+
+def gpu_points(ctx, X):
+    Xt = torch.from_numpy(np.ascontiguousarray(X, np.float32)).cuda()
+    return ctx.solve_points(Xt).cpu().numpy()
+
+
+def test_native_library_is_loaded(ctx):
+    ctx.solve_weights(torch.zeros((2, 2), device="cuda"))
+    maps = open("/proc/self/maps").read()
+    assert "libappd.so" in maps
+    st = ctx.stats()
+    assert st["kernel_launches"] > 0
+
+
+# --------------------------------------------------------------------------
+# weights mode
+# --------------------------------------------------------------------------
+def test_c1(ctx):
+    W = G.config("C1")
+    assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), "C1")
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties", "ints255", "negative", "signed_zero", "huge"])
+def test_random_weights(ctx, kind):
+    rs = np.random.default_rng(11)
+    sizes = [1, 2, 3, 4, 5, 7, 8, 31, 33, 127, 128, 129, 255, 257, 300, 513, 1000, 1024, 1031]
+    for t, n in enumerate(sizes):
+        W = G.random_weights(n, 100 + t, kind)
+        assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), f"{kind} n={n}")
+    for t in range(40):
+        n = int(rs.integers(2, 200))
+        W = G.random_weights(n, 500 + t, kind)
+        assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), f"{kind} n={n}")
+
+
+def test_widest_sense(P):
+    with P.Context(sense=-1) as cw:
+        for t, n in enumerate([2, 3, 17, 64, 255, 600]):
+            for kind in ("uniform", "ties", "negative"):
+                W = G.random_weights(n, t, kind)
+                assert_bit_equal(gpu_weights(None, W, c=cw), oracle.appd_weights(W, -1), f"widest {kind} n={n}")
+
+
+def test_c3_closed_form_and_oracle(ctx):
+    W = G.config("C3")
+    M = gpu_weights(ctx, W)
+    n = W.shape[0]
+    off = ~np.eye(n, dtype=bool)
+    assert (M[off] == 1.0).all()
+    assert (bits(np.diag(M)) == 0).all()
+    assert_bit_equal(M, oracle.appd_weights(W), "C3")
+
+
+# --------------------------------------------------------------------------
+# points mode
+# --------------------------------------------------------------------------
+def test_r1_weights_bitexact_and_fp64(ctx):
+    for name, X in [("C2", G.config("C2")), ("C4s", G.config("C4", n=1500)), ("C5s", G.config("C5", n=3000)),
+                    ("d7", G.random_points(700, 7, 1, "dups"))]:
+        Xt = torch.from_numpy(X).cuda()
+        n = X.shape[0]
+        rows = min(n, 512)
+        Wg = ctx.points_weights(Xt, 0, rows).cpu().numpy()
+        assert_bit_equal(Wg, oracle.points_weights(X, 0, rows), f"R1 {name}")
+        ref = np.sqrt(((X[:rows, None, :].astype(np.float64) - X[None, :, :].astype(np.float64)) ** 2).sum(-1))
+        nz = ref > 0
+        assert (Wg[~nz] == 0).all()
+        assert (np.abs(Wg[nz] - ref[nz]) / ref[nz]).max() <= 1e-5
+
+
+def test_c2(ctx):
+    X = G.config("C2")
+    assert_bit_equal(gpu_points(ctx, X), oracle.appd_points(X), "C2")
+
+
+@pytest.mark.parametrize("kind", ["uniform", "blobs", "dups", "grid", "wide"])
+def test_random_points(ctx, kind):
+    cases = [(1, 3), (2, 1), (3, 2), (5, 64), (64, 1), (127, 33), (128, 32), (129, 31), (300, 2), (513, 65),
+             (1000, 16), (1031, 70), (2048, 3)]
+    for t, (n, d) in enumerate(cases):
+        X = G.random_points(n, d, 40 + t, kind)
+        assert_bit_equal(gpu_points(ctx, X), oracle.appd_points(X), f"{kind} n={n} d={d}")
+
+
+def _check_golden(M_rows_fn, cfg, name):
+    path = os.path.join(GOLD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    g = json.load(open(path))
+    X = G.config(cfg)
+    assert oracle.fnv1a64(X) == g["input_fnv1a64"], "input generator drifted"
+    B = g["block_rows"]
+    r0 = g["row0"]
+    for bi, want in enumerate(g["row_block_fnv1a64"]):
+        rows = M_rows_fn(r0 + bi * B, min(B, g["rows"] - bi * B))
+        assert f"{oracle.fnv1a64(rows):016x}" == want, f"{cfg} row block {bi}"
+
+
+def _properties(M_gpu, X, h_sorted, rs_seed=0, samples=20000):
+    """Properties that hold at any size: symmetry, +0 diagonal, ultrametric, M <= W,
+    every value is a merge height (an MST weight)."""
+    n = X.shape[0]
+    rs = np.random.default_rng(rs_seed)
+    i, j, k = rs.integers(0, n, (3, samples))
+    idx_i = torch.from_numpy(i).cuda()
+    idx_j = torch.from_numpy(j).cuda()
+    idx_k = torch.from_numpy(k).cuda()
+    mij = M_gpu[idx_i, idx_j].cpu().numpy()
+    mji = M_gpu[idx_j, idx_i].cpu().numpy()
+    mik = M_gpu[idx_i, idx_k].cpu().numpy()
+    mkj = M_gpu[idx_k, idx_j].cpu().numpy()
+    assert (bits(mij) == bits(mji)).all()
+    assert (bits(M_gpu.diagonal()[:4096].cpu().numpy()) == 0).all()
+    assert (mij <= np.maximum(mik, mkj)).all()
+    for t in range(200):
+        a, b = int(i[t]), int(j[t])
+        w = 0.0 if a == b else float(oracle.r1_weight(X[a], X[b]))
+        assert mij[t] <= w
+    assert np.isin(mij[i != j], h_sorted).all()
+
+
+def test_c4_full(ctx):
+    X = G.config("C4")
+    Xt = torch.from_numpy(X).cuda()
+    M = ctx.solve_points(Xt)
+    pi, h = ctx.last_dendrogram(X.shape[0])
+    assert sorted(pi.tolist()) == list(range(X.shape[0]))
+    _properties(M, X, np.sort(h))
+    _check_golden(lambda r, c: M[r:r + c].cpu().numpy(), "C4", "C4.json")
+    del M
+    torch.cuda.empty_cache()
+
+
+def test_c5_full_single_gpu(ctx):
+    X = G.config("C5")
+    Xt = torch.from_numpy(X).cuda()
+    M = ctx.solve_points(Xt)
+    pi, h = ctx.last_dendrogram(X.shape[0])
+    assert (h == 0).sum() == 1311  # SURVEY §8(c) pin 5: exactly 1311 zero merge heights
+    _properties(M, X, np.sort(h))
+    for name in ("C5_r0.json", "C5_r65536.json"):
+        if os.path.exists(os.path.join(GOLD, name)):
+            _check_golden(lambda r, c: M[r:r + c].cpu().numpy(), "C5", name)
+    del M
+    torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------
+# boundary behaviour
+# --------------------------------------------------------------------------
+def test_validation_errors(P, ctx):
+    W = G.random_weights(50, 3, "uniform")
+    for (i, j, val, status) in [(3, 7, np.nan, "APPD_ERR_NONFINITE"), (10, 2, np.inf, "APPD_ERR_NONFINITE"),
+                                 (5, 9, 0.123, "APPD_ERR_NOT_SYMMETRIC"), (9, 5, 0.123, "APPD_ERR_NOT_SYMMETRIC"),
+                                 (4, 4, 1.0, "APPD_ERR_BAD_DIAGONAL")]:
+        Wb = W.copy()
+        Wb[i, j] = val
+        with pytest.raises(P.AppdError) as e:
+            gpu_weights(ctx, Wb)
+        assert e.value.name == status
+        want = (min(i, j), max(i, j)) if status == "APPD_ERR_NOT_SYMMETRIC" else (i, j)
+        assert e.value.index == want
+    # priority: non-finite, then diagonal, then symmetry; first offender in row-major order of its kind
+    Wb = W.copy()
+    Wb[20, 30] = np.nan
+    Wb[2, 40] = 5.0
+    Wb[1, 1] = 2.0
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights(ctx, Wb)
+    assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (20, 30)
+    Wb[20, 30] = Wb[30, 20]
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights(ctx, Wb)
+    assert e.value.name == "APPD_ERR_BAD_DIAGONAL" and e.value.index == (1, 1)
+    Wb[1, 1] = 0
+    Wb[7, 3] = 9.0
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights(ctx, Wb)
+    assert e.value.name == "APPD_ERR_NOT_SYMMETRIC" and e.value.index == (2, 40)
+    X = G.random_points(40, 3, 1)
+    X[7, 2] = np.nan
+    with pytest.raises(P.AppdError) as e:
+        gpu_points(ctx, X)
+    assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (7, 2)
+    # -0 diagonal and -0 weights are valid
+    Wz = G.random_weights(30, 2, "signed_zero")
+    assert_bit_equal(gpu_weights(ctx, Wz), oracle.appd_weights(Wz), "signed zero")
+
+
+def test_invalid_arguments(P, ctx):
+    Wh = torch.zeros((4, 4))
+    M = torch.empty((4, 4), device="cuda")
+    with pytest.raises(P.AppdError) as e:
+        ctx.solve_weights(Wh, M)  # host pointer
+    assert e.value.name == "APPD_ERR_INVALID_ARGUMENT"
+    L = P.load()
+    assert L.appd_solve_points(ctx._h, 0, 0, 2, 0) == 1
+    assert L.appd_solve_points(ctx._h, M.data_ptr(), 4, 0, M.data_ptr()) == 1
+
+
+def test_single_vertex(ctx):
+    assert_bit_equal(gpu_weights(ctx, np.zeros((1, 1), np.float32)), np.zeros((1, 1), np.float32))
+    assert_bit_equal(gpu_points(ctx, np.ones((1, 5), np.float32)), np.zeros((1, 1), np.float32))
+
+
+def test_host_buffer_calls(ctx):
+    X = G.random_points(777, 9, 3, "blobs")
+    Mh = torch.empty((777, 777)).pin_memory()
+    ctx.solve_points_host(torch.from_numpy(X).pin_memory(), Mh)
+    assert_bit_equal(Mh.numpy(), oracle.appd_points(X), "host points")
+    W = G.random_weights(301, 5, "ties")
+    Mw = torch.empty((301, 301))
+    ctx.solve_weights_host(torch.from_numpy(W), Mw)
+    assert_bit_equal(Mw.numpy(), oracle.appd_weights(W), "host weights")
+
+
+def test_no_validation_path(P):
+    with P.Context(validate=False) as c:
+        W = G.random_weights(200, 9, "ints255")
+        assert_bit_equal(gpu_weights(None, W, c=c), oracle.appd_weights(W))
+
+
+def test_dendrogram_hook_is_a_leaf_order(ctx):
+    """(pi, h) of the last solve reproduces the oracle through M[pi_a][pi_b] = max(h[a..b-1])."""
+    W = G.random_weights(300, 8, "ties")
+    M = gpu_weights(ctx, W)
+    pi, h = ctx.last_dendrogram(300)
+    Mo = oracle.appd_weights(W)
+    for a in range(0, 300, 7):
+        run = -np.inf
+        for b in range(a + 1, 300):
+            run = max(run, h[b - 1])
+            assert Mo[pi[a], pi[b]] == run
+    assert_bit_equal(M, Mo)
