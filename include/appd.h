@@ -85,7 +85,9 @@ typedef struct {
   int32_t sense;                 /* +1 minimax (default), -1 widest path (weights mode only) */
   int32_t timing;                /* 1 = record per-stage CUDA events (appd_get_stats), default 0 */
   int32_t dendrogram;            /* 0 auto, 1 host union-find, 2 GPU */
-  int32_t reserved[8];
+  int32_t points_engine;         /* points-mode MST scan: 0 auto, 1 exact FP32 (CUDA cores), 2 tensor-core
+                                    filter + exact recheck of the survivors (tcgen05) */
+  int32_t reserved[7];
 } appd_options;
 
 typedef struct {
@@ -99,6 +101,11 @@ typedef struct {
   int64_t kernel_launches; /* kernels launched by the last solve */
   int64_t fill_launches;   /* launches of the fill kernel in the last solve */
   int64_t fill_bytes;      /* bytes the fill wrote (algorithmic: rows * n * 4) */
+  int64_t tc_candidates;   /* points mode, tensor-core engine: survivors re-checked exactly (all rounds) */
+  int32_t points_engine;   /* engine used: 1 exact, 2 tensor core */
+  int32_t exact_rounds;    /* rounds that ran the exact scan (engine 1, or a candidate-buffer overflow) */
+  double ms_scan;          /* device time of the MST scan kernels (timing = 1) */
+  int64_t scan_launches;   /* launches of the MST scan kernels */
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */
@@ -136,6 +143,12 @@ appd_status appd_row_range_of(int64_t n, int32_t rank, int32_t world, int64_t* r
 /* R1 weights for rows [row0, row0+rows) of the complete graph of X (device, rows x n). */
 appd_status appd_points_weights(appd_ctx* ctx, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,
                                 float* Wblock);
+
+/* Test hook for the tensor-core engine: the raw fp32 accumulator of the first
+ * 128 (padded) rows against all columns (tc_out, 128 x npad, npad = n rounded up
+ * to 256) and a plain FP32 dot product of the same packed fp16 operands
+ * (ref_out, same shape).  Device pointers. */
+appd_status appd_debug_tc_gram(appd_ctx* ctx, const float* X, int64_t n, int64_t d, float* tc_out, float* ref_out);
 
 /* 128-byte ncclUniqueId for appd_options.nccl_unique_id (call on rank 0 only). */
 appd_status appd_get_nccl_unique_id(uint8_t out[128]);

@@ -44,7 +44,8 @@ class appd_options(ctypes.Structure):
         ("sense", ctypes.c_int32),
         ("timing", ctypes.c_int32),
         ("dendrogram", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 8),
+        ("points_engine", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 7),
     ]
 
 
@@ -68,6 +69,11 @@ class appd_stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("fill_launches", ctypes.c_int64),
         ("fill_bytes", ctypes.c_int64),
+        ("tc_candidates", ctypes.c_int64),
+        ("points_engine", ctypes.c_int32),
+        ("exact_rounds", ctypes.c_int32),
+        ("ms_scan", ctypes.c_double),
+        ("scan_launches", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -173,7 +179,7 @@ class Context:
 
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  variant: int = VARIANT_AUTO, validate: bool = True, sense: int = 1, timing: bool = False,
-                 dendrogram: int = 0):
+                 dendrogram: int = 0, points_engine: int = 0):
         L = load()
         o = appd_options()
         L.appd_options_init(ctypes.byref(o))
@@ -189,6 +195,7 @@ class Context:
         o.sense = sense
         o.timing = 1 if timing else 0
         o.dendrogram = dendrogram
+        o.points_engine = points_engine
         h = ctypes.c_void_p()
         s = L.appd_create(ctypes.byref(h), ctypes.byref(o))
         if s != APPD_OK:

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -337,13 +338,32 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   float* XT = nullptr;
   int64_t npad = 0, dpad = 0;
   appd_status s;
-  if (points) {
+  // points mode: tensor-core filter (engine 2) unless the exact engine is requested or
+  // the dimension does not fit the shared-memory ring
+  TcState tc;
+  bool use_tc = false;
+  if (points && c->opt.points_engine != 1 && n >= 2) {
+    s = tcf_prepare(c, X, n, d, &tc);
+    if (s == APPD_OK) use_tc = true;
+    else if (s != APPD_ERR_UNSUPPORTED || c->opt.points_engine == 2) return s;
+    c->last_error.clear();
+  }
+  c->stats.points_engine = points ? (use_tc ? 2 : 1) : 0;
+  int64_t rt_begin = 0, rt_end = 0;
+  if (use_tc) {
+    const int64_t T = tcf_row_tiles(&tc);
+    rt_begin = T * c->opt.rank / c->opt.world;
+    rt_end = T * (c->opt.rank + 1) / c->opt.world;
+  }
+  auto ensure_xt = [&]() -> appd_status {
+    if (XT) return APPD_OK;
     npad = (n + 127) / 128 * 128;
     dpad = (d + 31) / 32 * 32;
     XT = (float*)ws(c, S_XT, sizeof(float) * npad * dpad);
     if (!XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "XT workspace");
-    if ((s = launch_transpose_points(c, X, n, d, XT, npad, dpad))) return s;
-  }
+    return launch_transpose_points(c, X, n, d, XT, npad, dpad);
+  };
+  if (points && !use_tc && (s = ensure_xt())) return s;
   if ((s = launch_iota(c, comp, n))) return s;
   APPD_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(int) * 16, c->stream));
   int64_t k = n;
@@ -354,9 +374,49 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   while (k > 1) {
     if ((s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
-    if (points) s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
-    else s = launch_scan_weights(c, W, n, row0, rows, cmp, compbest, sense);
+    if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
+    const int64_t l0 = c->launches;
+    if (points && use_tc) {
+      bool overflowed = false;
+      if ((s = tcf_round(c, &tc, X, comp, rounds, compbest, rt_begin, rt_end, &overflowed))) return s;
+      c->stats.tc_candidates += tc.last_candidates;
+      if (overflowed) {  // candidate buffer too small for this input: exact scan for this round
+        if ((s = ensure_xt())) return s;
+        s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
+        c->stats.exact_rounds++;
+      } else if (getenv("APPD_TC_VERIFY")) {  // debug: compare with the exact scan, report to stderr
+        if ((s = ensure_xt())) return s;
+        u64* cb2 = (u64*)ws(c, S_TMP, sizeof(u64) * k);
+        if ((s = launch_fill_u64(c, cb2, k, KEY_NONE))) return s;
+        if ((s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, cb2))) return s;
+        std::vector<u64> a(k), b(k);
+        APPD_CUDA(c, cudaMemcpyAsync(a.data(), compbest, sizeof(u64) * k, cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaMemcpyAsync(b.data(), cb2, sizeof(u64) * k, cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        int bad = 0;
+        for (int64_t q = 0; q < k; q++)
+          if (a[q] != b[q]) {
+            if (bad < 5) {
+              int64_t u1, v1, u2, v2;
+              tri_decode(a[q] & ((1ull << 33) - 1), &u1, &v1);
+              tri_decode(b[q] & ((1ull << 33) - 1), &u2, &v2);
+              fprintf(stderr, "round %d comp %lld: tc (%lld,%lld) d2bits %llx  exact (%lld,%lld) d2bits %llx\n", rounds,
+                      (long long)q, (long long)u1, (long long)v1, a[q] >> 33, (long long)u2, (long long)v2, b[q] >> 33);
+            }
+            bad++;
+          }
+        fprintf(stderr, "round %d: k=%lld mismatching components %d candidates %u\n", rounds, (long long)k, bad,
+                tc.last_candidates);
+      }
+    } else if (points) {
+      s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
+      c->stats.exact_rounds++;
+    } else {
+      s = launch_scan_weights(c, W, n, row0, rows, cmp, compbest, sense);
+    }
     if (s) return s;
+    c->stats.scan_launches += c->launches - l0;
+    if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
     if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
     if ((s = launch_hook(c, compbest, k, comp, ks.shift, link))) return s;
     if ((s = launch_mutual(c, compbest, k, link, parent, mstkeys, counters))) return s;
@@ -366,6 +426,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
     int64_t knew = (int64_t)hostk[0] + hostk[1];
     rounds++;
     if (knew >= k || knew < 1) return fail(c, APPD_ERR_CUDA, "Boruvka made no progress (k = %lld)", (long long)k);
@@ -498,6 +559,15 @@ extern "C" appd_status appd_solve_points_host(appd_ctx* c, const float* X, int64
 extern "C" appd_status appd_solve_weights_host(appd_ctx* c, const float* W, int64_t n, float* M) {
   if (c && n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682");
   return solve_host(c, W, nullptr, n, 0, M);
+}
+
+extern "C" appd_status appd_debug_tc_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, float* tc_out,
+                                          float* ref_out) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1 || d < 1) return APPD_ERR_INVALID_ARGUMENT;
+  if ((s = check_device_ptr(c, X, "X"))) return s;
+  return tcf_debug_gram(c, X, n, d, tc_out, ref_out);
 }
 
 extern "C" appd_status appd_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0,

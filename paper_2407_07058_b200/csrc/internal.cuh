@@ -95,7 +95,7 @@ struct appd_ctx {
   void* nccl_comm = nullptr;
   int sm_count = 148;
   // workspace (grown on demand)
-  appd::DevBuf buf[32];
+  appd::DevBuf buf[64];
   // host-side copies of the last dendrogram
   std::vector<int32_t> last_pi;
   std::vector<float> last_h;
@@ -114,8 +114,35 @@ namespace appd {
 enum Slot {
   S_COMP = 0, S_COMPBEST, S_LINK, S_PARENT, S_NEWID, S_FLAGS, S_MSTKEYS, S_MSTKEYS_SORTED, S_COUNTERS,
   S_XT, S_PI, S_POS, S_H, S_ST, S_ROWS_SORTED, S_ROWPOS, S_TMP, S_TMP2, S_VALID, S_KEYS_TMP, S_PRIM,
-  S_HOST_IN, S_HOST_OUT, S_NSLOTS
+  S_HOST_IN, S_HOST_OUT,
+  S_TC_PART, S_TC_CENTER, S_TC_YA, S_TC_YB, S_TC_NRM, S_TC_LEN, S_TC_TML, S_TC_PERM, S_TC_SC, S_TC_KEYS,
+  S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT,
+  S_NSLOTS
 };
+static_assert(S_NSLOTS <= 64, "workspace slots");
+
+// tensor-core filtered points scan (k_tcfilter.cu)
+struct TcState {
+  int64_t n = 0, d = 0, npad = 0;
+  int dk = 0, K = 0, stages = 0;
+  float scale = 1.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f, gamma = 0.0f;
+  float* center = nullptr;
+  void* YA = nullptr;  // __half
+  void* YB = nullptr;
+  float *nrm = nullptr, *len = nullptr, *tile_maxlen = nullptr;
+  int *perm = nullptr, *sc = nullptr, *keys = nullptr, *cstart = nullptr, *cend = nullptr, *rs = nullptr,
+      *re = nullptr;
+  unsigned* UB = nullptr;
+  void* cand = nullptr;  // uint2
+  unsigned cand_cap = 0;
+  unsigned* counters = nullptr;
+  unsigned last_candidates = 0;
+};
+appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
+appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, u64* compbest,
+                      int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
+int64_t tcf_row_tiles(const TcState* st);
+appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, float* tc_out, float* ref_out);
 
 void* ws(appd_ctx* c, int slot, size_t bytes);  // grows; returns nullptr on OOM
 appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...);
