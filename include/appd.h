@@ -106,6 +106,7 @@ typedef struct {
   int32_t exact_rounds;    /* rounds that ran the exact scan (engine 1, or a candidate-buffer overflow) */
   double ms_scan;          /* device time of the MST scan kernels (timing = 1) */
   int64_t scan_launches;   /* launches of the MST scan kernels */
+  int64_t tc_fallback_rows; /* tensor-core engine: rows re-scanned exactly over all columns (all rounds) */
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */

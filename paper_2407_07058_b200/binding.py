@@ -74,6 +74,7 @@ class appd_stats(ctypes.Structure):
         ("exact_rounds", ctypes.c_int32),
         ("ms_scan", ctypes.c_double),
         ("scan_launches", ctypes.c_int64),
+        ("tc_fallback_rows", ctypes.c_int64),
     ]
 
     def as_dict(self):

@@ -152,6 +152,11 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   }
   for (int i = 0; i < 16; i++) cudaEventCreate(&c->ev[i]);
   c->ev_ready = true;
+  if (cudaHostAlloc((void**)&c->pinned_small, 64 * sizeof(unsigned), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    appd_destroy(c);
+    return APPD_ERR_OUT_OF_MEMORY;
+  }
   if (o.world > 1) {
     appd_status s = nccl_init(c, o.nccl_unique_id, o.rank, o.world);
     if (s != APPD_OK) {
@@ -189,6 +194,7 @@ extern "C" void appd_destroy(appd_ctx* c) {
     for (int i = 0; i < 16; i++) cudaEventDestroy(c->ev[i]);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->pinned_small) cudaFreeHost(c->pinned_small);
   cudaGetLastError();
   delete c;
 }
@@ -379,7 +385,6 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (points && use_tc) {
       bool overflowed = false;
       if ((s = tcf_round(c, &tc, X, comp, rounds, compbest, rt_begin, rt_end, &overflowed))) return s;
-      c->stats.tc_candidates += tc.last_candidates;
       if (overflowed) {  // candidate buffer too small for this input: exact scan for this round
         if ((s = ensure_xt())) return s;
         s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
@@ -405,8 +410,8 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
             }
             bad++;
           }
-        fprintf(stderr, "round %d: k=%lld mismatching components %d candidates %u\n", rounds, (long long)k, bad,
-                tc.last_candidates);
+        fprintf(stderr, "round %d: k=%lld mismatching components %d exact chunks %u fallback rows %u\n", rounds,
+                (long long)k, bad, tc.h_counters[2], tc.h_counters[0]);
       }
     } else if (points) {
       s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
@@ -427,6 +432,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
+    if (use_tc) {
+      c->stats.tc_candidates += (int64_t)tc.h_counters[2] * 32 + (int64_t)tc.h_counters[0] * n;
+      c->stats.tc_fallback_rows += tc.h_counters[0];
+    }
     int64_t knew = (int64_t)hostk[0] + hostk[1];
     rounds++;
     if (knew >= k || knew < 1) return fail(c, APPD_ERR_CUDA, "Boruvka made no progress (k = %lld)", (long long)k);

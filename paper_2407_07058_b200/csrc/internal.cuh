@@ -106,6 +106,7 @@ struct appd_ctx {
   // pinned host staging for host-buffer calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
 };
 
 namespace appd {
@@ -116,7 +117,8 @@ enum Slot {
   S_XT, S_PI, S_POS, S_H, S_ST, S_ROWS_SORTED, S_ROWPOS, S_TMP, S_TMP2, S_VALID, S_KEYS_TMP, S_PRIM,
   S_HOST_IN, S_HOST_OUT,
   S_TC_PART, S_TC_CENTER, S_TC_YA, S_TC_YB, S_TC_NRM, S_TC_LEN, S_TC_TML, S_TC_PERM, S_TC_SC, S_TC_KEYS,
-  S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT,
+  S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
+  S_TC_XTP, S_TC_CML,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 64, "workspace slots");
@@ -125,18 +127,19 @@ static_assert(S_NSLOTS <= 64, "workspace slots");
 struct TcState {
   int64_t n = 0, d = 0, npad = 0;
   int dk = 0, K = 0, stages = 0;
-  float scale = 1.0f, c1 = 0.0f, c2 = 0.0f, c3 = 0.0f, gamma = 0.0f;
+  float scale = 1.0f, c1 = 0.0f, c2 = 0.0f, k1 = 0.0f, k2 = 0.0f, k3 = 0.0f, gamma = 0.0f;
   float* center = nullptr;
   void* YA = nullptr;  // __half
   void* YB = nullptr;
-  float *nrm = nullptr, *len = nullptr, *tile_maxlen = nullptr;
+  float* XTp = nullptr;  // d x npad fp32, permuted columns (exact pass)
+  float *nrm = nullptr, *len = nullptr, *tile_maxlen = nullptr, *chunk_maxlen = nullptr;
   int *perm = nullptr, *sc = nullptr, *keys = nullptr, *cstart = nullptr, *cend = nullptr, *rs = nullptr,
       *re = nullptr;
   unsigned* UB = nullptr;
-  void* cand = nullptr;  // uint2
-  unsigned cand_cap = 0;
   unsigned* counters = nullptr;
-  unsigned last_candidates = 0;
+  unsigned* h_counters = nullptr;  // pinned host copy: [0] fallback rows, [2] exact chunks
+  int* fallback = nullptr;
+  float maxlen_scaled = 0.0f;
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, u64* compbest,

@@ -1,0 +1,5 @@
+python tools/c4_once.py > gpurun_out/c4_once.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1.csv python tools/c4_once.py > gpurun_out/ncu1.log 2>&1; echo "ncu1 $?"
+python tools/c4_once.py > gpurun_out/c4_once2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_tcf_scan -s 2 -c 1 -o gpurun_out/prof_tcf python tools/c4_once.py > gpurun_out/ncu2.log 2>&1; echo "ncu2 $?"
+ncu --set full --clock-control none --import-source on -k regex:k_fill -s 1 -c 1 -o gpurun_out/prof_fill python tools/c4_once.py > gpurun_out/ncu3.log 2>&1; echo "ncu3 $?"

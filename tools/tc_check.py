@@ -32,7 +32,7 @@ M = torch.empty((X.shape[0], X.shape[0]), device='cuda')
 for it in range(3):
     c2.solve_points(Xt, M)
     st = c2.stats()
-    print('C4 tc', {k: st[k] for k in ('rounds','tc_candidates','exact_rounds','ms_scan','ms_mst','ms_dendrogram','ms_fill','ms_total')}, flush=True)
+    print('C4 tc', {k: st[k] for k in ('rounds','tc_candidates','tc_fallback_rows','exact_rounds','ms_scan','ms_mst','ms_dendrogram','ms_fill','ms_total')}, flush=True)
 pi, h = c2.last_dendrogram(X.shape[0])
 print('C4 h sum', float(np.sort(h).astype(np.float64).sum()), 'zeros', int((h==0).sum()))
 print('ALL OK' if ok else 'MISMATCH')
