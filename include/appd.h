@@ -146,9 +146,9 @@ appd_status appd_points_weights(appd_ctx* ctx, const float* X, int64_t n, int64_
                                 float* Wblock);
 
 /* Test hook for the tensor-core engine: the raw fp32 accumulator of the first
- * 128 (padded) rows against all columns (tc_out, 128 x npad, npad = n rounded up
- * to 256) and a plain FP32 dot product of the same packed fp16 operands
- * (ref_out, same shape).  Device pointers. */
+ * 512 (padded) rows against all columns (tc_out, 512 x npad, npad = n rounded up
+ * to a multiple of 512) and a plain FP32 dot product of the same packed fp16
+ * operands (ref_out, same shape).  Device pointers. */
 appd_status appd_debug_tc_gram(appd_ctx* ctx, const float* X, int64_t n, int64_t d, float* tc_out, float* ref_out);
 
 /* 128-byte ncclUniqueId for appd_options.nccl_unique_id (call on rank 0 only). */

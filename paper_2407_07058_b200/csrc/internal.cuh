@@ -118,7 +118,7 @@ enum Slot {
   S_HOST_IN, S_HOST_OUT,
   S_TC_PART, S_TC_CENTER, S_TC_YA, S_TC_YB, S_TC_NRM, S_TC_LEN, S_TC_TML, S_TC_PERM, S_TC_SC, S_TC_KEYS,
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
-  S_TC_XTP, S_TC_CML,
+  S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 64, "workspace slots");
@@ -132,13 +132,17 @@ struct TcState {
   void* YA = nullptr;  // __half
   void* YB = nullptr;
   float* XTp = nullptr;  // d x npad fp32, permuted columns (exact pass)
-  float *nrm = nullptr, *len = nullptr, *tile_maxlen = nullptr, *chunk_maxlen = nullptr;
+  float *nrm = nullptr, *len = nullptr, *seg_maxlen = nullptr;
   int *perm = nullptr, *sc = nullptr, *keys = nullptr, *cstart = nullptr, *cend = nullptr, *rs = nullptr,
       *re = nullptr;
   unsigned* UB = nullptr;
   unsigned* counters = nullptr;
   unsigned* h_counters = nullptr;  // pinned host copy: [0] fallback rows, [2] exact chunks
   int* fallback = nullptr;
+  int* rowflag = nullptr;
+  float* TM = nullptr;      // [col tile][row] eligible maxima of G' from the scan
+  void* list = nullptr;     // uint2 (row, tile) pairs that need the exact check
+  unsigned list_cap = 0;
   float maxlen_scaled = 0.0f;
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);

@@ -1,0 +1,299 @@
+// k_tcscan.cu -- the tcgen05 scan of a points-mode Boruvka round (see k_tcfilter.cu
+// for the method).  Persistent kernel, one CTA per SM, 10 warps:
+//   warp 0   producer: 1-D bulk async copies (cp.async.bulk -> UBLKCP) of the packed
+//            fp16 operands; the 512-row block stays resident, 256-column tiles stream
+//            through a ring of shared-memory stages; mbarrier transaction counts
+//   warp 1   MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16 M=128 N=256
+//            K=16 slices; per column tile the four row tiles run in turn into two
+//            TMEM accumulators (2 x 256 fp32 columns); tcgen05.commit -> mbarriers
+//   warps 2-9 epilogue: tcgen05.ld 32x32b.x32 (software pipelined) -> per row and
+//            128-column segment the eligible maximum of G' (FMNMX3 trees), stored for
+//            the exact pass, and a running upper bound UB of the row's lightest edge.
+// Shared-memory traffic of an SS-mode MMA is (M + N) K 2 bytes per M N K MACs: with
+// M = 128, N = 256 that is 96 B/clk at the tensor rate, below the 128 B/clk of shared
+// memory; the 512-row block makes each column-operand byte read from L2 serve 512 rows.
+#include "tc_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace appd {
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// max of 32 values: 16 three-input maxima (FMNMX3)
+__device__ __forceinline__ float fmax32(const float (&v)[32]) {
+  const float a0 = fmax3(v[0], v[1], v[2]), a1 = fmax3(v[3], v[4], v[5]), a2 = fmax3(v[6], v[7], v[8]);
+  const float a3 = fmax3(v[9], v[10], v[11]), a4 = fmax3(v[12], v[13], v[14]), a5 = fmax3(v[15], v[16], v[17]);
+  const float a6 = fmax3(v[18], v[19], v[20]), a7 = fmax3(v[21], v[22], v[23]), a8 = fmax3(v[24], v[25], v[26]);
+  const float a9 = fmax3(v[27], v[28], v[29]), a10 = fmaxf(v[30], v[31]);
+  const float b0 = fmax3(a0, a1, a2), b1 = fmax3(a3, a4, a5), b2 = fmax3(a6, a7, a8), b3 = fmaxf(a9, a10);
+  return fmaxf(fmax3(b0, b1, b2), b3);
+}
+
+struct RowState {
+  int p;          // permuted row
+  bool valid;
+  float ni, li;   // |y^|^2, |y^|
+  int cs, ce;     // ineligible column range (the row's component)
+  float ub;       // running upper bound of s^2 r over eligible columns
+  float gbest;    // best segment maximum of G' seen so far
+};
+
+// eligible maximum of one 32-column chunk
+__device__ __forceinline__ float chunk_max(const float (&v)[32], const RowState& s, int q0, bool fast, int n) {
+  if (fast) return fmax32(v);
+  float m = -INFINITY;
+  if (s.valid && !(q0 >= s.cs && q0 + 32 <= s.ce)) {
+#pragma unroll
+    for (int t = 0; t < 32; t++) {
+      const int qq = q0 + t;
+      const bool el = (qq < s.cs || qq >= s.ce) && qq < n;
+      m = fmaxf(m, el ? v[t] : -INFINITY);
+    }
+  }
+  return m;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int K = P.K;
+  const int NST = P.stages;
+  const uint32_t gran_bytes = TC_M * K * 2;    // 128 points
+  const uint32_t a_bytes = TC_RT * gran_bytes;  // 512 points
+  const uint32_t b_bytes = TC_N * K * 2;        // 256 points
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + a_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)NST * b_bytes);
+  uint64_t* full = bars;         // [NST]
+  uint64_t* empty = bars + NST;  // [NST]
+  uint64_t* afull = bars + 2 * NST;
+  uint64_t* aempty = afull + 1;
+  uint64_t* tfull = aempty + 1;  // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; s++) {
+      ptx::mbar_init(full + s, 1);
+      ptx::mbar_init(empty + s, 1);
+    }
+    ptx::mbar_init(afull, 1);
+    ptx::mbar_init(aempty, 1);
+    for (int b = 0; b < 2; b++) {
+      ptx::mbar_init(tfull + b, 1);
+      ptx::mbar_init(tempty + b, 8);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int items = (P.rb_end - P.rb_begin) * P.col_splits;
+  const int per_split = (P.col_tiles + P.col_splits - 1) / P.col_splits;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0, aph = 0;
+      bool first = true;
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int rb = P.rb_begin + it / P.col_splits;
+        const int sp = it % P.col_splits;
+        const int ct0 = sp * per_split;
+        const int ct1 = min(P.col_tiles, ct0 + per_split);
+        if (!first) {
+          ptx::mbar_wait(aempty, aph);
+          aph ^= 1;
+        }
+        first = false;
+        ptx::mbar_expect_tx(afull, a_bytes);
+        ptx::bulk_g2s(sA, reinterpret_cast<const uint8_t*>(P.YA) + (size_t)rb * a_bytes, a_bytes, afull);
+        for (int ct = ct0; ct < ct1; ct++) {
+          ptx::mbar_wait(empty + stage, ph ^ 1);
+          ptx::mbar_expect_tx(full + stage, b_bytes);
+          ptx::bulk_g2s(sB + stage * b_bytes, reinterpret_cast<const uint8_t*>(P.YB) + (size_t)ct * b_bytes, b_bytes,
+                        full + stage);
+          if (++stage == NST) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = ptx::idesc_f16_f32(TC_M, TC_N);
+      const uint32_t sbo = (uint32_t)(K / 8) * 128u;
+      const uint32_t a0 = ptx::smem_u32(sA);
+      const uint32_t b0 = ptx::smem_u32(sB);
+      int stage = 0;
+      uint32_t ph = 0, aph = 0, tph[2] = {0, 0};
+      for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int sp = it % P.col_splits;
+        const int ct0 = sp * per_split;
+        const int ct1 = min(P.col_tiles, ct0 + per_split);
+        ptx::mbar_wait(afull, aph);
+        aph ^= 1;
+        for (int ct = ct0; ct < ct1; ct++) {
+          ptx::mbar_wait(full + stage, ph);
+          const uint32_t bs = b0 + stage * b_bytes;
+#pragma unroll
+          for (int r = 0; r < TC_RT; r++) {
+            const int b = r & 1;
+            ptx::mbar_wait(tempty + b, tph[b] ^ 1);
+            tph[b] ^= 1;
+            ptx::tc_fence_after();
+            for (int ks = 0; ks < K / 16; ks++) {
+              const uint64_t ad = ptx::sdesc(a0 + r * gran_bytes + ks * 256, 128, sbo);
+              const uint64_t bd = ptx::sdesc(bs + ks * 256, 128, sbo);
+              ptx::mma_f16(tmem + (uint32_t)(b * TC_N), ad, bd, idesc, ks > 0 ? 1u : 0u);
+            }
+            ptx::mma_commit(tfull + b);  // accumulator of row tile r ready
+          }
+          ptx::mma_commit(empty + stage);  // smem stage free once these MMAs complete
+          if (++stage == NST) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        ptx::mma_commit(aempty);  // row block free after the item's last MMA
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9) ----------------
+    // warp w may only read TMEM lanes 32*(w%4) .. +31: warp (q, h) reads lane quarter q
+    // and column half h (128 columns) of each accumulator; in phase r it holds a row of
+    // row tile r, so each thread owns four rows of the item.
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    uint32_t tph[2] = {0, 0};
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      const int rb = P.rb_begin + it / P.col_splits;
+      const int sp = it % P.col_splits;
+      const int ct0 = sp * per_split;
+      const int ct1 = min(P.col_tiles, ct0 + per_split);
+      RowState R[TC_RT];
+#pragma unroll
+      for (int r = 0; r < TC_RT; r++) {
+        RowState& s = R[r];
+        s.p = rb * TC_ROWS + r * TC_M + q * 32 + lane;
+        s.valid = s.p < P.n;
+        s.ni = s.valid ? P.nrm[s.p] : 0.0f;
+        s.li = s.valid ? P.len[s.p] : 0.0f;
+        s.cs = s.valid ? (P.round0 ? s.p : P.cs[s.p]) : 0;
+        s.ce = s.valid ? (P.round0 ? s.p + 1 : P.ce[s.p]) : 0;
+        s.ub = INFINITY;
+        s.gbest = -INFINITY;
+      }
+      for (int ct = ct0; ct < ct1; ct++) {
+        const int h0 = ct * TC_N + h * TC_TMG;  // first column of this warp's segment
+        const int seg = ct * (TC_N / TC_TMG) + h;
+#pragma unroll
+        for (int r = 0; r < TC_RT; r++) {
+          const int b = r & 1;
+          ptx::mbar_wait(tfull + b, tph[b]);
+          tph[b] ^= 1;
+          ptx::tc_fence_after();
+          RowState& s = R[r];
+          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TC_N + h * TC_TMG);
+          float va[32], vb[32];
+          if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
+            for (int c = 0; c < 4; c++) {
+              ptx::tmem_ld32(tb + c * 32, va);
+              ptx::tmem_ld_wait();
+              if (it == (int)blockIdx.x && P.dump) {
+                const int rloc = r * TC_M + q * 32 + lane;
+                for (int t = 0; t < 32; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + c * 32 + t] = va[t];
+              }
+            }
+          } else {
+            // warp-uniform fast path: valid rows whose component misses these real columns
+            const bool fast =
+                __all_sync(0xffffffffu, s.valid && (h0 + TC_TMG <= s.cs || h0 >= s.ce) && h0 + TC_TMG <= P.n);
+            // software pipeline: the TMEM load of the next chunk is in flight during processing
+            ptx::tmem_ld32(tb, va);
+            ptx::tmem_ld_wait();
+            ptx::reg_fence(va);
+            ptx::tmem_ld32(tb + 32, vb);
+            float m = chunk_max(va, s, h0, fast, P.n);
+            ptx::tmem_ld_wait();
+            ptx::reg_fence(vb);
+            ptx::tmem_ld32(tb + 64, va);
+            m = fmaxf(m, chunk_max(vb, s, h0 + 32, fast, P.n));
+            ptx::tmem_ld_wait();
+            ptx::reg_fence(va);
+            ptx::tmem_ld32(tb + 96, vb);
+            m = fmaxf(m, chunk_max(va, s, h0 + 64, fast, P.n));
+            ptx::tmem_ld_wait();
+            ptx::reg_fence(vb);
+            m = fmaxf(m, chunk_max(vb, s, h0 + 96, fast, P.n));
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty + b);
+            // eligible maximum of G' over this (row, segment); a warp's rows are
+            // consecutive, so the store is coalesced ([segment][row] layout)
+            if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
+            if (s.valid && m > s.gbest) {  // tighten the bound only when the best improves
+              s.gbest = m;
+              s.ub = fminf(s.ub, em_upper(P.em, s.ni - 2.0f * m, s.ni, s.li, P.seg_maxlen[seg]));
+            }
+            continue;
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tempty + b);
+        }
+      }
+      if (PASS == 0) {
+#pragma unroll
+        for (int r = 0; r < TC_RT; r++)
+          if (R[r].valid && R[r].ub < INFINITY) atomicMin(P.UB + R[r].p, __float_as_uint(fmaxf(R[r].ub, 0.0f)));
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+size_t tcf_smem_bytes(int K, int stages) {
+  return (size_t)TC_ROWS * K * 2 + (size_t)stages * TC_N * K * 2 + (2 * TC_MAX_STAGES + 6) * 8 + 16;
+}
+
+// deepest ring (<= TC_MAX_STAGES) that fits 227 KB of shared memory; 0 if fewer than 2 fit
+int tcf_stages(int K) {
+  for (int s = TC_MAX_STAGES; s >= 2; s--)
+    if (tcf_smem_bytes(K, s) <= 227 * 1024) return s;
+  return 0;
+}
+
+appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
+  // at least 120 KB so that exactly one CTA (and one 512-column TMEM allocation) fits per SM
+  size_t smem = tcf_smem_bytes(P.K, P.stages);
+  if (smem < 120 * 1024) smem = 120 * 1024;
+  static int attr_done = 0;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_tcf_scan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_done = 1;
+  }
+  const int items = (P.rb_end - P.rb_begin) * P.col_splits;
+  int grid = c->sm_count < items ? c->sm_count : items;
+  if (grid < 1) return APPD_OK;
+  if (pass == 0) k_tcf_scan<0><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  else k_tcf_scan<2><<<1, TC_THREADS, smem, c->stream>>>(P);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd

@@ -1,0 +1,73 @@
+// tc_common.cuh -- shared pieces of the tensor-core points-mode MST scan
+// (k_tcscan.cu: the tcgen05 kernel; k_tcfilter.cu: preparation, exact re-check, driver).
+#pragma once
+#include <cuda_fp16.h>
+
+#include "internal.cuh"
+
+namespace appd {
+
+// MMA: M = 128 rows (one TMEM lane per row) x N = 256 columns x K = 16 per instruction,
+// both operands from shared memory (K-major, no swizzle).  A work item keeps TC_RT = 4
+// row tiles (512 rows) resident in shared memory and streams 256-column tiles of the
+// column operand through a ring; TMEM holds two 256-column fp32 accumulators that the
+// four row tiles of a column tile use in turn (phase r -> buffer r % 2), so the
+// epilogue of one row tile overlaps the MMAs of the next.
+constexpr int TC_M = 128, TC_N = 256, TC_RT = 4, TC_ROWS = TC_M * TC_RT, TC_MAX_STAGES = 6;
+constexpr int TC_TMG = 128;      // granularity of the stored tile maxima (columns)
+constexpr int TC_THREADS = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
+
+// Error model (scaled units).  L = |y^_i|, R = max |y^_j| over the columns considered.
+//   delta = c1 (L + R) + c2       >= |(y^_i - y^_j) - s (x_i - x_j)|
+//   eta   = k1 R (L + R/2) + k2 (L^2 + R^2) + k3 (4 R^2 + (L + R)^2)
+//                                 >= |Dt - |y^_i - y^_j|^2|
+//   gamma                         >= |r - |x_i - x_j|^2| / |x_i - x_j|^2
+// Then  U = (1+gamma) (sqrt(max(Dt + eta, 0)) + delta)^2  >= s^2 r, and
+//   L <= UB  is implied by  Dt <= T = (sqrt(UB / (1-gamma)) + delta)^2 + eta.
+struct ErrModel {
+  float c1, c2, k1, k2, k3, gamma;
+};
+
+__device__ __forceinline__ float em_delta(const ErrModel& e, float L, float R) { return e.c1 * (L + R) + e.c2; }
+__device__ __forceinline__ float em_eta(const ErrModel& e, float L, float R) {
+  return e.k1 * R * (L + 0.5f * R) + e.k2 * (L * L + R * R) + e.k3 * (4.0f * R * R + (L + R) * (L + R));
+}
+// upper bound on s^2 r for a column whose Dt is dt
+__device__ __forceinline__ float em_upper(const ErrModel& e, float dt, float ni, float L, float R) {
+  const float r = sqrtf(fmaxf(dt + em_eta(e, L, R), 0.0f)) + em_delta(e, L, R);
+  return (1.0f + e.gamma) * r * r * (1.0f + 0x1p-18f) + 0x1p-18f * ni;
+}
+// G' threshold: a column can hold a candidate (L <= ub) only if G' >= thr
+__device__ __forceinline__ float em_thr(const ErrModel& e, float ub, float ni, float L, float R) {
+  const float r = sqrtf(ub / (1.0f - e.gamma)) + em_delta(e, L, R);
+  const float T = (r * r + em_eta(e, L, R)) * (1.0f + 0x1p-18f) + 0x1p-18f * ni;
+  return 0.5f * (ni - T);
+}
+
+struct TcParams {
+  const __half* YA;          // row operand granules (128 points x K, core-matrix layout)
+  const __half* YB;          // column operand granules
+  const float* nrm;          // |y^_p|^2 (fp32), permuted order
+  const float* len;          // |y^_p|
+  const float* seg_maxlen;   // max |y^_j| over each TC_TMG-column segment
+  const int* cs;             // per permuted row: first position of its component
+  const int* ce;             // per permuted row: one past the last position
+  unsigned* UB;              // per permuted row: upper bound (float bits, >= 0)
+  float* TM;                 // [segment][row]: eligible maximum of G' over the TC_TMG columns
+  int64_t tm_ld;             // leading dimension of TM (npad)
+  int n;                     // points
+  int K;                     // padded K (multiple of 16)
+  int stages;                // shared-memory ring depth for the column operand
+  int rb_begin, rb_end;      // this rank's 512-row blocks (permuted order)
+  int col_tiles;             // npad / 256
+  int col_splits;
+  ErrModel em;
+  int round0;   // singletons (eligibility = j != i)
+  float* dump;  // PASS 2 (test hook) only: raw accumulator of the first item
+};
+
+size_t tcf_smem_bytes(int K, int stages);
+int tcf_stages(int K);
+appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P);
+
+}  // namespace appd

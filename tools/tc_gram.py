@@ -8,8 +8,8 @@ L.appd_debug_tc_gram.argtypes = [ctypes.c_void_p]*2 + [ctypes.c_int64]*2 + [ctyp
 ctx = P.Context()
 for (n, d, kind) in [(256, 2, 'uniform'), (512, 64, 'blobs'), (300, 16, 'dups')]:
     X = torch.from_numpy(G.random_points(n, d, 1, kind)).cuda()
-    npad = (n + 255)//256*256
-    tc = torch.zeros((128, npad), device='cuda'); ref = torch.zeros((128, npad), device='cuda')
+    npad = (n + 511)//512*512
+    tc = torch.zeros((512, npad), device='cuda'); ref = torch.zeros((512, npad), device='cuda')
     s = L.appd_debug_tc_gram(ctx._h, X.data_ptr(), n, d, tc.data_ptr(), ref.data_ptr())
     a = tc.cpu().numpy(); b = ref.cpu().numpy()
     print(n, d, kind, 'status', s, 'maxabs', np.abs(a-b).max(), 'ref range', b.min(), b.max())
