@@ -12,6 +12,8 @@
 // Shared-memory traffic of an SS-mode MMA is (M + N) K 2 bytes per M N K MACs: with
 // M = 128, N = 256 that is 96 B/clk at the tensor rate, below the 128 B/clk of shared
 // memory; the 512-row block makes each column-operand byte read from L2 serve 512 rows.
+#include <cstdlib>
+
 #include "tc_common.cuh"
 #include "tc_ptx.cuh"
 
@@ -31,6 +33,40 @@ __device__ __forceinline__ float fmax32(const float (&v)[32]) {
   const float b0 = fmax3(a0, a1, a2), b1 = fmax3(a3, a4, a5), b2 = fmax3(a6, a7, a8), b3 = fmaxf(a9, a10);
   return fmaxf(fmax3(b0, b1, b2), b3);
 }
+
+// max of 64 values: 32 three-input maxima
+__device__ __forceinline__ float fmax64(const float (&v)[64]) {
+  float a[22];
+#pragma unroll
+  for (int i = 0; i < 21; i++) a[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[21] = v[63];
+  float b[8];
+#pragma unroll
+  for (int i = 0; i < 7; i++) b[i] = fmax3(a[3 * i], a[3 * i + 1], a[3 * i + 2]);
+  b[7] = a[21];
+  return fmaxf(fmax3(b[0], b[1], b[2]), fmax3(fmax3(b[3], b[4], b[5]), b[6], b[7]));
+}
+
+// max of 128 values: 64 three-input maxima
+__device__ __forceinline__ float fmax128(const float (&v)[128]) {
+  float a[43];
+#pragma unroll
+  for (int i = 0; i < 42; i++) a[i] = fmax3(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  a[42] = fmaxf(v[126], v[127]);
+  float b[15];
+#pragma unroll
+  for (int i = 0; i < 14; i++) b[i] = fmax3(a[3 * i], a[3 * i + 1], a[3 * i + 2]);
+  b[14] = a[42];
+  const float c0 = fmax3(b[0], b[1], b[2]), c1 = fmax3(b[3], b[4], b[5]), c2 = fmax3(b[6], b[7], b[8]);
+  const float c3 = fmax3(b[9], b[10], b[11]), c4 = fmax3(b[12], b[13], b[14]);
+  return fmaxf(fmax3(c0, c1, c2), fmaxf(c3, c4));
+}
+
+// one warp's TC_TMG accumulator columns: a single TMEM load and a 3-input max tree
+__device__ __forceinline__ void tmem_ld_seg(uint32_t taddr, float (&v)[64]) { ptx::tmem_ld64(taddr, v); }
+__device__ __forceinline__ void tmem_ld_seg(uint32_t taddr, float (&v)[128]) { ptx::tmem_ld128(taddr, v); }
+__device__ __forceinline__ float fmax_seg(const float (&v)[64]) { return fmax64(v); }
+__device__ __forceinline__ float fmax_seg(const float (&v)[128]) { return fmax128(v); }
 
 struct RowState {
   int p;          // permuted row
@@ -71,9 +107,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
   uint64_t* empty = bars + NST;  // [NST]
   uint64_t* afull = bars + 2 * NST;
   uint64_t* aempty = afull + 1;
-  uint64_t* tfull = aempty + 1;  // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = aempty + 1;         // [TC_NBUF]
+  uint64_t* tempty = tfull + TC_NBUF;  // [TC_NBUF]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + TC_NBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -83,9 +119,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     }
     ptx::mbar_init(afull, 1);
     ptx::mbar_init(aempty, 1);
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < TC_NBUF; b++) {
       ptx::mbar_init(tfull + b, 1);
-      ptx::mbar_init(tempty + b, 8);
+      ptx::mbar_init(tempty + b, TC_EPI_WARPS);
     }
     ptx::fence_mbar_init();
   }
@@ -118,9 +154,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
         ptx::bulk_g2s(sA, reinterpret_cast<const uint8_t*>(P.YA) + (size_t)rb * a_bytes, a_bytes, afull);
         for (int ct = ct0; ct < ct1; ct++) {
           ptx::mbar_wait(empty + stage, ph ^ 1);
-          ptx::mbar_expect_tx(full + stage, b_bytes);
-          ptx::bulk_g2s(sB + stage * b_bytes, reinterpret_cast<const uint8_t*>(P.YB) + (size_t)ct * b_bytes, b_bytes,
-                        full + stage);
+          if (PASS == 5 || PASS == 6) {  // experiment: no column-operand copies
+            ptx::mbar_arrive(full + stage);
+          } else {
+            ptx::mbar_expect_tx(full + stage, b_bytes);
+            ptx::bulk_g2s(sB + stage * b_bytes, reinterpret_cast<const uint8_t*>(P.YB) + (size_t)ct * b_bytes,
+                          b_bytes, full + stage);
+          }
           if (++stage == NST) {
             stage = 0;
             ph ^= 1;
@@ -130,13 +170,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // per column tile: 8 phases (row tile r, column half hh), phase i -> TMEM buffer i % 4
     if (lane == 0) {
-      const uint32_t idesc = ptx::idesc_f16_f32(TC_M, TC_N);
+      const uint32_t idesc = ptx::idesc_f16_f32(TC_M, TC_NA);
       const uint32_t sbo = (uint32_t)(K / 8) * 128u;
       const uint32_t a0 = ptx::smem_u32(sA);
       const uint32_t b0 = ptx::smem_u32(sB);
       int stage = 0;
-      uint32_t ph = 0, aph = 0, tph[2] = {0, 0};
+      uint32_t ph = 0, aph = 0, tph[TC_NBUF] = {};
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int sp = it % P.col_splits;
         const int ct0 = sp * per_split;
@@ -147,17 +188,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
           ptx::mbar_wait(full + stage, ph);
           const uint32_t bs = b0 + stage * b_bytes;
 #pragma unroll
-          for (int r = 0; r < TC_RT; r++) {
-            const int b = r & 1;
+          for (int i = 0; i < TC_RT * TC_HALVES; i++) {
+            const int r = i / TC_HALVES, hh = i % TC_HALVES, b = i % TC_NBUF;
             ptx::mbar_wait(tempty + b, tph[b] ^ 1);
             tph[b] ^= 1;
             ptx::tc_fence_after();
             for (int ks = 0; ks < K / 16; ks++) {
               const uint64_t ad = ptx::sdesc(a0 + r * gran_bytes + ks * 256, 128, sbo);
-              const uint64_t bd = ptx::sdesc(bs + ks * 256, 128, sbo);
-              ptx::mma_f16(tmem + (uint32_t)(b * TC_N), ad, bd, idesc, ks > 0 ? 1u : 0u);
+              const uint64_t bd = ptx::sdesc(bs + hh * gran_bytes + ks * 256, 128, sbo);
+              ptx::mma_f16(tmem + (uint32_t)(b * TC_NA), ad, bd, idesc, ks > 0 ? 1u : 0u);
             }
-            ptx::mma_commit(tfull + b);  // accumulator of row tile r ready
+            ptx::mma_commit(tfull + b);  // accumulator of (row tile r, half hh) ready
           }
           ptx::mma_commit(empty + stage);  // smem stage free once these MMAs complete
           if (++stage == NST) {
@@ -171,11 +212,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
   } else {
     // ---------------- epilogue (warps 2..9) ----------------
     // warp w may only read TMEM lanes 32*(w%4) .. +31: warp (q, h) reads lane quarter q
-    // and column half h (128 columns) of each accumulator; in phase r it holds a row of
-    // row tile r, so each thread owns four rows of the item.
+    // and 64-column half h of each 128-column accumulator; in the phases of row tile r
+    // it holds a row of row tile r, so each thread owns four rows of the item.
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
-    uint32_t tph[2] = {0, 0};
+    uint32_t tph[TC_NBUF] = {};
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       const int rb = P.rb_begin + it / P.col_splits;
       const int sp = it % P.col_splits;
@@ -195,62 +236,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
         s.gbest = -INFINITY;
       }
       for (int ct = ct0; ct < ct1; ct++) {
-        const int h0 = ct * TC_N + h * TC_TMG;  // first column of this warp's segment
-        const int seg = ct * (TC_N / TC_TMG) + h;
 #pragma unroll
-        for (int r = 0; r < TC_RT; r++) {
-          const int b = r & 1;
+        for (int i = 0; i < TC_RT * TC_HALVES; i++) {
+          const int r = i / TC_HALVES, hh = i % TC_HALVES, b = i % TC_NBUF;
+          const int h0 = ct * TC_N + hh * TC_NA + h * TC_TMG;  // first column of this warp's segment
+          const int seg = h0 / TC_TMG;
           ptx::mbar_wait(tfull + b, tph[b]);
           tph[b] ^= 1;
           ptx::tc_fence_after();
+          if (PASS == 3 || PASS == 6) {  // experiment: null epilogue (MMA + producer throughput only)
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty + b);
+            continue;
+          }
           RowState& s = R[r];
-          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TC_N + h * TC_TMG);
-          float va[32], vb[32];
-          if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
-            for (int c = 0; c < 4; c++) {
-              ptx::tmem_ld32(tb + c * 32, va);
-              ptx::tmem_ld_wait();
-              if (it == (int)blockIdx.x && P.dump) {
-                const int rloc = r * TC_M + q * 32 + lane;
-                for (int t = 0; t < 32; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + c * 32 + t] = va[t];
-              }
-            }
-          } else {
-            // warp-uniform fast path: valid rows whose component misses these real columns
-            const bool fast =
-                __all_sync(0xffffffffu, s.valid && (h0 + TC_TMG <= s.cs || h0 >= s.ce) && h0 + TC_TMG <= P.n);
-            // software pipeline: the TMEM load of the next chunk is in flight during processing
-            ptx::tmem_ld32(tb, va);
+          float v[TC_TMG];
+          tmem_ld_seg(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TC_NA + h * TC_TMG), v);
+          if (PASS == 4) {  // experiment: TMEM load only
             ptx::tmem_ld_wait();
-            ptx::reg_fence(va);
-            ptx::tmem_ld32(tb + 32, vb);
-            float m = chunk_max(va, s, h0, fast, P.n);
-            ptx::tmem_ld_wait();
-            ptx::reg_fence(vb);
-            ptx::tmem_ld32(tb + 64, va);
-            m = fmaxf(m, chunk_max(vb, s, h0 + 32, fast, P.n));
-            ptx::tmem_ld_wait();
-            ptx::reg_fence(va);
-            ptx::tmem_ld32(tb + 96, vb);
-            m = fmaxf(m, chunk_max(va, s, h0 + 64, fast, P.n));
-            ptx::tmem_ld_wait();
-            ptx::reg_fence(vb);
-            m = fmaxf(m, chunk_max(vb, s, h0 + 96, fast, P.n));
+            ptx::reg_fence(v);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(tempty + b);
-            // eligible maximum of G' over this (row, segment); a warp's rows are
-            // consecutive, so the store is coalesced ([segment][row] layout)
-            if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
-            if (s.valid && m > s.gbest) {  // tighten the bound only when the best improves
-              s.gbest = m;
-              s.ub = fminf(s.ub, em_upper(P.em, s.ni - 2.0f * m, s.ni, s.li, P.seg_maxlen[seg]));
+            if (v[lane] == 12345.678f && s.valid) P.TM[s.p] = v[63];
+            continue;
+          }
+          ptx::tmem_ld_wait();
+          ptx::reg_fence(v);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(tempty + b);  // accumulator consumed: free it early
+          if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
+            if (it == (int)blockIdx.x && P.dump) {
+              const int rloc = r * TC_M + q * 32 + lane;
+              for (int t = 0; t < TC_TMG; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + t] = v[t];
             }
             continue;
           }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(tempty + b);
+          // warp-uniform fast path: valid rows whose component misses these real columns
+          const bool fast =
+              __all_sync(0xffffffffu, s.valid && (h0 + TC_TMG <= s.cs || h0 >= s.ce) && h0 + TC_TMG <= P.n);
+          float m;
+          if (fast) {
+            m = fmax_seg(v);
+          } else {
+            m = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < TC_TMG / 32; c++) {
+              float w[32];
+#pragma unroll
+              for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
+              m = fmaxf(m, chunk_max(w, s, h0 + c * 32, false, P.n));
+            }
+          }
+          // eligible maximum of G' over this (row, segment); a warp's rows are
+          // consecutive, so the store is coalesced ([segment][row] layout)
+          if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
+          if (s.valid && m > s.gbest) {  // tighten the bound only when the best improves
+            s.gbest = m;
+            s.ub = fminf(s.ub, em_upper(P.em, s.ni - 2.0f * m, s.ni, s.li, P.seg_maxlen[seg]));
+          }
         }
       }
       if (PASS == 0) {
@@ -267,7 +312,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
 }
 
 size_t tcf_smem_bytes(int K, int stages) {
-  return (size_t)TC_ROWS * K * 2 + (size_t)stages * TC_N * K * 2 + (2 * TC_MAX_STAGES + 6) * 8 + 16;
+  return (size_t)TC_ROWS * K * 2 + (size_t)stages * TC_N * K * 2 + (2 * TC_MAX_STAGES + 2 + 2 * TC_NBUF) * 8 + 16;
 }
 
 // deepest ring (<= TC_MAX_STAGES) that fits 227 KB of shared memory; 0 if fewer than 2 fit
@@ -290,7 +335,20 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   const int items = (P.rb_end - P.rb_begin) * P.col_splits;
   int grid = c->sm_count < items ? c->sm_count : items;
   if (grid < 1) return APPD_OK;
-  if (pass == 0) k_tcf_scan<0><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  static const int exp_pass = getenv("APPD_TC_EXPERIMENT") ? atoi(getenv("APPD_TC_EXPERIMENT")) : 0;
+  if (pass == 0 && exp_pass == 3) {
+    cudaFuncSetAttribute(k_tcf_scan<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    k_tcf_scan<3><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  } else if (pass == 0 && exp_pass == 4) {
+    cudaFuncSetAttribute(k_tcf_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    k_tcf_scan<4><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  } else if (pass == 0 && exp_pass == 5) {
+    cudaFuncSetAttribute(k_tcf_scan<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    k_tcf_scan<5><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  } else if (pass == 0 && exp_pass == 6) {
+    cudaFuncSetAttribute(k_tcf_scan<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    k_tcf_scan<6><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  } else if (pass == 0) k_tcf_scan<0><<<grid, TC_THREADS, smem, c->stream>>>(P);
   else k_tcf_scan<2><<<1, TC_THREADS, smem, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;

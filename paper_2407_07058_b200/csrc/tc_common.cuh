@@ -14,8 +14,12 @@ namespace appd {
 // four row tiles of a column tile use in turn (phase r -> buffer r % 2), so the
 // epilogue of one row tile overlaps the MMAs of the next.
 constexpr int TC_M = 128, TC_N = 256, TC_RT = 4, TC_ROWS = TC_M * TC_RT, TC_MAX_STAGES = 6;
-constexpr int TC_TMG = 128;      // granularity of the stored tile maxima (columns)
-constexpr int TC_THREADS = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
+constexpr int TC_NA = 256;        // MMA N: accumulator width (TMEM columns per buffer)
+constexpr int TC_NBUF = 2;        // TMEM accumulator buffers (TC_NBUF x TC_NA = 512 columns)
+constexpr int TC_HALVES = TC_N / TC_NA;  // accumulators per (row tile, column tile)
+constexpr int TC_EPI_WARPS = 8;   // 4 lane quarters x 2 column halves of an accumulator
+constexpr int TC_TMG = TC_NA / 2; // columns per epilogue warp = granularity of the stored maxima
+constexpr int TC_THREADS = 32 * (2 + TC_EPI_WARPS);  // warp 0 producer, warp 1 MMA, then epilogue
 
 // Error model (scaled units).  L = |y^_i|, R = max |y^_j| over the columns considered.
 //   delta = c1 (L + R) + c2       >= |(y^_i - y^_j) - s (x_i - x_j)|
