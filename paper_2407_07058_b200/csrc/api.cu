@@ -36,6 +36,24 @@ void* ws(appd_ctx* c, int slot, size_t bytes) {
   return b.p;
 }
 
+void* pinned_host(appd_ctx* c, size_t bytes) {
+  if (c->pinned_bytes >= bytes && c->pinned) return c->pinned;
+  if (c->pinned) cudaFreeHost(c->pinned);
+  c->pinned = nullptr;
+  c->pinned_bytes = 0;
+  c->dend_pi = nullptr;
+  c->dend_h = nullptr;
+  c->have_dendrogram = false;
+  size_t want = (bytes + 65535) & ~(size_t)65535;
+  if (cudaHostAlloc(&c->pinned, want, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    c->pinned = nullptr;
+    return nullptr;
+  }
+  c->pinned_bytes = want;
+  return c->pinned;
+}
+
 appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...) {
   char msg[512];
   va_list ap;
@@ -215,9 +233,9 @@ extern "C" appd_status appd_get_stats(const appd_ctx* c, appd_stats* s) {
 }
 
 extern "C" appd_status appd_last_dendrogram(const appd_ctx* c, int32_t* pi, float* h, int64_t n) {
-  if (!c || !c->have_dendrogram || (int64_t)c->last_pi.size() != n) return APPD_ERR_INVALID_ARGUMENT;
-  if (pi) std::memcpy(pi, c->last_pi.data(), sizeof(int32_t) * n);
-  if (h && n > 1) std::memcpy(h, c->last_h.data(), sizeof(float) * (n - 1));
+  if (!c || !c->have_dendrogram || c->dend_n != n) return APPD_ERR_INVALID_ARGUMENT;
+  if (pi) std::memcpy(pi, c->dend_pi, sizeof(int32_t) * n);
+  if (h && n > 1) std::memcpy(h, c->dend_h, sizeof(float) * (n - 1));
   return APPD_OK;
 }
 
@@ -318,8 +336,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       if (s) return s;
     }
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->last_pi.assign(1, 0);
-    c->last_h.clear();
+    c->one_pi = 0;
+    c->dend_pi = &c->one_pi;
+    c->dend_h = nullptr;
+    c->dend_n = 1;
     c->have_dendrogram = true;
     c->stats.kernel_launches = c->launches;
     return APPD_OK;
@@ -455,15 +475,27 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   stage_event(c, 3);
 
   // ---- a5: dendrogram (v1: host union-find with list concatenation) ----
-  std::vector<u64> hkeys(n - 1);
-  APPD_CUDA(c, cudaMemcpyAsync(hkeys.data(), sorted, sizeof(u64) * (n - 1), cudaMemcpyDeviceToHost, c->stream));
+  // the GPU decodes the sorted keys to (u, v, w); pinned buffers keep the copies async
+  const int64_t m = n - 1;
+  int32_t* d_eu = (int32_t*)ws(c, S_EDGES, (sizeof(int32_t) * 2 + sizeof(float)) * m + 64);
+  if (!d_eu) return fail(c, APPD_ERR_OUT_OF_MEMORY, "edge workspace");
+  int32_t* d_ev = d_eu + m;
+  float* d_ew = (float*)(d_ev + m);
+  if ((s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
+  uint8_t* hp = (uint8_t*)pinned_host(c, 12 * (size_t)m + 8 * (size_t)n + 64);
+  if (!hp) return fail(c, APPD_ERR_OUT_OF_MEMORY, "pinned host buffer");
+  int32_t* h_e = (int32_t*)hp;                // eu, ev, ew (12 m bytes)
+  int32_t* h_pi = (int32_t*)(hp + 12 * m);    // pi (4 n)
+  float* h_h = (float*)(h_pi + n);            // h (4 (n - 1))
+  APPD_CUDA(c, cudaMemcpyAsync(h_e, d_eu, 12 * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  c->last_pi.resize(n);
-  c->last_h.resize(n - 1);
-  host_dendrogram(hkeys.data(), n, ks, c->last_pi.data(), c->last_h.data());
+  if ((int64_t)c->uf_scratch.size() < 5 * n) c->uf_scratch.resize(5 * n);
+  host_dendrogram_uvw(h_e, h_e + m, (const float*)(h_e + 2 * m), n, h_pi, h_h, c->uf_scratch.data());
+  c->dend_pi = h_pi;
+  c->dend_h = h_h;
+  c->dend_n = n;
   c->have_dendrogram = true;
   c->stats.dendrogram = 1;
-  const int64_t m = n - 1;
   int levels = 1;
   while ((1ll << levels) <= m) levels++;
   const int64_t stride = m;
@@ -471,8 +503,8 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int* pos = (int*)ws(c, S_POS, sizeof(int) * n);
   float* ST = (float*)ws(c, S_ST, sizeof(float) * stride * levels);
   if (!pi || !pos || !ST) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
-  APPD_CUDA(c, cudaMemcpyAsync(pi, c->last_pi.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
-  APPD_CUDA(c, cudaMemcpyAsync(ST, c->last_h.data(), sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaMemcpyAsync(pi, h_pi, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaMemcpyAsync(ST, h_h, sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
   stage_event(c, 4);
 
   // ---- a6: fill prep ----

@@ -18,6 +18,14 @@
 
 namespace appd {
 
+static inline int32_t find_root_arr(int32_t* parent, int32_t x) {
+  while (parent[x] != x) {
+    parent[x] = parent[parent[x]];  // path halving
+    x = parent[x];
+  }
+  return x;
+}
+
 static inline int find_root(std::vector<int32_t>& parent, int32_t x) {
   while (parent[x] != x) {
     parent[x] = parent[parent[x]];  // path halving
@@ -60,6 +68,42 @@ void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32
   }
   int32_t root = find_root(parent, 0);
   int32_t x = head[root];
+  for (int64_t a = 0; a < n; a++) {
+    pi[a] = x;
+    if (a < n - 1) h[a] = gap[x];
+    x = next[x];
+  }
+}
+
+}  // namespace appd
+
+namespace appd {
+
+// Same algorithm on pre-decoded edges (u, v, w) in ascending key order; union by size
+// with path halving; int32 arrays (n < 2^31).
+void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
+                         int32_t* scratch /* 5 n */) {
+  if (n == 1) { pi[0] = 0; return; }
+  int32_t* parent = scratch;
+  int32_t* size = scratch + n;
+  int32_t* head = scratch + 2 * n;
+  int32_t* tail = scratch + 3 * n;
+  int32_t* next = scratch + 4 * n;
+  std::vector<float> gap(n, 0.0f);
+  for (int64_t i = 0; i < n; i++) { parent[i] = (int32_t)i; size[i] = 1; head[i] = (int32_t)i; tail[i] = (int32_t)i; next[i] = -1; }
+  for (int64_t e = 0; e < n - 1; e++) {
+    int32_t ru = find_root_arr(parent, eu[e]), rv = find_root_arr(parent, ev[e]);
+    next[tail[ru]] = head[rv];
+    gap[tail[ru]] = ew[e];
+    const int32_t nh = head[ru], nt = tail[rv];
+    const int32_t r = size[ru] >= size[rv] ? ru : rv;
+    const int32_t o = r == ru ? rv : ru;
+    parent[o] = r;
+    size[r] = size[ru] + size[rv];
+    head[r] = nh;
+    tail[r] = nt;
+  }
+  int32_t x = head[find_root_arr(parent, 0)];
   for (int64_t a = 0; a < n; a++) {
     pi[a] = x;
     if (a < n - 1) h[a] = gap[x];

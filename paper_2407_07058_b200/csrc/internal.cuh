@@ -96,9 +96,11 @@ struct appd_ctx {
   int sm_count = 148;
   // workspace (grown on demand)
   appd::DevBuf buf[64];
-  // host-side copies of the last dendrogram
-  std::vector<int32_t> last_pi;
-  std::vector<float> last_h;
+  // the last dendrogram (in the pinned host buffer)
+  int32_t* dend_pi = nullptr;
+  float* dend_h = nullptr;
+  int64_t dend_n = 0;
+  int32_t one_pi = 0;
   bool have_dendrogram = false;
   // events for stage timing
   cudaEvent_t ev[16];
@@ -107,6 +109,7 @@ struct appd_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
+  std::vector<int32_t> uf_scratch;   // host dendrogram work arrays
 };
 
 namespace appd {
@@ -118,7 +121,7 @@ enum Slot {
   S_HOST_IN, S_HOST_OUT,
   S_TC_PART, S_TC_CENTER, S_TC_YA, S_TC_YB, S_TC_NRM, S_TC_LEN, S_TC_TML, S_TC_PERM, S_TC_SC, S_TC_KEYS,
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
-  S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV,
+  S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 64, "workspace slots");
@@ -212,6 +215,11 @@ appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t cou
 
 // host dendrogram (dendrogram_host.cpp)
 void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32_t* pi, float* h);
+void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
+                         int32_t* scratch /* 5 n */);
+appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const KeySpec& ks, int32_t* eu,
+                                int32_t* ev, float* ew);
+void* pinned_host(appd_ctx* c, size_t bytes);  // grows ctx->pinned
 
 // NCCL (nccl_shim.cpp)
 appd_status nccl_unique_id(uint8_t out[128], std::string* err);

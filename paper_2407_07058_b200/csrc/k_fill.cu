@@ -220,3 +220,38 @@ appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_
 }
 
 }  // namespace appd
+
+namespace appd {
+
+// sorted MST edge keys -> endpoints and weights (the dendrogram's input)
+__global__ void k_decode_edges(const u64* __restrict__ keys, int64_t m, int shift, int points, int sense,
+                               int32_t* __restrict__ eu, int32_t* __restrict__ ev, float* __restrict__ ew) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const u64 key = keys[e];
+    int64_t u, v;
+    tri_decode(key & ((1ull << shift) - 1), &u, &v);
+    const uint32_t wk = (uint32_t)(key >> shift);
+    float w;
+    if (points) {
+      w = __fsqrt_rn(__uint_as_float(wk));  // R1: the weight is sqrtf of the squared distance
+    } else {
+      const float mm = from_orderable(wk);
+      w = (sense > 0 ? mm : -mm) + 0.0f;
+    }
+    eu[e] = (int32_t)u;
+    ev[e] = (int32_t)v;
+    ew[e] = w;
+  }
+}
+
+appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const KeySpec& ks, int32_t* eu,
+                                int32_t* ev, float* ew) {
+  if (m <= 0) return APPD_OK;
+  int grid = (int)((m + 255) / 256);
+  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  k_decode_edges<<<grid, 256, 0, c->stream>>>(keys, m, ks.shift, ks.points ? 1 : 0, ks.sense, eu, ev, ew);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd
