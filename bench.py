@@ -162,11 +162,9 @@ def run_native(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(P.appd_get_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        from paper_2407_07058_b200.distributed import broadcast_nccl_id
+
+        nccl_id = broadcast_nccl_id()
 
     A, c = load_input(args.workload)
     n = c["n"]
