@@ -186,16 +186,20 @@ def run_native(args):
         else:
             ctx.solve_weights(Xd, M)
 
+    sampler = ClockSampler(local)
+    sampler.start()  # nvidia-smi needs ~0.5 s to start; it keeps sampling through the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    t_wait = time.perf_counter()
+    while not sampler.rows and time.perf_counter() - t_wait < 5.0:
+        time.sleep(0.05)
+    sampler.rows.clear()  # keep only samples taken from here on
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stats = []
-    sampler = ClockSampler(local)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     for s in range(args.steps):
         flush.fill_(float(s))  # L2 flush between timed steps (outside the events)
         ev[s][0].record(stream)
@@ -226,8 +230,26 @@ def run_native(args):
                 "algorithmic_bytes_per_launch": fill_bytes, "avg_launch_ms": fill_ms,
                 "peak_source": pk["source"]}
     stage_ms = {k: statistics.mean(s[k] for s in stats) for k in
-                ("ms_validate", "ms_mst", "ms_sort", "ms_dendrogram", "ms_prep", "ms_fill", "ms_total")}
-    if mst_ms > fill_ms and points:
+                ("ms_validate", "ms_mst", "ms_sort", "ms_dendrogram", "ms_prep", "ms_fill", "ms_total", "ms_scan",
+                 "ms_tcscan")}
+    fill_roof = {"kernel": "k_fill", "achieved_gbs": fill_gbs, "peak_gbs": pk["hbm_gbs"],
+                 "frac": fill_gbs / pk["hbm_gbs"], "avg_launch_ms": fill_ms, "algorithmic_bytes_per_launch": fill_bytes}
+    tc_ms = statistics.mean(s["ms_tcscan"] for s in stats)
+    tc_launches = stats[-1]["tcscan_launches"]
+    if points and tc_launches and tc_ms > fill_ms:
+        # tensor-core scan (one launch per Boruvka round): the algorithmic work is the Gram term
+        # -2 X^T X, 2*d flops per (row, column) pair; fp16 inputs run at the bf16 dense rate
+        flops = statistics.mean(s["tcscan_flops"] for s in stats) / tc_launches
+        avg = tc_ms / tc_launches
+        ach = flops / (avg / 1000) / 1e12
+        peak_tc = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops_sustained", 1377.8) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1400.0
+        roofline = {"bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
+                    "traffic": None, "kernel": "k_tcf_scan", "algorithmic_flops_per_launch": flops,
+                    "avg_launch_ms": avg, "launches_per_step": tc_launches,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 runs at the bf16 rate)",
+                    "fill": fill_roof}
+    elif mst_ms > fill_ms and points:
         # exact FP32 MST scan: 2*d lane-ops per (row, column) pair per Boruvka pass, ALU bound
         d = c["d"]
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count

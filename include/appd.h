@@ -107,6 +107,9 @@ typedef struct {
   double ms_scan;          /* device time of the MST scan kernels (timing = 1) */
   int64_t scan_launches;   /* launches of the MST scan kernels */
   int64_t tc_fallback_rows; /* tensor-core engine: rows re-scanned exactly over all columns (all rounds) */
+  double ms_tcscan;         /* tensor-core scan kernel time summed over rounds (timing = 1) */
+  int64_t tcscan_launches;  /* launches of the tensor-core scan kernel */
+  double tcscan_flops;      /* algorithmic flops of those launches: 2 * rows * n * d per round (the Gram term) */
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */

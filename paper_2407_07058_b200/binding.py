@@ -75,6 +75,9 @@ class appd_stats(ctypes.Structure):
         ("ms_scan", ctypes.c_double),
         ("scan_launches", ctypes.c_int64),
         ("tc_fallback_rows", ctypes.c_int64),
+        ("ms_tcscan", ctypes.c_double),
+        ("tcscan_launches", ctypes.c_int64),
+        ("tcscan_flops", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -453,7 +453,14 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
     if (use_tc) {
-      c->stats.tc_candidates += (int64_t)tc.h_counters[2] * 32 + (int64_t)tc.h_counters[0] * n;
+      if (c->opt.timing) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
+        cudaGetLastError();
+      }
+      c->stats.tcscan_launches++;
+      c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+      c->stats.tc_candidates += (int64_t)tc.h_counters[2] * 128 + (int64_t)tc.h_counters[0] * n;
       c->stats.tc_fallback_rows += tc.h_counters[0];
     }
     int64_t knew = (int64_t)hostk[0] + hostk[1];

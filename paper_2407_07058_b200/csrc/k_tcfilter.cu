@@ -514,7 +514,9 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   if (splits > P.col_tiles) splits = P.col_tiles;
   P.col_splits = splits;
   P.round0 = round == 0;
+  if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 0, P))) return s;
+  if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
 
   ExactParams E;
   E.XTp = st->XTp;
