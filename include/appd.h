@@ -87,7 +87,12 @@ typedef struct {
   int32_t dendrogram;            /* 0 auto, 1 host union-find, 2 GPU */
   int32_t points_engine;         /* points-mode MST scan: 0 auto, 1 exact FP32 (CUDA cores), 2 tensor-core
                                     filter + exact recheck of the survivors (tcgen05) */
-  int32_t reserved[7];
+  int32_t topk;                  /* tensor-core engine: per-row candidate cache length K built in round 0
+                                    (0 = auto (16), 4/8/16/32; -1 = no cache: every round scans all rows) */
+  int32_t finish_k;              /* tensor-core engine: finish the MST on the contracted component graph
+                                    once at most this many components remain (0 = auto (128), -1 = never;
+                                    at most 128) */
+  int32_t reserved[5];
 } appd_options;
 
 typedef struct {
@@ -110,6 +115,13 @@ typedef struct {
   double ms_tcscan;         /* tensor-core scan kernel time summed over rounds (timing = 1) */
   int64_t tcscan_launches;  /* launches of the tensor-core scan kernel */
   double tcscan_flops;      /* algorithmic flops of those launches: 2 * rows * n * d per round (the Gram term) */
+  int32_t topk;             /* cache length K used (0: no cache) */
+  int32_t rescan_rounds;    /* rounds >= 1 that needed a tensor-core re-scan */
+  int64_t cache_invalid_rows; /* rows whose round-0 candidate list overflowed (always re-scanned) */
+  int64_t rescan_rows;      /* rows re-scanned in rounds >= 1 (summed over rounds) */
+  int64_t rescan_blocks;    /* 512-row blocks re-scanned in rounds >= 1 (summed over rounds) */
+  int32_t cm_k;             /* components left when the component-matrix finish ran (0: not used) */
+  int32_t cm_pad;
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */

@@ -45,7 +45,9 @@ class appd_options(ctypes.Structure):
         ("timing", ctypes.c_int32),
         ("dendrogram", ctypes.c_int32),
         ("points_engine", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 7),
+        ("topk", ctypes.c_int32),
+        ("finish_k", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 5),
     ]
 
 
@@ -78,6 +80,13 @@ class appd_stats(ctypes.Structure):
         ("ms_tcscan", ctypes.c_double),
         ("tcscan_launches", ctypes.c_int64),
         ("tcscan_flops", ctypes.c_double),
+        ("topk", ctypes.c_int32),
+        ("rescan_rounds", ctypes.c_int32),
+        ("cache_invalid_rows", ctypes.c_int64),
+        ("rescan_rows", ctypes.c_int64),
+        ("rescan_blocks", ctypes.c_int64),
+        ("cm_k", ctypes.c_int32),
+        ("cm_pad", ctypes.c_int32),
     ]
 
     def as_dict(self):
@@ -183,7 +192,8 @@ class Context:
 
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  variant: int = VARIANT_AUTO, validate: bool = True, sense: int = 1, timing: bool = False,
-                 dendrogram: int = 0, points_engine: int = 0):
+                 dendrogram: int = 0, points_engine: int = 0, topk: int = 0,
+                 finish_k: int = 0):
         L = load()
         o = appd_options()
         L.appd_options_init(ctypes.byref(o))
@@ -200,6 +210,8 @@ class Context:
         o.timing = 1 if timing else 0
         o.dendrogram = dendrogram
         o.points_engine = points_engine
+        o.topk = topk
+        o.finish_k = finish_k
         h = ctypes.c_void_p()
         s = L.appd_create(ctypes.byref(h), ctypes.byref(o))
         if s != APPD_OK:

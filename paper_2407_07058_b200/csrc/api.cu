@@ -397,14 +397,82 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int* hostk = nullptr;
   int hk[2];
   hostk = hk;
+  const int finish_k = c->opt.finish_k == 0 ? 128 : std::min(c->opt.finish_k, 128);
   while (k > 1) {
+    // ---- component-matrix finish: the contracted k-node graph's exact edge keys ----
+    if (use_tc && tc.topk && rounds > 0 && finish_k > 0 && k <= finish_k) {
+      u64* WCM = (u64*)ws(c, S_TC_WCM, sizeof(u64) * k * k);
+      if (!WCM) return fail(c, APPD_ERR_OUT_OF_MEMORY, "component matrix");
+      bool ovf = false;
+      if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
+      if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf))) return s;
+      if (c->opt.world > 1) {  // every rank must take the same branch
+        u64* flag = (u64*)ws(c, S_TMP, sizeof(u64));
+        if (!flag) return fail(c, APPD_ERR_OUT_OF_MEMORY, "flag");
+        const u64 hf = ovf ? 1 : 0;
+        APPD_CUDA(c, cudaMemcpyAsync(flag, &hf, sizeof hf, cudaMemcpyHostToDevice, c->stream));
+        if ((s = nccl_allreduce_max_u64(c, flag, 1))) return s;
+        u64 hf2 = 0;
+        APPD_CUDA(c, cudaMemcpyAsync(&hf2, flag, sizeof hf2, cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        ovf = hf2 != 0;
+        if (!ovf && (s = nccl_allreduce_min_u64(c, WCM, k * k))) return s;
+      }
+      if (!ovf) {
+        std::vector<u64> w((size_t)(k * k));
+        int cnt = 0;
+        APPD_CUDA(c, cudaMemcpyAsync(w.data(), WCM, sizeof(u64) * k * k, cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaMemcpyAsync(&cnt, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
+        // Prim on the contracted graph (keys are a strict order: the MST is unique)
+        std::vector<u64> best((size_t)k, KEY_NONE), edges;
+        std::vector<char> in((size_t)k, 0);
+        in[0] = 1;
+        for (int64_t q = 1; q < k; q++) best[q] = std::min(w[q], w[(size_t)q * k]);
+        for (int64_t step = 1; step < k; step++) {
+          int64_t b = -1;
+          for (int64_t q = 0; q < k; q++)
+            if (!in[q] && (b < 0 || best[q] < best[b])) b = q;
+          if (b < 0 || best[b] == KEY_NONE) return fail(c, APPD_ERR_CUDA, "component matrix has no edge");
+          in[b] = 1;
+          edges.push_back(best[b]);
+          for (int64_t q = 0; q < k; q++)
+            if (!in[q]) best[q] = std::min(best[q], std::min(w[(size_t)b * k + q], w[(size_t)q * k + b]));
+        }
+        if (cnt + (int64_t)edges.size() != n - 1)
+          return fail(c, APPD_ERR_CUDA, "component matrix: %d + %zu edges, expected %lld", cnt, edges.size(),
+                      (long long)(n - 1));
+        APPD_CUDA(c, cudaMemcpyAsync(mstkeys + cnt, edges.data(), sizeof(u64) * edges.size(), cudaMemcpyHostToDevice,
+                                     c->stream));
+        const int total = cnt + (int)edges.size();
+        APPD_CUDA(c, cudaMemcpyAsync(counters, &total, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
+        c->stats.cm_k = (int)k;
+        c->stats.tcscan_launches++;
+        c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+        if (c->opt.timing) {
+          float ms = 0.0f;
+          if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
+          cudaGetLastError();
+        }
+        if (getenv("APPD_DEBUG_ROUNDS"))
+          fprintf(stderr, "[appd] component-matrix finish at k %lld: listed %u\n", (long long)k, tc.h_counters[1]);
+        rounds++;
+        k = 1;
+        break;
+      }
+    }
+    static const bool dbg = getenv("APPD_DEBUG_ROUNDS") != nullptr;
+    if (dbg) cudaEventRecord(c->ev[12], c->stream);
     if ((s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
     if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
     const int64_t l0 = c->launches;
     if (points && use_tc) {
       bool overflowed = false;
-      if ((s = tcf_round(c, &tc, X, comp, rounds, compbest, rt_begin, rt_end, &overflowed))) return s;
+      if ((s = tcf_round(c, &tc, X, comp, rounds, k, compbest, rt_begin, rt_end, &overflowed))) return s;
       if (overflowed) {  // candidate buffer too small for this input: exact scan for this round
         if ((s = ensure_xt())) return s;
         s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
@@ -450,20 +518,41 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (dbg) cudaEventRecord(c->ev[13], c->stream);
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
     if (use_tc) {
-      if (c->opt.timing) {
+      if (c->opt.timing && (rounds == 0 || !tc.topk || tc.last_rescan_rows > 0)) {
         float ms = 0.0f;
         if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
         cudaGetLastError();
       }
-      c->stats.tcscan_launches++;
-      c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
       c->stats.tc_candidates += (int64_t)tc.h_counters[2] * 128 + (int64_t)tc.h_counters[0] * n;
       c->stats.tc_fallback_rows += tc.h_counters[0];
+      c->stats.topk = tc.topk;
+      if (rounds == 0) {
+        c->stats.tcscan_launches++;
+        c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+        if (tc.topk) c->stats.cache_invalid_rows = tc.h_counters[0];
+      } else if (!tc.topk) {
+        c->stats.tcscan_launches++;
+        c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+      } else if (tc.last_rescan_rows > 0) {
+        const int64_t blocks = c->pinned_small[8];
+        c->stats.rescan_rounds++;
+        c->stats.rescan_rows += tc.last_rescan_rows;
+        c->stats.rescan_blocks += blocks;
+        c->stats.tcscan_launches++;
+        c->stats.tcscan_flops += 2.0 * (double)std::min<int64_t>(blocks * 512, n) * n * d;
+      }
     }
     int64_t knew = (int64_t)hostk[0] + hostk[1];
+    if (dbg && use_tc && rounds == 0 && tc.topk)
+      fprintf(stderr, "[appd] cache build: listed (row, 32-col chunk) pairs %u\n", tc.h_counters[5]);
+    if (dbg)
+      fprintf(stderr, "[appd] round %d (%.3f ms): k %lld -> %lld  rescan rows %lld blocks %u  exact tiles %u fallback %u\n",
+              rounds, ev_ms(c, 12, 13), (long long)k, (long long)knew, (long long)(use_tc ? tc.last_rescan_rows : 0),
+              use_tc ? c->pinned_small[8] : 0u, use_tc ? tc.h_counters[2] : 0u, use_tc ? tc.h_counters[0] : 0u);
     rounds++;
     if (knew >= k || knew < 1) return fail(c, APPD_ERR_CUDA, "Boruvka made no progress (k = %lld)", (long long)k);
     k = knew;

@@ -122,6 +122,8 @@ enum Slot {
   S_TC_PART, S_TC_CENTER, S_TC_YA, S_TC_YB, S_TC_NRM, S_TC_LEN, S_TC_TML, S_TC_PERM, S_TC_SC, S_TC_KEYS,
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
+  S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 64, "workspace slots");
@@ -147,10 +149,54 @@ struct TcState {
   void* list = nullptr;     // uint2 (row, tile) pairs that need the exact check
   unsigned list_cap = 0;
   float maxlen_scaled = 0.0f;
+  // round-0 candidate cache (k_cache.cu); topk == 0: no cache
+  int topk = 0, cap = 0;
+  int64_t cache_r0 = 0, cache_r1 = 0;  // original rows whose cache this rank holds
+  u64* ckey = nullptr;                 // [n][topk] exact edge keys, ascending
+  int* cj = nullptr;                   // [n][topk] other endpoint (original index)
+  int* ccnt = nullptr;                 // [n] entries (-1: invalid, always re-scanned)
+  int* need = nullptr;                 // [n] original order: re-scan this round
+  int* needp = nullptr;                // [npad] permuted order
+  int* blockflag = nullptr;            // [npad / 512 + 1]; rb_list follows, then the count
+  int* rb_list = nullptr;
+  int* rb_count = nullptr;
+  int* rows_list = nullptr;             // [n] flagged rows (original indices)
+  float* XT = nullptr;                 // d x npad original-order transpose (exact row kernel)
+  unsigned* compUB = nullptr;          // [n] component upper bound (scaled units, float bits)
+  float* UBK = nullptr;                // [npad]
+  float* thrK = nullptr;               // [npad]
+  unsigned* cand_cnt = nullptr;        // [npad]
+  u64* cand = nullptr;                 // [npad][cap]
+  // per-round statistics (host)
+  int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0;
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
-appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, u64* compbest,
-                      int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
+appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
+                      u64* compbest, int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
+
+appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, int64_t k, u64* WCM,
+                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow);
+
+// candidate cache (k_cache.cu)
+struct ErrModel;
+appd_status launch_topk_thr(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+                            const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
+                            float* thrK);
+appd_status launch_chunk_exact(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+                               const float* thrK, const float* UBK, const float* X, int n, int d, double s2,
+                               unsigned* cnt, u64* cand, int cap, unsigned* work);
+appd_status launch_topk_select(appd_ctx* c, int p_begin, int p_end, int n, int K, const unsigned* cnt,
+                               const u64* cand, int cap, u64* ckey, int* cj, int* ccnt, u64* compbest, int* fallback,
+                               unsigned* nfallback);
+appd_status launch_cache_lookup(appd_ctx* c, int r0, int r1, int K, int n, const u64* ckey, const int* cj,
+                                const int* ccnt, const int* comp, u64* compbest, int* need, unsigned* count,
+                                int* list);
+appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, int d, const int* rows,
+                              const unsigned* nrows, int max_rows, const int* comp, u64* compbest);
+appd_status launch_rescan_blocks(appd_ctx* c, int n, const int* perm, const int* need, int* needp, int* blockflag,
+                                 int nblocks, int* list, int* count);
+appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, double s2, const int* perm,
+                           const int* needp, const unsigned* UB, const int* comp, unsigned* compUB);
 int64_t tcf_row_tiles(const TcState* st);
 appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, float* tc_out, float* ref_out);
 

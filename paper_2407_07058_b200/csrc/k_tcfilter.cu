@@ -202,6 +202,10 @@ struct ExactParams {
   u64* compbest;
   unsigned* counters;  // [0] fallback rows, [1] listed tiles, [2] exact tiles evaluated
   int* fallback;
+  // re-scan rounds: only rows with needp[p] are filtered, against the tighter of their
+  // own bound and their component's (compUB, original-index component labels)
+  const int* needp;
+  const unsigned* compUB;
 };
 
 // One warp per 32 consecutive rows: every 64-column tile whose eligible maximum of G'
@@ -212,8 +216,10 @@ __global__ void k_filter_tiles(ExactParams E) {
   const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int p0 = E.p_begin + (blockIdx.x * warps + w) * 32; p0 < E.p_end; p0 += gridDim.x * warps * 32) {
     const int p = p0 + lane;
-    const bool valid = p < E.p_end;
-    const float ub = valid ? __uint_as_float(E.UB[p]) : 0.0f;
+    const bool valid = p < E.p_end && (!E.needp || E.needp[p]);
+    if (!__any_sync(0xffffffffu, valid)) continue;
+    float ub = valid ? __uint_as_float(E.UB[p]) : 0.0f;
+    if (valid && E.compUB) ub = fminf(ub, __uint_as_float(E.compUB[E.comp[E.perm[p]]]));
     const float ni = valid ? E.nrm[p] : 0.0f, li = valid ? E.len[p] : 0.0f;
     const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.maxlen) : INFINITY;
     bool flagged = false;
@@ -441,9 +447,38 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   st->h_counters = c->pinned_small;
   st->fallback = (int*)ws(c, S_TC_FALLBACK, sizeof(int) * (n + 1));
   st->rowflag = (int*)ws(c, S_TC_ROWFLAG, sizeof(int) * (n + 1));
-  st->TM = (float*)ws(c, S_TC_APPV, sizeof(float) * st->npad * (st->npad / TC_TMG));
+  // cache length: option (0 = auto 16, -1 = none); the cache needs K distinct 32-column chunks
+  st->topk = c->opt.topk == 0 ? 16 : (c->opt.topk < 0 ? 0 : c->opt.topk);
+  if (st->topk != 0 && st->topk != 4 && st->topk != 8 && st->topk != 16 && st->topk != 32)
+    return fail(c, APPD_ERR_INVALID_ARGUMENT, "topk = %d (0, -1, 4, 8, 16 or 32)", c->opt.topk);
+  // TM holds 32-column maxima in the cache-building round (4x the 128-column layout)
+  st->TM = (float*)ws(c, S_TC_APPV, sizeof(float) * st->npad * (st->npad / (st->topk ? 32 : TC_TMG)));
   st->list_cap = (unsigned)std::min<int64_t>(16 * n + 65536, (int64_t)1 << 30);
   st->list = ws(c, S_TC_APPPC, sizeof(uint2) * st->list_cap);
+  if (st->topk) {
+    st->cap = 4 * st->topk > 128 ? 128 : 4 * st->topk;
+    const int64_t nb = st->npad / TC_ROWS + 1;
+    st->ckey = (u64*)ws(c, S_TC_CKEY, sizeof(u64) * n * st->topk);
+    st->cj = (int*)ws(c, S_TC_CJ, sizeof(int) * n * st->topk);
+    st->ccnt = (int*)ws(c, S_TC_CCNT, sizeof(int) * n);
+    st->need = (int*)ws(c, S_TC_NEED, sizeof(int) * n);
+    st->needp = (int*)ws(c, S_TC_NEEDP, sizeof(int) * st->npad);
+    st->blockflag = (int*)ws(c, S_TC_BLOCKFLAG, sizeof(int) * (2 * nb + 8));
+    st->rb_list = st->blockflag ? st->blockflag + nb : nullptr;
+    st->rb_count = st->blockflag ? st->blockflag + 2 * nb : nullptr;
+    st->compUB = (unsigned*)ws(c, S_TC_COMPUB, sizeof(unsigned) * std::max<int64_t>(n, 128 * 128));
+    st->UBK = (float*)ws(c, S_TC_UBK, sizeof(float) * st->npad);
+    st->thrK = (float*)ws(c, S_TC_THRK, sizeof(float) * st->npad);
+    st->cand_cnt = (unsigned*)ws(c, S_TC_CANDCNT, sizeof(unsigned) * (st->npad + 8));
+    st->cand = (u64*)ws(c, S_TC_CANDK, sizeof(u64) * st->npad * st->cap);
+    st->rows_list = (int*)ws(c, S_TC_ROWLIST, sizeof(int) * (n + 1));
+    st->XT = (float*)ws(c, S_TC_XTO, sizeof(float) * st->npad * d);
+    if (!st->rows_list || !st->XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate cache workspace");
+    if (!st->ckey || !st->cj || !st->ccnt || !st->need || !st->needp || !st->blockflag || !st->compUB || !st->UBK ||
+        !st->thrK || !st->cand_cnt || !st->cand)
+      return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate cache workspace");
+  }
+  st->invalid_rows = 0;
   if (!st->YA || !st->YB || !st->XTp || !st->nrm || !st->len || !st->seg_maxlen ||
       !st->perm || !st->sc || !st->keys || !st->cstart || !st->cend || !st->rs || !st->re || !st->UB ||
       !st->counters || !st->fallback || !st->rowflag || !st->TM || !st->list)
@@ -482,14 +517,98 @@ static void fill_scan_params(const TcState* st, TcParams* P) {
   P->stages = st->stages;
   P->col_tiles = (int)(st->npad / TC_N);
   P->em = error_model(st);
+  P->seg32 = 0;
+  P->rb_list = nullptr;
+  P->rb_count = nullptr;
 }
 
-// one Boruvka round's scan: compbest[comp] = min over the component's rows of the exact edge key
-appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, u64* compbest,
-                      int64_t rb_begin, int64_t rb_end, bool* overflowed) {
+static void exact_params(const TcState* st, const TcParams& P, const int* comp, u64* compbest, int p_begin,
+                         int p_end, int round0, ExactParams* E) {
+  memset(E, 0, sizeof *E);
+  E->XTp = st->XTp;
+  E->npad = st->npad;
+  E->d = (int)st->d;
+  E->n = (int)st->n;
+  E->perm = st->perm;
+  E->nrm = st->nrm;
+  E->len = st->len;
+  E->seg_maxlen = st->seg_maxlen;
+  E->maxlen = st->maxlen_scaled;
+  E->cs = st->rs;
+  E->ce = st->re;
+  E->UB = st->UB;
+  E->TM = st->TM;
+  E->nseg = (int)(st->npad / TC_TMG);
+  E->p_begin = p_begin;
+  E->p_end = p_end;
+  E->list = (uint2*)st->list;
+  E->list_cap = st->list_cap;
+  E->rowflag = st->rowflag;
+  E->round0 = round0;
+  E->em = P.em;
+  E->comp = comp;
+  E->compbest = compbest;
+  E->counters = st->counters;
+  E->fallback = st->fallback;
+}
+
+// re-scans of at most this many rows run the exact row kernel instead of a tensor-core pass
+constexpr int kSmallRescan = 1024;
+
+static int col_splits_for(appd_ctx* c, int64_t row_blocks, int col_tiles) {
+  int splits = (int)std::max<int64_t>(1, (c->sm_count * 3 + row_blocks - 1) / std::max<int64_t>(row_blocks, 1));
+  return splits > col_tiles ? col_tiles : splits;
+}
+
+// filter + exact re-check of the listed (row, 128-column segment) pairs + full-row
+// fallback; compbest[comp] receives the exact minimum keys
+static appd_status exact_stage(appd_ctx* c, const ExactParams& E) {
+  const int rows = E.p_end - E.p_begin;
+  if (rows <= 0) return APPD_OK;
+  k_filter_tiles<<<std::min(c->sm_count * 8, (rows + 255) / 256), 256, 0, c->stream>>>(E);
+  APPD_LAUNCHED(c);
+  k_exact_tiles<<<c->sm_count * 16, 256, 0, c->stream>>>(E);
+  APPD_LAUNCHED(c);
+  k_exact_rows<<<c->sm_count * 2, 256, 0, c->stream>>>(E);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// One Boruvka round's scan: compbest[comp] = min over the component's rows of the exact
+// edge key.  With the candidate cache (st->topk > 0): round 0 builds the cache on the
+// tensor cores (32-column maxima) and takes every row's minimum from it; later rounds
+// serve rows from the cache and re-scan (tensor cores, 128-column maxima) only the
+// 512-row blocks holding rows whose cache cannot decide.  Without the cache every
+// round scans all of this rank's rows.
+appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
+                      u64* compbest, int64_t rb_begin, int64_t rb_end, bool* overflowed) {
   const int64_t n = st->n;
   const int grid_n = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+  const int T = (int)(st->npad / TC_ROWS);
+  const bool cache = st->topk > 0;
+  const double s2 = (double)st->scale * (double)st->scale;
   appd_status s;
+  *overflowed = false;
+  st->last_rescan_rows = 0;
+  st->last_rescan_blocks = 0;
+  st->h_counters[0] = st->h_counters[1] = st->h_counters[2] = 0;
+  c->pinned_small[8] = 0;
+  unsigned rescan_rows = 0;
+  if (cache && round > 0) {
+    APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
+    if ((s = launch_cache_lookup(c, (int)st->cache_r0, (int)st->cache_r1, st->topk, (int)n, st->ckey, st->cj,
+                                 st->ccnt, comp, compbest, st->need, st->counters + 3, st->rows_list)))
+      return s;
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, st->counters + 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    rescan_rows = c->pinned_small[9];
+    st->last_rescan_rows = rescan_rows;
+    if (rescan_rows == 0) return APPD_OK;  // every component decided by the cache
+    if (rescan_rows <= (unsigned)kSmallRescan)  // a few rows: exact FP32 rows, no permutation / tensor pass
+      return launch_rows_exact(c, st->XT, st->npad, (int)n, (int)st->d, st->rows_list, st->counters + 3,
+                               (int)rescan_rows, comp, compbest);
+  }
   if (round == 0) {
     if ((s = launch_iota(c, st->perm, n))) return s;
   } else {
@@ -507,56 +626,208 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
   TcParams P;
   fill_scan_params(st, &P);
+  P.round0 = round == 0;
+  const int p_begin = (int)(rb_begin * TC_ROWS);
+  const int p_end = (int)std::min<int64_t>(rb_end * TC_ROWS, n);
+  ExactParams E;
+
+  if (cache && round == 0) {
+    // original-order transpose for the exact row kernel (round 0: the permutation is the identity)
+    APPD_CUDA(c, cudaMemcpyAsync(st->XT, st->XTp, sizeof(float) * st->npad * st->d, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    // ---- cache-building scan: 32-column maxima of every row of this rank ----
+    P.rb_begin = (int)rb_begin;
+    P.rb_end = (int)rb_end;
+    P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
+    P.seg32 = 1;
+    if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
+    if ((s = launch_tcf_scan(c, 1, P))) return s;
+    if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    if (p_end > p_begin) {
+      const int nch = (int)(st->npad / 32);
+      APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
+      if ((s = launch_topk_thr(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
+                               st->maxlen_scaled, P.em, st->UBK, st->thrK)))
+        return s;
+      if ((s = launch_chunk_exact(c, st->TM, st->npad, nch, p_begin, p_end, st->thrK, st->UBK, X, (int)n,
+                                  (int)st->d, s2, st->cand_cnt, st->cand, st->cap, st->counters + 4)))
+        return s;
+      if ((s = launch_topk_select(c, p_begin, p_end, (int)n, st->topk, st->cand_cnt, st->cand, st->cap, st->ckey,
+                                  st->cj, st->ccnt, compbest, st->fallback, st->counters + 0)))
+        return s;
+      // rows whose candidate list overflowed: exact minimum over the whole row (singletons)
+      if ((s = launch_rows_exact(c, st->XT, st->npad, (int)n, (int)st->d, st->fallback, st->counters + 0,
+                                 p_end - p_begin, nullptr, compbest)))
+        return s;
+    }
+    st->cache_r0 = p_begin;
+    st->cache_r1 = p_end;
+  } else if (cache) {
+    // ---- re-scan of the blocks holding flagged rows ----
+    APPD_CUDA(c, cudaMemsetAsync(st->blockflag, 0, sizeof(int) * (2 * (T + 1) + 8), c->stream));
+    if ((s = launch_rescan_blocks(c, (int)n, st->perm, st->need, st->needp, st->blockflag, T, st->rb_list,
+                                  st->rb_count)))
+      return s;
+    P.rb_list = st->rb_list;
+    P.rb_count = st->rb_count;
+    P.rb_begin = 0;
+    P.rb_end = (int)std::min<int64_t>(T, rescan_rows);  // upper bound on the listed blocks (grid sizing)
+    P.col_splits = col_splits_for(c, P.rb_end, P.col_tiles);
+    if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
+    if ((s = launch_tcf_scan(c, 0, P))) return s;
+    if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    if ((s = launch_comp_ub(c, (int)n, (int)k, compbest, s2, st->perm, st->needp, st->UB, comp, st->compUB)))
+      return s;
+    exact_params(st, P, comp, compbest, 0, (int)n, 0, &E);
+    E.needp = st->needp;
+    E.compUB = st->compUB;
+    if ((s = exact_stage(c, E))) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 8, st->rb_count, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 c->stream));
+  } else {
+    // ---- no cache: every row of this rank ----
+    P.rb_begin = (int)rb_begin;
+    P.rb_end = (int)rb_end;
+    P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
+    if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
+    if ((s = launch_tcf_scan(c, 0, P))) return s;
+    if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    exact_params(st, P, comp, compbest, p_begin, p_end, round == 0, &E);
+    if ((s = exact_stage(c, E))) return s;
+  }
+  // statistics land in pinned memory; read after the round's stream synchronisation
+  APPD_CUDA(c, cudaMemcpyAsync(st->h_counters, st->counters, 8 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               c->stream));
+  return APPD_OK;
+}
+
+// Component-matrix finish (k_cache.cu): one tensor-core pass over this rank's rows,
+// then WCM[C][D] = exact minimum edge key between components C and D (k x k, device).
+// *listed_overflow is set when the candidate list overflowed (the caller then runs an
+// ordinary round instead).
+appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, int64_t k, u64* WCM,
+                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow) {
+  const int64_t n = st->n;
+  const int grid_n = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
+  appd_status s;
+  *listed_overflow = false;
+  k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
+  APPD_LAUNCHED(c);
+  if ((s = sort_pairs_i32(c, st->keys, st->sc, st->keys + n + 1, st->perm, n))) return s;
+  k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
+  APPD_LAUNCHED(c);
+  k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
+  APPD_LAUNCHED(c);
+  if ((s = tcf_pack(c, st, X))) return s;
+  APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));
+  APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
+  unsigned* CUB = st->compUB;  // k x k <= 128 x 128 words (the buffer holds n >= k^2 words or more)
+  APPD_CUDA(c, cudaMemsetAsync(CUB, 0x7F, sizeof(unsigned) * k * k, c->stream));  // ~3.4e38: permissive
+  APPD_CUDA(c, cudaMemsetAsync(WCM, 0xFF, sizeof(u64) * k * k, c->stream));
+  TcParams P;
+  fill_scan_params(st, &P);
+  P.round0 = 0;
   P.rb_begin = (int)rb_begin;
   P.rb_end = (int)rb_end;
-  const int64_t rbs = rb_end - rb_begin;
-  int splits = (int)std::max<int64_t>(1, (c->sm_count * 3 + rbs - 1) / std::max<int64_t>(rbs, 1));
-  if (splits > P.col_tiles) splits = P.col_tiles;
-  P.col_splits = splits;
-  P.round0 = round == 0;
+  P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 0, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
-
-  ExactParams E;
-  E.XTp = st->XTp;
-  E.npad = st->npad;
-  E.d = (int)st->d;
-  E.n = (int)n;
-  E.perm = st->perm;
-  E.nrm = st->nrm;
-  E.len = st->len;
-  E.seg_maxlen = st->seg_maxlen;
-  E.maxlen = st->maxlen_scaled;
-  E.cs = st->rs;
-  E.ce = st->re;
-  E.UB = st->UB;
-  E.TM = st->TM;
-  E.nseg = (int)(st->npad / TC_TMG);
-  E.p_begin = (int)(rb_begin * TC_ROWS);
-  E.p_end = (int)std::min<int64_t>(rb_end * TC_ROWS, n);
-  E.list = (uint2*)st->list;
-  E.list_cap = st->list_cap;
-  E.rowflag = st->rowflag;
-  E.round0 = round == 0;
-  E.em = P.em;
-  E.comp = comp;
-  E.compbest = compbest;
-  E.counters = st->counters;
-  E.fallback = st->fallback;
-  const int rows = E.p_end - E.p_begin;
-  if (rows > 0) {
-    k_filter_tiles<<<std::min(c->sm_count * 8, (rows + 255) / 256), 256, 0, c->stream>>>(E);
-    APPD_LAUNCHED(c);
-    k_exact_tiles<<<c->sm_count * 16, 256, 0, c->stream>>>(E);
-    APPD_LAUNCHED(c);
-    k_exact_rows<<<c->sm_count * 2, 256, 0, c->stream>>>(E);
-    APPD_LAUNCHED(c);
+  CmParams C;
+  memset(&C, 0, sizeof C);
+  C.TM = st->TM;
+  C.ld = st->npad;
+  C.nseg = (int)(st->npad / TC_TMG);
+  C.n = (int)n;
+  C.k = (int)k;
+  C.p_begin = (int)(rb_begin * TC_ROWS);
+  C.p_end = (int)std::min<int64_t>(rb_end * TC_ROWS, n);
+  C.sc = st->sc;
+  C.cstart = st->cstart;
+  C.cend = st->cend;
+  C.nrm = st->nrm;
+  C.len = st->len;
+  C.seg_maxlen = st->seg_maxlen;
+  C.maxlen = st->maxlen_scaled;
+  C.em = P.em;
+  C.CUB = CUB;
+  C.list = (uint2*)st->list;
+  C.list_cap = st->list_cap;
+  C.counters = st->counters;
+  C.XTp = st->XTp;
+  C.d = (int)st->d;
+  C.perm = st->perm;
+  C.WCM = WCM;
+  if ((s = launch_cm_rowub(c, C))) return s;
+  // Listing thresholds.  CUB[C][D] bounds the exact minimum w(C, D) from above (both
+  // directions bound the same w).  A contracted MST edge (C, D) also satisfies
+  // w(C, D) <= the largest bound on the path from C to D in the MST of the bounds
+  // (cut property), so T = min(sym bound, path maximum) keeps every MST edge's minimum
+  // pair listed; pairs above T are not MST edges and may come out inflated.
+  {
+    std::vector<unsigned> ub((size_t)(k * k));
+    APPD_CUDA(c, cudaMemcpyAsync(ub.data(), CUB, sizeof(unsigned) * k * k, cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    std::vector<float> sym((size_t)(k * k));
+    for (int64_t a = 0; a < k; a++)
+      for (int64_t b = 0; b < k; b++) {
+        float x, y;
+        memcpy(&x, &ub[a * k + b], 4);
+        memcpy(&y, &ub[b * k + a], 4);
+        sym[a * k + b] = std::min(x, y);
+      }
+    // Prim on the bounds, then the path maximum from every node (k <= 128)
+    std::vector<int> par((size_t)k, -1);
+    std::vector<float> key((size_t)k, INFINITY);
+    std::vector<char> in((size_t)k, 0);
+    key[0] = 0.0f;
+    for (int64_t it = 0; it < k; it++) {
+      int64_t b = -1;
+      for (int64_t q = 0; q < k; q++)
+        if (!in[q] && (b < 0 || key[q] < key[b])) b = q;
+      in[b] = 1;
+      for (int64_t q = 0; q < k; q++)
+        if (!in[q] && sym[b * k + q] < key[q]) {
+          key[q] = sym[b * k + q];
+          par[q] = (int)b;
+        }
+    }
+    std::vector<std::vector<std::pair<int, float>>> adj((size_t)k);
+    for (int64_t q = 1; q < k; q++)
+      if (par[q] >= 0) {
+        adj[q].push_back({par[q], key[q]});
+        adj[par[q]].push_back({(int)q, key[q]});
+      }
+    std::vector<unsigned> T((size_t)(k * k));
+    std::vector<float> pm((size_t)k);
+    std::vector<int> stack;
+    for (int64_t r = 0; r < k; r++) {
+      std::fill(pm.begin(), pm.end(), -1.0f);
+      pm[r] = 0.0f;
+      stack.assign(1, (int)r);
+      while (!stack.empty()) {
+        const int x = stack.back();
+        stack.pop_back();
+        for (auto& e : adj[x])
+          if (pm[e.first] < 0.0f) {
+            pm[e.first] = std::max(pm[x], e.second);
+            stack.push_back(e.first);
+          }
+      }
+      for (int64_t q = 0; q < k; q++) {
+        // unreachable (no bound anywhere): stay permissive
+        const float t = pm[q] < 0.0f ? sym[r * k + q] : std::min(sym[r * k + q], pm[q]);
+        memcpy(&T[r * k + q], &t, 4);
+      }
+    }
+    APPD_CUDA(c, cudaMemcpyAsync(CUB, T.data(), sizeof(unsigned) * k * k, cudaMemcpyHostToDevice, c->stream));
+    if ((s = launch_cm_exact(c, C))) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(st->h_counters, st->counters, 4 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));  // T must outlive the copy
   }
-  *overflowed = false;
-  // statistics land in pinned memory; read after the round's stream synchronisation
-  APPD_CUDA(c, cudaMemcpyAsync(st->h_counters, st->counters, 4 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                               c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (st->h_counters[1] > st->list_cap) *listed_overflow = true;
   return APPD_OK;
 }
 

@@ -92,7 +92,7 @@ __device__ __forceinline__ float chunk_max(const float (&v)[32], const RowState&
   return m;
 }
 
-template <int PASS>
+template <int PASS, bool SEG32 = false>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = P.K;
@@ -131,8 +131,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int items = (P.rb_end - P.rb_begin) * P.col_splits;
+  const int nrb = P.rb_list ? *P.rb_count : (P.rb_end - P.rb_begin);
+  const int items = nrb * P.col_splits;
   const int per_split = (P.col_tiles + P.col_splits - 1) / P.col_splits;
+  auto rb_of = [&](int it) -> int {
+    const int b = it / P.col_splits;
+    return P.rb_list ? __ldg(P.rb_list + b) : P.rb_begin + b;
+  };
 
   if (warp == 0) {
     // ---------------- producer ----------------
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
       uint32_t ph = 0, aph = 0;
       bool first = true;
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int rb = P.rb_begin + it / P.col_splits;
+        const int rb = rb_of(it);
         const int sp = it % P.col_splits;
         const int ct0 = sp * per_split;
         const int ct1 = min(P.col_tiles, ct0 + per_split);
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     const int h = (warp - 2) >> 2;
     uint32_t tph[TC_NBUF] = {};
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
-      const int rb = P.rb_begin + it / P.col_splits;
+      const int rb = rb_of(it);
       const int sp = it % P.col_splits;
       const int ct0 = sp * per_split;
       const int ct1 = min(P.col_tiles, ct0 + per_split);
@@ -277,21 +282,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
           const bool fast =
               __all_sync(0xffffffffu, s.valid && (h0 + TC_TMG <= s.cs || h0 >= s.ce) && h0 + TC_TMG <= P.n);
           float m;
-          if (fast) {
-            m = fmax_seg(v);
-          } else {
-            m = -INFINITY;
+          if (SEG32) {
+            // four 32-column maxima (the same FMNMX3 count as one 128-column tree)
+            float cm[TC_TMG / 32];
 #pragma unroll
             for (int c = 0; c < TC_TMG / 32; c++) {
               float w[32];
 #pragma unroll
               for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
-              m = fmaxf(m, chunk_max(w, s, h0 + c * 32, false, P.n));
+              cm[c] = chunk_max(w, s, h0 + c * 32, fast, P.n);
             }
+            m = cm[0];
+#pragma unroll
+            for (int c = 1; c < TC_TMG / 32; c++) m = fmaxf(m, cm[c]);
+            if (s.valid) {
+#pragma unroll
+              for (int c = 0; c < TC_TMG / 32; c++) P.TM[(int64_t)(h0 / 32 + c) * P.tm_ld + s.p] = cm[c];
+            }
+          } else {
+            if (fast) {
+              m = fmax_seg(v);
+            } else {
+              m = -INFINITY;
+#pragma unroll
+              for (int c = 0; c < TC_TMG / 32; c++) {
+                float w[32];
+#pragma unroll
+                for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
+                m = fmaxf(m, chunk_max(w, s, h0 + c * 32, false, P.n));
+              }
+            }
+            // eligible maximum of G' over this (row, segment); a warp's rows are
+            // consecutive, so the store is coalesced ([segment][row] layout)
+            if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
           }
-          // eligible maximum of G' over this (row, segment); a warp's rows are
-          // consecutive, so the store is coalesced ([segment][row] layout)
-          if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
           if (s.valid && m > s.gbest) {  // tighten the bound only when the best improves
             s.gbest = m;
             s.ub = fminf(s.ub, em_upper(P.em, s.ni - 2.0f * m, s.ni, s.li, P.seg_maxlen[seg]));
@@ -322,6 +346,9 @@ int tcf_stages(int K) {
   return 0;
 }
 
+// pass 0: scan (128-column maxima), 1: scan with 32-column maxima (cache-building
+// round), 2: test hook (raw accumulators).  With a row-block list the grid is sized
+// for the host's upper bound P.rb_end - P.rb_begin; the kernel reads the count.
 appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   // at least 120 KB so that exactly one CTA (and one 512-column TMEM allocation) fits per SM
   size_t smem = tcf_smem_bytes(P.K, P.stages);
@@ -329,6 +356,7 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   static int attr_done = 0;
   if (!attr_done) {
     cudaFuncSetAttribute(k_tcf_scan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_tcf_scan<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = 1;
   }
@@ -349,6 +377,7 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
     cudaFuncSetAttribute(k_tcf_scan<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     k_tcf_scan<6><<<grid, TC_THREADS, smem, c->stream>>>(P);
   } else if (pass == 0) k_tcf_scan<0><<<grid, TC_THREADS, smem, c->stream>>>(P);
+  else if (pass == 1) k_tcf_scan<0, true><<<grid, TC_THREADS, smem, c->stream>>>(P);
   else k_tcf_scan<2><<<1, TC_THREADS, smem, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;

@@ -68,7 +68,40 @@ struct TcParams {
   ErrModel em;
   int round0;   // singletons (eligibility = j != i)
   float* dump;  // PASS 2 (test hook) only: raw accumulator of the first item
+  // TM granularity: 0 -> one maximum per TC_TMG (128) columns; 1 -> per 32 columns
+  // (the cache-building round 0: 4x the maxima, 1/4 of the exact re-check work)
+  int seg32;
+  // optional row-block list (re-scan rounds): items = *rb_count x col_splits over
+  // rb_list[]; when null the blocks rb_begin .. rb_end-1 are scanned
+  const int* rb_list;
+  const int* rb_count;
 };
+
+struct CmParams {
+  const float* TM;      // [nseg][npad]
+  int64_t ld;
+  int nseg;
+  int n, k;
+  int p_begin, p_end;
+  const int* sc;        // sorted component label per position
+  const int* cstart;
+  const int* cend;
+  const float* nrm;
+  const float* len;
+  const float* seg_maxlen;
+  float maxlen;
+  ErrModel em;
+  unsigned* CUB;        // [k][k] float bits
+  uint2* list;
+  unsigned list_cap;
+  unsigned* counters;   // [1] listed pairs, [2] exact evaluated
+  const float* XTp;
+  int d;
+  const int* perm;
+  u64* WCM;             // [k][k]
+};
+appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P);
+appd_status launch_cm_exact(appd_ctx* c, const CmParams& P);
 
 size_t tcf_smem_bytes(int K, int stages);
 int tcf_stages(int K);
