@@ -88,7 +88,7 @@ typedef struct {
   int32_t points_engine;         /* points-mode MST scan: 0 auto, 1 exact FP32 (CUDA cores), 2 tensor-core
                                     filter + exact recheck of the survivors (tcgen05) */
   int32_t topk;                  /* tensor-core engine: per-row candidate cache length K built in round 0
-                                    (0 = auto (16), 4/8/16/32; -1 = no cache: every round scans all rows) */
+                                    (0 = auto (8), 4/8/16/32; -1 = no cache: every round scans all rows) */
   int32_t finish_k;              /* tensor-core engine: finish the MST on the contracted component graph
                                     once at most this many components remain (0 = auto (128), -1 = never;
                                     at most 128) */

@@ -458,7 +458,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
           cudaGetLastError();
         }
         if (getenv("APPD_DEBUG_ROUNDS"))
-          fprintf(stderr, "[appd] component-matrix finish at k %lld: listed %u\n", (long long)k, tc.h_counters[1]);
+          fprintf(stderr, "[appd] component-matrix finish at k %lld: listed chunk entries %lld\n", (long long)k, (long long)tc.last_list_entries);
         rounds++;
         k = 1;
         break;
@@ -548,7 +548,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     int64_t knew = (int64_t)hostk[0] + hostk[1];
     if (dbg && use_tc && rounds == 0 && tc.topk)
-      fprintf(stderr, "[appd] cache build: listed (row, 32-col chunk) pairs %u\n", tc.h_counters[5]);
+      fprintf(stderr, "[appd] cache build: listed (row, 32-col chunk) pairs %lld\n", (long long)tc.last_list_entries);
     if (dbg)
       fprintf(stderr, "[appd] round %d (%.3f ms): k %lld -> %lld  rescan rows %lld blocks %u  exact tiles %u fallback %u\n",
               rounds, ev_ms(c, 12, 13), (long long)k, (long long)knew, (long long)(use_tc ? tc.last_rescan_rows : 0),
@@ -585,7 +585,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   float* h_h = (float*)(h_pi + n);            // h (4 (n - 1))
   APPD_CUDA(c, cudaMemcpyAsync(h_e, d_eu, 12 * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  if ((int64_t)c->uf_scratch.size() < 5 * n) c->uf_scratch.resize(5 * n);
+  if ((int64_t)c->uf_scratch.size() < 8 * n) c->uf_scratch.resize(8 * n);
   host_dendrogram_uvw(h_e, h_e + m, (const float*)(h_e + 2 * m), n, h_pi, h_h, c->uf_scratch.data());
   c->dend_pi = h_pi;
   c->dend_h = h_h;

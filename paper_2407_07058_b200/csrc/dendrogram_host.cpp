@@ -79,36 +79,60 @@ void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32
 
 namespace appd {
 
-// Same algorithm on pre-decoded edges (u, v, w) in ascending key order; union by size
-// with path halving; int32 arrays (n < 2^31).
+// Same merges on pre-decoded edges (u, v, w) in ascending key order, recorded as the
+// Kruskal reconstruction tree (leaves 0..n-1, internal node n+e for edge e, children =
+// the two clusters it joins) instead of linked lists; the leaf order is then the
+// tree's in-order, computed top-down (a node's parent has a larger rank, so one pass
+// over the edges in descending order places every subtree): independent stores instead
+// of a dependent walk.  Union by size with path halving on one 16-byte record per
+// vertex (one cache line per step).  scratch: 8 n int32.
+namespace {
+struct UfNode {
+  int32_t parent, size, rootnode, pad;
+};
+inline int32_t uf_find(UfNode* a, int32_t x) {
+  while (a[x].parent != x) {
+    const int32_t p = a[x].parent;
+    a[x].parent = a[p].parent;  // path halving
+    x = a[x].parent;
+  }
+  return x;
+}
+}  // namespace
+
 void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
-                         int32_t* scratch /* 5 n */) {
-  if (n == 1) { pi[0] = 0; return; }
-  int32_t* parent = scratch;
-  int32_t* size = scratch + n;
-  int32_t* head = scratch + 2 * n;
-  int32_t* tail = scratch + 3 * n;
-  int32_t* next = scratch + 4 * n;
-  std::vector<float> gap(n, 0.0f);
-  for (int64_t i = 0; i < n; i++) { parent[i] = (int32_t)i; size[i] = 1; head[i] = (int32_t)i; tail[i] = (int32_t)i; next[i] = -1; }
-  for (int64_t e = 0; e < n - 1; e++) {
-    int32_t ru = find_root_arr(parent, eu[e]), rv = find_root_arr(parent, ev[e]);
-    next[tail[ru]] = head[rv];
-    gap[tail[ru]] = ew[e];
-    const int32_t nh = head[ru], nt = tail[rv];
-    const int32_t r = size[ru] >= size[rv] ? ru : rv;
-    const int32_t o = r == ru ? rv : ru;
-    parent[o] = r;
-    size[r] = size[ru] + size[rv];
-    head[r] = nh;
-    tail[r] = nt;
+                         int32_t* scratch /* 8 n */) {
+  if (n == 1) {
+    pi[0] = 0;
+    return;
   }
-  int32_t x = head[find_root_arr(parent, 0)];
-  for (int64_t a = 0; a < n; a++) {
-    pi[a] = x;
-    if (a < n - 1) h[a] = gap[x];
-    x = next[x];
+  const int64_t m = n - 1;
+  UfNode* a = reinterpret_cast<UfNode*>(scratch);  // 4 n
+  int32_t* kid = scratch + 4 * n;                  // 2 m: children of internal node n + e
+  int32_t* lsize = scratch + 6 * n;                // m: leaves under the first child
+  for (int64_t i = 0; i < n; i++) a[i] = {(int32_t)i, 1, (int32_t)i, 0};
+  for (int64_t e = 0; e < m; e++) {
+    const int32_t ru = uf_find(a, eu[e]), rv = uf_find(a, ev[e]);
+    kid[2 * e] = a[ru].rootnode;
+    kid[2 * e + 1] = a[rv].rootnode;
+    lsize[e] = a[ru].size;
+    const int32_t sz = a[ru].size + a[rv].size;
+    const int32_t r = a[ru].size >= a[rv].size ? ru : rv, o = r == ru ? rv : ru;
+    a[o].parent = r;
+    a[r].size = sz;
+    a[r].rootnode = (int32_t)(n + e);
   }
+  // in-order offsets; the union-find records are dead, their space holds 2n - 1 offsets
+  int32_t* off = scratch;
+  off[n + m - 1] = 0;
+  for (int64_t e = m - 1; e >= 0; e--) {
+    const int32_t o = off[n + e];
+    const int32_t o2 = o + lsize[e];
+    off[kid[2 * e]] = o;
+    off[kid[2 * e + 1]] = o2;
+    h[o2 - 1] = ew[e];  // the gap between the two clusters is their merge height
+  }
+  for (int64_t v = 0; v < n; v++) pi[off[v]] = (int32_t)v;
 }
 
 }  // namespace appd

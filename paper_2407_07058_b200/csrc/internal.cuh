@@ -95,7 +95,7 @@ struct appd_ctx {
   void* nccl_comm = nullptr;
   int sm_count = 148;
   // workspace (grown on demand)
-  appd::DevBuf buf[64];
+  appd::DevBuf buf[96];
   // the last dendrogram (in the pinned host buffer)
   int32_t* dend_pi = nullptr;
   float* dend_h = nullptr;
@@ -123,10 +123,10 @@ enum Slot {
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
-  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS,
   S_NSLOTS
 };
-static_assert(S_NSLOTS <= 64, "workspace slots");
+static_assert(S_NSLOTS <= 96, "workspace slots");
 
 // tensor-core filtered points scan (k_tcfilter.cu)
 struct TcState {
@@ -162,13 +162,16 @@ struct TcState {
   int* rb_count = nullptr;
   int* rows_list = nullptr;             // [n] flagged rows (original indices)
   float* XT = nullptr;                 // d x npad original-order transpose (exact row kernel)
+  unsigned* lista = nullptr;           // (chunk << 17 | row) candidate entries, then sorted
+  unsigned* listb = nullptr;
+  unsigned list_entries_cap = 0;
   unsigned* compUB = nullptr;          // [n] component upper bound (scaled units, float bits)
   float* UBK = nullptr;                // [npad]
   float* thrK = nullptr;               // [npad]
   unsigned* cand_cnt = nullptr;        // [npad]
   u64* cand = nullptr;                 // [npad][cap]
   // per-round statistics (host)
-  int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0;
+  int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0, last_list_entries = 0;
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
@@ -182,9 +185,6 @@ struct ErrModel;
 appd_status launch_topk_thr(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
                             const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
                             float* thrK);
-appd_status launch_chunk_exact(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                               const float* thrK, const float* UBK, const float* X, int n, int d, double s2,
-                               unsigned* cnt, u64* cand, int cap, unsigned* work);
 appd_status launch_topk_select(appd_ctx* c, int p_begin, int p_end, int n, int K, const unsigned* cnt,
                                const u64* cand, int cap, u64* ckey, int* cj, int* ccnt, u64* compbest, int* fallback,
                                unsigned* nfallback);
@@ -256,13 +256,14 @@ int prim_max_n();
 
 // sorting (CUB)
 appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count);
+appd_status sort_keys_u32_bits(appd_ctx* c, const unsigned* in, unsigned* out, int64_t count, int begin_bit, int end_bit);
 appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count);
 appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t count);
 
 // host dendrogram (dendrogram_host.cpp)
 void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32_t* pi, float* h);
 void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
-                         int32_t* scratch /* 5 n */);
+                         int32_t* scratch /* 8 n */);
 appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const KeySpec& ks, int32_t* eu,
                                 int32_t* ev, float* ew);
 void* pinned_host(appd_ctx* c, size_t bytes);  // grows ctx->pinned

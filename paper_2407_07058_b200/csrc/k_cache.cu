@@ -40,7 +40,7 @@ __global__ void k_topk_thr(const float* __restrict__ TM32, int64_t ld, int nch, 
     float top[K];
 #pragma unroll
     for (int t = 0; t < K; t++) top[t] = -INFINITY;
-    constexpr int U = 16;  // loads in flight
+    constexpr int U = 32;  // loads in flight
     for (int c = 0; c < nch; c += U) {
       float v[U];
 #pragma unroll
@@ -69,139 +69,247 @@ __global__ void k_topk_thr(const float* __restrict__ TM32, int64_t ld, int nch, 
   }
 }
 
-struct ChunkParams {
-  const float* TM32;
-  int64_t ld;
-  int nch;
-  int p_begin, p_end;
-  const float* thrK;
-  const float* UBK;
-  const float* X;    // n x d, original order (round 0: permuted == original)
-  int n, d;
-  double s2;         // scale^2 (exact power of two)
-  unsigned* cnt;     // per row: appended candidates
-  u64* cand;         // [row][cap]
-  int cap;
-  unsigned* work;    // [0]: next chunk (dynamic scheduling)
-};
+// list entries: (32-column chunk << LIST_SHIFT) | row position (n <= 2^17, chunks < 2^12)
+constexpr int LIST_SHIFT = 17;
+constexpr unsigned LIST_ROWMASK = (1u << LIST_SHIFT) - 1u;
 
-// One CTA per chunk (dynamic scheduling), 256 threads.  The chunk's 32 columns are
-// staged transposed in shared memory (colx[k][32]); the rows that list the chunk are
-// queued, then evaluated 128 at a time with the rows staged transposed as well
-// (rowx[k][128]): thread (ty, tx) owns a 4 x 4 micro-tile (rows 4ty.., columns 4tx..)
-// and runs the pinned R1 chain with two 128-bit shared loads per 32 FP32 operations.
-constexpr int CE_WIN = 2048, CE_RB = 128, CE_QCAP = CE_WIN + CE_RB;
-__global__ void __launch_bounds__(256) k_chunk_exact(ChunkParams C) {
+// warp-aggregated append of cnt entries per lane: returns this lane's first slot
+__device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned base = 0;
+  if (lane == 31 && total) base = atomicAdd(counter, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - cnt;
+}
+
+// Pass 2 over TM32 (thread per row, 32 loads in flight): every chunk whose maximum
+// meets the row's final threshold thrK is listed.  Slots are allocated once per batch
+// per warp.  A row whose entries do not fit is poisoned (cand_cnt = ~0: invalid cache,
+// exact full-row minimum).
+__global__ void k_topk_list(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
+                            const float* __restrict__ thrK, unsigned* __restrict__ list, unsigned* __restrict__ count,
+                            unsigned cap, unsigned* __restrict__ cand_cnt) {
+  const int lane = threadIdx.x & 31;
+  constexpr int U = 32;
+  for (int p0 = p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < p_end; p0 += gridDim.x * blockDim.x) {
+    const int p = p0 + lane;
+    const bool valid = p < p_end;
+    const float thr = valid ? thrK[p] : INFINITY;
+    bool lost = false;
+    for (int c0 = 0; c0 < nch; c0 += U) {
+      unsigned mask = 0;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const float v = (valid && c0 + u < nch) ? __ldcs(TM32 + (int64_t)(c0 + u) * ld + p) : -INFINITY;
+        mask |= (v >= thr && v > -INFINITY) ? (1u << u) : 0u;
+      }
+      if (!__any_sync(0xffffffffu, mask != 0)) continue;
+      unsigned slot = warp_alloc(count, __popc(mask));
+      while (mask) {
+        const int u = __ffs(mask) - 1;
+        mask &= mask - 1;
+        if (slot < cap) list[slot] = ((unsigned)(c0 + u) << LIST_SHIFT) | (unsigned)p;
+        else lost = true;
+        slot++;
+      }
+    }
+    if (lost) cand_cnt[p] = 0xFFFFFFFFu;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact R1 re-check of a chunk-sorted list of (32-column chunk, row) pairs.  One CTA
+// per chunk at a time (dynamic): the chunk's 32 columns are staged transposed in shared
+// memory (colx[k][32]), its listed rows 128 at a time (rowx[k][128]); thread (ty, tx)
+// owns a 4 x 4 micro-tile (rows 4ty.., columns 4tx..) and runs the pinned R1 chain
+// with two 128-bit shared loads per 32 FP32 operations.  Positions p, q index the
+// (possibly permuted) order; X is read at the original indices perm[p], perm[q].
+//   MODE 0 (cache build): append every column with s^2 r <= UBK[p] to row p's list;
+//   MODE 1 (component matrix): WCM[sc[p]][sc[q]] = min exact key over the pairs.
+// ---------------------------------------------------------------------------
+
+constexpr int LE_RB = 128;
+
+__device__ __forceinline__ unsigned lower_bound_u32(const unsigned* a, unsigned n, unsigned key) {
+  unsigned lo = 0, hi = n;
+  while (lo < hi) {
+    const unsigned mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// per chunk: first entry and number of 128-row batches (the sorted list's runs)
+__global__ void k_chunk_runs(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
+                             int nch, unsigned* __restrict__ run_lo, unsigned* __restrict__ run_nb) {
+  const unsigned total = min(*count, cap);
+  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+    const unsigned lo = lower_bound_u32(list, total, (unsigned)ch << LIST_SHIFT);
+    const unsigned hi = lower_bound_u32(list, total, (unsigned)(ch + 1) << LIST_SHIFT);
+    run_lo[ch] = lo;
+    run_nb[ch] = (hi - lo + LE_RB - 1) / LE_RB;
+  }
+}
+
+// Work item = (chunk, 128-row batch): item_start is the exclusive prefix of run_nb, so
+// dense candidate chunks (component boundaries) spread over many CTAs.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_list_exact(ListParams L) {
   extern __shared__ __align__(16) float sm[];
-  float* colx = sm;                  // [d][32]
-  float* rowx = sm + C.d * 32;       // [d][CE_RB]
-  int* queue = reinterpret_cast<int*>(rowx + C.d * CE_RB);  // [CE_QCAP]
-  __shared__ int qn;
-  __shared__ int chunk_s;
+  float* colx = sm;                 // [d][32]
+  float* rowx = sm + L.d * 32;      // [d][LE_RB]
+  __shared__ int rowp[LE_RB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  while (true) {
-    if (threadIdx.x == 0) chunk_s = (int)atomicAdd(C.work, 1u);
-    __syncthreads();
-    const int ch = chunk_s;
-    if (ch >= C.nch) break;
-    const int j0 = ch * 32;
-    for (int e = threadIdx.x; e < C.d * 32; e += blockDim.x) {
-      const int k = e >> 5, t = e & 31;
-      const int j = j0 + t;
-      colx[e] = j < C.n ? C.X[(int64_t)j * C.d + k] : 0.0f;
+  const unsigned total = min(*L.count, L.cap);
+  const unsigned items = L.item_start[L.nch - 1] + L.run_nb[L.nch - 1];
+  for (unsigned item = blockIdx.x; item < items; item += gridDim.x) {
+    // chunk = last ch with item_start[ch] <= item
+    int lo_c = 0, hi_c = L.nch - 1;
+    while (lo_c < hi_c) {
+      const int mid = (lo_c + hi_c + 1) >> 1;
+      if (L.item_start[mid] <= item) lo_c = mid;
+      else hi_c = mid - 1;
     }
-    if (threadIdx.x == 0) qn = 0;
-    __syncthreads();
-    // scan the chunk's column of TM32 window by window; the queue carries over windows
-    // and only full batches of CE_RB rows are evaluated until the last window
-    for (int pb = C.p_begin; pb < C.p_end; pb += CE_WIN) {
-      const int pe = min(C.p_end, pb + CE_WIN);
-      for (int o = threadIdx.x; o < CE_WIN; o += blockDim.x) {  // warp-uniform trip count (ballot)
-        const int p = pb + o;
-        bool want = false;
-        if (p < pe) {
-          const float m = __ldcs(C.TM32 + (int64_t)ch * C.ld + p);
-          want = m >= C.thrK[p] && m > -INFINITY;
+    const int ch = lo_c;
+    const unsigned b0 = L.run_lo[ch] + (item - L.item_start[ch]) * LE_RB;
+    unsigned hi = lower_bound_u32(L.list + b0, min((unsigned)LE_RB, total - b0), (unsigned)(ch + 1) << LIST_SHIFT);
+    const int nb = (int)hi;
+    __syncthreads();  // the previous item's readers of colx / rowx / rowp are done
+    const int q0 = ch * 32;
+    for (int e = threadIdx.x; e < L.d * 32; e += blockDim.x) {
+      const int k = e >> 5, t = e & 31;
+      const int q = q0 + t;
+      colx[e] = q < L.n ? L.X[(int64_t)(L.perm ? L.perm[q] : q) * L.d + k] : 0.0f;
+    }
+    int oq[4], Dq[4];
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int q = q0 + 4 * tx + b;
+      oq[b] = q < L.n ? (L.perm ? L.perm[q] : q) : -1;
+      Dq[b] = (MODE == 1 && q < L.n) ? L.sc[q] : -1;
+    }
+    {
+      if (threadIdx.x < LE_RB) rowp[threadIdx.x] = threadIdx.x < nb ? (int)(L.list[b0 + threadIdx.x] & LIST_ROWMASK) : -1;
+      __syncthreads();
+      // stage the batch's rows transposed: lane = row of a 32-row group, float4 loads
+      for (int g = warp; g < LE_RB / 32; g += blockDim.x >> 5) {
+        const int r = g * 32 + lane;
+        const int p = rowp[r];
+        const int op = p < 0 ? 0 : (L.perm ? L.perm[p] : p);
+        if ((L.d & 3) == 0) {
+          const float4* src = reinterpret_cast<const float4*>(L.X + (int64_t)op * L.d);
+          for (int k4 = 0; k4 < L.d / 4; k4++) {
+            const float4 v = p >= 0 ? __ldg(src + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            rowx[(4 * k4 + 0) * LE_RB + r] = v.x;
+            rowx[(4 * k4 + 1) * LE_RB + r] = v.y;
+            rowx[(4 * k4 + 2) * LE_RB + r] = v.z;
+            rowx[(4 * k4 + 3) * LE_RB + r] = v.w;
+          }
+        } else {
+          for (int k = 0; k < L.d; k++) rowx[k * LE_RB + r] = p >= 0 ? __ldg(L.X + (int64_t)op * L.d + k) : 0.0f;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, want);
-        int base = 0;
-        if (lane == 0 && bal) base = atomicAdd(&qn, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (want) queue[base + __popc(bal & ((1u << lane) - 1u))] = p;
       }
       __syncthreads();
-      const int nq = qn;
-      const bool last = pe >= C.p_end;
-      const int nproc = last ? nq : nq / CE_RB * CE_RB;
-      for (int b0 = 0; b0 < nproc; b0 += CE_RB) {
-        const int nb = min(CE_RB, nproc - b0);
-        // stage the batch's rows transposed: lane = row of a 32-row group, float4 loads
-        for (int g = warp; g < CE_RB / 32; g += blockDim.x >> 5) {
-          const int r = g * 32 + lane;
-          const int p = r < nb ? queue[b0 + r] : -1;
-          if ((C.d & 3) == 0) {
-            const float4* src = reinterpret_cast<const float4*>(C.X + (int64_t)(p < 0 ? 0 : p) * C.d);
-            for (int k4 = 0; k4 < C.d / 4; k4++) {
-              const float4 v = p >= 0 ? __ldg(src + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
-              rowx[(4 * k4 + 0) * CE_RB + r] = v.x;
-              rowx[(4 * k4 + 1) * CE_RB + r] = v.y;
-              rowx[(4 * k4 + 2) * CE_RB + r] = v.z;
-              rowx[(4 * k4 + 3) * CE_RB + r] = v.w;
-            }
-          } else {
-            for (int k = 0; k < C.d; k++) rowx[k * CE_RB + r] = p >= 0 ? __ldg(C.X + (int64_t)p * C.d + k) : 0.0f;
-          }
-        }
-        __syncthreads();
-        float acc[4][4];
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
+#pragma unroll 4
+      for (int k = 0; k < L.d; k++) {
+        const float4 xa = *reinterpret_cast<const float4*>(rowx + k * LE_RB + 4 * ty);
+        const float4 xb = *reinterpret_cast<const float4*>(colx + k * 32 + 4 * tx);
+        const float av[4] = {xa.x, xa.y, xa.z, xa.w};
+        const float bv[4] = {xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
         for (int a = 0; a < 4; a++)
 #pragma unroll
-          for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
-#pragma unroll 4
-        for (int k = 0; k < C.d; k++) {
-          const float4 xa = *reinterpret_cast<const float4*>(rowx + k * CE_RB + 4 * ty);
-          const float4 xb = *reinterpret_cast<const float4*>(colx + k * 32 + 4 * tx);
-          const float av[4] = {xa.x, xa.y, xa.z, xa.w};
-          const float bv[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-          for (int a = 0; a < 4; a++)
-#pragma unroll
-            for (int b = 0; b < 4; b++) {
-              const float t = __fsub_rn(av[a], bv[b]);
-              acc[a][b] = __fmaf_rn(t, t, acc[a][b]);
-            }
-        }
-        // R1 ends with sqrtf; the MST runs on d^2 (monotone, App. A.4)
+          for (int b = 0; b < 4; b++) {
+            const float t = __fsub_rn(av[a], bv[b]);
+            acc[a][b] = __fmaf_rn(t, t, acc[a][b]);
+          }
+      }
+      // R1 ends with sqrtf; the MST runs on d^2 (monotone, App. A.4)
+      if (MODE == 0) {
 #pragma unroll
         for (int a = 0; a < 4; a++) {
-          const int r = 4 * ty + a;
-          if (r >= nb) continue;
-          const int p = queue[b0 + r];
-          const double ubk = (double)C.UBK[p];
+          const int p = rowp[4 * ty + a];
+          if (p < 0) continue;
+          const int op = L.perm ? L.perm[p] : p;
+          const double ubk = (double)L.UBK[p];
 #pragma unroll
           for (int b = 0; b < 4; b++) {
-            const int j = j0 + 4 * tx + b;
-            if (j < C.n && j != p && (double)acc[a][b] * C.s2 <= ubk) {
-              const unsigned slot = atomicAdd(C.cnt + p, 1u);
-              if ((int)slot < C.cap)
-                C.cand[(int64_t)p * C.cap + slot] =
-                    ((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(p, j);
+            if (oq[b] >= 0 && oq[b] != op && (double)acc[a][b] * L.s2 <= ubk) {
+              const unsigned slot = atomicAdd(L.cnt + p, 1u);
+              if ((int)slot < L.ccap)
+                L.cand[(int64_t)p * L.ccap + slot] =
+                    ((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(op, oq[b]);
             }
           }
         }
-        __syncthreads();
-      }
-      // keep the remainder (< CE_RB rows) at the front of the queue
-      const int rem = nq - nproc;
-      int carry = 0;
-      if (threadIdx.x < rem) carry = queue[nproc + threadIdx.x];
-      __syncthreads();
-      if (threadIdx.x < rem) queue[threadIdx.x] = carry;
-      if (threadIdx.x == 0) {
-        if (nproc) atomicAdd(C.work + 1, (unsigned)nproc);  // statistics: listed (row, chunk)
-        qn = rem;
+      } else {
+        // component pair of each entry; the common case (one row component, one column
+        // component per thread and per warp) is reduced before a single atomicMin
+        int Ca[4], opa[4];
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          const int p = rowp[4 * ty + a];
+          Ca[a] = p >= 0 ? L.sc[p] : -1;
+          opa[a] = p >= 0 ? (L.perm ? L.perm[p] : p) : -1;
+        }
+        u64 key[4][4];
+        int cC = -2, cD = -2;
+        bool uni = true;
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const bool el = Ca[a] >= 0 && Dq[b] >= 0 && Dq[b] != Ca[a];
+            key[a][b] = el ? (((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(opa[a], oq[b]))
+                           : KEY_NONE;
+            if (el) {
+              if (cC == -2) { cC = Ca[a]; cD = Dq[b]; }
+              else if (cC != Ca[a] || cD != Dq[b]) uni = false;
+            }
+          }
+        u64 m = KEY_NONE;
+        if (uni) {
+#pragma unroll
+          for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) m = key[a][b] < m ? key[a][b] : m;
+        }
+        // warp: every lane uniform on one common pair (or without entries) -> one atomic
+        const bool has_pair = uni && cC >= 0;
+        const unsigned hb = __ballot_sync(0xffffffffu, has_pair);
+        const int src = hb ? __ffs(hb) - 1 : 0;
+        const int wC = __shfl_sync(0xffffffffu, cC, src), wD = __shfl_sync(0xffffffffu, cD, src);
+        const bool ok = uni && (cC < 0 || (cC == wC && cD == wD));
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const u64 other = __shfl_xor_sync(0xffffffffu, m, o);
+            m = other < m ? other : m;
+          }
+          if (lane == 0 && hb && m != KEY_NONE) atomicMin(L.WCM + (int64_t)wC * L.k + wD, m);
+        } else if (has_pair) {
+          if (m != KEY_NONE) atomicMin(L.WCM + (int64_t)cC * L.k + cD, m);
+        } else if (!uni) {
+#pragma unroll
+          for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++)
+              if (key[a][b] != KEY_NONE) atomicMin(L.WCM + (int64_t)Ca[a] * L.k + Dq[b], key[a][b]);
+        }
       }
       __syncthreads();
     }
@@ -229,7 +337,7 @@ __global__ void k_topk_select(int p_begin, int p_end, int n, int K, const unsign
   const int warps = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int p = p_begin + blockIdx.x * warps + w; p < p_end; p += gridDim.x * warps) {
     const unsigned c = cnt[p];
-    if ((int)c > cap || c == 0) {
+    if (c > (unsigned)cap || c == 0) {
       if (lane == 0) {
         ccnt[p] = -1;
         fallback[atomicAdd(nfallback, 1u)] = p;
@@ -461,30 +569,32 @@ appd_status launch_topk_thr(appd_ctx* c, int K, const float* TM32, int64_t ld, i
   return APPD_OK;
 }
 
-appd_status launch_chunk_exact(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                               const float* thrK, const float* UBK, const float* X, int n, int d, double s2,
-                               unsigned* cnt, u64* cand, int cap, unsigned* work) {
-  ChunkParams C;
-  C.TM32 = TM32;
-  C.ld = ld;
-  C.nch = nch;
-  C.p_begin = p_begin;
-  C.p_end = p_end;
-  C.thrK = thrK;
-  C.UBK = UBK;
-  C.X = X;
-  C.n = n;
-  C.d = d;
-  C.s2 = s2;
-  C.cnt = cnt;
-  C.cand = cand;
-  C.cap = cap;
-  C.work = work;
-  const size_t smem = (size_t)d * (32 + CE_RB) * 4 + CE_QCAP * 4;
-  if (smem > 227 * 1024) return APPD_ERR_UNSUPPORTED;
-  cudaFuncSetAttribute(k_chunk_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = std::min(nch, c->sm_count * 4);
-  k_chunk_exact<<<grid, 256, smem, c->stream>>>(C);
+appd_status launch_topk_list(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+                             const float* thrK, unsigned* list, unsigned* count, unsigned cap, unsigned* cand_cnt) {
+  const int rows = p_end - p_begin;
+  if (rows <= 0) return APPD_OK;
+  const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
+  k_topk_list<<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, thrK, list, count, cap, cand_cnt);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
+                              unsigned* item_start) {
+  const size_t smem = (size_t)L.d * (32 + LE_RB) * 4;
+  if (smem > 200 * 1024) return APPD_ERR_UNSUPPORTED;
+  k_chunk_runs<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(L.list, L.count, L.cap, L.nch, run_lo, run_nb);
+  APPD_LAUNCHED(c);
+  appd_status s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, L.nch);
+  if (s) return s;
+  const int grid = c->sm_count * 4;
+  if (mode == 0) {
+    cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_list_exact<0><<<grid, 256, smem, c->stream>>>(L);
+  } else {
+    cudaFuncSetAttribute(k_list_exact<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_list_exact<1><<<grid, 256, smem, c->stream>>>(L);
+  }
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -577,8 +687,9 @@ __global__ void k_cm_rowub(CmParams P) {
   }
 }
 
-// one warp per 32 consecutive rows; 8 segments' loads in flight.  CUB here holds the
-// listing thresholds T[C][D] (the host's path-pruned upper bounds, scaled units).
+// one warp per 32 consecutive rows; 16 segments' loads in flight, one slot allocation
+// per batch.  CUB here holds the listing thresholds T[C][D] (the host's path-pruned
+// upper bounds, scaled units).  A listed segment contributes its 32-column chunks.
 __global__ void k_cm_filter(CmParams P) {
   const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int nseg = min(P.nseg, (P.n + 127) / 128);
@@ -589,97 +700,46 @@ __global__ void k_cm_filter(CmParams P) {
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
     int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
     float cachedT = 0.0f;
-    constexpr int U = 8;
+    constexpr int U = 16;
     for (int s0 = 0; s0 < nseg; s0 += U) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
         v[u] = (valid && s0 + u < nseg) ? __ldcs(P.TM + (int64_t)(s0 + u) * P.ld + p) : -INFINITY;
+      unsigned mask = 0;
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const int s = s0 + u;
-        bool want = false;
-        if (v[u] > -INFINITY) {
-          const int q0 = s * 128;
-          const int D0 = __ldg(P.sc + q0), D1 = __ldg(P.sc + min(q0 + 127, P.n - 1));
-          float thr;
-          if (D0 == D1) {
-            if (D0 != cachedD) {
-              cachedD = D0;
-              cachedT = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + D0]), ni, li, P.maxlen);
-            }
-            thr = cachedT;
-          } else {  // straddling segment: the most permissive of its components
-            float ub = 0.0f;
-            for (int D = D0; D <= D1; D++)
-              if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
-            thr = em_thr(P.em, ub, ni, li, P.maxlen);
+        if (!(v[u] > -INFINITY)) continue;
+        const int q0 = (s0 + u) * 128;
+        const int D0 = __ldg(P.sc + q0), D1 = __ldg(P.sc + min(q0 + 127, P.n - 1));
+        float thr;
+        if (D0 == D1) {
+          if (D0 != cachedD) {
+            cachedD = D0;
+            cachedT = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + D0]), ni, li, P.maxlen);
           }
-          want = v[u] >= thr;
+          thr = cachedT;
+        } else {  // straddling segment: the most permissive of its components
+          float ub = 0.0f;
+          for (int D = D0; D <= D1; D++)
+            if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
+          thr = em_thr(P.em, ub, ni, li, P.maxlen);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, want);
-        if (bal) {
-          unsigned base = 0;
-          const int leader = __ffs(bal) - 1;
-          if (lane == leader) base = atomicAdd(P.counters + 1, (unsigned)__popc(bal));
-          base = __shfl_sync(0xffffffffu, base, leader);
-          if (want) {
-            const unsigned slot = base + __popc(bal & ((1u << lane) - 1u));
-            if (slot < P.list_cap) P.list[slot] = make_uint2((unsigned)p, (unsigned)s);
-          }
-        }
+        if (v[u] >= thr) mask |= 1u << u;
+      }
+      if (!__any_sync(0xffffffffu, mask != 0)) continue;
+      unsigned cnt = 0;
+      for (unsigned m = mask; m; m &= m - 1) cnt += (unsigned)min(4, (P.n - (s0 + __ffs(m) - 1) * 128 + 31) / 32);
+      unsigned slot = warp_alloc(P.counters + 1, cnt);
+      while (mask) {
+        const int s = s0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int nc = min(4, (P.n - s * 128 + 31) / 32);
+        for (int t = 0; t < nc; t++, slot++)
+          if (slot < P.list_cap) P.list[slot] = ((unsigned)(4 * s + t) << LIST_SHIFT) | (unsigned)p;
       }
     }
   }
-}
-
-__global__ void k_cm_exact(CmParams P) {
-  unsigned cnt = P.counters[1];
-  if (cnt > P.list_cap) cnt = P.list_cap;
-  const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (unsigned a = blockIdx.x * warps + w; a < cnt; a += gridDim.x * warps) {
-    const uint2 pt = P.list[a];
-    const int p = (int)pt.x, s = (int)pt.y;
-    const int C = P.sc[p];
-    const int oi = P.perm[p];
-    const float* xi = P.XTp + p;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const int q0 = s * 128 + lane;
-    for (int kk = 0; kk < P.d; kk++) {
-      const float x = __ldg(xi + (int64_t)kk * P.ld);
-      const float* row = P.XTp + (int64_t)kk * P.ld + q0;
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const float t = __fsub_rn(x, __ldg(row + u * 32));
-        acc[u] = __fmaf_rn(t, t, acc[u]);
-      }
-    }
-    u64 key[4];
-    int Dq[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int q = q0 + u * 32;
-      Dq[u] = q < P.n ? P.sc[q] : -1;
-      key[u] = (Dq[u] >= 0 && Dq[u] != C)
-                   ? (((u64)(__float_as_uint(acc[u]) & 0x7FFFFFFFu) << 33) | tri_index(oi, P.perm[q]))
-                   : KEY_NONE;
-    }
-    // per component of the segment (labels are contiguous in a sorted segment)
-    const int D0 = P.sc[s * 128], D1 = P.sc[min(s * 128 + 127, P.n - 1)];
-    for (int D = D0; D <= D1; D++) {
-      if (D == C) continue;
-      u64 m = KEY_NONE;
-#pragma unroll
-      for (int u = 0; u < 4; u++) m = (Dq[u] == D && key[u] < m) ? key[u] : m;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const u64 other = __shfl_xor_sync(0xffffffffu, m, o);
-        m = other < m ? other : m;
-      }
-      if (lane == 0 && m != KEY_NONE) atomicMin(P.WCM + (int64_t)C * P.k + D, m);
-    }
-  }
-  if (lane == 0 && blockIdx.x == 0 && w == 0) atomicAdd(P.counters + 2, cnt);
 }
 
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P) {
@@ -690,12 +750,10 @@ appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P) {
   return APPD_OK;
 }
 
-appd_status launch_cm_exact(appd_ctx* c, const CmParams& P) {
+appd_status launch_cm_filter(appd_ctx* c, const CmParams& P) {
   const int rows = P.p_end - P.p_begin;
   if (rows <= 0) return APPD_OK;
   k_cm_filter<<<std::min(c->sm_count * 8, (rows + 255) / 256), 256, 0, c->stream>>>(P);
-  APPD_LAUNCHED(c);
-  k_cm_exact<<<c->sm_count * 16, 256, 0, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

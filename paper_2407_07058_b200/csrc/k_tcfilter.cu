@@ -448,7 +448,7 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   st->fallback = (int*)ws(c, S_TC_FALLBACK, sizeof(int) * (n + 1));
   st->rowflag = (int*)ws(c, S_TC_ROWFLAG, sizeof(int) * (n + 1));
   // cache length: option (0 = auto 16, -1 = none); the cache needs K distinct 32-column chunks
-  st->topk = c->opt.topk == 0 ? 16 : (c->opt.topk < 0 ? 0 : c->opt.topk);
+  st->topk = c->opt.topk == 0 ? 8 : (c->opt.topk < 0 ? 0 : c->opt.topk);
   if (st->topk != 0 && st->topk != 4 && st->topk != 8 && st->topk != 16 && st->topk != 32)
     return fail(c, APPD_ERR_INVALID_ARGUMENT, "topk = %d (0, -1, 4, 8, 16 or 32)", c->opt.topk);
   // TM holds 32-column maxima in the cache-building round (4x the 128-column layout)
@@ -471,6 +471,10 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->thrK = (float*)ws(c, S_TC_THRK, sizeof(float) * st->npad);
     st->cand_cnt = (unsigned*)ws(c, S_TC_CANDCNT, sizeof(unsigned) * (st->npad + 8));
     st->cand = (u64*)ws(c, S_TC_CANDK, sizeof(u64) * st->npad * st->cap);
+    st->list_entries_cap = (unsigned)std::min<int64_t>(32 * n + 65536, (int64_t)1 << 31);
+    st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
+    st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
+    if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");
     st->rows_list = (int*)ws(c, S_TC_ROWLIST, sizeof(int) * (n + 1));
     st->XT = (float*)ws(c, S_TC_XTO, sizeof(float) * st->npad * d);
     if (!st->rows_list || !st->XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate cache workspace");
@@ -574,6 +578,52 @@ static appd_status exact_stage(appd_ctx* c, const ExactParams& E) {
   return APPD_OK;
 }
 
+static int bits_for(int64_t v) {
+  int b = 1;
+  while ((int64_t)1 << b < v) b++;
+  return b;
+}
+
+// sort the listed (chunk << 32 | row) entries by chunk and re-check them exactly:
+// mode 0 appends cache candidates, mode 1 reduces component-pair minima into WCM
+static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode, const int* perm,
+                              unsigned* count_dev, int k, u64* WCM) {
+  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  const unsigned cnt = std::min(c->pinned_small[16], st->list_entries_cap);
+  st->last_list_entries = c->pinned_small[16];
+  if (cnt == 0) return APPD_OK;
+  const int nch = (int)((st->n + 31) / 32);
+  appd_status s;
+  if ((s = sort_keys_u32_bits(c, st->lista, st->listb, cnt, 0, 17 + bits_for(nch + 1)))) return s;
+  APPD_CUDA(c, cudaMemcpyAsync(st->counters + 8, &cnt, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaMemsetAsync(st->counters + 10, 0, 2 * sizeof(unsigned), c->stream));
+  ListParams L;
+  memset(&L, 0, sizeof L);
+  L.list = st->listb;
+  L.count = st->counters + 8;
+  L.cap = cnt;
+  L.nch = nch;
+  L.n = (int)st->n;
+  L.d = (int)st->d;
+  L.X = X;
+  L.perm = perm;
+  unsigned* runs = (unsigned*)ws(c, S_TC_RUNS, sizeof(unsigned) * 3 * (nch + 1));
+  if (!runs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list runs");
+  L.run_lo = runs;
+  L.run_nb = runs + nch + 1;
+  L.item_start = runs + 2 * (nch + 1);
+  L.UBK = st->UBK;
+  L.s2 = (double)st->scale * (double)st->scale;
+  L.cnt = st->cand_cnt;
+  L.cand = st->cand;
+  L.ccap = st->cap;
+  L.sc = st->sc;
+  L.k = k;
+  L.WCM = WCM;
+  return launch_list_exact(c, mode, L, runs, runs + nch + 1, runs + 2 * (nch + 1));
+}
+
 // One Boruvka round's scan: compbest[comp] = min over the component's rows of the exact
 // edge key.  With the candidate cache (st->topk > 0): round 0 builds the cache on the
 // tensor cores (32-column maxima) and takes every row's minimum from it; later rounds
@@ -649,9 +699,10 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
       if ((s = launch_topk_thr(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
                                st->maxlen_scaled, P.em, st->UBK, st->thrK)))
         return s;
-      if ((s = launch_chunk_exact(c, st->TM, st->npad, nch, p_begin, p_end, st->thrK, st->UBK, X, (int)n,
-                                  (int)st->d, s2, st->cand_cnt, st->cand, st->cap, st->counters + 4)))
+      if ((s = launch_topk_list(c, st->TM, st->npad, nch, p_begin, p_end, st->thrK, st->lista, st->counters + 6,
+                                st->list_entries_cap, st->cand_cnt)))
         return s;
+      if ((s = exact_list(c, st, X, 0, nullptr, st->counters + 6, 0, nullptr))) return s;
       if ((s = launch_topk_select(c, p_begin, p_end, (int)n, st->topk, st->cand_cnt, st->cand, st->cap, st->ckey,
                                   st->cj, st->ccnt, compbest, st->fallback, st->counters + 0)))
         return s;
@@ -751,8 +802,8 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.maxlen = st->maxlen_scaled;
   C.em = P.em;
   C.CUB = CUB;
-  C.list = (uint2*)st->list;
-  C.list_cap = st->list_cap;
+  C.list = st->lista;
+  C.list_cap = st->list_entries_cap;
   C.counters = st->counters;
   C.XTp = st->XTp;
   C.d = (int)st->d;
@@ -821,13 +872,10 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
       }
     }
     APPD_CUDA(c, cudaMemcpyAsync(CUB, T.data(), sizeof(unsigned) * k * k, cudaMemcpyHostToDevice, c->stream));
-    if ((s = launch_cm_exact(c, C))) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(st->h_counters, st->counters, 4 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                 c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));  // T must outlive the copy
+    if ((s = launch_cm_filter(c, C))) return s;
+    if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;  // synchronises
   }
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  if (st->h_counters[1] > st->list_cap) *listed_overflow = true;
+  if (st->last_list_entries > st->list_entries_cap) *listed_overflow = true;
   return APPD_OK;
 }
 

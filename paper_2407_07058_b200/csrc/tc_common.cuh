@@ -92,16 +92,42 @@ struct CmParams {
   float maxlen;
   ErrModel em;
   unsigned* CUB;        // [k][k] float bits
-  uint2* list;
+  unsigned* list;       // (32-column chunk << 17 | row) entries
   unsigned list_cap;
-  unsigned* counters;   // [1] listed pairs, [2] exact evaluated
+  unsigned* counters;   // [1] listed chunk entries
   const float* XTp;
   int d;
   const int* perm;
   u64* WCM;             // [k][k]
 };
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P);
-appd_status launch_cm_exact(appd_ctx* c, const CmParams& P);
+appd_status launch_cm_filter(appd_ctx* c, const CmParams& P);
+
+struct ListParams {
+  const unsigned* list;   // (chunk << 17 | row), sorted ascending
+  const unsigned* count;  // entries (capped by cap)
+  unsigned cap;
+  int nch, n, d;
+  const float* X;
+  const int* perm;        // nullptr: identity
+  const unsigned* run_lo;     // per chunk: first entry of its run in the sorted list
+  const unsigned* run_nb;     // per chunk: 128-row batches
+  const unsigned* item_start; // exclusive prefix of run_nb
+  // MODE 0
+  const float* UBK;
+  double s2;
+  unsigned* cnt;
+  u64* cand;
+  int ccap;
+  // MODE 1
+  const int* sc;
+  int k;
+  u64* WCM;
+};
+appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
+                              unsigned* item_start);
+appd_status launch_topk_list(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+                             const float* thrK, unsigned* list, unsigned* count, unsigned cap, unsigned* cand_cnt);
 
 size_t tcf_smem_bytes(int K, int stages);
 int tcf_stages(int K);
