@@ -281,7 +281,8 @@ def random_points(n: int, d: int, seed: int, kind: str = "uniform") -> np.ndarra
 
     kinds: uniform (u24), blobs (Gaussian blobs), dups (10% exact duplicate
     rows), grid (small integer coordinates: heavy distance ties), wide
-    (magnitudes around 1e4 with fine offsets).
+    (magnitudes around 1e4 with fine offsets), clumps (about n/64 distinct
+    points, each repeated ~64 times: masses of zero-weight edges).
     """
     rng = SplitMix64(7919 * seed + 5)
     if kind == "uniform":
@@ -300,4 +301,8 @@ def random_points(n: int, d: int, seed: int, kind: str = "uniform") -> np.ndarra
         return rng.bounded(4, n * d).reshape(n, d).astype(np.float32)
     if kind == "wide":
         return (1.0e4 + rng.u53(n * d) * 3.0).reshape(n, d).astype(np.float32)
+    if kind == "clumps":
+        nb = max(1, n // 64)
+        base = rng.u24(nb * d).reshape(nb, d)
+        return np.ascontiguousarray(base[rng.bounded(nb, n)])
     raise KeyError(kind)

@@ -139,6 +139,63 @@ def test_random_points(ctx, kind):
         assert_bit_equal(gpu_points(ctx, X), oracle.appd_points(X), f"{kind} n={n} d={d}")
 
 
+# every points-mode engine configuration: the tensor-core filter with and
+# without the round-0 candidate cache and the component-matrix finish, several cache
+# lengths and finish thresholds, and the exact FP32 engine -- all bit-exact vs the oracle
+ENGINES = [
+    dict(),                                   # defaults: cache K=8, finish at k <= 128
+    dict(topk=-1, finish_k=-1),               # every round a full tensor-core scan
+    dict(topk=16, finish_k=-1),               # cache, Boruvka to the end (tensor-core re-scans)
+    dict(topk=4, finish_k=4),                 # short cache, late finish
+    dict(topk=32, finish_k=16),
+    dict(topk=-1, finish_k=128),              # finish without the cache
+    dict(points_engine=1),                    # exact FP32 engine
+]
+ENGINE_INPUTS = [("blobs", 3000, 16), ("uniform", 2500, 40), ("clumps", 3000, 8), ("grid", 2000, 5),
+                 ("dups", 4100, 64), ("wide", 1500, 3)]
+
+
+@pytest.fixture(scope="module")
+def engine_inputs():
+    return [(kind, n, d, G.random_points(n, d, 900 + t, kind)) for t, (kind, n, d) in enumerate(ENGINE_INPUTS)]
+
+
+@pytest.fixture(scope="module")
+def engine_refs(engine_inputs):
+    return [oracle.appd_points(X) for (_, _, _, X) in engine_inputs]
+
+
+@pytest.mark.parametrize("eng", range(len(ENGINES)))
+def test_points_engines(P, eng, engine_inputs, engine_refs):
+    c = P.Context(timing=True, **ENGINES[eng])
+    try:
+        for (kind, n, d, X), ref in zip(engine_inputs, engine_refs):
+            assert_bit_equal(gpu_points(c, X), ref, f"{ENGINES[eng]} {kind} n={n} d={d}")
+    finally:
+        c.close()
+
+
+def test_points_engine_paths_taken(P):
+    """The configurations above really take the paths they name (statistics)."""
+    X = G.config("C4", n=8192)
+    ref = oracle.appd_points(X)
+    c = P.Context(timing=True)
+    assert_bit_equal(gpu_points(c, X), ref, "C4 n=8192 defaults")
+    st = c.stats()
+    assert st["points_engine"] == 2 and st["topk"] == 8 and st["cm_k"] > 0
+    c.close()
+    c = P.Context(timing=True, topk=-1, finish_k=-1)
+    assert_bit_equal(gpu_points(c, X), ref, "C4 n=8192 no cache")
+    st = c.stats()
+    assert st["topk"] == 0 and st["cm_k"] == 0 and st["tcscan_launches"] == st["rounds"]
+    c.close()
+    Xc = G.random_points(3000, 8, 77, "clumps")  # > 4K zero-distance columns per row: cache overflow
+    c = P.Context(timing=True)
+    assert_bit_equal(gpu_points(c, Xc), oracle.appd_points(Xc), "clumps")
+    assert c.stats()["cache_invalid_rows"] > 0
+    c.close()
+
+
 def _check_golden(M_rows_fn, cfg, name):
     path = os.path.join(GOLD, name)
     if not os.path.exists(path):
