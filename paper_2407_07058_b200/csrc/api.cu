@@ -234,6 +234,14 @@ extern "C" appd_status appd_get_stats(const appd_ctx* c, appd_stats* s) {
 
 extern "C" appd_status appd_last_dendrogram(const appd_ctx* c, int32_t* pi, float* h, int64_t n) {
   if (!c || !c->have_dendrogram || c->dend_n != n) return APPD_ERR_INVALID_ARGUMENT;
+  if (c->dend_on_device && n > 1) {  // GPU dendrogram: the last solve's device buffers
+    cudaSetDevice(c->device);
+    if (pi && cudaMemcpy(pi, c->dend_pi, sizeof(int32_t) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return APPD_ERR_CUDA;
+    if (h && cudaMemcpy(h, c->dend_h, sizeof(float) * (n - 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return APPD_ERR_CUDA;
+    return APPD_OK;
+  }
   if (pi) std::memcpy(pi, c->dend_pi, sizeof(int32_t) * n);
   if (h && n > 1) std::memcpy(h, c->dend_h, sizeof(float) * (n - 1));
   return APPD_OK;
@@ -337,6 +345,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
     c->one_pi = 0;
+    c->dend_on_device = false;
     c->dend_pi = &c->one_pi;
     c->dend_h = nullptr;
     c->dend_n = 1;
@@ -578,20 +587,6 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int32_t* d_ev = d_eu + m;
   float* d_ew = (float*)(d_ev + m);
   if ((s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
-  uint8_t* hp = (uint8_t*)pinned_host(c, 12 * (size_t)m + 8 * (size_t)n + 64);
-  if (!hp) return fail(c, APPD_ERR_OUT_OF_MEMORY, "pinned host buffer");
-  int32_t* h_e = (int32_t*)hp;                // eu, ev, ew (12 m bytes)
-  int32_t* h_pi = (int32_t*)(hp + 12 * m);    // pi (4 n)
-  float* h_h = (float*)(h_pi + n);            // h (4 (n - 1))
-  APPD_CUDA(c, cudaMemcpyAsync(h_e, d_eu, 12 * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  if ((int64_t)c->uf_scratch.size() < 8 * n) c->uf_scratch.resize(8 * n);
-  host_dendrogram_uvw(h_e, h_e + m, (const float*)(h_e + 2 * m), n, h_pi, h_h, c->uf_scratch.data());
-  c->dend_pi = h_pi;
-  c->dend_h = h_h;
-  c->dend_n = n;
-  c->have_dendrogram = true;
-  c->stats.dendrogram = 1;
   int levels = 1;
   while ((1ll << levels) <= m) levels++;
   const int64_t stride = m;
@@ -599,8 +594,33 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int* pos = (int*)ws(c, S_POS, sizeof(int) * n);
   float* ST = (float*)ws(c, S_ST, sizeof(float) * stride * levels);
   if (!pi || !pos || !ST) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
-  APPD_CUDA(c, cudaMemcpyAsync(pi, h_pi, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
-  APPD_CUDA(c, cudaMemcpyAsync(ST, h_h, sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
+  c->dend_n = n;
+  if (c->opt.dendrogram != 1) {
+    // v2: Prim order of the MST on the GPU (k_dendro.cu); h lands in the sparse table's level 0
+    if ((s = gpu_dendrogram(c, d_eu, d_ev, d_ew, n, pi, ST))) return s;
+    c->dend_pi = pi;
+    c->dend_h = ST;
+    c->dend_on_device = true;
+    c->stats.dendrogram = 2;
+  } else {
+    // v1: host union-find (Kruskal reconstruction tree); pinned buffers keep the copies async
+    uint8_t* hp = (uint8_t*)pinned_host(c, 12 * (size_t)m + 8 * (size_t)n + 64);
+    if (!hp) return fail(c, APPD_ERR_OUT_OF_MEMORY, "pinned host buffer");
+    int32_t* h_e = (int32_t*)hp;                // eu, ev, ew (12 m bytes)
+    int32_t* h_pi = (int32_t*)(hp + 12 * m);    // pi (4 n)
+    float* h_h = (float*)(h_pi + n);            // h (4 (n - 1))
+    APPD_CUDA(c, cudaMemcpyAsync(h_e, d_eu, 12 * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if ((int64_t)c->uf_scratch.size() < 8 * n) c->uf_scratch.resize(8 * n);
+    host_dendrogram_uvw(h_e, h_e + m, (const float*)(h_e + 2 * m), n, h_pi, h_h, c->uf_scratch.data());
+    c->dend_pi = h_pi;
+    c->dend_h = h_h;
+    c->dend_on_device = false;
+    c->stats.dendrogram = 1;
+    APPD_CUDA(c, cudaMemcpyAsync(pi, h_pi, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    APPD_CUDA(c, cudaMemcpyAsync(ST, h_h, sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
+  }
+  c->have_dendrogram = true;
   stage_event(c, 4);
 
   // ---- a6: fill prep ----

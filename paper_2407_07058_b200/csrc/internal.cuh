@@ -102,6 +102,7 @@ struct appd_ctx {
   int64_t dend_n = 0;
   int32_t one_pi = 0;
   bool have_dendrogram = false;
+  bool dend_on_device = false;      // dend_pi / dend_h are device pointers (GPU dendrogram)
   // events for stage timing
   cudaEvent_t ev[16];
   bool ev_ready = false;
@@ -123,7 +124,7 @@ enum Slot {
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
-  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
@@ -264,6 +265,8 @@ appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t cou
 void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32_t* pi, float* h);
 void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
                          int32_t* scratch /* 8 n */);
+appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, const float* ew, int64_t n,
+                           int32_t* pi, float* h);
 appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const KeySpec& ks, int32_t* eu,
                                 int32_t* ev, float* ew);
 void* pinned_host(appd_ctx* c, size_t bytes);  // grows ctx->pinned

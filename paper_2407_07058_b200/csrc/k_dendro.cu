@@ -1,0 +1,292 @@
+// k_dendro.cu -- dendrogram on the GPU: the leaf order pi and
+// merge heights h from the MST, without a sequential union-find.
+//
+// P:L149 reads the APPD off the single-linkage dendrogram; any leaf order of it works
+// (DESIGN.md "leaf order").  Prim's visit order from a root is one (SURVEY App. A.3:
+// Prim never leaves a component of the threshold graph before finishing it), with
+// h[a] = the key of pi_{a+1} when Prim adds it = the weight of its tree edge.  On the
+// MST itself, Prim's order is a pre-order of the "record tree": rooting the MST at
+// vertex 0, let val(v) be the rank (position in the ascending key order) of v's parent
+// edge; the record parent of v is its nearest ancestor a with val(a) > val(v) (the
+// root has val = +inf).  Visiting the record tree in pre-order with children in
+// ascending val reproduces Prim's priority order: Prim finishes everything reachable
+// below a weight before crossing a heavier edge, and the heavier edges on the path to v
+// are exactly v's record ancestors.  (Checked against a heap-based Prim on 300 random
+// trees while building this, and end to end against the oracle by the parity tests.)
+//
+// Steps, all data-parallel:
+//   A  arcs (2 per edge) sorted by source = adjacency lists
+//   B  Euler-tour successor of every arc, cut at the root
+//   C  list ranking (pointer jumping) -> tour positions; the earlier arc of an edge
+//      points downwards: parent and val of every vertex
+//   D  nearest heavier ancestor by binary lifting (2^j-th ancestor + max val on the way)
+//   E  children sorted by (record parent, val); Euler tour of the record tree, list
+//      ranking, pre-order index = 1 + down arcs before the vertex's down arc
+//   F  pi[pre(v)] = v, h[a] = weight of the parent edge of pi[a+1]
+#include "internal.cuh"
+
+namespace appd {
+
+namespace {
+
+__global__ void k_arcs(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
+                       int* __restrict__ src, int* __restrict__ arc) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < 2 * m; a += gridDim.x * blockDim.x) {
+    const int e = a >> 1;
+    src[a] = (a & 1) ? ev[e] : eu[e];
+    arc[a] = a;
+  }
+}
+
+// adjacency ranges of the sorted sources + inverse position of every arc
+__global__ void k_adj(const int* __restrict__ ssrc, const int* __restrict__ sarc, int L, int* __restrict__ start,
+                      int* __restrict__ end, int* __restrict__ posarc) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const int x = ssrc[i];
+    if (i == 0 || ssrc[i - 1] != x) start[x] = i;
+    if (i == L - 1 || ssrc[i + 1] != x) end[x] = i + 1;
+    posarc[sarc[i]] = i;
+  }
+}
+
+// succ(x -> y) = the arc after (y -> x) in y's adjacency, cyclically; the tour starts
+// with the root's first arc and the arc leading back into it ends the list (-1)
+__global__ void k_euler_succ(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
+                             const int* __restrict__ sarc, const int* __restrict__ start,
+                             const int* __restrict__ end, const int* __restrict__ posarc, int root,
+                             int* __restrict__ succ, int* __restrict__ rank) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < 2 * m; a += gridDim.x * blockDim.x) {
+    const int e = a >> 1;
+    const int y = (a & 1) ? eu[e] : ev[e];  // head of a
+    int i = posarc[a ^ 1] + 1;
+    if (i == end[y]) i = start[y];
+    const int s = (y == root && i == start[y]) ? -1 : sarc[i];
+    succ[a] = s;
+    rank[a] = s < 0 ? 0 : 1;
+  }
+}
+
+// one pointer-jumping step (double buffered): rank = arcs after this one
+__global__ void k_rank_step(const int* __restrict__ nin, const int* __restrict__ rin, int L, int* __restrict__ nout,
+                            int* __restrict__ rout, int* __restrict__ active) {
+  int any = 0;
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+    const int nx = nin[a];
+    if (nx >= 0) {
+      rout[a] = rin[a] + rin[nx];
+      const int nn = nin[nx];
+      nout[a] = nn;
+      any |= nn >= 0;
+    } else {
+      rout[a] = rin[a];
+      nout[a] = -1;
+    }
+  }
+  if (any) *active = 1;
+}
+
+// the earlier arc of each edge points from parent to child
+__global__ void k_orient(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
+                         const int* __restrict__ rank, int* __restrict__ parent, int* __restrict__ val,
+                         int* __restrict__ child_of) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    // larger rank (more arcs after it) = earlier in the tour
+    const bool down0 = rank[2 * e] > rank[2 * e + 1];
+    const int c = down0 ? ev[e] : eu[e], p = down0 ? eu[e] : ev[e];
+    parent[c] = p;
+    val[c] = e;
+    child_of[e] = c;
+  }
+}
+
+__global__ void k_lift0(const int* __restrict__ parent, const int* __restrict__ val, int n, int* __restrict__ jump,
+                        int* __restrict__ mx) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const int p = parent[x];
+    jump[x] = p;
+    mx[x] = val[p];
+  }
+}
+__global__ void k_lift(const int* __restrict__ jin, const int* __restrict__ min_, int n, int* __restrict__ jout,
+                       int* __restrict__ mout) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    const int j = jin[x];
+    jout[x] = jin[j];
+    mout[x] = max(min_[x], min_[j]);
+  }
+}
+
+// record parent of v: its nearest ancestor with a larger val; sort key (rpar, val)
+__global__ void k_record_parent(const int* __restrict__ jump, const int* __restrict__ mx, int levels, int n,
+                                const int* __restrict__ parent, const int* __restrict__ val, int root,
+                                unsigned long long* __restrict__ key) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (v == root) continue;
+    const int w = val[v];
+    int cur = v;
+    for (int j = levels - 1; j >= 0; j--) {
+      const int64_t o = (int64_t)j * n + cur;
+      if (mx[o] < w) cur = jump[o];
+    }
+    const int rp = parent[cur];
+    key[w] = ((unsigned long long)(unsigned)rp << 32) | (unsigned)w;  // one entry per edge rank
+  }
+}
+
+// record-tree Euler tour over the sorted children S[i] = (rpar, val): arcs 2i (down
+// into child i) and 2i+1 (back up); first child of x and the S index of each vertex
+__global__ void k_rt_index(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+                           int* __restrict__ first, int* __restrict__ sidx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int rp = (int)(S[i] >> 32);
+    const int v = child_of[(int)(S[i] & 0xffffffffu)];
+    sidx[v] = i;
+    if (i == 0 || (int)(S[i - 1] >> 32) != rp) first[rp] = i;
+  }
+}
+__global__ void k_rt_succ(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+                          const int* __restrict__ first, const int* __restrict__ sidx, int root,
+                          int* __restrict__ succ, int* __restrict__ rank) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int rp = (int)(S[i] >> 32);
+    const int v = child_of[(int)(S[i] & 0xffffffffu)];
+    const int fc = first[v];
+    const int sd = fc >= 0 ? 2 * fc : 2 * i + 1;  // into the first child, else straight back up
+    int su;
+    if (i + 1 < m && (int)(S[i + 1] >> 32) == rp) su = 2 * (i + 1);  // next sibling
+    else su = rp == root ? -1 : 2 * sidx[rp] + 1;                    // up from the parent
+    succ[2 * i] = sd;
+    succ[2 * i + 1] = su;
+    rank[2 * i] = 1;
+    rank[2 * i + 1] = su < 0 ? 0 : 1;
+  }
+}
+
+// flag[position of down arc] = 1 (positions = L - 1 - rank)
+__global__ void k_down_flags(const int* __restrict__ rank, int m, int* __restrict__ flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    flag[2 * m - 1 - rank[2 * i]] = 1;
+}
+__global__ void k_emit(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+                       const int* __restrict__ rank, const int* __restrict__ downs_before,
+                       const float* __restrict__ ew, int root, int32_t* __restrict__ pi, float* __restrict__ h) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int e = (int)(S[i] & 0xffffffffu);
+    const int v = child_of[e];
+    const int pre = 1 + downs_before[2 * m - 1 - rank[2 * i]];
+    pi[pre] = v;
+    h[pre - 1] = ew[e];  // Prim's key of v: the weight of its tree edge
+    if (i == 0) pi[0] = root;
+  }
+}
+
+// pointer jumping until every list is resolved; (succ, rank) in buffers 0, results in
+// whichever buffer the last step wrote (returned through *out_rank)
+appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, int* rank1, int* active,
+                      int** out_rank) {
+  int* ni = succ0;
+  int* ri = rank0;
+  int* no = succ1;
+  int* ro = rank1;
+  const int grid = std::min(c->sm_count * 8, (L + 255) / 256);
+  int steps = 0;
+  while ((1 << steps) < L) steps++;
+  for (int s = 0; s < steps + 1; s++) {
+    k_rank_step<<<grid, 256, 0, c->stream>>>(ni, ri, L, no, ro, active);
+    APPD_LAUNCHED(c);
+    std::swap(ni, no);
+    std::swap(ri, ro);
+  }
+  *out_rank = ri;
+  return APPD_OK;
+}
+
+}  // namespace
+
+// eu/ev/ew: MST edges in ascending key order (device); pi, h: device outputs
+appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, const float* ew, int64_t n64,
+                           int32_t* pi, float* h) {
+  const int n = (int)n64, m = n - 1;
+  if (n == 1) {
+    APPD_CUDA(c, cudaMemsetAsync(pi, 0, sizeof(int32_t), c->stream));
+    return APPD_OK;
+  }
+  const int L = 2 * m;
+  int levels = 1;
+  while ((1 << levels) < n) levels++;
+  levels++;
+  // workspace (ints): 11 arc arrays of L (+2), 6 vertex arrays of n, child_of (m), lifting 2 levels n
+  const size_t ints = (size_t)12 * L + 8 * (size_t)n + 2 * (size_t)levels * n + 64;
+  int* w = (int*)ws(c, S_DENDRO, sizeof(int) * ints + sizeof(unsigned long long) * 2 * (size_t)m + 64);
+  if (!w) return fail(c, APPD_ERR_OUT_OF_MEMORY, "GPU dendrogram workspace");
+  int* src = w;
+  int* arc = src + L;
+  int* ssrc = arc + L;
+  int* sarc = ssrc + L;
+  int* succ0 = sarc + L;
+  int* rank0 = succ0 + L;
+  int* start = rank0 + L;
+  int* end = start + n;
+  int* posarc = end + n;  // L entries
+  int* parent = posarc + L;
+  int* val = parent + n;
+  int* child_of = val + n;
+  int* first = child_of + m;
+  int* sidx = first + n;
+  int* jump = sidx + n;
+  int* mx = jump + (size_t)levels * n;
+  int* succ1 = mx + (size_t)levels * n;
+  int* rank1 = succ1 + L;
+  int* flag = rank1 + L;           // L + 1
+  int* downs = flag + L + 1;       // L + 1
+  int* active = downs + L + 1;
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(((uintptr_t)(active + 8) + 15) & ~(uintptr_t)15);
+  unsigned long long* S = key + m;
+  const int gL = std::min(c->sm_count * 8, (L + 255) / 256), gn = std::min(c->sm_count * 8, (n + 255) / 256);
+  const int root = 0;
+  appd_status s;
+  // A: adjacency
+  k_arcs<<<gL, 256, 0, c->stream>>>(eu, ev, m, src, arc);
+  APPD_LAUNCHED(c);
+  if ((s = sort_pairs_i32(c, src, ssrc, arc, sarc, L))) return s;
+  k_adj<<<gL, 256, 0, c->stream>>>(ssrc, sarc, L, start, end, posarc);
+  APPD_LAUNCHED(c);
+  // B, C: Euler tour of the MST from the root, tour ranks
+  k_euler_succ<<<gL, 256, 0, c->stream>>>(eu, ev, m, sarc, start, end, posarc, root, succ0, rank0);
+  APPD_LAUNCHED(c);
+  int* rk = nullptr;
+  if ((s = list_rank(c, L, succ0, rank0, succ1, rank1, active, &rk))) return s;
+  // orientation: parent, val (edge rank of the parent edge), child of each edge
+  APPD_CUDA(c, cudaMemsetAsync(val + root, 0x7F, sizeof(int), c->stream));  // +inf
+  k_orient<<<gn, 256, 0, c->stream>>>(eu, ev, m, rk, parent, val, child_of);
+  APPD_LAUNCHED(c);
+  APPD_CUDA(c, cudaMemsetAsync(parent + root, 0, sizeof(int), c->stream));  // root = vertex 0 is its own parent
+  // D: binary lifting, nearest heavier ancestor
+  k_lift0<<<gn, 256, 0, c->stream>>>(parent, val, n, jump, mx);
+  APPD_LAUNCHED(c);
+  for (int j = 1; j < levels; j++) {
+    k_lift<<<gn, 256, 0, c->stream>>>(jump + (size_t)(j - 1) * n, mx + (size_t)(j - 1) * n, n, jump + (size_t)j * n,
+                                      mx + (size_t)j * n);
+    APPD_LAUNCHED(c);
+  }
+  k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, key);
+  APPD_LAUNCHED(c);
+  // E: record tree, children ascending by val
+  if ((s = sort_keys_u64(c, key, S, m))) return s;
+  APPD_CUDA(c, cudaMemsetAsync(first, 0xFF, sizeof(int) * n, c->stream));
+  k_rt_index<<<gn, 256, 0, c->stream>>>(S, m, child_of, first, sidx);
+  APPD_LAUNCHED(c);
+  k_rt_succ<<<gn, 256, 0, c->stream>>>(S, m, child_of, first, sidx, root, succ0, rank0);
+  APPD_LAUNCHED(c);
+  if ((s = list_rank(c, L, succ0, rank0, succ1, rank1, active, &rk))) return s;
+  APPD_CUDA(c, cudaMemsetAsync(flag, 0, sizeof(int) * (L + 1), c->stream));
+  k_down_flags<<<gn, 256, 0, c->stream>>>(rk, m, flag);
+  APPD_LAUNCHED(c);
+  if ((s = exclusive_scan_i32(c, flag, downs, L))) return s;
+  // F: outputs
+  k_emit<<<gn, 256, 0, c->stream>>>(S, m, child_of, rk, downs, ew, root, pi, h);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd

@@ -150,6 +150,7 @@ ENGINES = [
     dict(topk=32, finish_k=16),
     dict(topk=-1, finish_k=128),              # finish without the cache
     dict(points_engine=1),                    # exact FP32 engine
+    dict(dendrogram=1),                       # host union-find dendrogram instead of the GPU Prim order
 ]
 ENGINE_INPUTS = [("blobs", 3000, 16), ("uniform", 2500, 40), ("clumps", 3000, 8), ("grid", 2000, 5),
                  ("dups", 4100, 64), ("wide", 1500, 3)]
