@@ -38,50 +38,63 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons polled through NVML every ~2 ms while the timed region
+    runs (nvidia-smi's 100 ms loop is longer than the whole timed region)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.samples = []
+        self.reasons = set()
+        self.running = False
+        self.nv = None
+        self.t = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+            import pynvml as nv
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            return
+        self.running = True
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while self.running:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS.items():
+                    if r & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def clear(self):
+        self.samples = []
+        self.reasons = set()
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.running = False
+        if self.t:
             self.t.join(timeout=2)
-        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) > 8:
-                for nm, v in zip(names, r[5:9]):
-                    if v.strip().lower() == "active":
-                        reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = list(self.samples)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": sorted(self.reasons), "samples": len(sm),
+                "source": "NVML (nvmlDeviceGetClockInfo SM, clocks event reasons) every ~2 ms during the timed steps"}
 
 
 def load_input(workload: str):
@@ -186,15 +199,11 @@ def run_native(args):
         else:
             ctx.solve_weights(Xd, M)
 
-    sampler = ClockSampler(local)
-    sampler.start()  # nvidia-smi needs ~0.5 s to start; it keeps sampling through the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    t_wait = time.perf_counter()
-    while not sampler.rows and time.perf_counter() - t_wait < 5.0:
-        time.sleep(0.05)
-    sampler.rows.clear()  # keep only samples taken from here on
+    sampler = ClockSampler(local)
+    sampler.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stats = []
     if dist:
@@ -236,20 +245,34 @@ def run_native(args):
                  "frac": fill_gbs / pk["hbm_gbs"], "avg_launch_ms": fill_ms, "algorithmic_bytes_per_launch": fill_bytes}
     tc_ms = statistics.mean(s["ms_tcscan"] for s in stats)
     tc_launches = stats[-1]["tcscan_launches"]
-    if points and tc_launches and tc_ms > fill_ms:
-        # tensor-core scan (one launch per Boruvka round): the algorithmic work is the Gram term
-        # -2 X^T X, 2*d flops per (row, column) pair; fp16 inputs run at the bf16 dense rate
+    tc_info = None
+    if points and tc_launches:
+        # tensor-core scans (round 0 cache build + component-matrix pass): the algorithmic
+        # work is the Gram term -2 X^T X, 2*d flops per (row, column) pair per launch;
+        # fp16 inputs run at the bf16 dense rate
         flops = statistics.mean(s["tcscan_flops"] for s in stats) / tc_launches
         avg = tc_ms / tc_launches
         ach = flops / (avg / 1000) / 1e12
-        peak_tc = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops_sustained", 1377.8) \
-            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1400.0
-        roofline = {"bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
-                    "traffic": None, "kernel": "k_tcf_scan", "algorithmic_flops_per_launch": flops,
-                    "avg_launch_ms": avg, "launches_per_step": tc_launches,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 runs at the bf16 rate)",
-                    "fill": fill_roof}
-    elif mst_ms > fill_ms and points:
+        mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        peak_tc = json.load(open(mp)).get("bf16_tflops_sustained", 1377.8) if os.path.exists(mp) else 1400.0
+        tc_info = {"bound": "tensor", "achieved": ach, "peak": peak_tc, "unit": "TFLOP/s", "frac": ach / peak_tc,
+                   "kernel": "k_tcf_scan", "algorithmic_flops_per_launch": flops, "avg_launch_ms": avg,
+                   "launches_per_step": tc_launches, "ms_per_step": tc_ms,
+                   "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (fp16 runs at the bf16 rate)"}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get(args.workload, {}).get("k_fill")
+        if tj and tj.get("rows") == rows and tj.get("n") == n:
+            traffic = tj["dram_bytes_per_launch"]
+    if tc_info and tc_ms > fill_ms:
+        roofline = dict(tc_info, traffic=None, fill=fill_roof)
+    else:
+        roofline["traffic"] = traffic
+        roofline["traffic_source"] = "profiles/traffic.json (ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum)"
+        if tc_info:
+            roofline["tensor_scan"] = tc_info
+    if points and not tc_launches and mst_ms > fill_ms:
         # exact FP32 MST scan: 2*d lane-ops per (row, column) pair per Boruvka pass, ALU bound
         d = c["d"]
         sm_count = torch.cuda.get_device_properties(local).multi_processor_count
@@ -261,8 +284,7 @@ def run_native(args):
                     "traffic": None, "kernel": "k_scan_points (all Boruvka rounds)",
                     "algorithmic_ops_per_solve": ops, "avg_ms_per_solve": mst_ms,
                     "peak_source": f"{sm_count} SM x 128 FP32 lanes x {clk} MHz (median SM clock under load)",
-                    "fill": {"achieved_gbs": fill_gbs, "peak_gbs": pk["hbm_gbs"], "frac": fill_gbs / pk["hbm_gbs"],
-                             "avg_launch_ms": fill_ms}}
+                    "fill": fill_roof}
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
     e2e = None

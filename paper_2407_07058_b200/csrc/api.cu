@@ -316,15 +316,23 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   stage_event(c, 0);
 
   // ---- a1: validation ----
+  // Points mode with the tensor-core engine: the verdict is copied asynchronously and
+  // read after the engine's preparation, which synchronises anyway (deferred check).
+  const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 && n >= 2;
+  u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
   if (c->opt.validate) {
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
     if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
     APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
     appd_status s = points ? launch_validate_points(c, X, n, d, bad) : launch_validate_weights(c, W, n, row0, rows, bad);
     if (s) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (c->opt.validate && !defer_validation) {
+    appd_status s;
     u64 hb[3];
-    APPD_CUDA(c, cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    memcpy(hb, hbad, sizeof hb);
     if (c->opt.world > 1) {
       // every rank must agree on the verdict (else the others would hang in the next collective)
       u64* agree = (u64*)ws(c, S_TMP, sizeof(u64) * 3);
@@ -379,6 +387,13 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   bool use_tc = false;
   if (points && c->opt.points_engine != 1 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);
+    if (defer_validation) {  // tcf_prepare synchronised the stream: the verdict is in pinned memory
+      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      u64 hb[3];
+      memcpy(hb, hbad, sizeof hb);
+      appd_status sv = report_validation(c, hb, n, points, d);
+      if (sv) return sv;
+    }
     if (s == APPD_OK) use_tc = true;
     else if (s != APPD_ERR_UNSUPPORTED || c->opt.points_engine == 2) return s;
     c->last_error.clear();
@@ -531,7 +546,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
     if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
     if (use_tc) {
-      if (c->opt.timing && (rounds == 0 || !tc.topk || tc.last_rescan_rows > 0)) {
+      if (c->opt.timing && tc.scanned) {
         float ms = 0.0f;
         if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
         cudaGetLastError();
@@ -547,9 +562,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         c->stats.tcscan_launches++;
         c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
       } else if (tc.last_rescan_rows > 0) {
-        const int64_t blocks = c->pinned_small[8];
         c->stats.rescan_rounds++;
         c->stats.rescan_rows += tc.last_rescan_rows;
+      }
+      if (rounds > 0 && tc.topk && tc.scanned) {
+        const int64_t blocks = c->pinned_small[8];
         c->stats.rescan_blocks += blocks;
         c->stats.tcscan_launches++;
         c->stats.tcscan_flops += 2.0 * (double)std::min<int64_t>(blocks * 512, n) * n * d;

@@ -173,6 +173,7 @@ struct TcState {
   u64* cand = nullptr;                 // [npad][cap]
   // per-round statistics (host)
   int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0, last_list_entries = 0;
+  bool scanned = false;  // this round launched the tensor-core scan (ev[10] -> ev[11] bracket it)
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,

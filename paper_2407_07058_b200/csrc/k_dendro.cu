@@ -23,7 +23,11 @@
 //   E  children sorted by (record parent, val); Euler tour of the record tree, list
 //      ranking, pre-order index = 1 + down arcs before the vertex's down arc
 //   F  pi[pre(v)] = v, h[a] = weight of the parent edge of pi[a+1]
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace appd {
 
@@ -66,25 +70,6 @@ __global__ void k_euler_succ(const int32_t* __restrict__ eu, const int32_t* __re
   }
 }
 
-// one pointer-jumping step (double buffered): rank = arcs after this one
-__global__ void k_rank_step(const int* __restrict__ nin, const int* __restrict__ rin, int L, int* __restrict__ nout,
-                            int* __restrict__ rout, int* __restrict__ active) {
-  int any = 0;
-  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
-    const int nx = nin[a];
-    if (nx >= 0) {
-      rout[a] = rin[a] + rin[nx];
-      const int nn = nin[nx];
-      nout[a] = nn;
-      any |= nn >= 0;
-    } else {
-      rout[a] = rin[a];
-      nout[a] = -1;
-    }
-  }
-  if (any) *active = 1;
-}
-
 // the earlier arc of each edge points from parent to child
 __global__ void k_orient(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
                          const int* __restrict__ rank, int* __restrict__ parent, int* __restrict__ val,
@@ -107,15 +92,6 @@ __global__ void k_lift0(const int* __restrict__ parent, const int* __restrict__ 
     mx[x] = val[p];
   }
 }
-__global__ void k_lift(const int* __restrict__ jin, const int* __restrict__ min_, int n, int* __restrict__ jout,
-                       int* __restrict__ mout) {
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    const int j = jin[x];
-    jout[x] = jin[j];
-    mout[x] = max(min_[x], min_[j]);
-  }
-}
-
 // record parent of v: its nearest ancestor with a larger val; sort key (rpar, val)
 __global__ void k_record_parent(const int* __restrict__ jump, const int* __restrict__ mx, int levels, int n,
                                 const int* __restrict__ parent, const int* __restrict__ val, int root,
@@ -180,24 +156,66 @@ __global__ void k_emit(const unsigned long long* __restrict__ S, int m, const in
   }
 }
 
-// pointer jumping until every list is resolved; (succ, rank) in buffers 0, results in
-// whichever buffer the last step wrote (returned through *out_rank)
-appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, int* rank1, int* active,
+// all pointer-jumping steps in one cooperative launch (grid-wide barrier per step);
+// (succ, rank) start in buffers 0, the result lands in buffer (steps & 1)
+__global__ void k_rank_coop(int* __restrict__ n0, int* __restrict__ r0, int* __restrict__ n1, int* __restrict__ r1,
+                            int L, int steps) {
+  cg::grid_group grid = cg::this_grid();
+  for (int s = 0; s < steps; s++) {
+    const int* ni = (s & 1) ? n1 : n0;
+    const int* ri = (s & 1) ? r1 : r0;
+    int* no = (s & 1) ? n0 : n1;
+    int* ro = (s & 1) ? r0 : r1;
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
+      const int nx = ni[a];
+      if (nx >= 0) {
+        ro[a] = ri[a] + ri[nx];
+        no[a] = ni[nx];
+      } else {
+        ro[a] = ri[a];
+        no[a] = -1;
+      }
+    }
+    grid.sync();
+  }
+}
+
+// all binary-lifting levels in one cooperative launch
+__global__ void k_lift_coop(int* __restrict__ jump, int* __restrict__ mx, int n, int levels) {
+  cg::grid_group grid = cg::this_grid();
+  for (int j = 1; j < levels; j++) {
+    const int* jin = jump + (size_t)(j - 1) * n;
+    const int* min_ = mx + (size_t)(j - 1) * n;
+    int* jout = jump + (size_t)j * n;
+    int* mout = mx + (size_t)j * n;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+      const int q = jin[x];
+      jout[x] = jin[q];
+      mout[x] = max(min_[x], min_[q]);
+    }
+    grid.sync();
+  }
+}
+
+int coop_grid(appd_ctx* c, const void* fn) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return per_sm * c->sm_count;
+}
+
+appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, int* rank1, int* /*active*/,
                       int** out_rank) {
-  int* ni = succ0;
-  int* ri = rank0;
-  int* no = succ1;
-  int* ro = rank1;
-  const int grid = std::min(c->sm_count * 8, (L + 255) / 256);
   int steps = 0;
   while ((1 << steps) < L) steps++;
-  for (int s = 0; s < steps + 1; s++) {
-    k_rank_step<<<grid, 256, 0, c->stream>>>(ni, ri, L, no, ro, active);
-    APPD_LAUNCHED(c);
-    std::swap(ni, no);
-    std::swap(ri, ro);
-  }
-  *out_rank = ri;
+  steps++;
+  const int grid = std::min(coop_grid(c, (const void*)k_rank_coop), (L + 255) / 256);
+  void* args[] = {&succ0, &rank0, &succ1, &rank1, &L, &steps};
+  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_rank_coop, grid, 256, args, 0, c->stream));
+  c->launches++;
+  *out_rank = (steps & 1) ? rank1 : rank0;
   return APPD_OK;
 }
 
@@ -264,10 +282,12 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   // D: binary lifting, nearest heavier ancestor
   k_lift0<<<gn, 256, 0, c->stream>>>(parent, val, n, jump, mx);
   APPD_LAUNCHED(c);
-  for (int j = 1; j < levels; j++) {
-    k_lift<<<gn, 256, 0, c->stream>>>(jump + (size_t)(j - 1) * n, mx + (size_t)(j - 1) * n, n, jump + (size_t)j * n,
-                                      mx + (size_t)j * n);
-    APPD_LAUNCHED(c);
+  {
+    int nn = n, lv = levels;
+    const int grid = std::min(coop_grid(c, (const void*)k_lift_coop), (n + 255) / 256);
+    void* args[] = {&jump, &mx, &nn, &lv};
+    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_lift_coop, grid, 256, args, 0, c->stream));
+    c->launches++;
   }
   k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, key);
   APPD_LAUNCHED(c);

@@ -639,6 +639,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   const double s2 = (double)st->scale * (double)st->scale;
   appd_status s;
   *overflowed = false;
+  st->scanned = false;
   st->last_rescan_rows = 0;
   st->last_rescan_blocks = 0;
   st->h_counters[0] = st->h_counters[1] = st->h_counters[2] = 0;
@@ -693,6 +694,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 1, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    st->scanned = true;
     if (p_end > p_begin) {
       const int nch = (int)(st->npad / 32);
       APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
@@ -727,6 +729,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 0, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    st->scanned = true;
     if ((s = launch_comp_ub(c, (int)n, (int)k, compbest, s2, st->perm, st->needp, st->UB, comp, st->compUB)))
       return s;
     exact_params(st, P, comp, compbest, 0, (int)n, 0, &E);
@@ -743,6 +746,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 0, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
+    st->scanned = true;
     exact_params(st, P, comp, compbest, p_begin, p_end, round == 0, &E);
     if ((s = exact_stage(c, E))) return s;
   }
