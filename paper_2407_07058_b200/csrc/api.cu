@@ -475,7 +475,13 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
         c->stats.cm_k = (int)k;
         c->stats.tcscan_launches++;
-        c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+        if (c->opt.world == 1) {  // upper-triangle pass: row block rb against columns >= 512 rb
+          double pairs = 0.0;
+          for (int64_t rb = 0; rb * 512 < n; rb++) pairs += (double)std::min<int64_t>(512, n - rb * 512) * (n - rb * 512);
+          c->stats.tcscan_flops += 2.0 * pairs * d;
+        } else {
+          c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
+        }
         if (c->opt.timing) {
           float ms = 0.0f;
           if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;

@@ -670,8 +670,9 @@ __global__ void k_cm_rowub(CmParams P) {
     const int C = valid ? P.sc[p] : -1;
     const bool uni = __all_sync(0xffffffffu, C == __shfl_sync(0xffffffffu, C, 0));
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
+    const int smin = P.upper ? 4 * (p0 / 512) : 0;  // segments the (symmetric) scan wrote for these rows
     for (int D = 0; D < P.k; D++) {
-      const int s0 = (P.cstart[D] + 127) / 128, s1 = P.cend[D] / 128;  // segments inside D
+      const int s0 = max(smin, (P.cstart[D] + 127) / 128), s1 = P.cend[D] / 128;  // segments inside D
       float m = -INFINITY;
       if (valid && D != C)
         for (int s = s0; s < s1; s++) m = fmaxf(m, __ldcs(P.TM + (int64_t)s * P.ld + p));
@@ -701,7 +702,7 @@ __global__ void k_cm_filter(CmParams P) {
     int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
     float cachedT = 0.0f;
     constexpr int U = 16;
-    for (int s0 = 0; s0 < nseg; s0 += U) {
+    for (int s0 = P.upper ? 4 * (p0 / 512) : 0; s0 < nseg; s0 += U) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)

@@ -524,6 +524,7 @@ static void fill_scan_params(const TcState* st, TcParams* P) {
   P->seg32 = 0;
   P->rb_list = nullptr;
   P->rb_count = nullptr;
+  P->upper = 0;
 }
 
 static void exact_params(const TcState* st, const TcParams& P, const int* comp, u64* compbest, int p_begin,
@@ -784,7 +785,10 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   P.round0 = 0;
   P.rb_begin = (int)rb_begin;
   P.rb_end = (int)rb_end;
-  P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
+  // one rank: every unordered pair is needed from one side only -> upper-triangle pass
+  P.upper = c->opt.world == 1 && !getenv("APPD_CM_FULL");
+  P.col_splits = P.upper ? col_splits_for(c, (rb_end - rb_begin + 1) / 2, P.col_tiles)
+                         : col_splits_for(c, rb_end - rb_begin, P.col_tiles);
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 0, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
@@ -813,6 +817,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.d = (int)st->d;
   C.perm = st->perm;
   C.WCM = WCM;
+  C.upper = P.upper;
   if ((s = launch_cm_rowub(c, C))) return s;
   // Listing thresholds.  CUB[C][D] bounds the exact minimum w(C, D) from above (both
   // directions bound the same w).  A contracted MST edge (C, D) also satisfies

@@ -132,11 +132,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
   const uint32_t tmem = *tmem_slot;
 
   const int nrb = P.rb_list ? *P.rb_count : (P.rb_end - P.rb_begin);
-  const int items = nrb * P.col_splits;
+  // upper mode (symmetric pass): row block rb scans only column tiles >= 2 rb; blocks rb
+  // and (last - rb) form one pair of constant total length, cut into col_splits items
+  const int items = (P.upper ? (nrb + 1) / 2 : nrb) * P.col_splits;
   const int per_split = (P.col_tiles + P.col_splits - 1) / P.col_splits;
-  auto rb_of = [&](int it) -> int {
-    const int b = it / P.col_splits;
-    return P.rb_list ? __ldg(P.rb_list + b) : P.rb_begin + b;
+  // k-th (k = 0, 1) contiguous piece of work item it: row block and column-tile range
+  auto subitem = [&](int it, int k, int& rb, int& ct0, int& ct1) -> bool {
+    const int sp = it % P.col_splits;
+    if (!P.upper) {
+      if (k) return false;
+      const int b = it / P.col_splits;
+      rb = P.rb_list ? __ldg(P.rb_list + b) : P.rb_begin + b;
+      ct0 = sp * per_split;
+      ct1 = min(P.col_tiles, ct0 + per_split);
+      return ct0 < ct1;
+    }
+    const int q = it / P.col_splits;
+    const int rba = P.rb_begin + q, rbb = P.rb_end - 1 - q;
+    const int la = P.col_tiles - 2 * rba, lb = rbb != rba ? P.col_tiles - 2 * rbb : 0;
+    const int tot = la + lb;
+    const int x0 = (int)((int64_t)sp * tot / P.col_splits), x1 = (int)((int64_t)(sp + 1) * tot / P.col_splits);
+    if (k == 0) {
+      rb = rba;
+      ct0 = 2 * rba + x0;
+      ct1 = 2 * rba + min(x1, la);
+      return x0 < la && ct0 < ct1;
+    }
+    if (lb == 0 || x1 <= la) return false;
+    rb = rbb;
+    ct0 = 2 * rbb + max(x0, la) - la;
+    ct1 = 2 * rbb + x1 - la;
+    return ct0 < ct1;
   };
 
   if (warp == 0) {
@@ -145,11 +171,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       bool first = true;
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int rb = rb_of(it);
-        const int sp = it % P.col_splits;
-        const int ct0 = sp * per_split;
-        const int ct1 = min(P.col_tiles, ct0 + per_split);
+      for (int it = blockIdx.x; it < items; it += gridDim.x)
+      for (int sub = 0; sub < 2; sub++) {
+        int rb, ct0, ct1;
+        if (!subitem(it, sub, rb, ct0, ct1)) continue;
         if (!first) {
           ptx::mbar_wait(aempty, aph);
           aph ^= 1;
@@ -183,10 +208,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
       const uint32_t b0 = ptx::smem_u32(sB);
       int stage = 0;
       uint32_t ph = 0, aph = 0, tph[TC_NBUF] = {};
-      for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int sp = it % P.col_splits;
-        const int ct0 = sp * per_split;
-        const int ct1 = min(P.col_tiles, ct0 + per_split);
+      for (int it = blockIdx.x; it < items; it += gridDim.x)
+      for (int sub = 0; sub < 2; sub++) {
+        int rb, ct0, ct1;
+        if (!subitem(it, sub, rb, ct0, ct1)) continue;
         ptx::mbar_wait(afull, aph);
         aph ^= 1;
         for (int ct = ct0; ct < ct1; ct++) {
@@ -222,11 +247,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     uint32_t tph[TC_NBUF] = {};
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
-      const int rb = rb_of(it);
-      const int sp = it % P.col_splits;
-      const int ct0 = sp * per_split;
-      const int ct1 = min(P.col_tiles, ct0 + per_split);
+    for (int it = blockIdx.x; it < items; it += gridDim.x)
+    for (int sub = 0; sub < 2; sub++) {
+      int rb, ct0, ct1;
+      if (!subitem(it, sub, rb, ct0, ct1)) continue;
       RowState R[TC_RT];
 #pragma unroll
       for (int r = 0; r < TC_RT; r++) {
@@ -360,7 +384,7 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
     cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = 1;
   }
-  const int items = (P.rb_end - P.rb_begin) * P.col_splits;
+  const int items = (P.upper ? (P.rb_end - P.rb_begin + 1) / 2 : P.rb_end - P.rb_begin) * P.col_splits;
   int grid = c->sm_count < items ? c->sm_count : items;
   if (grid < 1) return APPD_OK;
   static const int exp_pass = getenv("APPD_TC_EXPERIMENT") ? atoi(getenv("APPD_TC_EXPERIMENT")) : 0;

@@ -75,6 +75,8 @@ struct TcParams {
   // rb_list[]; when null the blocks rb_begin .. rb_end-1 are scanned
   const int* rb_list;
   const int* rb_count;
+  // symmetric pass: row block rb scans column tiles >= 2 rb only (rb_list must be null)
+  int upper;
 };
 
 struct CmParams {
@@ -93,6 +95,7 @@ struct CmParams {
   ErrModel em;
   unsigned* CUB;        // [k][k] float bits
   unsigned* list;       // (32-column chunk << 17 | row) entries
+  int upper;            // TM holds only segments >= 4 (p / 512) of row p (symmetric pass)
   unsigned list_cap;
   unsigned* counters;   // [1] listed chunk entries
   const float* XTp;
