@@ -599,7 +599,9 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   stage_event(c, 2);
 
   // ---- a4: sort the MST edge keys ascending (Kruskal order = P:L98's descending removal reversed) ----
-  if ((s = sort_keys_u64(c, mstkeys, sorted, n - 1))) return s;
+  // only the weight bits decide the order: ties in any order are a valid Kruskal order
+  // (SURVEY App. A.5), and the radix passes over the pair index would be wasted
+  if ((s = sort_keys_u64_bits64(c, mstkeys, sorted, n - 1, ks.shift, 64))) return s;
   stage_event(c, 3);
 
   // ---- a5: dendrogram (v1: host union-find with list concatenation) ----

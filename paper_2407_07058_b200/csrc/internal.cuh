@@ -124,7 +124,7 @@ enum Slot {
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
-  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_ROWBUF,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
@@ -163,6 +163,7 @@ struct TcState {
   int* rb_count = nullptr;
   int* rows_list = nullptr;             // [n] flagged rows (original indices)
   float* XT = nullptr;                 // d x npad original-order transpose (exact row kernel)
+  u64* rowbuf = nullptr;               // [npad][96] (chunk << 32 | G' max bits) of the fused top-K scan
   unsigned* lista = nullptr;           // (chunk << 17 | row) candidate entries, then sorted
   unsigned* listb = nullptr;
   unsigned list_entries_cap = 0;
@@ -184,9 +185,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
 
 // candidate cache (k_cache.cu)
 struct ErrModel;
-appd_status launch_topk_thr(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                            const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
-                            float* thrK);
+
 appd_status launch_topk_select(appd_ctx* c, int p_begin, int p_end, int n, int K, const unsigned* cnt,
                                const u64* cand, int cap, u64* ckey, int* cj, int* ccnt, u64* compbest, int* fallback,
                                unsigned* nfallback);
@@ -260,6 +259,9 @@ int prim_max_n();
 appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count);
 appd_status sort_keys_u32_bits(appd_ctx* c, const unsigned* in, unsigned* out, int64_t count, int begin_bit, int end_bit);
 appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count);
+appd_status sort_pairs_i32_bits(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count,
+                                int end_bit);
+appd_status sort_keys_u64_bits64(appd_ctx* c, const u64* in, u64* out, int64_t count, int begin_bit, int end_bit);
 appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t count);
 
 // host dendrogram (dendrogram_host.cpp)

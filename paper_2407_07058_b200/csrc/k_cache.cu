@@ -6,14 +6,14 @@
 //
 // Round 0 (singletons) runs the tensor-core scan once with one maximum of G' per
 // 32 columns (TM32).  For each row p:
-//   k_topk_thr     the K-th largest chunk maximum gives an upper bound UBK of s^2 r
+//   k_topk_scan    the K-th largest chunk maximum gives an upper bound UBK of s^2 r
 //                  for K distinct columns (each chunk's best column), hence for the
-//                  row's K-th smallest exact R1 value;  thrK = the G' threshold below
-//                  which no column can have L <= UBK (tc_common.cuh error model);
-//   k_chunk_exact  every chunk with maximum >= thrK is re-evaluated with the exact R1
-//                  chain (one CTA per chunk: the chunk's 32 columns stay in shared
-//                  memory, one warp per listed row, one column per lane); every column
-//                  with s^2 r <= UBK is appended to the row's candidate list;
+//                  row's K-th smallest exact R1 value; every chunk whose maximum meets
+//                  the G' threshold of UBK (tc_common.cuh error model) is listed;
+//   k_list_exact   the listed (chunk, row) pairs, sorted by chunk, are re-evaluated
+//                  with the exact R1 chain (register-blocked, chunk columns and rows
+//                  staged in shared memory); every column with s^2 r <= UBK is
+//                  appended to the row's candidate list;
 //   k_topk_select  the K smallest exact edge keys of the list are the row's cache.
 // Every column not appended has s^2 r > UBK >= the K-th appended value, so the cache
 // is exactly the row's K smallest keys (keys are a strict order: weight, then pair
@@ -30,44 +30,6 @@
 #include "tc_common.cuh"
 
 namespace appd {
-
-// per row: UBK and the G' threshold thrK (float bits in UBK / thrK)
-template <int K>
-__global__ void k_topk_thr(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
-                           const float* __restrict__ nrm, const float* __restrict__ len, float maxlen, ErrModel em,
-                           float* __restrict__ UBK, float* __restrict__ thrK) {
-  for (int p = p_begin + blockIdx.x * blockDim.x + threadIdx.x; p < p_end; p += gridDim.x * blockDim.x) {
-    float top[K];
-#pragma unroll
-    for (int t = 0; t < K; t++) top[t] = -INFINITY;
-    constexpr int U = 32;  // loads in flight
-    for (int c = 0; c < nch; c += U) {
-      float v[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) v[u] = c + u < nch ? __ldcs(TM32 + (int64_t)(c + u) * ld + p) : -INFINITY;
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (v[u] > top[K - 1]) {  // branch-free insertion into the descending list
-          float x = v[u];
-#pragma unroll
-          for (int t = 0; t < K; t++) {
-            const float hi = fmaxf(top[t], x);
-            x = fminf(top[t], x);
-            top[t] = hi;
-          }
-        }
-      }
-    }
-    const float ni = nrm[p], li = len[p];
-    float ub = INFINITY, thr = -INFINITY;
-    if (top[K - 1] > -INFINITY) {
-      ub = em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen);
-      thr = em_thr(em, ub, ni, li, maxlen);
-    }
-    UBK[p] = ub;
-    thrK[p] = thr;
-  }
-}
 
 // list entries: (32-column chunk << LIST_SHIFT) | row position (n <= 2^17, chunks < 2^12)
 constexpr int LIST_SHIFT = 17;
@@ -89,39 +51,119 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
   return base + incl - cnt;
 }
 
-// Pass 2 over TM32 (thread per row, 32 loads in flight): every chunk whose maximum
-// meets the row's final threshold thrK is listed.  Slots are allocated once per batch
-// per warp.  A row whose entries do not fit is poisoned (cand_cnt = ~0: invalid cache,
-// exact full-row minimum).
-__global__ void k_topk_list(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
-                            const float* __restrict__ thrK, unsigned* __restrict__ list, unsigned* __restrict__ count,
-                            unsigned cap, unsigned* __restrict__ cand_cnt) {
+// One pass over TM32 (thread per row, 32 loads in flight): the running K largest chunk
+// maxima give a running threshold; every chunk passing it is buffered (the threshold only
+// tightens as the K-th largest grows, so the buffer holds every chunk that passes the
+// final threshold thrK).  At the end UBK is stored and the buffered chunks passing thrK
+// are listed.  A row whose buffer overflows re-reads its TM32 row once.
+template <int K>
+__global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
+                            const float* __restrict__ nrm, const float* __restrict__ len, float maxlen, ErrModel em,
+                            float* __restrict__ UBK, u64* __restrict__ rowbuf, int rbcap, unsigned* __restrict__ list,
+                            unsigned* __restrict__ count, unsigned cap, unsigned* __restrict__ cand_cnt) {
   const int lane = threadIdx.x & 31;
   constexpr int U = 32;
   for (int p0 = p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < p_end; p0 += gridDim.x * blockDim.x) {
     const int p = p0 + lane;
     const bool valid = p < p_end;
-    const float thr = valid ? thrK[p] : INFINITY;
-    bool lost = false;
+    const float ni = valid ? nrm[p] : 0.0f, li = valid ? len[p] : 0.0f;
+    float top[K];
+#pragma unroll
+    for (int t = 0; t < K; t++) top[t] = -INFINITY;
+    float thr = -INFINITY;
+    int nb = 0;
+    u64* buf = rowbuf + (int64_t)(valid ? p : 0) * rbcap;
     for (int c0 = 0; c0 < nch; c0 += U) {
-      unsigned mask = 0;
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) v[u] = (valid && c0 + u < nch) ? __ldcs(TM32 + (int64_t)(c0 + u) * ld + p) : -INFINITY;
+      const float kth0 = top[K - 1];
 #pragma unroll
       for (int u = 0; u < U; u++) {
-        const float v = (valid && c0 + u < nch) ? __ldcs(TM32 + (int64_t)(c0 + u) * ld + p) : -INFINITY;
-        mask |= (v >= thr && v > -INFINITY) ? (1u << u) : 0u;
+        if (v[u] > top[K - 1]) {  // branch-free insertion into the descending list
+          float x = v[u];
+#pragma unroll
+          for (int t = 0; t < K; t++) {
+            const float hi = fmaxf(top[t], x);
+            x = fminf(top[t], x);
+            top[t] = hi;
+          }
+        }
       }
-      if (!__any_sync(0xffffffffu, mask != 0)) continue;
-      unsigned slot = warp_alloc(count, __popc(mask));
-      while (mask) {
-        const int u = __ffs(mask) - 1;
-        mask &= mask - 1;
-        if (slot < cap) list[slot] = ((unsigned)(c0 + u) << LIST_SHIFT) | (unsigned)p;
-        else lost = true;
-        slot++;
+      if (top[K - 1] != kth0 && top[K - 1] > -INFINITY)
+        thr = em_thr(em, em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen), ni, li, maxlen);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (v[u] >= thr && v[u] > -INFINITY) {
+          if (nb < rbcap) buf[nb] = ((u64)(unsigned)(c0 + u) << 32) | __float_as_uint(v[u]);
+          nb++;
+        }
+      }
+    }
+    float ub = INFINITY;
+    if (valid && top[K - 1] > -INFINITY) {
+      ub = em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen);
+      thr = em_thr(em, ub, ni, li, maxlen);
+    } else {
+      thr = -INFINITY;
+    }
+    if (valid) UBK[p] = ub;
+    // emit: count, one warp allocation, write
+    const bool over = nb > rbcap;
+    unsigned mine = 0;
+    if (valid && !over) {
+      for (int j = 0; j < nb; j++) mine += __uint_as_float((unsigned)buf[j]) >= thr;
+    } else if (valid) {
+      for (int c = 0; c < nch; c++) {
+        const float v = TM32[(int64_t)c * ld + p];
+        mine += v >= thr && v > -INFINITY;
+      }
+    }
+    unsigned slot = warp_alloc(count, mine);
+    bool lost = false;
+    if (valid && !over) {
+      for (int j = 0; j < nb; j++) {
+        const u64 e = buf[j];
+        if (__uint_as_float((unsigned)e) >= thr) {
+          if (slot < cap) list[slot] = ((unsigned)(e >> 32) << LIST_SHIFT) | (unsigned)p;
+          else lost = true;
+          slot++;
+        }
+      }
+    } else if (valid) {
+      for (int c = 0; c < nch; c++) {
+        const float v = TM32[(int64_t)c * ld + p];
+        if (v >= thr && v > -INFINITY) {
+          if (slot < cap) list[slot] = ((unsigned)c << LIST_SHIFT) | (unsigned)p;
+          else lost = true;
+          slot++;
+        }
       }
     }
     if (lost) cand_cnt[p] = 0xFFFFFFFFu;
   }
+}
+
+appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+                             const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
+                             u64* rowbuf, int rbcap, unsigned* list, unsigned* count, unsigned cap,
+                             unsigned* cand_cnt) {
+  const int rows = p_end - p_begin;
+  if (rows <= 0) return APPD_OK;
+  const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
+#define APPD_TOPK_SCAN(KK)                                                                                        \
+  k_topk_scan<KK><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, rowbuf, \
+                                               rbcap, list, count, cap, cand_cnt)
+  switch (K) {
+    case 4: APPD_TOPK_SCAN(4); break;
+    case 8: APPD_TOPK_SCAN(8); break;
+    case 16: APPD_TOPK_SCAN(16); break;
+    case 32: APPD_TOPK_SCAN(32); break;
+    default: return fail(c, APPD_ERR_INVALID_ARGUMENT, "cache length K = %d (4, 8, 16 or 32)", K);
+  }
+#undef APPD_TOPK_SCAN
+  APPD_LAUNCHED(c);
+  return APPD_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -552,33 +594,6 @@ appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, 
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-appd_status launch_topk_thr(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                            const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
-                            float* thrK) {
-  const int rows = p_end - p_begin;
-  if (rows <= 0) return APPD_OK;
-  const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
-  switch (K) {
-    case 4: k_topk_thr<4><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, thrK); break;
-    case 8: k_topk_thr<8><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, thrK); break;
-    case 16: k_topk_thr<16><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, thrK); break;
-    case 32: k_topk_thr<32><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, thrK); break;
-    default: return fail(c, APPD_ERR_INVALID_ARGUMENT, "cache length K = %d (4, 8, 16 or 32)", K);
-  }
-  APPD_LAUNCHED(c);
-  return APPD_OK;
-}
-
-appd_status launch_topk_list(appd_ctx* c, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                             const float* thrK, unsigned* list, unsigned* count, unsigned cap, unsigned* cand_cnt) {
-  const int rows = p_end - p_begin;
-  if (rows <= 0) return APPD_OK;
-  const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
-  k_topk_list<<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, thrK, list, count, cap, cand_cnt);
-  APPD_LAUNCHED(c);
-  return APPD_OK;
-}
-
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start) {
   const size_t smem = (size_t)L.d * (32 + LE_RB) * 4;

@@ -26,6 +26,9 @@
 
 namespace appd {
 
+// per-row chunk buffer of the fused top-K scan (running threshold)
+constexpr int kRowBuf = 96;
+
 // ---------------------------------------------------------------------------
 // preparation kernels
 // ---------------------------------------------------------------------------
@@ -475,6 +478,8 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
     st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
     if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");
+    st->rowbuf = (u64*)ws(c, S_TC_ROWBUF, sizeof(u64) * st->npad * kRowBuf);
+    if (!st->rowbuf) return fail(c, APPD_ERR_OUT_OF_MEMORY, "top-K row buffer");
     st->rows_list = (int*)ws(c, S_TC_ROWLIST, sizeof(int) * (n + 1));
     st->XT = (float*)ws(c, S_TC_XTO, sizeof(float) * st->npad * d);
     if (!st->rows_list || !st->XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate cache workspace");
@@ -666,7 +671,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   } else {
     k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
     APPD_LAUNCHED(c);
-    if ((s = sort_pairs_i32(c, st->keys, st->sc, st->keys + n + 1, st->perm, n))) return s;
+    if ((s = sort_pairs_i32_bits(c, st->keys, st->sc, st->keys + n + 1, st->perm, n, bits_for(k + 1)))) return s;
     k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
     APPD_LAUNCHED(c);
     k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
@@ -699,10 +704,8 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (p_end > p_begin) {
       const int nch = (int)(st->npad / 32);
       APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
-      if ((s = launch_topk_thr(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
-                               st->maxlen_scaled, P.em, st->UBK, st->thrK)))
-        return s;
-      if ((s = launch_topk_list(c, st->TM, st->npad, nch, p_begin, p_end, st->thrK, st->lista, st->counters + 6,
+      if ((s = launch_topk_scan(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
+                                st->maxlen_scaled, P.em, st->UBK, st->rowbuf, kRowBuf, st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
         return s;
       if ((s = exact_list(c, st, X, 0, nullptr, st->counters + 6, 0, nullptr))) return s;
@@ -769,7 +772,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   *listed_overflow = false;
   k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
   APPD_LAUNCHED(c);
-  if ((s = sort_pairs_i32(c, st->keys, st->sc, st->keys + n + 1, st->perm, n))) return s;
+  if ((s = sort_pairs_i32_bits(c, st->keys, st->sc, st->keys + n + 1, st->perm, n, bits_for(k + 1)))) return s;
   k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
   APPD_LAUNCHED(c);
   k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
