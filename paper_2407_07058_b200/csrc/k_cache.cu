@@ -665,7 +665,7 @@ appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, doubl
 // computes every row's min to every component; the contracted k x k graph then
 // finishes the MST").  Points are sorted by component (labels 0..k-1, contiguous
 // column ranges [cstart, cend)), and one tensor-core pass has written TM[seg][p],
-// the eligible maximum of G' over each 128-column segment.
+// the eligible maximum of G' over each TC_TMG-column segment.
 //   k_cm_rowub   CUB[C][D] = min over rows p of C of the upper bound of s^2 r from the
 //                segments lying entirely inside D (an exact pair exists below it);
 //   k_cm_filter  lists (p, seg) whenever a pair (p, j), j in seg and in D != C, can
@@ -685,9 +685,9 @@ __global__ void k_cm_rowub(CmParams P) {
     const int C = valid ? P.sc[p] : -1;
     const bool uni = __all_sync(0xffffffffu, C == __shfl_sync(0xffffffffu, C, 0));
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
-    const int smin = P.upper ? 4 * (p0 / 512) : 0;  // segments the (symmetric) scan wrote for these rows
+    const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;  // segments the (symmetric) scan wrote for these rows
     for (int D = 0; D < P.k; D++) {
-      const int s0 = max(smin, (P.cstart[D] + 127) / 128), s1 = P.cend[D] / 128;  // segments inside D
+      const int s0 = max(smin, (P.cstart[D] + TC_TMG - 1) / TC_TMG), s1 = P.cend[D] / TC_TMG;  // segments inside D
       float m = -INFINITY;
       if (valid && D != C)
         for (int s = s0; s < s1; s++) m = fmaxf(m, __ldcs(P.TM + (int64_t)s * P.ld + p));
@@ -708,7 +708,7 @@ __global__ void k_cm_rowub(CmParams P) {
 // upper bounds, scaled units).  A listed segment contributes its 32-column chunks.
 __global__ void k_cm_filter(CmParams P) {
   const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int nseg = min(P.nseg, (P.n + 127) / 128);
+  const int nseg = min(P.nseg, (P.n + TC_TMG - 1) / TC_TMG);
   for (int p0 = P.p_begin + (blockIdx.x * warps + w) * 32; p0 < P.p_end; p0 += gridDim.x * warps * 32) {
     const int p = p0 + lane;
     const bool valid = p < P.p_end;
@@ -717,7 +717,7 @@ __global__ void k_cm_filter(CmParams P) {
     int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
     float cachedT = 0.0f;
     constexpr int U = 16;
-    for (int s0 = P.upper ? 4 * (p0 / 512) : 0; s0 < nseg; s0 += U) {
+    for (int s0 = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0; s0 < nseg; s0 += U) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
@@ -726,8 +726,8 @@ __global__ void k_cm_filter(CmParams P) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         if (!(v[u] > -INFINITY)) continue;
-        const int q0 = (s0 + u) * 128;
-        const int D0 = __ldg(P.sc + q0), D1 = __ldg(P.sc + min(q0 + 127, P.n - 1));
+        const int q0 = (s0 + u) * TC_TMG;
+        const int D0 = __ldg(P.sc + q0), D1 = __ldg(P.sc + min(q0 + TC_TMG - 1, P.n - 1));
         float thr;
         if (D0 == D1) {
           if (D0 != cachedD) {
@@ -745,14 +745,15 @@ __global__ void k_cm_filter(CmParams P) {
       }
       if (!__any_sync(0xffffffffu, mask != 0)) continue;
       unsigned cnt = 0;
-      for (unsigned m = mask; m; m &= m - 1) cnt += (unsigned)min(4, (P.n - (s0 + __ffs(m) - 1) * 128 + 31) / 32);
+      for (unsigned m = mask; m; m &= m - 1)
+        cnt += (unsigned)min(TC_TMG / 32, (P.n - (s0 + __ffs(m) - 1) * TC_TMG + 31) / 32);
       unsigned slot = warp_alloc(P.counters + 1, cnt);
       while (mask) {
         const int s = s0 + __ffs(mask) - 1;
         mask &= mask - 1;
-        const int nc = min(4, (P.n - s * 128 + 31) / 32);
+        const int nc = min(TC_TMG / 32, (P.n - s * TC_TMG + 31) / 32);
         for (int t = 0; t < nc; t++, slot++)
-          if (slot < P.list_cap) P.list[slot] = ((unsigned)(4 * s + t) << LIST_SHIFT) | (unsigned)p;
+          if (slot < P.list_cap) P.list[slot] = ((unsigned)((TC_TMG / 32) * s + t) << LIST_SHIFT) | (unsigned)p;
       }
     }
   }

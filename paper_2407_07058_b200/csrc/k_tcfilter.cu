@@ -697,6 +697,22 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     P.rb_end = (int)rb_end;
     P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
     P.seg32 = 1;
+    if (getenv("APPD_TC_BENCH")) {  // debug: time the scan variants in isolation (results discarded)
+      const char* names[] = {"seg128", "seg32", "", "null-epilogue", "tmem-load-only", "no-B-copies", "null+noB"};
+      for (int pass : {0, 1, 3, 4, 5, 6}) {
+        float best = 1e9f;
+        for (int rep = 0; rep < 5; rep++) {
+          cudaEventRecord(c->ev[14], c->stream);
+          if ((s = launch_tcf_scan(c, pass, P))) return s;
+          cudaEventRecord(c->ev[15], c->stream);
+          cudaEventSynchronize(c->ev[15]);
+          float ms = 0.0f;
+          cudaEventElapsedTime(&ms, c->ev[14], c->ev[15]);
+          best = std::min(best, ms);
+        }
+        fprintf(stderr, "[appd] tc bench %-16s %.3f ms\n", names[pass], best);
+      }
+    }
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 1, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);

@@ -68,32 +68,36 @@ __device__ __forceinline__ void tmem_ld_seg(uint32_t taddr, float (&v)[128]) { p
 __device__ __forceinline__ float fmax_seg(const float (&v)[64]) { return fmax64(v); }
 __device__ __forceinline__ float fmax_seg(const float (&v)[128]) { return fmax128(v); }
 
-struct RowState {
-  int p;          // permuted row
-  bool valid;
-  float ni, li;   // |y^|^2, |y^|
-  int cs, ce;     // ineligible column range (the row's component)
-  float ub;       // running upper bound of s^2 r over eligible columns
-  float gbest;    // best segment maximum of G' seen so far
-};
-
-// eligible maximum of one 32-column chunk
-__device__ __forceinline__ float chunk_max(const float (&v)[32], const RowState& s, int q0, bool fast, int n) {
+// eligible maximum of one 32-column chunk (row p of component range [cs, ce))
+__device__ __forceinline__ float chunk_max(const float (&v)[32], bool valid, int cs, int ce, int q0, bool fast,
+                                           int n) {
   if (fast) return fmax32(v);
   float m = -INFINITY;
-  if (s.valid && !(q0 >= s.cs && q0 + 32 <= s.ce)) {
+  if (valid && !(q0 >= cs && q0 + 32 <= ce)) {
 #pragma unroll
     for (int t = 0; t < 32; t++) {
       const int qq = q0 + t;
-      const bool el = (qq < s.cs || qq >= s.ce) && qq < n;
+      const bool el = (qq < cs || qq >= ce) && qq < n;
       m = fmaxf(m, el ? v[t] : -INFINITY);
     }
   }
   return m;
 }
 
+// epilogue warps per variant: the 32-column (cache) pass uses 16 warps of 64 columns,
+// the 128-column pass 8 warps of 128 columns (measured best for each)
+template <bool SEG32>
+struct EpiCfg {
+  static constexpr int warps = SEG32 ? 16 : 8;
+  static constexpr int cols = TC_NA / (warps / 4);  // accumulator columns per epilogue warp
+  static constexpr int threads = 32 * (2 + warps);
+};
+
 template <int PASS, bool SEG32 = false>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
+__global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams P) {
+  constexpr int EPI_WARPS = EpiCfg<SEG32>::warps;
+  constexpr int WCOLS = EpiCfg<SEG32>::cols;
+  static_assert(SEG32 || WCOLS == TC_TMG, "stored maxima granularity");
   extern __shared__ __align__(1024) uint8_t smem[];
   const int K = P.K;
   const int NST = P.stages;
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     ptx::mbar_init(aempty, 1);
     for (int b = 0; b < TC_NBUF; b++) {
       ptx::mbar_init(tfull + b, 1);
-      ptx::mbar_init(tempty + b, TC_EPI_WARPS);
+      ptx::mbar_init(tempty + b, EPI_WARPS);
     }
     ptx::fence_mbar_init();
   }
@@ -251,25 +255,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
     for (int sub = 0; sub < 2; sub++) {
       int rb, ct0, ct1;
       if (!subitem(it, sub, rb, ct0, ct1)) continue;
-      RowState R[TC_RT];
+      // lean per-row state (registers): component range and, for the bound, the best
+      // maximum so far and the running upper bound.  The cache-building pass (SEG32)
+      // needs no bound.  Row p = rb * 512 + r * 128 + q * 32 + lane.
+      int cs[TC_RT], ce[TC_RT];
+      float ub[TC_RT], gb[TC_RT];
+      const int pbase = rb * TC_ROWS + q * 32 + lane;
 #pragma unroll
       for (int r = 0; r < TC_RT; r++) {
-        RowState& s = R[r];
-        s.p = rb * TC_ROWS + r * TC_M + q * 32 + lane;
-        s.valid = s.p < P.n;
-        s.ni = s.valid ? P.nrm[s.p] : 0.0f;
-        s.li = s.valid ? P.len[s.p] : 0.0f;
-        s.cs = s.valid ? (P.round0 ? s.p : P.cs[s.p]) : 0;
-        s.ce = s.valid ? (P.round0 ? s.p + 1 : P.ce[s.p]) : 0;
-        s.ub = INFINITY;
-        s.gbest = -INFINITY;
+        const int p = pbase + r * TC_M;
+        const bool valid = p < P.n;
+        cs[r] = valid ? (P.round0 ? p : P.cs[p]) : 0;
+        ce[r] = valid ? (P.round0 ? p + 1 : P.ce[p]) : 0;
+        ub[r] = INFINITY;
+        gb[r] = -INFINITY;
       }
       for (int ct = ct0; ct < ct1; ct++) {
 #pragma unroll
         for (int i = 0; i < TC_RT * TC_HALVES; i++) {
           const int r = i / TC_HALVES, hh = i % TC_HALVES, b = i % TC_NBUF;
-          const int h0 = ct * TC_N + hh * TC_NA + h * TC_TMG;  // first column of this warp's segment
-          const int seg = h0 / TC_TMG;
+          const int h0 = ct * TC_N + hh * TC_NA + h * WCOLS;  // first column of this warp's segment
+          const int seg = h0 / WCOLS;
+          const int p = pbase + r * TC_M;
+          const bool valid = p < P.n;
           ptx::mbar_wait(tfull + b, tph[b]);
           tph[b] ^= 1;
           ptx::tc_fence_after();
@@ -278,78 +286,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcf_scan(TcParams P) {
             if (lane == 0) ptx::mbar_arrive(tempty + b);
             continue;
           }
-          RowState& s = R[r];
-          float v[TC_TMG];
-          tmem_ld_seg(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TC_NA + h * TC_TMG), v);
-          if (PASS == 4) {  // experiment: TMEM load only
-            ptx::tmem_ld_wait();
-            ptx::reg_fence(v);
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty + b);
-            if (v[lane] == 12345.678f && s.valid) P.TM[s.p] = v[63];
-            continue;
-          }
+          float v[WCOLS];
+          tmem_ld_seg(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TC_NA + h * WCOLS), v);
           ptx::tmem_ld_wait();
           ptx::reg_fence(v);
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(tempty + b);  // accumulator consumed: free it early
+          if (PASS == 4) {  // experiment: TMEM load only
+            if (v[0] == 12345.678f && valid) P.TM[p] = v[WCOLS - 1];
+            continue;
+          }
           if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
             if (it == (int)blockIdx.x && P.dump) {
               const int rloc = r * TC_M + q * 32 + lane;
-              for (int t = 0; t < TC_TMG; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + t] = v[t];
+              for (int t = 0; t < WCOLS; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + t] = v[t];
             }
             continue;
           }
           // warp-uniform fast path: valid rows whose component misses these real columns
           const bool fast =
-              __all_sync(0xffffffffu, s.valid && (h0 + TC_TMG <= s.cs || h0 >= s.ce) && h0 + TC_TMG <= P.n);
-          float m;
+              __all_sync(0xffffffffu, valid && (h0 + WCOLS <= cs[r] || h0 >= ce[r]) && h0 + WCOLS <= P.n);
           if (SEG32) {
-            // four 32-column maxima (the same FMNMX3 count as one 128-column tree)
-            float cm[TC_TMG / 32];
+            // 32-column maxima (the same FMNMX3 count as one tree over the segment)
 #pragma unroll
-            for (int c = 0; c < TC_TMG / 32; c++) {
+            for (int c = 0; c < WCOLS / 32; c++) {
               float w[32];
 #pragma unroll
               for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
-              cm[c] = chunk_max(w, s, h0 + c * 32, fast, P.n);
-            }
-            m = cm[0];
-#pragma unroll
-            for (int c = 1; c < TC_TMG / 32; c++) m = fmaxf(m, cm[c]);
-            if (s.valid) {
-#pragma unroll
-              for (int c = 0; c < TC_TMG / 32; c++) P.TM[(int64_t)(h0 / 32 + c) * P.tm_ld + s.p] = cm[c];
+              const float cm = chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, fast, P.n);
+              if (valid) P.TM[(int64_t)(h0 / 32 + c) * P.tm_ld + p] = cm;
             }
           } else {
+            float m;
             if (fast) {
               m = fmax_seg(v);
             } else {
               m = -INFINITY;
 #pragma unroll
-              for (int c = 0; c < TC_TMG / 32; c++) {
+              for (int c = 0; c < WCOLS / 32; c++) {
                 float w[32];
 #pragma unroll
                 for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
-                m = fmaxf(m, chunk_max(w, s, h0 + c * 32, false, P.n));
+                m = fmaxf(m, chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, false, P.n));
               }
             }
             // eligible maximum of G' over this (row, segment); a warp's rows are
             // consecutive, so the store is coalesced ([segment][row] layout)
-            if (s.valid) P.TM[(int64_t)seg * P.tm_ld + s.p] = m;
-          }
-          if (s.valid && m > s.gbest) {  // tighten the bound only when the best improves
-            s.gbest = m;
-            s.ub = fminf(s.ub, em_upper(P.em, s.ni - 2.0f * m, s.ni, s.li, P.seg_maxlen[seg]));
+            if (valid) P.TM[(int64_t)seg * P.tm_ld + p] = m;
+            if (valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
+              gb[r] = m;
+              const float ni = __ldg(P.nrm + p), li = __ldg(P.len + p);
+              ub[r] = fminf(ub[r], em_upper(P.em, ni - 2.0f * m, ni, li, P.seg_maxlen[seg]));
+            }
           }
         }
       }
-      if (PASS == 0) {
+      if (PASS == 0 && !SEG32) {
 #pragma unroll
-        for (int r = 0; r < TC_RT; r++)
-          if (R[r].valid && R[r].ub < INFINITY) atomicMin(P.UB + R[r].p, __float_as_uint(fmaxf(R[r].ub, 0.0f)));
+        for (int r = 0; r < TC_RT; r++) {
+          const int p = pbase + r * TC_M;
+          if (p < P.n && ub[r] < INFINITY) atomicMin(P.UB + p, __float_as_uint(fmaxf(ub[r], 0.0f)));
+        }
       }
     }
   }
@@ -388,21 +386,23 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   int grid = c->sm_count < items ? c->sm_count : items;
   if (grid < 1) return APPD_OK;
   static const int exp_pass = getenv("APPD_TC_EXPERIMENT") ? atoi(getenv("APPD_TC_EXPERIMENT")) : 0;
-  if (pass == 0 && exp_pass == 3) {
+  int ep = exp_pass;
+  if (pass >= 3) ep = pass;  // explicit experiment request (debug benchmark)
+  if (ep == 3) {
     cudaFuncSetAttribute(k_tcf_scan<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    k_tcf_scan<3><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  } else if (pass == 0 && exp_pass == 4) {
+    k_tcf_scan<3><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  } else if (ep == 4) {
     cudaFuncSetAttribute(k_tcf_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    k_tcf_scan<4><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  } else if (pass == 0 && exp_pass == 5) {
+    k_tcf_scan<4><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  } else if (ep == 5) {
     cudaFuncSetAttribute(k_tcf_scan<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    k_tcf_scan<5><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  } else if (pass == 0 && exp_pass == 6) {
+    k_tcf_scan<5><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  } else if (ep == 6) {
     cudaFuncSetAttribute(k_tcf_scan<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    k_tcf_scan<6><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  } else if (pass == 0) k_tcf_scan<0><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  else if (pass == 1) k_tcf_scan<0, true><<<grid, TC_THREADS, smem, c->stream>>>(P);
-  else k_tcf_scan<2><<<1, TC_THREADS, smem, c->stream>>>(P);
+    k_tcf_scan<6><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  } else if (pass == 0) k_tcf_scan<0><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  else if (pass == 1) k_tcf_scan<0, true><<<grid, EpiCfg<true>::threads, smem, c->stream>>>(P);
+  else k_tcf_scan<2><<<1, EpiCfg<false>::threads, smem, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
