@@ -76,7 +76,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
     for (int c0 = 0; c0 < nch; c0 += U) {
       float v[U];
 #pragma unroll
-      for (int u = 0; u < U; u++) v[u] = (valid && c0 + u < nch) ? __ldcs(TM32 + (int64_t)(c0 + u) * ld + p) : -INFINITY;
+      for (int u = 0; u < U; u++) v[u] = (valid && c0 + u < nch) ? __ldcs(TM32 + tm_index(c0 + u, p, nch)) : -INFINITY;
       const float kth0 = top[K - 1];
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -115,7 +115,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
       for (int j = 0; j < nb; j++) mine += __uint_as_float((unsigned)buf[j]) >= thr;
     } else if (valid) {
       for (int c = 0; c < nch; c++) {
-        const float v = TM32[(int64_t)c * ld + p];
+        const float v = TM32[tm_index(c, p, nch)];
         mine += v >= thr && v > -INFINITY;
       }
     }
@@ -132,7 +132,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
       }
     } else if (valid) {
       for (int c = 0; c < nch; c++) {
-        const float v = TM32[(int64_t)c * ld + p];
+        const float v = TM32[tm_index(c, p, nch)];
         if (v >= thr && v > -INFINITY) {
           if (slot < cap) list[slot] = ((unsigned)c << LIST_SHIFT) | (unsigned)p;
           else lost = true;
@@ -690,7 +690,7 @@ __global__ void k_cm_rowub(CmParams P) {
       const int s0 = max(smin, (P.cstart[D] + TC_TMG - 1) / TC_TMG), s1 = P.cend[D] / TC_TMG;  // segments inside D
       float m = -INFINITY;
       if (valid && D != C)
-        for (int s = s0; s < s1; s++) m = fmaxf(m, __ldcs(P.TM + (int64_t)s * P.ld + p));
+        for (int s = s0; s < s1; s++) m = fmaxf(m, __ldcs(P.TM + tm_index(s, p, P.nseg)));
       float ub = m > -INFINITY ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen) : INFINITY;
       if (uni) {
 #pragma unroll
@@ -721,7 +721,7 @@ __global__ void k_cm_filter(CmParams P) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
-        v[u] = (valid && s0 + u < nseg) ? __ldcs(P.TM + (int64_t)(s0 + u) * P.ld + p) : -INFINITY;
+        v[u] = (valid && s0 + u < nseg) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
       unsigned mask = 0;
 #pragma unroll
       for (int u = 0; u < U; u++) {

@@ -231,7 +231,7 @@ __global__ void k_filter_tiles(ExactParams E) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
-        v[u] = (valid && t0 + u < E.nseg) ? __ldcs(E.TM + (int64_t)(t0 + u) * E.npad + p) : -INFINITY;
+        v[u] = (valid && t0 + u < E.nseg) ? __ldcs(E.TM + tm_index(t0 + u, p, E.nseg)) : -INFINITY;
       bool any = false;
 #pragma unroll
       for (int u = 0; u < U; u++) any |= v[u] >= thr_min && v[u] > -INFINITY;
@@ -521,6 +521,7 @@ static void fill_scan_params(const TcState* st, TcParams* P) {
   P->UB = st->UB;
   P->TM = st->TM;
   P->tm_ld = st->npad;
+  P->tm_nseg = (int)(st->npad / 32);
   P->n = (int)st->n;
   P->K = st->K;
   P->stages = st->stages;

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
 #pragma unroll
               for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
               const float cm = chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, fast, P.n);
-              if (valid) P.TM[(int64_t)(h0 / 32 + c) * P.tm_ld + p] = cm;
+              if (valid) P.TM[tm_index(h0 / 32 + c, p, P.tm_nseg)] = cm;
             }
           } else {
             float m;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
             }
             // eligible maximum of G' over this (row, segment); a warp's rows are
             // consecutive, so the store is coalesced ([segment][row] layout)
-            if (valid) P.TM[(int64_t)seg * P.tm_ld + p] = m;
+            if (valid) P.TM[tm_index(seg, p, P.col_tiles * (TC_N / TC_TMG))] = m;
             if (valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
               gb[r] = m;
               const float ni = __ldg(P.nrm + p), li = __ldg(P.len + p);

@@ -48,6 +48,14 @@ __device__ __forceinline__ float em_thr(const ErrModel& e, float ub, float ni, f
   return 0.5f * (ni - T);
 }
 
+// Stored maxima layout, row-block major: element (segment s, row p) of a table with
+// nseg segments lives at (p / 512) * nseg * 512 + s * 512 + p % 512, so the writes of
+// one 512-row work item fill one contiguous region (few TLB pages) and a warp's 32
+// consecutive rows stay one 128-byte line per segment.
+__host__ __device__ __forceinline__ int64_t tm_index(int s, int p, int nseg) {
+  return (int64_t)(p >> 9) * nseg * 512 + (int64_t)s * 512 + (p & 511);
+}
+
 struct TcParams {
   const __half* YA;          // row operand granules (128 points x K, core-matrix layout)
   const __half* YB;          // column operand granules
@@ -58,7 +66,8 @@ struct TcParams {
   const int* ce;             // per permuted row: one past the last position
   unsigned* UB;              // per permuted row: upper bound (float bits, >= 0)
   float* TM;                 // [segment][row]: eligible maximum of G' over the TC_TMG columns
-  int64_t tm_ld;             // leading dimension of TM (npad)
+  int64_t tm_ld;             // leading dimension of TM (npad), [segment][row] layout (128-column tables)
+  int tm_nseg;               // segments per row of the row-block-major 32-column table (npad / 32)
   int n;                     // points
   int K;                     // padded K (multiple of 16)
   int stages;                // shared-memory ring depth for the column operand
