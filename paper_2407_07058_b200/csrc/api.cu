@@ -418,13 +418,13 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   APPD_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(int) * 16, c->stream));
   int64_t k = n;
   int rounds = 0;
-  int* hostk = nullptr;
-  int hk[2];
-  hostk = hk;
+  int* hostk = reinterpret_cast<int*>(c->pinned_small + 24);  // pinned: the copies stay asynchronous
   const int finish_k = c->opt.finish_k == 0 ? 128 : std::min(c->opt.finish_k, 128);
+  bool cm_timing_pending = false;
   while (k > 1) {
     // ---- component-matrix finish: the contracted k-node graph's exact edge keys ----
     if (use_tc && tc.topk && rounds > 0 && finish_k > 0 && k <= finish_k) {
+      tc.lookup_pending = false;  // the component matrix replaces the queued lookup
       u64* WCM = (u64*)ws(c, S_TC_WCM, sizeof(u64) * k * k);
       if (!WCM) return fail(c, APPD_ERR_OUT_OF_MEMORY, "component matrix");
       bool ovf = false;
@@ -443,36 +443,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         if (!ovf && (s = nccl_allreduce_min_u64(c, WCM, k * k))) return s;
       }
       if (!ovf) {
-        std::vector<u64> w((size_t)(k * k));
-        int cnt = 0;
-        APPD_CUDA(c, cudaMemcpyAsync(w.data(), WCM, sizeof(u64) * k * k, cudaMemcpyDeviceToHost, c->stream));
-        APPD_CUDA(c, cudaMemcpyAsync(&cnt, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        // Prim on the contracted graph on the device (keys are a strict order: the MST is
+        // unique); its k - 1 edges are appended to mstkeys, the count checked at the end
+        if ((s = launch_cm_prim(c, WCM, (int)k, mstkeys, counters))) return s;
         if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
-        // Prim on the contracted graph (keys are a strict order: the MST is unique)
-        std::vector<u64> best((size_t)k, KEY_NONE), edges;
-        std::vector<char> in((size_t)k, 0);
-        in[0] = 1;
-        for (int64_t q = 1; q < k; q++) best[q] = std::min(w[q], w[(size_t)q * k]);
-        for (int64_t step = 1; step < k; step++) {
-          int64_t b = -1;
-          for (int64_t q = 0; q < k; q++)
-            if (!in[q] && (b < 0 || best[q] < best[b])) b = q;
-          if (b < 0 || best[b] == KEY_NONE) return fail(c, APPD_ERR_CUDA, "component matrix has no edge");
-          in[b] = 1;
-          edges.push_back(best[b]);
-          for (int64_t q = 0; q < k; q++)
-            if (!in[q]) best[q] = std::min(best[q], std::min(w[(size_t)b * k + q], w[(size_t)q * k + b]));
-        }
-        if (cnt + (int64_t)edges.size() != n - 1)
-          return fail(c, APPD_ERR_CUDA, "component matrix: %d + %zu edges, expected %lld", cnt, edges.size(),
-                      (long long)(n - 1));
-        APPD_CUDA(c, cudaMemcpyAsync(mstkeys + cnt, edges.data(), sizeof(u64) * edges.size(), cudaMemcpyHostToDevice,
-                                     c->stream));
-        const int total = cnt + (int)edges.size();
-        APPD_CUDA(c, cudaMemcpyAsync(counters, &total, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-        if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
+        cm_timing_pending = c->opt.timing != 0;  // read after the final synchronisation
         c->stats.cm_k = (int)k;
         c->stats.tcscan_launches++;
         if (c->opt.world == 1) {  // upper-triangle pass: row block rb against columns >= 512 rb
@@ -496,7 +471,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     static const bool dbg = getenv("APPD_DEBUG_ROUNDS") != nullptr;
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
-    if ((s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
+    if (!(use_tc && tc.lookup_pending) && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
     if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
     const int64_t l0 = c->launches;
@@ -546,6 +521,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if ((s = launch_jump(c, parent, k, flags))) return s;
     if ((s = exclusive_scan_i32(c, flags, newid, k))) return s;
     if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
+    // the next round's cache lookup rides on this round's synchronisation (labels are final)
+    if (use_tc && tc.topk && c->opt.world == 1) {
+      if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
+      if ((s = tcf_lookup_async(c, &tc, comp, compbest))) return s;
+    }
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
@@ -590,12 +570,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     k = knew;
   }
   c->stats.rounds = rounds;
-  {
-    int cnt = 0;
-    APPD_CUDA(c, cudaMemcpyAsync(&cnt, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (cnt != n - 1) return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", cnt, (long long)(n - 1));
-  }
+  // MST edge count: checked at the final synchronisation (an internal consistency check)
+  int* mst_count = reinterpret_cast<int*>(c->pinned_small + 26);
+  *mst_count = -1;
+  APPD_CUDA(c, cudaMemcpyAsync(mst_count, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   stage_event(c, 2);
 
   // ---- a4: sort the MST edge keys ascending (Kruskal order = P:L98's descending removal reversed) ----
@@ -670,6 +648,9 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if ((s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, stride, n, M, row0, sense < 0))) return s;
   stage_event(c, 6);
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (*mst_count != n - 1)
+    return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", *mst_count, (long long)(n - 1));
+  if (cm_timing_pending) c->stats.ms_scan += ev_ms(c, 8, 9);
   c->stats.fill_bytes = rows * n * 4;
   c->stats.kernel_launches = c->launches;
   if (c->opt.timing) {

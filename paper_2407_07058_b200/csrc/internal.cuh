@@ -175,11 +175,14 @@ struct TcState {
   // per-round statistics (host)
   int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0, last_list_entries = 0;
   bool scanned = false;  // this round launched the tensor-core scan (ev[10] -> ev[11] bracket it)
+  bool lookup_pending = false;  // next round's cache lookup already queued (tcf_lookup_async)
 };
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
                       u64* compbest, int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
 
+appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters);
+appd_status tcf_lookup_async(appd_ctx* c, TcState* st, const int* comp, u64* compbest);
 appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, int64_t k, u64* WCM,
                    int64_t rb_begin, int64_t rb_end, bool* listed_overflow);
 

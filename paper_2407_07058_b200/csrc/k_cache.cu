@@ -759,6 +759,172 @@ __global__ void k_cm_filter(CmParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Contracted-graph steps of the component-matrix finish, one CTA (k <= 128 nodes, one
+// thread per node).  Both are Prim's algorithm on a dense k x k matrix.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_argmin_f(float v, int idx, float* sv, int* si, float& out_v, int& out_i) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov < v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+  }
+  if (lane == 0) { sv[w] = v; si[w] = idx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float bv = sv[0];
+    int bi = si[0];
+    for (int t = 1; t < (int)(blockDim.x >> 5); t++)
+      if (sv[t] < bv || (sv[t] == bv && si[t] < bi)) { bv = sv[t]; bi = si[t]; }
+    sv[0] = bv;
+    si[0] = bi;
+  }
+  __syncthreads();
+  out_v = sv[0];
+  out_i = si[0];
+  __syncthreads();
+}
+
+// Listing thresholds.  CUB[C][D] bounds w(C, D) from above (both directions bound the
+// same w).  An MST edge (C, D) of the contracted graph satisfies w(C, D) <= the largest
+// bound on the path from C to D in the MST of the bounds (cut property), so
+// T = min(symmetric bound, path maximum) keeps every MST edge's minimum pair listed;
+// pairs above T are not MST edges and may come out inflated.  Output T (k x k).
+__global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
+                                                       unsigned* __restrict__ T) {
+  __shared__ int par[128];
+  __shared__ float pw[128];
+  __shared__ int cstart[129], kids[128];
+  __shared__ float sv[4];
+  __shared__ int si[4];
+  const int q = threadIdx.x;
+  auto bound = [&](int a, int b) -> float {
+    return fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
+  };
+  // Prim from node 0 on the symmetric bounds
+  bool in = q == 0;
+  float key = (q < k && q > 0) ? bound(0, q) : INFINITY;
+  int from = 0;
+  if (q < k) {
+    par[q] = -1;
+    pw[q] = 0.0f;
+  }
+  __syncthreads();
+  for (int step = 1; step < k; step++) {
+    float bv;
+    int bi;
+    block_argmin_f((q < k && !in) ? key : INFINITY, q, sv, si, bv, bi);
+    if (q == bi) {
+      in = true;
+      par[q] = from;
+      pw[q] = key;
+    }
+    if (q < k && !in) {
+      const float w = bound(bi, q);
+      if (w < key) {
+        key = w;
+        from = bi;
+      }
+    }
+  }
+  __syncthreads();
+  // children lists (CSR) of the tree rooted at 0
+  if (q == 0) {
+    for (int t = 0; t <= k; t++) cstart[t] = 0;
+    for (int t = 1; t < k; t++) cstart[par[t] + 1]++;
+    for (int t = 0; t < k; t++) cstart[t + 1] += cstart[t];
+    int fill[128];
+    for (int t = 0; t < k; t++) fill[t] = cstart[t];
+    for (int t = 1; t < k; t++) kids[fill[par[t]]++] = t;
+  }
+  __syncthreads();
+  if (q >= k) return;
+  // path maxima from root q: DFS over parent + children
+  float pm[128];
+  int stack[128];
+  for (int t = 0; t < k; t++) pm[t] = -1.0f;
+  pm[q] = 0.0f;
+  int sp = 0;
+  stack[sp++] = q;
+  while (sp) {
+    const int x = stack[--sp];
+    const int pp = par[x];
+    if (pp >= 0 && pm[pp] < 0.0f) {
+      pm[pp] = fmaxf(pm[x], pw[x]);
+      stack[sp++] = pp;
+    }
+    for (int e = cstart[x]; e < cstart[x + 1]; e++) {
+      const int y = kids[e];
+      if (pm[y] < 0.0f) {
+        pm[y] = fmaxf(pm[x], pw[y]);
+        stack[sp++] = y;
+      }
+    }
+  }
+  for (int t = 0; t < k; t++) {
+    const float b = bound(q, t);
+    T[(int64_t)q * k + t] = __float_as_uint(pm[t] < 0.0f ? b : fminf(b, pm[t]));
+  }
+}
+
+// Final contracted MST: Prim on min(WCM[C][D], WCM[D][C]) (exact keys, a strict order),
+// the k - 1 edge keys appended to mstkeys at counters[0]
+__global__ void __launch_bounds__(128) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
+                                                 int* __restrict__ counters) {
+  __shared__ u64 sv[4];
+  __shared__ int si[4];
+  __shared__ int base;
+  const int q = threadIdx.x, lane = q & 31, w = q >> 5;
+  auto wk = [&](int a, int b) -> u64 {
+    const u64 x = WCM[(int64_t)a * k + b], y = WCM[(int64_t)b * k + a];
+    return x < y ? x : y;
+  };
+  bool in = q == 0;
+  u64 key = (q < k && q > 0) ? wk(0, q) : KEY_NONE;
+  if (q == 0) base = counters[0];
+  __syncthreads();
+  for (int step = 1; step < k; step++) {
+    u64 v = (q < k && !in) ? key : KEY_NONE;
+    int idx = (q < k && !in) ? q : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov < v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    if (lane == 0) { sv[w] = v; si[w] = idx; }
+    __syncthreads();
+    u64 bv = sv[0];
+    int bi = si[0];
+    for (int t = 1; t < (int)(blockDim.x >> 5); t++)
+      if (sv[t] < bv || (sv[t] == bv && si[t] < bi)) { bv = sv[t]; bi = si[t]; }
+    __syncthreads();
+    if (bv == KEY_NONE) break;  // disconnected: the edge-count check reports it
+    if (q == bi) {
+      in = true;
+      mstkeys[base + step - 1] = key;
+    }
+    if (q < k && !in) {
+      const u64 x = wk(bi, q);
+      if (x < key) key = x;
+    }
+    if (q == 0) counters[0] = base + step;
+  }
+}
+
+appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T) {
+  k_cm_thresholds<<<1, 128, 0, c->stream>>>(CUB, k, T);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters) {
+  k_cm_prim<<<1, 128, 0, c->stream>>>(WCM, k, mstkeys, counters);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P) {
   const int rows = P.p_end - P.p_begin;
   if (rows <= 0) return APPD_OK;

@@ -469,7 +469,7 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->blockflag = (int*)ws(c, S_TC_BLOCKFLAG, sizeof(int) * (2 * nb + 8));
     st->rb_list = st->blockflag ? st->blockflag + nb : nullptr;
     st->rb_count = st->blockflag ? st->blockflag + 2 * nb : nullptr;
-    st->compUB = (unsigned*)ws(c, S_TC_COMPUB, sizeof(unsigned) * std::max<int64_t>(n, 128 * 128));
+    st->compUB = (unsigned*)ws(c, S_TC_COMPUB, sizeof(unsigned) * std::max<int64_t>(n, 2 * 128 * 128));
     st->UBK = (float*)ws(c, S_TC_UBK, sizeof(float) * st->npad);
     st->thrK = (float*)ws(c, S_TC_THRK, sizeof(float) * st->npad);
     st->cand_cnt = (unsigned*)ws(c, S_TC_CANDCNT, sizeof(unsigned) * (st->npad + 8));
@@ -631,6 +631,20 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   return launch_list_exact(c, mode, L, runs, runs + nch + 1, runs + 2 * (nch + 1));
 }
 
+// Queue the cache lookup of the next round (compbest must hold KEY_NONE): per-row first
+// eligible cached key -> compbest, flagged rows -> rows_list; the count lands in
+// pinned_small[9] at the caller's next synchronisation.
+appd_status tcf_lookup_async(appd_ctx* c, TcState* st, const int* comp, u64* compbest) {
+  APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
+  appd_status s = launch_cache_lookup(c, (int)st->cache_r0, (int)st->cache_r1, st->topk, (int)st->n, st->ckey, st->cj,
+                                      st->ccnt, comp, compbest, st->need, st->counters + 3, st->rows_list);
+  if (s) return s;
+  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, st->counters + 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               c->stream));
+  st->lookup_pending = true;
+  return APPD_OK;
+}
+
 // One Boruvka round's scan: compbest[comp] = min over the component's rows of the exact
 // edge key.  With the candidate cache (st->topk > 0): round 0 builds the cache on the
 // tensor cores (32-column maxima) and takes every row's minimum from it; later rounds
@@ -653,13 +667,11 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   c->pinned_small[8] = 0;
   unsigned rescan_rows = 0;
   if (cache && round > 0) {
-    APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
-    if ((s = launch_cache_lookup(c, (int)st->cache_r0, (int)st->cache_r1, st->topk, (int)n, st->ckey, st->cj,
-                                 st->ccnt, comp, compbest, st->need, st->counters + 3, st->rows_list)))
-      return s;
-    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, st->counters + 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                 c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (!st->lookup_pending) {
+      if ((s = tcf_lookup_async(c, st, comp, compbest))) return s;
+      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    st->lookup_pending = false;  // the caller synchronised after queueing it
     rescan_rows = c->pinned_small[9];
     st->last_rescan_rows = rescan_rows;
     if (rescan_rows == 0) return APPD_OK;  // every component decided by the cache
@@ -839,71 +851,12 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.WCM = WCM;
   C.upper = P.upper;
   if ((s = launch_cm_rowub(c, C))) return s;
-  // Listing thresholds.  CUB[C][D] bounds the exact minimum w(C, D) from above (both
-  // directions bound the same w).  A contracted MST edge (C, D) also satisfies
-  // w(C, D) <= the largest bound on the path from C to D in the MST of the bounds
-  // (cut property), so T = min(sym bound, path maximum) keeps every MST edge's minimum
-  // pair listed; pairs above T are not MST edges and may come out inflated.
-  {
-    std::vector<unsigned> ub((size_t)(k * k));
-    APPD_CUDA(c, cudaMemcpyAsync(ub.data(), CUB, sizeof(unsigned) * k * k, cudaMemcpyDeviceToHost, c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-    std::vector<float> sym((size_t)(k * k));
-    for (int64_t a = 0; a < k; a++)
-      for (int64_t b = 0; b < k; b++) {
-        float x, y;
-        memcpy(&x, &ub[a * k + b], 4);
-        memcpy(&y, &ub[b * k + a], 4);
-        sym[a * k + b] = std::min(x, y);
-      }
-    // Prim on the bounds, then the path maximum from every node (k <= 128)
-    std::vector<int> par((size_t)k, -1);
-    std::vector<float> key((size_t)k, INFINITY);
-    std::vector<char> in((size_t)k, 0);
-    key[0] = 0.0f;
-    for (int64_t it = 0; it < k; it++) {
-      int64_t b = -1;
-      for (int64_t q = 0; q < k; q++)
-        if (!in[q] && (b < 0 || key[q] < key[b])) b = q;
-      in[b] = 1;
-      for (int64_t q = 0; q < k; q++)
-        if (!in[q] && sym[b * k + q] < key[q]) {
-          key[q] = sym[b * k + q];
-          par[q] = (int)b;
-        }
-    }
-    std::vector<std::vector<std::pair<int, float>>> adj((size_t)k);
-    for (int64_t q = 1; q < k; q++)
-      if (par[q] >= 0) {
-        adj[q].push_back({par[q], key[q]});
-        adj[par[q]].push_back({(int)q, key[q]});
-      }
-    std::vector<unsigned> T((size_t)(k * k));
-    std::vector<float> pm((size_t)k);
-    std::vector<int> stack;
-    for (int64_t r = 0; r < k; r++) {
-      std::fill(pm.begin(), pm.end(), -1.0f);
-      pm[r] = 0.0f;
-      stack.assign(1, (int)r);
-      while (!stack.empty()) {
-        const int x = stack.back();
-        stack.pop_back();
-        for (auto& e : adj[x])
-          if (pm[e.first] < 0.0f) {
-            pm[e.first] = std::max(pm[x], e.second);
-            stack.push_back(e.first);
-          }
-      }
-      for (int64_t q = 0; q < k; q++) {
-        // unreachable (no bound anywhere): stay permissive
-        const float t = pm[q] < 0.0f ? sym[r * k + q] : std::min(sym[r * k + q], pm[q]);
-        memcpy(&T[r * k + q], &t, 4);
-      }
-    }
-    APPD_CUDA(c, cudaMemcpyAsync(CUB, T.data(), sizeof(unsigned) * k * k, cudaMemcpyHostToDevice, c->stream));
-    if ((s = launch_cm_filter(c, C))) return s;
-    if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;  // synchronises
-  }
+  // listing thresholds on the device (bound MST + path maxima, k_cache.cu)
+  unsigned* T = CUB + 128 * 128;
+  if ((s = launch_cm_thresholds(c, CUB, (int)k, T))) return s;
+  C.CUB = T;
+  if ((s = launch_cm_filter(c, C))) return s;
+  if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;  // synchronises
   if (st->last_list_entries > st->list_entries_cap) *listed_overflow = true;
   return APPD_OK;
 }

@@ -114,6 +114,7 @@ struct CmParams {
 };
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P);
 appd_status launch_cm_filter(appd_ctx* c, const CmParams& P);
+appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T);
 
 struct ListParams {
   const unsigned* list;   // (chunk << 17 | row), sorted ascending
