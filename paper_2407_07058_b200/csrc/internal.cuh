@@ -214,11 +214,13 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
     if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
   } while (0)
 
-#define APPD_LAUNCHED(c)                                                     \
-  do {                                                                       \
-    (c)->launches++;                                                         \
-    cudaError_t _e = cudaGetLastError();                                     \
-    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, "kernel launch");  \
+#define APPD_STR2(x) #x
+#define APPD_STR(x) APPD_STR2(x)
+#define APPD_LAUNCHED(c)                                                                        \
+  do {                                                                                          \
+    (c)->launches++;                                                                            \
+    cudaError_t _e = cudaGetLastError();                                                        \
+    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, "kernel launch " __FILE__ ":" APPD_STR(__LINE__)); \
   } while (0)
 
 // ---- kernels (k_*.cu) ----

@@ -55,31 +55,41 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
 // maxima give a running threshold; every chunk passing it is buffered (the threshold only
 // tightens as the K-th largest grows, so the buffer holds every chunk that passes the
 // final threshold thrK).  At the end UBK is stored and the buffered chunks passing thrK
-// are listed.  A row whose buffer overflows re-reads its TM32 row once.
+// are listed.  A row whose buffer overflows re-reads its TM32 row once; a row whose list
+// entries do not fit is poisoned (cand_cnt = 2^31: invalid cache, exact full-row minimum).
 template <int K>
 __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
                             const float* __restrict__ nrm, const float* __restrict__ len, float maxlen, ErrModel em,
                             float* __restrict__ UBK, u64* __restrict__ rowbuf, int rbcap, unsigned* __restrict__ list,
                             unsigned* __restrict__ count, unsigned cap, unsigned* __restrict__ cand_cnt) {
   const int lane = threadIdx.x & 31;
-  constexpr int U = 32;
+  constexpr int U4 = 8;  // 8 x 128-bit loads = 32 chunk maxima per batch
   for (int p0 = p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < p_end; p0 += gridDim.x * blockDim.x) {
     const int p = p0 + lane;
     const bool valid = p < p_end;
     const float ni = valid ? nrm[p] : 0.0f, li = valid ? len[p] : 0.0f;
+    // running K largest chunk maxima (K distinct chunks, hence K distinct columns)
     float top[K];
 #pragma unroll
     for (int t = 0; t < K; t++) top[t] = -INFINITY;
     float thr = -INFINITY;
     int nb = 0;
     u64* buf = rowbuf + (int64_t)(valid ? p : 0) * rbcap;
-    for (int c0 = 0; c0 < nch; c0 += U) {
-      float v[U];
+    const float4* row4 = reinterpret_cast<const float4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
+    for (int c0 = 0; c0 < nch; c0 += 4 * U4) {
+      float v[4 * U4];
 #pragma unroll
-      for (int u = 0; u < U; u++) v[u] = (valid && c0 + u < nch) ? __ldcs(TM32 + tm_index(c0 + u, p, nch)) : -INFINITY;
+      for (int u = 0; u < U4; u++) {
+        float4 x = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (valid && c0 + 4 * u < nch) x = __ldcs(row4 + (int64_t)((c0 >> 2) + u) * 512);
+        v[4 * u] = x.x;
+        v[4 * u + 1] = x.y;
+        v[4 * u + 2] = x.z;
+        v[4 * u + 3] = x.w;
+      }
       const float kth0 = top[K - 1];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
+      for (int u = 0; u < 4 * U4; u++) {
         if (v[u] > top[K - 1]) {  // branch-free insertion into the descending list
           float x = v[u];
 #pragma unroll
@@ -92,9 +102,16 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
       }
       if (top[K - 1] != kth0 && top[K - 1] > -INFINITY)
         thr = em_thr(em, em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen), ni, li, maxlen);
+      float bm = v[0];
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (v[u] >= thr && v[u] > -INFINITY) {
+      for (int u = 1; u < 4 * U4; u++) bm = fmaxf(bm, v[u]);
+      if (bm >= thr && bm > -INFINITY) {
+        unsigned mask = 0;
+#pragma unroll
+        for (int u = 0; u < 4 * U4; u++) mask |= (v[u] >= thr && v[u] > -INFINITY) ? (1u << u) : 0u;
+        while (mask) {
+          const int u = __ffs(mask) - 1;
+          mask &= mask - 1;
           if (nb < rbcap) buf[nb] = ((u64)(unsigned)(c0 + u) << 32) | __float_as_uint(v[u]);
           nb++;
         }
@@ -115,7 +132,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
       for (int j = 0; j < nb; j++) mine += __uint_as_float((unsigned)buf[j]) >= thr;
     } else if (valid) {
       for (int c = 0; c < nch; c++) {
-        const float v = TM32[tm_index(c, p, nch)];
+        const float v = TM32[tm32_index(c, p, nch)];
         mine += v >= thr && v > -INFINITY;
       }
     }
@@ -132,7 +149,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
       }
     } else if (valid) {
       for (int c = 0; c < nch; c++) {
-        const float v = TM32[tm_index(c, p, nch)];
+        const float v = TM32[tm32_index(c, p, nch)];
         if (v >= thr && v > -INFINITY) {
           if (slot < cap) list[slot] = ((unsigned)c << LIST_SHIFT) | (unsigned)p;
           else lost = true;
@@ -140,7 +157,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
         }
       }
     }
-    if (lost) cand_cnt[p] = 0xFFFFFFFFu;
+    if (lost) cand_cnt[p] = 0x80000000u;  // poisoned: later appends cannot wrap it back below the cap
   }
 }
 
@@ -292,7 +309,7 @@ __global__ void __launch_bounds__(256) k_list_exact(ListParams L) {
           for (int b = 0; b < 4; b++) {
             if (oq[b] >= 0 && oq[b] != op && (double)acc[a][b] * L.s2 <= ubk) {
               const unsigned slot = atomicAdd(L.cnt + p, 1u);
-              if ((int)slot < L.ccap)
+              if (slot < (unsigned)L.ccap)
                 L.cand[(int64_t)p * L.ccap + slot] =
                     ((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(op, oq[b]);
             }

@@ -94,7 +94,7 @@ __global__ void k_lift0(const int* __restrict__ parent, const int* __restrict__ 
 }
 // record parent of v: its nearest ancestor with a larger val; sort key (rpar, val)
 __global__ void k_record_parent(const int* __restrict__ jump, const int* __restrict__ mx, int levels, int n,
-                                const int* __restrict__ parent, const int* __restrict__ val, int root,
+                                const int* __restrict__ parent, const int* __restrict__ val, int root, int sh,
                                 unsigned long long* __restrict__ key) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     if (v == root) continue;
@@ -105,31 +105,33 @@ __global__ void k_record_parent(const int* __restrict__ jump, const int* __restr
       if (mx[o] < w) cur = jump[o];
     }
     const int rp = parent[cur];
-    key[w] = ((unsigned long long)(unsigned)rp << 32) | (unsigned)w;  // one entry per edge rank
+    key[w] = ((unsigned long long)(unsigned)rp << sh) | (unsigned)w;  // one entry per edge rank
   }
 }
 
 // record-tree Euler tour over the sorted children S[i] = (rpar, val): arcs 2i (down
 // into child i) and 2i+1 (back up); first child of x and the S index of each vertex
-__global__ void k_rt_index(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+__global__ void k_rt_index(const unsigned long long* __restrict__ S, int m, int sh, const int* __restrict__ child_of,
                            int* __restrict__ first, int* __restrict__ sidx) {
+  const unsigned long long lo = (1ull << sh) - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const int rp = (int)(S[i] >> 32);
-    const int v = child_of[(int)(S[i] & 0xffffffffu)];
+    const int rp = (int)(S[i] >> sh);
+    const int v = child_of[(int)(S[i] & lo)];
     sidx[v] = i;
-    if (i == 0 || (int)(S[i - 1] >> 32) != rp) first[rp] = i;
+    if (i == 0 || (int)(S[i - 1] >> sh) != rp) first[rp] = i;
   }
 }
-__global__ void k_rt_succ(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+__global__ void k_rt_succ(const unsigned long long* __restrict__ S, int m, int sh, const int* __restrict__ child_of,
                           const int* __restrict__ first, const int* __restrict__ sidx, int root,
                           int* __restrict__ succ, int* __restrict__ rank) {
+  const unsigned long long lo = (1ull << sh) - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const int rp = (int)(S[i] >> 32);
-    const int v = child_of[(int)(S[i] & 0xffffffffu)];
+    const int rp = (int)(S[i] >> sh);
+    const int v = child_of[(int)(S[i] & lo)];
     const int fc = first[v];
     const int sd = fc >= 0 ? 2 * fc : 2 * i + 1;  // into the first child, else straight back up
     int su;
-    if (i + 1 < m && (int)(S[i + 1] >> 32) == rp) su = 2 * (i + 1);  // next sibling
+    if (i + 1 < m && (int)(S[i + 1] >> sh) == rp) su = 2 * (i + 1);  // next sibling
     else su = rp == root ? -1 : 2 * sidx[rp] + 1;                    // up from the parent
     succ[2 * i] = sd;
     succ[2 * i + 1] = su;
@@ -143,11 +145,11 @@ __global__ void k_down_flags(const int* __restrict__ rank, int m, int* __restric
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
     flag[2 * m - 1 - rank[2 * i]] = 1;
 }
-__global__ void k_emit(const unsigned long long* __restrict__ S, int m, const int* __restrict__ child_of,
+__global__ void k_emit(const unsigned long long* __restrict__ S, int m, int sh, const int* __restrict__ child_of,
                        const int* __restrict__ rank, const int* __restrict__ downs_before,
                        const float* __restrict__ ew, int root, int32_t* __restrict__ pi, float* __restrict__ h) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const int e = (int)(S[i] & 0xffffffffu);
+    const int e = (int)(S[i] & ((1ull << sh) - 1));
     const int v = child_of[e];
     const int pre = 1 + downs_before[2 * m - 1 - rank[2 * i]];
     pi[pre] = v;
@@ -266,7 +268,9 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   // A: adjacency
   k_arcs<<<gL, 256, 0, c->stream>>>(eu, ev, m, src, arc);
   APPD_LAUNCHED(c);
-  if ((s = sort_pairs_i32(c, src, ssrc, arc, sarc, L))) return s;
+  int sh = 1;
+  while ((1 << sh) < n) sh++;
+  if ((s = sort_pairs_i32_bits(c, src, ssrc, arc, sarc, L, sh))) return s;
   k_adj<<<gL, 256, 0, c->stream>>>(ssrc, sarc, L, start, end, posarc);
   APPD_LAUNCHED(c);
   // B, C: Euler tour of the MST from the root, tour ranks
@@ -289,14 +293,14 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_lift_coop, grid, 256, args, 0, c->stream));
     c->launches++;
   }
-  k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, key);
+  k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, sh, key);
   APPD_LAUNCHED(c);
   // E: record tree, children ascending by val
-  if ((s = sort_keys_u64(c, key, S, m))) return s;
+  if ((s = sort_keys_u64_bits64(c, key, S, m, 0, 2 * sh))) return s;
   APPD_CUDA(c, cudaMemsetAsync(first, 0xFF, sizeof(int) * n, c->stream));
-  k_rt_index<<<gn, 256, 0, c->stream>>>(S, m, child_of, first, sidx);
+  k_rt_index<<<gn, 256, 0, c->stream>>>(S, m, sh, child_of, first, sidx);
   APPD_LAUNCHED(c);
-  k_rt_succ<<<gn, 256, 0, c->stream>>>(S, m, child_of, first, sidx, root, succ0, rank0);
+  k_rt_succ<<<gn, 256, 0, c->stream>>>(S, m, sh, child_of, first, sidx, root, succ0, rank0);
   APPD_LAUNCHED(c);
   if ((s = list_rank(c, L, succ0, rank0, succ1, rank1, active, &rk))) return s;
   APPD_CUDA(c, cudaMemsetAsync(flag, 0, sizeof(int) * (L + 1), c->stream));
@@ -304,7 +308,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   APPD_LAUNCHED(c);
   if ((s = exclusive_scan_i32(c, flag, downs, L))) return s;
   // F: outputs
-  k_emit<<<gn, 256, 0, c->stream>>>(S, m, child_of, rk, downs, ew, root, pi, h);
+  k_emit<<<gn, 256, 0, c->stream>>>(S, m, sh, child_of, rk, downs, ew, root, pi, h);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -474,7 +474,11 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->thrK = (float*)ws(c, S_TC_THRK, sizeof(float) * st->npad);
     st->cand_cnt = (unsigned*)ws(c, S_TC_CANDCNT, sizeof(unsigned) * (st->npad + 8));
     st->cand = (u64*)ws(c, S_TC_CANDK, sizeof(u64) * st->npad * st->cap);
-    st->list_entries_cap = (unsigned)std::min<int64_t>(32 * n + 65536, (int64_t)1 << 31);
+    // every (row, chunk) pair when that is small (tiny n lists everything), else 32 per row
+    const int64_t all_pairs = n * ((n + 31) / 32);
+    st->list_entries_cap =
+        (unsigned)std::min<int64_t>(std::max<int64_t>(32 * n + 65536, all_pairs <= (4 << 20) ? all_pairs : 0),
+                                    (int64_t)1 << 31);
     st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
     st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
     if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");

@@ -307,16 +307,20 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
           // warp-uniform fast path: valid rows whose component misses these real columns
           const bool fast =
               __all_sync(0xffffffffu, valid && (h0 + WCOLS <= cs[r] || h0 >= ce[r]) && h0 + WCOLS <= P.n);
-          if (SEG32) {
-            // 32-column maxima (the same FMNMX3 count as one tree over the segment)
+          if constexpr (SEG32) {
+            // 32-column maxima (the same FMNMX3 count as one tree over the segment); the
+            // warp's two chunks are adjacent in the packed table: one 8-byte store
+            static_assert(WCOLS == 64, "32-column pass: two chunks per epilogue warp");
+            float cm[2];
 #pragma unroll
-            for (int c = 0; c < WCOLS / 32; c++) {
+            for (int c = 0; c < 2; c++) {
               float w[32];
 #pragma unroll
               for (int t = 0; t < 32; t++) w[t] = v[c * 32 + t];
-              const float cm = chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, fast, P.n);
-              if (valid) P.TM[tm_index(h0 / 32 + c, p, P.tm_nseg)] = cm;
+              cm[c] = chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, fast, P.n);
             }
+            if (valid)
+              *reinterpret_cast<float2*>(P.TM + tm32_index(h0 / 32, p, P.tm_nseg)) = make_float2(cm[0], cm[1]);
           } else {
             float m;
             if (fast) {

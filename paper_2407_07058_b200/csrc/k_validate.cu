@@ -81,17 +81,33 @@ appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int6
   return APPD_OK;
 }
 
+// first non-finite coordinate (row-major element index); 16-byte loads when aligned
 __global__ void k_validate_points(const float* __restrict__ X, int64_t total, u64* __restrict__ out3) {
   u64 bad = KEY_NONE;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
-    if (!isfinite(X[e])) bad = min(bad, (u64)e);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const int64_t t4 = total >> 2;
+    for (int64_t e = tid; e < t4; e += stride) {
+      const float4 v = __ldcs(X4 + e);
+      if (!isfinite(v.x)) bad = min(bad, (u64)(4 * e));
+      else if (!isfinite(v.y)) bad = min(bad, (u64)(4 * e + 1));
+      else if (!isfinite(v.z)) bad = min(bad, (u64)(4 * e + 2));
+      else if (!isfinite(v.w)) bad = min(bad, (u64)(4 * e + 3));
+    }
+    for (int64_t e = (t4 << 2) + tid; e < total; e += stride)
+      if (!isfinite(X[e])) bad = min(bad, (u64)e);
+  } else {
+    for (int64_t e = tid; e < total; e += stride)
+      if (!isfinite(X[e])) bad = min(bad, (u64)e);
+  }
   if (bad != KEY_NONE) atomicMin(out3, bad);
 }
 
 appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64_t d, u64* out3) {
   int64_t total = n * d;
-  int grid = (int)((total + 255) / 256);
-  if (grid > c->sm_count * 8) grid = c->sm_count * 8;
+  int grid = (int)((total / 4 + 255) / 256);
+  if (grid > c->sm_count * 16) grid = c->sm_count * 16;
   if (grid < 1) grid = 1;
   k_validate_points<<<grid, 256, 0, c->stream>>>(X, total, out3);
   APPD_LAUNCHED(c);

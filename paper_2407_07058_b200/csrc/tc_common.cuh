@@ -56,6 +56,13 @@ __host__ __device__ __forceinline__ int64_t tm_index(int s, int p, int nseg) {
   return (int64_t)(p >> 9) * nseg * 512 + (int64_t)s * 512 + (p & 511);
 }
 
+// The 32-column table additionally packs 4 consecutive chunks of a row together
+// (16 bytes), so a reader loads 4 chunk maxima per 128-bit access:
+//   (p / 512) * nch * 512 + (c / 4) * 2048 + (p % 512) * 4 + c % 4     (nch % 4 == 0)
+__host__ __device__ __forceinline__ int64_t tm32_index(int c, int p, int nch) {
+  return (int64_t)(p >> 9) * nch * 512 + (int64_t)(c >> 2) * 2048 + (p & 511) * 4 + (c & 3);
+}
+
 struct TcParams {
   const __half* YA;          // row operand granules (128 points x K, core-matrix layout)
   const __half* YB;          // column operand granules
