@@ -479,6 +479,8 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->list_entries_cap =
         (unsigned)std::min<int64_t>(std::max<int64_t>(32 * n + 65536, all_pairs <= (4 << 20) ? all_pairs : 0),
                                     (int64_t)1 << 31);
+    if (const char* t = getenv("APPD_TEST_LIST_CAP"))  // test hook: force list overflow (poisoned rows)
+      st->list_entries_cap = (unsigned)std::max(1, atoi(t));
     st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
     st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
     if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");

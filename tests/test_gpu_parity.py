@@ -197,6 +197,21 @@ def test_points_engine_paths_taken(P):
     c.close()
 
 
+def test_points_list_overflow_is_exact(P, monkeypatch):
+    """A candidate list far too small for the input: rows whose entries are lost are
+    poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the
+    result must not change."""
+    X = G.random_points(3000, 16, 901, "blobs")
+    ref = oracle.appd_points(X)
+    monkeypatch.setenv("APPD_TEST_LIST_CAP", "5000")
+    c = P.Context(timing=True)
+    try:
+        assert_bit_equal(gpu_points(c, X), ref, "list overflow")
+        assert c.stats()["cache_invalid_rows"] > 0
+    finally:
+        c.close()
+
+
 def _check_golden(M_rows_fn, cfg, name):
     path = os.path.join(GOLD, name)
     if not os.path.exists(path):
