@@ -403,13 +403,34 @@ __global__ void k_topk_select(int p_begin, int p_end, int n, int K, const unsign
       }
       continue;
     }
+    const int take = min((int)c, K);
+    if (cap <= 32) {
+      // one key per lane: bitonic sort across the warp, lanes 0 .. take-1 hold the answer
+      u64 x = lane < (int)c ? cand[(int64_t)p * cap + lane] : KEY_NONE;
+#pragma unroll
+      for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          const u64 y = __shfl_xor_sync(0xffffffffu, x, stride);
+          const bool up = (lane & size) == 0;  // ascending block
+          const bool lower = (lane & stride) == 0;
+          const u64 lo = x < y ? x : y, hi = x < y ? y : x;
+          x = (lower == up) ? lo : hi;
+        }
+      if (lane < take) {
+        ckey[(int64_t)p * K + lane] = x;
+        cj[(int64_t)p * K + lane] = other_end(x & ((1ull << 33) - 1), p);
+        if (lane == 0) compbest[p] = x;
+      }
+      if (lane == 0) ccnt[p] = take;
+      continue;
+    }
     u64 mine[4];  // cap <= 128
 #pragma unroll
     for (int u = 0; u < 4; u++) {
       const int e = lane + 32 * u;
       mine[u] = e < (int)c ? cand[(int64_t)p * cap + e] : KEY_NONE;
     }
-    const int take = min((int)c, K);
     for (int t = 0; t < take; t++) {
       u64 lm = mine[0];
 #pragma unroll
@@ -549,23 +570,33 @@ __global__ void __launch_bounds__(256) k_rows_exact(const float* __restrict__ XT
 #pragma unroll
       for (int u = 0; u < 4; u++) acc[r][u] = 0.0f;
     const int jb = blk * RE_COLS + threadIdx.x;
-    for (int k = 0; k < d; k++) {
-      float y[4];
+    // 8 coordinates' column values loaded ahead of their use (L2 latency), then the
+    // R1 chain in order k = 0, 1, ... (XT is zero padded beyond n: no column guard needed
+    // for the loads, only for the keys)
+    constexpr int KB = 8;
+    for (int k0 = 0; k0 < d; k0 += KB) {
+      float y[KB][4];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int j = jb + u * 256;
-        y[u] = j < n ? __ldg(XT + (int64_t)k * ldx + j) : 0.0f;
-      }
-      const float4 xa = *reinterpret_cast<const float4*>(xr + k * RE_R);
-      const float4 xb = *reinterpret_cast<const float4*>(xr + k * RE_R + 4);
-      const float xv[RE_R] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-      for (int r = 0; r < RE_R; r++)
+      for (int kk = 0; kk < KB; kk++)
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-          const float t = __fsub_rn(xv[r], y[u]);
-          acc[r][u] = __fmaf_rn(t, t, acc[r][u]);
+          const int j = jb + u * 256;
+          y[kk][u] = (k0 + kk < d && j < ldx) ? __ldg(XT + (int64_t)(k0 + kk) * ldx + j) : 0.0f;
         }
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) {
+        if (k0 + kk >= d) break;
+        const float4 xa = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R);
+        const float4 xb = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R + 4);
+        const float xv[RE_R] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+        for (int r = 0; r < RE_R; r++)
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const float t = __fsub_rn(xv[r], y[kk][u]);
+            acc[r][u] = __fmaf_rn(t, t, acc[r][u]);
+          }
+      }
     }
 #pragma unroll
     for (int r = 0; r < RE_R; r++) {
@@ -693,8 +724,20 @@ appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, doubl
 // k <= 128 nodes) plus the edges of the earlier rounds is the MST.
 // ===========================================================================
 
+// per 128-column segment: (first, last) component label of its real columns
+__global__ void k_seg_comp(const int* __restrict__ sc, int n, int nseg, int2* __restrict__ segd) {
+  for (int sg = blockIdx.x * blockDim.x + threadIdx.x; sg < nseg; sg += gridDim.x * blockDim.x) {
+    const int q0 = sg * TC_TMG;
+    segd[sg] = q0 < n ? make_int2(sc[q0], sc[min(q0 + TC_TMG - 1, n - 1)]) : make_int2(-1, -1);
+  }
+}
+
+// segments are sorted by component: stream each row's stored maxima in order (16 loads
+// in flight), keep the running maximum of the current component's full segments and
+// flush its bound when the component changes
 __global__ void k_cm_rowub(CmParams P) {
   const int lane = threadIdx.x & 31;
+  const int nseg_n = P.n / TC_TMG;  // full segments only (a partial last segment bounds nothing)
   for (int p0 = P.p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < P.p_end;
        p0 += gridDim.x * blockDim.x) {
     const int p = p0 + lane;
@@ -702,21 +745,42 @@ __global__ void k_cm_rowub(CmParams P) {
     const int C = valid ? P.sc[p] : -1;
     const bool uni = __all_sync(0xffffffffu, C == __shfl_sync(0xffffffffu, C, 0));
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
-    const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;  // segments the (symmetric) scan wrote for these rows
-    for (int D = 0; D < P.k; D++) {
-      const int s0 = max(smin, (P.cstart[D] + TC_TMG - 1) / TC_TMG), s1 = P.cend[D] / TC_TMG;  // segments inside D
-      float m = -INFINITY;
-      if (valid && D != C)
-        for (int s = s0; s < s1; s++) m = fmaxf(m, __ldcs(P.TM + tm_index(s, p, P.nseg)));
-      float ub = m > -INFINITY ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen) : INFINITY;
-      if (uni) {
+    const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;  // segments the scan wrote
+    auto flush = [&](int D, float m) {
+      float ub = (m > -INFINITY && D != C && valid) ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen) : INFINITY;
+      if (uni) {  // D is warp-uniform (segment order is the same for every lane)
 #pragma unroll
         for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
-        if (lane == 0 && C >= 0 && ub < INFINITY) atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
-      } else if (valid && ub < INFINITY) {
+        if (lane == 0 && C >= 0 && ub < INFINITY)
+          atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
+      } else if (ub < INFINITY) {
         atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
       }
+    };
+    int curD = -1;
+    float m = -INFINITY;
+    constexpr int U = 16;
+    for (int s0 = smin; s0 < nseg_n; s0 += U) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        v[u] = (valid && s0 + u < nseg_n) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int s = s0 + u;
+        if (s >= nseg_n) break;
+        const int2 dd = P.segd[s];
+        const int D0 = dd.x, D1 = dd.y;
+        if (D0 != D1) continue;  // straddling segment: bounds neither component alone
+        if (D0 != curD) {
+          if (curD >= 0) flush(curD, m);
+          curD = D0;
+          m = -INFINITY;
+        }
+        m = fmaxf(m, v[u]);
+      }
     }
+    if (curD >= 0) flush(curD, m);
   }
 }
 
@@ -743,8 +807,8 @@ __global__ void k_cm_filter(CmParams P) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         if (!(v[u] > -INFINITY)) continue;
-        const int q0 = (s0 + u) * TC_TMG;
-        const int D0 = __ldg(P.sc + q0), D1 = __ldg(P.sc + min(q0 + TC_TMG - 1, P.n - 1));
+        const int2 dd = P.segd[s0 + u];
+        const int D0 = dd.x, D1 = dd.y;
         float thr;
         if (D0 == D1) {
           if (D0 != cachedD) {
@@ -780,75 +844,67 @@ __global__ void k_cm_filter(CmParams P) {
 // Contracted-graph steps of the component-matrix finish, one CTA (k <= 128 nodes, one
 // thread per node).  Both are Prim's algorithm on a dense k x k matrix.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void block_argmin_f(float v, int idx, float* sv, int* si, float& out_v, int& out_i) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-    if (ov < v || (ov == v && oi < idx)) { v = ov; idx = oi; }
-  }
-  if (lane == 0) { sv[w] = v; si[w] = idx; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float bv = sv[0];
-    int bi = si[0];
-    for (int t = 1; t < (int)(blockDim.x >> 5); t++)
-      if (sv[t] < bv || (sv[t] == bv && si[t] < bi)) { bv = sv[t]; bi = si[t]; }
-    sv[0] = bv;
-    si[0] = bi;
-  }
-  __syncthreads();
-  out_v = sv[0];
-  out_i = si[0];
-  __syncthreads();
-}
-
 // Listing thresholds.  CUB[C][D] bounds w(C, D) from above (both directions bound the
 // same w).  An MST edge (C, D) of the contracted graph satisfies w(C, D) <= the largest
 // bound on the path from C to D in the MST of the bounds (cut property), so
 // T = min(symmetric bound, path maximum) keeps every MST edge's minimum pair listed;
 // pairs above T are not MST edges and may come out inflated.  Output T (k x k).
-__global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
+__global__ void __launch_bounds__(256) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
                                                        unsigned* __restrict__ T) {
+  extern __shared__ float symb[];  // [k][k] symmetric bounds
   __shared__ int par[128];
   __shared__ float pw[128];
   __shared__ int cstart[129], kids[128];
-  __shared__ float sv[4];
-  __shared__ int si[4];
-  const int q = threadIdx.x;
-  auto bound = [&](int a, int b) -> float {
-    return fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
-  };
-  // Prim from node 0 on the symmetric bounds
-  bool in = q == 0;
-  float key = (q < k && q > 0) ? bound(0, q) : INFINITY;
-  int from = 0;
-  if (q < k) {
-    par[q] = -1;
-    pw[q] = 0.0f;
+  const int lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
+    const int a = e / k, b = e % k;
+    symb[e] = fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
   }
   __syncthreads();
+  if (threadIdx.x < 32) {
+  // Prim from node 0, one warp: lane owns nodes lane, lane + 32, ... (k <= 128)
+  float key[4];
+  int from[4];
+  bool in[4];
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int q = lane + 32 * t;
+    in[t] = q == 0 || q >= k;
+    key[t] = (q < k && q > 0) ? symb[q] : INFINITY;
+    from[t] = 0;
+    if (q < k) { par[q] = -1; pw[q] = 0.0f; }
+  }
   for (int step = 1; step < k; step++) {
-    float bv;
-    int bi;
-    block_argmin_f((q < k && !in) ? key : INFINITY, q, sv, si, bv, bi);
-    if (q == bi) {
-      in = true;
-      par[q] = from;
-      pw[q] = key;
+    float bv = INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+      if (!in[t] && (key[t] < bv || (key[t] == bv && lane + 32 * t < bi))) { bv = key[t]; bi = lane + 32 * t; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if (q < k && !in) {
-      const float w = bound(bi, q);
-      if (w < key) {
-        key = w;
-        from = bi;
+    if ((bi & 31) == lane) {
+      const int t = bi >> 5;
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (u == t) { in[u] = true; par[bi] = from[u]; pw[bi] = key[u]; }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int q = lane + 32 * t;
+      if (!in[t]) {
+        const float w = symb[bi * k + q];
+        if (w < key[t]) { key[t] = w; from[t] = bi; }
       }
     }
   }
+  }  // warp 0
   __syncthreads();
   // children lists (CSR) of the tree rooted at 0
-  if (q == 0) {
+  if (threadIdx.x == 0) {
     for (int t = 0; t <= k; t++) cstart[t] = 0;
     for (int t = 1; t < k; t++) cstart[par[t] + 1]++;
     for (int t = 0; t < k; t++) cstart[t + 1] += cstart[t];
@@ -857,87 +913,108 @@ __global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restric
     for (int t = 1; t < k; t++) kids[fill[par[t]]++] = t;
   }
   __syncthreads();
-  if (q >= k) return;
-  // path maxima from root q: DFS over parent + children
-  float pm[128];
-  int stack[128];
-  for (int t = 0; t < k; t++) pm[t] = -1.0f;
-  pm[q] = 0.0f;
-  int sp = 0;
-  stack[sp++] = q;
-  while (sp) {
-    const int x = stack[--sp];
-    const int pp = par[x];
-    if (pp >= 0 && pm[pp] < 0.0f) {
-      pm[pp] = fmaxf(pm[x], pw[x]);
-      stack[sp++] = pp;
-    }
-    for (int e = cstart[x]; e < cstart[x + 1]; e++) {
-      const int y = kids[e];
-      if (pm[y] < 0.0f) {
-        pm[y] = fmaxf(pm[x], pw[y]);
-        stack[sp++] = y;
+  // path maxima from every root r (one thread per root): DFS over parent + children
+  for (int r = threadIdx.x; r < k; r += blockDim.x) {
+    float pm[128];
+    int stack[128];
+    for (int t = 0; t < k; t++) pm[t] = -1.0f;
+    pm[r] = 0.0f;
+    int sp = 0;
+    stack[sp++] = r;
+    while (sp) {
+      const int x = stack[--sp];
+      const int pp = par[x];
+      if (pp >= 0 && pm[pp] < 0.0f) {
+        pm[pp] = fmaxf(pm[x], pw[x]);
+        stack[sp++] = pp;
+      }
+      for (int e = cstart[x]; e < cstart[x + 1]; e++) {
+        const int y = kids[e];
+        if (pm[y] < 0.0f) {
+          pm[y] = fmaxf(pm[x], pw[y]);
+          stack[sp++] = y;
+        }
       }
     }
-  }
-  for (int t = 0; t < k; t++) {
-    const float b = bound(q, t);
-    T[(int64_t)q * k + t] = __float_as_uint(pm[t] < 0.0f ? b : fminf(b, pm[t]));
+    for (int t = 0; t < k; t++) {
+      const float b = symb[r * k + t];
+      T[(int64_t)r * k + t] = __float_as_uint(pm[t] < 0.0f ? b : fminf(b, pm[t]));
+    }
   }
 }
 
 // Final contracted MST: Prim on min(WCM[C][D], WCM[D][C]) (exact keys, a strict order),
 // the k - 1 edge keys appended to mstkeys at counters[0]
-__global__ void __launch_bounds__(128) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
+__global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
                                                  int* __restrict__ counters) {
-  __shared__ u64 sv[4];
-  __shared__ int si[4];
-  __shared__ int base;
-  const int q = threadIdx.x, lane = q & 31, w = q >> 5;
-  auto wk = [&](int a, int b) -> u64 {
+  extern __shared__ u64 wsym[];  // [k][k] symmetric minima
+  const int lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
+    const int a = e / k, b = e % k;
     const u64 x = WCM[(int64_t)a * k + b], y = WCM[(int64_t)b * k + a];
-    return x < y ? x : y;
-  };
-  bool in = q == 0;
-  u64 key = (q < k && q > 0) ? wk(0, q) : KEY_NONE;
-  if (q == 0) base = counters[0];
+    wsym[e] = x < y ? x : y;
+  }
   __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int base = counters[0];
+  u64 key[4];
+  bool in[4];
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int q = lane + 32 * t;
+    in[t] = q == 0 || q >= k;
+    key[t] = (q < k && q > 0) ? wsym[q] : KEY_NONE;
+  }
+  int added = 0;
   for (int step = 1; step < k; step++) {
-    u64 v = (q < k && !in) ? key : KEY_NONE;
-    int idx = (q < k && !in) ? q : 0x7fffffff;
+    u64 bv = KEY_NONE;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < 4; t++)
+      if (!in[t] && (key[t] < bv || (key[t] == bv && lane + 32 * t < bi))) { bv = key[t]; bi = lane + 32 * t; }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      const u64 ov = __shfl_xor_sync(0xffffffffu, v, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (ov < v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+      const u64 ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if (lane == 0) { sv[w] = v; si[w] = idx; }
-    __syncthreads();
-    u64 bv = sv[0];
-    int bi = si[0];
-    for (int t = 1; t < (int)(blockDim.x >> 5); t++)
-      if (sv[t] < bv || (sv[t] == bv && si[t] < bi)) { bv = sv[t]; bi = si[t]; }
-    __syncthreads();
     if (bv == KEY_NONE) break;  // disconnected: the edge-count check reports it
-    if (q == bi) {
-      in = true;
-      mstkeys[base + step - 1] = key;
+    if (lane == 0) mstkeys[base + step - 1] = bv;
+    added = step;
+    if ((bi & 31) == lane) {
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (u == (bi >> 5)) in[u] = true;
     }
-    if (q < k && !in) {
-      const u64 x = wk(bi, q);
-      if (x < key) key = x;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int q = lane + 32 * t;
+      if (!in[t]) {
+        const u64 x = wsym[bi * k + q];
+        if (x < key[t]) key[t] = x;
+      }
     }
-    if (q == 0) counters[0] = base + step;
   }
+  if (lane == 0) counters[0] = base + added;
 }
 
 appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T) {
-  k_cm_thresholds<<<1, 128, 0, c->stream>>>(CUB, k, T);
+  const size_t smem = sizeof(float) * k * k;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_thresholds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cm_thresholds<<<1, 256, smem, c->stream>>>(CUB, k, T);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
 appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters) {
-  k_cm_prim<<<1, 128, 0, c->stream>>>(WCM, k, mstkeys, counters);
+  const size_t smem = sizeof(u64) * k * k;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_prim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cm_prim<<<1, 256, smem, c->stream>>>(WCM, k, mstkeys, counters);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+appd_status launch_seg_comp(appd_ctx* c, const int* sc, int n, int nseg, int2* segd) {
+  k_seg_comp<<<(nseg + 255) / 256, 256, 0, c->stream>>>(sc, n, nseg, segd);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -856,6 +856,10 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.perm = st->perm;
   C.WCM = WCM;
   C.upper = P.upper;
+  int2* segd = (int2*)ws(c, S_TC_SEGD, sizeof(int2) * (C.nseg + 1));
+  if (!segd) return fail(c, APPD_ERR_OUT_OF_MEMORY, "segment descriptors");
+  if ((s = launch_seg_comp(c, st->sc, (int)n, C.nseg, segd))) return s;
+  C.segd = segd;
   if ((s = launch_cm_rowub(c, C))) return s;
   // listing thresholds on the device (bound MST + path maxima, k_cache.cu)
   unsigned* T = CUB + 128 * 128;

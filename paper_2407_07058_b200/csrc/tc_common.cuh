@@ -112,6 +112,7 @@ struct CmParams {
   unsigned* CUB;        // [k][k] float bits
   unsigned* list;       // (32-column chunk << 17 | row) entries
   int upper;            // TM holds only segments >= 4 (p / 512) of row p (symmetric pass)
+  const int2* segd;     // per segment: first and last component label of its real columns
   unsigned list_cap;
   unsigned* counters;   // [1] listed chunk entries
   const float* XTp;
@@ -121,6 +122,7 @@ struct CmParams {
 };
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P);
 appd_status launch_cm_filter(appd_ctx* c, const CmParams& P);
+appd_status launch_seg_comp(appd_ctx* c, const int* sc, int n, int nseg, int2* segd);
 appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T);
 
 struct ListParams {
