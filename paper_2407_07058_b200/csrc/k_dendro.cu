@@ -199,13 +199,16 @@ __global__ void k_lift_coop(int* __restrict__ jump, int* __restrict__ mx, int n,
   }
 }
 
+// one 1024-thread block per SM: the grid-wide barrier of every step is cheapest with
+// the fewest blocks, and 148 x 1024 threads cover the 2(n-1) arcs in a few strides
+constexpr int kCoopThreads = 1024;
 int coop_grid(appd_ctx* c, const void* fn) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0) != cudaSuccess || per_sm < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCoopThreads, 0) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     per_sm = 1;
   }
-  return per_sm * c->sm_count;
+  return c->sm_count;  // (per_sm >= 1 checked: co-residency is guaranteed)
 }
 
 appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, int* rank1, int* /*active*/,
@@ -213,9 +216,9 @@ appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, in
   int steps = 0;
   while ((1 << steps) < L) steps++;
   steps++;
-  const int grid = std::min(coop_grid(c, (const void*)k_rank_coop), (L + 255) / 256);
+  const int grid = std::min(coop_grid(c, (const void*)k_rank_coop), (L + kCoopThreads - 1) / kCoopThreads);
   void* args[] = {&succ0, &rank0, &succ1, &rank1, &L, &steps};
-  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_rank_coop, grid, 256, args, 0, c->stream));
+  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_rank_coop, grid, kCoopThreads, args, 0, c->stream));
   c->launches++;
   *out_rank = (steps & 1) ? rank1 : rank0;
   return APPD_OK;
@@ -288,9 +291,9 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   APPD_LAUNCHED(c);
   {
     int nn = n, lv = levels;
-    const int grid = std::min(coop_grid(c, (const void*)k_lift_coop), (n + 255) / 256);
+    const int grid = std::min(coop_grid(c, (const void*)k_lift_coop), (n + kCoopThreads - 1) / kCoopThreads);
     void* args[] = {&jump, &mx, &nn, &lv};
-    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_lift_coop, grid, 256, args, 0, c->stream));
+    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_lift_coop, grid, kCoopThreads, args, 0, c->stream));
     c->launches++;
   }
   k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, sh, key);

@@ -87,6 +87,9 @@ __device__ __forceinline__ float rmq(const float* __restrict__ ST, int64_t strid
 constexpr int FILL_THREADS = 256;
 constexpr int FILL_R = 128;  // rows per tile (consecutive in leaf order)
 
+// positions spanned by one tile whose in-tile range maxima come from shared memory
+constexpr int FILL_SPAN = 256, FILL_LV = 8;  // 2^FILL_LV >= FILL_SPAN
+
 template <int VEC, bool WIDEST>
 __global__ void __launch_bounds__(FILL_THREADS)
     k_fill(const int* __restrict__ rows_sorted, const int* __restrict__ rowpos, int64_t nrows,
@@ -95,6 +98,10 @@ __global__ void __launch_bounds__(FILL_THREADS)
   __shared__ float sS[FILL_R], sP[FILL_R];
   __shared__ int64_t sOff[FILL_R];
   __shared__ int sA[FILL_R];
+  // sparse table of h over the tile's position range [aL, aR): columns whose position
+  // lies inside it (the tile's own points, and other ranks' in between) need a direct
+  // range maximum per element; from shared memory when the span fits
+  __shared__ float sST[FILL_LV][FILL_SPAN];
   const float ID = WIDEST ? INFINITY : -INFINITY;
   const int64_t t0 = (int64_t)blockIdx.y * FILL_R;
   int R = (int)((nrows - t0) < FILL_R ? (nrows - t0) : FILL_R);
@@ -124,6 +131,18 @@ __global__ void __launch_bounds__(FILL_THREADS)
   }
   const bool warp_inside = __any_sync(0xffffffffu, any_inside);
   const bool in_range = jbase < n;
+  const int span = aR - aL;  // h[aL .. aR-1]
+  const bool local = span <= FILL_SPAN;
+  if (local) {
+    for (int i = threadIdx.x; i < span; i += FILL_THREADS) sST[0][i] = __ldg(ST + aL + i);
+    __syncthreads();
+    for (int k = 1; (1 << k) <= span; k++) {
+      const int half = 1 << (k - 1);
+      for (int i = threadIdx.x; i + (1 << k) <= span; i += FILL_THREADS)
+        sST[k][i] = comb<WIDEST>(sST[k - 1][i], sST[k - 1][i + half]);
+      __syncthreads();
+    }
+  }
   __syncthreads();
 #pragma unroll 4
   for (int t = 0; t < R; t++) {
@@ -136,8 +155,16 @@ __global__ void __launch_bounds__(FILL_THREADS)
 #pragma unroll
       for (int q = 0; q < VEC; q++) {
         if (side[q] == 2) {
-          int bb = b[q];
-          v[q] = (bb == at) ? 0.0f : (bb < at ? rmq<WIDEST>(ST, stride, bb, at) : rmq<WIDEST>(ST, stride, at, bb));
+          const int bb = b[q];
+          const int l = min(bb, at), r = max(bb, at);
+          if (bb == at) {
+            v[q] = 0.0f;
+          } else if (local) {  // RMQ(l, r) from the tile's shared-memory table
+            const int k = 31 - __clz(r - l);
+            v[q] = comb<WIDEST>(sST[k][l - aL], sST[k][r - aL - (1 << k)]);
+          } else {
+            v[q] = rmq<WIDEST>(ST, stride, l, r);
+          }
         }
       }
     }

@@ -1,0 +1,60 @@
+// Write-bandwidth microbenchmark for the APPD fill's store pattern (16 GiB matrix):
+// (a) linear 16-byte stores, (b) tiles of 128 rows in random order x W contiguous
+// columns per CTA (the fill's shape), for W in {1024, 2048, 4096}.
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_runtime.h>
+
+__global__ void k_linear(float4* p, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    __stcs(p + i, make_float4(1.f, 2.f, 3.f, 4.f));
+}
+template <int W>
+__global__ void __launch_bounds__(256) k_tiles(float* M, const int* rows, int n) {
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  for (int t = 0; t < 128; t++) {
+    float* dst = M + (int64_t)rows[t0 + t] * n + (int64_t)blockIdx.x * W;
+#pragma unroll
+    for (int c = 0; c < W / 1024; c++)
+      __stcs(reinterpret_cast<float4*>(dst + c * 1024) + threadIdx.x, make_float4(1.f, 2.f, 3.f, (float)t));
+  }
+}
+int main() {
+  const int n = 65536;
+  const size_t bytes = (size_t)n * n * 4;
+  float* M;
+  cudaMalloc(&M, bytes);
+  std::vector<int> h(n);
+  for (int i = 0; i < n; i++) h[i] = i;
+  std::shuffle(h.begin(), h.end(), std::mt19937(1));
+  int* rows;
+  cudaMalloc(&rows, n * 4);
+  cudaMemcpy(rows, h.data(), n * 4, cudaMemcpyHostToDevice);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto time = [&](auto f, const char* name) {
+    f();
+    cudaDeviceSynchronize();
+    float best = 1e9;
+    for (int r = 0; r < 5; r++) {
+      cudaEventRecord(a);
+      f();
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      best = std::min(best, ms);
+    }
+    printf("%-28s %.3f ms  %.2f TB/s\n", name, best, bytes / (best * 1e-3) / 1e12);
+  };
+  time([&] { k_linear<<<148 * 16, 256>>>((float4*)M, bytes / 16); }, "linear");
+  time([&] { k_tiles<1024><<<dim3(n / 1024, n / 128), 256>>>(M, rows, n); }, "tiles 128 x 4 KB");
+  time([&] { k_tiles<2048><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles 128 x 8 KB");
+  time([&] { k_tiles<4096><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles 128 x 16 KB");
+  time([&] { cudaMemsetAsync(M, 0, bytes); }, "cudaMemset");
+  return 0;
+}
