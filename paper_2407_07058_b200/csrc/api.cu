@@ -419,6 +419,33 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int64_t k = n;
   int rounds = 0;
   int* hostk = reinterpret_cast<int*>(c->pinned_small + 24);  // pinned: the copies stay asynchronous
+  // weights mode: round-0 candidate cache (exact per-row top-K of W)
+  const int wtopk = points ? 0 : (c->opt.topk == 0 ? 8 : (c->opt.topk < 0 ? 0 : c->opt.topk));
+  if (wtopk && wtopk != 4 && wtopk != 8 && wtopk != 16 && wtopk != 32)
+    return fail(c, APPD_ERR_INVALID_ARGUMENT, "topk = %d (0, -1, 4, 8, 16 or 32)", c->opt.topk);
+  u64* w_ckey = nullptr;
+  int *w_cj = nullptr, *w_ccnt = nullptr, *w_need = nullptr, *w_list = nullptr;
+  unsigned* w_count = nullptr;
+  bool w_pending = false;
+  if (wtopk) {
+    w_ckey = (u64*)ws(c, S_TC_CKEY, sizeof(u64) * n * wtopk);
+    w_cj = (int*)ws(c, S_TC_CJ, sizeof(int) * n * wtopk);
+    w_ccnt = (int*)ws(c, S_TC_CCNT, sizeof(int) * n);
+    w_need = (int*)ws(c, S_TC_NEED, sizeof(int) * n);
+    w_list = (int*)ws(c, S_TC_ROWLIST, sizeof(int) * (n + 1));
+    w_count = (unsigned*)ws(c, S_TC_CNT, 64);
+    if (!w_ckey || !w_cj || !w_ccnt || !w_need || !w_list || !w_count)
+      return fail(c, APPD_ERR_OUT_OF_MEMORY, "weights candidate cache");
+  }
+  auto w_lookup_async = [&]() -> appd_status {
+    APPD_CUDA(c, cudaMemsetAsync(w_count, 0, 64, c->stream));
+    appd_status s2 = launch_cache_lookup(c, (int)row0, (int)(row0 + rows), wtopk, (int)n, w_ckey, w_cj, w_ccnt, comp,
+                                         compbest, w_need, w_count, w_list);
+    if (s2) return s2;
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, w_count, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    w_pending = true;
+    return APPD_OK;
+  };
   const int finish_k = c->opt.finish_k == 0 ? 128 : std::min(c->opt.finish_k, 128);
   bool cm_timing_pending = false;
   while (k > 1) {
@@ -471,7 +498,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     static const bool dbg = getenv("APPD_DEBUG_ROUNDS") != nullptr;
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
-    if (!(use_tc && tc.lookup_pending) && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
+    if (!(use_tc && tc.lookup_pending) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
     if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
     const int64_t l0 = c->launches;
@@ -509,6 +536,20 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     } else if (points) {
       s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
       c->stats.exact_rounds++;
+    } else if (wtopk && rounds == 0) {
+      s = launch_scan_weights_topk(c, W, n, row0, rows, wtopk, sense, w_ckey, w_cj, w_ccnt, compbest);
+    } else if (wtopk) {
+      // cached round: rows without an eligible cached key whose K-th key is below their
+      // component's best are re-scanned
+      if (!w_pending) {
+        if ((s = w_lookup_async())) return s;
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      }
+      w_pending = false;
+      const unsigned cnt = c->pinned_small[9];
+      c->stats.rescan_rows += cnt;
+      if (cnt) c->stats.rescan_rounds++;
+      s = launch_scan_weights_list(c, W, n, row0, w_list, w_count, (int)cnt, comp, compbest, sense);
     } else {
       s = launch_scan_weights(c, W, n, row0, rows, cmp, compbest, sense);
     }
@@ -525,6 +566,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (use_tc && tc.topk && c->opt.world == 1) {
       if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
       if ((s = tcf_lookup_async(c, &tc, comp, compbest))) return s;
+    }
+    if (wtopk && c->opt.world == 1) {
+      if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
+      if ((s = w_lookup_async())) return s;
     }
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));

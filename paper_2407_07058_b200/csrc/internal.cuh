@@ -232,6 +232,11 @@ appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64
 // Boruvka
 appd_status launch_scan_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
                                 const int* comp, u64* compbest, int sense);
+appd_status launch_scan_weights_topk(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows, int K,
+                                     int sense, u64* ckey, int* cj, int* ccnt, u64* compbest);
+appd_status launch_scan_weights_list(appd_ctx* c, const float* W, int64_t n, int64_t row0, const int* list,
+                                     const unsigned* count, int max_rows, const int* comp, u64* compbest,
+                                     int sense);
 appd_status launch_transpose_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* XT, int64_t npad,
                                     int64_t dpad);
 appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,

@@ -87,6 +87,239 @@ __global__ void __launch_bounds__(256) k_scan_weights(const float* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// weights mode, round 0 with the candidate cache: per row the K smallest (w, j), j != i,
+// exactly (the per-row order (w, j) is the global edge-key order, see above).  Each
+// thread keeps a sorted local top-K of its columns (insertion only when a column beats
+// its K-th), then each warp and finally warp 0 extract the CTA's K smallest.  Writes the
+// cache (ckey = global keys, cj = column) and compbest[i] (singletons).
+// ---------------------------------------------------------------------------
+template <int K, int SENSE>
+__global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restrict__ W, int64_t n, int64_t row0,
+                                                         int64_t rows, u64* __restrict__ ckey, int* __restrict__ cj,
+                                                         int* __restrict__ ccnt, u64* __restrict__ compbest) {
+  // pass 1: per-thread minimum (columns visited in increasing j: strict '<' keeps the
+  // smallest j); the K-th smallest of the 256 minima bounds the row's K-th key (they are
+  // K distinct columns).  pass 2 (the row again, from L2): every key <= that bound is
+  // collected; a warp sorts them (bitonic, 64 at a time) and keeps the K smallest.
+  constexpr int CAP = 64;
+  __shared__ u64 tmin[256];
+  __shared__ u64 cand[CAP];
+  __shared__ u64 tau_s;
+  __shared__ int ncand;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = (n & 3) == 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t i = row0 + r;
+    const float* Wr = W + r * n;
+    auto keyof = [&](float w, int64_t j) -> u64 {
+      float m = SENSE > 0 ? w : -w;
+      m = m + 0.0f;  // -0 -> +0 (reading Q5)
+      return ((u64)orderable(m) << 32) | (u64)j;
+    };
+    u64 mine = KEY_NONE;
+    if (vec) {
+      const float4* W4 = reinterpret_cast<const float4*>(Wr);
+      for (int64_t q = threadIdx.x; q < (n >> 2); q += 256) {
+        const float4 w = __ldcg(W4 + q);
+        const float ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int64_t j = 4 * q + e;
+          if (j != i) {
+            const u64 kk = keyof(ws[e], j);
+            mine = kk < mine ? kk : mine;
+          }
+        }
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < n; j += 256)
+        if (j != i) {
+          const u64 kk = keyof(__ldcg(Wr + j), j);
+          mine = kk < mine ? kk : mine;
+        }
+    }
+    tmin[threadIdx.x] = mine;
+    if (threadIdx.x == 0) ncand = 0;
+    __syncthreads();
+    if (warp == 0) {
+      // K-th smallest of the 256 minima: 8 per lane, bitonic-sorted lane lists merged by K rounds
+      u64 v[8];
+#pragma unroll
+      for (int t = 0; t < 8; t++) v[t] = tmin[lane * 8 + t];
+#pragma unroll
+      for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 7 - a; b++)
+          if (v[b] > v[b + 1]) { const u64 x = v[b]; v[b] = v[b + 1]; v[b + 1] = x; }
+      int h = 0;
+      u64 kth = KEY_NONE;
+      for (int t = 0; t < K; t++) {
+        u64 head = KEY_NONE;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (u == h) head = v[u];
+        u64 best = head;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
+          best = other < best ? other : best;
+        }
+        if (best != KEY_NONE && head == best) h++;
+        kth = best;  // after K rounds: the K-th smallest (KEY_NONE if fewer than K exist)
+      }
+      if (lane == 0) tau_s = kth;
+    }
+    __syncthreads();
+    const u64 tau = tau_s;
+    // pass 2: keys <= tau
+    if (vec) {
+      const float4* W4 = reinterpret_cast<const float4*>(Wr);
+      for (int64_t q = threadIdx.x; q < (n >> 2); q += 256) {
+        const float4 w = __ldcs(W4 + q);
+        const float ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int64_t j = 4 * q + e;
+          if (j != i) {
+            const u64 kk = keyof(ws[e], j);
+            if (kk <= tau) {
+              const int slot = atomicAdd(&ncand, 1);
+              if (slot < CAP) cand[slot] = kk;
+            }
+          }
+        }
+      }
+    } else {
+      for (int64_t j = threadIdx.x; j < n; j += 256)
+        if (j != i) {
+          const u64 kk = keyof(__ldcs(Wr + j), j);
+          if (kk <= tau) {
+            const int slot = atomicAdd(&ncand, 1);
+            if (slot < CAP) cand[slot] = kk;
+          }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int nc = ncand;
+      if (nc > CAP) {  // more than CAP keys tie below the bound: no cache for this row
+        if (lane == 0) {
+          ccnt[i] = -1;
+          // its round-0 minimum: the smallest thread minimum
+          u64 b = KEY_NONE;
+          for (int t = 0; t < 256; t++) b = tmin[t] < b ? tmin[t] : b;
+          if (b != KEY_NONE) compbest[i] = (b & 0xFFFFFFFF00000000ull) | tri_index(i, (int64_t)(b & 0xFFFFFFFFull));
+        }
+      } else {
+        // bitonic sort of 64 (two per lane: lane and lane + 32)
+        u64 x0 = lane < nc ? cand[lane] : KEY_NONE, x1 = lane + 32 < nc ? cand[lane + 32] : KEY_NONE;
+        // sort each 32 ascending, then merge the two halves
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+          for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const bool up = (lane & size) == 0, lower = (lane & stride) == 0;
+            u64 y = __shfl_xor_sync(0xffffffffu, x0, stride);
+            u64 lo = x0 < y ? x0 : y, hi = x0 < y ? y : x0;
+            x0 = (lower == up) ? lo : hi;
+            y = __shfl_xor_sync(0xffffffffu, x1, stride);
+            lo = x1 < y ? x1 : y;
+            hi = x1 < y ? y : x1;
+            x1 = (lower == up) ? lo : hi;
+          }
+        // the K (<= 32) smallest of two sorted lists: lane t takes rank t by merging
+        const u64 y1 = __shfl_sync(0xffffffffu, x1, 31 - lane);  // reversed second list
+        u64 m = x0 < y1 ? x0 : y1;                              // bitonic sequence of the 32 smallest
+#pragma unroll
+        for (int stride = 16; stride > 0; stride >>= 1) {
+          const u64 y = __shfl_xor_sync(0xffffffffu, m, stride);
+          const bool lower = (lane & stride) == 0;
+          m = lower ? (m < y ? m : y) : (m < y ? y : m);
+        }
+        const int take = (int)(nc < K ? nc : K);
+        if (lane < take) {
+          const int64_t j = (int64_t)(m & 0xFFFFFFFFull);
+          const u64 g = (m & 0xFFFFFFFF00000000ull) | tri_index(i, j);
+          ckey[i * K + lane] = g;
+          cj[i * K + lane] = (int)j;
+          if (lane == 0) compbest[i] = g;
+        }
+        if (lane == 0) ccnt[i] = take;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// weights mode: exact scan of a list of rows (component-filtered argmin, re-scans)
+template <int SENSE>
+__global__ void __launch_bounds__(256) k_scan_weights_list(const float* __restrict__ W, int64_t n, int64_t row0,
+                                                         const int* __restrict__ list,
+                                                         const unsigned* __restrict__ count,
+                                                         const int* __restrict__ comp, u64* __restrict__ compbest) {
+  __shared__ u64 red[8];
+  const unsigned cnt = *count;
+  for (unsigned e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const int64_t i = list[e];
+    const float* Wr = W + (i - row0) * n;
+    const int ci = comp[i];
+    u64 best = KEY_NONE;
+    for (int64_t j = threadIdx.x; j < n; j += 256) {
+      if (__ldg(comp + j) == ci) continue;
+      float m = SENSE > 0 ? __ldcs(Wr + j) : -__ldcs(Wr + j);
+      m = m + 0.0f;
+      const u64 loc = ((u64)orderable(m) << 32) | (u64)j;
+      best = loc < best ? loc : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other < best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u64 b = red[0];
+      for (int t = 1; t < 8; t++) b = red[t] < b ? red[t] : b;
+      if (b != KEY_NONE) {
+        const int64_t j = (int64_t)(b & 0xFFFFFFFFull);
+        atomicMin(compbest + ci, (b & 0xFFFFFFFF00000000ull) | tri_index(i, j));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+appd_status launch_scan_weights_topk(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows, int K,
+                                     int sense, u64* ckey, int* cj, int* ccnt, u64* compbest) {
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>(rows, 1), (int64_t)c->sm_count * 8);
+#define APPD_WTOPK(KK)                                                                                       \
+  (sense > 0 ? (k_scan_weights_topk<KK, 1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)) \
+             : (k_scan_weights_topk<KK, -1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)))
+  switch (K) {
+    case 4: APPD_WTOPK(4); break;
+    case 8: APPD_WTOPK(8); break;
+    case 16: APPD_WTOPK(16); break;
+    case 32: APPD_WTOPK(32); break;
+    default: return fail(c, APPD_ERR_INVALID_ARGUMENT, "cache length K = %d (4, 8, 16 or 32)", K);
+  }
+#undef APPD_WTOPK
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+appd_status launch_scan_weights_list(appd_ctx* c, const float* W, int64_t n, int64_t row0, const int* list,
+                                     const unsigned* count, int max_rows, const int* comp, u64* compbest,
+                                     int sense) {
+  if (max_rows <= 0) return APPD_OK;
+  const int grid = std::min(max_rows, c->sm_count * 8);
+  if (sense > 0) k_scan_weights_list<1><<<grid, 256, 0, c->stream>>>(W, n, row0, list, count, comp, compbest);
+  else k_scan_weights_list<-1><<<grid, 256, 0, c->stream>>>(W, n, row0, list, count, comp, compbest);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
 appd_status launch_scan_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
                                 const int* comp, u64* compbest, int sense) {
   int grid = (int)(rows < (int64_t)c->sm_count * 8 ? rows : (int64_t)c->sm_count * 8);

@@ -9,12 +9,15 @@ namespace appd {
 
 __device__ __forceinline__ uint32_t canon_bits(float w) { return __float_as_uint(w + 0.0f); }
 
-// 32x32 tile pairs (I,J) and (J,I), I <= J, inside the square [row0, row0+rows)^2
-// of global indices; W is the rank's row block (rows x n, first row = row0).
-__global__ void k_validate_square(const float* __restrict__ W, int64_t n, int64_t row0, int64_t rows,
-                                  int64_t tiles, u64* __restrict__ out3) {
-  __shared__ float a[32][33];
-  __shared__ float b[32][33];
+// 64x64 tile pairs (I,J) and (J,I), I <= J, inside the square [row0, row0+rows)^2 of
+// global indices; W is the rank's row block (rows x n, first row = row0).  Both tiles
+// are read with 16-byte loads (256-byte row segments), all issued before any shared-
+// memory store; the transposed compare goes through padded shared memory.
+constexpr int VT = 64;
+__global__ void __launch_bounds__(256) k_validate_square(const float* __restrict__ W, int64_t n, int64_t row0,
+                                                         int64_t rows, int64_t tiles, u64* __restrict__ out3) {
+  __shared__ float a[VT][VT + 1];
+  __shared__ float b[VT][VT + 1];
   // map blockIdx.x to (I, J) with I <= J over a T x T upper triangle
   const int64_t p = blockIdx.x, T = tiles;
   // pairs before row I: f(I) = I*T - I*(I-1)/2; largest I with f(I) <= p
@@ -23,24 +26,55 @@ __global__ void k_validate_square(const float* __restrict__ W, int64_t n, int64_
   if (I < 0) I = 0;
   while (I > 0 && I * T - I * (I - 1) / 2 > p) I--;
   while ((I + 1) * T - (I + 1) * I / 2 <= p) I++;
-  int64_t J = I + (p - (I * T - I * (I - 1) / 2));
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int r = ty; r < 32; r += 8) {
-    int64_t li = I * 32 + r, lj = J * 32 + tx;  // local square coords
-    a[r][tx] = (li < rows && lj < rows) ? W[li * n + row0 + lj] : 0.0f;
-    int64_t mi = J * 32 + r, mj = I * 32 + tx;
-    b[r][tx] = (mi < rows && mj < rows) ? W[mi * n + row0 + mj] : 0.0f;
+  const int64_t J = I + (p - (I * T - I * (I - 1) / 2));
+  const bool vec = ((n | row0) & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
+  const int c4 = threadIdx.x & 15, r0 = threadIdx.x >> 4;
+  float4 va[VT / 16], vb[VT / 16];
+#pragma unroll
+  for (int s4 = 0; s4 < VT / 16; s4++) {
+    const int r = r0 + 16 * s4;
+    const int64_t li = I * VT + r, mi = J * VT + r;
+    const int64_t lj = J * VT + 4 * c4, mj = I * VT + 4 * c4;
+    if (vec && li < rows && lj + 3 < rows) {
+      va[s4] = __ldcs(reinterpret_cast<const float4*>(W + li * n + row0 + lj));
+    } else {
+      va[s4].x = (li < rows && lj + 0 < rows) ? W[li * n + row0 + lj + 0] : 0.0f;
+      va[s4].y = (li < rows && lj + 1 < rows) ? W[li * n + row0 + lj + 1] : 0.0f;
+      va[s4].z = (li < rows && lj + 2 < rows) ? W[li * n + row0 + lj + 2] : 0.0f;
+      va[s4].w = (li < rows && lj + 3 < rows) ? W[li * n + row0 + lj + 3] : 0.0f;
+    }
+    if (vec && mi < rows && mj + 3 < rows) {
+      vb[s4] = __ldcs(reinterpret_cast<const float4*>(W + mi * n + row0 + mj));
+    } else {
+      vb[s4].x = (mi < rows && mj + 0 < rows) ? W[mi * n + row0 + mj + 0] : 0.0f;
+      vb[s4].y = (mi < rows && mj + 1 < rows) ? W[mi * n + row0 + mj + 1] : 0.0f;
+      vb[s4].z = (mi < rows && mj + 2 < rows) ? W[mi * n + row0 + mj + 2] : 0.0f;
+      vb[s4].w = (mi < rows && mj + 3 < rows) ? W[mi * n + row0 + mj + 3] : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int s4 = 0; s4 < VT / 16; s4++) {
+    const int r = r0 + 16 * s4;
+    a[r][4 * c4 + 0] = va[s4].x;
+    a[r][4 * c4 + 1] = va[s4].y;
+    a[r][4 * c4 + 2] = va[s4].z;
+    a[r][4 * c4 + 3] = va[s4].w;
+    b[r][4 * c4 + 0] = vb[s4].x;
+    b[r][4 * c4 + 1] = vb[s4].y;
+    b[r][4 * c4 + 2] = vb[s4].z;
+    b[r][4 * c4 + 3] = vb[s4].w;
   }
   __syncthreads();
   u64 bad_nf = KEY_NONE, bad_diag = KEY_NONE, bad_sym = KEY_NONE;
-  for (int r = ty; r < 32; r += 8) {
-    int64_t li = I * 32 + r, lj = J * 32 + tx;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  for (int r = ty; r < VT; r += 4) {
+    const int64_t li = I * VT + r, lj = J * VT + tx;
     if (li < rows && lj < rows) {
-      int64_t gi = row0 + li, gj = row0 + lj;
-      float x = a[r][tx];           // W[gi][gj]
-      float y = b[tx][r];           // W[gj][gi]
-      u64 idx = (u64)(gi * n + gj);
-      u64 idxT = (u64)(gj * n + gi);
+      const int64_t gi = row0 + li, gj = row0 + lj;
+      const float x = a[r][tx];  // W[gi][gj]
+      const float y = b[tx][r];  // W[gj][gi]
+      const u64 idx = (u64)(gi * n + gj);
+      const u64 idxT = (u64)(gj * n + gi);
       if (!isfinite(x)) bad_nf = min(bad_nf, idx);
       if (!isfinite(y)) bad_nf = min(bad_nf, idxT);
       if (gi == gj) {
@@ -50,9 +84,18 @@ __global__ void k_validate_square(const float* __restrict__ W, int64_t n, int64_
       }
     }
   }
-  if (bad_nf != KEY_NONE) atomicMin(out3 + 0, bad_nf);
-  if (bad_diag != KEY_NONE) atomicMin(out3 + 1, bad_diag);
-  if (bad_sym != KEY_NONE) atomicMin(out3 + 2, bad_sym);
+  // one atomic per kind per warp
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad_nf = min(bad_nf, __shfl_xor_sync(0xffffffffu, bad_nf, o));
+    bad_diag = min(bad_diag, __shfl_xor_sync(0xffffffffu, bad_diag, o));
+    bad_sym = min(bad_sym, __shfl_xor_sync(0xffffffffu, bad_sym, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad_nf != KEY_NONE) atomicMin(out3 + 0, bad_nf);
+    if (bad_diag != KEY_NONE) atomicMin(out3 + 1, bad_diag);
+    if (bad_sym != KEY_NONE) atomicMin(out3 + 2, bad_sym);
+  }
 }
 
 // finiteness of the columns outside the diagonal square (world > 1)
@@ -69,10 +112,10 @@ __global__ void k_validate_finite_rest(const float* __restrict__ W, int64_t n, i
 }
 
 appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows, u64* out3) {
-  int64_t T = (rows + 31) / 32;
+  int64_t T = (rows + VT - 1) / VT;
   int64_t pairs = T * (T + 1) / 2;
   if (pairs > 0x7FFFFFFFll) return fail(c, APPD_ERR_UNSUPPORTED, "validation grid too large");
-  k_validate_square<<<(unsigned)pairs, dim3(32, 8), 0, c->stream>>>(W, n, row0, rows, T, out3);
+  k_validate_square<<<(unsigned)pairs, 256, 0, c->stream>>>(W, n, row0, rows, T, out3);
   APPD_LAUNCHED(c);
   if (rows < n) {
     k_validate_finite_rest<<<c->sm_count * 8, 256, 0, c->stream>>>(W, n, row0, rows, out3);

@@ -90,6 +90,19 @@ def test_random_weights(ctx, kind):
         assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), f"{kind} n={n}")
 
 
+@pytest.mark.parametrize("topk", [0, -1, 4, 32])
+def test_weights_cache_lengths(P, topk):
+    """Weights mode with and without the round-0 candidate cache (several K), incl. ties."""
+    c = P.Context(timing=True, topk=topk)
+    try:
+        for t, (n, kind) in enumerate([(300, "uniform"), (257, "ties"), (700, "ints255"), (129, "negative"),
+                                       (1000, "ties")]):
+            W = G.random_weights(n, 500 + t, kind)
+            assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), f"topk={topk} {kind} n={n}")
+    finally:
+        c.close()
+
+
 def test_widest_sense(P):
     with P.Context(sense=-1) as cw:
         for t, n in enumerate([2, 3, 17, 64, 255, 600]):
