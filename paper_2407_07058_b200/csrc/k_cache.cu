@@ -218,10 +218,25 @@ __global__ void k_chunk_runs(const unsigned* __restrict__ list, const unsigned* 
   }
 }
 
+// item table: item -> (chunk, first list entry, rows), one thread per chunk
+__global__ void k_item_table(const unsigned* __restrict__ run_lo, const unsigned* __restrict__ run_nb,
+                             const unsigned* __restrict__ item_start, const unsigned* __restrict__ list,
+                             const unsigned* __restrict__ count, unsigned cap, int nch, int4* __restrict__ table) {
+  const unsigned total = min(*count, cap);
+  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+    const unsigned lo = run_lo[ch], nb = run_nb[ch], base = item_start[ch];
+    const unsigned hi = lower_bound_u32(list, total, (unsigned)(ch + 1) << LIST_SHIFT);
+    for (unsigned b = 0; b < nb; b++) {
+      const unsigned b0 = lo + b * LE_RB;
+      table[base + b] = make_int4(ch, (int)b0, (int)min((unsigned)LE_RB, hi - b0), 0);
+    }
+  }
+}
+
 // Work item = (chunk, 128-row batch): item_start is the exclusive prefix of run_nb, so
 // dense candidate chunks (component boundaries) spread over many CTAs.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_list_exact(ListParams L) {
+__global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParams L) {
   extern __shared__ __align__(16) float sm[];
   float* colx = sm;                 // [d][32]
   float* rowx = sm + L.d * 32;      // [d][LE_RB]
@@ -231,17 +246,10 @@ __global__ void __launch_bounds__(256) k_list_exact(ListParams L) {
   const unsigned total = min(*L.count, L.cap);
   const unsigned items = L.item_start[L.nch - 1] + L.run_nb[L.nch - 1];
   for (unsigned item = blockIdx.x; item < items; item += gridDim.x) {
-    // chunk = last ch with item_start[ch] <= item
-    int lo_c = 0, hi_c = L.nch - 1;
-    while (lo_c < hi_c) {
-      const int mid = (lo_c + hi_c + 1) >> 1;
-      if (L.item_start[mid] <= item) lo_c = mid;
-      else hi_c = mid - 1;
-    }
-    const int ch = lo_c;
-    const unsigned b0 = L.run_lo[ch] + (item - L.item_start[ch]) * LE_RB;
-    unsigned hi = lower_bound_u32(L.list + b0, min((unsigned)LE_RB, total - b0), (unsigned)(ch + 1) << LIST_SHIFT);
-    const int nb = (int)hi;
+    const int4 td = __ldg(L.items + item);  // (chunk, first entry, rows)
+    const int ch = td.x;
+    const unsigned b0 = (unsigned)td.y;
+    const int nb = td.z;
     __syncthreads();  // the previous item's readers of colx / rowx / rowp are done
     const int q0 = ch * 32;
     for (int e = threadIdx.x; e < L.d * 32; e += blockDim.x) {
@@ -650,7 +658,10 @@ appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsign
   APPD_LAUNCHED(c);
   appd_status s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, L.nch);
   if (s) return s;
-  const int grid = c->sm_count * 4;
+  k_item_table<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(run_lo, run_nb, item_start, L.list, L.count, L.cap, L.nch,
+                                                          const_cast<int4*>(L.items));
+  APPD_LAUNCHED(c);
+  const int grid = c->sm_count * (mode == 0 ? 5 : 4);  // 5 x 40 KB of shared memory fit an SM
   if (mode == 0) {
     cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_list_exact<0><<<grid, 256, smem, c->stream>>>(L);

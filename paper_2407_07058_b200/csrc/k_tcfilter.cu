@@ -626,6 +626,10 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   L.run_lo = runs;
   L.run_nb = runs + nch + 1;
   L.item_start = runs + 2 * (nch + 1);
+  // item table: at most ceil(count / 128) + nch items
+  int4* items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
+  if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
+  L.items = items;
   L.UBK = st->UBK;
   L.s2 = (double)st->scale * (double)st->scale;
   L.cnt = st->cand_cnt;

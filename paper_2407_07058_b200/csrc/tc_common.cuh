@@ -135,6 +135,7 @@ struct ListParams {
   const unsigned* run_lo;     // per chunk: first entry of its run in the sorted list
   const unsigned* run_nb;     // per chunk: 128-row batches
   const unsigned* item_start; // exclusive prefix of run_nb
+  const int4* items;          // per work item: chunk, first list entry, rows
   // MODE 0
   const float* UBK;
   double s2;
