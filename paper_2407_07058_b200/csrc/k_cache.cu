@@ -76,17 +76,26 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
     int nb = 0;
     u64* buf = rowbuf + (int64_t)(valid ? p : 0) * rbcap;
     const float4* row4 = reinterpret_cast<const float4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
+    // software pipeline: the next batch's loads are in flight while this batch is processed
+    float4 nx[U4];
+#pragma unroll
+    for (int u = 0; u < U4; u++)
+      nx[u] = (valid && 4 * u < nch) ? __ldcs(row4 + (int64_t)u * 512)
+                                      : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
     for (int c0 = 0; c0 < nch; c0 += 4 * U4) {
       float v[4 * U4];
 #pragma unroll
       for (int u = 0; u < U4; u++) {
-        float4 x = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        if (valid && c0 + 4 * u < nch) x = __ldcs(row4 + (int64_t)((c0 >> 2) + u) * 512);
-        v[4 * u] = x.x;
-        v[4 * u + 1] = x.y;
-        v[4 * u + 2] = x.z;
-        v[4 * u + 3] = x.w;
+        v[4 * u] = nx[u].x;
+        v[4 * u + 1] = nx[u].y;
+        v[4 * u + 2] = nx[u].z;
+        v[4 * u + 3] = nx[u].w;
       }
+      const int c1 = c0 + 4 * U4;
+#pragma unroll
+      for (int u = 0; u < U4; u++)
+        nx[u] = (valid && c1 + 4 * u < nch) ? __ldcs(row4 + (int64_t)((c1 >> 2) + u) * 512)
+                                            : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
       const float kth0 = top[K - 1];
 #pragma unroll
       for (int u = 0; u < 4 * U4; u++) {
