@@ -16,9 +16,10 @@ for rep in sys.argv[1:]:
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         print(rep, "no data"); continue
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    print("==", rep, vals[hdr.index("Kernel Name")][:60] if "Kernel Name" in hdr else "")
-    for w in WANT:
-        if w in hdr:
-            i = hdr.index(w)
-            print(f"  {w:80s} {vals[i]:>16s} {units[i]}")
+    hdr, units = rows[0], rows[1]
+    for vals in rows[2:]:
+        print("==", rep, vals[hdr.index("Kernel Name")][:60] if "Kernel Name" in hdr else "")
+        for w in WANT:
+            if w in hdr:
+                i = hdr.index(w)
+                print(f"  {w:80s} {vals[i]:>16s} {units[i]}")
