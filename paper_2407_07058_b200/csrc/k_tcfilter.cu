@@ -758,6 +758,8 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     }
     st->cache_r0 = p_begin;
     st->cache_r1 = p_end;
+    // rows outside this rank's cache are never flagged (multi-rank: need[] is read for all rows)
+    APPD_CUDA(c, cudaMemsetAsync(st->need, 0, sizeof(int) * n, c->stream));
   } else if (cache) {
     // ---- re-scan of the blocks holding flagged rows ----
     APPD_CUDA(c, cudaMemsetAsync(st->blockflag, 0, sizeof(int) * (2 * (T + 1) + 8), c->stream));
