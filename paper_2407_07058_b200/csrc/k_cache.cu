@@ -227,6 +227,62 @@ __global__ void k_chunk_runs(const unsigned* __restrict__ list, const unsigned* 
   }
 }
 
+// counting sort of the list by chunk (no host-side count): histogram, scatter
+__global__ void k_chunk_hist(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
+                             unsigned* __restrict__ hist) {
+  const unsigned total = min(*count, cap);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
+    atomicAdd(hist + (list[e] >> LIST_SHIFT), 1u);
+}
+__global__ void k_chunk_scatter(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
+                                const unsigned* __restrict__ offs, unsigned* __restrict__ cursor,
+                                unsigned* __restrict__ out) {
+  const unsigned total = min(*count, cap);
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const unsigned v = list[e], ch = v >> LIST_SHIFT;
+    out[offs[ch] + atomicAdd(cursor + ch, 1u)] = v;
+  }
+}
+// runs from the histogram: run_lo = offsets, run_nb = 128-row batches
+__global__ void k_runs_from_hist(const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, int nch,
+                                 unsigned* __restrict__ run_lo, unsigned* __restrict__ run_nb) {
+  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+    run_lo[ch] = offs[ch];
+    run_nb[ch] = (hist[ch] + LE_RB - 1) / LE_RB;
+  }
+}
+__global__ void k_item_table_h(const unsigned* __restrict__ run_lo, const unsigned* __restrict__ run_nb,
+                               const unsigned* __restrict__ item_start, const unsigned* __restrict__ hist, int nch,
+                               int4* __restrict__ table) {
+  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
+    const unsigned lo = run_lo[ch], nb = run_nb[ch], base = item_start[ch], hi = lo + hist[ch];
+    for (unsigned b = 0; b < nb; b++) {
+      const unsigned b0 = lo + b * LE_RB;
+      table[base + b] = make_int4(ch, (int)b0, (int)min((unsigned)LE_RB, hi - b0), 0);
+    }
+  }
+}
+
+appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsigned* count, unsigned cap, int nch,
+                                 unsigned* hist, unsigned* offs, unsigned* cursor, unsigned* out, unsigned* run_lo,
+                                 unsigned* run_nb, unsigned* item_start, int4* items) {
+  const int g = c->sm_count * 8;
+  APPD_CUDA(c, cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nch + 1), c->stream));
+  APPD_CUDA(c, cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (nch + 1), c->stream));
+  k_chunk_hist<<<g, 256, 0, c->stream>>>(list, count, cap, hist);
+  APPD_LAUNCHED(c);
+  appd_status s = exclusive_scan_i32(c, (const int*)hist, (int*)offs, nch + 1);
+  if (s) return s;
+  k_chunk_scatter<<<g, 256, 0, c->stream>>>(list, count, cap, offs, cursor, out);
+  APPD_LAUNCHED(c);
+  k_runs_from_hist<<<(nch + 255) / 256, 256, 0, c->stream>>>(hist, offs, nch, run_lo, run_nb);
+  APPD_LAUNCHED(c);
+  if ((s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, nch))) return s;
+  k_item_table_h<<<(nch + 255) / 256, 256, 0, c->stream>>>(run_lo, run_nb, item_start, hist, nch, items);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
 // item table: item -> (chunk, first list entry, rows), one thread per chunk
 __global__ void k_item_table(const unsigned* __restrict__ run_lo, const unsigned* __restrict__ run_nb,
                              const unsigned* __restrict__ item_start, const unsigned* __restrict__ list,
@@ -663,13 +719,15 @@ appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsign
                               unsigned* item_start) {
   const size_t smem = (size_t)L.d * (32 + LE_RB) * 4;
   if (smem > 200 * 1024) return APPD_ERR_UNSUPPORTED;
-  k_chunk_runs<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(L.list, L.count, L.cap, L.nch, run_lo, run_nb);
-  APPD_LAUNCHED(c);
-  appd_status s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, L.nch);
-  if (s) return s;
-  k_item_table<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(run_lo, run_nb, item_start, L.list, L.count, L.cap, L.nch,
-                                                          const_cast<int4*>(L.items));
-  APPD_LAUNCHED(c);
+  if (run_lo) {  // sorted list: runs and items from binary searches (else prepared by the caller)
+    k_chunk_runs<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(L.list, L.count, L.cap, L.nch, run_lo, run_nb);
+    APPD_LAUNCHED(c);
+    appd_status s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, L.nch);
+    if (s) return s;
+    k_item_table<<<(L.nch + 255) / 256, 256, 0, c->stream>>>(run_lo, run_nb, item_start, L.list, L.count, L.cap,
+                                                            L.nch, const_cast<int4*>(L.items));
+    APPD_LAUNCHED(c);
+  }
   const int grid = c->sm_count * (mode == 0 ? 5 : 4);  // 5 x 40 KB of shared memory fit an SM
   if (mode == 0) {
     cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -601,34 +601,50 @@ static int bits_for(int64_t v) {
 // mode 0 appends cache candidates, mode 1 reduces component-pair minima into WCM
 static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode, const int* perm,
                               unsigned* count_dev, int k, u64* WCM) {
-  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  const unsigned cnt = std::min(c->pinned_small[16], st->list_entries_cap);
-  st->last_list_entries = c->pinned_small[16];
-  if (cnt == 0) return APPD_OK;
   const int nch = (int)((st->n + 31) / 32);
   appd_status s;
-  if ((s = sort_keys_u32_bits(c, st->lista, st->listb, cnt, 0, 17 + bits_for(nch + 1)))) return s;
-  APPD_CUDA(c, cudaMemcpyAsync(st->counters + 8, &cnt, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
-  APPD_CUDA(c, cudaMemsetAsync(st->counters + 10, 0, 2 * sizeof(unsigned), c->stream));
+  unsigned cnt;
+  unsigned* runs = (unsigned*)ws(c, S_TC_RUNS, sizeof(unsigned) * 6 * (nch + 2));
+  if (!runs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list runs");
+  unsigned *run_lo = runs, *run_nb = runs + (nch + 2), *item_start = runs + 2 * (nch + 2);
+  unsigned *hist = runs + 3 * (nch + 2), *offs = runs + 4 * (nch + 2), *cursor = runs + 5 * (nch + 2);
+  const bool counting = mode == 0;  // rows within a chunk may come in any order: no host round trip
+  int4* items;
+  if (counting) {
+    cnt = st->list_entries_cap;  // capacity bound; the kernels read the real count on the device
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 c->stream));  // statistics, read after a later synchronisation
+    items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
+    if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
+    if ((s = launch_list_counting(c, st->lista, count_dev, cnt, nch, hist, offs, cursor, st->listb, run_lo, run_nb,
+                                  item_start, items)))
+      return s;
+  } else {
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                 c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    cnt = std::min(c->pinned_small[16], st->list_entries_cap);
+    st->last_list_entries = c->pinned_small[16];
+    if (cnt == 0) return APPD_OK;
+    // the component-matrix reduction wants the rows of a chunk in order: full sort
+    if ((s = sort_keys_u32_bits(c, st->lista, st->listb, cnt, 0, 17 + bits_for(nch + 1)))) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(st->counters + 8, &cnt, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
+    items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
+    if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
+  }
   ListParams L;
   memset(&L, 0, sizeof L);
   L.list = st->listb;
-  L.count = st->counters + 8;
+  L.count = counting ? count_dev : st->counters + 8;
   L.cap = cnt;
   L.nch = nch;
   L.n = (int)st->n;
   L.d = (int)st->d;
   L.X = X;
   L.perm = perm;
-  unsigned* runs = (unsigned*)ws(c, S_TC_RUNS, sizeof(unsigned) * 3 * (nch + 1));
-  if (!runs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list runs");
-  L.run_lo = runs;
-  L.run_nb = runs + nch + 1;
-  L.item_start = runs + 2 * (nch + 1);
-  // item table: at most ceil(count / 128) + nch items
-  int4* items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
-  if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
+  L.run_lo = run_lo;
+  L.run_nb = run_nb;
+  L.item_start = item_start;
   L.items = items;
   L.UBK = st->UBK;
   L.s2 = (double)st->scale * (double)st->scale;
@@ -638,7 +654,7 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   L.sc = st->sc;
   L.k = k;
   L.WCM = WCM;
-  return launch_list_exact(c, mode, L, runs, runs + nch + 1, runs + 2 * (nch + 1));
+  return launch_list_exact(c, mode, L, counting ? nullptr : run_lo, run_nb, item_start);
 }
 
 // Queue the cache lookup of the next round (compbest must hold KEY_NONE): per-row first

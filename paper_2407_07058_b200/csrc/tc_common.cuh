@@ -147,6 +147,9 @@ struct ListParams {
   int k;
   u64* WCM;
 };
+appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsigned* count, unsigned cap, int nch,
+                                 unsigned* hist, unsigned* offs, unsigned* cursor, unsigned* out, unsigned* run_lo,
+                                 unsigned* run_nb, unsigned* item_start, int4* items);
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
