@@ -605,7 +605,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     int64_t knew = (int64_t)hostk[0] + hostk[1];
     if (dbg && use_tc && rounds == 0 && tc.topk)
-      fprintf(stderr, "[appd] cache build: listed (row, 32-col chunk) pairs %lld\n", (long long)tc.last_list_entries);
+      fprintf(stderr, "[appd] cache build: listed (row, 32-col chunk) pairs %u\n", c->pinned_small[16]);
     if (dbg)
       fprintf(stderr, "[appd] round %d (%.3f ms): k %lld -> %lld  rescan rows %lld blocks %u  exact tiles %u fallback %u\n",
               rounds, ev_ms(c, 12, 13), (long long)k, (long long)knew, (long long)(use_tc ? tc.last_rescan_rows : 0),

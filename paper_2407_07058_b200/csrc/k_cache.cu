@@ -813,11 +813,16 @@ __global__ void k_seg_comp(const int* __restrict__ sc, int n, int nseg, int2* __
 // segments are sorted by component: stream each row's stored maxima in order (16 loads
 // in flight), keep the running maximum of the current component's full segments and
 // flush its bound when the component changes
+constexpr int CM_SPLIT = 4;  // warps per 32-row group, each over a quarter of the segments
 __global__ void k_cm_rowub(CmParams P) {
   const int lane = threadIdx.x & 31;
   const int nseg_n = P.n / TC_TMG;  // full segments only (a partial last segment bounds nothing)
-  for (int p0 = P.p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < P.p_end;
-       p0 += gridDim.x * blockDim.x) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int groups = (P.p_end - P.p_begin + 31) / 32;
+  for (int64_t task = gw; task < (int64_t)groups * CM_SPLIT; task += nw) {
+    const int p0 = P.p_begin + (int)(task / CM_SPLIT) * 32;
+    const int part = (int)(task % CM_SPLIT);
     const int p = p0 + lane;
     const bool valid = p < P.p_end;
     const int C = valid ? P.sc[p] : -1;
@@ -838,15 +843,17 @@ __global__ void k_cm_rowub(CmParams P) {
     int curD = -1;
     float m = -INFINITY;
     constexpr int U = 16;
-    for (int s0 = smin; s0 < nseg_n; s0 += U) {
+    const int span = (nseg_n - smin + CM_SPLIT - 1) / CM_SPLIT;
+    const int sbeg = smin + part * span, send = min(nseg_n, sbeg + span);
+    for (int s0 = sbeg; s0 < send; s0 += U) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
-        v[u] = (valid && s0 + u < nseg_n) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+        v[u] = (valid && s0 + u < send) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int s = s0 + u;
-        if (s >= nseg_n) break;
+        if (s >= send) break;
         const int2 dd = P.segd[s];
         const int D0 = dd.x, D1 = dd.y;
         if (D0 != D1) continue;  // straddling segment: bounds neither component alone
@@ -866,9 +873,14 @@ __global__ void k_cm_rowub(CmParams P) {
 // per batch.  CUB here holds the listing thresholds T[C][D] (the host's path-pruned
 // upper bounds, scaled units).  A listed segment contributes its 32-column chunks.
 __global__ void k_cm_filter(CmParams P) {
-  const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int nseg = min(P.nseg, (P.n + TC_TMG - 1) / TC_TMG);
-  for (int p0 = P.p_begin + (blockIdx.x * warps + w) * 32; p0 < P.p_end; p0 += gridDim.x * warps * 32) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int groups = (P.p_end - P.p_begin + 31) / 32;
+  for (int64_t task = gw; task < (int64_t)groups * CM_SPLIT; task += nw) {
+    const int p0 = P.p_begin + (int)(task / CM_SPLIT) * 32;
+    const int part = (int)(task % CM_SPLIT);
     const int p = p0 + lane;
     const bool valid = p < P.p_end;
     const int C = valid ? P.sc[p] : 0;
@@ -876,11 +888,14 @@ __global__ void k_cm_filter(CmParams P) {
     int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
     float cachedT = 0.0f;
     constexpr int U = 16;
-    for (int s0 = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0; s0 < nseg; s0 += U) {
+    const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;
+    const int span = (nseg - smin + CM_SPLIT - 1) / CM_SPLIT;
+    const int sbeg = smin + part * span, send = min(nseg, sbeg + span);
+    for (int s0 = sbeg; s0 < send; s0 += U) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
-        v[u] = (valid && s0 + u < nseg) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+        v[u] = (valid && s0 + u < send) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
       unsigned mask = 0;
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -1100,7 +1115,7 @@ appd_status launch_seg_comp(appd_ctx* c, const int* sc, int n, int nseg, int2* s
 appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P) {
   const int rows = P.p_end - P.p_begin;
   if (rows <= 0) return APPD_OK;
-  k_cm_rowub<<<std::min(c->sm_count * 8, (rows + 255) / 256), 256, 0, c->stream>>>(P);
+  k_cm_rowub<<<std::min(c->sm_count * 16, (rows * CM_SPLIT + 255) / 256), 256, 0, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -1108,7 +1123,7 @@ appd_status launch_cm_rowub(appd_ctx* c, const CmParams& P) {
 appd_status launch_cm_filter(appd_ctx* c, const CmParams& P) {
   const int rows = P.p_end - P.p_begin;
   if (rows <= 0) return APPD_OK;
-  k_cm_filter<<<std::min(c->sm_count * 8, (rows + 255) / 256), 256, 0, c->stream>>>(P);
+  k_cm_filter<<<std::min(c->sm_count * 16, (rows * CM_SPLIT + 255) / 256), 256, 0, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
