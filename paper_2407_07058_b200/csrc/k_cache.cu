@@ -942,97 +942,71 @@ __global__ void k_cm_filter(CmParams P) {
 // bound on the path from C to D in the MST of the bounds (cut property), so
 // T = min(symmetric bound, path maximum) keeps every MST edge's minimum pair listed;
 // pairs above T are not MST edges and may come out inflated.  Output T (k x k).
-__global__ void __launch_bounds__(256) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
+__global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
                                                        unsigned* __restrict__ T) {
-  extern __shared__ float symb[];  // [k][k] symmetric bounds
-  __shared__ int par[128];
-  __shared__ float pw[128];
-  __shared__ int cstart[129], kids[128];
-  const int lane = threadIdx.x & 31;
+  extern __shared__ float symb[];   // [k][k] symmetric bounds, then [k][k] path maxima
+  float* pm = symb + k * k;
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  __shared__ int sel[2];            // node joining the tree and its tree neighbour
+  __shared__ float selw;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
     const int a = e / k, b = e % k;
     symb[e] = fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
+    pm[e] = 0.0f;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-  // Prim from node 0, one warp: lane owns nodes lane, lane + 32, ... (k <= 128)
-  float key[4];
-  int from[4];
-  bool in[4];
-#pragma unroll
-  for (int t = 0; t < 4; t++) {
-    const int q = lane + 32 * t;
-    in[t] = q == 0 || q >= k;
-    key[t] = (q < k && q > 0) ? symb[q] : INFINITY;
-    from[t] = 0;
-    if (q < k) { par[q] = -1; pw[q] = 0.0f; }
-  }
+  // Prim from node 0, thread q owns node q (k <= 128 <= blockDim); when q joins through
+  // tree neighbour f with bound w, every node x already in the tree gets
+  // pm[x][q] = pm[q][x] = max(pm[x][f], w): the path maxima of the bound MST, O(k) per step
+  const int q = threadIdx.x;
+  const int lane = q & 31, w = q >> 5;
+  bool in = q == 0 || q >= k;
+  float key = (q < k && q > 0) ? symb[q] : INFINITY;
+  int from = 0;
   for (int step = 1; step < k; step++) {
-    float bv = INFINITY;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int t = 0; t < 4; t++)
-      if (!in[t] && (key[t] < bv || (key[t] == bv && lane + 32 * t < bi))) { bv = key[t]; bi = lane + 32 * t; }
+    float bv = in ? INFINITY : key;
+    int bi = in ? 0x7fffffff : q;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if ((bi & 31) == lane) {
-      const int t = bi >> 5;
-#pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (u == t) { in[u] = true; par[bi] = from[u]; pw[bi] = key[u]; }
+    if (lane == 0) { sv[w] = bv; si[w] = bi; }
+    __syncthreads();
+    if (q == 0) {
+      float b2 = sv[0];
+      int i2 = si[0];
+      for (int t = 1; t < (int)(blockDim.x >> 5); t++)
+        if (sv[t] < b2 || (sv[t] == b2 && si[t] < i2)) { b2 = sv[t]; i2 = si[t]; }
+      sel[0] = i2;
     }
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int q = lane + 32 * t;
-      if (!in[t]) {
-        const float w = symb[bi * k + q];
-        if (w < key[t]) { key[t] = w; from[t] = bi; }
-      }
+    __syncthreads();
+    const int nq = sel[0];
+    if (q == nq) {
+      sel[1] = from;
+      selw = key;
+      in = true;
     }
+    __syncthreads();
+    const int f = sel[1];
+    const float wq = selw;
+    // in-tree nodes x (before nq joined): path max to nq
+    if (q < k && in && q != nq) {
+      const float v = fmaxf(pm[q * k + f], wq);
+      pm[q * k + nq] = v;
+      pm[nq * k + q] = v;
+    }
+    if (q < k && !in) {
+      const float wn = symb[nq * k + q];
+      if (wn < key) { key = wn; from = nq; }
+    }
+    __syncthreads();
   }
-  }  // warp 0
-  __syncthreads();
-  // children lists (CSR) of the tree rooted at 0
-  if (threadIdx.x == 0) {
-    for (int t = 0; t <= k; t++) cstart[t] = 0;
-    for (int t = 1; t < k; t++) cstart[par[t] + 1]++;
-    for (int t = 0; t < k; t++) cstart[t + 1] += cstart[t];
-    int fill[128];
-    for (int t = 0; t < k; t++) fill[t] = cstart[t];
-    for (int t = 1; t < k; t++) kids[fill[par[t]]++] = t;
-  }
-  __syncthreads();
-  // path maxima from every root r (one thread per root): DFS over parent + children
-  for (int r = threadIdx.x; r < k; r += blockDim.x) {
-    float pm[128];
-    int stack[128];
-    for (int t = 0; t < k; t++) pm[t] = -1.0f;
-    pm[r] = 0.0f;
-    int sp = 0;
-    stack[sp++] = r;
-    while (sp) {
-      const int x = stack[--sp];
-      const int pp = par[x];
-      if (pp >= 0 && pm[pp] < 0.0f) {
-        pm[pp] = fmaxf(pm[x], pw[x]);
-        stack[sp++] = pp;
-      }
-      for (int e = cstart[x]; e < cstart[x + 1]; e++) {
-        const int y = kids[e];
-        if (pm[y] < 0.0f) {
-          pm[y] = fmaxf(pm[x], pw[y]);
-          stack[sp++] = y;
-        }
-      }
-    }
-    for (int t = 0; t < k; t++) {
-      const float b = symb[r * k + t];
-      T[(int64_t)r * k + t] = __float_as_uint(pm[t] < 0.0f ? b : fminf(b, pm[t]));
-    }
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int a = e / k, b = e % k;
+    T[e] = __float_as_uint(a == b ? symb[e] : fminf(symb[e], pm[e]));
   }
 }
 
@@ -1092,9 +1066,9 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
 }
 
 appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T) {
-  const size_t smem = sizeof(float) * k * k;
+  const size_t smem = sizeof(float) * 2 * k * k;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_thresholds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cm_thresholds<<<1, 256, smem, c->stream>>>(CUB, k, T);
+  k_cm_thresholds<<<1, 128, smem, c->stream>>>(CUB, k, T);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
