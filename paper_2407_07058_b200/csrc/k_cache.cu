@@ -317,10 +317,23 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
     const int nb = td.z;
     __syncthreads();  // the previous item's readers of colx / rowx / rowp are done
     const int q0 = ch * 32;
-    for (int e = threadIdx.x; e < L.d * 32; e += blockDim.x) {
-      const int k = e >> 5, t = e & 31;
-      const int q = q0 + t;
-      colx[e] = q < L.n ? L.X[(int64_t)(L.perm ? L.perm[q] : q) * L.d + k] : 0.0f;
+    if ((L.d & 3) == 0) {  // 16-byte loads along k, lane = column (conflict-free transposed stores)
+      for (int e = threadIdx.x; e < (L.d >> 2) * 32; e += blockDim.x) {
+        const int t = e & 31, k4 = e >> 5;
+        const int q = q0 + t;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (q < L.n) v = __ldg(reinterpret_cast<const float4*>(L.X + (int64_t)(L.perm ? L.perm[q] : q) * L.d) + k4);
+        colx[(4 * k4 + 0) * 32 + t] = v.x;
+        colx[(4 * k4 + 1) * 32 + t] = v.y;
+        colx[(4 * k4 + 2) * 32 + t] = v.z;
+        colx[(4 * k4 + 3) * 32 + t] = v.w;
+      }
+    } else {
+      for (int e = threadIdx.x; e < L.d * 32; e += blockDim.x) {
+        const int k = e >> 5, t = e & 31;
+        const int q = q0 + t;
+        colx[e] = q < L.n ? L.X[(int64_t)(L.perm ? L.perm[q] : q) * L.d + k] : 0.0f;
+      }
     }
     int oq[4], Dq[4];
 #pragma unroll
@@ -332,21 +345,24 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
     {
       if (threadIdx.x < LE_RB) rowp[threadIdx.x] = threadIdx.x < nb ? (int)(L.list[b0 + threadIdx.x] & LIST_ROWMASK) : -1;
       __syncthreads();
-      // stage the batch's rows transposed: lane = row of a 32-row group, float4 loads
-      for (int g = warp; g < LE_RB / 32; g += blockDim.x >> 5) {
-        const int r = g * 32 + lane;
+      // stage the batch's rows transposed: lane = row of a 32-row group, float4 loads; the 8
+      // warps split the 4 row groups x 2 halves of k
+      for (int g = warp; g < 2 * (LE_RB / 32); g += blockDim.x >> 5) {
+        const int r = (g >> 1) * 32 + lane;
         const int p = rowp[r];
         const int op = p < 0 ? 0 : (L.perm ? L.perm[p] : p);
         if ((L.d & 3) == 0) {
           const float4* src = reinterpret_cast<const float4*>(L.X + (int64_t)op * L.d);
-          for (int k4 = 0; k4 < L.d / 4; k4++) {
+          const int kh = (L.d / 4 + 1) / 2;  // float4s in the first half of k
+          const int k4a = (g & 1) ? kh : 0, k4b = (g & 1) ? L.d / 4 : kh;
+          for (int k4 = k4a; k4 < k4b; k4++) {
             const float4 v = p >= 0 ? __ldg(src + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
             rowx[(4 * k4 + 0) * LE_RB + r] = v.x;
             rowx[(4 * k4 + 1) * LE_RB + r] = v.y;
             rowx[(4 * k4 + 2) * LE_RB + r] = v.z;
             rowx[(4 * k4 + 3) * LE_RB + r] = v.w;
           }
-        } else {
+        } else if ((g & 1) == 0) {
           for (int k = 0; k < L.d; k++) rowx[k * LE_RB + r] = p >= 0 ? __ldg(L.X + (int64_t)op * L.d + k) : 0.0f;
         }
       }
