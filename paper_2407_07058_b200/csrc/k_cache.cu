@@ -59,7 +59,8 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
 // entries do not fit is poisoned (cand_cnt = 2^31: invalid cache, exact full-row minimum).
 template <int K>
 __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
-                            const float* __restrict__ nrm, const float* __restrict__ len, float maxlen, ErrModel em,
+                            const float* __restrict__ nrm, const float* __restrict__ len, float maxlen,
+                            const float* __restrict__ err, const float* __restrict__ maxerr, ErrModel em,
                             float* __restrict__ UBK, u64* __restrict__ rowbuf, int rbcap, unsigned* __restrict__ list,
                             unsigned* __restrict__ count, unsigned cap, unsigned* __restrict__ cand_cnt) {
   const int lane = threadIdx.x & 31;
@@ -68,6 +69,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
     const int p = p0 + lane;
     const bool valid = p < p_end;
     const float ni = valid ? nrm[p] : 0.0f, li = valid ? len[p] : 0.0f;
+    const float dl = em_delta2(valid ? err[p] : 0.0f, *maxerr);
     // running K largest chunk maxima (K distinct chunks, hence K distinct columns)
     float top[K];
 #pragma unroll
@@ -110,7 +112,7 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
         }
       }
       if (top[K - 1] != kth0 && top[K - 1] > -INFINITY)
-        thr = em_thr(em, em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen), ni, li, maxlen);
+        thr = em_thr(em, em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen, dl), ni, li, maxlen, dl);
       float bm = v[0];
 #pragma unroll
       for (int u = 1; u < 4 * U4; u++) bm = fmaxf(bm, v[u]);
@@ -128,8 +130,8 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
     }
     float ub = INFINITY;
     if (valid && top[K - 1] > -INFINITY) {
-      ub = em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen);
-      thr = em_thr(em, ub, ni, li, maxlen);
+      ub = em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen, dl);
+      thr = em_thr(em, ub, ni, li, maxlen, dl);
     } else {
       thr = -INFINITY;
     }
@@ -171,14 +173,15 @@ __global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch,
 }
 
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                             const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
+                             const float* nrm, const float* len, float maxlen, const float* err,
+                             const float* maxerr, const ErrModel& em, float* UBK,
                              u64* rowbuf, int rbcap, unsigned* list, unsigned* count, unsigned cap,
                              unsigned* cand_cnt) {
   const int rows = p_end - p_begin;
   if (rows <= 0) return APPD_OK;
   const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
 #define APPD_TOPK_SCAN(KK)                                                                                        \
-  k_topk_scan<KK><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, em, UBK, rowbuf, \
+  k_topk_scan<KK><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, err, maxerr, em, UBK, rowbuf, \
                                                rbcap, list, count, cap, cand_cnt)
   switch (K) {
     case 4: APPD_TOPK_SCAN(4); break;
@@ -844,9 +847,10 @@ __global__ void k_cm_rowub(CmParams P) {
     const int C = valid ? P.sc[p] : -1;
     const bool uni = __all_sync(0xffffffffu, C == __shfl_sync(0xffffffffu, C, 0));
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
+    const float dl = em_delta2(valid ? P.err[p] : 0.0f, *P.maxerr);
     const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;  // segments the scan wrote
     auto flush = [&](int D, float m) {
-      float ub = (m > -INFINITY && D != C && valid) ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen) : INFINITY;
+      float ub = (m > -INFINITY && D != C && valid) ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen, dl) : INFINITY;
       if (uni) {  // D is warp-uniform (segment order is the same for every lane)
 #pragma unroll
         for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
@@ -901,6 +905,7 @@ __global__ void k_cm_filter(CmParams P) {
     const bool valid = p < P.p_end;
     const int C = valid ? P.sc[p] : 0;
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
+    const float dl = em_delta2(valid ? P.err[p] : 0.0f, *P.maxerr);
     int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
     float cachedT = 0.0f;
     constexpr int U = 16;
@@ -922,14 +927,14 @@ __global__ void k_cm_filter(CmParams P) {
         if (D0 == D1) {
           if (D0 != cachedD) {
             cachedD = D0;
-            cachedT = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + D0]), ni, li, P.maxlen);
+            cachedT = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + D0]), ni, li, P.maxlen, dl);
           }
           thr = cachedT;
         } else {  // straddling segment: the most permissive of its components
           float ub = 0.0f;
           for (int D = D0; D <= D1; D++)
             if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
-          thr = em_thr(P.em, ub, ni, li, P.maxlen);
+          thr = em_thr(P.em, ub, ni, li, P.maxlen, dl);
         }
         if (v[u] >= thr) mask |= 1u << u;
       }

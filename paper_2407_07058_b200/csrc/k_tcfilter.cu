@@ -77,8 +77,10 @@ __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const fl
 // B augment = -65504 (never a maximum).
 __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, int K, const int* __restrict__ perm,
                        const float* __restrict__ c, float scale, int64_t npad, __half* __restrict__ YA,
-                       __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len) {
+                       __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
+                       float* __restrict__ err, unsigned* __restrict__ maxerr) {
   const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  float emax = 0.0f;
   for (int64_t p = (int64_t)blockIdx.x * warps + w; p < npad; p += (int64_t)gridDim.x * warps) {
     const int64_t gidx = p / 128;
     const int pl = (int)(p % 128), g = pl / 8, r = pl % 8;
@@ -87,9 +89,23 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
     const bool real = p < n;
     const int64_t i = real ? perm[p] : 0;
     float s = 0.0f;
+    // E^2 = |y^ - s (x - c)|^2: per coordinate e = (y^ - y) - s dt with y = s fl(x - c) and
+    // dt = (x - c) - fl(x - c) exact by TwoSum; y^ - y is exact (Sterbenz: y^ = fp16(y)).
+    // Only a - s dt and the squares / sum round (relative (d + 4) 2^-24 over the sum,
+    // covered by the margin applied below).
+    float e2 = 0.0f;
     for (int k = lane; k < dk; k += 32) {
       __half hv = __float2half_rn(0.0f);
-      if (real && k < d) hv = __float2half_rn(scale * (X[i * d + k] - c[k]));
+      if (real && k < d) {
+        const float xk = X[i * d + k], ck = c[k];
+        const float t = __fsub_rn(xk, ck);
+        const float bb = __fsub_rn(t, xk);
+        const float dt = __fadd_rn(__fsub_rn(xk, __fsub_rn(t, bb)), __fsub_rn(-ck, bb));  // TwoSum error
+        const float y = scale * t;
+        hv = __float2half_rn(y);
+        const float ek = __fsub_rn(__fsub_rn(__half2float(hv), y), scale * dt);
+        e2 = __fmaf_ru(ek, ek, e2);
+      }
       const float hf = __half2float(hv);
       s = fmaf(hf, hf, s);
       const int64_t off = (int64_t)g * (K / 8) * 64 + (k / 8) * 64 + r * 8 + (k % 8);  // in halves
@@ -98,6 +114,8 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) e2 = __fadd_ru(e2, __shfl_xor_sync(0xffffffffu, e2, o));
     for (int k = dk + lane; k < K; k += 32) {
       const int64_t off = (int64_t)g * (K / 8) * 64 + (k / 8) * 64 + r * 8 + (k % 8);
       __half a = __float2half_rn(0.0f), b = __float2half_rn(0.0f);
@@ -117,7 +135,20 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
     if (lane == 0) {
       nrm[p] = real ? s : 0.0f;
       len[p] = real ? sqrtf(s) : 0.0f;
+      // rounded up, with a relative margin for the rounded subtraction and squares
+      const float E = real ? __fsqrt_ru(__fmul_ru(e2, 1.0f + (float)(d + 8) * 0x1p-23f)) + 1e-30f : 0.0f;
+      err[p] = E;
+      emax = fmaxf(emax, E);
     }
+  }
+  // one atomic per block for the global maximum (a single address: atomics serialise)
+  __shared__ float wmax[32];
+  if (lane == 0) wmax[w] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int t = 0; t < warps; t++) m = fmaxf(m, wmax[t]);
+    if (m > 0.0f) atomicMax(maxerr, __float_as_uint(m));
   }
 }
 
@@ -141,14 +172,24 @@ __global__ void k_transpose_perm(const float* __restrict__ X, int64_t n, int d, 
 }
 
 // max |y^| over each TC_TMG-column segment (one warp per segment)
-__global__ void k_seg_maxlen(const float* __restrict__ len, int64_t nseg, float* __restrict__ seg_max) {
+__global__ void k_seg_maxlen(const float* __restrict__ len, const float* __restrict__ err, int64_t nseg,
+                             float* __restrict__ seg_max, float* __restrict__ seg_maxerr) {
   const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int64_t g = (int64_t)blockIdx.x * warps + w; g < nseg; g += (int64_t)gridDim.x * warps) {
-    float m = 0.0f;
-    for (int t = lane; t < TC_TMG; t += 32) m = fmaxf(m, len[g * TC_TMG + t]);
+    float m = 0.0f, me = 0.0f;
+    for (int t = lane; t < TC_TMG; t += 32) {
+      m = fmaxf(m, len[g * TC_TMG + t]);
+      me = fmaxf(me, err[g * TC_TMG + t]);
+    }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) seg_max[g] = m;
+    for (int o = 16; o; o >>= 1) {
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      me = fmaxf(me, __shfl_xor_sync(0xffffffffu, me, o));
+    }
+    if (lane == 0) {
+      seg_max[g] = m;
+      seg_maxerr[g] = me;
+    }
   }
 }
 
@@ -190,6 +231,9 @@ struct ExactParams {
   const float* len;
   const float* seg_maxlen;
   float maxlen;  // max |y^| over all points
+  const float* err;         // E_p (permuted)
+  const float* seg_maxerr;  // per segment max E
+  const float* maxerr;      // max E (device)
   const int* cs;
   const int* ce;
   const unsigned* UB;
@@ -224,7 +268,8 @@ __global__ void k_filter_tiles(ExactParams E) {
     float ub = valid ? __uint_as_float(E.UB[p]) : 0.0f;
     if (valid && E.compUB) ub = fminf(ub, __uint_as_float(E.compUB[E.comp[E.perm[p]]]));
     const float ni = valid ? E.nrm[p] : 0.0f, li = valid ? E.len[p] : 0.0f;
-    const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.maxlen) : INFINITY;
+    const float ei = valid ? E.err[p] : 0.0f, emax = *E.maxerr;
+    const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.maxlen, em_delta2(ei, emax)) : INFINITY;
     bool flagged = false;
     constexpr int U = 8;  // segments per batch: U independent coalesced loads in flight
     for (int t0 = 0; t0 < E.nseg; t0 += U) {
@@ -239,7 +284,7 @@ __global__ void k_filter_tiles(ExactParams E) {
 #pragma unroll
       for (int u = 0; u < U; u++) {
         bool want = v[u] >= thr_min && v[u] > -INFINITY;
-        if (want) want = v[u] >= em_thr(E.em, ub, ni, li, E.seg_maxlen[t0 + u]);
+        if (want) want = v[u] >= em_thr(E.em, ub, ni, li, E.seg_maxlen[t0 + u], em_delta2(ei, E.seg_maxerr[t0 + u]));
         const unsigned bal = __ballot_sync(0xffffffffu, want);
         if (bal) {
           unsigned base = 0;
@@ -438,6 +483,10 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   st->nrm = (float*)ws(c, S_TC_NRM, sizeof(float) * st->npad);
   st->len = (float*)ws(c, S_TC_LEN, sizeof(float) * st->npad);
   st->seg_maxlen = (float*)ws(c, S_TC_TML, sizeof(float) * (st->npad / TC_TMG));
+  st->err = (float*)ws(c, S_TC_ERR, sizeof(float) * st->npad + 64);
+  st->seg_maxerr = (float*)ws(c, S_TC_SEGERR, sizeof(float) * (st->npad / TC_TMG) + 64);
+  if (!st->err || !st->seg_maxerr) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc error norms");
+  st->maxerr = reinterpret_cast<unsigned*>(st->err + st->npad);
   st->perm = (int*)ws(c, S_TC_PERM, sizeof(int) * (n + 1));
   st->sc = (int*)ws(c, S_TC_SC, sizeof(int) * (n + 1));
   st->keys = (int*)ws(c, S_TC_KEYS, sizeof(int) * 2 * (n + 1));
@@ -503,14 +552,16 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
 
 static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X) {
   const int64_t n = st->n;
+  APPD_CUDA(c, cudaMemsetAsync(st->maxerr, 0, sizeof(unsigned), c->stream));
   k_pack<<<c->sm_count * 8, 256, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->scale,
-                                                  st->npad, (__half*)st->YA, (__half*)st->YB, st->nrm, st->len);
+                                                  st->npad, (__half*)st->YA, (__half*)st->YB, st->nrm, st->len,
+                                                  st->err, st->maxerr);
   APPD_LAUNCHED(c);
   const dim3 tg((unsigned)(st->npad / 32), (unsigned)((st->d + 31) / 32));
   k_transpose_perm<<<tg, dim3(32, 8), 0, c->stream>>>(X, n, (int)st->d, st->perm, st->npad, st->XTp);
   APPD_LAUNCHED(c);
   k_seg_maxlen<<<(unsigned)std::min<int64_t>(c->sm_count * 8, (st->npad / TC_TMG + 7) / 8), 256, 0, c->stream>>>(
-      st->len, st->npad / TC_TMG, st->seg_maxlen);
+      st->len, st->err, st->npad / TC_TMG, st->seg_maxlen, st->seg_maxerr);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -522,6 +573,8 @@ static void fill_scan_params(const TcState* st, TcParams* P) {
   P->nrm = st->nrm;
   P->len = st->len;
   P->seg_maxlen = st->seg_maxlen;
+  P->err = st->err;
+  P->seg_maxerr = st->seg_maxerr;
   P->cs = st->rs;
   P->ce = st->re;
   P->UB = st->UB;
@@ -551,6 +604,9 @@ static void exact_params(const TcState* st, const TcParams& P, const int* comp, 
   E->len = st->len;
   E->seg_maxlen = st->seg_maxlen;
   E->maxlen = st->maxlen_scaled;
+  E->err = st->err;
+  E->seg_maxerr = st->seg_maxerr;
+  E->maxerr = reinterpret_cast<const float*>(st->maxerr);
   E->cs = st->rs;
   E->ce = st->re;
   E->UB = st->UB;
@@ -760,7 +816,8 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
       const int nch = (int)(st->npad / 32);
       APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
       if ((s = launch_topk_scan(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
-                                st->maxlen_scaled, P.em, st->UBK, st->rowbuf, kRowBuf, st->lista, st->counters + 6,
+                                st->maxlen_scaled, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
+                                st->rowbuf, kRowBuf, st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
         return s;
       if ((s = exact_list(c, st, X, 0, nullptr, st->counters + 6, 0, nullptr))) return s;
@@ -868,6 +925,8 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.len = st->len;
   C.seg_maxlen = st->seg_maxlen;
   C.maxlen = st->maxlen_scaled;
+  C.err = st->err;
+  C.maxerr = reinterpret_cast<const float*>(st->maxerr);
   C.em = P.em;
   C.CUB = CUB;
   C.list = st->lista;

@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
             if (valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
               gb[r] = m;
               const float ni = __ldg(P.nrm + p), li = __ldg(P.len + p);
-              ub[r] = fminf(ub[r], em_upper(P.em, ni - 2.0f * m, ni, li, P.seg_maxlen[seg]));
+              ub[r] = fminf(ub[r], em_upper(P.em, ni - 2.0f * m, ni, li, P.seg_maxlen[seg],
+                                            em_delta2(__ldg(P.err + p), P.seg_maxerr[seg])));
             }
           }
         }

@@ -32,18 +32,21 @@ struct ErrModel {
   float c1, c2, k1, k2, k3, gamma;
 };
 
-__device__ __forceinline__ float em_delta(const ErrModel& e, float L, float R) { return e.c1 * (L + R) + e.c2; }
+// delta from the per-point fp16 rounding-error norms: |(y^_i - y^_j) - s (x_i - x_j)| <=
+// E_i + E_j with E_p = |y^_p - s (x_p - c)| computed exactly (k_pack, double, rounded up);
+// the worst case E_p <= c1 |y^_p| + c2 is what e.c1 / e.c2 bound
+__device__ __forceinline__ float em_delta2(float Ei, float Ej) { return (Ei + Ej) * (1.0f + 0x1p-20f) + 1e-30f; }
 __device__ __forceinline__ float em_eta(const ErrModel& e, float L, float R) {
   return e.k1 * R * (L + 0.5f * R) + e.k2 * (L * L + R * R) + e.k3 * (4.0f * R * R + (L + R) * (L + R));
 }
 // upper bound on s^2 r for a column whose Dt is dt
-__device__ __forceinline__ float em_upper(const ErrModel& e, float dt, float ni, float L, float R) {
-  const float r = sqrtf(fmaxf(dt + em_eta(e, L, R), 0.0f)) + em_delta(e, L, R);
+__device__ __forceinline__ float em_upper(const ErrModel& e, float dt, float ni, float L, float R, float delta) {
+  const float r = sqrtf(fmaxf(dt + em_eta(e, L, R), 0.0f)) + delta;
   return (1.0f + e.gamma) * r * r * (1.0f + 0x1p-18f) + 0x1p-18f * ni;
 }
 // G' threshold: a column can hold a candidate (L <= ub) only if G' >= thr
-__device__ __forceinline__ float em_thr(const ErrModel& e, float ub, float ni, float L, float R) {
-  const float r = sqrtf(ub / (1.0f - e.gamma)) + em_delta(e, L, R);
+__device__ __forceinline__ float em_thr(const ErrModel& e, float ub, float ni, float L, float R, float delta) {
+  const float r = sqrtf(ub / (1.0f - e.gamma)) + delta;
   const float T = (r * r + em_eta(e, L, R)) * (1.0f + 0x1p-18f) + 0x1p-18f * ni;
   return 0.5f * (ni - T);
 }
@@ -69,6 +72,8 @@ struct TcParams {
   const float* nrm;          // |y^_p|^2 (fp32), permuted order
   const float* len;          // |y^_p|
   const float* seg_maxlen;   // max |y^_j| over each TC_TMG-column segment
+  const float* err;          // E_p, permuted order
+  const float* seg_maxerr;   // max E_j over each TC_TMG-column segment
   const int* cs;             // per permuted row: first position of its component
   const int* ce;             // per permuted row: one past the last position
   unsigned* UB;              // per permuted row: upper bound (float bits, >= 0)
@@ -108,6 +113,8 @@ struct CmParams {
   const float* len;
   const float* seg_maxlen;
   float maxlen;
+  const float* err;     // E_p (permuted order)
+  const float* maxerr;  // max E over all points (device)
   ErrModel em;
   unsigned* CUB;        // [k][k] float bits
   unsigned* list;       // (32-column chunk << 17 | row) entries
@@ -153,7 +160,8 @@ appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsign
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
-                             const float* nrm, const float* len, float maxlen, const ErrModel& em, float* UBK,
+                             const float* nrm, const float* len, float maxlen, const float* err,
+                             const float* maxerr, const ErrModel& em, float* UBK,
                              u64* rowbuf, int rbcap, unsigned* list, unsigned* count, unsigned cap,
                              unsigned* cand_cnt);
 
