@@ -628,11 +628,6 @@ static void exact_params(const TcState* st, const TcParams& P, const int* comp, 
 // re-scans of at most this many rows run the exact row kernel instead of a tensor-core pass
 constexpr int kSmallRescan = 1024;
 
-static int col_splits_for(appd_ctx* c, int64_t row_blocks, int col_tiles) {
-  int splits = (int)std::max<int64_t>(1, (c->sm_count * 3 + row_blocks - 1) / std::max<int64_t>(row_blocks, 1));
-  return splits > col_tiles ? col_tiles : splits;
-}
-
 // filter + exact re-check of the listed (row, 128-column segment) pairs + full-row
 // fallback; compbest[comp] receives the exact minimum keys
 static appd_status exact_stage(appd_ctx* c, const ExactParams& E) {
@@ -790,7 +785,6 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     // ---- cache-building scan: 32-column maxima of every row of this rank ----
     P.rb_begin = (int)rb_begin;
     P.rb_end = (int)rb_end;
-    P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
     P.seg32 = 1;
     if (getenv("APPD_TC_BENCH")) {  // debug: time the scan variants in isolation (results discarded)
       const char* names[] = {"seg128", "seg32", "", "null-epilogue", "tmem-load-only", "no-B-copies", "null+noB"};
@@ -843,7 +837,6 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     P.rb_count = st->rb_count;
     P.rb_begin = 0;
     P.rb_end = (int)std::min<int64_t>(T, rescan_rows);  // upper bound on the listed blocks (grid sizing)
-    P.col_splits = col_splits_for(c, P.rb_end, P.col_tiles);
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 0, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
@@ -860,7 +853,6 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     // ---- no cache: every row of this rank ----
     P.rb_begin = (int)rb_begin;
     P.rb_end = (int)rb_end;
-    P.col_splits = col_splits_for(c, rb_end - rb_begin, P.col_tiles);
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 0, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
@@ -904,8 +896,6 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   P.rb_end = (int)rb_end;
   // one rank: every unordered pair is needed from one side only -> upper-triangle pass
   P.upper = c->opt.world == 1 && !getenv("APPD_CM_FULL");
-  P.col_splits = P.upper ? col_splits_for(c, (rb_end - rb_begin + 1) / 2, P.col_tiles)
-                         : col_splits_for(c, rb_end - rb_begin, P.col_tiles);
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 0, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
@@ -983,7 +973,6 @@ appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, fl
   fill_scan_params(&st, &P);
   P.rb_begin = 0;
   P.rb_end = 1;
-  P.col_splits = 1;
   P.round0 = 1;
   P.dump = tc_out;
   if ((s = launch_tcf_scan(c, 2, P))) return s;

@@ -12,6 +12,7 @@
 // Shared-memory traffic of an SS-mode MMA is (M + N) K 2 bytes per M N K MACs: with
 // M = 128, N = 256 that is 96 B/clk at the tensor rate, below the 128 B/clk of shared
 // memory; the 512-row block makes each column-operand byte read from L2 serve 512 rows.
+#include <algorithm>
 #include <cstdlib>
 
 #include "tc_common.cuh"
@@ -136,37 +137,40 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
   const uint32_t tmem = *tmem_slot;
 
   const int nrb = P.rb_list ? *P.rb_count : (P.rb_end - P.rb_begin);
-  // upper mode (symmetric pass): row block rb scans only column tiles >= 2 rb; blocks rb
-  // and (last - rb) form one pair of constant total length, cut into col_splits items
-  const int items = (P.upper ? (nrb + 1) / 2 : nrb) * P.col_splits;
-  const int per_split = (P.col_tiles + P.col_splits - 1) / P.col_splits;
-  // k-th (k = 0, 1) contiguous piece of work item it: row block and column-tile range
-  auto subitem = [&](int it, int k, int& rb, int& ct0, int& ct1) -> bool {
-    const int sp = it % P.col_splits;
+  // Work = a sequence of column-tile units, split evenly over the persistent CTAs (at
+  // most one tile of imbalance).  Plain mode: row block b's units are its col_tiles
+  // tiles.  Upper mode (symmetric pass): row block rb scans only column tiles >= 2 rb;
+  // blocks rb and (last - rb) are laid end to end into one virtual row of constant
+  // length L, so a CTA's contiguous range touches few row blocks (one A load each).
+  const int C = P.col_tiles;
+  const int L = P.upper ? 2 * C - 2 * (P.rb_begin + P.rb_end - 1) : C;
+  const int vrows = P.upper ? nrb / 2 : nrb;
+  const int U = vrows * L + ((P.upper && (nrb & 1)) ? C - 2 * (P.rb_begin + nrb / 2) : 0);
+  const int ubeg = (int)((int64_t)blockIdx.x * U / gridDim.x), uend = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+  // next piece (one row block, column tiles [ct0, ct1)) of this CTA's range; advances u
+  auto next_piece = [&](int& u, int& rb, int& ct0, int& ct1) -> bool {
+    if (u >= uend) return false;
+    const int q = u / L, x = u % L;
+    const int left = uend - u;
     if (!P.upper) {
-      if (k) return false;
-      const int b = it / P.col_splits;
-      rb = P.rb_list ? __ldg(P.rb_list + b) : P.rb_begin + b;
-      ct0 = sp * per_split;
-      ct1 = min(P.col_tiles, ct0 + per_split);
-      return ct0 < ct1;
+      rb = P.rb_list ? __ldg(P.rb_list + q) : P.rb_begin + q;
+      ct0 = x;
+      ct1 = min(C, x + left);
+    } else {
+      const int rba = P.rb_begin + q, rbb = P.rb_end - 1 - q;
+      const int la = C - 2 * rba;
+      if (x < la) {
+        rb = rba;
+        ct0 = 2 * rba + x;
+        ct1 = 2 * rba + min(la, x + left);
+      } else {
+        rb = rbb;
+        ct0 = 2 * rbb + (x - la);
+        ct1 = 2 * rbb + min(L - la, x - la + left);
+      }
     }
-    const int q = it / P.col_splits;
-    const int rba = P.rb_begin + q, rbb = P.rb_end - 1 - q;
-    const int la = P.col_tiles - 2 * rba, lb = rbb != rba ? P.col_tiles - 2 * rbb : 0;
-    const int tot = la + lb;
-    const int x0 = (int)((int64_t)sp * tot / P.col_splits), x1 = (int)((int64_t)(sp + 1) * tot / P.col_splits);
-    if (k == 0) {
-      rb = rba;
-      ct0 = 2 * rba + x0;
-      ct1 = 2 * rba + min(x1, la);
-      return x0 < la && ct0 < ct1;
-    }
-    if (lb == 0 || x1 <= la) return false;
-    rb = rbb;
-    ct0 = 2 * rbb + max(x0, la) - la;
-    ct1 = 2 * rbb + x1 - la;
-    return ct0 < ct1;
+    u += ct1 - ct0;
+    return true;
   };
 
   if (warp == 0) {
@@ -175,10 +179,8 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
       int stage = 0;
       uint32_t ph = 0, aph = 0;
       bool first = true;
-      for (int it = blockIdx.x; it < items; it += gridDim.x)
-      for (int sub = 0; sub < 2; sub++) {
-        int rb, ct0, ct1;
-        if (!subitem(it, sub, rb, ct0, ct1)) continue;
+      int rb, ct0, ct1;
+      for (int u = ubeg; next_piece(u, rb, ct0, ct1);) {
         if (!first) {
           ptx::mbar_wait(aempty, aph);
           aph ^= 1;
@@ -212,10 +214,8 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
       const uint32_t b0 = ptx::smem_u32(sB);
       int stage = 0;
       uint32_t ph = 0, aph = 0, tph[TC_NBUF] = {};
-      for (int it = blockIdx.x; it < items; it += gridDim.x)
-      for (int sub = 0; sub < 2; sub++) {
-        int rb, ct0, ct1;
-        if (!subitem(it, sub, rb, ct0, ct1)) continue;
+      int rb, ct0, ct1;
+      for (int u = ubeg; next_piece(u, rb, ct0, ct1);) {
         ptx::mbar_wait(afull, aph);
         aph ^= 1;
         for (int ct = ct0; ct < ct1; ct++) {
@@ -251,10 +251,8 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
     uint32_t tph[TC_NBUF] = {};
-    for (int it = blockIdx.x; it < items; it += gridDim.x)
-    for (int sub = 0; sub < 2; sub++) {
-      int rb, ct0, ct1;
-      if (!subitem(it, sub, rb, ct0, ct1)) continue;
+    int rb, ct0, ct1;
+    for (int u = ubeg; next_piece(u, rb, ct0, ct1);) {
       // lean per-row state (registers): component range and, for the bound, the best
       // maximum so far and the running upper bound.  The cache-building pass (SEG32)
       // needs no bound.  Row p = rb * 512 + r * 128 + q * 32 + lane.
@@ -298,7 +296,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
             continue;
           }
           if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
-            if (it == (int)blockIdx.x && P.dump) {
+            if (P.dump && rb == P.rb_begin) {
               const int rloc = r * TC_M + q * 32 + lane;
               for (int t = 0; t < WCOLS; t++) P.dump[(int64_t)rloc * P.col_tiles * TC_N + h0 + t] = v[t];
             }
@@ -387,8 +385,11 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
     cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = 1;
   }
-  const int items = (P.upper ? (P.rb_end - P.rb_begin + 1) / 2 : P.rb_end - P.rb_begin) * P.col_splits;
-  int grid = c->sm_count < items ? c->sm_count : items;
+  // column-tile units (host upper bound when the row-block list is read on the device)
+  const int64_t nrb = P.rb_end - P.rb_begin;
+  const int64_t units = P.upper ? (nrb + 1) / 2 * (int64_t)(2 * P.col_tiles - 2 * (P.rb_begin + P.rb_end - 1))
+                                : nrb * P.col_tiles;
+  int grid = (int)std::min<int64_t>(c->sm_count, units);
   if (grid < 1) return APPD_OK;
   static const int exp_pass = getenv("APPD_TC_EXPERIMENT") ? atoi(getenv("APPD_TC_EXPERIMENT")) : 0;
   int ep = exp_pass;

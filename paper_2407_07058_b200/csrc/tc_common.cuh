@@ -85,15 +85,14 @@ struct TcParams {
   int stages;                // shared-memory ring depth for the column operand
   int rb_begin, rb_end;      // this rank's 512-row blocks (permuted order)
   int col_tiles;             // npad / 256
-  int col_splits;
   ErrModel em;
   int round0;   // singletons (eligibility = j != i)
   float* dump;  // PASS 2 (test hook) only: raw accumulator of the first item
   // TM granularity: 0 -> one maximum per TC_TMG (128) columns; 1 -> per 32 columns
   // (the cache-building round 0: 4x the maxima, 1/4 of the exact re-check work)
   int seg32;
-  // optional row-block list (re-scan rounds): items = *rb_count x col_splits over
-  // rb_list[]; when null the blocks rb_begin .. rb_end-1 are scanned
+  // optional row-block list (re-scan rounds): the *rb_count blocks of
+  // rb_list[] (col_tiles units each); when null the blocks rb_begin .. rb_end-1
   const int* rb_list;
   const int* rb_count;
   // symmetric pass: row block rb scans column tiles >= 2 rb only (rb_list must be null)
