@@ -51,138 +51,292 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
   return base + incl - cnt;
 }
 
-// One pass over TM32 (thread per row, 32 loads in flight): the running K largest chunk
-// maxima give a running threshold; every chunk passing it is buffered (the threshold only
-// tightens as the K-th largest grows, so the buffer holds every chunk that passes the
-// final threshold thrK).  At the end UBK is stored and the buffered chunks passing thrK
-// are listed.  A row whose buffer overflows re-reads its TM32 row once; a row whose list
-// entries do not fit is poisoned (cand_cnt = 2^31: invalid cache, exact full-row minimum).
+// One pass over TM32.  A CTA of TK_PARTS warps takes 32 rows (lane = row); warp w scans
+// the w-th quarter of the chunks, 32 maxima per batch with the next batch's loads in
+// flight (cp.async ring), storing the maximum of every 8-chunk group (shared memory)
+// and keeping the running K largest BATCH maxima (one insertion per 32 chunks).  K
+// batches hold K distinct chunks, so the merged K-th largest batch maximum gK is a lower
+// bound of the row's K-th largest chunk maximum.  Every group whose maximum reaches
+// t = min(thr(gK), gK) is then read again (two 16-byte loads, TK_RG groups per lane in
+// flight): its chunks >= t are kept (shared memory) and enter the chunk-level top-K.
+// Every chunk of the row's K largest is >= gK >= t, so the merged chunk-level list is
+// the exact K largest, which give UBK and the listing threshold thrK >= t; the kept
+// chunks passing thrK are listed.  A (row, quarter) keeping more than TK_SEL chunks reads
+// its flagged groups once more; a row whose list entries do not fit is poisoned
+// (cand_cnt = 2^31: invalid cache, exact full-row minimum).
+constexpr int TK_PARTS = 4;
+constexpr int TK_BATCH = 32;  // chunk maxima per batch (8 x 128-bit loads)
+constexpr int TK_SEL = 16;    // kept chunks per (row, quarter) in shared memory
+constexpr int TK_RG = 4;      // flagged groups re-read together
+constexpr int TK_STAGES = 4;  // cp.async ring depth (batches; 3 in flight while one is processed)
+
+// 16-byte asynchronous global -> shared copy (L2 only); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// insert x into the descending list top[0..K) (branch-free network)
 template <int K>
-__global__ void k_topk_scan(const float* __restrict__ TM32, int64_t ld, int nch, int p_begin, int p_end,
-                            const float* __restrict__ nrm, const float* __restrict__ len, float maxlen,
-                            const float* __restrict__ err, const float* __restrict__ maxerr, ErrModel em,
-                            float* __restrict__ UBK, u64* __restrict__ rowbuf, int rbcap, unsigned* __restrict__ list,
-                            unsigned* __restrict__ count, unsigned cap, unsigned* __restrict__ cand_cnt) {
-  const int lane = threadIdx.x & 31;
-  constexpr int U4 = 8;  // 8 x 128-bit loads = 32 chunk maxima per batch
-  for (int p0 = p_begin + (blockIdx.x * blockDim.x + threadIdx.x) - lane; p0 < p_end; p0 += gridDim.x * blockDim.x) {
+__device__ __forceinline__ void topk_insert(float (&top)[K], float x) {
+#pragma unroll
+  for (int t = 0; t < K; t++) {
+    const float hi = fmaxf(top[t], x);
+    x = fminf(top[t], x);
+    top[t] = hi;
+  }
+}
+
+// merge the other quarters' descending lists (shared memory) into top
+template <int K>
+__device__ __forceinline__ void topk_merge(float (&top)[K], const float (*stop)[K][32], int w, int lane) {
+#pragma unroll
+  for (int o = 0; o < TK_PARTS; o++) {
+    if (o == w) continue;
+    for (int t = 0; t < K; t++) {
+      const float x = stop[o][t][lane];
+      if (!(x > top[K - 1])) break;  // lists are descending
+      topk_insert(top, x);
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __restrict__ TM32, int nch, int p_begin,
+                                                             int p_end, const float* __restrict__ nrm,
+                                                             const float* __restrict__ len, float maxlen,
+                                                             const float* __restrict__ err,
+                                                             const float* __restrict__ maxerr, ErrModel em,
+                                                             float* __restrict__ UBK, unsigned* __restrict__ list,
+                                                             unsigned* __restrict__ count, unsigned cap,
+                                                             unsigned* __restrict__ cand_cnt, int ngq) {
+  extern __shared__ float sgm[];                  // [TK_PARTS][ngq][32] 8-chunk group maxima
+  __shared__ float stop[TK_PARTS][K][32];         // per-quarter top-K lists for the merges
+  __shared__ float sval[TK_PARTS][TK_SEL][32];    // kept chunks: value
+  __shared__ unsigned short sidx[TK_PARTS][TK_SEL][32];  //   and chunk index
+  __shared__ int slost[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int U4 = TK_BATCH / 4;
+  const int nch4 = (nch + 3) >> 2;
+  const int g0 = (int)((int64_t)w * nch4 / TK_PARTS), g1 = (int)((int64_t)(w + 1) * nch4 / TK_PARTS);
+  const int cb = 4 * g0, cend = min(nch, 4 * g1);  // this warp's chunk range
+  const int nbat = (cend - cb + TK_BATCH - 1) / TK_BATCH;
+  const int ng = (cend - cb + 7) / 8;               // 8-chunk groups of this quarter (<= ngq)
+  float* gm = sgm + (size_t)w * ngq * 32 + lane;    // gm[g * 32]
+  // cp.async ring after the group maxima: [TK_PARTS][TK_STAGES][U4][32] float4
+  float4* ring = reinterpret_cast<float4*>(sgm + (size_t)TK_PARTS * ngq * 32) + (size_t)w * TK_STAGES * U4 * 32 + lane;
+  const float4 NEG = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  for (int p0 = p_begin + 32 * blockIdx.x; p0 < p_end; p0 += 32 * gridDim.x) {
     const int p = p0 + lane;
     const bool valid = p < p_end;
-    const float ni = valid ? nrm[p] : 0.0f, li = valid ? len[p] : 0.0f;
-    const float dl = em_delta2(valid ? err[p] : 0.0f, *maxerr);
-    // running K largest chunk maxima (K distinct chunks, hence K distinct columns)
+    if (w == 0) slost[lane] = 0;
+    const float4* row4 = reinterpret_cast<const float4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
+    // the 16-byte group of chunks c .. c+3 (c a multiple of 4; chunks past cend read as -inf)
+    auto load4 = [&](int c) -> float4 {
+      float4 x = (valid && c < cend) ? __ldcs(row4 + (int64_t)(c >> 2) * 512) : NEG;
+      if (c + 1 >= cend) x.y = -INFINITY;
+      if (c + 2 >= cend) x.z = -INFINITY;
+      if (c + 3 >= cend) x.w = -INFINITY;
+      return x;
+    };
+    // ---- scan: group maxima and the top-K of group maxima.  Batches are staged by
+    // cp.async into a TK_STAGES ring (each lane copies and reads only its own row's 16-byte
+    // pieces, so its own wait_group orders them; no warp synchronisation)
     float top[K];
 #pragma unroll
     for (int t = 0; t < K; t++) top[t] = -INFINITY;
-    float thr = -INFINITY;
-    int nb = 0;
-    u64* buf = rowbuf + (int64_t)(valid ? p : 0) * rbcap;
-    const float4* row4 = reinterpret_cast<const float4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
-    // software pipeline: the next batch's loads are in flight while this batch is processed
-    float4 nx[U4];
+    auto issue = [&](int b) {
+      if (b < nbat) {
 #pragma unroll
-    for (int u = 0; u < U4; u++)
-      nx[u] = (valid && 4 * u < nch) ? __ldcs(row4 + (int64_t)u * 512)
-                                      : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-    for (int c0 = 0; c0 < nch; c0 += 4 * U4) {
-      float v[4 * U4];
-#pragma unroll
-      for (int u = 0; u < U4; u++) {
-        v[4 * u] = nx[u].x;
-        v[4 * u + 1] = nx[u].y;
-        v[4 * u + 2] = nx[u].z;
-        v[4 * u + 3] = nx[u].w;
+        for (int u = 0; u < U4; u++) {
+          const int c = cb + b * TK_BATCH + 4 * u;
+          const bool ok = valid && c < cend;
+          cp_async16(&ring[((b % TK_STAGES) * U4 + u) * 32], row4 + (int64_t)((ok ? c : cb) >> 2) * 512, ok ? 16 : 0);
+        }
       }
-      const int c1 = c0 + 4 * U4;
+      cp_async_commit();
+    };
 #pragma unroll
-      for (int u = 0; u < U4; u++)
-        nx[u] = (valid && c1 + 4 * u < nch) ? __ldcs(row4 + (int64_t)((c1 >> 2) + u) * 512)
-                                            : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      const float kth0 = top[K - 1];
+    for (int b = 0; b < TK_STAGES - 1; b++) issue(b);
+    for (int b = 0; b < nbat; b++) {
+      issue(b + TK_STAGES - 1);
+      cp_async_wait<TK_STAGES - 1>();
+      float4 v[U4];
 #pragma unroll
-      for (int u = 0; u < 4 * U4; u++) {
-        if (v[u] > top[K - 1]) {  // branch-free insertion into the descending list
-          float x = v[u];
+      for (int u = 0; u < U4; u++) v[u] = ring[((b % TK_STAGES) * U4 + u) * 32];
+      if (cb + (b + 1) * TK_BATCH > cend) {  // the quarter's ragged last batch (warp-uniform)
 #pragma unroll
-          for (int t = 0; t < K; t++) {
-            const float hi = fmaxf(top[t], x);
-            x = fminf(top[t], x);
-            top[t] = hi;
+        for (int u = 0; u < U4; u++) {
+          const int c = cb + b * TK_BATCH + 4 * u;
+          if (c >= cend) v[u].x = -INFINITY;
+          if (c + 1 >= cend) v[u].y = -INFINITY;
+          if (c + 2 >= cend) v[u].z = -INFINITY;
+          if (c + 3 >= cend) v[u].w = -INFINITY;
+        }
+      }
+      // (rows past p_end hold zero-filled data; nothing of theirs is written)
+      float bm = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < TK_BATCH / 8; q++) {
+        const float4 a = v[2 * q], c = v[2 * q + 1];
+        const float m = fmax3f(fmax3f(a.x, a.y, a.z), fmax3f(a.w, c.x, c.y), fmaxf(c.z, c.w));
+        const int g = b * (TK_BATCH / 8) + q;
+        if (g < ng) gm[g * 32] = m;
+        bm = fmaxf(bm, m);
+      }
+      // top-K of BATCH maxima: K batches hold K distinct chunks
+      if (bm > top[K - 1]) topk_insert(top, bm);
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int t = 0; t < K; t++) stop[w][t][lane] = top[t];
+    __syncthreads();
+    topk_merge(top, stop, w, lane);
+    const float gK = top[K - 1];
+    float ni = 0.0f, li = 0.0f, dl = 0.0f;
+    if (valid) {
+      ni = nrm[p];
+      li = len[p];
+      dl = em_delta2(err[p], *maxerr);
+    }
+    // capture threshold t (fewer than K finite group maxima: every finite chunk)
+    float tcap = valid ? -INFINITY : INFINITY;
+    if (valid && gK > -INFINITY) tcap = fminf(gK, em_thr(em, em_upper(em, ni - 2.0f * gK, ni, li, maxlen, dl), ni, li, maxlen, dl));
+    auto flagged = [&](int g) {
+      const float m = gm[g * 32];
+      return m >= tcap && m > -INFINITY;
+    };
+    // ---- re-read the flagged groups (bit masks, ng <= 128): keep chunks >= t,
+    // chunk-level top-K
+    unsigned long long fm0 = 0, fm1 = 0;
+    for (int g = 0; g < ng; g++) {
+      if (!flagged(g)) continue;
+      if (g < 64) fm0 |= 1ull << g;
+      else fm1 |= 1ull << (g - 64);
+    }
+    int jmax = __popcll(fm0) + __popcll(fm1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+#pragma unroll
+    for (int t = 0; t < K; t++) top[t] = -INFINITY;
+    unsigned kept = 0;
+    for (int j = 0; j < jmax; j += TK_RG) {
+      int gg[TK_RG];
+      float4 a[TK_RG], bq[TK_RG];
+#pragma unroll
+      for (int r = 0; r < TK_RG; r++) {
+        if (fm0) {
+          gg[r] = __ffsll(fm0) - 1;
+          fm0 &= fm0 - 1;
+        } else if (fm1) {
+          gg[r] = 63 + __ffsll(fm1);
+          fm1 &= fm1 - 1;
+        } else {
+          gg[r] = -1;
+        }
+        const int c = cb + 8 * gg[r];
+        a[r] = gg[r] >= 0 ? load4(c) : NEG;
+        bq[r] = gg[r] >= 0 ? load4(c + 4) : NEG;
+      }
+#pragma unroll
+      for (int r = 0; r < TK_RG; r++) {
+        const float vv[8] = {a[r].x, a[r].y, a[r].z, a[r].w, bq[r].x, bq[r].y, bq[r].z, bq[r].w};
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (vv[u] >= tcap && vv[u] > -INFINITY) {
+            if (kept < TK_SEL) {
+              sval[w][kept][lane] = vv[u];
+              sidx[w][kept][lane] = (unsigned short)(cb + 8 * gg[r] + u);
+            }
+            kept++;
+            if (vv[u] > top[K - 1]) topk_insert(top, vv[u]);
           }
-        }
-      }
-      if (top[K - 1] != kth0 && top[K - 1] > -INFINITY)
-        thr = em_thr(em, em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen, dl), ni, li, maxlen, dl);
-      float bm = v[0];
-#pragma unroll
-      for (int u = 1; u < 4 * U4; u++) bm = fmaxf(bm, v[u]);
-      if (bm >= thr && bm > -INFINITY) {
-        unsigned mask = 0;
-#pragma unroll
-        for (int u = 0; u < 4 * U4; u++) mask |= (v[u] >= thr && v[u] > -INFINITY) ? (1u << u) : 0u;
-        while (mask) {
-          const int u = __ffs(mask) - 1;
-          mask &= mask - 1;
-          if (nb < rbcap) buf[nb] = ((u64)(unsigned)(c0 + u) << 32) | __float_as_uint(v[u]);
-          nb++;
-        }
       }
     }
-    float ub = INFINITY;
+    __syncthreads();  // every warp has merged the group-level lists
+#pragma unroll
+    for (int t = 0; t < K; t++) stop[w][t][lane] = top[t];
+    __syncthreads();
+    topk_merge(top, stop, w, lane);
+    // fewer than K finite chunks: UBK = inf and every finite chunk is listed
+    float ub = INFINITY, thr = tcap;
     if (valid && top[K - 1] > -INFINITY) {
       ub = em_upper(em, ni - 2.0f * top[K - 1], ni, li, maxlen, dl);
       thr = em_thr(em, ub, ni, li, maxlen, dl);
-    } else {
-      thr = -INFINITY;
     }
-    if (valid) UBK[p] = ub;
-    // emit: count, one warp allocation, write
-    const bool over = nb > rbcap;
+    if (valid && w == 0) UBK[p] = ub;
+    // ---- list the kept chunks passing thrK: count, one warp allocation, write
     unsigned mine = 0;
-    if (valid && !over) {
-      for (int j = 0; j < nb; j++) mine += __uint_as_float((unsigned)buf[j]) >= thr;
-    } else if (valid) {
-      for (int c = 0; c < nch; c++) {
-        const float v = TM32[tm32_index(c, p, nch)];
-        mine += v >= thr && v > -INFINITY;
+    if (kept <= TK_SEL) {
+      for (unsigned t = 0; t < kept; t++) mine += sval[w][t][lane] >= thr;
+    } else {
+      for (int g = 0; g < ng; g++) {
+        if (!flagged(g)) continue;
+        const float4 x0 = load4(cb + 8 * g), x1 = load4(cb + 8 * g + 4);
+        const float vv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int u = 0; u < 8; u++) mine += vv[u] >= thr && vv[u] > -INFINITY;
       }
     }
     unsigned slot = warp_alloc(count, mine);
     bool lost = false;
-    if (valid && !over) {
-      for (int j = 0; j < nb; j++) {
-        const u64 e = buf[j];
-        if (__uint_as_float((unsigned)e) >= thr) {
-          if (slot < cap) list[slot] = ((unsigned)(e >> 32) << LIST_SHIFT) | (unsigned)p;
+    if (kept <= TK_SEL) {
+      for (unsigned t = 0; t < kept; t++)
+        if (sval[w][t][lane] >= thr) {
+          if (slot < cap) list[slot] = ((unsigned)sidx[w][t][lane] << LIST_SHIFT) | (unsigned)p;
           else lost = true;
           slot++;
         }
-      }
-    } else if (valid) {
-      for (int c = 0; c < nch; c++) {
-        const float v = TM32[tm32_index(c, p, nch)];
-        if (v >= thr && v > -INFINITY) {
-          if (slot < cap) list[slot] = ((unsigned)c << LIST_SHIFT) | (unsigned)p;
-          else lost = true;
-          slot++;
-        }
+    } else {  // more than TK_SEL kept chunks (rare): read the flagged groups again
+      for (int g = 0; g < ng; g++) {
+        if (!flagged(g)) continue;
+        const float4 x0 = load4(cb + 8 * g), x1 = load4(cb + 8 * g + 4);
+        const float vv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (vv[u] >= thr && vv[u] > -INFINITY) {
+            if (slot < cap) list[slot] = ((unsigned)(cb + 8 * g + u) << LIST_SHIFT) | (unsigned)p;
+            else lost = true;
+            slot++;
+          }
       }
     }
-    if (lost) cand_cnt[p] = 0x80000000u;  // poisoned: later appends cannot wrap it back below the cap
+    if (lost) slost[lane] = 1;
+    __syncthreads();  // shared state reused by the next row group
+    if (w == 0 && valid && slost[lane]) cand_cnt[p] = 0x80000000u;  // poisoned (cannot wrap back below the cap)
   }
 }
 
-appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
                              const float* nrm, const float* len, float maxlen, const float* err,
-                             const float* maxerr, const ErrModel& em, float* UBK,
-                             u64* rowbuf, int rbcap, unsigned* list, unsigned* count, unsigned cap,
-                             unsigned* cand_cnt) {
+                             const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
+                             unsigned cap, unsigned* cand_cnt) {
   const int rows = p_end - p_begin;
   if (rows <= 0) return APPD_OK;
-  const int grid = std::min(c->sm_count * 8, (rows + 127) / 128);
-#define APPD_TOPK_SCAN(KK)                                                                                        \
-  k_topk_scan<KK><<<grid, 128, 0, c->stream>>>(TM32, ld, nch, p_begin, p_end, nrm, len, maxlen, err, maxerr, em, UBK, rowbuf, \
-                                               rbcap, list, count, cap, cand_cnt)
+  const int grid = std::min(c->sm_count * 16, (rows + 31) / 32);
+  // groups per quarter: the largest quarter has ceil(ceil(nch/4)/TK_PARTS) 16-byte groups
+  const int q4 = ((nch + 3) / 4 + TK_PARTS - 1) / TK_PARTS;
+  const int ngq = (4 * q4 + 7) / 8;
+  const size_t smem = sizeof(float) * TK_PARTS * ngq * 32 + sizeof(float4) * TK_PARTS * TK_STAGES * (TK_BATCH / 4) * 32;
+  if (ngq > 128) return fail(c, APPD_ERR_UNSUPPORTED, "top-K scan: %d chunks per row", nch);
+#define APPD_TOPK_SCAN(KK)                                                                                     \
+  do {                                                                                                         \
+    cudaFuncSetAttribute(k_topk_scan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);            \
+    k_topk_scan<KK><<<grid, 32 * TK_PARTS, smem, c->stream>>>(TM32, nch, p_begin, p_end, nrm, len, maxlen, err, \
+                                                              maxerr, em, UBK, list, count, cap, cand_cnt, ngq); \
+  } while (0)
   switch (K) {
     case 4: APPD_TOPK_SCAN(4); break;
     case 8: APPD_TOPK_SCAN(8); break;
@@ -370,6 +524,8 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
         }
       }
       __syncthreads();
+      // warp w holds rows 16 w .. 16 w + 15: skip the padding of a chunk's ragged last batch
+      if (16 * warp < nb) {
       float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -462,6 +618,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
               if (key[a][b] != KEY_NONE) atomicMin(L.WCM + (int64_t)Ca[a] * L.k + Dq[b], key[a][b]);
         }
       }
+      }  // 16 * warp < nb
       __syncthreads();
     }
   }

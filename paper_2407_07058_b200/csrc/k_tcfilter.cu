@@ -27,7 +27,6 @@
 namespace appd {
 
 // per-row chunk buffer of the fused top-K scan (running threshold)
-constexpr int kRowBuf = 96;
 
 // ---------------------------------------------------------------------------
 // preparation kernels
@@ -533,8 +532,6 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
     st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
     if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");
-    st->rowbuf = (u64*)ws(c, S_TC_ROWBUF, sizeof(u64) * st->npad * kRowBuf);
-    if (!st->rowbuf) return fail(c, APPD_ERR_OUT_OF_MEMORY, "top-K row buffer");
     st->rows_list = (int*)ws(c, S_TC_ROWLIST, sizeof(int) * (n + 1));
     st->XT = (float*)ws(c, S_TC_XTO, sizeof(float) * st->npad * d);
     if (!st->rows_list || !st->XT) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate cache workspace");
@@ -809,9 +806,9 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (p_end > p_begin) {
       const int nch = (int)(st->npad / 32);
       APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
-      if ((s = launch_topk_scan(c, st->topk, st->TM, st->npad, nch, p_begin, p_end, st->nrm, st->len,
+      if ((s = launch_topk_scan(c, st->topk, st->TM, nch, p_begin, p_end, st->nrm, st->len,
                                 st->maxlen_scaled, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
-                                st->rowbuf, kRowBuf, st->lista, st->counters + 6,
+                                st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
         return s;
       if ((s = exact_list(c, st, X, 0, nullptr, st->counters + 6, 0, nullptr))) return s;
@@ -884,7 +881,6 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
   APPD_LAUNCHED(c);
   if ((s = tcf_pack(c, st, X))) return s;
-  APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));
   APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
   unsigned* CUB = st->compUB;  // k x k <= 128 x 128 words (the buffer holds n >= k^2 words or more)
   APPD_CUDA(c, cudaMemsetAsync(CUB, 0x7F, sizeof(unsigned) * k * k, c->stream));  // ~3.4e38: permissive
@@ -897,7 +893,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   // one rank: every unordered pair is needed from one side only -> upper-triangle pass
   P.upper = c->opt.world == 1 && !getenv("APPD_CM_FULL");
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
-  if ((s = launch_tcf_scan(c, 0, P))) return s;
+  if ((s = launch_tcf_scan(c, 7, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
   CmParams C;
   memset(&C, 0, sizeof C);

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
             // eligible maximum of G' over this (row, segment); a warp's rows are
             // consecutive, so the store is coalesced ([segment][row] layout)
             if (valid) P.TM[tm_index(seg, p, P.col_tiles * (TC_N / TC_TMG))] = m;
-            if (valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
+            if (PASS == 0 && valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
               gb[r] = m;
               const float ni = __ldg(P.nrm + p), li = __ldg(P.len + p);
               ub[r] = fminf(ub[r], em_upper(P.em, ni - 2.0f * m, ni, li, P.seg_maxlen[seg],
@@ -371,8 +371,9 @@ int tcf_stages(int K) {
   return 0;
 }
 
-// pass 0: scan (128-column maxima), 1: scan with 32-column maxima (cache-building
-// round), 2: test hook (raw accumulators).  With a row-block list the grid is sized
+// pass 0: scan (TC_TMG-column maxima + row bound UB), 1: scan with 32-column maxima
+// (cache-building round), 2: test hook (raw accumulators), 7: TC_TMG-column maxima only
+// (component-matrix pass: its bounds come from k_cm_rowub).  With a row-block list the grid is sized
 // for the host's upper bound P.rb_end - P.rb_begin; the kernel reads the count.
 appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   // at least 120 KB so that exactly one CTA (and one 512-column TMEM allocation) fits per SM
@@ -383,6 +384,7 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
     cudaFuncSetAttribute(k_tcf_scan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_tcf_scan<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_done = 1;
   }
   // column-tile units (host upper bound when the row-block list is read on the device)
@@ -408,6 +410,7 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
     k_tcf_scan<6><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
   } else if (pass == 0) k_tcf_scan<0><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
   else if (pass == 1) k_tcf_scan<0, true><<<grid, EpiCfg<true>::threads, smem, c->stream>>>(P);
+  else if (pass == 7) k_tcf_scan<7><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
   else k_tcf_scan<2><<<1, EpiCfg<false>::threads, smem, c->stream>>>(P);
   APPD_LAUNCHED(c);
   return APPD_OK;

@@ -158,11 +158,10 @@ appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsign
                                  unsigned* run_nb, unsigned* item_start, int4* items);
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
-appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int64_t ld, int nch, int p_begin, int p_end,
+appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
                              const float* nrm, const float* len, float maxlen, const float* err,
-                             const float* maxerr, const ErrModel& em, float* UBK,
-                             u64* rowbuf, int rbcap, unsigned* list, unsigned* count, unsigned cap,
-                             unsigned* cand_cnt);
+                             const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
+                             unsigned cap, unsigned* cand_cnt);
 
 
 size_t tcf_smem_bytes(int K, int stages);
