@@ -783,107 +783,143 @@ __global__ void k_comp_ub(int n, const int* __restrict__ perm, const int* __rest
 
 // ---------------------------------------------------------------------------
 // Exact minimum eligible edge of a list of rows (original indices): small re-scans
-// and rows whose cache overflowed.  Work item = 8 listed rows x 1024 columns; each
-// thread holds 4 columns, every column value loaded once serves the 8 rows (rows in
-// shared memory).  XT: d x ldx original-order transpose (zero padded to ldx).
-// comp == nullptr: singletons (eligible = j != i).
+// and rows whose cache overflowed.  Work item = 16 listed rows x 256 columns; each
+// thread holds one column, every column value loaded once serves the 16 rows (rows in
+// shared memory, staged when the row group changes); the next 8 coordinates' column
+// values are loaded while the current ones are used.  A CTA takes a contiguous range
+// of items (row group major) and keeps each row's best key per thread, reduced over
+// the CTA only when the row group changes.  XT: d x ldx original-order transpose (zero
+// padded to ldx).  comp == nullptr: singletons (eligible = j != i).
 // ---------------------------------------------------------------------------
-constexpr int RE_R = 8, RE_COLS = 1024;
-__global__ void __launch_bounds__(256) k_rows_exact(const float* __restrict__ XT, int64_t ldx, int n, int d,
-                                                   const int* __restrict__ rows, const unsigned* __restrict__ nrows,
-                                                   const int* __restrict__ comp, u64* __restrict__ compbest) {
+constexpr int RE_R = 16, RE_COLS = 256;
+template <bool FULL>  // FULL: d % 16 == 0 (no coordinate guards in the inner loop)
+__global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__ XT, int64_t ldx, int n, int d,
+                                                      const int* __restrict__ rows, const unsigned* __restrict__ nrows,
+                                                      const int* __restrict__ comp, u64* __restrict__ compbest) {
   extern __shared__ float xr[];  // [d][RE_R]
   __shared__ u64 red[8][RE_R];
+  __shared__ int sri[RE_R], sci[RE_R];
   const int nr = (int)*nrows;
   const int ngroups = (nr + RE_R - 1) / RE_R;
   const int nblk = (n + RE_COLS - 1) / RE_COLS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int item = blockIdx.x; item < ngroups * nblk; item += gridDim.x) {
-    const int g = item / nblk, blk = item % nblk;
-    int ri[RE_R], ci[RE_R];
+  constexpr int KB = 8;
+  const int64_t total = (int64_t)ngroups * nblk;
+  const int i0 = (int)(total * blockIdx.x / gridDim.x), i1 = (int)(total * (blockIdx.x + 1) / gridDim.x);
+  u64 best[RE_R];
+  int g_cur = -1;
+  // reduce the per-thread minima of row group g_cur over the CTA, one atomic per row
+  auto flush = [&]() {
 #pragma unroll
     for (int r = 0; r < RE_R; r++) {
-      const int idx = g * RE_R + r;
-      ri[r] = idx < nr ? rows[idx] : -1;
-      ci[r] = ri[r] >= 0 ? (comp ? comp[ri[r]] : ri[r]) : -1;
-    }
-    __syncthreads();  // previous item's readers of xr / red are done
-    for (int e = threadIdx.x; e < d * RE_R; e += blockDim.x) {
-      const int k = e / RE_R, r = e % RE_R;
-      xr[e] = ri[r] >= 0 ? XT[(int64_t)k * ldx + ri[r]] : 0.0f;
-    }
-    __syncthreads();
-    float acc[RE_R][4];
-#pragma unroll
-    for (int r = 0; r < RE_R; r++)
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc[r][u] = 0.0f;
-    const int jb = blk * RE_COLS + threadIdx.x;
-    // 8 coordinates' column values loaded ahead of their use (L2 latency), then the
-    // R1 chain in order k = 0, 1, ... (XT is zero padded beyond n: no column guard needed
-    // for the loads, only for the keys)
-    constexpr int KB = 8;
-    for (int k0 = 0; k0 < d; k0 += KB) {
-      float y[KB][4];
-#pragma unroll
-      for (int kk = 0; kk < KB; kk++)
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int j = jb + u * 256;
-          y[kk][u] = (k0 + kk < d && j < ldx) ? __ldg(XT + (int64_t)(k0 + kk) * ldx + j) : 0.0f;
-        }
-#pragma unroll
-      for (int kk = 0; kk < KB; kk++) {
-        if (k0 + kk >= d) break;
-        const float4 xa = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R);
-        const float4 xb = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R + 4);
-        const float xv[RE_R] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-        for (int r = 0; r < RE_R; r++)
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const float t = __fsub_rn(xv[r], y[kk][u]);
-            acc[r][u] = __fmaf_rn(t, t, acc[r][u]);
-          }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RE_R; r++) {
-      u64 best = KEY_NONE;
-      if (ri[r] >= 0) {
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int j = jb + u * 256;
-          if (j < n && (comp ? __ldg(comp + j) != ci[r] : j != ri[r])) {
-            const u64 key = ((u64)(__float_as_uint(acc[r][u]) & 0x7FFFFFFFu) << 33) | tri_index(ri[r], j);
-            best = key < best ? key : best;
-          }
-        }
-      }
+      u64 b = best[r];
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
-        const u64 other = __shfl_xor_sync(0xffffffffu, best, o);
-        best = other < best ? other : best;
+        const u64 other = __shfl_xor_sync(0xffffffffu, b, o);
+        b = other < b ? other : b;
       }
-      if (lane == 0) red[warp][r] = best;
+      if (lane == 0) red[warp][r] = b;
     }
     __syncthreads();
-    if (threadIdx.x < RE_R && ri[threadIdx.x] >= 0) {
-      u64 best = KEY_NONE;
-      for (int w = 0; w < 8; w++) best = red[w][threadIdx.x] < best ? red[w][threadIdx.x] : best;
-      if (best != KEY_NONE) atomicMin(compbest + ci[threadIdx.x], best);
+    if (threadIdx.x < RE_R && sri[threadIdx.x] >= 0) {
+      u64 b = KEY_NONE;
+      for (int w = 0; w < 8; w++) b = red[w][threadIdx.x] < b ? red[w][threadIdx.x] : b;
+      if (b != KEY_NONE) atomicMin(compbest + sci[threadIdx.x], b);
+    }
+  };
+  for (int item = i0; item < i1; item++) {
+    const int g = item / nblk, blk = item % nblk;
+    if (g != g_cur) {
+      if (g_cur >= 0) flush();
+      __syncthreads();  // readers of xr / sri / red are done
+      if (threadIdx.x < RE_R) {
+        const int idx = g * RE_R + threadIdx.x;
+        const int ri = idx < nr ? rows[idx] : -1;
+        sri[threadIdx.x] = ri;
+        sci[threadIdx.x] = ri >= 0 ? (comp ? comp[ri] : ri) : -1;
+      }
+      for (int e = threadIdx.x; e < d * RE_R; e += blockDim.x) {
+        const int k = e / RE_R, r = e % RE_R;
+        const int idx = g * RE_R + r;
+        const int ri = idx < nr ? rows[idx] : -1;
+        xr[e] = ri >= 0 ? XT[(int64_t)k * ldx + ri] : 0.0f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < RE_R; r++) best[r] = KEY_NONE;
+      g_cur = g;
+    }
+    float acc[RE_R];
+#pragma unroll
+    for (int r = 0; r < RE_R; r++) acc[r] = 0.0f;
+    const int j = blk * RE_COLS + threadIdx.x;
+    // XT is zero padded beyond n up to ldx (a multiple of 128 >= the column blocks' end):
+    // no column guard for the loads, only for the keys
+    const float* xcol = XT + j;
+    auto load_block = [&](int k0, float (&y)[KB]) {
+      const float* src = xcol + (int64_t)k0 * ldx;
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) y[kk] = (FULL || k0 + kk < d) ? __ldg(src + (int64_t)kk * ldx) : 0.0f;
+    };
+    // the R1 chain in order k = 0, 1, ...; two register buffers in turn (the next
+    // block's loads in flight while one is used)
+    auto step = [&](int k0, const float (&y)[KB]) {
+#pragma unroll
+      for (int kk = 0; kk < KB; kk++) {
+        if (!FULL && k0 + kk >= d) break;
+        float xv[RE_R];
+#pragma unroll
+        for (int q = 0; q < RE_R / 4; q++) {
+          const float4 x4 = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R + 4 * q);
+          xv[4 * q] = x4.x;
+          xv[4 * q + 1] = x4.y;
+          xv[4 * q + 2] = x4.z;
+          xv[4 * q + 3] = x4.w;
+        }
+#pragma unroll
+        for (int r = 0; r < RE_R; r++) {
+          const float t = __fsub_rn(xv[r], y[kk]);
+          acc[r] = __fmaf_rn(t, t, acc[r]);
+        }
+      }
+    };
+    float ya[KB], yb[KB];
+    load_block(0, ya);
+    for (int k0 = 0; k0 < d; k0 += 2 * KB) {
+      if (FULL || k0 + KB < d) load_block(k0 + KB, yb);
+      step(k0, ya);
+      if (!FULL && k0 + KB >= d) break;
+      if (k0 + 2 * KB < d) load_block(k0 + 2 * KB, ya);
+      step(k0 + KB, yb);
+    }
+    if (j < n) {
+      const int cj = comp ? __ldg(comp + j) : j;
+#pragma unroll
+      for (int r = 0; r < RE_R; r++) {
+        const int ri = sri[r];
+        if (ri >= 0 && cj != sci[r]) {
+          const u64 key = ((u64)(__float_as_uint(acc[r]) & 0x7FFFFFFFu) << 33) | tri_index(ri, j);
+          best[r] = key < best[r] ? key : best[r];
+        }
+      }
     }
   }
+  if (g_cur >= 0) flush();
 }
 
 appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, int d, const int* rows,
                               const unsigned* nrows, int max_rows, const int* comp, u64* compbest) {
   if (max_rows <= 0) return APPD_OK;
   const int64_t items = (int64_t)((max_rows + RE_R - 1) / RE_R) * ((n + RE_COLS - 1) / RE_COLS);
-  const int grid = (int)std::min<int64_t>(items, (int64_t)c->sm_count * 8);
+  const int grid = (int)std::min<int64_t>(items, (int64_t)c->sm_count * 2);  // persistent: 2 CTAs per SM
   const size_t smem = (size_t)d * RE_R * 4;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_rows_exact<<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
+  if (d % 16 == 0) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_rows_exact<true><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
+  } else {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_rows_exact<false><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
+  }
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -84,16 +84,14 @@ __global__ void k_orient(const int32_t* __restrict__ eu, const int32_t* __restri
   }
 }
 
-__global__ void k_lift0(const int* __restrict__ parent, const int* __restrict__ val, int n, int* __restrict__ jump,
-                        int* __restrict__ mx) {
+__global__ void k_lift0(const int* __restrict__ parent, const int* __restrict__ val, int n, int2* __restrict__ jm) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
     const int p = parent[x];
-    jump[x] = p;
-    mx[x] = val[p];
+    jm[x] = make_int2(p, val[p]);
   }
 }
 // record parent of v: its nearest ancestor with a larger val; sort key (rpar, val)
-__global__ void k_record_parent(const int* __restrict__ jump, const int* __restrict__ mx, int levels, int n,
+__global__ void k_record_parent(const int2* __restrict__ jm, int levels, int n,
                                 const int* __restrict__ parent, const int* __restrict__ val, int root, int sh,
                                 unsigned long long* __restrict__ key) {
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
@@ -101,8 +99,8 @@ __global__ void k_record_parent(const int* __restrict__ jump, const int* __restr
     const int w = val[v];
     int cur = v;
     for (int j = levels - 1; j >= 0; j--) {
-      const int64_t o = (int64_t)j * n + cur;
-      if (mx[o] < w) cur = jump[o];
+      const int2 q = jm[(int64_t)j * n + cur];  // (2^j-th ancestor, max val on the way)
+      if (q.y < w) cur = q.x;
     }
     const int rp = parent[cur];
     key[w] = ((unsigned long long)(unsigned)rp << sh) | (unsigned)w;  // one entry per edge rank
@@ -158,42 +156,68 @@ __global__ void k_emit(const unsigned long long* __restrict__ S, int m, int sh, 
   }
 }
 
-// all pointer-jumping steps in one cooperative launch (grid-wide barrier per step);
-// (succ, rank) start in buffers 0, the result lands in buffer (steps & 1)
-__global__ void k_rank_coop(int* __restrict__ n0, int* __restrict__ r0, int* __restrict__ n1, int* __restrict__ r1,
-                            int L, int steps) {
+// all pointer-jumping steps in one cooperative launch (grid-wide barrier per step).
+// Each thread keeps its E arcs' (succ, rank) in registers, so a step is ONE dependent
+// 8-byte load of the successor's pair from the previous step's buffer (ping-pong A/B).
+template <int E>
+__global__ void k_rank_coop(const int* __restrict__ succ0, const int* __restrict__ rank0, int2* __restrict__ A,
+                            int2* __restrict__ B, int* __restrict__ out_rank, int L, int steps) {
   cg::grid_group grid = cg::this_grid();
+  const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int nx[E], rk[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int a = tid + e * T;
+    nx[e] = a < L ? succ0[a] : -1;
+    rk[e] = a < L ? rank0[a] : 0;
+    if (a < L) A[a] = make_int2(nx[e], rk[e]);
+  }
+  grid.sync();
   for (int s = 0; s < steps; s++) {
-    const int* ni = (s & 1) ? n1 : n0;
-    const int* ri = (s & 1) ? r1 : r0;
-    int* no = (s & 1) ? n0 : n1;
-    int* ro = (s & 1) ? r0 : r1;
-    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < L; a += gridDim.x * blockDim.x) {
-      const int nx = ni[a];
-      if (nx >= 0) {
-        ro[a] = ri[a] + ri[nx];
-        no[a] = ni[nx];
-      } else {
-        ro[a] = ri[a];
-        no[a] = -1;
+    const int2* in = (s & 1) ? B : A;
+    int2* out = (s & 1) ? A : B;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int a = tid + e * T;
+      if (a >= L) continue;
+      if (nx[e] >= 0) {
+        const int2 q = in[nx[e]];
+        rk[e] += q.y;
+        nx[e] = q.x;
       }
+      out[a] = make_int2(nx[e], rk[e]);
     }
     grid.sync();
   }
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int a = tid + e * T;
+    if (a < L) out_rank[a] = rk[e];
+  }
 }
 
-// all binary-lifting levels in one cooperative launch
-__global__ void k_lift_coop(int* __restrict__ jump, int* __restrict__ mx, int n, int levels) {
+// all binary-lifting levels in one cooperative launch: level j of x from level j-1 of
+// its 2^(j-1)-th ancestor (own pair in registers: one dependent 8-byte load per level)
+template <int E>
+__global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
   cg::grid_group grid = cg::this_grid();
+  const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  int2 cur[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int x = tid + e * T;
+    cur[e] = x < n ? jm[x] : make_int2(0, 0);
+  }
   for (int j = 1; j < levels; j++) {
-    const int* jin = jump + (size_t)(j - 1) * n;
-    const int* min_ = mx + (size_t)(j - 1) * n;
-    int* jout = jump + (size_t)j * n;
-    int* mout = mx + (size_t)j * n;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-      const int q = jin[x];
-      jout[x] = jin[q];
-      mout[x] = max(min_[x], min_[q]);
+    const int2* in = jm + (size_t)(j - 1) * n;
+    int2* out = jm + (size_t)j * n;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int x = tid + e * T;
+      if (x >= n) continue;
+      const int2 q = in[cur[e].x];
+      cur[e] = make_int2(q.x, max(cur[e].y, q.y));
+      out[x] = cur[e];
     }
     grid.sync();
   }
@@ -202,25 +226,22 @@ __global__ void k_lift_coop(int* __restrict__ jump, int* __restrict__ mx, int n,
 // one 1024-thread block per SM: the grid-wide barrier of every step is cheapest with
 // the fewest blocks, and 148 x 1024 threads cover the 2(n-1) arcs in a few strides
 constexpr int kCoopThreads = 1024;
-int coop_grid(appd_ctx* c, const void* fn) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCoopThreads, 0) != cudaSuccess || per_sm < 1) {
-    cudaGetLastError();
-    per_sm = 1;
-  }
-  return c->sm_count;  // (per_sm >= 1 checked: co-residency is guaranteed)
+int coop_grid(appd_ctx* c, int items) {
+  return std::max(1, std::min(c->sm_count, (items + kCoopThreads - 1) / kCoopThreads));
 }
 
-appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int* succ1, int* rank1, int* /*active*/,
-                      int** out_rank) {
+appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int2* A, int2* B, int* out_rank) {
   int steps = 0;
   while ((1 << steps) < L) steps++;
   steps++;
-  const int grid = std::min(coop_grid(c, (const void*)k_rank_coop), (L + kCoopThreads - 1) / kCoopThreads);
-  void* args[] = {&succ0, &rank0, &succ1, &rank1, &L, &steps};
-  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_rank_coop, grid, kCoopThreads, args, 0, c->stream));
+  const int grid = coop_grid(c, L);
+  const int E = (L + grid * kCoopThreads - 1) / (grid * kCoopThreads);
+  void* args[] = {&succ0, &rank0, &A, &B, &out_rank, &L, &steps};
+  const void* fn = E <= 1 ? (const void*)k_rank_coop<1> : E <= 2 ? (const void*)k_rank_coop<2>
+                 : E <= 4 ? (const void*)k_rank_coop<4> : E <= 8 ? (const void*)k_rank_coop<8> : nullptr;
+  if (!fn) return fail(c, APPD_ERR_UNSUPPORTED, "GPU dendrogram: %d arcs", L);
+  APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, grid, kCoopThreads, args, 0, c->stream));
   c->launches++;
-  *out_rank = (steps & 1) ? rank1 : rank0;
   return APPD_OK;
 }
 
@@ -238,10 +259,17 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   int levels = 1;
   while ((1 << levels) < n) levels++;
   levels++;
-  // workspace (ints): 11 arc arrays of L (+2), 6 vertex arrays of n, child_of (m), lifting 2 levels n
-  const size_t ints = (size_t)12 * L + 8 * (size_t)n + 2 * (size_t)levels * n + 64;
-  int* w = (int*)ws(c, S_DENDRO, sizeof(int) * ints + sizeof(unsigned long long) * 2 * (size_t)m + 64);
-  if (!w) return fail(c, APPD_ERR_OUT_OF_MEMORY, "GPU dendrogram workspace");
+  // workspace: int2 arrays first (8-byte aligned): lifting levels (levels x n), the two
+  // pointer-jumping buffers (L each); then ints: 10 arc arrays of L (+2), 6 vertex
+  // arrays of n, child_of (m); then the 64-bit record keys
+  const size_t i2 = (size_t)levels * n + 2 * (size_t)L;
+  const size_t ints = (size_t)10 * L + 8 * (size_t)n + 64;
+  int2* w2 = (int2*)ws(c, S_DENDRO, sizeof(int2) * i2 + sizeof(int) * ints + sizeof(unsigned long long) * 2 * (size_t)m + 64);
+  if (!w2) return fail(c, APPD_ERR_OUT_OF_MEMORY, "GPU dendrogram workspace");
+  int2* jm = w2;
+  int2* bufA = jm + (size_t)levels * n;
+  int2* bufB = bufA + L;
+  int* w = reinterpret_cast<int*>(bufB + L);
   int* src = w;
   int* arc = src + L;
   int* ssrc = arc + L;
@@ -256,14 +284,10 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   int* child_of = val + n;
   int* first = child_of + m;
   int* sidx = first + n;
-  int* jump = sidx + n;
-  int* mx = jump + (size_t)levels * n;
-  int* succ1 = mx + (size_t)levels * n;
-  int* rank1 = succ1 + L;
-  int* flag = rank1 + L;           // L + 1
+  int* rk = sidx + n;              // L: tour ranks
+  int* flag = rk + L;              // L + 1
   int* downs = flag + L + 1;       // L + 1
-  int* active = downs + L + 1;
-  unsigned long long* key = reinterpret_cast<unsigned long long*>(((uintptr_t)(active + 8) + 15) & ~(uintptr_t)15);
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(((uintptr_t)(downs + L + 8) + 15) & ~(uintptr_t)15);
   unsigned long long* S = key + m;
   const int gL = std::min(c->sm_count * 8, (L + 255) / 256), gn = std::min(c->sm_count * 8, (n + 255) / 256);
   const int root = 0;
@@ -279,24 +303,27 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   // B, C: Euler tour of the MST from the root, tour ranks
   k_euler_succ<<<gL, 256, 0, c->stream>>>(eu, ev, m, sarc, start, end, posarc, root, succ0, rank0);
   APPD_LAUNCHED(c);
-  int* rk = nullptr;
-  if ((s = list_rank(c, L, succ0, rank0, succ1, rank1, active, &rk))) return s;
+  if ((s = list_rank(c, L, succ0, rank0, bufA, bufB, rk))) return s;
   // orientation: parent, val (edge rank of the parent edge), child of each edge
   APPD_CUDA(c, cudaMemsetAsync(val + root, 0x7F, sizeof(int), c->stream));  // +inf
   k_orient<<<gn, 256, 0, c->stream>>>(eu, ev, m, rk, parent, val, child_of);
   APPD_LAUNCHED(c);
   APPD_CUDA(c, cudaMemsetAsync(parent + root, 0, sizeof(int), c->stream));  // root = vertex 0 is its own parent
   // D: binary lifting, nearest heavier ancestor
-  k_lift0<<<gn, 256, 0, c->stream>>>(parent, val, n, jump, mx);
+  k_lift0<<<gn, 256, 0, c->stream>>>(parent, val, n, jm);
   APPD_LAUNCHED(c);
   {
     int nn = n, lv = levels;
-    const int grid = std::min(coop_grid(c, (const void*)k_lift_coop), (n + kCoopThreads - 1) / kCoopThreads);
-    void* args[] = {&jump, &mx, &nn, &lv};
-    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_lift_coop, grid, kCoopThreads, args, 0, c->stream));
+    const int grid = coop_grid(c, n);
+    const int E = (n + grid * kCoopThreads - 1) / (grid * kCoopThreads);
+    const void* fn = E <= 1 ? (const void*)k_lift_coop<1> : E <= 2 ? (const void*)k_lift_coop<2>
+                   : E <= 4 ? (const void*)k_lift_coop<4> : E <= 8 ? (const void*)k_lift_coop<8> : nullptr;
+    if (!fn) return fail(c, APPD_ERR_UNSUPPORTED, "GPU dendrogram: n = %d", n);
+    void* args[] = {&jm, &nn, &lv};
+    APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, grid, kCoopThreads, args, 0, c->stream));
     c->launches++;
   }
-  k_record_parent<<<gn, 256, 0, c->stream>>>(jump, mx, levels, n, parent, val, root, sh, key);
+  k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
   APPD_LAUNCHED(c);
   // E: record tree, children ascending by val
   if ((s = sort_keys_u64_bits64(c, key, S, m, 0, 2 * sh))) return s;
@@ -305,7 +332,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   APPD_LAUNCHED(c);
   k_rt_succ<<<gn, 256, 0, c->stream>>>(S, m, sh, child_of, first, sidx, root, succ0, rank0);
   APPD_LAUNCHED(c);
-  if ((s = list_rank(c, L, succ0, rank0, succ1, rank1, active, &rk))) return s;
+  if ((s = list_rank(c, L, succ0, rank0, bufA, bufB, rk))) return s;
   APPD_CUDA(c, cudaMemsetAsync(flag, 0, sizeof(int) * (L + 1), c->stream));
   k_down_flags<<<gn, 256, 0, c->stream>>>(rk, m, flag);
   APPD_LAUNCHED(c);

@@ -15,6 +15,8 @@
 // so the inner loop is one select + one max per element: the kernel is bound by
 // HBM write bandwidth (n^2 * 4 bytes).  RMQ is a sparse table over h
 // (ST[k][i] = max h[i .. i+2^k-1]).  Widest sense: min instead of max.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace appd {
@@ -56,8 +58,42 @@ __global__ void k_st_level(float* ST, int64_t m, int64_t stride, int k) {
     cur[i] = WIDEST ? fminf(a, b) : fmaxf(a, b);
   }
 }
+// levels 1 .. kl (kl <= ST_LO) in one pass: a block computes level-k entries
+// [i0, i0 + ST_B) for every k from level 0 [i0, i0 + ST_B + 2^kl - 1) in shared memory
+constexpr int ST_LO = 8, ST_B = 2048;
+template <bool WIDEST>
+__global__ void __launch_bounds__(256) k_st_levels_lo(float* ST, int64_t m, int64_t stride, int kl) {
+  __shared__ float buf[2][ST_B + (1 << ST_LO)];
+  const float ID = WIDEST ? INFINITY : -INFINITY;
+  const int64_t i0 = (int64_t)blockIdx.x * ST_B;
+  int need = ST_B + (1 << kl) - 1;
+  for (int i = threadIdx.x; i < need; i += blockDim.x) buf[0][i] = i0 + i < m ? ST[i0 + i] : ID;
+  __syncthreads();
+  for (int k = 1; k <= kl; k++) {
+    const int half = 1 << (k - 1);
+    need -= half;
+    const float* prev = buf[(k - 1) & 1];
+    float* cur = buf[k & 1];
+    const int64_t cnt = m - (1ll << k) + 1;
+    float* out = ST + (int64_t)k * stride;
+    for (int i = threadIdx.x; i < need; i += blockDim.x) {
+      const float v = WIDEST ? fminf(prev[i], prev[i + half]) : fmaxf(prev[i], prev[i + half]);
+      cur[i] = v;
+      if (i < ST_B && i0 + i < cnt) out[i0 + i] = v;
+    }
+    __syncthreads();
+  }
+}
+
 appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, int64_t stride, int widest) {
-  for (int k = 1; k < levels; k++) {
+  const int kl = std::min(ST_LO, levels - 1);
+  if (kl >= 1) {
+    const int grid = (int)((m + ST_B - 1) / ST_B);
+    if (widest) k_st_levels_lo<true><<<grid, 256, 0, c->stream>>>(ST, m, stride, kl);
+    else k_st_levels_lo<false><<<grid, 256, 0, c->stream>>>(ST, m, stride, kl);
+    APPD_LAUNCHED(c);
+  }
+  for (int k = kl + 1; k < levels; k++) {
     int64_t cnt = m - (1ll << k) + 1;
     int grid = (int)((cnt + 255) / 256);
     if (grid > c->sm_count * 8) grid = c->sm_count * 8;

@@ -33,39 +33,72 @@ namespace appd {
 // ---------------------------------------------------------------------------
 
 // per-block partial column sums (fp64), fixed partition => deterministic
+// column sums in fp64, deterministic order: block b sums rows [b R, (b+1) R); thread
+// slots (row lane l, dim k) with RL = 256 / d lanes (>= 1) sum rows l, l + RL, ..., then
+// the lanes are added in order
 __global__ void k_center_partial(const float* __restrict__ X, int64_t n, int d, int rows_per_block,
                                  double* __restrict__ part) {
+  __shared__ double red[256];
+  const int RL = d >= 256 ? 1 : 256 / d;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(n, r0 + rows_per_block);
-  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+  for (int k0 = 0; k0 < d; k0 += 256) {  // d > 256: dims in slices of 256
+    const int slot = threadIdx.x, l = slot / min(d, 256), k = k0 + slot % min(d, 256);
     double s = 0.0;
-    for (int64_t r = r0; r < r1; r++) s += (double)X[r * d + k];
-    part[(int64_t)blockIdx.x * d + k] = s;
+    if (l < RL && k < d)
+      for (int64_t r = r0 + l; r < r1; r += RL) s += (double)__ldg(X + r * d + k);
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < min(d, 256) && k0 + (int)threadIdx.x < d) {
+      double t = 0.0;
+      for (int q = 0; q < RL; q++) t += red[q * min(d, 256) + threadIdx.x];
+      part[(int64_t)blockIdx.x * d + k0 + threadIdx.x] = t;
+    }
+    __syncthreads();
   }
 }
+// one warp per dimension: lanes sum partials b = lane, lane + 32, ..., then a fixed tree
 __global__ void k_center_final(const double* __restrict__ part, int blocks, int64_t n, int d, float* __restrict__ c) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d; k += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < blocks; b++) s += part[(int64_t)b * d + k];
-    c[k] = (float)(s / (double)n);
-  }
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= d) return;
+  double s = 0.0;
+  for (int b = lane; b < blocks; b += 32) s += part[(int64_t)b * d + w];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) c[w] = (float)(s / (double)n);
 }
-// max |x_i - c| (fp32, order independent)
+// max |x_i - c| (fp32; sets the scale only): one thread per point, block maximum, one atomic
 __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ c,
                          unsigned* __restrict__ out) {
-  const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
   float best = 0.0f;
-  for (int64_t i = (int64_t)blockIdx.x * warps + w; i < n; i += (int64_t)gridDim.x * warps) {
+  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.0f;
-    for (int k = lane; k < d; k += 32) {
-      const float t = X[i * d + k] - c[k];
-      s += t * t;
+    if (vec) {
+      const float4* x4 = reinterpret_cast<const float4*>(X + i * d);
+      for (int k = 0; k < d; k += 4) {
+        const float4 v = __ldg(x4 + k / 4);
+        const float t0 = v.x - c[k], t1 = v.y - c[k + 1], t2 = v.z - c[k + 2], t3 = v.w - c[k + 3];
+        s += t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
+      }
+    } else {
+      for (int k = 0; k < d; k++) {
+        const float t = X[i * d + k] - c[k];
+        s += t * t;
+      }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     best = fmaxf(best, s);
   }
-  if (lane == 0) atomicMax(out, __float_as_uint(sqrtf(best)));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __shared__ float wb[32];
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int t = 0; t < (int)(blockDim.x >> 5); t++) m = fmaxf(m, wb[t]);
+    atomicMax(out, __float_as_uint(sqrtf(m)));
+  }
 }
 
 // pack point perm[p] into the row (YA) and column (YB) operand granules:
@@ -73,80 +106,99 @@ __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const fl
 // with g = (p%128)/8, r = p%8 (K-major, no swizzle: 8-row x 16-byte core matrices).
 // y^ = fp16(scale * (x - c)); K columns: [y^ (d), zero pad to dk, then
 // A: 1, 1, 0..; B: hi(-|y^|^2/2), lo(-|y^|^2/2), 0..].  Padding points: A = 0,
-// B augment = -65504 (never a maximum).
+// B augment = -65504 (never a maximum).  One thread per point, one 16-byte store per
+// 8 coordinates (lanes = consecutive points: 128-byte runs per core matrix).
 __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, int K, const int* __restrict__ perm,
                        const float* __restrict__ c, float scale, int64_t npad, __half* __restrict__ YA,
                        __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
                        float* __restrict__ err, unsigned* __restrict__ maxerr) {
-  const int warps = blockDim.x / 32, w = threadIdx.x / 32, lane = threadIdx.x & 31;
   float emax = 0.0f;
-  for (int64_t p = (int64_t)blockIdx.x * warps + w; p < npad; p += (int64_t)gridDim.x * warps) {
+  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npad; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gidx = p / 128;
     const int pl = (int)(p % 128), g = pl / 8, r = pl % 8;
-    __half* ga = YA + gidx * 128 * K;
-    __half* gb = YB + gidx * 128 * K;
+    uint4* ga = reinterpret_cast<uint4*>(YA + gidx * 128 * K + (int64_t)g * (K / 8) * 64 + r * 8);
+    uint4* gb = reinterpret_cast<uint4*>(YB + gidx * 128 * K + (int64_t)g * (K / 8) * 64 + r * 8);
     const bool real = p < n;
     const int64_t i = real ? perm[p] : 0;
+    const float* xi = X + i * d;
     float s = 0.0f;
     // E^2 = |y^ - s (x - c)|^2: per coordinate e = (y^ - y) - s dt with y = s fl(x - c) and
     // dt = (x - c) - fl(x - c) exact by TwoSum; y^ - y is exact (Sterbenz: y^ = fp16(y)).
     // Only a - s dt and the squares / sum round (relative (d + 4) 2^-24 over the sum,
-    // covered by the margin applied below).
+    // covered by the margin applied below); round-up FMAs keep the sum an upper bound.
     float e2 = 0.0f;
-    for (int k = lane; k < dk; k += 32) {
-      __half hv = __float2half_rn(0.0f);
-      if (real && k < d) {
-        const float xk = X[i * d + k], ck = c[k];
-        const float t = __fsub_rn(xk, ck);
-        const float bb = __fsub_rn(t, xk);
-        const float dt = __fadd_rn(__fsub_rn(xk, __fsub_rn(t, bb)), __fsub_rn(-ck, bb));  // TwoSum error
-        const float y = scale * t;
-        hv = __float2half_rn(y);
-        const float ek = __fsub_rn(__fsub_rn(__half2float(hv), y), scale * dt);
-        e2 = __fmaf_ru(ek, ek, e2);
+    for (int k8 = 0; k8 < dk; k8 += 8) {
+      float xv[8];
+      if (real && vec && k8 + 8 <= d) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(xi + k8));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(xi + k8 + 4));
+        xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+        xv[4] = b.x; xv[5] = b.y; xv[6] = b.z; xv[7] = b.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; u++) xv[u] = (real && k8 + u < d) ? __ldg(xi + k8 + u) : 0.0f;
       }
-      const float hf = __half2float(hv);
-      s = fmaf(hf, hf, s);
-      const int64_t off = (int64_t)g * (K / 8) * 64 + (k / 8) * 64 + r * 8 + (k % 8);  // in halves
-      ga[off] = hv;
-      gb[off] = hv;
+      __half hv[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int k = k8 + u;
+        hv[u] = __float2half_rn(0.0f);
+        if (real && k < d) {
+          const float xk = xv[u], ck = c[k];
+          const float t = __fsub_rn(xk, ck);
+          const float bb = __fsub_rn(t, xk);
+          const float dt = __fadd_rn(__fsub_rn(xk, __fsub_rn(t, bb)), __fsub_rn(-ck, bb));  // TwoSum error
+          const float y = scale * t;
+          hv[u] = __float2half_rn(y);
+          const float ek = __fsub_rn(__fsub_rn(__half2float(hv[u]), y), scale * dt);
+          e2 = __fmaf_ru(ek, ek, e2);
+        }
+        const float hf = __half2float(hv[u]);
+        s = fmaf(hf, hf, s);
+      }
+      uint4 pk;
+      pk.x = (uint32_t)__half_as_ushort(hv[0]) | ((uint32_t)__half_as_ushort(hv[1]) << 16);
+      pk.y = (uint32_t)__half_as_ushort(hv[2]) | ((uint32_t)__half_as_ushort(hv[3]) << 16);
+      pk.z = (uint32_t)__half_as_ushort(hv[4]) | ((uint32_t)__half_as_ushort(hv[5]) << 16);
+      pk.w = (uint32_t)__half_as_ushort(hv[6]) | ((uint32_t)__half_as_ushort(hv[7]) << 16);
+      ga[(k8 / 8) * 8] = pk;  // (k/8)*64 halves = 8 x 16 bytes
+      gb[(k8 / 8) * 8] = pk;
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) e2 = __fadd_ru(e2, __shfl_xor_sync(0xffffffffu, e2, o));
-    for (int k = dk + lane; k < K; k += 32) {
-      const int64_t off = (int64_t)g * (K / 8) * 64 + (k / 8) * 64 + r * 8 + (k % 8);
-      __half a = __float2half_rn(0.0f), b = __float2half_rn(0.0f);
-      if (k == dk || k == dk + 1) {
+    // augment columns [dk, K): A = (1, 1, 0 ..), B = (hi, lo, 0 ..) of -|y^|^2 / 2
+    for (int k8 = dk; k8 < K; k8 += 8) {
+      uint4 a = make_uint4(0u, 0u, 0u, 0u), b = make_uint4(0u, 0u, 0u, 0u);
+      if (k8 == dk) {
         if (real) {
-          a = __float2half_rn(1.0f);
+          const uint32_t one = __half_as_ushort(__float2half_rn(1.0f));
+          a.x = one | (one << 16);
           const float hn = -0.5f * s;
           const __half hi = __float2half_rn(hn);
-          b = (k == dk) ? hi : __float2half_rn(hn - __half2float(hi));
+          const __half lo = __float2half_rn(hn - __half2float(hi));
+          b.x = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
         } else {
-          b = (k == dk) ? __float2half_rn(-65504.0f) : __float2half_rn(0.0f);
+          b.x = (uint32_t)__half_as_ushort(__float2half_rn(-65504.0f));
         }
       }
-      ga[off] = a;
-      gb[off] = b;
+      ga[(k8 / 8) * 8] = a;
+      gb[(k8 / 8) * 8] = b;
     }
-    if (lane == 0) {
-      nrm[p] = real ? s : 0.0f;
-      len[p] = real ? sqrtf(s) : 0.0f;
-      // rounded up, with a relative margin for the rounded subtraction and squares
-      const float E = real ? __fsqrt_ru(__fmul_ru(e2, 1.0f + (float)(d + 8) * 0x1p-23f)) + 1e-30f : 0.0f;
-      err[p] = E;
-      emax = fmaxf(emax, E);
-    }
+    nrm[p] = real ? s : 0.0f;
+    len[p] = real ? sqrtf(s) : 0.0f;
+    // rounded up, with a relative margin for the rounded subtraction and squares
+    const float E = real ? __fsqrt_ru(__fmul_ru(e2, 1.0f + (float)(d + 8) * 0x1p-23f)) + 1e-30f : 0.0f;
+    err[p] = E;
+    emax = fmaxf(emax, E);
   }
   // one atomic per block for the global maximum (a single address: atomics serialise)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
   __shared__ float wmax[32];
-  if (lane == 0) wmax[w] = emax;
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = emax;
   __syncthreads();
   if (threadIdx.x == 0) {
     float m = 0.0f;
-    for (int t = 0; t < warps; t++) m = fmaxf(m, wmax[t]);
+    for (int t = 0; t < (int)(blockDim.x >> 5); t++) m = fmaxf(m, wmax[t]);
     if (m > 0.0f) atomicMax(maxerr, __float_as_uint(m));
   }
 }
@@ -430,17 +482,19 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   st->K = st->dk + 16;
   st->stages = tcf_stages(st->K);
   if (st->stages == 0) return APPD_ERR_UNSUPPORTED;
-  const int blocks = (int)((n + 255) / 256);
+  const int rpb = 64;  // rows per partial sum
+  const int blocks = (int)((n + rpb - 1) / rpb);
   double* part = (double*)ws(c, S_TC_PART, sizeof(double) * blocks * d);
   st->center = (float*)ws(c, S_TC_CENTER, sizeof(float) * (d + 1) + 64);
   if (!part || !st->center) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc center");
-  k_center_partial<<<blocks, 128, 0, c->stream>>>(X, n, (int)d, 256, part);
+  k_center_partial<<<blocks, 256, 0, c->stream>>>(X, n, (int)d, rpb, part);
   APPD_LAUNCHED(c);
-  k_center_final<<<(unsigned)((d + 127) / 128), 128, 0, c->stream>>>(part, blocks, n, (int)d, st->center);
+  k_center_final<<<(unsigned)((d + 7) / 8), 256, 0, c->stream>>>(part, blocks, n, (int)d, st->center);
   APPD_LAUNCHED(c);
   unsigned* maxlen = (unsigned*)(st->center + d);
   APPD_CUDA(c, cudaMemsetAsync(maxlen, 0, sizeof(unsigned), c->stream));
-  k_maxlen<<<c->sm_count * 4, 256, 0, c->stream>>>(X, n, (int)d, st->center, maxlen);
+  k_maxlen<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8), 256, 0, c->stream>>>(
+      X, n, (int)d, st->center, maxlen);
   APPD_LAUNCHED(c);
   APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 32, maxlen, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -547,16 +601,20 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   return APPD_OK;
 }
 
-static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X) {
+// xt: the d x npad fp32 transpose of the packed order for the exact kernels (nullptr:
+// not needed)
+static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X, float* xt) {
   const int64_t n = st->n;
   APPD_CUDA(c, cudaMemsetAsync(st->maxerr, 0, sizeof(unsigned), c->stream));
-  k_pack<<<c->sm_count * 8, 256, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->scale,
+  k_pack<<<(unsigned)std::min<int64_t>((st->npad + 127) / 128, (int64_t)c->sm_count * 16), 128, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->scale,
                                                   st->npad, (__half*)st->YA, (__half*)st->YB, st->nrm, st->len,
                                                   st->err, st->maxerr);
   APPD_LAUNCHED(c);
-  const dim3 tg((unsigned)(st->npad / 32), (unsigned)((st->d + 31) / 32));
-  k_transpose_perm<<<tg, dim3(32, 8), 0, c->stream>>>(X, n, (int)st->d, st->perm, st->npad, st->XTp);
-  APPD_LAUNCHED(c);
+  if (xt) {
+    const dim3 tg((unsigned)(st->npad / 32), (unsigned)((st->d + 31) / 32));
+    k_transpose_perm<<<tg, dim3(32, 8), 0, c->stream>>>(X, n, (int)st->d, st->perm, st->npad, xt);
+    APPD_LAUNCHED(c);
+  }
   k_seg_maxlen<<<(unsigned)std::min<int64_t>(c->sm_count * 8, (st->npad / TC_TMG + 7) / 8), 256, 0, c->stream>>>(
       st->len, st->err, st->npad / TC_TMG, st->seg_maxlen, st->seg_maxerr);
   APPD_LAUNCHED(c);
@@ -764,7 +822,9 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
     APPD_LAUNCHED(c);
   }
-  if ((s = tcf_pack(c, st, X))) return s;
+  // round 0 of the cache: the permutation is the identity, so the transpose is the
+  // original-order one the exact row kernel reads
+  if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp))) return s;
   APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));  // ~3.4e38
   APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
   APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
@@ -776,9 +836,6 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   ExactParams E;
 
   if (cache && round == 0) {
-    // original-order transpose for the exact row kernel (round 0: the permutation is the identity)
-    APPD_CUDA(c, cudaMemcpyAsync(st->XT, st->XTp, sizeof(float) * st->npad * st->d, cudaMemcpyDeviceToDevice,
-                                 c->stream));
     // ---- cache-building scan: 32-column maxima of every row of this rank ----
     P.rb_begin = (int)rb_begin;
     P.rb_end = (int)rb_end;
@@ -880,7 +937,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   APPD_LAUNCHED(c);
   k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
   APPD_LAUNCHED(c);
-  if ((s = tcf_pack(c, st, X))) return s;
+  if ((s = tcf_pack(c, st, X, nullptr))) return s;  // the component-matrix kernels read X
   APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
   unsigned* CUB = st->compUB;  // k x k <= 128 x 128 words (the buffer holds n >= k^2 words or more)
   APPD_CUDA(c, cudaMemsetAsync(CUB, 0x7F, sizeof(unsigned) * k * k, c->stream));  // ~3.4e38: permissive
@@ -963,7 +1020,7 @@ appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, fl
   appd_status s = tcf_prepare(c, X, n, d, &st);
   if (s) return s;
   if ((s = launch_iota(c, st.perm, n))) return s;
-  if ((s = tcf_pack(c, &st, X))) return s;
+  if ((s = tcf_pack(c, &st, X, nullptr))) return s;
   APPD_CUDA(c, cudaMemsetAsync(st.counters, 0, 64, c->stream));
   TcParams P;
   fill_scan_params(&st, &P);

@@ -8,10 +8,18 @@ rows = list(csv.reader(io.StringIO(out)))
 hi = next(i for i, r in enumerate(rows) if "Source" in r)
 h = rows[hi]
 A = h.index("Address"); S = h.index("Source"); W = h.index("Warp Stall Sampling (All Samples)"); I = h.index("Instructions Executed")
-body = [r for r in rows[hi + 1:] if len(r) > W]
-tot = sum(float(r[W] or 0) for r in body)
-tins = sum(float(r[I] or 0) for r in body)
+# first kernel only (a report with several kernels repeats the header)
+body = []
+for r in rows[hi + 1:]:
+    if "Source" in r or (len(r) > 0 and r[0] == "Kernel Name"):
+        break
+    if len(r) > max(W, I): body.append(r)
+def f(x):
+    try: return float(x or 0)
+    except ValueError: return 0.0
+tot = sum(f(r[W]) for r in body)
+tins = sum(f(r[I]) for r in body)
 print(f"samples {tot:.0f}  warp-instructions {tins:.0f}")
-res = sorted(((float(r[W] or 0), k, r) for k, r in enumerate(body)), reverse=True)[:top]
+res = sorted(((f(r[W]), k, r) for k, r in enumerate(body)), reverse=True)[:top]
 for w, k, r in sorted(res, key=lambda x: x[1]):
     print(f"{100*w/tot:5.1f}%  #{k:<5d} inst={r[I]:>9s}  {r[S][:90]}")
