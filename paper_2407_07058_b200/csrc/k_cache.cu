@@ -82,6 +82,25 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// packed FP32 pairs (FADD2 / FFMA2 on sm_100a): each half is the IEEE round-to-nearest
+// result of the scalar operation, so the R1 chain is unchanged, at half the issue slots
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// acc + (a - b)^2 per half: sub.rn then fma.rn (the R1 step)
+__device__ __forceinline__ unsigned long long f2_r1_step(unsigned long long a, unsigned long long b,
+                                                         unsigned long long acc) {
+  unsigned long long t, r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(a), "l"(b));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(t), "l"(acc));
+  return r;
+}
+
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -849,9 +868,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
       for (int r = 0; r < RE_R; r++) best[r] = KEY_NONE;
       g_cur = g;
     }
-    float acc[RE_R];
+    unsigned long long acc2[RE_R / 2];  // rows (2 i, 2 i + 1) packed
 #pragma unroll
-    for (int r = 0; r < RE_R; r++) acc[r] = 0.0f;
+    for (int r = 0; r < RE_R / 2; r++) acc2[r] = 0ull;
     const int j = blk * RE_COLS + threadIdx.x;
     // XT is zero padded beyond n up to ldx (a multiple of 128 >= the column blocks' end):
     // no column guard for the loads, only for the keys
@@ -867,19 +886,12 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
 #pragma unroll
       for (int kk = 0; kk < KB; kk++) {
         if (!FULL && k0 + kk >= d) break;
-        float xv[RE_R];
+        const unsigned long long yy = f2pack(y[kk], y[kk]);
 #pragma unroll
         for (int q = 0; q < RE_R / 4; q++) {
-          const float4 x4 = *reinterpret_cast<const float4*>(xr + (k0 + kk) * RE_R + 4 * q);
-          xv[4 * q] = x4.x;
-          xv[4 * q + 1] = x4.y;
-          xv[4 * q + 2] = x4.z;
-          xv[4 * q + 3] = x4.w;
-        }
-#pragma unroll
-        for (int r = 0; r < RE_R; r++) {
-          const float t = __fsub_rn(xv[r], y[kk]);
-          acc[r] = __fmaf_rn(t, t, acc[r]);
+          const ulonglong2 x4 = *reinterpret_cast<const ulonglong2*>(xr + (k0 + kk) * RE_R + 4 * q);
+          acc2[2 * q] = f2_r1_step(x4.x, yy, acc2[2 * q]);
+          acc2[2 * q + 1] = f2_r1_step(x4.y, yy, acc2[2 * q + 1]);
         }
       }
     };
@@ -892,6 +904,9 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
       if (k0 + 2 * KB < d) load_block(k0 + 2 * KB, ya);
       step(k0 + KB, yb);
     }
+    float acc[RE_R];
+#pragma unroll
+    for (int r = 0; r < RE_R / 2; r++) f2unpack(acc2[r], acc[2 * r], acc[2 * r + 1]);
     if (j < n) {
       const int cj = comp ? __ldg(comp + j) : j;
 #pragma unroll
@@ -1053,32 +1068,30 @@ __global__ void k_cm_rowub(CmParams P) {
         atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
       }
     };
-    int curD = -1;
-    float m = -INFINITY;
     constexpr int U = 16;
     const int span = (nseg_n - smin + CM_SPLIT - 1) / CM_SPLIT;
     const int sbeg = smin + part * span, send = min(nseg_n, sbeg + span);
-    for (int s0 = sbeg; s0 < send; s0 += U) {
-      float v[U];
-#pragma unroll
-      for (int u = 0; u < U; u++)
-        v[u] = (valid && s0 + u < send) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int s = s0 + u;
-        if (s >= send) break;
-        const int2 dd = P.segd[s];
-        const int D0 = dd.x, D1 = dd.y;
-        if (D0 != D1) continue;  // straddling segment: bounds neither component alone
-        if (D0 != curD) {
-          if (curD >= 0) flush(curD, m);
-          curD = D0;
-          m = -INFINITY;
-        }
-        m = fmaxf(m, v[u]);
+    // runs of full segments of one component D (positions sorted by component: the full
+    // segments of D are those below cend[D] / TC_TMG); straddling segments are skipped
+    for (int s = sbeg; s < send;) {
+      const int2 dd = P.segd[s];
+      if (dd.x != dd.y) {
+        s++;
+        continue;
       }
+      const int D = dd.x;
+      const int e = max(s + 1, min(send, P.cend[D] / TC_TMG));
+      float m = -INFINITY;
+      for (int s0 = s; s0 < e; s0 += U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = (valid && s0 + u < e) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+#pragma unroll
+        for (int u = 0; u < U; u++) m = fmaxf(m, v[u]);
+      }
+      flush(D, m);
+      s = e;
     }
-    if (curD >= 0) flush(curD, m);
   }
 }
 
@@ -1099,50 +1112,47 @@ __global__ void k_cm_filter(CmParams P) {
     const int C = valid ? P.sc[p] : 0;
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
     const float dl = em_delta2(valid ? P.err[p] : 0.0f, *P.maxerr);
-    int cachedD = -1;  // threshold of the last uniform segment's component (segments are sorted)
-    float cachedT = 0.0f;
     constexpr int U = 16;
     const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;
     const int span = (nseg - smin + CM_SPLIT - 1) / CM_SPLIT;
     const int sbeg = smin + part * span, send = min(nseg, sbeg + span);
-    for (int s0 = sbeg; s0 < send; s0 += U) {
-      float v[U];
+    // runs of segments with one threshold: the full segments of a component D (below
+    // cend[D] / TC_TMG), or a single straddling segment (most permissive of its components)
+    for (int s = sbeg; s < send;) {
+      const int2 dd = P.segd[s];
+      int e;
+      float thr;
+      if (dd.x == dd.y) {
+        e = max(s + 1, min(send, P.cend[dd.x] / TC_TMG));
+        thr = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + dd.x]), ni, li, P.maxlen, dl);
+      } else {
+        e = s + 1;
+        float ub = 0.0f;
+        for (int D = dd.x; D <= dd.y; D++)
+          if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
+        thr = em_thr(P.em, ub, ni, li, P.maxlen, dl);
+      }
+      for (int s0 = s; s0 < e; s0 += U) {
+        float v[U];
 #pragma unroll
-      for (int u = 0; u < U; u++)
-        v[u] = (valid && s0 + u < send) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
-      unsigned mask = 0;
+        for (int u = 0; u < U; u++) v[u] = (valid && s0 + u < e) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+        unsigned mask = 0;
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        if (!(v[u] > -INFINITY)) continue;
-        const int2 dd = P.segd[s0 + u];
-        const int D0 = dd.x, D1 = dd.y;
-        float thr;
-        if (D0 == D1) {
-          if (D0 != cachedD) {
-            cachedD = D0;
-            cachedT = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + D0]), ni, li, P.maxlen, dl);
-          }
-          thr = cachedT;
-        } else {  // straddling segment: the most permissive of its components
-          float ub = 0.0f;
-          for (int D = D0; D <= D1; D++)
-            if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
-          thr = em_thr(P.em, ub, ni, li, P.maxlen, dl);
+        for (int u = 0; u < U; u++) mask |= (v[u] >= thr && v[u] > -INFINITY) ? 1u << u : 0u;
+        if (!__any_sync(0xffffffffu, mask != 0)) continue;
+        unsigned cnt = 0;
+        for (unsigned m = mask; m; m &= m - 1)
+          cnt += (unsigned)min(TC_TMG / 32, (P.n - (s0 + __ffs(m) - 1) * TC_TMG + 31) / 32);
+        unsigned slot = warp_alloc(P.counters + 1, cnt);
+        while (mask) {
+          const int sg = s0 + __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int nc = min(TC_TMG / 32, (P.n - sg * TC_TMG + 31) / 32);
+          for (int t = 0; t < nc; t++, slot++)
+            if (slot < P.list_cap) P.list[slot] = ((unsigned)((TC_TMG / 32) * sg + t) << LIST_SHIFT) | (unsigned)p;
         }
-        if (v[u] >= thr) mask |= 1u << u;
       }
-      if (!__any_sync(0xffffffffu, mask != 0)) continue;
-      unsigned cnt = 0;
-      for (unsigned m = mask; m; m &= m - 1)
-        cnt += (unsigned)min(TC_TMG / 32, (P.n - (s0 + __ffs(m) - 1) * TC_TMG + 31) / 32);
-      unsigned slot = warp_alloc(P.counters + 1, cnt);
-      while (mask) {
-        const int s = s0 + __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int nc = min(TC_TMG / 32, (P.n - s * TC_TMG + 31) / 32);
-        for (int t = 0; t < nc; t++, slot++)
-          if (slot < P.list_cap) P.list[slot] = ((unsigned)((TC_TMG / 32) * s + t) << LIST_SHIFT) | (unsigned)p;
-      }
+      s = e;
     }
   }
 }

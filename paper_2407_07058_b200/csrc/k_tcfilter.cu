@@ -841,7 +841,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     P.rb_end = (int)rb_end;
     P.seg32 = 1;
     if (getenv("APPD_TC_BENCH")) {  // debug: time the scan variants in isolation (results discarded)
-      const char* names[] = {"seg128", "seg32", "", "null-epilogue", "tmem-load-only", "no-B-copies", "null+noB"};
+      const char* names[] = {"seg64", "seg32", "", "null-epilogue", "tmem-load-only", "no-B-copies", "null+noB"};
       for (int pass : {0, 1, 3, 4, 5, 6}) {
         float best = 1e9f;
         for (int rep = 0; rep < 5; rep++) {

@@ -17,8 +17,8 @@ constexpr int TC_M = 128, TC_N = 256, TC_RT = 4, TC_ROWS = TC_M * TC_RT, TC_MAX_
 constexpr int TC_NA = 256;        // MMA N: accumulator width (TMEM columns per buffer)
 constexpr int TC_NBUF = 2;        // TMEM accumulator buffers (TC_NBUF x TC_NA = 512 columns)
 constexpr int TC_HALVES = TC_N / TC_NA;  // accumulators per (row tile, column tile)
-constexpr int TC_EPI_WARPS = 8;   // 4 lane quarters x 2 column halves of an accumulator
-constexpr int TC_TMG = TC_NA / 2; // columns per epilogue warp = granularity of the stored maxima
+constexpr int TC_EPI_WARPS = 16;  // 4 lane quarters x 4 column quarters of an accumulator
+constexpr int TC_TMG = TC_NA / 4; // columns per epilogue warp = granularity of the stored maxima
 constexpr int TC_THREADS = 32 * (2 + TC_EPI_WARPS);  // warp 0 producer, warp 1 MMA, then epilogue
 
 // Error model (scaled units).  L = |y^_i|, R = max |y^_j| over the columns considered.
@@ -88,7 +88,7 @@ struct TcParams {
   ErrModel em;
   int round0;   // singletons (eligibility = j != i)
   float* dump;  // PASS 2 (test hook) only: raw accumulator of the first item
-  // TM granularity: 0 -> one maximum per TC_TMG (128) columns; 1 -> per 32 columns
+  // TM granularity: 0 -> one maximum per TC_TMG (64) columns; 1 -> per 32 columns
   // (the cache-building round 0: 4x the maxima, 1/4 of the exact re-check work)
   int seg32;
   // optional row-block list (re-scan rounds): the *rb_count blocks of
