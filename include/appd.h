@@ -121,7 +121,7 @@ typedef struct {
   int64_t rescan_rows;      /* rows re-scanned in rounds >= 1 (summed over rounds) */
   int64_t rescan_blocks;    /* 512-row blocks re-scanned in rounds >= 1 (summed over rounds) */
   int32_t cm_k;             /* components left when the component-matrix finish ran (0: not used) */
-  int32_t cm_pad;
+  int32_t cm_retries;       /* solves repeated without the component matrix (its candidate list overflowed) */
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */

@@ -86,7 +86,7 @@ class appd_stats(ctypes.Structure):
         ("rescan_rows", ctypes.c_int64),
         ("rescan_blocks", ctypes.c_int64),
         ("cm_k", ctypes.c_int32),
-        ("cm_pad", ctypes.c_int32),
+        ("cm_retries", ctypes.c_int32),
     ]
 
     def as_dict(self):

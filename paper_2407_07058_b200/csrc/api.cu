@@ -447,7 +447,8 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     return APPD_OK;
   };
   const int finish_k = c->opt.finish_k == 0 ? 128 : std::min(c->opt.finish_k, 128);
-  bool cm_timing_pending = false;
+  bool cm_timing_pending = false, cm_status_pending = false;
+  c->pinned_small[48] = 0;
   while (k > 1) {
     // ---- component-matrix finish: the contracted k-node graph's exact edge keys ----
     if (use_tc && tc.topk && rounds > 0 && finish_k > 0 && k <= finish_k) {
@@ -456,7 +457,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       if (!WCM) return fail(c, APPD_ERR_OUT_OF_MEMORY, "component matrix");
       bool ovf = false;
       if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
-      if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf))) return s;
+      if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf, c->opt.world > 1))) return s;
       if (c->opt.world > 1) {  // every rank must take the same branch
         u64* flag = (u64*)ws(c, S_TMP, sizeof(u64));
         if (!flag) return fail(c, APPD_ERR_OUT_OF_MEMORY, "flag");
@@ -472,7 +473,14 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       if (!ovf) {
         // Prim on the contracted graph on the device (keys are a strict order: the MST is
         // unique); its k - 1 edges are appended to mstkeys, the count checked at the end
-        if ((s = launch_cm_prim(c, WCM, (int)k, mstkeys, counters))) return s;
+        // (one rank: a listing overflow is detected on the device, read at the end)
+        unsigned* cm_status = reinterpret_cast<unsigned*>(counters + 4);
+        if ((s = launch_cm_prim(c, WCM, (int)k, mstkeys, counters, tc.counters + 1, tc.list_entries_cap, tc.cstart,
+                                tc.perm, cm_status)))
+          return s;
+        APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 48, cm_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                     c->stream));
+        cm_status_pending = true;
         if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
         cm_timing_pending = c->opt.timing != 0;  // read after the final synchronisation
         c->stats.cm_k = (int)k;
@@ -693,6 +701,17 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if ((s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, stride, n, M, row0, sense < 0))) return s;
   stage_event(c, 6);
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (cm_status_pending && c->pinned_small[48] == 1) {
+    // the component matrix's candidate list overflowed: solve again without it (rare)
+    const int fk = c->opt.finish_k;
+    c->opt.finish_k = -1;
+    const appd_status s2 = solve(c, W, X, n, d, M);
+    c->opt.finish_k = fk;
+    c->stats.cm_retries++;
+    return s2;
+  }
+  if (cm_status_pending && c->pinned_small[48] != 0)
+    return fail(c, APPD_ERR_CUDA, "component matrix disconnected (internal error)");
   if (*mst_count != n - 1)
     return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", *mst_count, (long long)(n - 1));
   if (cm_timing_pending) c->stats.ms_scan += ev_ms(c, 8, 9);

@@ -182,10 +182,12 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
                       u64* compbest, int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
 
-appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters);
+appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters,
+                           const unsigned* list_count, unsigned list_cap, const int* cstart, const int* perm,
+                           unsigned* status);
 appd_status tcf_lookup_async(appd_ctx* c, TcState* st, const int* comp, u64* compbest);
 appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, int64_t k, u64* WCM,
-                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow);
+                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow, bool check_now);
 
 // candidate cache (k_cache.cu)
 struct ErrModel;

@@ -413,10 +413,21 @@ __global__ void k_chunk_hist(const unsigned* __restrict__ list, const unsigned* 
 __global__ void k_chunk_scatter(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
                                 const unsigned* __restrict__ offs, unsigned* __restrict__ cursor,
                                 unsigned* __restrict__ out) {
+  // warp-aggregated per chunk: the lanes of one chunk take consecutive slots in lane
+  // order, so runs of rows listed together (one filter warp: consecutive rows, mostly one
+  // component) stay together and in order
   const unsigned total = min(*count, cap);
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const unsigned v = list[e], ch = v >> LIST_SHIFT;
-    out[offs[ch] + atomicAdd(cursor + ch, 1u)] = v;
+  const int lane = threadIdx.x & 31;
+  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < total; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + lane;
+    const bool ok = e < total;
+    const unsigned v = ok ? list[e] : 0xFFFFFFFFu, ch = v >> LIST_SHIFT;
+    const unsigned peers = __match_any_sync(0xffffffffu, ch);
+    const int leader = __ffs(peers) - 1;
+    unsigned base = 0;
+    if (ok && lane == leader) base = atomicAdd(cursor + ch, (unsigned)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    if (ok) out[offs[ch] + base + __popc(peers & ((1u << lane) - 1u))] = v;
   }
 }
 // runs from the histogram: run_lo = offsets, run_nb = 128-row batches
@@ -1139,17 +1150,28 @@ __global__ void k_cm_filter(CmParams P) {
         unsigned mask = 0;
 #pragma unroll
         for (int u = 0; u < U; u++) mask |= (v[u] >= thr && v[u] > -INFINITY) ? 1u << u : 0u;
-        if (!__any_sync(0xffffffffu, mask != 0)) continue;
-        unsigned cnt = 0;
-        for (unsigned m = mask; m; m &= m - 1)
-          cnt += (unsigned)min(TC_TMG / 32, (P.n - (s0 + __ffs(m) - 1) * TC_TMG + 31) / 32);
-        unsigned slot = warp_alloc(P.counters + 1, cnt);
-        while (mask) {
-          const int sg = s0 + __ffs(mask) - 1;
-          mask &= mask - 1;
+        unsigned any = __reduce_or_sync(0xffffffffu, mask);
+        // chunk-major emission: for each flagged segment and chunk, the warp's rows in
+        // lane order (consecutive rows, mostly one component), so that the chunk runs of
+        // the counting sort keep rows of one component together (k_list_exact<1>)
+        while (any) {
+          const int u = __ffs(any) - 1;
+          any &= any - 1;
+          const bool mine = (mask >> u) & 1u;
+          const unsigned bal = __ballot_sync(0xffffffffu, mine);
+          const int sg = s0 + u;
           const int nc = min(TC_TMG / 32, (P.n - sg * TC_TMG + 31) / 32);
-          for (int t = 0; t < nc; t++, slot++)
-            if (slot < P.list_cap) P.list[slot] = ((unsigned)((TC_TMG / 32) * sg + t) << LIST_SHIFT) | (unsigned)p;
+          const unsigned cntw = (unsigned)__popc(bal);
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(P.counters + 1, cntw * (unsigned)nc);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (mine) {
+            const unsigned rank = (unsigned)__popc(bal & ((1u << lane) - 1u));
+            for (int t = 0; t < nc; t++) {
+              const unsigned slot = base + (unsigned)t * cntw + rank;
+              if (slot < P.list_cap) P.list[slot] = ((unsigned)((TC_TMG / 32) * sg + t) << LIST_SHIFT) | (unsigned)p;
+            }
+          }
         }
       }
       s = e;
@@ -1236,8 +1258,15 @@ __global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restric
 
 // Final contracted MST: Prim on min(WCM[C][D], WCM[D][C]) (exact keys, a strict order),
 // the k - 1 edge keys appended to mstkeys at counters[0]
+// If the listing overflowed (*list_count > list_cap: minima may be missing) or the
+// matrix is disconnected, the remaining k - 1 - added edges are placeholders of a star
+// over component representatives (valid indices, largest key) so that every later
+// kernel stays in bounds, and status records why (1 overflow, 2 disconnected): the host
+// re-solves without the component matrix, or reports the inconsistency.
 __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
-                                                 int* __restrict__ counters) {
+                                                 int* __restrict__ counters, const unsigned* __restrict__ list_count,
+                                                 unsigned list_cap, const int* __restrict__ cstart,
+                                                 const int* __restrict__ perm, unsigned* __restrict__ status) {
   extern __shared__ u64 wsym[];  // [k][k] symmetric minima
   const int lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
@@ -1248,6 +1277,7 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
   __syncthreads();
   if (threadIdx.x >= 32) return;
   const int base = counters[0];
+  const bool overflow = *list_count > list_cap;
   u64 key[4];
   bool in[4];
 #pragma unroll
@@ -1269,7 +1299,7 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if (bv == KEY_NONE) break;  // disconnected: the edge-count check reports it
+    if (bv == KEY_NONE || overflow) break;
     if (lane == 0) mstkeys[base + step - 1] = bv;
     added = step;
     if ((bi & 31) == lane) {
@@ -1286,6 +1316,21 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
       }
     }
   }
+  if (added < k - 1) {  // placeholders: component 0 (in the tree) to every node not in it
+    const int r0 = perm[cstart[0]];
+    int off = base + added;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int q = lane + 32 * t;
+      const bool need = q < k && !in[t];
+      const unsigned bal = __ballot_sync(0xffffffffu, need);
+      if (need)
+        mstkeys[off + __popc(bal & ((1u << lane) - 1u))] = (0x7F7FFFFFull << 33) | tri_index(r0, perm[cstart[q]]);
+      off += __popc(bal);
+    }
+    if (lane == 0) *status = overflow ? 1u : 2u;
+    added = k - 1;
+  }
   if (lane == 0) counters[0] = base + added;
 }
 
@@ -1296,10 +1341,12 @@ appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsign
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
-appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters) {
+appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters,
+                           const unsigned* list_count, unsigned list_cap, const int* cstart, const int* perm,
+                           unsigned* status) {
   const size_t smem = sizeof(u64) * k * k;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_prim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cm_prim<<<1, 256, smem, c->stream>>>(WCM, k, mstkeys, counters);
+  k_cm_prim<<<1, 256, smem, c->stream>>>(WCM, k, mstkeys, counters, list_count, list_cap, cstart, perm, status);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -714,34 +714,20 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   if (!runs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list runs");
   unsigned *run_lo = runs, *run_nb = runs + (nch + 2), *item_start = runs + 2 * (nch + 2);
   unsigned *hist = runs + 3 * (nch + 2), *offs = runs + 4 * (nch + 2), *cursor = runs + 5 * (nch + 2);
-  const bool counting = mode == 0;  // rows within a chunk may come in any order: no host round trip
-  int4* items;
-  if (counting) {
-    cnt = st->list_entries_cap;  // capacity bound; the kernels read the real count on the device
-    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                 c->stream));  // statistics, read after a later synchronisation
-    items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
-    if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
-    if ((s = launch_list_counting(c, st->lista, count_dev, cnt, nch, hist, offs, cursor, st->listb, run_lo, run_nb,
-                                  item_start, items)))
-      return s;
-  } else {
-    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                 c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-    cnt = std::min(c->pinned_small[16], st->list_entries_cap);
-    st->last_list_entries = c->pinned_small[16];
-    if (cnt == 0) return APPD_OK;
-    // the component-matrix reduction wants the rows of a chunk in order: full sort
-    if ((s = sort_keys_u32_bits(c, st->lista, st->listb, cnt, 0, 17 + bits_for(nch + 1)))) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(st->counters + 8, &cnt, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
-    items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
-    if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
-  }
+  // counting sort by chunk on the device (no host round trip); the count is read at a
+  // later synchronisation for the statistics (and the component-matrix overflow check)
+  cnt = st->list_entries_cap;  // capacity bound; the kernels read the real count on the device
+  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                               c->stream));
+  int4* items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
+  if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
+  if ((s = launch_list_counting(c, st->lista, count_dev, cnt, nch, hist, offs, cursor, st->listb, run_lo, run_nb,
+                                item_start, items)))
+    return s;
   ListParams L;
   memset(&L, 0, sizeof L);
   L.list = st->listb;
-  L.count = counting ? count_dev : st->counters + 8;
+  L.count = count_dev;
   L.cap = cnt;
   L.nch = nch;
   L.n = (int)st->n;
@@ -760,7 +746,7 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   L.sc = st->sc;
   L.k = k;
   L.WCM = WCM;
-  return launch_list_exact(c, mode, L, counting ? nullptr : run_lo, run_nb, item_start);
+  return launch_list_exact(c, mode, L, nullptr, run_nb, item_start);
 }
 
 // Queue the cache lookup of the next round (compbest must hold KEY_NONE): per-row first
@@ -924,8 +910,11 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
 // then WCM[C][D] = exact minimum edge key between components C and D (k x k, device).
 // *listed_overflow is set when the candidate list overflowed (the caller then runs an
 // ordinary round instead).
+// check_now: synchronise and report a listing overflow here (multi-rank: every rank must
+// agree before the reduction); otherwise the overflow is detected on the device by the
+// contracted-graph Prim (k_cm_prim) and reported at the caller's final synchronisation
 appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, int64_t k, u64* WCM,
-                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow) {
+                   int64_t rb_begin, int64_t rb_end, bool* listed_overflow, bool check_now) {
   const int64_t n = st->n;
   const int grid_n = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
   appd_status s;
@@ -990,8 +979,12 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   if ((s = launch_cm_thresholds(c, CUB, (int)k, T))) return s;
   C.CUB = T;
   if ((s = launch_cm_filter(c, C))) return s;
-  if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;  // synchronises
-  if (st->last_list_entries > st->list_entries_cap) *listed_overflow = true;
+  if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;
+  if (check_now) {
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    st->last_list_entries = c->pinned_small[16];
+    if (st->last_list_entries > st->list_entries_cap) *listed_overflow = true;
+  }
   return APPD_OK;
 }
 
