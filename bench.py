@@ -349,6 +349,63 @@ def run_native(args):
     return 0
 
 
+def run_floyd(args):
+    """NEXT-2: appd_floyd_weights, the paper's minimax Floyd-Warshall, on a
+    seeded uniform n x n W (one GPU).  Metric: (min, max) relaxations per second (n^3 per
+    solve).  Roofline: ALU pipe, 1.5 FMNMX instructions per relaxation (two maxima and one
+    3-input minimum per pair of k) against 64 lanes/clk/SM x SMs x the sampled SM clock."""
+    import numpy as np
+    import torch
+    import paper_2407_07058_b200 as P
+    import oracle
+    from synth import generators as G
+    n = args.floyd
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    W = torch.from_numpy(np.ascontiguousarray(G.random_weights(n, 7, "uniform"), np.float32)).to(dev)
+    M = torch.empty((n, n), device=dev)
+    ctx = P.Context(timing=True)
+    for _ in range(max(args.warmup, 1)):
+        ctx.floyd_weights(W, M)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    sampler.start()
+    ts = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.floyd_weights(W, M)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    ms = statistics.mean(ts)
+    relax = float(n) ** 3 / (ms / 1000)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    pk = peaks()
+    clk = clocks["sm_mhz"] or pk["sm_max_mhz"]
+    peak_alu = sm_count * 64 * clk * 1e6 / 1e12
+    ach = relax * 1.5 / 1e12
+    # oracle (the literal triple loop, one core) on a bounded sample size
+    ns = 384
+    Ws = G.random_weights(ns, 7, "uniform")
+    t0 = time.perf_counter()
+    oracle.floyd(Ws)
+    tcpu = time.perf_counter() - t0
+    line = {"metric": "minimax Floyd-Warshall relaxations/s (NEXT-2)", "value": relax, "unit": "relaxations/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"floyd_n{n}", "n": n, "weights": "uniform open (0,1), seed 7"},
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak_alu, "unit": "T inst-lanes/s",
+                         "frac": ach / peak_alu, "traffic": None, "kernel": "k_fw_tiles",
+                         "peak_source": "64 ALU lanes/clk/SM (FMNMX) x SMs x sampled SM clock (B200_PROFILING.md)"},
+            "cpu_baseline": {"value": float(ns) ** 3 / tcpu, "unit": "relaxations/s", "cores": 1, "kind": "oracle",
+                             "sample": f"oracle_floyd at n={ns} ({tcpu:.2f} s)"},
+            "gpu_launches": ctx.stats()["kernel_launches"], "clocks": clocks}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,7 +417,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--floyd", type=int, default=0, help="NEXT-2: time appd_floyd_weights at this n instead")
     args = ap.parse_args()
+    if args.floyd:
+        return run_floyd(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_native(args)

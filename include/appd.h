@@ -147,6 +147,16 @@ appd_status appd_solve_points(appd_ctx* ctx, const float* X, int64_t n, int64_t 
 appd_status appd_solve_points_host(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host);
 appd_status appd_solve_weights_host(appd_ctx* ctx, const float* W_host, int64_t n, float* M_host);
 
+/* NEXT-2: the paper's comparison algorithm, the minimax variant of
+ * Floyd–Warshall ("a modified version of the Floyd-Warshall algorithm", Fig. floyd
+ * k outermost, M[i][j] = min(M[i][j], max(M[i][k], M[k][j])); O(n^3)),
+ * as a blocked (min, max) closure on the GPU.  W, M: DEVICE n x n fp32 row-major, distinct
+ * buffers (M is overwritten; W is read only).  Same validation and error behaviour as
+ * appd_solve_weights; opt.sense -1 gives the widest-path APPD.  -0 reads as +0 and the
+ * diagonal is +0 (Q3, Q5), so M is bit-identical to appd_solve_weights' result.  One
+ * rank only (world > 1: APPD_ERR_UNSUPPORTED); n <= 65536. */
+appd_status appd_floyd_weights(appd_ctx* ctx, const float* W, int64_t n, float* M);
+
 void appd_destroy(appd_ctx* ctx); /* NULL-safe; frees the workspace and the NCCL communicator */
 
 /* ---- support ---- */

@@ -95,7 +95,7 @@ class appd_stats(ctypes.Structure):
 
 EXPORTS = [
     "appd_options_init", "appd_create", "appd_set_stream", "appd_solve_weights", "appd_solve_points",
-    "appd_solve_points_host", "appd_solve_weights_host", "appd_destroy", "appd_row_range", "appd_row_range_of",
+    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_destroy", "appd_row_range", "appd_row_range_of",
     "appd_points_weights", "appd_get_nccl_unique_id", "appd_get_stats", "appd_last_dendrogram",
     "appd_error_index", "appd_last_error", "appd_status_string", "appd_version",
 ]
@@ -120,6 +120,7 @@ def load(path: str = LIB_PATH):
     L.appd_solve_points.argtypes = [P, P, I64, I64, P]
     L.appd_solve_points_host.argtypes = [P, P, I64, I64, P]
     L.appd_solve_weights_host.argtypes = [P, P, I64, P]
+    L.appd_floyd_weights.argtypes = [P, P, I64, P]
     L.appd_destroy.restype = None
     L.appd_destroy.argtypes = [P]
     L.appd_row_range.argtypes = [P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -261,6 +262,17 @@ class Context:
         s = self._L.appd_solve_weights(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_weights")
+        return M
+
+    def floyd_weights(self, W, M=None):
+        """appd_floyd_weights (NEXT-2): the minimax Floyd–Warshall closure of the n x n W
+        on the GPU (one rank); M must not alias W."""
+        _check_tensor(W, "W")
+        n = W.shape[-1]
+        M = self._out(n, M)
+        s = self._L.appd_floyd_weights(self._h, _ptr(W), n, _ptr(M))
+        if s != APPD_OK:
+            self._raise(s, "appd_floyd_weights")
         return M
 
     def solve_points(self, X, M=None):

@@ -746,6 +746,52 @@ extern "C" appd_status appd_solve_weights(appd_ctx* c, const float* W, int64_t n
   return solve(c, W, nullptr, n, 0, M);
 }
 
+// NEXT-2: the paper's comparison algorithm (minimax Floyd–Warshall) on
+// the GPU, k_floyd.cu.  Single rank (O(n^3); no sharding); same validation as
+// appd_solve_weights; opt.sense selects minimax (+1) or widest (-1).
+extern "C" appd_status appd_floyd_weights(appd_ctx* c, const float* W, int64_t n, float* M) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
+  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_floyd_weights runs on one rank (world = %d)", c->opt.world);
+  if (n > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "appd_floyd_weights: n = %lld > 65536 (O(n^3))", (long long)n);
+  if ((s = check_device_ptr(c, W, "W"))) return s;
+  if ((s = check_device_ptr(c, M, "M"))) return s;
+  if (W == M) return fail(c, APPD_ERR_INVALID_ARGUMENT, "W and M must not alias");
+  std::memset(&c->stats, 0, sizeof c->stats);
+  c->stats.struct_size = sizeof(appd_stats);
+  c->stats.n = n;
+  c->stats.rows = n;
+  c->launches = 0;
+  c->have_dendrogram = false;
+  c->err_i = c->err_j = -1;
+  c->last_error.clear();
+  stage_event(c, 0);
+  if (c->opt.validate) {
+    u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
+    if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
+    u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);
+    APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
+    if ((s = launch_validate_weights(c, W, n, 0, n, bad))) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    u64 hb[3];
+    memcpy(hb, hbad, sizeof hb);
+    if ((s = report_validation(c, hb, n, false, 0))) return s;
+  }
+  stage_event(c, 1);
+  if ((s = floyd_weights(c, W, n, M, c->opt.sense >= 0 ? 1 : -1))) return s;
+  stage_event(c, 6);
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  c->stats.kernel_launches = c->launches;
+  c->stats.fill_bytes = n * n * 4;
+  if (c->opt.timing) {
+    c->stats.ms_validate = ev_ms(c, 0, 1);
+    c->stats.ms_total = ev_ms(c, 0, 6);
+  }
+  return APPD_OK;
+}
+
 extern "C" appd_status appd_solve_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M) {
   appd_status s = enter(c);
   if (s) return s;

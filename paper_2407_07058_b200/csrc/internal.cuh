@@ -182,6 +182,7 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
                       u64* compbest, int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
 
+appd_status floyd_weights(appd_ctx* c, const float* W, int64_t n, float* M, int sense);
 appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int* counters,
                            const unsigned* list_count, unsigned list_cap, const int* cstart, const int* perm,
                            unsigned* status);

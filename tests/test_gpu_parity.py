@@ -122,6 +122,53 @@ def test_c3_closed_form_and_oracle(ctx):
 
 
 # --------------------------------------------------------------------------
+# NEXT-2: the paper's comparison algorithm (minimax Floyd-Warshall) on the GPU
+# --------------------------------------------------------------------------
+def gpu_floyd(c, W):
+    Wt = torch.from_numpy(np.ascontiguousarray(W, np.float32)).cuda()
+    return c.floyd_weights(Wt).cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties", "negative", "signed_zero", "huge"])
+def test_floyd_against_oracle_floyd(ctx, kind):
+    """Blocked (min, max) closure vs the oracle's literal triple loop, ragged
+    tile counts (tile 128) included; and vs Algorithm 4 (the same APPD, reading Q9)."""
+    for t, n in enumerate([1, 2, 3, 5, 31, 127, 128, 129, 200, 256, 257, 385]):
+        W = G.random_weights(n, 700 + t, kind)
+        want = oracle.floyd(W)
+        assert_bit_equal(gpu_floyd(ctx, W), want, f"floyd {kind} n={n}")
+    W = G.random_weights(1000, 799, kind)
+    assert_bit_equal(gpu_floyd(ctx, W), oracle.appd_weights(W), f"floyd {kind} n=1000 vs Algorithm 4")
+
+
+def test_floyd_widest(P):
+    with P.Context(sense=-1) as cw:
+        for t, n in enumerate([2, 3, 64, 129, 300]):
+            for kind in ("uniform", "ties", "negative"):
+                W = G.random_weights(n, 40 + t, kind)
+                assert_bit_equal(gpu_floyd(cw, W), oracle.floyd(W, -1), f"floyd widest {kind} n={n}")
+
+
+def test_floyd_equals_boruvka_path_c1_c3(ctx):
+    """C1 against the oracle; the C3 recipe at n = 4096 (32 tiles, heavy ties) against
+    the Boruvka path's result and Algorithm 4."""
+    W = G.config("C1")
+    assert_bit_equal(gpu_floyd(ctx, W), oracle.appd_weights(W), "floyd C1")
+    W = G.config("C3", n=4096)
+    Mf = gpu_floyd(ctx, W)
+    assert_bit_equal(Mf, gpu_weights(ctx, W), "floyd C3 n=4096 vs Boruvka path")
+    assert_bit_equal(Mf, oracle.appd_weights(W), "floyd C3 n=4096 vs Algorithm 4")
+
+
+def test_floyd_validation(ctx, P):
+    W = G.random_weights(130, 5, "uniform")
+    W[3, 7] = np.float32(0.123)  # asymmetric
+    with pytest.raises(P.AppdError) as e:
+        gpu_floyd(ctx, W)
+    assert e.value.name == "APPD_ERR_NOT_SYMMETRIC" and e.value.index == (3, 7)
+
+
+# --------------------------------------------------------------------------
 # points mode
 # --------------------------------------------------------------------------
 def test_r1_weights_bitexact_and_fp64(ctx):
