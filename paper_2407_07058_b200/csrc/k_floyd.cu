@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(1024) k_fw_phase1(float* __restrict__ M, int n
 // mode 0: phase 3 over (I, J), I, J != kb; mode 1: phase 2 (row panels J != kb, then
 // column panels I != kb).
 template <int SENSE>
-__global__ void __launch_bounds__(256, 1) k_fw_tiles(float* __restrict__ M, int n, int kb, int mode) {
+__global__ void __launch_bounds__(256, 2) k_fw_tiles(float* __restrict__ M, int n, int kb, int mode) {
   extern __shared__ __align__(16) float fsm[];
   float* As = fsm;                          // [2][FW_T][FW_AS]
   float* Bs = fsm + 2 * FW_T * FW_AS;       // [2][FW_KC][FW_BS]
