@@ -147,6 +147,17 @@ appd_status appd_solve_points(appd_ctx* ctx, const float* X, int64_t n, int64_t 
 appd_status appd_solve_points_host(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host);
 appd_status appd_solve_weights_host(appd_ctx* ctx, const float* W_host, int64_t n, float* M_host);
 
+/* NEXT-4 ("at least O(n^2)"): points mode with the n x n output
+ * streamed to HOST memory in blocks of block_rows original rows (0: ~1 GiB per block), so
+ * n is bounded by host memory, not HBM.  X_host: n x d fp32 (host); M_host: n x n fp32
+ * host buffer (pinned for full PCIe overlap; pageable works, slower).  The MST and the
+ * dendrogram run once; each block's rows are filled into one of two device buffers while
+ * the previous block is copied out on a second stream.  Same results, validation and
+ * errors as appd_solve_points; one rank only; the device holds X, the O(n) state and
+ * 2 x block_rows x n floats. */
+appd_status appd_solve_points_stream(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host,
+                                     int64_t block_rows);
+
 /* NEXT-2: the paper's comparison algorithm, the minimax variant of
  * Floyd–Warshall ("a modified version of the Floyd-Warshall algorithm", Fig. floyd
  * k outermost, M[i][j] = min(M[i][j], max(M[i][k], M[k][j])); O(n^3)),

@@ -95,7 +95,7 @@ class appd_stats(ctypes.Structure):
 
 EXPORTS = [
     "appd_options_init", "appd_create", "appd_set_stream", "appd_solve_weights", "appd_solve_points",
-    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_destroy", "appd_row_range", "appd_row_range_of",
+    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_solve_points_stream", "appd_destroy", "appd_row_range", "appd_row_range_of",
     "appd_points_weights", "appd_get_nccl_unique_id", "appd_get_stats", "appd_last_dendrogram",
     "appd_error_index", "appd_last_error", "appd_status_string", "appd_version",
 ]
@@ -121,6 +121,7 @@ def load(path: str = LIB_PATH):
     L.appd_solve_points_host.argtypes = [P, P, I64, I64, P]
     L.appd_solve_weights_host.argtypes = [P, P, I64, P]
     L.appd_floyd_weights.argtypes = [P, P, I64, P]
+    L.appd_solve_points_stream.argtypes = [P, P, I64, I64, P, I64]
     L.appd_destroy.restype = None
     L.appd_destroy.argtypes = [P]
     L.appd_row_range.argtypes = [P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -273,6 +274,21 @@ class Context:
         s = self._L.appd_floyd_weights(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_floyd_weights")
+        return M
+
+    def solve_points_stream(self, X, M, block_rows=0):
+        """appd_solve_points_stream (NEXT-4): X and M are HOST (CPU) float32 tensors, M n x n
+        (pinned for overlap); M is written in blocks of block_rows rows (0 = auto)."""
+        _check_tensor(X, "X")
+        _check_tensor(M, "M")
+        n, d = X.shape
+        if X.is_cuda or M.is_cuda:
+            raise ValueError("solve_points_stream takes host tensors")
+        if M.numel() != n * n:
+            raise ValueError(f"M must hold {n} x {n} floats")
+        s = self._L.appd_solve_points_stream(self._h, _ptr(X), n, d, _ptr(M), int(block_rows))
+        if s != APPD_OK:
+            self._raise(s, "appd_solve_points_stream")
         return M
 
     def solve_points(self, X, M=None):

@@ -211,6 +211,9 @@ extern "C" void appd_destroy(appd_ctx* c) {
   if (c->ev_ready)
     for (int i = 0; i < 16; i++) cudaEventDestroy(c->ev[i]);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->sev_ready)
+    for (int i = 0; i < 4; i++) cudaEventDestroy(c->sev[i]);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pinned_small) cudaFreeHost(c->pinned_small);
   cudaGetLastError();
@@ -347,7 +350,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   stage_event(c, 1);
 
   if (n == 1) {
-    if (rows > 0) {
+    if (c->stream_out) {
+      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      c->stream_out[0] = 0.0f;
+    } else if (rows > 0) {
       appd_status s = launch_set_diag_zero_single(c, M);
       if (s) return s;
     }
@@ -685,6 +691,69 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   const int* rows_sorted = pi;
   int* rowpos = (int*)ws(c, S_ROWPOS, sizeof(int) * n);
   if (!rowpos) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
+  if (c->stream_out) {
+    // ---- NEXT-4: M streamed to host memory in blocks of R original rows.  Per block the
+    // rows' leaf positions are gathered and sorted (the multi-rank fill path), the fill
+    // writes a device block buffer (two, alternating) and copy_stream moves it to the host
+    // while the next block is filled.
+    const int64_t R = std::min<int64_t>(c->stream_block, n);
+    float* dblk = (float*)ws(c, S_HOST_OUT, sizeof(float) * 2 * R * n);
+    int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (R + 1));
+    int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (R + 1));
+    if (!dblk || !keys || !rs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "stream block buffers (%lld rows)", (long long)R);
+    if (!c->copy_stream && cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(c, APPD_ERR_CUDA, "copy stream");
+    if (!c->sev_ready) {
+      for (int i = 0; i < 4; i++)
+        if (cudaEventCreateWithFlags(&c->sev[i], cudaEventDisableTiming) != cudaSuccess)
+          return fail(c, APPD_ERR_CUDA, "stream events");
+      c->sev_ready = true;
+    }
+    stage_event(c, 5);
+    int64_t blocks = 0;
+    for (int64_t b0 = 0; b0 < n; b0 += R, blocks++) {
+      const int64_t rr = std::min(R, n - b0);
+      const int buf = (int)(blocks & 1);
+      float* dst = dblk + (size_t)buf * R * n;
+      if (blocks >= 2) APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + buf], 0));  // buffer copied out
+      if ((s = launch_gather_rowpos(c, pos, b0, rr, keys, keys + rr + 1))) return s;
+      if ((s = sort_pairs_i32(c, keys, rowpos, keys + rr + 1, rs, rr))) return s;
+      if ((s = launch_fill(c, rs, rowpos, rr, pos, ST, stride, n, dst, b0, sense < 0))) return s;
+      APPD_CUDA(c, cudaEventRecord(c->sev[buf], c->stream));
+      APPD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->sev[buf], 0));
+      APPD_CUDA(c, cudaMemcpyAsync(c->stream_out + (size_t)b0 * n, dst, sizeof(float) * rr * n,
+                                   cudaMemcpyDeviceToHost, c->copy_stream));
+      APPD_CUDA(c, cudaEventRecord(c->sev[2 + buf], c->copy_stream));
+    }
+    APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)((blocks - 1) & 1)], 0));  // last copy done
+    if (blocks >= 2) APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)(blocks & 1)], 0));
+    stage_event(c, 6);
+    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (cm_status_pending && c->pinned_small[48] == 1) {
+      const int fk = c->opt.finish_k;
+      c->opt.finish_k = -1;
+      const appd_status s2 = solve(c, W, X, n, d, M);
+      c->opt.finish_k = fk;
+      c->stats.cm_retries++;
+      return s2;
+    }
+    if (cm_status_pending && c->pinned_small[48] != 0)
+      return fail(c, APPD_ERR_CUDA, "component matrix disconnected (internal error)");
+    if (*mst_count != n - 1)
+      return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", *mst_count, (long long)(n - 1));
+    c->stats.fill_bytes = n * n * 4;
+    c->stats.kernel_launches = c->launches;
+    if (c->opt.timing) {
+      c->stats.ms_validate = ev_ms(c, 0, 1);
+      c->stats.ms_mst = ev_ms(c, 1, 2);
+      c->stats.ms_sort = ev_ms(c, 2, 3);
+      c->stats.ms_dendrogram = ev_ms(c, 3, 4);
+      c->stats.ms_prep = ev_ms(c, 4, 5);
+      c->stats.ms_fill = ev_ms(c, 5, 6);
+      c->stats.ms_total = ev_ms(c, 0, 6);
+    }
+    return APPD_OK;
+  }
   if (c->opt.world == 1) {
     if ((s = launch_iota(c, rowpos, n))) return s;
   } else {
@@ -827,6 +896,29 @@ static appd_status solve_host(appd_ctx* c, const float* Wh, const float* Xh, int
 extern "C" appd_status appd_solve_points_host(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M) {
   if (c && n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072");
   return solve_host(c, nullptr, X, n, d, M);
+}
+
+// NEXT-4: points mode with M streamed to host memory in row blocks (n beyond HBM)
+extern "C" appd_status appd_solve_points_stream(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M,
+                                                int64_t block_rows) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (!X || !M) return fail(c, APPD_ERR_INVALID_ARGUMENT, "NULL host buffer");
+  if (n < 1 || d < 1 || block_rows < 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n, d, block_rows");
+  if (n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072");
+  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_stream runs on one rank");
+  // default block: 1 GiB of rows per buffer (two buffers), at least 128 rows
+  const int64_t R = block_rows ? block_rows : std::max<int64_t>(128, ((int64_t)1 << 28) / n);
+  float* din = (float*)ws(c, S_HOST_IN, sizeof(float) * n * d);
+  if (!din) return fail(c, APPD_ERR_OUT_OF_MEMORY, "device copy of X");
+  APPD_CUDA(c, cudaMemcpyAsync(din, X, sizeof(float) * n * d, cudaMemcpyHostToDevice, c->stream));
+  c->stream_out = M;
+  c->stream_block = R;
+  s = solve(c, nullptr, din, n, d, nullptr);
+  c->stream_out = nullptr;
+  c->stream_block = 0;
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  return s;
 }
 
 extern "C" appd_status appd_solve_weights_host(appd_ctx* c, const float* W, int64_t n, float* M) {

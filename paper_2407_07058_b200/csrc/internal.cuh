@@ -111,6 +111,13 @@ struct appd_ctx {
   size_t pinned_bytes = 0;
   unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
   std::vector<int32_t> uf_scratch;   // host dendrogram work arrays
+  // streamed output (NEXT-4, appd_solve_points_stream): M rows go to this host buffer in
+  // blocks of stream_block rows, two device block buffers, copies on copy_stream
+  float* stream_out = nullptr;
+  int64_t stream_block = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t sev[4];  // filled[2], copied[2]
+  bool sev_ready = false;
 };
 
 namespace appd {

@@ -257,6 +257,31 @@ def test_points_engine_paths_taken(P):
     c.close()
 
 
+def test_points_stream_to_host(ctx):
+    """NEXT-4: M streamed to host memory in row blocks (ragged last block, one block,
+    several blocks) equals the oracle and the device-resident path bit for bit."""
+    for t, (kind, n, d, block) in enumerate([("blobs", 1, 3, 0), ("blobs", 2, 3, 1), ("uniform", 300, 5, 128),
+                                             ("clumps", 3000, 8, 256), ("dups", 2500, 16, 0), ("blobs", 4100, 64, 1000)]):
+        X = G.random_points(n, d, 950 + t, kind)
+        M = torch.empty((n, n), dtype=torch.float32).pin_memory()
+        ctx.solve_points_stream(torch.from_numpy(X), M, block)
+        got = M.numpy()
+        assert_bit_equal(got, oracle.appd_points(X), f"stream {kind} n={n} block={block}")
+        assert_bit_equal(got, gpu_points(ctx, X), f"stream vs device {kind} n={n}")
+
+
+def test_points_stream_large_vs_device(ctx):
+    """32768 points (4 GiB of output) in 3000-row blocks against the device path."""
+    X = G.config("C4", n=32768)
+    n = X.shape[0]
+    M = torch.empty((n, n), dtype=torch.float32).pin_memory()
+    ctx.solve_points_stream(torch.from_numpy(X), M, 3000)
+    ref = ctx.solve_points(torch.from_numpy(X).cuda()).cpu()
+    assert torch.equal(M.view(torch.int32), ref.view(torch.int32))
+    st = ctx.stats()
+    assert st["fill_bytes"] == n * n * 4
+
+
 def test_points_list_overflow_is_exact(P, monkeypatch):
     """A candidate list far too small for the input: rows whose entries are lost are
     poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the
