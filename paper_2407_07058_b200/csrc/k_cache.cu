@@ -556,25 +556,38 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
       __syncthreads();
       // warp w holds rows 16 w .. 16 w + 15: skip the padding of a chunk's ragged last batch
       if (16 * warp < nb) {
-      float acc[4][4];
+      // packed pairs (FADD2 / FFMA2): rows P0 = (a0, a1), P1 = (a2, a3); columns
+      // Q0 = (b0, b1), Q1 = (b2, b3) and their swaps (b1, b0), (b3, b2) built in registers.
+      // P - Q gives (a0 b0, a1 b1), P - Qs gives (a0 b1, a1 b0): 16 pairs in 8 + 8 packed
+      // instructions per coordinate, each half the R1 step of its pair
+      unsigned long long acc2[2][2][2];  // [row pair][column pair][swapped]
 #pragma unroll
-      for (int a = 0; a < 4; a++)
+      for (int a = 0; a < 2; a++)
 #pragma unroll
-        for (int b = 0; b < 4; b++) acc[a][b] = 0.0f;
+        for (int b = 0; b < 2; b++) acc2[a][b][0] = acc2[a][b][1] = 0ull;
 #pragma unroll 4
       for (int k = 0; k < L.d; k++) {
-        const float4 xa = *reinterpret_cast<const float4*>(rowx + k * LE_RB + 4 * ty);
+        const ulonglong2 xa = *reinterpret_cast<const ulonglong2*>(rowx + k * LE_RB + 4 * ty);
         const float4 xb = *reinterpret_cast<const float4*>(colx + k * 32 + 4 * tx);
-        const float av[4] = {xa.x, xa.y, xa.z, xa.w};
-        const float bv[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-#pragma unroll
-          for (int b = 0; b < 4; b++) {
-            const float t = __fsub_rn(av[a], bv[b]);
-            acc[a][b] = __fmaf_rn(t, t, acc[a][b]);
-          }
+        const unsigned long long q0 = f2pack(xb.x, xb.y), q1 = f2pack(xb.z, xb.w);
+        const unsigned long long s0 = f2pack(xb.y, xb.x), s1 = f2pack(xb.w, xb.z);
+        acc2[0][0][0] = f2_r1_step(xa.x, q0, acc2[0][0][0]);
+        acc2[0][0][1] = f2_r1_step(xa.x, s0, acc2[0][0][1]);
+        acc2[0][1][0] = f2_r1_step(xa.x, q1, acc2[0][1][0]);
+        acc2[0][1][1] = f2_r1_step(xa.x, s1, acc2[0][1][1]);
+        acc2[1][0][0] = f2_r1_step(xa.y, q0, acc2[1][0][0]);
+        acc2[1][0][1] = f2_r1_step(xa.y, s0, acc2[1][0][1]);
+        acc2[1][1][0] = f2_r1_step(xa.y, q1, acc2[1][1][0]);
+        acc2[1][1][1] = f2_r1_step(xa.y, s1, acc2[1][1][1]);
       }
+      float acc[4][4];
+#pragma unroll
+      for (int pa = 0; pa < 2; pa++)
+#pragma unroll
+        for (int pb = 0; pb < 2; pb++) {
+          f2unpack(acc2[pa][pb][0], acc[2 * pa][2 * pb], acc[2 * pa + 1][2 * pb + 1]);
+          f2unpack(acc2[pa][pb][1], acc[2 * pa][2 * pb + 1], acc[2 * pa + 1][2 * pb]);
+        }
       // R1 ends with sqrtf; the MST runs on d^2 (monotone, App. A.4)
       if (MODE == 0) {
 #pragma unroll
