@@ -530,13 +530,13 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
       Dq[b] = (MODE == 1 && q < L.n) ? L.sc[q] : -1;
     }
     {
-      if (threadIdx.x < LE_RB) rowp[threadIdx.x] = threadIdx.x < nb ? (int)(L.list[b0 + threadIdx.x] & LIST_ROWMASK) : -1;
-      __syncthreads();
       // stage the batch's rows transposed: lane = row of a 32-row group, float4 loads; the 8
-      // warps split the 4 row groups x 2 halves of k
+      // warps split the 4 row groups x 2 halves of k; each reads its row's list entry itself
+      // (no barrier between the list read and the row loads)
       for (int g = warp; g < 2 * (LE_RB / 32); g += blockDim.x >> 5) {
         const int r = (g >> 1) * 32 + lane;
-        const int p = rowp[r];
+        const int p = r < nb ? (int)(__ldg(L.list + b0 + r) & LIST_ROWMASK) : -1;
+        if ((g & 1) == 0) rowp[r] = p;
         const int op = p < 0 ? 0 : (L.perm ? L.perm[p] : p);
         if ((L.d & 3) == 0) {
           const float4* src = reinterpret_cast<const float4*>(L.X + (int64_t)op * L.d);
