@@ -65,8 +65,20 @@ __global__ void __launch_bounds__(256) k_validate_square(const float* __restrict
     b[r][4 * c4 + 3] = vb[s4].w;
   }
   __syncthreads();
-  u64 bad_nf = KEY_NONE, bad_diag = KEY_NONE, bad_sym = KEY_NONE;
+  // fast path: 32-bit tests only (non-finite: exponent all ones; asymmetric: different bits
+  // unless both are zeros of either sign; bad diagonal: a non-zero on the diagonal); the
+  // exact first offenders are located only in a tile that has one
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  const bool diag_tile = I == J;
+  unsigned flag = 0;
+  for (int r = ty; r < VT; r += 4) {
+    const uint32_t bx = __float_as_uint(a[r][tx]), by = __float_as_uint(b[tx][r]);
+    flag |= ((bx & 0x7F800000u) == 0x7F800000u) | ((by & 0x7F800000u) == 0x7F800000u);
+    flag |= (bx != by) & (((bx | by) << 1) != 0u);
+    if (diag_tile) flag |= (r == tx) & ((bx << 1) != 0u);
+  }
+  if (!__syncthreads_or(flag)) return;
+  u64 bad_nf = KEY_NONE, bad_diag = KEY_NONE, bad_sym = KEY_NONE;
   for (int r = ty; r < VT; r += 4) {
     const int64_t li = I * VT + r, lj = J * VT + tx;
     if (li < rows && lj < rows) {

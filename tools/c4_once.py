@@ -9,6 +9,7 @@ topk = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 fk = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 X = torch.from_numpy(np.ascontiguousarray(G.config(name), np.float32)).cuda()
 c = P.Context(timing=True, topk=topk, finish_k=fk)
+weights = G.CONFIGS[name]["mode"] == "weights"
 for _ in range(2):
-    M = c.solve_points(X); torch.cuda.synchronize()
+    M = c.solve_weights(X) if weights else c.solve_points(X); torch.cuda.synchronize()
 print(c.stats())

@@ -1,13 +1,4 @@
 cd $GRAFT_REPO_ROOT
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python tools/cfg_times.py C3 > gpurun_out/ncu_c3.log 2>&1; echo "ncu $?"
-python - <<'PY'
-import csv, collections
-rows=list(csv.reader(open('gpurun_out/launches_c3.csv')))
-hi=next(i for i,r in enumerate(rows) if 'Kernel Name' in r); hdr=rows[hi]; data=rows[hi+1:]
-ki=hdr.index('Kernel Name'); vi=hdr.index('Metric Value')
-data=data[2*len(data)//3:]
-agg=collections.OrderedDict()
-for r in data:
-    nm=r[ki].split('(')[0][:50]; a=agg.setdefault(nm,[0,0.0]); a[0]+=1; a[1]+=float(r[vi].replace(',',''))
-for k,(c,t) in sorted(agg.items(), key=lambda x:-x[1][1])[:12]: print(f"{k:50s} {c:4d} {t/1e3:9.1f} us")
-PY
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c3.csv python tools/c4_once.py C3 > gpurun_out/ncu_c3.log 2>&1; echo "ncu $?"
+python tools/launches.py gpurun_out/launches_c3.csv | head -8
+ncu --set full --clock-control none --import-source on -k regex:k_scan_weights_topk -s 1 -c 1 -o gpurun_out/full_wtopk -f python tools/c4_once.py C3 > gpurun_out/ncu_wtopk.log 2>&1; echo "ncu wtopk $?"
