@@ -117,28 +117,46 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
       m = m + 0.0f;  // -0 -> +0 (reading Q5)
       return ((u64)orderable(m) << 32) | (u64)j;
     };
-    u64 mine = KEY_NONE;
+    // one float compare per element (validated input: no NaN; -0 == +0 as in the key);
+    // strict '<' (widest: '>') in increasing j keeps the smallest j among equal weights,
+    // so (w, j) is the thread's minimum key
+    auto better = [&](float a, float b) -> bool { return SENSE > 0 ? a < b : a > b; };
+    float bw = SENSE > 0 ? INFINITY : -INFINITY;
+    int64_t bj = -1;
     if (vec) {
+      // four 16-byte loads in flight per thread, then the four in order of j
       const float4* W4 = reinterpret_cast<const float4*>(Wr);
-      for (int64_t q = threadIdx.x; q < (n >> 2); q += 256) {
-        const float4 w = __ldcg(W4 + q);
-        const float ws[4] = {w.x, w.y, w.z, w.w};
+      const int64_t n4 = n >> 2;
+      for (int64_t q0 = threadIdx.x; q0 < n4; q0 += 4 * 256) {
+        float4 w[4];
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const int64_t j = 4 * q + e;
-          if (j != i) {
-            const u64 kk = keyof(ws[e], j);
-            mine = kk < mine ? kk : mine;
+        for (int u = 0; u < 4; u++)
+          w[u] = q0 + u * 256 < n4 ? __ldcg(W4 + q0 + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int64_t q = q0 + u * 256;
+          if (q >= n4) break;
+          const float ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int64_t j = 4 * q + e;
+            if (better(ws[e], bw) && j != i) {
+              bw = ws[e];
+              bj = j;
+            }
           }
         }
       }
     } else {
-      for (int64_t j = threadIdx.x; j < n; j += 256)
-        if (j != i) {
-          const u64 kk = keyof(__ldcg(Wr + j), j);
-          mine = kk < mine ? kk : mine;
+      for (int64_t j = threadIdx.x; j < n; j += 256) {
+        const float w = __ldcg(Wr + j);
+        if (better(w, bw) && j != i) {
+          bw = w;
+          bj = j;
         }
+      }
     }
+    const u64 mine = bj >= 0 ? keyof(bw, bj) : KEY_NONE;
     tmin[threadIdx.x] = mine;
     if (threadIdx.x == 0) ncand = 0;
     __syncthreads();
@@ -172,22 +190,35 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
     }
     __syncthreads();
     const u64 tau = tau_s;
+    // tau's weight as a float of the row's sense (keys are orderable(+-w) << 32 | j)
+    const float tau_f = tau == KEY_NONE ? (SENSE > 0 ? INFINITY : -INFINITY)
+                                        : (SENSE > 0 ? from_orderable((uint32_t)(tau >> 32))
+                                                     : -from_orderable((uint32_t)(tau >> 32)));
     // pass 2: keys <= tau
     if (vec) {
       const float4* W4 = reinterpret_cast<const float4*>(Wr);
-      for (int64_t q = threadIdx.x; q < (n >> 2); q += 256) {
-        const float4 w = __ldcs(W4 + q);
-        const float ws[4] = {w.x, w.y, w.z, w.w};
+      const int64_t n4 = n >> 2;
+      for (int64_t q0 = threadIdx.x; q0 < n4; q0 += 4 * 256) {
+        float4 wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          wv[u] = q0 + u * 256 < n4 ? __ldcs(W4 + q0 + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+        const int64_t q = q0 + u * 256;
+        if (q >= n4) break;
+        const float ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const int64_t j = 4 * q + e;
-          if (j != i) {
+          if ((SENSE > 0 ? ws[e] <= tau_f : ws[e] >= tau_f) && j != i) {  // cheap float test first
             const u64 kk = keyof(ws[e], j);
             if (kk <= tau) {
               const int slot = atomicAdd(&ncand, 1);
               if (slot < CAP) cand[slot] = kk;
             }
           }
+        }
         }
       }
     } else {
