@@ -571,11 +571,16 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     c->stats.scan_launches += c->launches - l0;
     if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
     if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
-    if ((s = launch_hook(c, compbest, k, comp, ks.shift, link))) return s;
-    if ((s = launch_mutual(c, compbest, k, link, parent, mstkeys, counters))) return s;
-    if ((s = launch_jump(c, parent, k, flags))) return s;
-    if ((s = exclusive_scan_i32(c, flags, newid, k))) return s;
-    if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
+    s = launch_contract(c, compbest, k, comp, n, ks.shift, link, parent, mstkeys, counters, flags, newid);
+    if (s == APPD_ERR_UNSUPPORTED) {
+      if ((s = launch_hook(c, compbest, k, comp, ks.shift, link))) return s;
+      if ((s = launch_mutual(c, compbest, k, link, parent, mstkeys, counters))) return s;
+      if ((s = launch_jump(c, parent, k, flags))) return s;
+      if ((s = exclusive_scan_i32(c, flags, newid, k))) return s;
+      if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
+    } else if (s) {
+      return s;
+    }
     // the next round's cache lookup rides on this round's synchronisation (labels are final)
     if (use_tc && tc.topk && c->opt.world == 1) {
       if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;

@@ -9,9 +9,12 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace appd {
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------
 // weights mode: one CTA per row (grid-stride), float4 loads of W's row, the
@@ -715,6 +718,123 @@ appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vi
   if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
   APPD_CUDA(c, cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)count, 0, 32, c->stream));
   c->launches += 4;
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One Boruvka contraction in a single cooperative launch (grid-wide barriers between the
+// steps of k_hook, k_mutual, k_jump, the exclusive scan of the root flags and k_relabel):
+// the same operations in the same order, one launch instead of six.  newid[k] = roots.
+// ---------------------------------------------------------------------------
+constexpr int kContractThreads = 1024;
+__global__ void __launch_bounds__(kContractThreads) k_contract(const u64* __restrict__ compbest, int k,
+                                                             int* __restrict__ comp, int n, int shift,
+                                                             int* __restrict__ link, int* __restrict__ parent,
+                                                             u64* __restrict__ mstkeys, int* __restrict__ counters,
+                                                             int* __restrict__ flags, int* __restrict__ newid,
+                                                             int* __restrict__ blocksum) {
+  cg::grid_group grid = cg::this_grid();
+  const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  // hook: the component at the other end of each component's lightest edge
+  for (int c = tid; c < k; c += T) {
+    const u64 key = compbest[c];
+    if (key == KEY_NONE) {
+      link[c] = c;
+      continue;
+    }
+    int64_t u, v;
+    tri_decode(key & ((1ull << shift) - 1), &u, &v);
+    const int cu = comp[u], cv = comp[v];
+    link[c] = (cu == c) ? cv : cu;
+  }
+  grid.sync();
+  // mutual pairs: the smaller id is the root, the shared edge is recorded once
+  for (int c = tid; c < k; c += T) {
+    const int o = link[c];
+    if (o == c) {
+      parent[c] = c;
+      continue;
+    }
+    const bool mutual = link[o] == c;
+    parent[c] = (mutual && c < o) ? c : o;
+    if (!(mutual && c > o)) mstkeys[atomicAdd(counters, 1)] = compbest[c];
+  }
+  grid.sync();
+  // pointer jumping to the roots
+  for (int c = tid; c < k; c += T) {
+    int p = parent[c];
+    while (true) {
+      const int pp = parent[p];
+      if (pp == p) break;
+      p = pp;
+    }
+    parent[c] = p;
+    flags[c] = p == c ? 1 : 0;
+  }
+  grid.sync();
+  // exclusive scan of the flags: block b owns [b S, (b+1) S)
+  __shared__ int wsum[kContractThreads / 32];
+  __shared__ int carry_s;
+  const int S = (k + gridDim.x - 1) / gridDim.x;
+  const int lo = min(k, (int)blockIdx.x * S), hi = min(k, lo + S);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = lo; base < hi; base += kContractThreads) {
+    const int i = base + threadIdx.x;
+    const int f = i < hi ? flags[i] : 0;
+    int x = f;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int before = carry_s + (warp ? wsum[warp - 1] : 0) + x - f;
+    if (i < hi) newid[i] = before;  // block-local exclusive prefix
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s += wsum[kContractThreads / 32 - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
+  grid.sync();
+  int off = 0;
+  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
+  for (int i = lo + threadIdx.x; i < hi; i += kContractThreads) newid[i] += off;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) newid[k] = off + carry_s;
+  grid.sync();
+  // relabel the points
+  for (int i = tid; i < n; i += T) comp[i] = newid[parent[comp[i]]];
+}
+
+appd_status launch_contract(appd_ctx* c, const u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
+                            int* parent, u64* mstkeys, int* counters, int* flags, int* newid) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_contract, kContractThreads, 0) != cudaSuccess)
+      per_sm = 0;
+    cudaGetLastError();
+  }
+  if (per_sm < 1) return APPD_ERR_UNSUPPORTED;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (std::max(k, n) + kContractThreads - 1) /
+                                                                                kContractThreads));
+  int* blocksum = (int*)ws(c, S_TMP2, sizeof(int) * (grid + 1) + 64);
+  if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "contract workspace");
+  int kk = (int)k, nn = (int)n;
+  void* args[] = {&compbest, &kk, &comp, &nn, &shift, &link, &parent, &mstkeys, &counters, &flags, &newid, &blocksum};
+  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract, grid, kContractThreads, args, 0, c->stream));
+  c->launches++;
   return APPD_OK;
 }
 
