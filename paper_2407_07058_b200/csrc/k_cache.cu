@@ -835,7 +835,7 @@ __global__ void k_comp_ub(int n, const int* __restrict__ perm, const int* __rest
 // padded to ldx).  comp == nullptr: singletons (eligible = j != i).
 // ---------------------------------------------------------------------------
 constexpr int RE_R = 16, RE_COLS = 256;
-template <bool FULL>  // FULL: d % 16 == 0 (no coordinate guards in the inner loop)
+template <bool FULL>  // FULL: d % 64 == 0 (no coordinate guards in the inner loop)
 __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__ XT, int64_t ldx, int n, int d,
                                                       const int* __restrict__ rows, const unsigned* __restrict__ nrows,
                                                       const int* __restrict__ comp, u64* __restrict__ compbest) {
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
   const int ngroups = (nr + RE_R - 1) / RE_R;
   const int nblk = (n + RE_COLS - 1) / RE_COLS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int KB = 8;
+  constexpr int KB = 64;
   const int64_t total = (int64_t)ngroups * nblk;
   const int i0 = (int)(total * blockIdx.x / gridDim.x), i1 = (int)(total * (blockIdx.x + 1) / gridDim.x);
   u64 best[RE_R];
@@ -899,14 +899,13 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
     // XT is zero padded beyond n up to ldx (a multiple of 128 >= the column blocks' end):
     // no column guard for the loads, only for the keys
     const float* xcol = XT + j;
-    auto load_block = [&](int k0, float (&y)[KB]) {
+    // the R1 chain in order k = 0, 1, ...: all KB = 64 coordinates of the column loaded at
+    // once (one L2 latency per item and 64-coordinate chunk instead of one per 8)
+    for (int k0 = 0; k0 < d; k0 += KB) {
+      float y[KB];
       const float* src = xcol + (int64_t)k0 * ldx;
 #pragma unroll
       for (int kk = 0; kk < KB; kk++) y[kk] = (FULL || k0 + kk < d) ? __ldg(src + (int64_t)kk * ldx) : 0.0f;
-    };
-    // the R1 chain in order k = 0, 1, ...; two register buffers in turn (the next
-    // block's loads in flight while one is used)
-    auto step = [&](int k0, const float (&y)[KB]) {
 #pragma unroll
       for (int kk = 0; kk < KB; kk++) {
         if (!FULL && k0 + kk >= d) break;
@@ -918,15 +917,6 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
           acc2[2 * q + 1] = f2_r1_step(x4.y, yy, acc2[2 * q + 1]);
         }
       }
-    };
-    float ya[KB], yb[KB];
-    load_block(0, ya);
-    for (int k0 = 0; k0 < d; k0 += 2 * KB) {
-      if (FULL || k0 + KB < d) load_block(k0 + KB, yb);
-      step(k0, ya);
-      if (!FULL && k0 + KB >= d) break;
-      if (k0 + 2 * KB < d) load_block(k0 + 2 * KB, ya);
-      step(k0 + KB, yb);
     }
     float acc[RE_R];
 #pragma unroll
@@ -952,7 +942,7 @@ appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, 
   const int64_t items = (int64_t)((max_rows + RE_R - 1) / RE_R) * ((n + RE_COLS - 1) / RE_COLS);
   const int grid = (int)std::min<int64_t>(items, (int64_t)c->sm_count * 2);  // persistent: 2 CTAs per SM
   const size_t smem = (size_t)d * RE_R * 4;
-  if (d % 16 == 0) {
+  if (d % 64 == 0) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_rows_exact<true><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
   } else {
