@@ -183,7 +183,8 @@ def run_native(args):
     n = c["n"]
     points = c["mode"] == "points"
     stream = torch.cuda.current_stream()
-    ctx = P.Context(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id, timing=True)
+    ctx = P.Context(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id, timing=True,
+                    metric=args.metric)
     row0, rows = ctx.row_range(n)
     if points:
         Xd = torch.from_numpy(A).cuda()
@@ -330,6 +331,7 @@ def run_native(args):
             "warmup": args.warmup, "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "desc": c["desc"], "n": n, "d": c.get("d", 0), "mode": c["mode"],
+                       **({"metric": ["euclidean", "manhattan", "chebyshev"][args.metric]} if args.metric else {}),
                        "parallelism": f"rows{world}", "l2": "1 GiB write between timed steps (outside events)",
                        "timing": "per-step CUDA events on the solve stream, max over ranks"},
             "roofline": roofline,
@@ -418,6 +420,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--floyd", type=int, default=0, help="NEXT-2: time appd_floyd_weights at this n instead")
+    ap.add_argument("--metric", type=int, default=0, help="NEXT-3 points metric: 0 Euclidean, 1 Manhattan, 2 Chebyshev")
     args = ap.parse_args()
     if args.floyd:
         return run_floyd(args)

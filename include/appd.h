@@ -92,7 +92,11 @@ typedef struct {
   int32_t finish_k;              /* tensor-core engine: finish the MST on the contracted component graph
                                     once at most this many components remain (0 = auto (128), -1 = never;
                                     at most 128) */
-  int32_t reserved[5];
+  int32_t metric;                /* points mode (NEXT-3): 0 Euclidean R1 (default), 1 Manhattan (L1: fp32
+                                    sum of |x_k - y_k| in k order), 2 Chebyshev (L-inf: max |x_k - y_k|);
+                                    L1 / L-inf run the exact FP32 engine (the tensor-core filter is
+                                    Euclidean) and the MST on the distance itself */
+  int32_t reserved[4];
 } appd_options;
 
 typedef struct {

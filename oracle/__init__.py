@@ -57,6 +57,11 @@ def lib():
         L.oracle_dist_f64.argtypes = [P, P, I64]
         L.oracle_points_weights.restype = None
         L.oracle_points_weights.argtypes = [P, I64, I64, I64, I64, P]
+        L.oracle_points_weights_metric.restype = None
+        L.oracle_points_weights_metric.argtypes = [P, I64, I64, ctypes.c_int, I64, I64, P]
+        L.oracle_metric_weight.restype = ctypes.c_float
+        L.oracle_metric_weight.argtypes = [P, P, I64, ctypes.c_int]
+        L.oracle_appd_points_metric.argtypes = [P, I64, I64, ctypes.c_int, P, P]
         L.oracle_prim_weights.argtypes = [P, I64, ctypes.c_int, P, P, P]
         L.oracle_prim_points.argtypes = [P, I64, I64, P, P, P]
         L.oracle_appd_weights.argtypes = [P, I64, ctypes.c_int, P, P]
@@ -96,13 +101,17 @@ def appd_weights(W, sense: int = 1, with_stats: bool = False):
     return (M, st.as_dict()) if with_stats else M
 
 
-def appd_points(X, with_stats: bool = False):
-    """Algorithm 4 on the complete graph of R1 weights of the points X (n x d)."""
+def appd_points(X, with_stats: bool = False, metric: int = 0):
+    """Algorithm 4 on the complete graph of the points X (n x d): R1 weights (metric 0),
+    Manhattan (1) or Chebyshev (2) distances (NEXT-3)."""
     X = _f32(X)
     n, d = X.shape
     M = np.empty((n, n), dtype=np.float32)
     st = Stats()
-    _check(lib().oracle_appd_points(_ptr(X), n, d, _ptr(M), ctypes.byref(st)), "appd_points")
+    if metric == 0:
+        _check(lib().oracle_appd_points(_ptr(X), n, d, _ptr(M), ctypes.byref(st)), "appd_points")
+    else:
+        _check(lib().oracle_appd_points_metric(_ptr(X), n, d, metric, _ptr(M), ctypes.byref(st)), "appd_points")
     return (M, st.as_dict()) if with_stats else M
 
 
@@ -186,13 +195,16 @@ def dist_f64(xi, xj) -> float:
     return float(lib().oracle_dist_f64(_ptr(xi), _ptr(xj), xi.shape[0]))
 
 
-def points_weights(X, r0: int = 0, R: int | None = None):
-    """Row block [r0, r0+R) of the R1 weight matrix."""
+def points_weights(X, r0: int = 0, R: int | None = None, metric: int = 0):
+    """Row block [r0, r0+R) of the weight matrix (R1, or the metric of NEXT-3)."""
     X = _f32(X)
     n, d = X.shape
     R = n - r0 if R is None else R
     Wb = np.empty((R, n), dtype=np.float32)
-    lib().oracle_points_weights(_ptr(X), n, d, r0, R, _ptr(Wb))
+    if metric == 0:
+        lib().oracle_points_weights(_ptr(X), n, d, r0, R, _ptr(Wb))
+    else:
+        lib().oracle_points_weights_metric(_ptr(X), n, d, metric, r0, R, _ptr(Wb))
     return Wb
 
 

@@ -11,6 +11,7 @@
  *
  * What is here (each function cites the passage it follows):
  *   oracle_r1_dist2 / oracle_r1_weight  points -> weight, the pinned R1 formula
+ *   oracle_metric_weight (+ _metric API)  NEXT-3: Manhattan / Chebyshev weights
  *                                       (reading Q6: Euclidean, fixed
  *                                       order fmaf chain, fp32)
  *   oracle_dist_f64                     fp64 Euclidean distance (R1 checker)
@@ -83,6 +84,23 @@ float oracle_r1_weight(const float* xi, const float* xj, int64_t d) {
   return sqrtf(oracle_r1_dist2(xi, xj, d));
 }
 
+/* ---------------------------------------------------------------------------
+ * NEXT-3 ("other point metrics"): pluggable point metrics.
+ * metric 0: R1 above (Euclidean); 1: Manhattan, acc = +0; for k in order:
+ * acc = fl(acc + |fl(x_i[k] - x_j[k])|); 2: Chebyshev, acc = max over k of
+ * |fl(x_i[k] - x_j[k])|.  The weight is the distance itself (no square root).
+ * ------------------------------------------------------------------------- */
+float oracle_metric_weight(const float* xi, const float* xj, int64_t d, int metric) {
+  if (metric == 0) return oracle_r1_weight(xi, xj, d);
+  float acc = 0.0f;
+  for (int64_t k = 0; k < d; k++) {
+    float t = fabsf(xi[k] - xj[k]);
+    if (metric == 1) acc = acc + t;
+    else if (t > acc) acc = t;
+  }
+  return acc;
+}
+
 /* fp64 Euclidean distance, the checker R1 is held to (BASELINE north star: 1e-5 rel). */
 double oracle_dist_f64(const float* xi, const float* xj, int64_t d) {
   double s = 0.0;
@@ -110,11 +128,12 @@ typedef struct {
   const float* W;
   const float* X;
   int64_t n, d;
+  int metric; /* points: 0 R1, 1 Manhattan, 2 Chebyshev */
 } wsrc;
 
 static float wget(const wsrc* s, int64_t i, int64_t j) {
   if (s->W) return canon(s->W[i * s->n + j]);
-  return oracle_r1_weight(s->X + i * s->d, s->X + j * s->d, s->d);
+  return oracle_metric_weight(s->X + i * s->d, s->X + j * s->d, s->d, s->metric);
 }
 
 /* ---------------------------------------------------------------------------
@@ -159,13 +178,13 @@ static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
 
 int oracle_prim_weights(const float* W, int64_t n, int sense, int32_t* eu, int32_t* ev, float* ew) {
   if (!W || n < 1) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0};
+  wsrc s = {W, NULL, n, 0, 0};
   return prim(&s, sense, eu, ev, ew);
 }
 
 int oracle_prim_points(const float* X, int64_t n, int64_t d, int32_t* eu, int32_t* ev, float* ew) {
   if (!X || n < 1 || d < 1) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d};
+  wsrc s = {NULL, X, n, d, 0};
   return prim(&s, +1, eu, ev, ew);
 }
 
@@ -304,28 +323,43 @@ out:
 /* Algorithm 4 on a weight matrix.  sense +1 minimax, -1 widest. */
 int oracle_appd_weights(const float* W, int64_t n, int sense, float* M, oracle_stats* st) {
   if (!W || !M || n < 1 || (sense != 1 && sense != -1)) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0};
+  wsrc s = {W, NULL, n, 0, 0};
   return algo4(&s, sense, 0, n, M, st);
 }
 
 /* Algorithm 4 on points (complete graph of R1 weights). */
 int oracle_appd_points(const float* X, int64_t n, int64_t d, float* M, oracle_stats* st) {
   if (!X || !M || n < 1 || d < 1) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d};
+  wsrc s = {NULL, X, n, d, 0};
   return algo4(&s, +1, 0, n, M, st);
+}
+
+/* Algorithm 4 on points under a pluggable metric (NEXT-3). */
+int oracle_appd_points_metric(const float* X, int64_t n, int64_t d, int metric, float* M, oracle_stats* st) {
+  if (!X || !M || n < 1 || d < 1 || metric < 0 || metric > 2) return ORACLE_ERR_ARG;
+  wsrc s = {NULL, X, n, d, metric};
+  return algo4(&s, +1, 0, n, M, st);
+}
+
+/* Row block [r0, r0+R) of the metric weight matrix, row-major R x n. */
+void oracle_points_weights_metric(const float* X, int64_t n, int64_t d, int metric, int64_t r0, int64_t R,
+                                  float* Wblk) {
+  for (int64_t i = 0; i < R; i++)
+    for (int64_t j = 0; j < n; j++)
+      Wblk[i * n + j] = (r0 + i == j) ? 0.0f : oracle_metric_weight(X + (r0 + i) * d, X + j * d, d, metric);
 }
 
 /* R5: rows [r0, r0+R) only, M is R x n. */
 int oracle_appd_points_rows(const float* X, int64_t n, int64_t d, int64_t r0, int64_t R, float* M,
                             oracle_stats* st) {
   if (!X || !M || n < 1 || d < 1 || r0 < 0 || R < 1 || r0 + R > n) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d};
+  wsrc s = {NULL, X, n, d, 0};
   return algo4(&s, +1, r0, R, M, st);
 }
 
 int oracle_appd_weights_rows(const float* W, int64_t n, int64_t r0, int64_t R, float* M, oracle_stats* st) {
   if (!W || !M || n < 1 || r0 < 0 || R < 1 || r0 + R > n) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0};
+  wsrc s = {W, NULL, n, 0, 0};
   return algo4(&s, +1, r0, R, M, st);
 }
 
@@ -401,7 +435,7 @@ int oracle_mst_path(const float* W, int64_t n, float* M) {
   int rc = ORACLE_OK;
   if (!eu || !ev || !ew || !off || !adj_v || !adj_w || !stack || !from) { rc = ORACLE_ERR_NOMEM; goto out; }
   {
-    wsrc s = {W, NULL, n, 0};
+    wsrc s = {W, NULL, n, 0, 0};
     rc = prim(&s, +1, eu, ev, ew);
     if (rc) goto out;
   }

@@ -47,7 +47,8 @@ class appd_options(ctypes.Structure):
         ("points_engine", ctypes.c_int32),
         ("topk", ctypes.c_int32),
         ("finish_k", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 5),
+        ("metric", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 4),
     ]
 
 
@@ -195,7 +196,7 @@ class Context:
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  variant: int = VARIANT_AUTO, validate: bool = True, sense: int = 1, timing: bool = False,
                  dendrogram: int = 0, points_engine: int = 0, topk: int = 0,
-                 finish_k: int = 0):
+                 finish_k: int = 0, metric: int = 0):
         L = load()
         o = appd_options()
         L.appd_options_init(ctypes.byref(o))
@@ -214,6 +215,7 @@ class Context:
         o.points_engine = points_engine
         o.topk = topk
         o.finish_k = finish_k
+        o.metric = metric
         h = ctypes.c_void_p()
         s = L.appd_create(ctypes.byref(h), ctypes.byref(o))
         if s != APPD_OK:

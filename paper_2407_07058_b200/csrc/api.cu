@@ -137,6 +137,7 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return APPD_ERR_INVALID_ARGUMENT;
   if (o.sense != 1 && o.sense != -1) return APPD_ERR_INVALID_ARGUMENT;
   if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.metric < 0 || o.metric > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.world > 1 && !o.nccl_unique_id) return APPD_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -321,7 +322,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // ---- a1: validation ----
   // Points mode with the tensor-core engine: the verdict is copied asynchronously and
   // read after the engine's preparation, which synchronises anyway (deferred check).
-  const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 && n >= 2;
+  if (points && c->opt.metric != 0 && c->opt.points_engine == 2)
+    return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine computes Euclidean distances only (metric = %d)",
+                c->opt.metric);
+  const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 &&
+                                c->opt.metric == 0 && n >= 2;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
   if (c->opt.validate) {
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
@@ -373,6 +378,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   ks.points = points;
   ks.shift = points ? 33 : 32;
   ks.sense = sense;
+  ks.metric = points ? c->opt.metric : 0;
   int* comp = (int*)ws(c, S_COMP, sizeof(int) * n);
   u64* compbest = (u64*)ws(c, S_COMPBEST, sizeof(u64) * n);
   int* link = (int*)ws(c, S_LINK, sizeof(int) * n);
@@ -391,7 +397,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // the dimension does not fit the shared-memory ring
   TcState tc;
   bool use_tc = false;
-  if (points && c->opt.points_engine != 1 && n >= 2) {
+  if (points && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);
     if (defer_validation) {  // tcf_prepare synchronised the stream: the verdict is in pinned memory
       APPD_CUDA(c, cudaStreamSynchronize(c->stream));

@@ -68,6 +68,7 @@ struct KeySpec {
   int shift;     // 32 (weights) or 33 (points)
   bool points;   // key weight is bits(d^2)
   int sense;     // +1 minimax, -1 widest (weights only)
+  int metric = 0;  // points: 0 Euclidean (key = bits(d^2), weight sqrtf), 1 L1, 2 L-inf (key = bits(d))
 };
 
 // ---------------------------------------------------------------------------

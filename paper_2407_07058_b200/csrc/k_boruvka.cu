@@ -410,7 +410,17 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <bool ROUND0>
+// METRIC (NEXT-3): 0 the pinned R1 chain (squared Euclidean), 1 Manhattan (acc + |t| in k
+// order), 2 Chebyshev (max |t|); the zero-padded coordinates add 0 / leave the max.
+template <int METRIC>
+__device__ __forceinline__ float metric_step(float a, float b, float acc) {
+  const float t = __fsub_rn(a, b);
+  if (METRIC == 0) return __fmaf_rn(t, t, acc);
+  if (METRIC == 1) return __fadd_rn(acc, fabsf(t));
+  return fmaxf(acc, fabsf(t));
+}
+
+template <bool ROUND0, int METRIC = 0>
 __global__ void __launch_bounds__(256, 2)
     k_scan_points(const float* __restrict__ XT, int64_t n, int64_t npad, int dpad, int64_t row0, int64_t rows,
                   int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest) {
@@ -492,10 +502,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int a = 0; a < 8; a++)
 #pragma unroll
-        for (int b = 0; b < 8; b++) {
-          float t = __fsub_rn(av[a], bv[b]);
-          acc[a][b] = __fmaf_rn(t, t, acc[a][b]);
-        }
+        for (int b = 0; b < 8; b++) acc[a][b] = metric_step<METRIC>(av[a], bv[b], acc[a][b]);
     }
     if (kc == nk - 1) {
       // epilogue of this column tile: component-filtered running argmin per row.
@@ -538,8 +545,12 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
   const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_scan_points<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_scan_points<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
@@ -552,12 +563,19 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
   int64_t per = (col_tiles + splits - 1) / splits;
   splits = (col_tiles + per - 1) / per;
   dim3 grid((unsigned)row_blocks, (unsigned)splits);
-  if (comp == nullptr)
-    k_scan_points<true><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp,
-                                                       compbest);
-  else
-    k_scan_points<false><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp,
-                                                        compbest);
+#define APPD_SCAN_POINTS(R0, MT) \
+  k_scan_points<R0, MT><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp, compbest)
+  const int mt = c->opt.metric;
+  if (comp == nullptr) {
+    if (mt == 1) APPD_SCAN_POINTS(true, 1);
+    else if (mt == 2) APPD_SCAN_POINTS(true, 2);
+    else APPD_SCAN_POINTS(true, 0);
+  } else {
+    if (mt == 1) APPD_SCAN_POINTS(false, 1);
+    else if (mt == 2) APPD_SCAN_POINTS(false, 2);
+    else APPD_SCAN_POINTS(false, 0);
+  }
+#undef APPD_SCAN_POINTS
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

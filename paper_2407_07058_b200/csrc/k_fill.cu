@@ -259,16 +259,18 @@ appd_status launch_set_diag_zero_single(appd_ctx* c, float* M) {
 
 // K11 test hook: R1 weights of a row block, the same pinned chain as the MST scan
 __global__ void k_points_weights(const float* __restrict__ X, int64_t n, int64_t d, int64_t row0, int64_t rows,
-                                 float* __restrict__ Wb) {
+                                 float* __restrict__ Wb, int metric) {
   int64_t total = rows * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = e / n, j = e % n, i = row0 + r;
     float acc = 0.0f;
     for (int64_t k = 0; k < d; k++) {
       float t = __fsub_rn(X[i * d + k], X[j * d + k]);
-      acc = __fmaf_rn(t, t, acc);
+      if (metric == 1) acc = __fadd_rn(acc, fabsf(t));      // Manhattan (NEXT-3)
+      else if (metric == 2) acc = fmaxf(acc, fabsf(t));     // Chebyshev
+      else acc = __fmaf_rn(t, t, acc);                      // R1
     }
-    Wb[e] = (i == j) ? 0.0f : __fsqrt_rn(acc);
+    Wb[e] = (i == j) ? 0.0f : (metric == 0 ? __fsqrt_rn(acc) : acc);
   }
 }
 appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,
@@ -277,7 +279,7 @@ appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_
   int grid = (int)((total + 255) / 256);
   if (grid > c->sm_count * 16) grid = c->sm_count * 16;
   if (grid < 1) grid = 1;
-  k_points_weights<<<grid, 256, 0, c->stream>>>(X, n, d, row0, rows, Wb);
+  k_points_weights<<<grid, 256, 0, c->stream>>>(X, n, d, row0, rows, Wb, c->opt.metric);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -287,7 +289,7 @@ appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_
 namespace appd {
 
 // sorted MST edge keys -> endpoints and weights (the dendrogram's input)
-__global__ void k_decode_edges(const u64* __restrict__ keys, int64_t m, int shift, int points, int sense,
+__global__ void k_decode_edges(const u64* __restrict__ keys, int64_t m, int shift, int points, int sense, int metric,
                                int32_t* __restrict__ eu, int32_t* __restrict__ ev, float* __restrict__ ew) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const u64 key = keys[e];
@@ -296,7 +298,8 @@ __global__ void k_decode_edges(const u64* __restrict__ keys, int64_t m, int shif
     const uint32_t wk = (uint32_t)(key >> shift);
     float w;
     if (points) {
-      w = __fsqrt_rn(__uint_as_float(wk));  // R1: the weight is sqrtf of the squared distance
+      // R1: the weight is sqrtf of the squared distance; L1 / L-inf keys hold the distance
+      w = metric == 0 ? __fsqrt_rn(__uint_as_float(wk)) : __uint_as_float(wk);
     } else {
       const float mm = from_orderable(wk);
       w = (sense > 0 ? mm : -mm) + 0.0f;
@@ -312,7 +315,7 @@ appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const K
   if (m <= 0) return APPD_OK;
   int grid = (int)((m + 255) / 256);
   if (grid > c->sm_count * 8) grid = c->sm_count * 8;
-  k_decode_edges<<<grid, 256, 0, c->stream>>>(keys, m, ks.shift, ks.points ? 1 : 0, ks.sense, eu, ev, ew);
+  k_decode_edges<<<grid, 256, 0, c->stream>>>(keys, m, ks.shift, ks.points ? 1 : 0, ks.sense, ks.metric, eu, ev, ew);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

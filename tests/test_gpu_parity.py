@@ -282,6 +282,25 @@ def test_points_stream_large_vs_device(ctx):
     assert st["fill_bytes"] == n * n * 4
 
 
+@pytest.mark.parametrize("metric", [1, 2])
+def test_points_metrics(P, metric):
+    """NEXT-3: Manhattan / Chebyshev point metrics (exact FP32 engine) against the oracle,
+    bit for bit, and the weights hook against the oracle's metric weights."""
+    with P.Context(metric=metric) as c:
+        for t, (kind, n, d) in enumerate([("blobs", 1, 3), ("blobs", 2, 2), ("uniform", 300, 5), ("clumps", 1500, 8),
+                                          ("grid", 1000, 3), ("dups", 2100, 16), ("blobs", 700, 70)]):
+            X = G.random_points(n, d, 970 + t, kind)
+            assert_bit_equal(gpu_points(c, X), oracle.appd_points(X, metric=metric), f"metric {metric} {kind} n={n}")
+        X = G.random_points(600, 9, 990, "uniform")
+        Wg = c.points_weights(torch.from_numpy(X).cuda(), 0, 200).cpu().numpy()
+        assert_bit_equal(Wg, oracle.points_weights(X, 0, 200, metric=metric), f"metric {metric} weights")
+        assert c.stats()["points_engine"] == 1
+    with P.Context(metric=metric, points_engine=2) as c2:
+        with pytest.raises(P.AppdError) as e:
+            gpu_points(c2, G.random_points(100, 4, 1, "blobs"))
+        assert e.value.name == "APPD_ERR_UNSUPPORTED"
+
+
 def test_points_list_overflow_is_exact(P, monkeypatch):
     """A candidate list far too small for the input: rows whose entries are lost are
     poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the

@@ -405,3 +405,52 @@ def test_r1_symmetry_zero_and_fp64_bound():
 def test_dist_f64_exact_small():
     assert oracle.dist_f64(np.array([0, 0], np.float32), np.array([3, 4], np.float32)) == 5.0
     assert oracle.r1_weight(np.array([1, 2, 2], np.float32), np.zeros(3, np.float32)) == 3.0
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: pluggable point metrics (Manhattan, Chebyshev)
+# --------------------------------------------------------------------------
+def _int_points(n, d, seed, lo=-50, hi=50):
+    rs = np.random.default_rng(seed)
+    return rs.integers(lo, hi + 1, size=(n, d)).astype(np.float32)
+
+
+@pytest.mark.parametrize("metric", [1, 2])
+def test_metric_points_equal_weights_path_on_integer_points(metric):
+    """Integer coordinates make every fp32 operation of L1 / L-inf exact, so the weight
+    matrix is fixed by integer arithmetic (numpy int64) independently of the oracle's
+    metric code; the points path must then equal Algorithm 4 on that W, and the
+    minimax Floyd-Warshall variant on it."""
+    for t, (n, d) in enumerate([(2, 1), (3, 2), (7, 3), (40, 2), (200, 5), (333, 8)]):
+        X = _int_points(n, d, 60 + t)
+        D = np.abs(X[:, None, :].astype(np.int64) - X[None, :, :].astype(np.int64))
+        W = (D.sum(-1) if metric == 1 else D.max(-1)).astype(np.float32)
+        np.fill_diagonal(W, 0.0)
+        assert_bit_equal(oracle.points_weights(X, metric=metric), W)
+        M = oracle.appd_points(X, metric=metric)
+        assert_bit_equal(M, oracle.appd_weights(W))
+        if n <= 64:
+            assert_bit_equal(M, oracle.floyd(W))
+        if n <= 7:
+            assert_bit_equal(M, oracle.brute(W))
+
+
+def test_metric_worked_example():
+    """(0,0), (2,2), (4,0): Manhattan distances 4, 4, 4; Chebyshev 2, 4, 2; Euclidean
+    sqrt 8, 4, sqrt 8 -> every off-diagonal APPD entry is 4, 2 and sqrtf(8)."""
+    X = np.array([[0, 0], [2, 2], [4, 0]], np.float32)
+    off = ~np.eye(3, dtype=bool)
+    for metric, want in [(1, 4.0), (2, 2.0), (0, float(np.sqrt(np.float32(8.0))))]:
+        M = oracle.appd_points(X, metric=metric)
+        assert (M[off] == np.float32(want)).all(), (metric, M)
+        assert (bits(np.diag(M)) == 0).all()
+
+
+def test_metrics_coincide_in_one_dimension():
+    """d = 1: |x - y| for all three metrics (sqrtf of a correctly rounded square of t is
+    |t| in round-to-nearest without overflow or underflow)."""
+    rs = np.random.default_rng(5)
+    X = (rs.standard_normal((150, 1)) * 10).astype(np.float32)
+    M0 = oracle.appd_points(X)
+    for metric in (1, 2):
+        assert_bit_equal(oracle.appd_points(X, metric=metric), M0)
