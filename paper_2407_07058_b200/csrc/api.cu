@@ -517,6 +517,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       }
     }
     static const bool dbg = getenv("APPD_DEBUG_ROUNDS") != nullptr;
+    static const bool tc_verify = getenv("APPD_TC_VERIFY") != nullptr;
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
     if (!(use_tc && tc.lookup_pending) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
@@ -529,7 +530,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         if ((s = ensure_xt())) return s;
         s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
         c->stats.exact_rounds++;
-      } else if (getenv("APPD_TC_VERIFY")) {  // debug: compare with the exact scan, report to stderr
+      } else if (tc_verify) {  // debug: compare with the exact scan, report to stderr
         if ((s = ensure_xt())) return s;
         u64* cb2 = (u64*)ws(c, S_TMP, sizeof(u64) * k);
         if ((s = launch_fill_u64(c, cb2, k, KEY_NONE))) return s;
@@ -577,7 +578,33 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     c->stats.scan_launches += c->launches - l0;
     if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
     if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
-    s = launch_contract(c, compbest, k, comp, n, ks.shift, link, parent, mstkeys, counters, flags, newid);
+    // the next round's cache lookup rides on this round's synchronisation (labels are
+    // final): one rank, fused into the cooperative contraction when it can run
+    LookupArgs la;
+    bool fused_lookup = false;
+    if (use_tc && tc.topk && c->opt.world == 1) {
+      la.r0 = (int)tc.cache_r0;
+      la.r1 = (int)tc.cache_r1;
+      la.K = tc.topk;
+      la.ckey = tc.ckey;
+      la.cj = tc.cj;
+      la.ccnt = tc.ccnt;
+      la.need = tc.need;
+      la.count = tc.counters + 3;
+      la.list = tc.rows_list;
+    } else if (wtopk && c->opt.world == 1) {
+      la.r0 = (int)row0;
+      la.r1 = (int)(row0 + rows);
+      la.K = wtopk;
+      la.ckey = w_ckey;
+      la.cj = w_cj;
+      la.ccnt = w_ccnt;
+      la.need = w_need;
+      la.count = w_count;
+      la.list = w_list;
+    }
+    s = launch_contract(c, compbest, k, comp, n, ks.shift, link, parent, mstkeys, counters, flags, newid,
+                        la.ckey ? &la : nullptr);
     if (s == APPD_ERR_UNSUPPORTED) {
       if ((s = launch_hook(c, compbest, k, comp, ks.shift, link))) return s;
       if ((s = launch_mutual(c, compbest, k, link, parent, mstkeys, counters))) return s;
@@ -586,15 +613,23 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       if ((s = launch_relabel(c, comp, n, parent, newid))) return s;
     } else if (s) {
       return s;
+    } else {
+      fused_lookup = la.ckey != nullptr;
     }
-    // the next round's cache lookup rides on this round's synchronisation (labels are final)
-    if (use_tc && tc.topk && c->opt.world == 1) {
-      if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
-      if ((s = tcf_lookup_async(c, &tc, comp, compbest))) return s;
-    }
-    if (wtopk && c->opt.world == 1) {
-      if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
-      if ((s = w_lookup_async())) return s;
+    if (fused_lookup) {
+      APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, la.count, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                   c->stream));
+      if (use_tc && tc.topk) tc.lookup_pending = true;
+      else w_pending = true;
+    } else {
+      if (use_tc && tc.topk && c->opt.world == 1) {
+        if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
+        if ((s = tcf_lookup_async(c, &tc, comp, compbest))) return s;
+      }
+      if (wtopk && c->opt.world == 1) {
+        if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
+        if ((s = w_lookup_async())) return s;
+      }
     }
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));

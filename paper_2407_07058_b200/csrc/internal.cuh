@@ -260,10 +260,24 @@ appd_status launch_mutual(appd_ctx* c, const u64* compbest, int64_t k, const int
                           u64* mstkeys, int* counters /*[0]=mst count*/);
 appd_status launch_jump(appd_ctx* c, int* parent, int64_t k, int* flags);
 appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent, const int* newid);
-// hook + mutual + jump + scan + relabel in one cooperative launch (APPD_ERR_UNSUPPORTED if
-// the device cannot co-schedule it: the caller then runs the separate kernels)
-appd_status launch_contract(appd_ctx* c, const u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
-                            int* parent, u64* mstkeys, int* counters, int* flags, int* newid);
+// the next round's candidate-cache lookup, queued in the same cooperative launch as the
+// contraction (ckey == nullptr: none): compbest[0..n) = KEY_NONE, *count = 0, then
+// k_cache_lookup and k_rescan_select over rows [r0, r1)
+struct LookupArgs {
+  int r0 = 0, r1 = 0, K = 0;
+  const u64* ckey = nullptr;
+  const int* cj = nullptr;
+  const int* ccnt = nullptr;
+  int* need = nullptr;
+  unsigned* count = nullptr;
+  int* list = nullptr;
+};
+// hook + mutual + jump + scan + relabel (+ the lookup) in one cooperative launch
+// (APPD_ERR_UNSUPPORTED if the device cannot co-schedule it: the caller then runs the
+// separate kernels)
+appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
+                            int* parent, u64* mstkeys, int* counters, int* flags, int* newid,
+                            const LookupArgs* look = nullptr);
 
 // fill
 appd_status launch_positions(appd_ctx* c, const int* pi, int64_t n, int* pos);

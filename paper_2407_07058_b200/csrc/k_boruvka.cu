@@ -745,12 +745,12 @@ appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vi
 // the same operations in the same order, one launch instead of six.  newid[k] = roots.
 // ---------------------------------------------------------------------------
 constexpr int kContractThreads = 1024;
-__global__ void __launch_bounds__(kContractThreads) k_contract(const u64* __restrict__ compbest, int k,
+__global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__ compbest, int k,
                                                              int* __restrict__ comp, int n, int shift,
                                                              int* __restrict__ link, int* __restrict__ parent,
                                                              u64* __restrict__ mstkeys, int* __restrict__ counters,
                                                              int* __restrict__ flags, int* __restrict__ newid,
-                                                             int* __restrict__ blocksum) {
+                                                             int* __restrict__ blocksum, LookupArgs la) {
   cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   // hook: the component at the other end of each component's lightest edge
@@ -834,10 +834,43 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(const u64* __rest
   grid.sync();
   // relabel the points
   for (int i = tid; i < n; i += T) comp[i] = newid[parent[comp[i]]];
+  if (!la.ckey) return;
+  // the next round's cache lookup (k_cache_lookup, k_rescan_select) on the final labels
+  grid.sync();
+  for (int i = tid; i < n; i += T) compbest[i] = KEY_NONE;
+  if (tid == 0) *la.count = 0u;
+  grid.sync();
+  for (int i = la.r0 + tid; i < la.r1; i += T) {
+    const int c = la.ccnt[i];
+    const int ci = comp[i];
+    int flag = 1;
+    if (c > 0) {
+      for (int t = 0; t < c; t++) {
+        const int j = la.cj[(int64_t)i * la.K + t];
+        if (comp[j] != ci) {
+          atomicMin(compbest + ci, la.ckey[(int64_t)i * la.K + t]);
+          flag = 0;
+          break;
+        }
+      }
+      if (flag && c == n - 1) flag = 0;  // every other point cached, none eligible
+    }
+    la.need[i] = flag;
+  }
+  grid.sync();
+  for (int i = la.r0 + tid; i < la.r1; i += T) {
+    if (!la.need[i]) continue;
+    const int c = la.ccnt[i];
+    if (c > 0 && la.ckey[(int64_t)i * la.K + (c - 1)] >= compbest[comp[i]]) {
+      la.need[i] = 0;
+      continue;
+    }
+    la.list[atomicAdd(la.count, 1u)] = i;
+  }
 }
 
-appd_status launch_contract(appd_ctx* c, const u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
-                            int* parent, u64* mstkeys, int* counters, int* flags, int* newid) {
+appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
+                            int* parent, u64* mstkeys, int* counters, int* flags, int* newid, const LookupArgs* look) {
   static int per_sm = -1;
   if (per_sm < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_contract, kContractThreads, 0) != cudaSuccess)
@@ -850,7 +883,9 @@ appd_status launch_contract(appd_ctx* c, const u64* compbest, int64_t k, int* co
   int* blocksum = (int*)ws(c, S_TMP2, sizeof(int) * (grid + 1) + 64);
   if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "contract workspace");
   int kk = (int)k, nn = (int)n;
-  void* args[] = {&compbest, &kk, &comp, &nn, &shift, &link, &parent, &mstkeys, &counters, &flags, &newid, &blocksum};
+  LookupArgs la = look ? *look : LookupArgs{};
+  void* args[] = {&compbest, &kk, &comp, &nn, &shift, &link, &parent, &mstkeys, &counters, &flags, &newid, &blocksum,
+                  &la};
   APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract, grid, kContractThreads, args, 0, c->stream));
   c->launches++;
   return APPD_OK;

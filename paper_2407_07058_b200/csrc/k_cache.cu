@@ -352,7 +352,11 @@ appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int
   if (ngq > 128) return fail(c, APPD_ERR_UNSUPPORTED, "top-K scan: %d chunks per row", nch);
 #define APPD_TOPK_SCAN(KK)                                                                                     \
   do {                                                                                                         \
-    cudaFuncSetAttribute(k_topk_scan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);            \
+    static bool attr_##KK = false;                                                                             \
+    if (!attr_##KK) {                                                                                          \
+      cudaFuncSetAttribute(k_topk_scan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);          \
+      attr_##KK = true;                                                                                        \
+    }                                                                                                          \
     k_topk_scan<KK><<<grid, 32 * TK_PARTS, smem, c->stream>>>(TM32, nch, p_begin, p_end, nrm, len, maxlen, err, \
                                                               maxerr, em, UBK, list, count, cap, cand_cnt, ngq); \
   } while (0)
@@ -970,13 +974,14 @@ appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsign
     APPD_LAUNCHED(c);
   }
   const int grid = c->sm_count * (mode == 0 ? 5 : 4);  // 5 x 40 KB of shared memory fit an SM
-  if (mode == 0) {
-    cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_list_exact<0><<<grid, 256, smem, c->stream>>>(L);
-  } else {
-    cudaFuncSetAttribute(k_list_exact<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_list_exact<1><<<grid, 256, smem, c->stream>>>(L);
+  static size_t attr_smem[2] = {0, 0};  // set once per size (attribute calls cost host time)
+  if (attr_smem[mode ? 1 : 0] < smem) {
+    if (mode == 0) cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else cudaFuncSetAttribute(k_list_exact<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_smem[mode ? 1 : 0] = smem;
   }
+  if (mode == 0) k_list_exact<0><<<grid, 256, smem, c->stream>>>(L);
+  else k_list_exact<1><<<grid, 256, smem, c->stream>>>(L);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
