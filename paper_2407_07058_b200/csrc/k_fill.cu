@@ -17,9 +17,12 @@
 // (ST[k][i] = max h[i .. i+2^k-1]).  Widest sense: min instead of max.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
 
 namespace appd {
+namespace cg = cooperative_groups;
 
 __global__ void k_positions(const int* __restrict__ pi, int64_t n, int* __restrict__ pos) {
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
@@ -85,6 +88,21 @@ __global__ void __launch_bounds__(256) k_st_levels_lo(float* ST, int64_t m, int6
   }
 }
 
+// levels k0 .. levels-1 in one cooperative launch (a grid-wide barrier between levels)
+template <bool WIDEST>
+__global__ void __launch_bounds__(1024) k_st_levels_hi(float* ST, int64_t m, int64_t stride, int k0, int levels) {
+  cg::grid_group grid = cg::this_grid();
+  for (int k = k0; k < levels; k++) {
+    const int64_t half = 1ll << (k - 1);
+    const float* prev = ST + (int64_t)(k - 1) * stride;
+    float* cur = ST + (int64_t)k * stride;
+    const int64_t cnt = m - (1ll << k) + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+      cur[i] = WIDEST ? fminf(prev[i], prev[i + half]) : fmaxf(prev[i], prev[i + half]);
+    grid.sync();
+  }
+}
+
 appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, int64_t stride, int widest) {
   const int kl = std::min(ST_LO, levels - 1);
   if (kl >= 1) {
@@ -92,6 +110,20 @@ appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, i
     if (widest) k_st_levels_lo<true><<<grid, 256, 0, c->stream>>>(ST, m, stride, kl);
     else k_st_levels_lo<false><<<grid, 256, 0, c->stream>>>(ST, m, stride, kl);
     APPD_LAUNCHED(c);
+  }
+  if (kl + 1 < levels) {  // the remaining levels: one cooperative launch
+    int k0 = kl + 1, lv = levels;
+    int64_t mm = m, st = stride;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (m + 1023) / 1024));
+    void* args[] = {&ST, &mm, &st, &k0, &lv};
+    const cudaError_t e = cudaLaunchCooperativeKernel(widest ? (const void*)k_st_levels_hi<true>
+                                                              : (const void*)k_st_levels_hi<false>,
+                                                       grid, 1024, args, 0, c->stream);
+    if (e == cudaSuccess) {
+      c->launches++;
+      return APPD_OK;
+    }
+    cudaGetLastError();  // not co-schedulable: one launch per level
   }
   for (int k = kl + 1; k < levels; k++) {
     int64_t cnt = m - (1ll << k) + 1;
