@@ -880,7 +880,7 @@ appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, in
   if (per_sm < 1) return APPD_ERR_UNSUPPORTED;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (std::max(k, n) + kContractThreads - 1) /
                                                                                 kContractThreads));
-  int* blocksum = (int*)ws(c, S_TMP2, sizeof(int) * (grid + 1) + 64);
+  int* blocksum = (int*)ws(c, S_SCAN, sizeof(int) * (grid + 1) + 64);
   if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "contract workspace");
   int kk = (int)k, nn = (int)n;
   LookupArgs la = look ? *look : LookupArgs{};

@@ -223,6 +223,202 @@ __global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused cooperative versions of the two tours (one launch each instead of 6-8):
+//   k_tour1: Euler successors of the MST (k_euler_succ), list ranking, orientation
+//            (k_orient + the root fix-ups), binary lifting (k_lift0 + k_lift_coop);
+//   k_tour2: record-tree index and successors (k_rt_index, k_rt_succ), list ranking,
+//            down flags, their exclusive scan and the outputs (k_emit).
+// The same operations in the same order, separated by grid-wide barriers.
+// ---------------------------------------------------------------------------
+template <int E>
+__device__ __forceinline__ void pj_steps(cg::grid_group& grid, int (&nx)[E], int (&rk)[E], int2* A, int2* B, int L,
+                                         int steps, int tid, int T) {
+  for (int s = 0; s < steps; s++) {
+    const int2* in = (s & 1) ? B : A;
+    int2* out = (s & 1) ? A : B;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int a = tid + e * T;
+      if (a >= L) continue;
+      if (nx[e] >= 0) {
+        const int2 q = in[nx[e]];
+        rk[e] += q.y;
+        nx[e] = q.x;
+      }
+      out[a] = make_int2(nx[e], rk[e]);
+    }
+    grid.sync();
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
+                                                int n, const int* __restrict__ sarc, const int* __restrict__ start,
+                                                const int* __restrict__ end, const int* __restrict__ posarc, int root,
+                                                int2* A, int2* B, int* rkout, int* parent, int* val, int* child_of,
+                                                int2* jm, int levels, int steps) {
+  cg::grid_group grid = cg::this_grid();
+  const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = 2 * m;
+  int nx[E], rk[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {  // Euler successors (k_euler_succ)
+    const int a = tid + e * T;
+    nx[e] = -1;
+    rk[e] = 0;
+    if (a < L) {
+      const int ed = a >> 1;
+      const int y = (a & 1) ? eu[ed] : ev[ed];
+      int i = posarc[a ^ 1] + 1;
+      if (i == end[y]) i = start[y];
+      nx[e] = (y == root && i == start[y]) ? -1 : sarc[i];
+      rk[e] = nx[e] < 0 ? 0 : 1;
+      A[a] = make_int2(nx[e], rk[e]);
+    }
+  }
+  if (tid == 0) {
+    val[root] = 0x7F7F7F7F;  // +inf: the root's parent edge
+    parent[root] = root;
+  }
+  grid.sync();
+  pj_steps<E>(grid, nx, rk, A, B, L, steps, tid, T);
+#pragma unroll
+  for (int e = 0; e < E; e++)
+    if (tid + e * T < L) rkout[tid + e * T] = rk[e];
+  grid.sync();
+  for (int ed = tid; ed < m; ed += T) {  // orientation (k_orient): the earlier arc points down
+    const bool down0 = rkout[2 * ed] > rkout[2 * ed + 1];
+    const int ch = down0 ? ev[ed] : eu[ed], p = down0 ? eu[ed] : ev[ed];
+    parent[ch] = p;
+    val[ch] = ed;
+    child_of[ed] = ch;
+  }
+  grid.sync();
+  int2 cur[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {  // lifting level 0 (k_lift0)
+    const int x = tid + e * T;
+    cur[e] = make_int2(0, 0);
+    if (x < n) {
+      const int p = parent[x];
+      cur[e] = make_int2(p, val[p]);
+      jm[x] = cur[e];
+    }
+  }
+  grid.sync();
+  for (int j = 1; j < levels; j++) {  // k_lift_coop
+    const int2* in = jm + (size_t)(j - 1) * n;
+    int2* out = jm + (size_t)j * n;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      const int x = tid + e * T;
+      if (x >= n) continue;
+      const int2 q = in[cur[e].x];
+      cur[e] = make_int2(q.x, max(cur[e].y, q.y));
+      out[x] = cur[e];
+    }
+    grid.sync();
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __restrict__ S, int m, int n, int sh,
+                                                const int* __restrict__ child_of, int* first, int* sidx, int root,
+                                                int2* A, int2* B, int* rkout, int* flag, int* downs, int* blocksum,
+                                                const float* __restrict__ ew, int32_t* __restrict__ pi,
+                                                float* __restrict__ h, int steps) {
+  cg::grid_group grid = cg::this_grid();
+  const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = 2 * m;
+  const unsigned long long lo = (1ull << sh) - 1;
+  for (int x = tid; x < n; x += T) first[x] = -1;
+  for (int q = tid; q <= L; q += T) flag[q] = 0;
+  grid.sync();
+  for (int i = tid; i < m; i += T) {  // k_rt_index
+    const int rp = (int)(S[i] >> sh);
+    const int v = child_of[(int)(S[i] & lo)];
+    sidx[v] = i;
+    if (i == 0 || (int)(S[i - 1] >> sh) != rp) first[rp] = i;
+  }
+  grid.sync();
+  for (int i = tid; i < m; i += T) {  // k_rt_succ
+    const int rp = (int)(S[i] >> sh);
+    const int v = child_of[(int)(S[i] & lo)];
+    const int fc = first[v];
+    const int sd = fc >= 0 ? 2 * fc : 2 * i + 1;
+    int su;
+    if (i + 1 < m && (int)(S[i + 1] >> sh) == rp) su = 2 * (i + 1);
+    else su = rp == root ? -1 : 2 * sidx[rp] + 1;
+    A[2 * i] = make_int2(sd, 1);
+    A[2 * i + 1] = make_int2(su, su < 0 ? 0 : 1);
+  }
+  grid.sync();
+  int nx[E], rk[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int a = tid + e * T;
+    const int2 v = a < L ? A[a] : make_int2(-1, 0);
+    nx[e] = v.x;
+    rk[e] = v.y;
+  }
+  pj_steps<E>(grid, nx, rk, A, B, L, steps, tid, T);
+#pragma unroll
+  for (int e = 0; e < E; e++)
+    if (tid + e * T < L) rkout[tid + e * T] = rk[e];
+  grid.sync();
+  for (int i = tid; i < m; i += T) flag[L - 1 - rkout[2 * i]] = 1;  // k_down_flags
+  grid.sync();
+  // exclusive scan of flag[0..L) into downs: block b owns [b S, (b+1) S)
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int Sg = (L + gridDim.x - 1) / gridDim.x;
+  const int lo_i = min(L, (int)blockIdx.x * Sg), hi_i = min(L, lo_i + Sg);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = lo_i; base < hi_i; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int f = i < hi_i ? flag[i] : 0;
+    int x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    if (i < hi_i) downs[i] = carry_s + (warp ? wsum[warp - 1] : 0) + x - f;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s += wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
+  grid.sync();
+  int off = 0;
+  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
+  for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) downs[i] += off;
+  grid.sync();
+  for (int i = tid; i < m; i += T) {  // k_emit
+    const int e = (int)(S[i] & lo);
+    const int v = child_of[e];
+    const int pre = 1 + downs[L - 1 - rkout[2 * i]];
+    pi[pre] = v;
+    h[pre - 1] = ew[e];
+    if (i == 0) pi[0] = root;
+  }
+}
+
 // one 1024-thread block per SM: the grid-wide barrier of every step is cheapest with
 // the fewest blocks, and 148 x 1024 threads cover the 2(n-1) arcs in a few strides
 constexpr int kCoopThreads = 1024;
@@ -300,6 +496,36 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   if ((s = sort_pairs_i32_bits(c, src, ssrc, arc, sarc, L, sh))) return s;
   k_adj<<<gL, 256, 0, c->stream>>>(ssrc, sarc, L, start, end, posarc);
   APPD_LAUNCHED(c);
+  int steps = 0;
+  while ((1 << steps) < L) steps++;
+  steps++;
+  const int cgrid = coop_grid(c, L);
+  const int cE = (L + cgrid * kCoopThreads - 1) / (cgrid * kCoopThreads);
+  int* blocksum = (int*)ws(c, S_SCAN, sizeof(int) * (cgrid + 1) + 64);
+  if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "dendrogram scan workspace");
+  if (cE <= 4) {
+    // fused cooperative tours (the separate kernels below are the fallback)
+    {
+      int mm = m, nn = n, rt = root, lv = levels, st = steps;
+      void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &rt, &bufA, &bufB, &rk, &parent, &val,
+                      &child_of, &jm, &lv, &st};
+      const void* fn = cE <= 1 ? (const void*)k_tour1<1> : cE <= 2 ? (const void*)k_tour1<2> : (const void*)k_tour1<4>;
+      APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, cgrid, kCoopThreads, args, 0, c->stream));
+      c->launches++;
+    }
+    k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
+    APPD_LAUNCHED(c);
+    if ((s = sort_keys_u64_bits64(c, key, S, m, 0, 2 * sh))) return s;
+    {
+      int mm = m, nn = n, shh = sh, rt = root, st = steps;
+      void* args[] = {&S, &mm, &nn, &shh, &child_of, &first, &sidx, &rt, &bufA, &bufB, &rk, &flag, &downs, &blocksum,
+                      &ew, &pi, &h, &st};
+      const void* fn = cE <= 1 ? (const void*)k_tour2<1> : cE <= 2 ? (const void*)k_tour2<2> : (const void*)k_tour2<4>;
+      APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, cgrid, kCoopThreads, args, 0, c->stream));
+      c->launches++;
+    }
+    return APPD_OK;
+  }
   // B, C: Euler tour of the MST from the root, tour ranks
   k_euler_succ<<<gL, 256, 0, c->stream>>>(eu, ev, m, sarc, start, end, posarc, root, succ0, rank0);
   APPD_LAUNCHED(c);
