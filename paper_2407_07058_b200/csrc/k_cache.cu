@@ -1196,68 +1196,80 @@ __global__ void k_cm_filter(CmParams P) {
 // bound on the path from C to D in the MST of the bounds (cut property), so
 // T = min(symmetric bound, path maximum) keeps every MST edge's minimum pair listed;
 // pairs above T are not MST edges and may come out inflated.  Output T (k x k).
+// warp argmin of (64-bit key, 32-bit index) pairs, smallest index among equal keys, with
+// three redux.sync reductions (high word, low word among the winners, index among the
+// winners) instead of a five-level shuffle tree of 64-bit pairs
+__device__ __forceinline__ void warp_argmin_u64(u64& key, int& idx) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+  const bool win = hi == mhi && lo == mlo;
+  const int mi = (int)__reduce_min_sync(0xffffffffu, win ? (unsigned)idx : 0xffffffffu);
+  key = ((u64)mhi << 32) | mlo;
+  idx = mi;
+}
+
 __global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
                                                        unsigned* __restrict__ T) {
   extern __shared__ float symb[];   // [k][k] symmetric bounds, then [k][k] path maxima
   float* pm = symb + k * k;
-  __shared__ float sv[8];
-  __shared__ int si[8];
-  __shared__ int sel[2];            // node joining the tree and its tree neighbour
-  __shared__ float selw;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
     const int a = e / k, b = e % k;
     symb[e] = fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
     pm[e] = 0.0f;
   }
   __syncthreads();
-  // Prim from node 0, thread q owns node q (k <= 128 <= blockDim); when q joins through
-  // tree neighbour f with bound w, every node x already in the tree gets
-  // pm[x][q] = pm[q][x] = max(pm[x][f], w): the path maxima of the bound MST, O(k) per step
-  const int q = threadIdx.x;
-  const int lane = q & 31, w = q >> 5;
-  bool in = q == 0 || q >= k;
-  float key = (q < k && q > 0) ? symb[q] : INFINITY;
-  int from = 0;
-  for (int step = 1; step < k; step++) {
-    float bv = in ? INFINITY : key;
-    int bi = in ? 0x7fffffff : q;
+  // Prim from node 0 in one warp, lane l owning nodes l + 32 t (k <= 128); when node nq
+  // joins through tree neighbour f with bound w, every node x already in the tree gets
+  // pm[x][nq] = pm[nq][x] = max(pm[x][f], w): the path maxima of the bound MST
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    bool in[4];
+    float key[4];
+    int from[4];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    for (int t = 0; t < 4; t++) {
+      const int q = lane + 32 * t;
+      in[t] = q == 0 || q >= k;
+      key[t] = (q < k && q > 0) ? symb[q] : INFINITY;
+      from[t] = 0;
     }
-    if (lane == 0) { sv[w] = bv; si[w] = bi; }
-    __syncthreads();
-    if (q == 0) {
-      float b2 = sv[0];
-      int i2 = si[0];
-      for (int t = 1; t < (int)(blockDim.x >> 5); t++)
-        if (sv[t] < b2 || (sv[t] == b2 && si[t] < i2)) { b2 = sv[t]; i2 = si[t]; }
-      sel[0] = i2;
+    for (int step = 1; step < k; step++) {
+      // (orderable bound, node) argmin; bounds are >= 0 or +inf, so the float bits order
+      u64 bv = KEY_NONE;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const u64 kv = in[t] ? KEY_NONE : (((u64)__float_as_uint(key[t]) << 32) | (unsigned)(lane + 32 * t));
+        if (kv < bv) { bv = kv; bi = lane + 32 * t; }
+      }
+      warp_argmin_u64(bv, bi);
+      const int nq = bi;
+      // the joining node's tree neighbour and bound, from its owner lane
+      int fo = 0;
+      float wo = 0.0f;
+#pragma unroll
+      for (int t = 0; t < 4; t++)
+        if (lane + 32 * t == nq) { fo = from[t]; wo = key[t]; in[t] = true; }
+      const int f = __shfl_sync(0xffffffffu, fo, nq & 31);
+      const float wq = __shfl_sync(0xffffffffu, wo, nq & 31);
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int q = lane + 32 * t;
+        if (q >= k) continue;
+        if (in[t] && q != nq) {  // in-tree nodes (before nq joined): path max to nq
+          const float v = fmaxf(pm[q * k + f], wq);
+          pm[q * k + nq] = v;
+          pm[nq * k + q] = v;
+        } else if (!in[t]) {
+          const float wn = symb[nq * k + q];
+          if (wn < key[t]) { key[t] = wn; from[t] = nq; }
+        }
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    const int nq = sel[0];
-    if (q == nq) {
-      sel[1] = from;
-      selw = key;
-      in = true;
-    }
-    __syncthreads();
-    const int f = sel[1];
-    const float wq = selw;
-    // in-tree nodes x (before nq joined): path max to nq
-    if (q < k && in && q != nq) {
-      const float v = fmaxf(pm[q * k + f], wq);
-      pm[q * k + nq] = v;
-      pm[nq * k + q] = v;
-    }
-    if (q < k && !in) {
-      const float wn = symb[nq * k + q];
-      if (wn < key) { key = wn; from = nq; }
-    }
-    __syncthreads();
   }
+  __syncthreads();
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int a = e / k, b = e % k;
     T[e] = __float_as_uint(a == b ? symb[e] : fminf(symb[e], pm[e]));
@@ -1301,12 +1313,7 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
 #pragma unroll
     for (int t = 0; t < 4; t++)
       if (!in[t] && (key[t] < bv || (key[t] == bv && lane + 32 * t < bi))) { bv = key[t]; bi = lane + 32 * t; }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const u64 ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
+    warp_argmin_u64(bv, bi);
     if (bv == KEY_NONE || overflow) break;
     if (lane == 0) mstkeys[base + step - 1] = bv;
     added = step;
