@@ -690,7 +690,40 @@ __global__ void k_topk_select(int p_begin, int p_end, int n, int K, const unsign
                               int* __restrict__ cj, int* __restrict__ ccnt, u64* __restrict__ compbest,
                               int* __restrict__ fallback, unsigned* __restrict__ nfallback) {
   const int warps = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int p = p_begin + blockIdx.x * warps + w; p < p_end; p += gridDim.x * warps) {
+  // rows in pairs: two rows with at most 16 candidates each are sorted together, one per
+  // half warp (a 16-wide bitonic network); otherwise each row takes the whole warp
+  for (int p0 = p_begin + 2 * (blockIdx.x * warps + w); p0 < p_end; p0 += 2 * gridDim.x * warps) {
+    const unsigned ca = cnt[p0], cb = p0 + 1 < p_end ? cnt[p0 + 1] : 0u;
+    if (ca >= 1 && ca <= 16 && cb <= 16 && ca <= (unsigned)cap && cb <= (unsigned)cap) {
+      const int half = lane >> 4, hl = lane & 15;
+      const int p = p0 + half;
+      const unsigned c = half ? cb : ca;
+      const bool live = p < p_end && c >= 1;
+      u64 x = (live && hl < (int)c) ? cand[(int64_t)p * cap + hl] : KEY_NONE;
+#pragma unroll
+      for (int size = 2; size <= 16; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          const u64 y = __shfl_xor_sync(0xffffffffu, x, stride);
+          const bool up = (hl & size) == 0;
+          const bool lower = (hl & stride) == 0;
+          const u64 lo = x < y ? x : y, hi = x < y ? y : x;
+          x = (lower == up) ? lo : hi;
+        }
+      const int take = min((int)c, K);
+      if (p < p_end && c == 0 && hl == 0) {  // the second row without candidates
+        ccnt[p] = -1;
+        fallback[atomicAdd(nfallback, 1u)] = p;
+      }
+      if (live && hl < take) {
+        ckey[(int64_t)p * K + hl] = x;
+        cj[(int64_t)p * K + hl] = other_end(x & ((1ull << 33) - 1), p);
+        if (hl == 0) compbest[p] = x;
+      }
+      if (live && hl == 0) ccnt[p] = take;
+      continue;
+    }
+    for (int p = p0; p < min(p0 + 2, p_end); p++) {
     const unsigned c = cnt[p];
     if (c > (unsigned)cap || c == 0) {
       if (lane == 0) {
@@ -749,6 +782,7 @@ __global__ void k_topk_select(int p_begin, int p_end, int n, int K, const unsign
     }
     // a row whose list holds every other point (n - 1 <= K) is complete
     if (lane == 0) ccnt[p] = take;
+    }
   }
 }
 
