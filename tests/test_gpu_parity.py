@@ -301,6 +301,23 @@ def test_points_metrics(P, metric):
         assert e.value.name == "APPD_ERR_UNSUPPORTED"
 
 
+def test_permutation_equivariance_large(ctx):
+    """relabelling the input relabels the APPD, M(P X) = P M(X) P^T, bit for
+    bit, at sizes beyond the oracle's reach and with heavy ties (the engines break ties by
+    index, so every tie decision changes under the permutation)."""
+    g = torch.Generator().manual_seed(5)
+    X = torch.from_numpy(G.random_points(20000, 16, 41, "clumps")).cuda()
+    p = torch.randperm(X.shape[0], generator=g).cuda()
+    M = ctx.solve_points(X)
+    Mp = ctx.solve_points(X[p].contiguous())
+    assert torch.equal(Mp.view(torch.int32), M[p][:, p].contiguous().view(torch.int32))
+    W = torch.from_numpy(G.random_weights(3000, 42, "ties")).cuda()
+    q = torch.randperm(W.shape[0], generator=g).cuda()
+    M = ctx.solve_weights(W)
+    Mq = ctx.solve_weights(W[q][:, q].contiguous())
+    assert torch.equal(Mq.view(torch.int32), M[q][:, q].contiguous().view(torch.int32))
+
+
 def test_points_list_overflow_is_exact(P, monkeypatch):
     """A candidate list far too small for the input: rows whose entries are lost are
     poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the
