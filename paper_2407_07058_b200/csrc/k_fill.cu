@@ -16,6 +16,7 @@
 // HBM write bandwidth (n^2 * 4 bytes).  RMQ is a sparse table over h
 // (ST[k][i] = max h[i .. i+2^k-1]).  Widest sense: min instead of max.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -158,13 +159,20 @@ constexpr int FILL_R = 128;  // rows per tile (consecutive in leaf order)
 // positions spanned by one tile whose in-tile range maxima come from shared memory
 constexpr int FILL_SPAN = 256, FILL_LV = 8;  // 2^FILL_LV >= FILL_SPAN
 
-template <int VEC, bool WIDEST>
+// output store flavour (STORE: 0 streaming / evict-first st.global.cs, 1 default st.global)
+template <int STORE>
+__device__ __forceinline__ void fill_store4(float* dst, float4 v) {
+  if (STORE == 0) __stcs(reinterpret_cast<float4*>(dst), v);
+  else *reinterpret_cast<float4*>(dst) = v;
+}
+
+template <int VEC, bool WIDEST, int STORE = 0>
 __global__ void __launch_bounds__(FILL_THREADS)
     k_fill(const int* __restrict__ rows_sorted, const int* __restrict__ rowpos, int64_t nrows,
            const int* __restrict__ pos, const float* __restrict__ ST, int64_t stride, int64_t n,
            float* __restrict__ M, int64_t row0) {
-  __shared__ float sS[FILL_R], sP[FILL_R];
-  __shared__ int64_t sOff[FILL_R];
+  __shared__ float2 sSP[FILL_R];   // (S, P) of each row: one 8-byte broadcast load per row
+  __shared__ float* sPtr[FILL_R];  // the row's first element in M
   __shared__ int sA[FILL_R];
   // sparse table of h over the tile's position range [aL, aR): columns whose position
   // lies inside it (the tile's own points, and other ranks' in between) need a direct
@@ -178,9 +186,8 @@ __global__ void __launch_bounds__(FILL_THREADS)
     int t = threadIdx.x;
     int at = rowpos[t0 + t];
     sA[t] = at;
-    sOff[t] = ((int64_t)rows_sorted[t0 + t] - row0) * n;
-    sS[t] = (at < aR) ? rmq<WIDEST>(ST, stride, at, aR) : ID;
-    sP[t] = (at > aL) ? rmq<WIDEST>(ST, stride, aL, at) : ID;
+    sPtr[t] = M + ((int64_t)rows_sorted[t0 + t] - row0) * n;
+    sSP[t] = make_float2((at < aR) ? rmq<WIDEST>(ST, stride, at, aR) : ID, (at > aL) ? rmq<WIDEST>(ST, stride, aL, at) : ID);
   }
   // this thread's VEC columns
   const int64_t jbase = (int64_t)blockIdx.x * (FILL_THREADS * VEC) + (int64_t)threadIdx.x * VEC;
@@ -214,7 +221,8 @@ __global__ void __launch_bounds__(FILL_THREADS)
   __syncthreads();
 #pragma unroll 4
   for (int t = 0; t < R; t++) {
-    const float S = sS[t], P = sP[t];
+    const float2 SP = sSP[t];
+    const float S = SP.x, P = SP.y;
     float v[VEC];
 #pragma unroll
     for (int q = 0; q < VEC; q++) v[q] = comb<WIDEST>(side[q] == 0 ? S : P, base[q]);
@@ -236,9 +244,14 @@ __global__ void __launch_bounds__(FILL_THREADS)
         }
       }
     }
-    float* dst = M + sOff[t] + jbase;
-    if (VEC == 4) {
-      if (in_range) __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+    float* dst = sPtr[t] + jbase;
+    if (VEC == 8) {  // one 32-byte streaming store (st.global.cs.v8.f32, sm_100)
+      if (in_range)
+        asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
+                     "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                     : "memory");
+    } else if (VEC == 4) {
+      if (in_range) fill_store4<STORE>(dst, make_float4(v[0], v[1], v[2], v[3]));
     } else {
 #pragma unroll
       for (int q = 0; q < VEC; q++)
@@ -250,16 +263,24 @@ __global__ void __launch_bounds__(FILL_THREADS)
 appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
                         const float* ST, int64_t stride, int64_t n, float* M, int64_t row0, int widest) {
   if (nrows <= 0) return APPD_OK;
+  const bool vec8 = (n % 8) == 0 && ((uintptr_t)M % 32) == 0;
   const bool vec4 = (n % 4) == 0 && ((uintptr_t)M % 16) == 0;
-  const int cols_per_cta = FILL_THREADS * (vec4 ? 4 : 1);
+  const int cols_per_cta = FILL_THREADS * (vec8 ? 8 : vec4 ? 4 : 1);
   dim3 grid((unsigned)((n + cols_per_cta - 1) / cols_per_cta), (unsigned)((nrows + FILL_R - 1) / FILL_R));
   if (grid.y > 65535u) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
-  if (vec4) {
-    if (widest) k_fill<4, true><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<4, false><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  // 32-byte stores by default (measured: fewer instructions per byte); APPD_FILL_VEC=4 picks 16-byte
+  static const int want = getenv("APPD_FILL_VEC") ? atoi(getenv("APPD_FILL_VEC")) : 8;
+  if (vec8 && want == 8) {
+    if (widest) k_fill<8, true, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<8, false, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  } else if (vec4) {
+    dim3 g4((unsigned)((n + FILL_THREADS * 4 - 1) / (FILL_THREADS * 4)), grid.y);
+    if (widest) k_fill<4, true, 0><<<g4, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<4, false, 0><<<g4, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
   } else {
-    if (widest) k_fill<1, true><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<1, false><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    dim3 g1((unsigned)((n + FILL_THREADS - 1) / FILL_THREADS), grid.y);
+    if (widest) k_fill<1, true><<<g1, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<1, false><<<g1, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
   }
   APPD_LAUNCHED(c);
   c->stats.fill_launches++;

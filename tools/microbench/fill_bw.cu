@@ -12,6 +12,31 @@ __global__ void k_linear(float4* p, size_t n4) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
     __stcs(p + i, make_float4(1.f, 2.f, 3.f, 4.f));
 }
+__global__ void k_linear_plain(float4* p, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_float4(1.f, 2.f, 3.f, 4.f);
+}
+// 32-byte stores (st.global.v8.f32, sm_100)
+__global__ void k_linear_v8(float* p, size_t n8) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+    float* q = p + 8 * i;
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(q), "f"(1.f), "f"(2.f), "f"(3.f),
+                 "f"(4.f), "f"(5.f), "f"(6.f), "f"(7.f), "f"(8.f)
+                 : "memory");
+  }
+}
+template <int W>
+__global__ void __launch_bounds__(256) k_tiles_v8(float* M, const int* rows, int n) {
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  for (int t = 0; t < 128; t++) {
+    float* dst = M + (int64_t)rows[t0 + t] * n + (int64_t)blockIdx.x * W + 8 * threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < W / 2048; c++)
+      asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + c * 2048), "f"(1.f),
+                   "f"(2.f), "f"(3.f), "f"(4.f), "f"(5.f), "f"(6.f), "f"(7.f), "f"((float)t)
+                   : "memory");
+  }
+}
 template <int W>
 __global__ void __launch_bounds__(256) k_tiles(float* M, const int* rows, int n) {
   const int64_t t0 = (int64_t)blockIdx.y * 128;
@@ -56,5 +81,9 @@ int main() {
   time([&] { k_tiles<2048><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles 128 x 8 KB");
   time([&] { k_tiles<4096><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles 128 x 16 KB");
   time([&] { cudaMemsetAsync(M, 0, bytes); }, "cudaMemset");
+  time([&] { k_linear_plain<<<148 * 16, 256>>>((float4*)M, bytes / 16); }, "linear plain");
+  time([&] { k_linear_v8<<<148 * 16, 256>>>(M, bytes / 32); }, "linear v8 (32 B)");
+  time([&] { k_tiles_v8<2048><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8 128 x 8 KB");
+  time([&] { k_linear<<<148 * 64, 256>>>((float4*)M, bytes / 16); }, "linear (more CTAs)");
   return 0;
 }
