@@ -154,7 +154,7 @@ __device__ __forceinline__ float rmq(const float* __restrict__ ST, int64_t strid
 }
 
 constexpr int FILL_THREADS = 256;
-constexpr int FILL_R = 128;  // rows per tile (consecutive in leaf order)
+constexpr int FILL_R = 128;  // max rows per tile (consecutive in leaf order; <= FILL_THREADS)
 
 // positions spanned by one tile whose in-tile range maxima come from shared memory
 constexpr int FILL_SPAN = 256, FILL_LV = 8;  // 2^FILL_LV >= FILL_SPAN
@@ -166,7 +166,7 @@ __device__ __forceinline__ void fill_store4(float* dst, float4 v) {
   else *reinterpret_cast<float4*>(dst) = v;
 }
 
-template <int VEC, bool WIDEST, int STORE = 0>
+template <int VEC, bool WIDEST, int STORE = 0, int RT = FILL_R>
 __global__ void __launch_bounds__(FILL_THREADS)
     k_fill(const int* __restrict__ rows_sorted, const int* __restrict__ rowpos, int64_t nrows,
            const int* __restrict__ pos, const float* __restrict__ ST, int64_t stride, int64_t n,
@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(FILL_THREADS)
   // range maximum per element; from shared memory when the span fits
   __shared__ float sST[FILL_LV][FILL_SPAN];
   const float ID = WIDEST ? INFINITY : -INFINITY;
-  const int64_t t0 = (int64_t)blockIdx.y * FILL_R;
-  int R = (int)((nrows - t0) < FILL_R ? (nrows - t0) : FILL_R);
+  const int64_t t0 = (int64_t)blockIdx.y * RT;
+  int R = (int)((nrows - t0) < RT ? (nrows - t0) : RT);
   const int aL = rowpos[t0], aR = rowpos[t0 + R - 1];
   if (threadIdx.x < R) {
     int t = threadIdx.x;
@@ -205,6 +205,15 @@ __global__ void __launch_bounds__(FILL_THREADS)
     else { side[q] = 2; base[q] = ID; any_inside = true; }
   }
   const bool warp_inside = __any_sync(0xffffffffu, any_inside);
+  // predicate-free selection per row: v = comb(comb'(S, cS), comb'(P, cP), base) with
+  // cS = +-inf (pass S / block it) by side, so no per-column predicates stay live
+  const float PASS = WIDEST ? -INFINITY : INFINITY;  // comb'(x, PASS) = x
+  float cS[VEC], cP[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; q++) {
+    cS[q] = side[q] == 0 ? PASS : ID;
+    cP[q] = side[q] == 1 ? PASS : ID;
+  }
   const bool in_range = jbase < n;
   const int span = aR - aL;  // h[aL .. aR-1]
   const bool local = span <= FILL_SPAN;
@@ -225,7 +234,12 @@ __global__ void __launch_bounds__(FILL_THREADS)
     const float S = SP.x, P = SP.y;
     float v[VEC];
 #pragma unroll
-    for (int q = 0; q < VEC; q++) v[q] = comb<WIDEST>(side[q] == 0 ? S : P, base[q]);
+    for (int q = 0; q < VEC; q++) {
+      // minimax: max(min(S, cS), min(P, cP), base); widest: min(max(S, cS), max(P, cP), base)
+      const float xs = WIDEST ? fmaxf(S, cS[q]) : fminf(S, cS[q]);
+      const float xp = WIDEST ? fmaxf(P, cP[q]) : fminf(P, cP[q]);
+      v[q] = comb<WIDEST>(comb<WIDEST>(xs, xp), base[q]);
+    }
     if (warp_inside) {
       const int at = sA[t];
 #pragma unroll
