@@ -217,15 +217,10 @@ __global__ void __launch_bounds__(FILL_THREADS)
   const bool in_range = jbase < n;
   const int span = aR - aL;  // h[aL .. aR-1]
   const bool local = span <= FILL_SPAN;
-  if (local) {
-    for (int i = threadIdx.x; i < span; i += FILL_THREADS) sST[0][i] = __ldg(ST + aL + i);
-    __syncthreads();
-    for (int k = 1; (1 << k) <= span; k++) {
-      const int half = 1 << (k - 1);
+  if (local) {  // the global table's levels over [aL, aR): independent loads, one barrier
+    for (int k = 0; (1 << k) <= span; k++)
       for (int i = threadIdx.x; i + (1 << k) <= span; i += FILL_THREADS)
-        sST[k][i] = comb<WIDEST>(sST[k - 1][i], sST[k - 1][i + half]);
-      __syncthreads();
-    }
+        sST[k][i] = __ldg(ST + (int64_t)k * stride + aL + i);
   }
   __syncthreads();
 #pragma unroll 4
