@@ -71,7 +71,9 @@ typedef enum {
 
 /* MST variant (appd_options.variant) */
 #define APPD_VARIANT_AUTO 0
-#define APPD_VARIANT_PRIM 1    /* single-CTA Prim, emits the leaf order directly (n <= 4096, world == 1) */
+#define APPD_VARIANT_PRIM 1    /* Prim's n sequential steps: not built on the GPU — a
+                                  grid-wide barrier per step loses to Borůvka at every size measured;
+                                  appd_create rejects it with APPD_ERR_UNSUPPORTED (the oracle is Prim) */
 #define APPD_VARIANT_BORUVKA 2 /* row-parallel Boruvka rounds (any n, shards over ranks) */
 
 typedef struct {

@@ -137,6 +137,7 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return APPD_ERR_INVALID_ARGUMENT;
   if (o.sense != 1 && o.sense != -1) return APPD_ERR_INVALID_ARGUMENT;
   if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.variant == APPD_VARIANT_PRIM) return APPD_ERR_UNSUPPORTED;  // not built (appd.h)
   if (o.metric < 0 || o.metric > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.world > 1 && !o.nccl_unique_id) return APPD_ERR_INVALID_ARGUMENT;
   int ndev = 0;

@@ -83,6 +83,12 @@ def test_options_defaults_and_create_without_gpu(lib):
     lib.appd_options_init(ctypes.byref(bad))
     bad.struct_size = 3
     assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
+    lib.appd_options_init(ctypes.byref(bad))
+    bad.variant = 1  # Prim: documented as not built
+    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 5
+    lib.appd_options_init(ctypes.byref(bad))
+    bad.metric = 3  # metrics are 0, 1, 2
+    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
     lib.appd_destroy(None)  # NULL-safe
 
 
