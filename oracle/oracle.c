@@ -169,7 +169,10 @@ static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
       if (done[u]) continue;
       float w = wget(s, v, u);
       float k = sense > 0 ? w : -w;
-      if (k < key[u]) { key[u] = k; parent[u] = (int32_t)v; }
+      /* an edge of weight +inf (points whose squared distance overflows fp32) is still an
+       * edge of the complete graph (reading Q14): the first tree vertex to
+       * offer one becomes the parent */
+      if (parent[u] < 0 || k < key[u]) { key[u] = k; parent[u] = (int32_t)v; }
     }
   }
   free(key); free(parent); free(done);

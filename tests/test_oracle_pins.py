@@ -454,3 +454,17 @@ def test_metrics_coincide_in_one_dimension():
     M0 = oracle.appd_points(X)
     for metric in (1, 2):
         assert_bit_equal(oracle.appd_points(X, metric=metric), M0)
+
+
+def test_overflowing_distances_are_infinite_edges():
+    """Reading Q14: points whose squared distance overflows fp32 are joined by an edge of
+    weight +inf (the graph is complete).  Closed form: the ordinary half keeps
+    its own APPD, every entry across the halves and between huge points is +inf."""
+    rs = np.random.default_rng(8)
+    X = (rs.standard_normal((120, 5)) * 1e20).astype(np.float32)
+    X[:60] *= np.float32(1e-20)
+    M = oracle.appd_points(X)
+    assert_bit_equal(M[:60, :60], oracle.appd_points(X[:60]))
+    assert np.isinf(M[:60, 60:]).all() and np.isinf(M[60:, :60]).all()
+    off = ~np.eye(60, dtype=bool)
+    assert np.isinf(M[60:, 60:][off]).all() and (bits(np.diag(M)) == 0).all()
