@@ -399,18 +399,23 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   TcState tc;
   bool use_tc = false;
   if (points && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
-    s = tcf_prepare(c, X, n, d, &tc);
-    if (defer_validation) {  // tcf_prepare synchronised the stream: the verdict is in pinned memory
-      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-      u64 hb[3];
-      memcpy(hb, hbad, sizeof hb);
-      appd_status sv = report_validation(c, hb, n, points, d);
-      if (sv) return sv;
+    s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
+    if (s == APPD_OK) {
+      use_tc = true;
+    } else {
+      if (defer_validation) {  // the verdict decides before any fallback
+        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        u64 hb[3];
+        memcpy(hb, hbad, sizeof hb);
+        appd_status sv = report_validation(c, hb, n, points, d);
+        if (sv) return sv;
+      }
+      if (s != APPD_ERR_UNSUPPORTED || c->opt.points_engine == 2) return s;
     }
-    if (s == APPD_OK) use_tc = true;
-    else if (s != APPD_ERR_UNSUPPORTED || c->opt.points_engine == 2) return s;
     c->last_error.clear();
   }
+  // read at the first synchronisation of the round loop
+  bool check_first_sync = use_tc;
   c->stats.points_engine = points ? (use_tc ? 2 : 1) : 0;
   int64_t rt_begin = 0, rt_end = 0;
   if (use_tc) {
@@ -636,6 +641,24 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (check_first_sync) {
+      check_first_sync = false;
+      if (defer_validation) {  // the input verdict, queued before the engine started
+        u64 hb[3];
+        memcpy(hb, hbad, sizeof hb);
+        appd_status sv = report_validation(c, hb, n, points, d);
+        if (sv) return sv;
+      }
+      if (c->pinned_small[50] == 0) {  // coordinates too large for the filter: exact engine
+        if (c->opt.points_engine == 2)
+          return fail(c, APPD_ERR_UNSUPPORTED, "coordinates too large for the tensor-core filter");
+        const int pe = c->opt.points_engine;
+        c->opt.points_engine = 1;
+        const appd_status s2 = solve(c, W, X, n, d, M);
+        c->opt.points_engine = pe;
+        return s2;
+      }
+    }
     if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
     if (use_tc) {
       if (c->opt.timing && tc.scanned) {

@@ -132,16 +132,25 @@ enum Slot {
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
-  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
 
 // tensor-core filtered points scan (k_tcfilter.cu)
+// the scaling of the packed operands, computed on the device from max |x - c| (no host
+// round trip): y^ = fp16(scale (x - c)); maxlen bounds |y^|; s2 = scale^2; ok = 0 when the
+// coordinates are too large for the filter (the solve then falls back to the exact engine)
+struct TcScale {
+  float scale, maxlen;
+  double s2;
+  int ok, pad;
+};
 struct TcState {
   int64_t n = 0, d = 0, npad = 0;
   int dk = 0, K = 0, stages = 0;
-  float scale = 1.0f, c1 = 0.0f, c2 = 0.0f, k1 = 0.0f, k2 = 0.0f, k3 = 0.0f, gamma = 0.0f;
+  float c1 = 0.0f, c2 = 0.0f, k1 = 0.0f, k2 = 0.0f, k3 = 0.0f, gamma = 0.0f;
+  TcScale* dscale = nullptr;  // device
   float* center = nullptr;
   void* YA = nullptr;  // __half
   void* YB = nullptr;
@@ -159,7 +168,6 @@ struct TcState {
   float* TM = nullptr;      // [col tile][row] eligible maxima of G' from the scan
   void* list = nullptr;     // uint2 (row, tile) pairs that need the exact check
   unsigned list_cap = 0;
-  float maxlen_scaled = 0.0f;
   // round-0 candidate cache (k_cache.cu); topk == 0: no cache
   int topk = 0, cap = 0;
   int64_t cache_r0 = 0, cache_r1 = 0;  // original rows whose cache this rank holds
@@ -211,7 +219,7 @@ appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, 
                               const unsigned* nrows, int max_rows, const int* comp, u64* compbest);
 appd_status launch_rescan_blocks(appd_ctx* c, int n, const int* perm, const int* need, int* needp, int* blockflag,
                                  int nblocks, int* list, int* count);
-appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, double s2, const int* perm,
+appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, const TcScale* s2, const int* perm,
                            const int* needp, const unsigned* UB, const int* comp, unsigned* compUB);
 int64_t tcf_row_tiles(const TcState* st);
 appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, float* tc_out, float* ref_out);

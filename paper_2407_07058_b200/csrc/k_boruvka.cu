@@ -515,7 +515,9 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
         for (int a = 0; a < 8; a++) {
           bool elig = ROUND0 ? (j < n && j != ri[a]) : (cj != cr[a] && cj >= 0);
-          if (elig && acc[a][b] < bd[a]) { bd[a] = acc[a][b]; bj[a] = j; }
+          // the first eligible column is taken even at +inf (coordinates whose squares
+          // overflow): every component must choose an edge
+          if (elig && (bj[a] < 0 || acc[a][b] < bd[a])) { bd[a] = acc[a][b]; bj[a] = j; }
         }
       }
     }

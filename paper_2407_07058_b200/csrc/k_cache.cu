@@ -135,7 +135,7 @@ __device__ __forceinline__ void topk_merge(float (&top)[K], const float (*stop)[
 template <int K>
 __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __restrict__ TM32, int nch, int p_begin,
                                                              int p_end, const float* __restrict__ nrm,
-                                                             const float* __restrict__ len, float maxlen,
+                                                             const float* __restrict__ len, const TcScale* __restrict__ sc,
                                                              const float* __restrict__ err,
                                                              const float* __restrict__ maxerr, ErrModel em,
                                                              float* __restrict__ UBK, unsigned* __restrict__ list,
@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
   __shared__ unsigned short sidx[TK_PARTS][TK_SEL][32];  //   and chunk index
   __shared__ int slost[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float maxlen = sc->maxlen;
   constexpr int U4 = TK_BATCH / 4;
   const int nch4 = (nch + 3) >> 2;
   const int g0 = (int)((int64_t)w * nch4 / TK_PARTS), g1 = (int)((int64_t)(w + 1) * nch4 / TK_PARTS);
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
 }
 
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
-                             const float* nrm, const float* len, float maxlen, const float* err,
+                             const float* nrm, const float* len, const TcScale* sc, const float* err,
                              const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
                              unsigned cap, unsigned* cand_cnt) {
   const int rows = p_end - p_begin;
@@ -357,7 +358,7 @@ appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int
       cudaFuncSetAttribute(k_topk_scan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);          \
       attr_##KK = true;                                                                                        \
     }                                                                                                          \
-    k_topk_scan<KK><<<grid, 32 * TK_PARTS, smem, c->stream>>>(TM32, nch, p_begin, p_end, nrm, len, maxlen, err, \
+    k_topk_scan<KK><<<grid, 32 * TK_PARTS, smem, c->stream>>>(TM32, nch, p_begin, p_end, nrm, len, sc, err, \
                                                               maxerr, em, UBK, list, count, cap, cand_cnt, ngq); \
   } while (0)
   switch (K) {
@@ -494,6 +495,7 @@ __global__ void k_item_table(const unsigned* __restrict__ run_lo, const unsigned
 template <int MODE>
 __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParams L) {
   extern __shared__ __align__(16) float sm[];
+  const double s2 = MODE == 0 ? L.tsc->s2 : 0.0;
   float* colx = sm;                 // [d][32]
   float* rowx = sm + L.d * 32;      // [d][LE_RB]
   __shared__ int rowp[LE_RB];
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
           const double ubk = (double)L.UBK[p];
 #pragma unroll
           for (int b = 0; b < 4; b++) {
-            if (oq[b] >= 0 && oq[b] != op && (double)acc[a][b] * L.s2 <= ubk) {
+            if (oq[b] >= 0 && oq[b] != op && (double)acc[a][b] * s2 <= ubk) {
               const unsigned slot = atomicAdd(L.cnt + p, 1u);
               if (slot < (unsigned)L.ccap)
                 L.cand[(int64_t)p * L.ccap + slot] =
@@ -843,7 +845,9 @@ __global__ void k_compact_blocks(int nblocks, const int* __restrict__ blockflag,
 
 // compUB[comp] = min over flagged rows of UB (scaled units), seeded by the cached
 // component minima s^2 d^2(compbest) (rounded up)
-__global__ void k_comp_ub_seed(int k, const u64* __restrict__ compbest, double s2, unsigned* __restrict__ compUB) {
+__global__ void k_comp_ub_seed(int k, const u64* __restrict__ compbest, const TcScale* __restrict__ sc,
+                               unsigned* __restrict__ compUB) {
+  const double s2 = sc->s2;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
     const u64 key = compbest[c];
     float v = INFINITY;
@@ -1055,7 +1059,7 @@ appd_status launch_rescan_blocks(appd_ctx* c, int n, const int* perm, const int*
   return APPD_OK;
 }
 
-appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, double s2, const int* perm,
+appd_status launch_comp_ub(appd_ctx* c, int n, int k, const u64* compbest, const TcScale* s2, const int* perm,
                            const int* needp, const unsigned* UB, const int* comp, unsigned* compUB) {
   k_comp_ub_seed<<<(k + 255) / 256, 256, 0, c->stream>>>(k, compbest, s2, compUB);
   APPD_LAUNCHED(c);
@@ -1096,6 +1100,7 @@ __global__ void k_seg_comp(const int* __restrict__ sc, int n, int nseg, int2* __
 constexpr int CM_SPLIT = 4;  // warps per 32-row group, each over a quarter of the segments
 __global__ void k_cm_rowub(CmParams P) {
   const int lane = threadIdx.x & 31;
+  const float maxlen_ = P.tsc->maxlen;
   const int nseg_n = P.n / TC_TMG;  // full segments only (a partial last segment bounds nothing)
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1111,7 +1116,7 @@ __global__ void k_cm_rowub(CmParams P) {
     const float dl = em_delta2(valid ? P.err[p] : 0.0f, *P.maxerr);
     const int smin = P.upper ? (TC_ROWS / TC_TMG) * (p0 / TC_ROWS) : 0;  // segments the scan wrote
     auto flush = [&](int D, float m) {
-      float ub = (m > -INFINITY && D != C && valid) ? em_upper(P.em, ni - 2.0f * m, ni, li, P.maxlen, dl) : INFINITY;
+      float ub = (m > -INFINITY && D != C && valid) ? em_upper(P.em, ni - 2.0f * m, ni, li, maxlen_, dl) : INFINITY;
       if (uni) {  // D is warp-uniform (segment order is the same for every lane)
 #pragma unroll
         for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
@@ -1153,6 +1158,7 @@ __global__ void k_cm_rowub(CmParams P) {
 // upper bounds, scaled units).  A listed segment contributes its 32-column chunks.
 __global__ void k_cm_filter(CmParams P) {
   const int lane = threadIdx.x & 31;
+  const float maxlen_ = P.tsc->maxlen;
   const int nseg = min(P.nseg, (P.n + TC_TMG - 1) / TC_TMG);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1177,13 +1183,13 @@ __global__ void k_cm_filter(CmParams P) {
       float thr;
       if (dd.x == dd.y) {
         e = max(s + 1, min(send, P.cend[dd.x] / TC_TMG));
-        thr = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + dd.x]), ni, li, P.maxlen, dl);
+        thr = em_thr(P.em, __uint_as_float(P.CUB[(int64_t)C * P.k + dd.x]), ni, li, maxlen_, dl);
       } else {
         e = s + 1;
         float ub = 0.0f;
         for (int D = dd.x; D <= dd.y; D++)
           if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
-        thr = em_thr(P.em, ub, ni, li, P.maxlen, dl);
+        thr = em_thr(P.em, ub, ni, li, maxlen_, dl);
       }
       for (int s0 = s; s0 < e; s0 += U) {
         float v[U];

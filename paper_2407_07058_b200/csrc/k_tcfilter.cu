@@ -109,10 +109,11 @@ __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const fl
 // B augment = -65504 (never a maximum).  One thread per point, one 16-byte store per
 // 8 coordinates (lanes = consecutive points: 128-byte runs per core matrix).
 __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, int K, const int* __restrict__ perm,
-                       const float* __restrict__ c, float scale, int64_t npad, __half* __restrict__ YA,
+                       const float* __restrict__ c, const TcScale* __restrict__ sc, int64_t npad, __half* __restrict__ YA,
                        __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
                        float* __restrict__ err, unsigned* __restrict__ maxerr) {
   float emax = 0.0f;
+  const float scale = sc->scale;
   const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npad; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gidx = p / 128;
@@ -281,7 +282,7 @@ struct ExactParams {
   const float* nrm;
   const float* len;
   const float* seg_maxlen;
-  float maxlen;  // max |y^| over all points
+  const TcScale* tsc;  // device: maxlen bounds |y^|  // max |y^| over all points
   const float* err;         // E_p (permuted)
   const float* seg_maxerr;  // per segment max E
   const float* maxerr;      // max E (device)
@@ -320,7 +321,7 @@ __global__ void k_filter_tiles(ExactParams E) {
     if (valid && E.compUB) ub = fminf(ub, __uint_as_float(E.compUB[E.comp[E.perm[p]]]));
     const float ni = valid ? E.nrm[p] : 0.0f, li = valid ? E.len[p] : 0.0f;
     const float ei = valid ? E.err[p] : 0.0f, emax = *E.maxerr;
-    const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.maxlen, em_delta2(ei, emax)) : INFINITY;
+    const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.tsc->maxlen, em_delta2(ei, emax)) : INFINITY;
     bool flagged = false;
     constexpr int U = 8;  // segments per batch: U independent coalesced loads in flight
     for (int t0 = 0; t0 < E.nseg; t0 += U) {
@@ -474,6 +475,24 @@ static ErrModel error_model(const TcState* st) {
   return e;
 }
 
+// scale = 2^e with scale * max|x - c| in [2^6.5, 2^7.5): |y^|^2 < 2^15, fp16 range safe;
+// fp16 rounding can lift |y^| by 2^-11 relative (plus subnormal slack): maxlen margin
+__global__ void k_tc_scale(const unsigned* __restrict__ maxlen_bits, TcScale* __restrict__ out) {
+  const float ml = __uint_as_float(*maxlen_bits);
+  TcScale r;
+  r.ok = ml < INFINITY ? 1 : 0;
+  int e = 0;
+  if (ml > 0.0f && r.ok) {
+    e = (int)floor(7.0 - log2((double)ml) + 0.5);
+    e = max(-100, min(100, e));
+  }
+  r.scale = (float)ldexp(1.0, e);
+  r.maxlen = r.ok ? (float)((double)ml * r.scale * (1.0 + ldexp(1.0, -10)) + 1e-6) : 0.0f;
+  r.s2 = (double)r.scale * (double)r.scale;
+  r.pad = 0;
+  *out = r;
+}
+
 appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st) {
   st->n = n;
   st->d = d;
@@ -496,20 +515,13 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   k_maxlen<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8), 256, 0, c->stream>>>(
       X, n, (int)d, st->center, maxlen);
   APPD_LAUNCHED(c);
-  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 32, maxlen, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
-  float ml;
-  memcpy(&ml, c->pinned_small + 32, 4);
-  if (!(ml < INFINITY)) return APPD_ERR_UNSUPPORTED;  // coordinates too large for the filter
-  // scale = 2^e with scale * max|y| in [2^6.5, 2^7.5): |y^|^2 < 2^15, fp16 range safe
-  int e = 0;
-  if (ml > 0.0f) {
-    e = (int)std::floor(7.0 - std::log2((double)ml) + 0.5);
-    e = std::max(-100, std::min(100, e));
-  }
-  st->scale = (float)std::ldexp(1.0, e);
-  // fp16 rounding can lift |y^| by 2^-11 relative (plus subnormal slack)
-  st->maxlen_scaled = (float)((double)ml * st->scale * (1.0 + std::ldexp(1.0, -10)) + 1e-6);
+  // the scale on the device (no host round trip); its ok flag is read at the caller's next
+  // synchronisation (coordinates too large for the filter: the solve falls back)
+  st->dscale = (TcScale*)ws(c, S_TC_SCALE, sizeof(TcScale));
+  if (!st->dscale) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc scale");
+  k_tc_scale<<<1, 1, 0, c->stream>>>(maxlen, st->dscale);
+  APPD_LAUNCHED(c);
+  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 50, &st->dscale->ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   // Error model in scaled units (tc_common.cuh):
   //  delta: each fp16 coordinate is within 2^-11 (relative, normal range) or 2^-25
   //    (absolute, subnormal) of s*(x - c); centring x - c in fp32 adds 2^-24 relative;
@@ -606,7 +618,7 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
 static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X, float* xt) {
   const int64_t n = st->n;
   APPD_CUDA(c, cudaMemsetAsync(st->maxerr, 0, sizeof(unsigned), c->stream));
-  k_pack<<<(unsigned)std::min<int64_t>((st->npad + 127) / 128, (int64_t)c->sm_count * 16), 128, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->scale,
+  k_pack<<<(unsigned)std::min<int64_t>((st->npad + 127) / 128, (int64_t)c->sm_count * 16), 128, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->dscale,
                                                   st->npad, (__half*)st->YA, (__half*)st->YB, st->nrm, st->len,
                                                   st->err, st->maxerr);
   APPD_LAUNCHED(c);
@@ -658,7 +670,7 @@ static void exact_params(const TcState* st, const TcParams& P, const int* comp, 
   E->nrm = st->nrm;
   E->len = st->len;
   E->seg_maxlen = st->seg_maxlen;
-  E->maxlen = st->maxlen_scaled;
+  E->tsc = st->dscale;
   E->err = st->err;
   E->seg_maxerr = st->seg_maxerr;
   E->maxerr = reinterpret_cast<const float*>(st->maxerr);
@@ -739,7 +751,7 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   L.item_start = item_start;
   L.items = items;
   L.UBK = st->UBK;
-  L.s2 = (double)st->scale * (double)st->scale;
+  L.tsc = st->dscale;
   L.cnt = st->cand_cnt;
   L.cand = st->cand;
   L.ccap = st->cap;
@@ -775,7 +787,6 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   const int grid_n = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
   const int T = (int)(st->npad / TC_ROWS);
   const bool cache = st->topk > 0;
-  const double s2 = (double)st->scale * (double)st->scale;
   appd_status s;
   *overflowed = false;
   st->scanned = false;
@@ -850,7 +861,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
       const int nch = (int)(st->npad / 32);
       APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
       if ((s = launch_topk_scan(c, st->topk, st->TM, nch, p_begin, p_end, st->nrm, st->len,
-                                st->maxlen_scaled, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
+                                st->dscale, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
                                 st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
         return s;
@@ -881,7 +892,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if ((s = launch_tcf_scan(c, 0, P))) return s;
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
     st->scanned = true;
-    if ((s = launch_comp_ub(c, (int)n, (int)k, compbest, s2, st->perm, st->needp, st->UB, comp, st->compUB)))
+    if ((s = launch_comp_ub(c, (int)n, (int)k, compbest, st->dscale, st->perm, st->needp, st->UB, comp, st->compUB)))
       return s;
     exact_params(st, P, comp, compbest, 0, (int)n, 0, &E);
     E.needp = st->needp;
@@ -956,7 +967,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   C.nrm = st->nrm;
   C.len = st->len;
   C.seg_maxlen = st->seg_maxlen;
-  C.maxlen = st->maxlen_scaled;
+  C.tsc = st->dscale;
   C.err = st->err;
   C.maxerr = reinterpret_cast<const float*>(st->maxerr);
   C.em = P.em;

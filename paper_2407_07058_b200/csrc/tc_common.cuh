@@ -111,7 +111,7 @@ struct CmParams {
   const float* nrm;
   const float* len;
   const float* seg_maxlen;
-  float maxlen;
+  const TcScale* tsc;  // device: maxlen bounds |y^| (scaled units)
   const float* err;     // E_p (permuted order)
   const float* maxerr;  // max E over all points (device)
   ErrModel em;
@@ -144,7 +144,7 @@ struct ListParams {
   const int4* items;          // per work item: chunk, first list entry, rows
   // MODE 0
   const float* UBK;
-  double s2;
+  const TcScale* tsc;  // device: s2 = scale^2
   unsigned* cnt;
   u64* cand;
   int ccap;
@@ -159,7 +159,7 @@ appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsign
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
-                             const float* nrm, const float* len, float maxlen, const float* err,
+                             const float* nrm, const float* len, const TcScale* sc, const float* err,
                              const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
                              unsigned cap, unsigned* cand_cnt);
 

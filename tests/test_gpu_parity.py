@@ -318,6 +318,21 @@ def test_permutation_equivariance_large(ctx):
     assert torch.equal(Mq.view(torch.int32), M[q][:, q].contiguous().view(torch.int32))
 
 
+def test_points_too_large_for_the_filter(P):
+    """Coordinates whose squares overflow fp32: the device-side scale reports it at the
+    first synchronisation and the solve is redone on the exact engine (same result as the
+    oracle, infinite distances included)."""
+    rs = np.random.default_rng(8)
+    X = (rs.standard_normal((300, 6)) * 1e20).astype(np.float32)
+    X[:150] *= np.float32(1e-20)  # half of the points at ordinary scale
+    with P.Context(timing=True) as c:
+        assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), "huge coordinates")
+        assert c.stats()["points_engine"] == 1
+        Xs = G.random_points(500, 8, 3, "blobs")  # the same context keeps working afterwards
+        assert_bit_equal(gpu_points(c, Xs), oracle.appd_points(Xs), "after fallback")
+        assert c.stats()["points_engine"] == 2
+
+
 def test_points_list_overflow_is_exact(P, monkeypatch):
     """A candidate list far too small for the input: rows whose entries are lost are
     poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the
