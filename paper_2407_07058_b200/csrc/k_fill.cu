@@ -279,7 +279,14 @@ appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, 
   if (grid.y > 65535u) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
   // 32-byte stores by default (measured: fewer instructions per byte); APPD_FILL_VEC=4 picks 16-byte
   static const int want = getenv("APPD_FILL_VEC") ? atoi(getenv("APPD_FILL_VEC")) : 8;
-  if (vec8 && want == 8) {
+  // small matrices: 64-row tiles when 128-row tiles would leave fewer than ~6 waves of
+  // the 4 resident CTAs per SM (the last, partial wave dominates)
+  const bool small = (int64_t)grid.x * grid.y < (int64_t)c->sm_count * 4 * 6;
+  if (vec8 && want == 8 && small) {
+    dim3 g64(grid.x, (unsigned)((nrows + 63) / 64));
+    if (widest) k_fill<8, true, 0, 64><<<g64, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+    else k_fill<8, false, 0, 64><<<g64, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  } else if (vec8 && want == 8) {
     if (widest) k_fill<8, true, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
     else k_fill<8, false, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
   } else if (vec4) {
