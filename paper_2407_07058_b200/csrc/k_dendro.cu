@@ -252,15 +252,81 @@ __device__ __forceinline__ void pj_steps(cg::grid_group& grid, int (&nx)[E], int
   }
 }
 
+// exclusive prefix sum of in[0..count) into out over the whole cooperative grid: block b
+// scans its contiguous segment, the block totals are added in order (grid barriers inside;
+// every thread of the grid must call it)
+__device__ void grid_exclusive_scan(cg::grid_group& grid, const int* in, int* out, int count, int* blocksum) {
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int Sg = (count + gridDim.x - 1) / gridDim.x;
+  const int lo_i = min(count, (int)blockIdx.x * Sg), hi_i = min(count, lo_i + Sg);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = lo_i; base < hi_i; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int f = i < hi_i ? in[i] : 0;
+    int x = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    if (i < hi_i) out[i] = carry_s + (warp ? wsum[warp - 1] : 0) + x - f;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
+  grid.sync();
+  int off = 0;
+  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
+  for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) out[i] += off;
+  grid.sync();
+}
+
 template <int E>
 __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
-                                                int n, const int* __restrict__ sarc, const int* __restrict__ start,
-                                                const int* __restrict__ end, const int* __restrict__ posarc, int root,
-                                                int2* A, int2* B, int* rkout, int* parent, int* val, int* child_of,
-                                                int2* jm, int levels, int steps) {
+                                                int n, int* sarc, int* start, int* end, int* posarc, int* deg,
+                                                int* cursor, int* blocksum, int root, int2* A, int2* B, int* rkout,
+                                                int* parent, int* val, int* child_of, int2* jm, int levels,
+                                                int steps) {
   cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
+  // adjacency (CSR by source vertex; the order inside a list is irrelevant: the rooted
+  // orientation, the only thing this tour produces, is unique)
+  for (int x = tid; x < n; x += T) {
+    deg[x] = 0;
+    cursor[x] = 0;
+  }
+  grid.sync();
+  for (int ed = tid; ed < m; ed += T) {
+    atomicAdd(deg + eu[ed], 1);
+    atomicAdd(deg + ev[ed], 1);
+  }
+  grid.sync();
+  grid_exclusive_scan(grid, deg, start, n, blocksum);
+  for (int x = tid; x < n; x += T) end[x] = start[x] + deg[x];
+  for (int a = tid; a < L; a += T) {
+    const int src = (a & 1) ? ev[a >> 1] : eu[a >> 1];
+    const int p = start[src] + atomicAdd(cursor + src, 1);
+    sarc[p] = a;
+    posarc[a] = p;
+  }
+  grid.sync();
   int nx[E], rk[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {  // Euler successors (k_euler_succ)
@@ -369,46 +435,7 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
   grid.sync();
   for (int i = tid; i < m; i += T) flag[L - 1 - rkout[2 * i]] = 1;  // k_down_flags
   grid.sync();
-  // exclusive scan of flag[0..L) into downs: block b owns [b S, (b+1) S)
-  __shared__ int wsum[32];
-  __shared__ int carry_s;
-  const int Sg = (L + gridDim.x - 1) / gridDim.x;
-  const int lo_i = min(L, (int)blockIdx.x * Sg), hi_i = min(L, lo_i + Sg);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry_s = 0;
-  __syncthreads();
-  for (int base = lo_i; base < hi_i; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int f = i < hi_i ? flag[i] : 0;
-    int x = f;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      int w = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    if (i < hi_i) downs[i] = carry_s + (warp ? wsum[warp - 1] : 0) + x - f;
-    __syncthreads();
-    if (threadIdx.x == 0) carry_s += wsum[31];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
-  grid.sync();
-  int off = 0;
-  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
-  for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) downs[i] += off;
-  grid.sync();
+  grid_exclusive_scan(grid, flag, downs, L, blocksum);
   for (int i = tid; i < m; i += T) {  // k_emit
     const int e = (int)(S[i] & lo);
     const int v = child_of[e];
@@ -488,14 +515,8 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   const int gL = std::min(c->sm_count * 8, (L + 255) / 256), gn = std::min(c->sm_count * 8, (n + 255) / 256);
   const int root = 0;
   appd_status s;
-  // A: adjacency
-  k_arcs<<<gL, 256, 0, c->stream>>>(eu, ev, m, src, arc);
-  APPD_LAUNCHED(c);
   int sh = 1;
   while ((1 << sh) < n) sh++;
-  if ((s = sort_pairs_i32_bits(c, src, ssrc, arc, sarc, L, sh))) return s;
-  k_adj<<<gL, 256, 0, c->stream>>>(ssrc, sarc, L, start, end, posarc);
-  APPD_LAUNCHED(c);
   int steps = 0;
   while ((1 << steps) < L) steps++;
   steps++;
@@ -506,9 +527,10 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   if (cE <= 4) {
     // fused cooperative tours (the separate kernels below are the fallback)
     {
+      // the adjacency (CSR) is built inside the tour: src / arc serve as degree / cursor
       int mm = m, nn = n, rt = root, lv = levels, st = steps;
-      void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &rt, &bufA, &bufB, &rk, &parent, &val,
-                      &child_of, &jm, &lv, &st};
+      void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &src, &arc, &blocksum, &rt, &bufA, &bufB,
+                      &rk, &parent, &val, &child_of, &jm, &lv, &st};
       const void* fn = cE <= 1 ? (const void*)k_tour1<1> : cE <= 2 ? (const void*)k_tour1<2> : (const void*)k_tour1<4>;
       APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, cgrid, kCoopThreads, args, 0, c->stream));
       c->launches++;
@@ -526,6 +548,12 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     }
     return APPD_OK;
   }
+  // A: adjacency
+  k_arcs<<<gL, 256, 0, c->stream>>>(eu, ev, m, src, arc);
+  APPD_LAUNCHED(c);
+  if ((s = sort_pairs_i32_bits(c, src, ssrc, arc, sarc, L, sh))) return s;
+  k_adj<<<gL, 256, 0, c->stream>>>(ssrc, sarc, L, start, end, posarc);
+  APPD_LAUNCHED(c);
   // B, C: Euler tour of the MST from the root, tour ranks
   k_euler_succ<<<gL, 256, 0, c->stream>>>(eu, ev, m, sarc, start, end, posarc, root, succ0, rank0);
   APPD_LAUNCHED(c);
