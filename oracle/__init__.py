@@ -65,6 +65,8 @@ def lib():
         L.oracle_prim_weights.argtypes = [P, I64, ctypes.c_int, P, P, P]
         L.oracle_prim_points.argtypes = [P, I64, I64, P, P, P]
         L.oracle_appd_weights.argtypes = [P, I64, ctypes.c_int, P, P]
+        L.oracle_appd_weights_f64.argtypes = [P, I64, ctypes.c_int, P, P]
+        L.oracle_prim_weights_f64.argtypes = [P, I64, ctypes.c_int, P, P, P]
         L.oracle_appd_points.argtypes = [P, I64, I64, P, P]
         L.oracle_appd_points_rows.argtypes = [P, I64, I64, I64, I64, P, P]
         L.oracle_appd_weights_rows.argtypes = [P, I64, I64, I64, P, P]
@@ -99,6 +101,28 @@ def appd_weights(W, sense: int = 1, with_stats: bool = False):
     st = Stats()
     _check(lib().oracle_appd_weights(_ptr(W), n, sense, _ptr(M), ctypes.byref(st)), "appd_weights")
     return (M, st.as_dict()) if with_stats else M
+
+
+def appd_weights_f64(W, sense: int = 1, with_stats: bool = False):
+    """NEXT-3: Algorithm 4 on a dense symmetric fp64 weight matrix, fp64 M."""
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    n = W.shape[0]
+    M = np.empty((n, n), dtype=np.float64)
+    st = Stats()
+    _check(lib().oracle_appd_weights_f64(_ptr(W), n, sense, _ptr(M), ctypes.byref(st)), "appd_weights_f64")
+    return (M, st.as_dict()) if with_stats else M
+
+
+def prim_weights_f64(W, sense: int = 1):
+    """NEXT-3: Prim on an fp64 weight matrix: (eu, ev, ew) in attachment order."""
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    n = W.shape[0]
+    m = max(n - 1, 0)
+    eu = np.empty(m, dtype=np.int32)
+    ev = np.empty(m, dtype=np.int32)
+    ew = np.empty(m, dtype=np.float64)
+    _check(lib().oracle_prim_weights_f64(_ptr(W), n, sense, _ptr(eu), _ptr(ev), _ptr(ew)), "prim_weights_f64")
+    return eu, ev, ew
 
 
 def appd_points(X, with_stats: bool = False, metric: int = 0):

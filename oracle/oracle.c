@@ -28,6 +28,8 @@
  *                                       path, n <= 9    -- checker
  *   oracle_mst_path                     max edge on the MST path -- checker
  *
+ *   oracle_appd_weights_f64 / oracle_prim_weights_f64
+ *                                       NEXT-3: the same on fp64 weights
  * Precision: the paper does not fix one; BASELINE.json fixes fp32 weights.
  * Every APPD value is a copied weight (only comparisons are made), so the
  * oracle works on the fp32 weights directly.  -0.0 is read as +0.0 (DESIGN.md
@@ -128,11 +130,15 @@ typedef struct {
   const float* W;
   const float* X;
   int64_t n, d;
-  int metric; /* points: 0 R1, 1 Manhattan, 2 Chebyshev */
+  int metric;       /* points: 0 R1, 1 Manhattan, 2 Chebyshev */
+  const double* Wd; /* NEXT-3: fp64 weight matrix ("float64"), used when W and X are NULL */
 } wsrc;
 
-static float wget(const wsrc* s, int64_t i, int64_t j) {
+/* Weights are handled as doubles: every fp32 weight converts exactly, and the method only
+ * compares and copies weights, so the fp32 results are unchanged by the wider type. */
+static double wget(const wsrc* s, int64_t i, int64_t j) {
   if (s->W) return canon(s->W[i * s->n + j]);
+  if (s->Wd) { double w = s->Wd[i * s->n + j]; return w == 0.0 ? 0.0 : w; }
   return oracle_metric_weight(s->X + i * s->d, s->X + j * s->d, s->d, s->metric);
 }
 
@@ -144,9 +150,9 @@ static float wget(const wsrc* s, int64_t i, int64_t j) {
  * For sense -1 the keys are the negated weights; the recorded weight is the
  * original one.
  * ------------------------------------------------------------------------- */
-static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
+static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, double* ew) {
   int64_t n = s->n;
-  float* key = (float*)malloc(sizeof(float) * n);
+  double* key = (double*)malloc(sizeof(double) * n);
   int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * n);
   unsigned char* done = (unsigned char*)calloc(n, 1);
   if (!key || !parent || !done) {
@@ -167,8 +173,8 @@ static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
     }
     for (int64_t u = 0; u < n; u++) {
       if (done[u]) continue;
-      float w = wget(s, v, u);
-      float k = sense > 0 ? w : -w;
+      double w = wget(s, v, u);
+      double k = sense > 0 ? w : -w;
       /* an edge of weight +inf (points whose squared distance overflows fp32) is still an
        * edge of the complete graph (reading Q14): the first tree vertex to
        * offer one becomes the parent */
@@ -179,16 +185,32 @@ static int prim(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
   return ORACLE_OK;
 }
 
+static int prim_f32(const wsrc* s, int sense, int32_t* eu, int32_t* ev, float* ew) {
+  double* w = (double*)malloc(sizeof(double) * (s->n > 1 ? s->n - 1 : 1));
+  if (!w) return ORACLE_ERR_NOMEM;
+  int rc = prim(s, sense, eu, ev, w);
+  for (int64_t e = 0; rc == ORACLE_OK && e < s->n - 1; e++) ew[e] = (float)w[e]; /* exact: copies of fp32 weights */
+  free(w);
+  return rc;
+}
+
 int oracle_prim_weights(const float* W, int64_t n, int sense, int32_t* eu, int32_t* ev, float* ew) {
   if (!W || n < 1) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0, 0};
-  return prim(&s, sense, eu, ev, ew);
+  wsrc s = {W, NULL, n, 0, 0, NULL};
+  return prim_f32(&s, sense, eu, ev, ew);
 }
 
 int oracle_prim_points(const float* X, int64_t n, int64_t d, int32_t* eu, int32_t* ev, float* ew) {
   if (!X || n < 1 || d < 1) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d, 0};
-  return prim(&s, +1, eu, ev, ew);
+  wsrc s = {NULL, X, n, d, 0, NULL};
+  return prim_f32(&s, +1, eu, ev, ew);
+}
+
+/* NEXT-3: Prim on an fp64 weight matrix. */
+int oracle_prim_weights_f64(const double* W, int64_t n, int sense, int32_t* eu, int32_t* ev, double* ew) {
+  if (!W || n < 1) return ORACLE_ERR_ARG;
+  wsrc s = {NULL, NULL, n, 0, 0, W};
+  return prim(&s, sense, eu, ev, ew);
 }
 
 /* ---------------------------------------------------------------------------
@@ -196,7 +218,7 @@ int oracle_prim_points(const float* X, int64_t n, int64_t d, int32_t* eu, int32_
  * for widest.  Ties: ascending seq, so the order is total.
  * ------------------------------------------------------------------------- */
 typedef struct {
-  float w;
+  double w;
   int32_t seq;
 } sort_item;
 
@@ -225,18 +247,19 @@ static int cmp_asc(const void* a, const void* b) {
  * an iterative DFS over the live forest.  Only rows in [r0, r0+R) are
  * stored (R5); R = n stores everything.  M is R x n, row-major.
  * ------------------------------------------------------------------------- */
-static int algo4(const wsrc* s, int sense, int64_t r0, int64_t R, float* M, oracle_stats* st) {
+/* M (fp32) or Md (fp64) receives the output; every stored value is a copied weight */
+static int algo4(const wsrc* s, int sense, int64_t r0, int64_t R, float* M, double* Md, oracle_stats* st) {
   int64_t n = s->n;
   oracle_stats local = {0, 0, 0, 0, 0};
   if (n == 1) {
-    if (R == 1) M[0] = 0.0f;
+    if (R == 1) { if (Md) Md[0] = 0.0; else M[0] = 0.0f; }
     if (st) *st = local;
     return ORACLE_OK;
   }
   int64_t m = n - 1;
   int32_t* eu = (int32_t*)malloc(sizeof(int32_t) * m);
   int32_t* ev = (int32_t*)malloc(sizeof(int32_t) * m);
-  float* ew = (float*)malloc(sizeof(float) * m);
+  double* ew = (double*)malloc(sizeof(double) * m);
   sort_item* order = (sort_item*)malloc(sizeof(sort_item) * m);
   /* forest adjacency in CSR form with a live flag per edge */
   int64_t* off = (int64_t*)calloc(n + 1, sizeof(int64_t));
@@ -274,11 +297,13 @@ static int algo4(const wsrc* s, int sense, int64_t r0, int64_t R, float* M, orac
     free(fill);
   }
   for (int64_t i = 0; i < n; i++) mark[i] = -1;
-  for (int64_t i = 0; i < R; i++) M[i * n + (r0 + i)] = 0.0f; /* diagonal: the empty path */
+  for (int64_t i = 0; i < R; i++) { /* diagonal: the empty path */
+    if (Md) Md[i * n + (r0 + i)] = 0.0; else M[i * n + (r0 + i)] = 0.0f;
+  }
 
   for (int64_t k = 0; k < m; k++) {
     int32_t e = order[k].seq;
-    float w = ew[e];
+    double w = ew[e];
     live[e] = 0; /* delete the edge from the forest */
     int32_t* trees[2] = {tree1, tree2};
     int64_t sizes[2] = {0, 0};
@@ -306,8 +331,13 @@ static int algo4(const wsrc* s, int sense, int64_t r0, int64_t R, float* M, orac
       int64_t a = tree1[x];
       for (int64_t y = 0; y < sizes[1]; y++) {
         int64_t b = tree2[y];
-        if (a >= r0 && a < r0 + R) M[(a - r0) * n + b] = w;
-        if (b >= r0 && b < r0 + R) M[(b - r0) * n + a] = w;
+        if (Md) {
+          if (a >= r0 && a < r0 + R) Md[(a - r0) * n + b] = w;
+          if (b >= r0 && b < r0 + R) Md[(b - r0) * n + a] = w;
+        } else {
+          if (a >= r0 && a < r0 + R) M[(a - r0) * n + b] = (float)w;
+          if (b >= r0 && b < r0 + R) M[(b - r0) * n + a] = (float)w;
+        }
       }
     }
     local.writes += sizes[0] * sizes[1];
@@ -326,22 +356,30 @@ out:
 /* Algorithm 4 on a weight matrix.  sense +1 minimax, -1 widest. */
 int oracle_appd_weights(const float* W, int64_t n, int sense, float* M, oracle_stats* st) {
   if (!W || !M || n < 1 || (sense != 1 && sense != -1)) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0, 0};
-  return algo4(&s, sense, 0, n, M, st);
+  wsrc s = {W, NULL, n, 0, 0, NULL};
+  return algo4(&s, sense, 0, n, M, NULL, st);
+}
+
+/* NEXT-3: Algorithm 4 on an fp64 weight matrix ("float64"), fp64 output.  The
+ * method only compares and copies weights, so it is the same procedure in the wider type. */
+int oracle_appd_weights_f64(const double* W, int64_t n, int sense, double* M, oracle_stats* st) {
+  if (!W || !M || n < 1 || (sense != 1 && sense != -1)) return ORACLE_ERR_ARG;
+  wsrc s = {NULL, NULL, n, 0, 0, W};
+  return algo4(&s, sense, 0, n, NULL, M, st);
 }
 
 /* Algorithm 4 on points (complete graph of R1 weights). */
 int oracle_appd_points(const float* X, int64_t n, int64_t d, float* M, oracle_stats* st) {
   if (!X || !M || n < 1 || d < 1) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d, 0};
-  return algo4(&s, +1, 0, n, M, st);
+  wsrc s = {NULL, X, n, d, 0, NULL};
+  return algo4(&s, +1, 0, n, M, NULL, st);
 }
 
 /* Algorithm 4 on points under a pluggable metric (NEXT-3). */
 int oracle_appd_points_metric(const float* X, int64_t n, int64_t d, int metric, float* M, oracle_stats* st) {
   if (!X || !M || n < 1 || d < 1 || metric < 0 || metric > 2) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d, metric};
-  return algo4(&s, +1, 0, n, M, st);
+  wsrc s = {NULL, X, n, d, metric, NULL};
+  return algo4(&s, +1, 0, n, M, NULL, st);
 }
 
 /* Row block [r0, r0+R) of the metric weight matrix, row-major R x n. */
@@ -356,14 +394,14 @@ void oracle_points_weights_metric(const float* X, int64_t n, int64_t d, int metr
 int oracle_appd_points_rows(const float* X, int64_t n, int64_t d, int64_t r0, int64_t R, float* M,
                             oracle_stats* st) {
   if (!X || !M || n < 1 || d < 1 || r0 < 0 || R < 1 || r0 + R > n) return ORACLE_ERR_ARG;
-  wsrc s = {NULL, X, n, d, 0};
-  return algo4(&s, +1, r0, R, M, st);
+  wsrc s = {NULL, X, n, d, 0, NULL};
+  return algo4(&s, +1, r0, R, M, NULL, st);
 }
 
 int oracle_appd_weights_rows(const float* W, int64_t n, int64_t r0, int64_t R, float* M, oracle_stats* st) {
   if (!W || !M || n < 1 || r0 < 0 || R < 1 || r0 + R > n) return ORACLE_ERR_ARG;
-  wsrc s = {W, NULL, n, 0, 0};
-  return algo4(&s, +1, r0, R, M, st);
+  wsrc s = {W, NULL, n, 0, 0, NULL};
+  return algo4(&s, +1, r0, R, M, NULL, st);
 }
 
 /* ---------------------------------------------------------------------------
@@ -438,8 +476,8 @@ int oracle_mst_path(const float* W, int64_t n, float* M) {
   int rc = ORACLE_OK;
   if (!eu || !ev || !ew || !off || !adj_v || !adj_w || !stack || !from) { rc = ORACLE_ERR_NOMEM; goto out; }
   {
-    wsrc s = {W, NULL, n, 0, 0};
-    rc = prim(&s, +1, eu, ev, ew);
+    wsrc s = {W, NULL, n, 0, 0, NULL};
+    rc = prim_f32(&s, +1, eu, ev, ew);
     if (rc) goto out;
   }
   for (int64_t e = 0; e < m; e++) { off[eu[e] + 1]++; off[ev[e] + 1]++; }

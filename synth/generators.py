@@ -276,6 +276,36 @@ def random_weights(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
     return W
 
 
+def random_weights_f64(n: int, seed: int, kind: str = "uniform") -> np.ndarray:
+    """Symmetric fp64 weight matrix with +0 diagonal (NEXT-3, S:L77 fp64 weights).
+
+    kinds: uniform (u53 on [0, 1)), fine_ties (1 + k 2^-40 with k in 0..7: distinct in
+    fp64, all one value in fp32, with ties), negative (integers -3..3 plus k 2^-45),
+    signed_zero (values in {-0, +0, 1, 1 + 2^-50}), huge (magnitudes 1e-300 .. 1e300).
+    """
+    rng = SplitMix64(1000033 * seed + 29)
+    W = np.zeros((n, n), dtype=np.float64)
+    for i in range(n - 1):
+        c = n - 1 - i
+        if kind == "uniform":
+            row = rng.u53(c)
+        elif kind == "fine_ties":
+            row = 1.0 + rng.bounded(8, c).astype(np.float64) * 2.0 ** -40
+        elif kind == "negative":
+            row = (rng.bounded(7, c).astype(np.float64) - 3.0) + rng.bounded(3, c).astype(np.float64) * 2.0 ** -45
+        elif kind == "signed_zero":
+            row = np.array([0.0, 0.0, 1.0, 1.0 + 2.0 ** -50])[rng.bounded(4, c)]
+        elif kind == "huge":
+            row = 10.0 ** (rng.u53(c) * 600.0 - 300.0)
+        else:
+            raise KeyError(kind)
+        W[i, i + 1:] = row
+    W += W.T
+    if kind == "signed_zero":
+        W[W == 0] = -0.0  # -0 both triangles (symmetric bitwise), diagonal too
+    return W
+
+
 def random_points(n: int, d: int, seed: int, kind: str = "uniform") -> np.ndarray:
     """n x d fp32 points.
 

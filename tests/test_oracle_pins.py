@@ -468,3 +468,56 @@ def test_overflowing_distances_are_infinite_edges():
     assert np.isinf(M[:60, 60:]).all() and np.isinf(M[60:, :60]).all()
     off = ~np.eye(60, dtype=bool)
     assert np.isinf(M[60:, 60:][off]).all() and (bits(np.diag(M)) == 0).all()
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: fp64 weights.  Pinned to an independent algorithm written here (the
+# minimax / widest closure of Floyd-Warshall, P:L44 / S:L235, in numpy float64), to a
+# three-vertex case whose answer is fixed by Eq. 1-2 by hand, and to the pinned fp32
+# oracle on fp32-representable inputs.
+# --------------------------------------------------------------------------
+def floyd_closure_f64(W, sense):
+    M = np.where(W == 0, 0.0, W).astype(np.float64)
+    n = M.shape[0]
+    for k in range(n):
+        via = np.maximum(M[:, k:k + 1], M[k:k + 1, :]) if sense > 0 else np.minimum(M[:, k:k + 1], M[k:k + 1, :])
+        M = np.minimum(M, via) if sense > 0 else np.maximum(M, via)
+    np.fill_diagonal(M, 0.0)
+    return M
+
+
+def assert_f64_bit_equal(a, b):
+    a = np.asarray(a, np.float64) + 0.0  # canonical +0 (reading Q5)
+    b = np.asarray(b, np.float64) + 0.0
+    assert a.shape == b.shape
+    bad = np.nonzero(a.view(np.uint64) != b.view(np.uint64))
+    assert bad[0].size == 0, f"{bad[0].size} mismatches, first at {bad[0][0]},{bad[1][0]}: {a[bad[0][0], bad[1][0]]!r} vs {b[bad[0][0], bad[1][0]]!r}"
+
+
+@pytest.mark.parametrize("kind", ["uniform", "fine_ties", "negative", "signed_zero", "huge"])
+@pytest.mark.parametrize("sense", [1, -1])
+def test_f64_equals_floyd_closure(kind, sense):
+    for seed in range(4):
+        W = G.random_weights_f64(37 + 5 * seed, seed, kind)
+        assert_f64_bit_equal(oracle.appd_weights_f64(W, sense), floyd_closure_f64(W, sense))
+
+
+def test_f64_three_vertex_by_hand():
+    # Eq. 1-2: the path 0-2-1 has max edge 1 + 2^-41 < 1 + 2^-40 = w01, so d(0,1) = 1 + 2^-41;
+    # in fp32 every weight here rounds to 1.0 (a plausible truncation would give 1.0)
+    a, b = 1.0 + 2.0 ** -40, 1.0 + 2.0 ** -41
+    W = np.array([[0, a, b], [a, 0, 1.0], [b, 1.0, 0]], np.float64)
+    M = oracle.appd_weights_f64(W, 1)
+    assert M[0, 1] == b and M[1, 0] == b and M[0, 2] == b and M[1, 2] == 1.0
+    Mw = oracle.appd_weights_f64(W, -1)  # widest: best bottleneck between 0 and 1 is the edge itself
+    assert Mw[0, 1] == a and Mw[1, 2] == b and Mw[0, 2] == b
+    eu, ev, ew = oracle.prim_weights_f64(W, 1)
+    assert sorted(ew.tolist()) == [1.0, b]
+
+
+@pytest.mark.parametrize("kind", REGIMES)
+def test_f64_equals_f32_on_representable_inputs(kind):
+    W = G.random_weights(48, 7, kind)
+    M32 = oracle.appd_weights(W, 1)
+    M64 = oracle.appd_weights_f64(W.astype(np.float64), 1)
+    assert_f64_bit_equal(M64, M32.astype(np.float64))
