@@ -164,6 +164,16 @@ appd_status appd_solve_weights_host(appd_ctx* ctx, const float* W_host, int64_t 
 appd_status appd_solve_points_stream(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host,
                                      int64_t block_rows);
 
+/* NEXT-3 ("float64" weights): appd_solve_weights on an fp64 weight
+ * matrix.  W: DEVICE n x n fp64 row-major; M: DEVICE n x n fp64, distinct from W.  The
+ * method only compares and copies weights, so every M entry is bit-identical to
+ * a W entry (or +0 on the diagonal) and to the fp64 oracle.  Same validation (finite, +-0
+ * diagonal, symmetric after -0 -> +0; first offender by row-major index) and errors as
+ * appd_solve_weights; opt.sense -1 gives the widest-path APPD.  One rank only (world > 1:
+ * APPD_ERR_UNSUPPORTED); no candidate cache (every round rescans W); n <= 92682.
+ * appd_get_dendrogram is not available after this call (APPD_ERR_INVALID_ARGUMENT). */
+appd_status appd_solve_weights_f64(appd_ctx* ctx, const double* W, int64_t n, double* M);
+
 /* NEXT-2: the paper's comparison algorithm, the minimax variant of
  * Floyd–Warshall ("a modified version of the Floyd-Warshall algorithm", Fig. floyd
  * k outermost, M[i][j] = min(M[i][j], max(M[i][k], M[k][j])); O(n^3)),

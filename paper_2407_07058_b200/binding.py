@@ -96,7 +96,7 @@ class appd_stats(ctypes.Structure):
 
 EXPORTS = [
     "appd_options_init", "appd_create", "appd_set_stream", "appd_solve_weights", "appd_solve_points",
-    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_solve_points_stream", "appd_destroy", "appd_row_range", "appd_row_range_of",
+    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_solve_points_stream", "appd_solve_weights_f64", "appd_destroy", "appd_row_range", "appd_row_range_of",
     "appd_points_weights", "appd_get_nccl_unique_id", "appd_get_stats", "appd_last_dendrogram",
     "appd_error_index", "appd_last_error", "appd_status_string", "appd_version",
 ]
@@ -122,6 +122,7 @@ def load(path: str = LIB_PATH):
     L.appd_solve_points_host.argtypes = [P, P, I64, I64, P]
     L.appd_solve_weights_host.argtypes = [P, P, I64, P]
     L.appd_floyd_weights.argtypes = [P, P, I64, P]
+    L.appd_solve_weights_f64.argtypes = [P, P, I64, P]
     L.appd_solve_points_stream.argtypes = [P, P, I64, I64, P, I64]
     L.appd_destroy.restype = None
     L.appd_destroy.argtypes = [P]
@@ -161,8 +162,9 @@ def _check_tensor(t, name, dtype_name="float32"):
 
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32 (got {t.dtype})")
+    want = getattr(torch, dtype_name)
+    if t.dtype != want:
+        raise TypeError(f"{name} must be {dtype_name} (got {t.dtype})")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
 
@@ -276,6 +278,22 @@ class Context:
         s = self._L.appd_floyd_weights(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_floyd_weights")
+        return M
+
+    def solve_weights_f64(self, W, M=None):
+        """appd_solve_weights_f64 (NEXT-3): W and M are n x n float64 CUDA tensors (one rank)."""
+        import torch
+
+        _check_tensor(W, "W", "float64")
+        n = W.shape[-1]
+        if M is None:
+            M = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{self.device}")
+        _check_tensor(M, "M", "float64")
+        if M.numel() != n * n:
+            raise ValueError(f"M must hold {n} x {n} doubles")
+        s = self._L.appd_solve_weights_f64(self._h, _ptr(W), n, _ptr(M))
+        if s != APPD_OK:
+            self._raise(s, "appd_solve_weights_f64")
         return M
 
     def solve_points_stream(self, X, M, block_rows=0):

@@ -304,6 +304,7 @@ static appd_status report_validation(appd_ctx* c, const u64 bad[3], int64_t n, b
 // The whole pipeline.  X (points) or W (weights) is a device pointer.
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
+  const bool f64 = c->f64_W != nullptr;  // NEXT-3 (k_f64.cu): W and M are c->f64_W / c->f64_M
   const int sense = points ? 1 : c->opt.sense;
   int64_t row0, rows;
   appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
@@ -333,7 +334,9 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
     if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
     APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
-    appd_status s = points ? launch_validate_points(c, X, n, d, bad) : launch_validate_weights(c, W, n, row0, rows, bad);
+    appd_status s = points ? launch_validate_points(c, X, n, d, bad)
+                    : f64  ? launch_validate_weights_f64(c, c->f64_W, n, bad)
+                           : launch_validate_weights(c, W, n, row0, rows, bad);
     if (s) return s;
     APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
   }
@@ -360,7 +363,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       APPD_CUDA(c, cudaStreamSynchronize(c->stream));
       c->stream_out[0] = 0.0f;
     } else if (rows > 0) {
-      appd_status s = launch_set_diag_zero_single(c, M);
+      appd_status s = f64 ? launch_set_diag_zero_single_f64(c, c->f64_M) : launch_set_diag_zero_single(c, M);
       if (s) return s;
     }
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -438,7 +441,15 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   int rounds = 0;
   int* hostk = reinterpret_cast<int*>(c->pinned_small + 24);  // pinned: the copies stay asynchronous
   // weights mode: round-0 candidate cache (exact per-row top-K of W)
-  const int wtopk = points ? 0 : (c->opt.topk == 0 ? 8 : (c->opt.topk < 0 ? 0 : c->opt.topk));
+  const int wtopk = (points || f64) ? 0 : (c->opt.topk == 0 ? 8 : (c->opt.topk < 0 ? 0 : c->opt.topk));
+  u64 *f64_compw = nullptr, *f64_roww = nullptr;
+  int* f64_rowj = nullptr;
+  if (f64) {
+    f64_compw = (u64*)ws(c, S_F64_A, sizeof(u64) * 2 * n);
+    f64_roww = f64_compw ? f64_compw + n : nullptr;
+    f64_rowj = (int*)ws(c, S_F64_B, sizeof(int) * n);
+    if (!f64_compw || !f64_rowj) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fp64 round workspace");
+  }
   if (wtopk && wtopk != 4 && wtopk != 8 && wtopk != 16 && wtopk != 32)
     return fail(c, APPD_ERR_INVALID_ARGUMENT, "topk = %d (0, -1, 4, 8, 16 or 32)", c->opt.topk);
   u64* w_ckey = nullptr;
@@ -558,6 +569,8 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     } else if (points) {
       s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
       c->stats.exact_rounds++;
+    } else if (f64) {
+      s = launch_scan_weights_f64(c, c->f64_W, n, k, rounds == 0, sense, comp, f64_compw, f64_roww, f64_rowj, compbest);
     } else if (wtopk && rounds == 0) {
       s = launch_scan_weights_topk(c, W, n, row0, rows, wtopk, sense, w_ckey, w_cj, w_ccnt, compbest);
     } else if (wtopk) {
@@ -703,17 +716,28 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // ---- a4: sort the MST edge keys ascending (Kruskal order = P:L98's descending removal reversed) ----
   // only the weight bits decide the order: ties in any order are a valid Kruskal order
   // (SURVEY App. A.5), and the radix passes over the pair index would be wasted
-  if ((s = sort_keys_u64_bits64(c, mstkeys, sorted, n - 1, ks.shift, 64))) return s;
-  stage_event(c, 3);
-
-  // ---- a5: dendrogram (v1: host union-find with list concatenation) ----
-  // the GPU decodes the sorted keys to (u, v, w); pinned buffers keep the copies async
   const int64_t m = n - 1;
+  double* hw = nullptr;  // fp64: weight of each rank (k_f64.cu)
   int32_t* d_eu = (int32_t*)ws(c, S_EDGES, (sizeof(int32_t) * 2 + sizeof(float)) * m + 64);
   if (!d_eu) return fail(c, APPD_ERR_OUT_OF_MEMORY, "edge workspace");
   int32_t* d_ev = d_eu + m;
   float* d_ew = (float*)(d_ev + m);
-  if ((s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
+  if (f64) {
+    // the keys hold pair indices only: sort by the fp64 weights, relabel by rank
+    hw = (double*)ws(c, S_F64_HW, sizeof(double) * (m + 1));
+    u64* wk = (u64*)ws(c, S_F64_A, sizeof(u64) * 2 * n);
+    int* ix = (int*)ws(c, S_F64_B, sizeof(int) * 2 * n);
+    if (!hw || !wk || !ix) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fp64 edge workspace");
+    if ((s = launch_edges_f64(c, mstkeys, m, c->f64_W, n, sense, wk, wk + n, ix, ix + n, d_eu, d_ev, d_ew, hw)))
+      return s;
+  } else if ((s = sort_keys_u64_bits64(c, mstkeys, sorted, n - 1, ks.shift, 64))) {
+    return s;
+  }
+  stage_event(c, 3);
+
+  // ---- a5: dendrogram (v1: host union-find with list concatenation) ----
+  // the GPU decodes the sorted keys to (u, v, w); pinned buffers keep the copies async
+  if (!f64 && (s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
   int levels = 1;
   while ((1ll << levels) <= m) levels++;
   const int64_t stride = m;
@@ -747,12 +771,14 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(pi, h_pi, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(ST, h_h, sizeof(float) * m, cudaMemcpyHostToDevice, c->stream));
   }
-  c->have_dendrogram = true;
+  c->have_dendrogram = !f64;  // fp64: the device h holds ranks, not weights
   stage_event(c, 4);
 
   // ---- a6: fill prep ----
   if ((s = launch_positions(c, pi, n, pos))) return s;
-  if ((s = launch_sparse_table(c, ST, m, levels, stride, sense < 0))) return s;
+  // fp64: ranks increase along the Kruskal order in either sense, so the max-combination
+  const bool widest_fill = sense < 0 && !f64;
+  if ((s = launch_sparse_table(c, ST, m, levels, stride, widest_fill))) return s;
   const int* rows_sorted = pi;
   int* rowpos = (int*)ws(c, S_ROWPOS, sizeof(int) * n);
   if (!rowpos) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
@@ -832,7 +858,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   stage_event(c, 5);
 
   // ---- a7: fill ----
-  if ((s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, stride, n, M, row0, sense < 0))) return s;
+  if (f64) {
+    if ((s = launch_fill_f64(c, rows_sorted, rowpos, rows, pos, ST, stride, n, c->f64_M, row0, hw))) return s;
+  } else if ((s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, stride, n, M, row0, sense < 0))) {
+    return s;
+  }
   stage_event(c, 6);
   APPD_CUDA(c, cudaStreamSynchronize(c->stream));
   if (cm_status_pending && c->pinned_small[48] == 1) {
@@ -854,7 +884,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
     cudaGetLastError();
   }
-  c->stats.fill_bytes = rows * n * 4;
+  c->stats.fill_bytes = rows * n * (f64 ? 8 : 4);
   c->stats.kernel_launches = c->launches;
   if (c->opt.timing) {
     c->stats.ms_validate = ev_ms(c, 0, 1);
@@ -883,6 +913,27 @@ extern "C" appd_status appd_solve_weights(appd_ctx* c, const float* W, int64_t n
   if ((s = check_device_ptr(c, W, "W"))) return s;
   if ((s = check_device_ptr(c, M, "M"))) return s;
   return solve(c, W, nullptr, n, 0, M);
+}
+
+// NEXT-3: fp64 weight matrix, fp64 output (k_f64.cu).  One rank; no streaming.
+extern "C" appd_status appd_solve_weights_f64(appd_ctx* c, const double* W, int64_t n, double* M) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
+  if (n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682 (32-bit pair index)");
+  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_weights_f64 runs on one rank (world = %d)", c->opt.world);
+  if ((s = check_device_ptr(c, W, "W"))) return s;
+  if ((s = check_device_ptr(c, M, "M"))) return s;
+  if ((const void*)W == (const void*)M) return fail(c, APPD_ERR_INVALID_ARGUMENT, "W and M must not alias");
+  c->f64_W = W;
+  c->f64_M = M;
+  float* saved = c->stream_out;
+  c->stream_out = nullptr;
+  s = solve(c, nullptr, nullptr, n, 0, nullptr);
+  c->stream_out = saved;
+  c->f64_W = nullptr;
+  c->f64_M = nullptr;
+  return s;
 }
 
 // NEXT-2: the paper's comparison algorithm (minimax Floyd–Warshall) on

@@ -85,6 +85,9 @@ struct NcclApi;  // nccl_shim.cpp
 
 struct appd_ctx {
   appd_options opt;
+  // NEXT-3: set for the duration of appd_solve_weights_f64 (k_f64.cu)
+  const double* f64_W = nullptr;
+  double* f64_M = nullptr;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -132,7 +135,7 @@ enum Slot {
   S_TC_CSTART, S_TC_CEND, S_TC_RS, S_TC_RE, S_TC_UB, S_TC_CAND, S_TC_CNT, S_TC_RECV, S_TC_RECC, S_TC_FALLBACK,
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
-  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE,
+  S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE, S_F64_A, S_F64_B, S_F64_HW,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
@@ -292,6 +295,15 @@ appd_status launch_positions(appd_ctx* c, const int* pi, int64_t n, int* pos);
 appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, int64_t stride, int widest);
 appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
                         const float* ST, int64_t stride, int64_t n, float* M, int64_t row0, int widest);
+appd_status launch_fill_f64(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
+                            const float* ST, int64_t stride, int64_t n, double* M, int64_t row0, const double* hw);
+appd_status launch_validate_weights_f64(appd_ctx* c, const double* W, int64_t n, u64* out3);
+appd_status launch_scan_weights_f64(appd_ctx* c, const double* W, int64_t n, int64_t k, bool round0, int sense,
+                                    const int* comp, u64* compw, u64* roww, int* rowj, u64* compbest);
+appd_status launch_edges_f64(appd_ctx* c, const u64* mstkeys, int64_t m, const double* W, int64_t n, int sense,
+                             u64* wkey, u64* wkey_sorted, int* idx, int* idx_sorted, int32_t* eu, int32_t* ev,
+                             float* ew, double* hw);
+appd_status launch_set_diag_zero_single_f64(appd_ctx* c, double* M);
 appd_status launch_sqrt_inplace(appd_ctx* c, float* h, int64_t m);
 appd_status launch_set_diag_zero_single(appd_ctx* c, float* M);
 appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t row0, int64_t rows,

@@ -166,13 +166,17 @@ __device__ __forceinline__ void fill_store4(float* dst, float4 v) {
   else *reinterpret_cast<float4*>(dst) = v;
 }
 
-template <int VEC, bool WIDEST, int STORE = 0, int RT = FILL_R>
+// OT = double (NEXT-3, k_f64.cu): the values are ranks r + 1 of the fp64 MST weights and
+// the store maps each through hw[r + 1] (hw[0] = +0 for the diagonal)
+template <int VEC, bool WIDEST, int STORE = 0, int RT = FILL_R, typename OT = float>
 __global__ void __launch_bounds__(FILL_THREADS)
     k_fill(const int* __restrict__ rows_sorted, const int* __restrict__ rowpos, int64_t nrows,
            const int* __restrict__ pos, const float* __restrict__ ST, int64_t stride, int64_t n,
-           float* __restrict__ M, int64_t row0) {
+           OT* __restrict__ M, int64_t row0, const double* __restrict__ hw = nullptr) {
   __shared__ float2 sSP[FILL_R];   // (S, P) of each row: one 8-byte broadcast load per row
-  __shared__ float* sPtr[FILL_R];  // the row's first element in M
+  __shared__ OT* sPtr[FILL_R];     // the row's first element in M
+  constexpr bool F64 = sizeof(OT) == 8;
+  __shared__ double2 sSPd[F64 ? FILL_R : 1];  // fp64: the weights of S and P
   __shared__ int sA[FILL_R];
   // sparse table of h over the tile's position range [aL, aR): columns whose position
   // lies inside it (the tile's own points, and other ranks' in between) need a direct
@@ -188,6 +192,7 @@ __global__ void __launch_bounds__(FILL_THREADS)
     sA[t] = at;
     sPtr[t] = M + ((int64_t)rows_sorted[t0 + t] - row0) * n;
     sSP[t] = make_float2((at < aR) ? rmq<WIDEST>(ST, stride, at, aR) : ID, (at > aL) ? rmq<WIDEST>(ST, stride, aL, at) : ID);
+    if constexpr (F64) sSPd[t] = make_double2(__ldg(hw + (int)fmaxf(sSP[t].x, 0.0f)), __ldg(hw + (int)fmaxf(sSP[t].y, 0.0f)));
   }
   // this thread's VEC columns
   const int64_t jbase = (int64_t)blockIdx.x * (FILL_THREADS * VEC) + (int64_t)threadIdx.x * VEC;
@@ -205,6 +210,13 @@ __global__ void __launch_bounds__(FILL_THREADS)
     else { side[q] = 2; base[q] = ID; any_inside = true; }
   }
   const bool warp_inside = __any_sync(0xffffffffu, any_inside);
+  // fp64: each value is S, P or base (or an inside range maximum): the rank comparison
+  // picks which, so only the per-column weights are looked up, once
+  double based[F64 ? VEC : 1];
+  if constexpr (F64) {
+#pragma unroll
+    for (int q = 0; q < VEC; q++) based[q] = side[q] == 2 ? 0.0 : __ldg(hw + (int)fmaxf(base[q], 0.0f));
+  }
   // predicate-free selection per row: v = comb(comb'(S, cS), comb'(P, cP), base) with
   // cS = +-inf (pass S / block it) by side, so no per-column predicates stay live
   const float PASS = WIDEST ? -INFINITY : INFINITY;  // comb'(x, PASS) = x
@@ -253,20 +265,59 @@ __global__ void __launch_bounds__(FILL_THREADS)
         }
       }
     }
-    float* dst = sPtr[t] + jbase;
-    if (VEC == 8) {  // one 32-byte streaming store (st.global.cs.v8.f32, sm_100)
+    OT* dst = sPtr[t] + jbase;
+    if constexpr (sizeof(OT) == 8) {
+      double o[VEC];
+      const double2 SPd = sSPd[t];
+#pragma unroll
+      for (int q = 0; q < VEC; q++) {
+        if (side[q] == 2) o[q] = __ldg(hw + (int)fmaxf(v[q], 0.0f));
+        else o[q] = v[q] == base[q] ? based[q] : (side[q] == 0 ? SPd.x : SPd.y);
+      }
+      if (VEC % 4 == 0 && in_range && jbase + VEC <= n) {  // whole 32-byte sectors per store (st.global.cs.v4.f64)
+#pragma unroll
+        for (int q = 0; q < VEC; q += 4)
+          asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + q), "d"(o[q]), "d"(o[q + 1]),
+                       "d"(o[q + 2]), "d"(o[q + 3])
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int q = 0; q < VEC; q++)
+          if (jbase + q < n) __stcs(reinterpret_cast<double*>(dst) + q, o[q]);
+      }
+    } else if (VEC == 8) {  // one 32-byte streaming store (st.global.cs.v8.f32, sm_100)
       if (in_range)
         asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
                      "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                      : "memory");
     } else if (VEC == 4) {
-      if (in_range) fill_store4<STORE>(dst, make_float4(v[0], v[1], v[2], v[3]));
+      if (in_range) fill_store4<STORE>(reinterpret_cast<float*>(dst), make_float4(v[0], v[1], v[2], v[3]));
     } else {
 #pragma unroll
       for (int q = 0; q < VEC; q++)
-        if (jbase + q < n) __stcs(dst + q, v[q]);
+        if (jbase + q < n) __stcs(reinterpret_cast<float*>(dst) + q, v[q]);
     }
   }
+}
+
+// NEXT-3: fp64 output of rank-valued h (minimax sense on ranks, see k_f64.cu)
+appd_status launch_fill_f64(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
+                            const float* ST, int64_t stride, int64_t n, double* M, int64_t row0, const double* hw) {
+  if (nrows <= 0) return APPD_OK;
+  const bool even = (n % 4) == 0 && ((uintptr_t)M % 32) == 0;
+  if (even) {
+    // 64-row tiles (measured at n = 16384: 0.50 ms against 0.55 ms with 128-row tiles)
+    dim3 g((unsigned)((n + FILL_THREADS * 8 - 1) / (FILL_THREADS * 8)), (unsigned)((nrows + 63) / 64));
+    k_fill<8, false, 0, 64, double><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n,
+                                                                       M, row0, hw);
+  } else {
+    dim3 g((unsigned)((n + FILL_THREADS - 1) / FILL_THREADS), (unsigned)((nrows + 63) / 64));
+    k_fill<1, false, 0, 64, double><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n,
+                                                                       M, row0, hw);
+  }
+  APPD_LAUNCHED(c);
+  c->stats.fill_launches++;
+  return APPD_OK;
 }
 
 appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,

@@ -502,3 +502,65 @@ def test_dendrogram_hook_is_a_leaf_order(ctx):
             run = max(run, h[b - 1])
             assert Mo[pi[a], pi[b]] == run
     assert_bit_equal(M, Mo)
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: fp64 weights (k_f64.cu) against the fp64 oracle, bit-exact
+# --------------------------------------------------------------------------
+def gpu_weights_f64(c, W):
+    Wt = torch.from_numpy(np.ascontiguousarray(W, np.float64)).cuda()
+    return c.solve_weights_f64(Wt).cpu().numpy()
+
+
+def assert_f64_bit_equal(got, want, what=""):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64) + 0.0
+    assert got.shape == want.shape, (got.shape, want.shape)
+    bad = np.nonzero(got.view(np.uint64) != want.view(np.uint64))
+    if bad[0].size:
+        idx = tuple(b[0] for b in bad)
+        raise AssertionError(f"{what}: {bad[0].size} mismatching entries, first {idx}: gpu {got[idx]!r} oracle {want[idx]!r}")
+
+
+@pytest.mark.parametrize("kind", ["uniform", "fine_ties", "negative", "signed_zero", "huge"])
+def test_f64_weights_against_oracle(P, kind):
+    """Ragged sizes (odd n takes the scalar fill), both senses, values that collide in fp32."""
+    for sense in (1, -1):
+        with P.Context(sense=sense) as c:
+            for t, n in enumerate([1, 2, 3, 5, 31, 64, 127, 300, 513, 1000]):
+                W = G.random_weights_f64(n, 900 + t, kind)
+                assert_f64_bit_equal(gpu_weights_f64(c, W), oracle.appd_weights_f64(W, sense), f"f64 {kind} sense {sense} n={n}")
+
+
+def test_f64_fine_ties_n4096(ctx):
+    W = G.random_weights_f64(4096, 77, "fine_ties")
+    assert_f64_bit_equal(gpu_weights_f64(ctx, W), oracle.appd_weights_f64(W, 1), "f64 fine_ties n=4096")
+
+
+def test_f64_equals_f32_path_on_c3(ctx):
+    """The C3 recipe at full size (n = 16384, heavy ties) in fp64: the result equals the fp32
+    path's, widened (the method copies weights), compared on the device."""
+    W = torch.from_numpy(G.config("C3")).cuda()
+    M32 = ctx.solve_weights(W)
+    M64 = ctx.solve_weights_f64(W.double())
+    assert bool((M64 == M32.double()).all()) and not bool(torch.signbit(M64).any())
+    st = ctx.stats()
+    assert st["fill_bytes"] == 16384 * 16384 * 8
+
+
+def test_f64_validation(ctx, P):
+    W = G.random_weights_f64(70, 3, "uniform")
+    W2 = W.copy(); W2[3, 7] = W2[3, 7] + 2.0 ** -50  # asymmetric beyond fp32 precision
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights_f64(ctx, W2)
+    assert e.value.name == "APPD_ERR_NOT_SYMMETRIC" and e.value.index == (3, 7)
+    W3 = W.copy(); W3[40, 40] = 1e-300
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights_f64(ctx, W3)
+    assert e.value.name == "APPD_ERR_BAD_DIAGONAL" and e.value.index == (40, 40)
+    W4 = W.copy(); W4[50, 2] = np.inf; W4[2, 50] = np.inf
+    with pytest.raises(P.AppdError) as e:
+        gpu_weights_f64(ctx, W4)
+    assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (2, 50)
+    with pytest.raises(TypeError):
+        ctx.solve_weights_f64(torch.zeros((4, 4), dtype=torch.float32, device="cuda"))
