@@ -182,7 +182,12 @@ def run_native(args):
     A, c = load_input(args.workload)
     n = c["n"]
     points = c["mode"] == "points"
-    stream = torch.cuda.current_stream()
+    # one explicit stream for torch (L2 flush, events, copies) and the library: the legacy
+    # default stream's handle is 0, which the library would replace by a private stream,
+    # leaving the flush unordered with the solve
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     ctx = P.Context(device=local, stream=stream.cuda_stream, rank=rank, world=world, nccl_id=nccl_id, timing=True,
                     metric=args.metric)
     row0, rows = ctx.row_range(n)

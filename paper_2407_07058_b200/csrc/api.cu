@@ -271,6 +271,8 @@ static inline void stage_event(appd_ctx* c, int idx) {
   if (c->opt.timing) cudaEventRecord(c->ev[idx], c->stream);
 }
 
+
+
 static float ev_ms(appd_ctx* c, int a, int b) {
   float ms = 0.0f;
   if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
@@ -319,6 +321,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   c->have_dendrogram = false;
   c->err_i = c->err_j = -1;
   c->last_error.clear();
+  host_mark("solve entry", true);
   stage_event(c, 0);
 
   // ---- a1: validation ----
@@ -357,6 +360,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if ((s = report_validation(c, hb, n, points, d))) return s;
   }
   stage_event(c, 1);
+  host_mark("validation queued");
 
   if (n == 1) {
     if (c->stream_out) {
@@ -403,6 +407,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   bool use_tc = false;
   if (points && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
+    host_mark("tcf_prepare queued");
     if (s == APPD_OK) {
       use_tc = true;
     } else {
@@ -591,6 +596,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (s) return s;
     c->stats.scan_launches += c->launches - l0;
     if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
+    host_mark("round scan queued");
     if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
     // the next round's cache lookup rides on this round's synchronisation (labels are
     // final): one rank, fused into the cooperative contraction when it can run
@@ -648,7 +654,9 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
+    host_mark("round queued, synchronising");
     APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    host_mark("round synchronised");
     if (check_first_sync) {
       check_first_sync = false;
       if (defer_validation) {  // the input verdict, queued before the engine started

@@ -3,6 +3,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdint.h>
 #include <string.h>
 
@@ -125,6 +128,16 @@ struct appd_ctx {
 };
 
 namespace appd {
+
+// APPD_DEBUG_HOST=1: host-side microseconds since the solve started, at marked points
+inline void host_mark(const char* what, bool reset = false) {
+  static const bool on = getenv("APPD_DEBUG_HOST") != nullptr;
+  static std::chrono::steady_clock::time_point t0;
+  if (!on) return;
+  const auto now = std::chrono::steady_clock::now();
+  if (reset) t0 = now;
+  fprintf(stderr, "[host] %8.1f us  %s\n", std::chrono::duration<double, std::micro>(now - t0).count(), what);
+}
 
 // workspace slots
 enum Slot {

@@ -822,6 +822,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   // round 0 of the cache: the permutation is the identity, so the transpose is the
   // original-order one the exact row kernel reads
   if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp))) return s;
+  host_mark("tcf_round: pack queued");
   APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));  // ~3.4e38
   APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
   APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
@@ -855,6 +856,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     }
     if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
     if ((s = launch_tcf_scan(c, 1, P))) return s;
+  host_mark("tcf_round: tc scan r0 queued");
     if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
     st->scanned = true;
     if (p_end > p_begin) {
@@ -865,7 +867,9 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
                                 st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
         return s;
+      host_mark("tcf_round: topk scan queued");
       if ((s = exact_list(c, st, X, 0, nullptr, st->counters + 6, 0, nullptr))) return s;
+  host_mark("tcf_round: exact_list queued");
       if ((s = launch_topk_select(c, p_begin, p_end, (int)n, st->topk, st->cand_cnt, st->cand, st->cap, st->ckey,
                                   st->cj, st->ccnt, compbest, st->fallback, st->counters + 0)))
         return s;
