@@ -151,7 +151,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * T / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.workload, "n": n_s, "d": c.get("d", 0), "mode": c["mode"]},
+        # the same workload as the CUDA arm's line; each step is the bounded sample below
+        "config": {"workload": args.workload, "desc": c["desc"], "n": c["n"], "d": c.get("d", 0), "mode": c["mode"],
+                   "sample_n": n_s},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
