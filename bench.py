@@ -150,7 +150,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * T / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         # the same workload as the CUDA arm's line; each step is the bounded sample below
         "config": {"workload": args.workload, "desc": c["desc"], "n": c["n"], "d": c.get("d", 0), "mode": c["mode"],
                    "sample_n": n_s},
@@ -351,7 +351,7 @@ def run_native(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "desc": c["desc"], "n": n, "d": c.get("d", 0), "mode": c["mode"],
                        **({"metric": ["euclidean", "manhattan", "chebyshev"][args.metric]} if args.metric else {}),
@@ -419,7 +419,7 @@ def run_floyd(args):
     tcpu = time.perf_counter() - t0
     line = {"metric": "minimax Floyd-Warshall relaxations/s (NEXT-2)", "value": relax, "unit": "relaxations/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"floyd_n{n}", "n": n, "weights": "uniform open (0,1), seed 7"},
             "roofline": {"bound": "alu", "achieved": ach, "peak": peak_alu, "unit": "T inst-lanes/s",
                          "frac": ach / peak_alu, "traffic": None, "kernel": "k_fw_tiles",
