@@ -9,7 +9,10 @@ W32 = torch.from_numpy(G.config("C3", n=n)).cuda()
 W64 = W32.double()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 c = P.Context(timing=True)
-for name, W, fn in (("fp32", W32, c.solve_weights), ("fp64", W64, c.solve_weights_f64)):
+arms = (("fp32", W32, c.solve_weights), ("fp64", W64, c.solve_weights_f64))
+if os.environ.get("F64_ONLY"):
+    arms = arms[1:]
+for name, W, fn in arms:
     M = fn(W); torch.cuda.synchronize()
     ts, st = [], []
     for _ in range(5):
