@@ -28,7 +28,7 @@ __device__ __forceinline__ u64 orderable64(double x) {
 // ---- a1: validation (the fp32 kernel's rules: finite, +-0 diagonal, symmetric after
 // -0 -> +0; first offender of each kind by row-major index).  Tile pair (I, J), I <= J:
 // the (I, J) tile and the transposed (J, I) tile through shared memory.
-constexpr int VT64 = 32;
+constexpr int VT64 = 64;  // 64 x 64 doubles per tile: 512-byte row segments, 32 loads in flight per thread
 __global__ void __launch_bounds__(256) k_validate_f64(const double* __restrict__ W, int64_t n, int64_t T,
                                                       u64* __restrict__ out3) {
   // blockIdx.x -> (I, J), I <= J, over the T x T upper triangle (row I holds T - I pairs)
@@ -39,32 +39,42 @@ __global__ void __launch_bounds__(256) k_validate_f64(const double* __restrict__
   while (I > 0 && I * T - I * (I - 1) / 2 > p) I--;
   while ((I + 1) * T - (I + 1) * I / 2 <= p) I++;
   const int64_t J = I + (p - (I * T - I * (I - 1) / 2));
-  __shared__ double b[VT64][VT64 + 1];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  double av[VT64 / 8], bv[VT64 / 8];
+  extern __shared__ double b[];  // [VT64][VT64 + 1]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8; columns tx and tx + 32
+  constexpr int RPT = VT64 / 8;                             // rows per thread
+  double av[RPT][2], bv[RPT][2];
 #pragma unroll
-  for (int s8 = 0; s8 < VT64 / 8; s8++) {  // all loads first: tile (I, J) and tile (J, I)
+  for (int s8 = 0; s8 < RPT; s8++) {  // all loads first: tile (I, J) and tile (J, I)
     const int r = ty + 8 * s8;
-    const int64_t ia = I * VT64 + r, ja = J * VT64 + tx, ib = J * VT64 + r, jb = I * VT64 + tx;
-    av[s8] = (ia < n && ja < n) ? __ldcs(W + ia * n + ja) : 0.0;
-    bv[s8] = (ib < n && jb < n) ? __ldcs(W + ib * n + jb) : 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int cc = tx + 32 * h;
+      const int64_t ia = I * VT64 + r, ja = J * VT64 + cc, ib = J * VT64 + r, jb = I * VT64 + cc;
+      av[s8][h] = (ia < n && ja < n) ? __ldcs(W + ia * n + ja) : 0.0;
+      bv[s8][h] = (ib < n && jb < n) ? __ldcs(W + ib * n + jb) : 0.0;
+    }
   }
 #pragma unroll
-  for (int s8 = 0; s8 < VT64 / 8; s8++) b[ty + 8 * s8][tx] = bv[s8];
+  for (int s8 = 0; s8 < RPT; s8++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) b[(ty + 8 * s8) * (VT64 + 1) + tx + 32 * h] = bv[s8][h];
   __syncthreads();
   u64 nf = KEY_NONE, dg = KEY_NONE, as = KEY_NONE;
 #pragma unroll
-  for (int s8 = 0; s8 < VT64 / 8; s8++) {
-    const int r = ty + 8 * s8;
-    const int64_t i = I * VT64 + r, j = J * VT64 + tx;
-    if (i >= n || j >= n) continue;
-    const double a = av[s8];
-    const double t = b[tx][r];  // W[j][i]
-    const u64 ij = (u64)(i * n + j), ji = (u64)(j * n + i);
-    if (!isfinite(a)) nf = min(nf, ij);
-    if (!isfinite(t)) nf = min(nf, ji);
-    if (i == j && a != 0.0) dg = min(dg, ij);
-    if (i < j && a != t) as = min(as, ij);  // numeric != on finite values == bitwise after -0 -> +0
+  for (int s8 = 0; s8 < RPT; s8++) {
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int r = ty + 8 * s8, cc = tx + 32 * h;
+      const int64_t i = I * VT64 + r, j = J * VT64 + cc;
+      if (i >= n || j >= n) continue;
+      const double a = av[s8][h];
+      const double t = b[cc * (VT64 + 1) + r];  // W[j][i]
+      const u64 ij = (u64)(i * n + j), ji = (u64)(j * n + i);
+      if (!isfinite(a)) nf = min(nf, ij);
+      if (!isfinite(t)) nf = min(nf, ji);
+      if (i == j && a != 0.0) dg = min(dg, ij);
+      if (i < j && a != t) as = min(as, ij);  // numeric != on finite values == bitwise after -0 -> +0
+    }
   }
   if (!__syncthreads_or(nf != KEY_NONE || dg != KEY_NONE || as != KEY_NONE)) return;
   if (nf != KEY_NONE) atomicMin(out3 + 0, nf);
@@ -76,7 +86,13 @@ appd_status launch_validate_weights_f64(appd_ctx* c, const double* W, int64_t n,
   const int64_t T = (n + VT64 - 1) / VT64;
   const int64_t pairs = T * (T + 1) / 2;
   if (pairs > 0x7FFFFFFFll) return fail(c, APPD_ERR_UNSUPPORTED, "fp64 validation grid");
-  k_validate_f64<<<(unsigned)pairs, 256, 0, c->stream>>>(W, n, T, out3);
+  const size_t smem = sizeof(double) * VT64 * (VT64 + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_validate_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_validate_f64<<<(unsigned)pairs, 256, smem, c->stream>>>(W, n, T, out3);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
