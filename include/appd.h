@@ -39,7 +39,10 @@
  *     returned by appd_row_range, and M points to that rows x n block.  Points
  *     mode: X is replicated on every rank.  Weights mode: W points to the
  *     rank's rows x n row block; symmetry is checked inside the rank's diagonal
- *     block only.
+ *     block only.  Every solve starts with an agreement collective over (entry
+ *     point, n, d, the options that steer the control flow, and in points mode a
+ *     position-keyed 64-bit checksum of X): if any rank differs, every rank
+ *     returns APPD_ERR_INVALID_ARGUMENT instead of hanging in a later collective.
  *   - Validation reports one offender: the first non-finite value in row-major
  *     order if there is any, else the first nonzero diagonal entry, else the
  *     first asymmetric pair (i, j) with i < j in row-major order.
@@ -98,8 +101,31 @@ typedef struct {
                                     sum of |x_k - y_k| in k order), 2 Chebyshev (L-inf: max |x_k - y_k|);
                                     L1 / L-inf run the exact FP32 engine (the tensor-core filter is
                                     Euclidean) and the MST on the distance itself */
+  /* world > 1: exchange backend.  NULL (default): NCCL over NVLink, communicator built
+   * from nccl_unique_id.  Non-NULL: every collective of the solve (the solve-start
+   * agreement, the validation verdict, the per-round all-reduce(min) of per-component edge
+   * keys, the component-matrix all-reduce) is copied to host memory and handed to this
+   * callback, which must all-reduce `count` uint64 words in place over the `world` ranks
+   * (op APPD_REDUCE_MIN or APPD_REDUCE_MAX, unsigned order) and return 0; any other value
+   * makes the call fail with APPD_ERR_NCCL (context poisoned).  For MPI / gloo users and
+   * the multi-process tests; results are identical to the NCCL backend. */
+  int32_t (*host_allreduce)(void* user, uint64_t* words, int64_t count, int32_t op);
+  void* host_allreduce_user;
+  int32_t timeout_ms;            /* world > 1, NCCL backend: deadline of every wait on work that
+                                    contains a collective (0 = 300000 ms).  Past it, or when
+                                    ncclCommGetAsyncError reports an error, the communicator is
+                                    aborted and the call returns APPD_ERR_NCCL (poisoned) instead
+                                    of hanging on a dead or diverged peer */
+  int32_t list_cap;              /* tensor-core engine: capacity (entries) of the round-0 candidate
+                                    list, 0 = auto (32 n + 65536).  Rows whose candidates do not fit
+                                    are answered exactly by a full-row scan, so a small value only
+                                    slows the solve (used by the tests to force that path) */
   int32_t reserved[4];
 } appd_options;
+
+/* op argument of appd_options.host_allreduce */
+#define APPD_REDUCE_MIN 0
+#define APPD_REDUCE_MAX 1
 
 typedef struct {
   uint32_t struct_size; /* = sizeof(appd_stats) */
@@ -128,6 +154,7 @@ typedef struct {
   int64_t rescan_blocks;    /* 512-row blocks re-scanned in rounds >= 1 (summed over rounds) */
   int32_t cm_k;             /* components left when the component-matrix finish ran (0: not used) */
   int32_t cm_retries;       /* solves repeated without the component matrix (its candidate list overflowed) */
+  int64_t collectives;      /* world > 1: all-reduces issued by the last solve (agreement, verdict, rounds) */
 } appd_stats;
 
 /* Fill *opt with defaults (device 0, own stream, world 1, AUTO, validate, minimax). */
@@ -171,7 +198,7 @@ appd_status appd_solve_points_stream(appd_ctx* ctx, const float* X_host, int64_t
  * diagonal, symmetric after -0 -> +0; first offender by row-major index) and errors as
  * appd_solve_weights; opt.sense -1 gives the widest-path APPD.  One rank only (world > 1:
  * APPD_ERR_UNSUPPORTED); no candidate cache (every round rescans W); n <= 92682.
- * appd_get_dendrogram is not available after this call (APPD_ERR_INVALID_ARGUMENT). */
+ * appd_last_dendrogram is not available after this call (APPD_ERR_INVALID_ARGUMENT). */
 appd_status appd_solve_weights_f64(appd_ctx* ctx, const double* W, int64_t n, double* M);
 
 /* NEXT-2: the paper's comparison algorithm, the minimax variant of

@@ -29,6 +29,13 @@ STATUS = {
     9: "APPD_ERR_POISONED",
 }
 VARIANT_AUTO, VARIANT_PRIM, VARIANT_BORUVKA = 0, 1, 2
+REDUCE_MIN, REDUCE_MAX = 0, 1
+# appd_options.host_allreduce: int32 (*)(void* user, uint64_t* words, int64_t count, int32 op)
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64),
+                                     ctypes.c_int64, ctypes.c_int32)
+# cudaStreamLegacy: the legacy default stream (torch's default stream has handle 0, which
+# appd_set_stream would read as "library-owned stream")
+CUDA_STREAM_LEGACY = 0x1
 
 
 class appd_options(ctypes.Structure):
@@ -48,6 +55,10 @@ class appd_options(ctypes.Structure):
         ("topk", ctypes.c_int32),
         ("finish_k", ctypes.c_int32),
         ("metric", ctypes.c_int32),
+        ("host_allreduce", HOST_ALLREDUCE_FN),
+        ("host_allreduce_user", ctypes.c_void_p),
+        ("timeout_ms", ctypes.c_int32),
+        ("list_cap", ctypes.c_int32),
         ("reserved", ctypes.c_int32 * 4),
     ]
 
@@ -88,6 +99,7 @@ class appd_stats(ctypes.Structure):
         ("rescan_blocks", ctypes.c_int64),
         ("cm_k", ctypes.c_int32),
         ("cm_retries", ctypes.c_int32),
+        ("collectives", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -104,11 +116,13 @@ EXPORTS = [
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libappd.so (raises OSError if it has not been built)."""
+def load(path: str | None = None):
+    """Load libappd.so (raises OSError if it has not been built).  APPD_LIB names another
+    build of the same ABI (the development library, tools/ only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("APPD_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise OSError(f"{path} not built: run `python -m paper_2407_07058_b200.build`")
     L = ctypes.CDLL(path)
@@ -198,13 +212,40 @@ class Context:
     def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
                  variant: int = VARIANT_AUTO, validate: bool = True, sense: int = 1, timing: bool = False,
                  dendrogram: int = 0, points_engine: int = 0, topk: int = 0,
-                 finish_k: int = 0, metric: int = 0):
+                 finish_k: int = 0, metric: int = 0, host_allreduce=None, timeout_ms: int = 0,
+                 list_cap: int = 0):
+        """stream: a cudaStream_t handle (int) every call runs on; None (default) follows
+        torch.cuda.current_stream(device) at each call, so the library's work is ordered
+        with the torch kernels that produced its inputs and that read its outputs.
+        host_allreduce: world > 1 exchange through host memory instead of NCCL, a Python
+        callable (words: numpy uint64 array, op: REDUCE_MIN / REDUCE_MAX) -> None that
+        all-reduces `words` in place over the ranks (e.g. torch.distributed with gloo)."""
         L = load()
         o = appd_options()
         L.appd_options_init(ctypes.byref(o))
         o.device = device
-        o.cuda_stream = stream
+        self._follow_torch_stream = stream is None
+        o.cuda_stream = stream if stream is not None else self._torch_stream(device)
         o.rank, o.world = rank, world
+        o.timeout_ms = timeout_ms
+        o.list_cap = list_cap
+        self._xchg = None
+        if host_allreduce is not None:
+            import numpy as np
+
+            def _cb(user, words, count, op, _f=host_allreduce):
+                try:
+                    arr = np.ctypeslib.as_array(words, shape=(count,))
+                    _f(arr, int(op))
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported to the library as a failed exchange
+                    import traceback
+
+                    traceback.print_exc()
+                    return 1
+
+            self._xchg = HOST_ALLREDUCE_FN(_cb)  # kept alive with the context
+            o.host_allreduce = self._xchg
         self._id = None
         if nccl_id is not None:
             self._id = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
@@ -224,10 +265,33 @@ class Context:
             raise AppdError(s, "appd_create")
         self._h = h
         self._L = L
+        self._stream_h = o.cuda_stream
         self.device = device
         self.rank, self.world = rank, world
 
     # -- helpers --
+    @staticmethod
+    def _torch_stream(device):
+        try:
+            import torch
+
+            if not torch.cuda.is_available():
+                return None
+            h = torch.cuda.current_stream(device).cuda_stream
+            return h if h else CUDA_STREAM_LEGACY
+        except Exception:  # noqa: BLE001
+            return None
+
+    def _sync_stream(self):
+        """Follow torch's current stream (inputs made by pending torch kernels)."""
+        if self._follow_torch_stream:
+            h = self._torch_stream(self.device)
+            if h is not None and h != self._stream_h:
+                s = self._L.appd_set_stream(self._h, h)
+                if s != APPD_OK:
+                    self._raise(s, "appd_set_stream")
+                self._stream_h = h
+
     def _raise(self, s, what):
         i, j = ctypes.c_int64(-1), ctypes.c_int64(-1)
         self._L.appd_error_index(self._h, ctypes.byref(i), ctypes.byref(j))
@@ -236,6 +300,8 @@ class Context:
         raise AppdError(s, f"{what}: {msg}", idx)
 
     def set_stream(self, stream):
+        self._follow_torch_stream = False
+        self._stream_h = stream
         s = self._L.appd_set_stream(self._h, stream)
         if s != APPD_OK:
             self._raise(s, "appd_set_stream")
@@ -263,7 +329,11 @@ class Context:
         """appd_solve_weights: W is this rank's rows x n block (n x n for world 1)."""
         _check_tensor(W, "W")
         n = W.shape[-1]
+        _, rows = self.row_range(n)
+        if tuple(W.shape) != (rows, n):
+            raise ValueError(f"W must be this rank's {rows} x {n} row block (got {tuple(W.shape)})")
         M = self._out(n, M)
+        self._sync_stream()
         s = self._L.appd_solve_weights(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_weights")
@@ -274,7 +344,10 @@ class Context:
         on the GPU (one rank); M must not alias W."""
         _check_tensor(W, "W")
         n = W.shape[-1]
+        if tuple(W.shape) != (n, n):
+            raise ValueError(f"W must be n x n (got {tuple(W.shape)})")
         M = self._out(n, M)
+        self._sync_stream()
         s = self._L.appd_floyd_weights(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_floyd_weights")
@@ -286,11 +359,14 @@ class Context:
 
         _check_tensor(W, "W", "float64")
         n = W.shape[-1]
+        if tuple(W.shape) != (n, n):
+            raise ValueError(f"W must be n x n (got {tuple(W.shape)})")
         if M is None:
             M = torch.empty((n, n), dtype=torch.float64, device=f"cuda:{self.device}")
         _check_tensor(M, "M", "float64")
         if M.numel() != n * n:
             raise ValueError(f"M must hold {n} x {n} doubles")
+        self._sync_stream()
         s = self._L.appd_solve_weights_f64(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_weights_f64")
@@ -306,6 +382,7 @@ class Context:
             raise ValueError("solve_points_stream takes host tensors")
         if M.numel() != n * n:
             raise ValueError(f"M must hold {n} x {n} floats")
+        self._sync_stream()
         s = self._L.appd_solve_points_stream(self._h, _ptr(X), n, d, _ptr(M), int(block_rows))
         if s != APPD_OK:
             self._raise(s, "appd_solve_points_stream")
@@ -316,6 +393,7 @@ class Context:
         _check_tensor(X, "X")
         n, d = X.shape
         M = self._out(n, M)
+        self._sync_stream()
         s = self._L.appd_solve_points(self._h, _ptr(X), n, d, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_points")
@@ -326,6 +404,10 @@ class Context:
         _check_tensor(X, "X")
         _check_tensor(M, "M")
         n, d = X.shape
+        _, rows = self.row_range(n)
+        if M.numel() != rows * n:
+            raise ValueError(f"M must hold {rows} x {n} floats")
+        self._sync_stream()
         s = self._L.appd_solve_points_host(self._h, _ptr(X), n, d, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_points_host")
@@ -335,6 +417,10 @@ class Context:
         _check_tensor(W, "W")
         _check_tensor(M, "M")
         n = W.shape[-1]
+        _, rows = self.row_range(n)
+        if tuple(W.shape) != (rows, n) or M.numel() != rows * n:
+            raise ValueError(f"W and M must be this rank's {rows} x {n} row blocks")
+        self._sync_stream()
         s = self._L.appd_solve_weights_host(self._h, _ptr(W), n, _ptr(M))
         if s != APPD_OK:
             self._raise(s, "appd_solve_weights_host")
@@ -349,6 +435,7 @@ class Context:
         rows = n - row0 if rows is None else rows
         if out is None:
             out = torch.empty((rows, n), dtype=torch.float32, device=X.device)
+        self._sync_stream()
         s = self._L.appd_points_weights(self._h, _ptr(X), n, d, row0, rows, _ptr(out))
         if s != APPD_OK:
             self._raise(s, "appd_points_weights")

@@ -139,7 +139,8 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.variant == APPD_VARIANT_PRIM) return APPD_ERR_UNSUPPORTED;  // not built (appd.h)
   if (o.metric < 0 || o.metric > 2) return APPD_ERR_INVALID_ARGUMENT;
-  if (o.world > 1 && !o.nccl_unique_id) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.world > 1 && !o.nccl_unique_id && !o.host_allreduce) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.timeout_ms < 0 || o.list_cap < 0) return APPD_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -303,6 +304,83 @@ static appd_status report_validation(appd_ctx* c, const u64 bad[3], int64_t n, b
               (long long)c->err_j, (long long)c->err_j, (long long)c->err_i);
 }
 
+// world > 1: every rank must enter the solve with the same problem, or the ranks would
+// take different branches and hang in a later collective.  One all-reduce
+// (min) over the words v and ~v: v agrees on every rank iff min(v) == v and min(~v) == ~v.
+static appd_status agree(appd_ctx* c, const float* X, int64_t n, int64_t d, int mode) {
+  constexpr int NW = 7;
+  u64 v[NW];
+  v[0] = (u64)n;
+  v[1] = (u64)d;
+  v[2] = (u64)mode | (u64)(c->stream_out ? 1 : 0) << 8 | (u64)(uint32_t)c->opt.world << 32;
+  v[3] = (u64)(c->opt.sense + 1) | (u64)(c->opt.validate & 15) << 4 | (u64)(c->opt.metric & 15) << 8 |
+         (u64)(c->opt.points_engine & 15) << 12 | (u64)(c->opt.dendrogram & 15) << 16 |
+         (u64)(c->opt.variant & 15) << 20;
+  v[4] = (u64)(uint32_t)c->opt.topk | (u64)(uint32_t)c->opt.finish_k << 32;
+  v[5] = 0;
+  v[6] = (u64)(uint32_t)c->opt.list_cap;
+  u64* dv = (u64*)ws(c, S_TMP, sizeof(u64) * 2 * NW);
+  if (!dv) return fail(c, APPD_ERR_OUT_OF_MEMORY, "agreement buffer");
+  if (X) {  // points mode: X is replicated, so its checksum must agree too
+    appd_status s = launch_checksum_words(c, X, n * d, dv);
+    if (s) return s;
+    APPD_CUDA(c, cudaMemcpyAsync(&v[5], dv, sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+    APPD_SYNC(c);
+  }
+  u64 h[2 * NW];
+  for (int i = 0; i < NW; i++) {
+    h[i] = v[i];
+    h[NW + i] = ~v[i];
+  }
+  APPD_CUDA(c, cudaMemcpyAsync(dv, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  appd_status s = nccl_allreduce_min_u64(c, dv, 2 * NW);
+  if (s) return s;
+  APPD_CUDA(c, cudaMemcpyAsync(h, dv, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  APPD_SYNC(c);
+  static const char* what[NW] = {"n", "d", "entry point / world", "options (sense, validate, metric, engine, dendrogram, variant)",
+                                 "options (topk, finish_k)", "the checksum of X", "options (list_cap)"};
+  for (int i = 0; i < NW; i++)
+    if (h[i] != v[i] || h[NW + i] != ~v[i])
+      return fail(c, APPD_ERR_INVALID_ARGUMENT, "ranks disagree on %s at solve start (this rank %llu)", what[i],
+                  (unsigned long long)v[i]);
+  return APPD_OK;
+}
+
+#ifdef APPD_DEV_HOOKS
+// development builds, APPD_CHECK=1: the MST edges must form a spanning tree and pi must be
+// a permutation (reported to stderr with the stage; the solve continues)
+static void dev_check(appd_ctx* c, const char* what, const int32_t* d_eu, const int32_t* d_ev, int64_t m,
+                      const int* d_pi, int64_t n) {
+  static const bool on = dev_env("APPD_CHECK") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(c->stream);
+  std::vector<int32_t> eu(m), ev(m), pi(n);
+  if (d_eu) {
+    cudaMemcpy(eu.data(), d_eu, 4 * m, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ev.data(), d_ev, 4 * m, cudaMemcpyDeviceToHost);
+    std::vector<int32_t> p(n);
+    for (int64_t i = 0; i < n; i++) p[i] = (int32_t)i;
+    auto find = [&](int32_t x) { while (p[x] != x) x = p[x] = p[p[x]]; return x; };
+    int64_t bad = 0;
+    for (int64_t e = 0; e < m; e++) {
+      if (eu[e] < 0 || eu[e] >= n || ev[e] < 0 || ev[e] >= n) { bad++; continue; }
+      int32_t a = find(eu[e]), b = find(ev[e]);
+      if (a == b) bad++; else p[a] = b;
+    }
+    if (bad) fprintf(stderr, "[appd check] rank %d %s: %lld bad MST edges (n %lld)\n", c->opt.rank, what, (long long)bad, (long long)n);
+  }
+  if (d_pi) {
+    cudaMemcpy(pi.data(), d_pi, 4 * n, cudaMemcpyDeviceToHost);
+    std::vector<char> seen(n, 0);
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; i++) {
+      if (pi[i] < 0 || pi[i] >= n || seen[pi[i]]) bad++; else seen[pi[i]] = 1;
+    }
+    if (bad) fprintf(stderr, "[appd check] rank %d %s: pi is not a permutation (%lld bad)\n", c->opt.rank, what, (long long)bad);
+  }
+}
+#endif
+
 // The whole pipeline.  X (points) or W (weights) is a device pointer.
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
@@ -322,6 +400,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   c->err_i = c->err_j = -1;
   c->last_error.clear();
   host_mark("solve entry", true);
+  if (c->opt.world > 1) {
+    appd_status sa = agree(c, X, n, points ? d : 0, points ? 2 : (f64 ? 3 : 1));
+    if (sa) return sa;
+  }
   stage_event(c, 0);
 
   // ---- a1: validation ----
@@ -346,7 +428,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if (c->opt.validate && !defer_validation) {
     appd_status s;
     u64 hb[3];
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     memcpy(hb, hbad, sizeof hb);
     if (c->opt.world > 1) {
       // every rank must agree on the verdict (else the others would hang in the next collective)
@@ -355,7 +437,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       APPD_CUDA(c, cudaMemcpyAsync(agree, hb, sizeof hb, cudaMemcpyHostToDevice, c->stream));
       if ((s = nccl_allreduce_min_u64(c, agree, 3))) return s;
       APPD_CUDA(c, cudaMemcpyAsync(hb, agree, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
-      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      APPD_SYNC(c);
     }
     if ((s = report_validation(c, hb, n, points, d))) return s;
   }
@@ -364,13 +446,13 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
 
   if (n == 1) {
     if (c->stream_out) {
-      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      APPD_SYNC(c);
       c->stream_out[0] = 0.0f;
     } else if (rows > 0) {
       appd_status s = f64 ? launch_set_diag_zero_single_f64(c, c->f64_M) : launch_set_diag_zero_single(c, M);
       if (s) return s;
     }
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     c->one_pi = 0;
     c->dend_on_device = false;
     c->dend_pi = &c->one_pi;
@@ -412,7 +494,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       use_tc = true;
     } else {
       if (defer_validation) {  // the verdict decides before any fallback
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        APPD_SYNC(c);
         u64 hb[3];
         memcpy(hb, hbad, sizeof hb);
         appd_status sv = report_validation(c, hb, n, points, d);
@@ -500,7 +582,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         if ((s = nccl_allreduce_max_u64(c, flag, 1))) return s;
         u64 hf2 = 0;
         APPD_CUDA(c, cudaMemcpyAsync(&hf2, flag, sizeof hf2, cudaMemcpyDeviceToHost, c->stream));
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        APPD_SYNC(c);
         ovf = hf2 != 0;
         if (!ovf && (s = nccl_allreduce_min_u64(c, WCM, k * k))) return s;
       }
@@ -526,15 +608,15 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         } else {
           c->stats.tcscan_flops += 2.0 * (double)(std::min<int64_t>(rt_end * 512, n) - rt_begin * 512) * n * d;
         }
-        if (getenv("APPD_DEBUG_ROUNDS"))
+        if (dev_env("APPD_DEBUG_ROUNDS"))
           fprintf(stderr, "[appd] component-matrix finish at k %lld (listing count checked at the end)\n", (long long)k);
         rounds++;
         k = 1;
         break;
       }
     }
-    static const bool dbg = getenv("APPD_DEBUG_ROUNDS") != nullptr;
-    static const bool tc_verify = getenv("APPD_TC_VERIFY") != nullptr;
+    static const bool dbg = dev_env("APPD_DEBUG_ROUNDS") != nullptr;
+    static const bool tc_verify = dev_env("APPD_TC_VERIFY") != nullptr;
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
     if (!(use_tc && tc.lookup_pending) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
@@ -555,7 +637,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         std::vector<u64> a(k), b(k);
         APPD_CUDA(c, cudaMemcpyAsync(a.data(), compbest, sizeof(u64) * k, cudaMemcpyDeviceToHost, c->stream));
         APPD_CUDA(c, cudaMemcpyAsync(b.data(), cb2, sizeof(u64) * k, cudaMemcpyDeviceToHost, c->stream));
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        APPD_SYNC(c);
         int bad = 0;
         for (int64_t q = 0; q < k; q++)
           if (a[q] != b[q]) {
@@ -583,7 +665,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       // component's best are re-scanned
       if (!w_pending) {
         if ((s = w_lookup_async())) return s;
-        APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+        APPD_SYNC(c);
       }
       w_pending = false;
       const unsigned cnt = c->pinned_small[9];
@@ -655,7 +737,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
     host_mark("round queued, synchronising");
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     host_mark("round synchronised");
     if (check_first_sync) {
       check_first_sync = false;
@@ -756,7 +838,13 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   c->dend_n = n;
   if (c->opt.dendrogram != 1) {
     // v2: Prim order of the MST on the GPU (k_dendro.cu); h lands in the sparse table's level 0
+#ifdef APPD_DEV_HOOKS
+    dev_check(c, "edges", d_eu, d_ev, m, nullptr, n);
+#endif
     if ((s = gpu_dendrogram(c, d_eu, d_ev, d_ew, n, pi, ST))) return s;
+#ifdef APPD_DEV_HOOKS
+    dev_check(c, "dendrogram", nullptr, nullptr, 0, pi, n);
+#endif
     c->dend_pi = pi;
     c->dend_h = ST;
     c->dend_on_device = true;
@@ -769,7 +857,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     int32_t* h_pi = (int32_t*)(hp + 12 * m);    // pi (4 n)
     float* h_h = (float*)(h_pi + n);            // h (4 (n - 1))
     APPD_CUDA(c, cudaMemcpyAsync(h_e, d_eu, 12 * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     if ((int64_t)c->uf_scratch.size() < 8 * n) c->uf_scratch.resize(8 * n);
     host_dendrogram_uvw(h_e, h_e + m, (const float*)(h_e + 2 * m), n, h_pi, h_h, c->uf_scratch.data());
     c->dend_pi = h_pi;
@@ -827,7 +915,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)((blocks - 1) & 1)], 0));  // last copy done
     if (blocks >= 2) APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)(blocks & 1)], 0));
     stage_event(c, 6);
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     if (cm_status_pending && c->pinned_small[48] == 1) {
       const int fk = c->opt.finish_k;
       c->opt.finish_k = -1;
@@ -872,7 +960,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     return s;
   }
   stage_event(c, 6);
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  APPD_SYNC(c);
   if (cm_status_pending && c->pinned_small[48] == 1) {
     // the component matrix's candidate list overflowed: solve again without it (rare)
     const int fk = c->opt.finish_k;
@@ -918,8 +1006,12 @@ extern "C" appd_status appd_solve_weights(appd_ctx* c, const float* W, int64_t n
   if (s) return s;
   if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
   if (n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682 (32-bit pair index)");
-  if ((s = check_device_ptr(c, W, "W"))) return s;
-  if ((s = check_device_ptr(c, M, "M"))) return s;
+  int64_t row0, rows;
+  appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
+  if (rows > 0 || W || M) {  // a rank that owns no rows may pass NULL blocks
+    if ((s = check_device_ptr(c, W, "W"))) return s;
+    if ((s = check_device_ptr(c, M, "M"))) return s;
+  }
   return solve(c, W, nullptr, n, 0, M);
 }
 
@@ -972,7 +1064,7 @@ extern "C" appd_status appd_floyd_weights(appd_ctx* c, const float* W, int64_t n
     APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
     if ((s = launch_validate_weights(c, W, n, 0, n, bad))) return s;
     APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     u64 hb[3];
     memcpy(hb, hbad, sizeof hb);
     if ((s = report_validation(c, hb, n, false, 0))) return s;
@@ -980,7 +1072,7 @@ extern "C" appd_status appd_floyd_weights(appd_ctx* c, const float* W, int64_t n
   stage_event(c, 1);
   if ((s = floyd_weights(c, W, n, M, c->opt.sense >= 0 ? 1 : -1))) return s;
   stage_event(c, 6);
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  APPD_SYNC(c);
   c->stats.kernel_launches = c->launches;
   c->stats.fill_bytes = n * n * 4;
   if (c->opt.timing) {
@@ -997,7 +1089,9 @@ extern "C" appd_status appd_solve_points(appd_ctx* c, const float* X, int64_t n,
   if (n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072 (33-bit pair index)");
   if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
   if ((s = check_device_ptr(c, X, "X"))) return s;
-  if ((s = check_device_ptr(c, M, "M"))) return s;
+  int64_t row0, rows;
+  appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
+  if ((rows > 0 || M) && (s = check_device_ptr(c, M, "M"))) return s;  // no rows: M may be NULL
   return solve(c, nullptr, X, n, d, M);
 }
 
@@ -1018,7 +1112,7 @@ static appd_status solve_host(appd_ctx* c, const float* Wh, const float* Xh, int
   s = Xh ? solve(c, nullptr, din, n, d, dout) : solve(c, din, nullptr, n, 0, dout);
   if (s) return s;
   APPD_CUDA(c, cudaMemcpyAsync(Mh, dout, out_bytes, cudaMemcpyDeviceToHost, c->stream));
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  APPD_SYNC(c);
   return APPD_OK;
 }
 
@@ -1072,6 +1166,6 @@ extern "C" appd_status appd_points_weights(appd_ctx* c, const float* X, int64_t 
   if ((s = check_device_ptr(c, X, "X"))) return s;
   if ((s = check_device_ptr(c, Wb, "Wblock"))) return s;
   if ((s = launch_points_weights(c, X, n, d, row0, rows, Wb))) return s;
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  APPD_SYNC(c);
   return APPD_OK;
 }

@@ -9,6 +9,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -117,6 +118,7 @@ struct appd_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
+  std::vector<unsigned long long> host_xchg;  // host exchange backend staging (opt.host_allreduce)
   std::vector<int32_t> uf_scratch;   // host dendrogram work arrays
   // streamed output (NEXT-4, appd_solve_points_stream): M rows go to this host buffer in
   // blocks of stream_block rows, two device block buffers, copies on copy_stream
@@ -129,9 +131,29 @@ struct appd_ctx {
 
 namespace appd {
 
+// Per-device one-time setup.  cudaFuncSetAttribute and occupancy are properties of the
+// current device, and one process may hold contexts on several devices (each on its own
+// host thread), so every "done" flag is a per-device bit set atomically.
+inline unsigned long long dev_bit(const appd_ctx* c) { return 1ull << (c->device & 63); }
+inline bool needs_setup(const std::atomic<unsigned long long>& done, const appd_ctx* c) {
+  return (done.load(std::memory_order_acquire) & dev_bit(c)) == 0;
+}
+inline void setup_done(std::atomic<unsigned long long>& done, const appd_ctx* c) {
+  done.fetch_or(dev_bit(c), std::memory_order_acq_rel);
+}
+
+// Development hooks (debug prints, timing experiments, verification against the exact
+// engine) read environment variables only in builds with -DAPPD_DEV_HOOKS; the product
+// build never consults the environment.
+#ifdef APPD_DEV_HOOKS
+inline const char* dev_env(const char* name) { return getenv(name); }
+#else
+inline const char* dev_env(const char*) { return nullptr; }
+#endif
+
 // APPD_DEBUG_HOST=1: host-side microseconds since the solve started, at marked points
 inline void host_mark(const char* what, bool reset = false) {
-  static const bool on = getenv("APPD_DEBUG_HOST") != nullptr;
+  static const bool on = dev_env("APPD_DEBUG_HOST") != nullptr;
   static std::chrono::steady_clock::time_point t0;
   if (!on) return;
   const auto now = std::chrono::steady_clock::now();
@@ -250,13 +272,36 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
     if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
   } while (0)
 
+#define APPD_SYNC(c)                                 \
+  do {                                               \
+    appd_status _s = appd::sync_stream(c);           \
+    if (_s != APPD_OK) return _s;                    \
+  } while (0)
+
 #define APPD_STR2(x) #x
 #define APPD_STR(x) APPD_STR2(x)
+#ifdef APPD_DEV_HOOKS
+// development builds: APPD_SYNC_EACH=1 synchronises after every launch, so an
+// asynchronous fault is reported at the kernel that caused it
+#define APPD_DEV_SYNC_EACH(c)                                                                    \
+  do {                                                                                          \
+    static const bool _each = appd::dev_env("APPD_SYNC_EACH") != nullptr;                      \
+    if (_each) {                                                                                \
+      cudaError_t _e2 = cudaStreamSynchronize((c)->stream);                                     \
+      if (_e2 != cudaSuccess) return appd::cuda_fail(c, _e2, "kernel " __FILE__ ":" APPD_STR(__LINE__)); \
+    }                                                                                           \
+  } while (0)
+#else
+#define APPD_DEV_SYNC_EACH(c) \
+  do {                        \
+  } while (0)
+#endif
 #define APPD_LAUNCHED(c)                                                                        \
   do {                                                                                          \
     (c)->launches++;                                                                            \
     cudaError_t _e = cudaGetLastError();                                                        \
     if (_e != cudaSuccess) return appd::cuda_fail(c, _e, "kernel launch " __FILE__ ":" APPD_STR(__LINE__)); \
+    APPD_DEV_SYNC_EACH(c);                                                                      \
   } while (0)
 
 // ---- kernels (k_*.cu) ----
@@ -264,6 +309,8 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
 appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
                                     u64* out3 /*device, 3 minima*/);
 appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64_t d, u64* out3);
+// position-keyed 64-bit checksum of count 32-bit words (world > 1 solve-start agreement)
+appd_status launch_checksum_words(appd_ctx* c, const void* x, int64_t count, u64* out);
 
 // Boruvka
 appd_status launch_scan_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,
@@ -352,6 +399,9 @@ appd_status nccl_unique_id(uint8_t out[128], std::string* err);
 appd_status nccl_init(appd_ctx* c, const uint8_t* id, int rank, int world);
 appd_status nccl_allreduce_min_u64(appd_ctx* c, u64* buf, int64_t count);
 appd_status nccl_allreduce_max_u64(appd_ctx* c, u64* buf, int64_t count);
+// wait for the context stream (world > 1 NCCL: polled against opt.timeout_ms and the
+// communicator's asynchronous error; the communicator is aborted on failure)
+appd_status sync_stream(appd_ctx* c);
 void nccl_destroy(appd_ctx* c);
 
 }  // namespace appd

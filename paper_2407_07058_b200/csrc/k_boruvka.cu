@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) k_scan_weights(const float* __restrict__ 
                                                       int64_t rows, const int* __restrict__ comp,
                                                       u64* __restrict__ compbest) {
   __shared__ u64 red[8];
-  const bool vec = (n & 3) == 0;
+  const bool vec = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const int64_t i = row0 + r;
     const float* Wr = W + r * n;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
   __shared__ u64 tau_s;
   __shared__ int ncand;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool vec = (n & 3) == 0;
+  const bool vec = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const int64_t i = row0 + r;
     const float* Wr = W + r * n;
@@ -545,15 +545,16 @@ __global__ void __launch_bounds__(256, 2)
 appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
                                int64_t rows, const int* comp, u64* compbest) {
   const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4;
-  static bool attr = false;
-  if (!attr) {
+  if (rows <= 0) return APPD_OK;
+  static std::atomic<unsigned long long> attr{0};
+  if (needs_setup(attr, c)) {
     cudaFuncSetAttribute(k_scan_points<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    setup_done(attr, c);
   }
   int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
   int64_t col_tiles = npad / PT_BN;
@@ -873,11 +874,13 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
 
 appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, int64_t n, int shift, int* link,
                             int* parent, u64* mstkeys, int* counters, int* flags, int* newid, const LookupArgs* look) {
-  static int per_sm = -1;
+  static std::atomic<int> per_sm_plus1[64];  // 0: not yet measured on that device
+  int per_sm = per_sm_plus1[c->device & 63].load() - 1;
   if (per_sm < 0) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_contract, kContractThreads, 0) != cudaSuccess)
       per_sm = 0;
     cudaGetLastError();
+    per_sm_plus1[c->device & 63].store(per_sm + 1);
   }
   if (per_sm < 1) return APPD_ERR_UNSUPPORTED;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (std::max(k, n) + kContractThreads - 1) /

@@ -353,10 +353,10 @@ appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int
   if (ngq > 128) return fail(c, APPD_ERR_UNSUPPORTED, "top-K scan: %d chunks per row", nch);
 #define APPD_TOPK_SCAN(KK)                                                                                     \
   do {                                                                                                         \
-    static bool attr_##KK = false;                                                                             \
-    if (!attr_##KK) {                                                                                          \
+    static std::atomic<unsigned long long> attr_##KK{0};                                                       \
+    if (needs_setup(attr_##KK, c)) {                                                                           \
       cudaFuncSetAttribute(k_topk_scan<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);          \
-      attr_##KK = true;                                                                                        \
+      setup_done(attr_##KK, c);                                                                                \
     }                                                                                                          \
     k_topk_scan<KK><<<grid, 32 * TK_PARTS, smem, c->stream>>>(TM32, nch, p_begin, p_end, nrm, len, sc, err, \
                                                               maxerr, em, UBK, list, count, cap, cand_cnt, ngq); \

@@ -87,10 +87,10 @@ appd_status launch_validate_weights_f64(appd_ctx* c, const double* W, int64_t n,
   const int64_t pairs = T * (T + 1) / 2;
   if (pairs > 0x7FFFFFFFll) return fail(c, APPD_ERR_UNSUPPORTED, "fp64 validation grid");
   const size_t smem = sizeof(double) * VT64 * (VT64 + 1);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (needs_setup(attr, c)) {
     cudaFuncSetAttribute(k_validate_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    setup_done(attr, c);
   }
   k_validate_f64<<<(unsigned)pairs, 256, smem, c->stream>>>(W, n, T, out3);
   APPD_LAUNCHED(c);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_scan_weights_f64(const double* __restri
     const int ci = ROUND0 ? (int)i : comp[i];
     u64 bw = KEY_NONE;
     int bj = -1;
-    const bool vec = (n & 1) == 0;
+    const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
     if (vec) {
       const double2* W2 = reinterpret_cast<const double2*>(Wr);
       const int2* C2 = reinterpret_cast<const int2*>(comp);

@@ -157,7 +157,7 @@ constexpr int FILL_THREADS = 256;
 constexpr int FILL_R = 128;  // max rows per tile (consecutive in leaf order; <= FILL_THREADS)
 
 // positions spanned by one tile whose in-tile range maxima come from shared memory
-constexpr int FILL_SPAN = 256, FILL_LV = 8;  // 2^FILL_LV >= FILL_SPAN
+constexpr int FILL_SPAN = 256, FILL_LV = 8;  // spans < FILL_SPAN: levels 0 .. FILL_LV - 1
 
 // output store flavour (STORE: 0 streaming / evict-first st.global.cs, 1 default st.global)
 template <int STORE>
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(FILL_THREADS)
   }
   const bool in_range = jbase < n;
   const int span = aR - aL;  // h[aL .. aR-1]
-  const bool local = span <= FILL_SPAN;
+  const bool local = span < FILL_SPAN;  // levels k <= log2(span) < FILL_LV
   if (local) {  // the global table's levels over [aL, aR): independent loads, one barrier
     for (int k = 0; (1 << k) <= span; k++)
       for (int i = threadIdx.x; i + (1 << k) <= span; i += FILL_THREADS)
@@ -329,7 +329,7 @@ appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, 
   dim3 grid((unsigned)((n + cols_per_cta - 1) / cols_per_cta), (unsigned)((nrows + FILL_R - 1) / FILL_R));
   if (grid.y > 65535u) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
   // 32-byte stores by default (measured: fewer instructions per byte); APPD_FILL_VEC=4 picks 16-byte
-  static const int want = getenv("APPD_FILL_VEC") ? atoi(getenv("APPD_FILL_VEC")) : 8;
+  static const int want = dev_env("APPD_FILL_VEC") ? atoi(dev_env("APPD_FILL_VEC")) : 8;
   // small matrices: 64-row tiles when 128-row tiles would leave fewer than ~6 waves of
   // the 4 resident CTAs per SM (the last, partial wave dominates)
   const bool small = (int64_t)grid.x * grid.y < (int64_t)c->sm_count * 4 * 6;

@@ -215,13 +215,13 @@ static appd_status fw_run(appd_ctx* c, float* M, int64_t n64, int sense) {
   const int T = (n + FW_T - 1) / FW_T;
   const size_t smem = sizeof(float) * (2 * FW_T * FW_AS + 2 * FW_KC * FW_BS);
   const size_t smem1 = sizeof(float) * FW_T * (FW_T + 1);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (needs_setup(attr, c)) {
     cudaFuncSetAttribute(k_fw_tiles<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_fw_tiles<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_fw_phase1<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     cudaFuncSetAttribute(k_fw_phase1<-1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-    attr = true;
+    setup_done(attr, c);
   }
   for (int kb = 0; kb < T; kb++) {
     if (sense > 0) k_fw_phase1<1><<<1, 1024, smem1, c->stream>>>(M, n, kb);

@@ -593,8 +593,8 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
     st->list_entries_cap =
         (unsigned)std::min<int64_t>(std::max<int64_t>(32 * n + 65536, all_pairs <= (4 << 20) ? all_pairs : 0),
                                     (int64_t)1 << 31);
-    if (const char* t = getenv("APPD_TEST_LIST_CAP"))  // test hook: force list overflow (poisoned rows)
-      st->list_entries_cap = (unsigned)std::max(1, atoi(t));
+    if (c->opt.list_cap > 0)  // option (tests): a small capacity forces the overflow path (poisoned rows)
+      st->list_entries_cap = (unsigned)c->opt.list_cap;
     st->lista = (unsigned*)ws(c, S_TC_LISTA, sizeof(unsigned) * st->list_entries_cap);
     st->listb = (unsigned*)ws(c, S_TC_LISTB, sizeof(unsigned) * st->list_entries_cap);
     if (!st->lista || !st->listb) return fail(c, APPD_ERR_OUT_OF_MEMORY, "candidate list workspace");
@@ -798,7 +798,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   if (cache && round > 0) {
     if (!st->lookup_pending) {
       if ((s = tcf_lookup_async(c, st, comp, compbest))) return s;
-      APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+      APPD_SYNC(c);
     }
     st->lookup_pending = false;  // the caller synchronised after queueing it
     rescan_rows = c->pinned_small[9];
@@ -838,7 +838,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     P.rb_begin = (int)rb_begin;
     P.rb_end = (int)rb_end;
     P.seg32 = 1;
-    if (getenv("APPD_TC_BENCH")) {  // debug: time the scan variants in isolation (results discarded)
+    if (dev_env("APPD_TC_BENCH")) {  // debug: time the scan variants in isolation (results discarded)
       const char* names[] = {"seg64", "seg32", "", "null-epilogue", "tmem-load-only", "no-B-copies", "null+noB"};
       for (int pass : {0, 1, 3, 4, 5, 6}) {
         float best = 1e9f;
@@ -952,7 +952,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   P.rb_begin = (int)rb_begin;
   P.rb_end = (int)rb_end;
   // one rank: every unordered pair is needed from one side only -> upper-triangle pass
-  P.upper = c->opt.world == 1 && !getenv("APPD_CM_FULL");
+  P.upper = c->opt.world == 1 && !dev_env("APPD_CM_FULL");
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 7, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
@@ -996,7 +996,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   if ((s = launch_cm_filter(c, C))) return s;
   if ((s = exact_list(c, st, X, 1, st->perm, st->counters + 1, (int)k, WCM))) return s;
   if (check_now) {
-    APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+    APPD_SYNC(c);
     st->last_list_entries = c->pinned_small[16];
     if (st->last_list_entries > st->list_entries_cap) *listed_overflow = true;
   }
@@ -1040,7 +1040,7 @@ appd_status tcf_debug_gram(appd_ctx* c, const float* X, int64_t n, int64_t d, fl
   k_ref_gram<<<c->sm_count * 4, 256, 0, c->stream>>>((const __half*)st.YA, (const __half*)st.YB, st.K, st.npad,
                                                       ref_out);
   APPD_LAUNCHED(c);
-  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  APPD_SYNC(c);
   return APPD_OK;
 }
 

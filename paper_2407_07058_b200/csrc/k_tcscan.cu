@@ -379,13 +379,13 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   // at least 120 KB so that exactly one CTA (and one 512-column TMEM allocation) fits per SM
   size_t smem = tcf_smem_bytes(P.K, P.stages);
   if (smem < 120 * 1024) smem = 120 * 1024;
-  static int attr_done = 0;
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_done{0};
+  if (needs_setup(attr_done, c)) {
     cudaFuncSetAttribute(k_tcf_scan<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_tcf_scan<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = 1;
+    setup_done(attr_done, c);
   }
   // column-tile units (host upper bound when the row-block list is read on the device)
   const int64_t nrb = P.rb_end - P.rb_begin;
@@ -393,9 +393,12 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
                                 : nrb * P.col_tiles;
   int grid = (int)std::min<int64_t>(c->sm_count, units);
   if (grid < 1) return APPD_OK;
+#ifdef APPD_DEV_HOOKS
+  // development builds only (-DAPPD_DEV_HOOKS): pipeline experiments 3-6 (null epilogue,
+  // TMEM load only, no column-operand copies) selected by APPD_TC_EXPERIMENT or pass >= 3
   static const int exp_pass = getenv("APPD_TC_EXPERIMENT") ? atoi(getenv("APPD_TC_EXPERIMENT")) : 0;
   int ep = exp_pass;
-  if (pass >= 3) ep = pass;  // explicit experiment request (debug benchmark)
+  if (pass >= 3) ep = pass;
   if (ep == 3) {
     cudaFuncSetAttribute(k_tcf_scan<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     k_tcf_scan<3><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
@@ -408,7 +411,13 @@ appd_status launch_tcf_scan(appd_ctx* c, int pass, const TcParams& P) {
   } else if (ep == 6) {
     cudaFuncSetAttribute(k_tcf_scan<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     k_tcf_scan<6><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
-  } else if (pass == 0) k_tcf_scan<0><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
+  }
+  if (ep >= 3 && ep <= 6) {
+    APPD_LAUNCHED(c);
+    return APPD_OK;
+  }
+#endif
+  if (pass == 0) k_tcf_scan<0><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
   else if (pass == 1) k_tcf_scan<0, true><<<grid, EpiCfg<true>::threads, smem, c->stream>>>(P);
   else if (pass == 7) k_tcf_scan<7><<<grid, EpiCfg<false>::threads, smem, c->stream>>>(P);
   else k_tcf_scan<2><<<1, EpiCfg<false>::threads, smem, c->stream>>>(P);

@@ -127,9 +127,11 @@ appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int6
   int64_t T = (rows + VT - 1) / VT;
   int64_t pairs = T * (T + 1) / 2;
   if (pairs > 0x7FFFFFFFll) return fail(c, APPD_ERR_UNSUPPORTED, "validation grid too large");
-  k_validate_square<<<(unsigned)pairs, 256, 0, c->stream>>>(W, n, row0, rows, T, out3);
-  APPD_LAUNCHED(c);
-  if (rows < n) {
+  if (pairs > 0) {
+    k_validate_square<<<(unsigned)pairs, 256, 0, c->stream>>>(W, n, row0, rows, T, out3);
+    APPD_LAUNCHED(c);
+  }
+  if (rows > 0 && rows < n) {
     k_validate_finite_rest<<<c->sm_count * 8, 256, 0, c->stream>>>(W, n, row0, rows, out3);
     APPD_LAUNCHED(c);
   }
@@ -165,6 +167,38 @@ appd_status launch_validate_points(appd_ctx* c, const float* X, int64_t n, int64
   if (grid > c->sm_count * 16) grid = c->sm_count * 16;
   if (grid < 1) grid = 1;
   k_validate_points<<<grid, 256, 0, c->stream>>>(X, total, out3);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+}  // namespace appd
+
+namespace appd {
+
+// Solve-start agreement (world > 1): a position-keyed 64-bit checksum of
+// the input words, sum over i of mix(i * phi + bits(x_i)) mod 2^64 (order-free to
+// compute, position- and value-sensitive), so ranks holding different X disagree.
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) k_checksum_words(const uint32_t* __restrict__ x, int64_t count,
+                                                        u64* __restrict__ out) {
+  u64 acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    acc += mix64((u64)i * 0x9E3779B97F4A7C15ull + __ldg(x + i));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+appd_status launch_checksum_words(appd_ctx* c, const void* x, int64_t count, u64* out) {
+  APPD_CUDA(c, cudaMemsetAsync(out, 0, sizeof(u64), c->stream));
+  if (count <= 0) return APPD_OK;
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, (int64_t)c->sm_count * 4);
+  k_checksum_words<<<grid, 256, 0, c->stream>>>(reinterpret_cast<const uint32_t*>(x), count, out);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -10,9 +10,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "internal.cuh"
 
@@ -26,6 +28,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclGetErrorString) errorString = nullptr;
   decltype(&ncclCommGetAsyncError) asyncError = nullptr;
+  decltype(&ncclCommAbort) commAbort = nullptr;
 };
 
 static NcclApi g_nccl;
@@ -48,6 +51,7 @@ static bool load_nccl(std::string* err) {
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(so, "ncclCommDestroy");
   g_nccl.errorString = (decltype(g_nccl.errorString))dlsym(so, "ncclGetErrorString");
   g_nccl.asyncError = (decltype(g_nccl.asyncError))dlsym(so, "ncclCommGetAsyncError");
+  g_nccl.commAbort = (decltype(g_nccl.commAbort))dlsym(so, "ncclCommAbort");
   if (!g_nccl.getUniqueId || !g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.commDestroy) {
     if (err) *err = "libnccl.so.2 lacks a required symbol";
     return false;
@@ -70,6 +74,7 @@ appd_status nccl_unique_id(uint8_t out[128], std::string* err) {
 }
 
 appd_status nccl_init(appd_ctx* c, const uint8_t* idbytes, int rank, int world) {
+  if (c->opt.host_allreduce) return APPD_OK;  // host exchange backend: no communicator
   std::string err;
   if (!load_nccl(&err)) return fail(c, APPD_ERR_NCCL, "%s", err.c_str());
   ncclUniqueId id;
@@ -84,12 +89,75 @@ appd_status nccl_init(appd_ctx* c, const uint8_t* idbytes, int rank, int world) 
   return APPD_OK;
 }
 
+// a failed or timed-out collective: abort the communicator (peers blocked in it return
+// with an error instead of hanging) and poison the context
+static appd_status nccl_abort(appd_ctx* c, const char* why) {
+  if (c->nccl_comm && g_nccl.commAbort) g_nccl.commAbort((ncclComm_t)c->nccl_comm);
+  c->nccl_comm = nullptr;
+  c->poisoned = true;
+  return fail(c, APPD_ERR_NCCL, "%s", why);
+}
+
+// Wait for the context stream.  One rank, or the host exchange backend (whose callback
+// blocks on the host): a plain synchronisation.  NCCL backend: poll the stream and the
+// communicator's asynchronous error against the deadline opt.timeout_ms, so a dead or
+// diverged peer ends the call with APPD_ERR_NCCL instead of a hang.
+appd_status sync_stream(appd_ctx* c) {
+  if (c->opt.world == 1 || !c->nccl_comm) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    return e == cudaSuccess ? APPD_OK : cuda_fail(c, e, "cudaStreamSynchronize");
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t limit_ms = c->opt.timeout_ms > 0 ? c->opt.timeout_ms : 300000;
+  for (int spin = 0;; spin++) {
+    cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) return APPD_OK;
+    if (e != cudaErrorNotReady) return cuda_fail(c, e, "cudaStreamQuery");
+    if (g_nccl.asyncError) {
+      ncclResult_t ar = ncclSuccess;
+      if (g_nccl.asyncError((ncclComm_t)c->nccl_comm, &ar) != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "NCCL asynchronous error: %s", g_nccl.errorString ? g_nccl.errorString(ar) : "?");
+        return nccl_abort(c, msg);
+      }
+    }
+    const int64_t el = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (el > limit_ms) {
+      char msg[160];
+      snprintf(msg, sizeof msg, "collective wait exceeded timeout_ms = %lld (a peer rank is missing or diverged)",
+               (long long)limit_ms);
+      return nccl_abort(c, msg);
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// host exchange backend: device words -> pinned host -> user all-reduce -> device
+static appd_status host_allreduce(appd_ctx* c, u64* buf, int64_t count, int op) {
+  if (count <= 0) return APPD_OK;
+  if ((int64_t)c->host_xchg.size() < count) c->host_xchg.resize(count);
+  u64* h = c->host_xchg.data();
+  APPD_CUDA(c, cudaMemcpyAsync(h, buf, sizeof(u64) * count, cudaMemcpyDeviceToHost, c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));
+  const int32_t r = c->opt.host_allreduce(c->opt.host_allreduce_user, reinterpret_cast<uint64_t*>(h), count, op);
+  if (r != 0) {
+    c->poisoned = true;
+    return fail(c, APPD_ERR_NCCL, "host_allreduce callback returned %d", (int)r);
+  }
+  APPD_CUDA(c, cudaMemcpyAsync(buf, h, sizeof(u64) * count, cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaStreamSynchronize(c->stream));  // h is reused by the next exchange
+  return APPD_OK;
+}
+
 static appd_status allreduce(appd_ctx* c, u64* buf, int64_t count, ncclRedOp_t op) {
+  c->stats.collectives++;
+  if (c->opt.host_allreduce) return host_allreduce(c, buf, count, op == ncclMin ? APPD_REDUCE_MIN : APPD_REDUCE_MAX);
   if (!c->nccl_comm) return fail(c, APPD_ERR_NCCL, "no communicator");
   ncclResult_t r = g_nccl.allReduce(buf, buf, (size_t)count, ncclUint64, op, (ncclComm_t)c->nccl_comm, c->stream);
   if (r != ncclSuccess) {
-    c->poisoned = true;
-    return fail(c, APPD_ERR_NCCL, "ncclAllReduce: %s", g_nccl.errorString ? g_nccl.errorString(r) : "?");
+    char msg[160];
+    snprintf(msg, sizeof msg, "ncclAllReduce: %s", g_nccl.errorString ? g_nccl.errorString(r) : "?");
+    return nccl_abort(c, msg);
   }
   return APPD_OK;
 }

@@ -35,3 +35,24 @@ def create_distributed_context(device: int, stream=None, group=None, **kw) -> Co
     rank = dist.get_rank(group)
     nid = broadcast_nccl_id(group=group) if world > 1 else None
     return Context(device=device, stream=stream, rank=rank, world=world, nccl_id=nid, **kw)
+
+
+def gloo_host_allreduce(group=None):
+    """A host exchange backend (appd_options.host_allreduce) over torch.distributed: the
+    uint64 words are all-reduced in place on the CPU (gloo), unsigned order kept by flipping
+    the sign bit into int64.  Lets N processes drive libappd's world > 1 path without NCCL
+    (MPI-style deployments, and the multi-process tests on one GPU)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from .binding import REDUCE_MIN
+
+    sign = np.uint64(1 << 63)
+
+    def allreduce(words, op):
+        t = torch.from_numpy((words ^ sign).view(np.int64).copy())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN if op == REDUCE_MIN else dist.ReduceOp.MAX, group=group)
+        words[:] = t.numpy().view(np.uint64) ^ sign
+
+    return allreduce

@@ -270,6 +270,18 @@ def test_points_stream_to_host(ctx):
         assert_bit_equal(got, gpu_points(ctx, X), f"stream vs device {kind} n={n}")
 
 
+def test_points_stream_tile_span_256(ctx):
+    """Regression (round 2): a fill tile whose rows' leaf positions span exactly 256 read
+    level 8 of the tile's 8-level shared-memory table (out of bounds).  Blocks of 128
+    original rows at n = 257 span 256 positions whenever a block holds both end leaves;
+    over 24 inputs that happens many times.  Each result must equal the oracle."""
+    for t in range(24):
+        X = G.random_points(257, 2, 4000 + t, "uniform")
+        M = torch.empty((257, 257), dtype=torch.float32).pin_memory()
+        ctx.solve_points_stream(torch.from_numpy(X), M, 128)
+        assert_bit_equal(M.numpy(), oracle.appd_points(X), f"span-256 stream seed {4000 + t}")
+
+
 def test_points_stream_large_vs_device(ctx):
     """32768 points (4 GiB of output) in 3000-row blocks against the device path."""
     X = G.config("C4", n=32768)
@@ -333,14 +345,13 @@ def test_points_too_large_for_the_filter(P):
         assert c.stats()["points_engine"] == 2
 
 
-def test_points_list_overflow_is_exact(P, monkeypatch):
+def test_points_list_overflow_is_exact(P):
     """A candidate list far too small for the input: rows whose entries are lost are
     poisoned (invalid cache, exact full-row minimum, re-scanned every round), and the
     result must not change."""
     X = G.random_points(3000, 16, 901, "blobs")
     ref = oracle.appd_points(X)
-    monkeypatch.setenv("APPD_TEST_LIST_CAP", "5000")
-    c = P.Context(timing=True)
+    c = P.Context(timing=True, list_cap=5000)
     try:
         assert_bit_equal(gpu_points(c, X), ref, "list overflow")
         st = c.stats()
