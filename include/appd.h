@@ -74,10 +74,17 @@ typedef enum {
 
 /* MST variant (appd_options.variant) */
 #define APPD_VARIANT_AUTO 0
-#define APPD_VARIANT_PRIM 1    /* Prim's n sequential steps: not built on the GPU — a
-                                  grid-wide barrier per step loses to Borůvka at every size measured;
-                                  appd_create rejects it with APPD_ERR_UNSUPPORTED (the oracle is Prim) */
+#define APPD_VARIANT_PRIM 1    /* Prim's n - 1 sequential steps in ONE persistent
+                                  CTA with the input in shared memory; it emits the leaf order and merge
+                                  heights directly (no edge sort, no dendrogram build) and validates the
+                                  input in the same launch.  Fits weights n <= 300 and points with
+                                  n * (d + 3) <= ~56K words and n <= 2048; needs the whole input (not with
+                                  sharded weights, the streamed output or fp64): otherwise a solve returns
+                                  APPD_ERR_UNSUPPORTED.  Points with world > 1 run it on every rank. */
 #define APPD_VARIANT_BORUVKA 2 /* row-parallel Boruvka rounds (any n, shards over ranks) */
+/* APPD_VARIANT_AUTO takes Prim where it fits and is faster by measurement (weights n <= 300;
+ * points n <= 1024 with n * (d + 8) <= 20480, default engine; profiles/r02/crossover.txt),
+ * else Boruvka. */
 
 typedef struct {
   uint32_t struct_size;          /* = sizeof(appd_options); set by appd_options_init */

@@ -137,7 +137,6 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return APPD_ERR_INVALID_ARGUMENT;
   if (o.sense != 1 && o.sense != -1) return APPD_ERR_INVALID_ARGUMENT;
   if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
-  if (o.variant == APPD_VARIANT_PRIM) return APPD_ERR_UNSUPPORTED;  // not built (appd.h)
   if (o.metric < 0 || o.metric > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.world > 1 && !o.nccl_unique_id && !o.host_allreduce) return APPD_ERR_INVALID_ARGUMENT;
   if (o.timeout_ms < 0 || o.list_cap < 0) return APPD_ERR_INVALID_ARGUMENT;
@@ -381,6 +380,100 @@ static void dev_check(appd_ctx* c, const char* what, const int32_t* d_eu, const 
 }
 #endif
 
+// ---------------------------------------------------------------------------
+// The Prim variant (k_prim.cu): one single-CTA launch validates the
+// input, runs Prim's n - 1 steps and writes (pi, h) with the fill's preparation; the fill
+// follows.  AUTO takes it below the measured crossover with Boruvka (DESIGN.md §5,
+// profiles/r02/crossover.txt); it needs the whole input, so sharded weights (world > 1)
+// and the streamed output always take Boruvka; points with world > 1 run it replicated.
+// measured (profiles/r02/crossover.txt, whole solves): weights -- Prim wins at every n it
+// fits (n <= 300: 0.08-0.14 ms against 0.32-0.39 ms); points -- Prim wins while one SM's
+// O(n^2 d) distance work stays small: n = 1024 at d = 2 (0.46 vs 0.68 ms), n = 256 at
+// d = 16 and d = 64, and loses at n = 2048 (d = 2), n = 1024 (d = 16), n = 512 (d = 64)
+constexpr int64_t kPrimAutoMaxWeights = 300;
+constexpr int64_t kPrimAutoMaxPoints = 1024, kPrimAutoMaxPointWork = 20480;  // n * (d + 8)
+
+static bool prim_requested(const appd_ctx* c) { return c->opt.variant == APPD_VARIANT_PRIM; }
+
+static bool want_prim(const appd_ctx* c, int64_t n, int64_t d, bool points, bool f64) {
+  if (f64 || c->stream_out || n < 2) return false;
+  if (!points && c->opt.world > 1) return false;
+  if (!prim_fits(n, d, points)) return false;
+  if (prim_requested(c)) return true;
+  if (c->opt.variant != APPD_VARIANT_AUTO) return false;
+  if (points && c->opt.points_engine != 0) return false;
+  if (!points) return n <= kPrimAutoMaxWeights;
+  return n <= kPrimAutoMaxPoints && n * (d + 8) <= kPrimAutoMaxPointWork;
+}
+
+static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
+  const bool points = X != nullptr;
+  const int sense = points ? 1 : c->opt.sense;
+  int64_t row0, rows;
+  appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
+  c->stats.variant = APPD_VARIANT_PRIM;
+  c->stats.dendrogram = 0;
+  const int64_t m = n - 1;
+  int levels = 1;
+  while ((1ll << levels) <= m) levels++;
+  int* pi = (int*)ws(c, S_PI, sizeof(int) * n);
+  int* pos = (int*)ws(c, S_POS, sizeof(int) * n);
+  int* rowpos = (int*)ws(c, S_ROWPOS, sizeof(int) * n);
+  float* ST = (float*)ws(c, S_ST, sizeof(float) * m * levels);
+  if (!pi || !pos || !rowpos || !ST) return fail(c, APPD_ERR_OUT_OF_MEMORY, "Prim workspace (n = %lld)", (long long)n);
+  u64* bad = nullptr;
+  u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);
+  if (c->opt.validate) {
+    bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
+    if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
+    APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
+  }
+  stage_event(c, 1);
+  // small n: the same launch also fills M (prim_fuses_fill); rows == 0: nothing to fill
+  const bool fused = prim_fuses_fill(n) && rows > 0;
+  appd_status s = launch_prim(c, W, X, n, d, sense, points ? c->opt.metric : 0, bad, pi, pos, rowpos, ST, m, levels,
+                              fused ? M : nullptr, row0, rows);
+  if (s) return s;
+  if (bad) APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+  for (int e = 2; e <= 4; e++) stage_event(c, e);
+  const int* rows_sorted = pi;
+  if (c->opt.world > 1 && !fused) {  // replicated Prim, this rank's rows in leaf order
+    int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (rows + 1));
+    int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (rows + 1));
+    if (!keys || !rs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
+    if ((s = launch_gather_rowpos(c, pos, row0, rows, keys, keys + rows + 1))) return s;
+    if ((s = sort_pairs_i32(c, keys, rowpos, keys + rows + 1, rs, rows))) return s;
+    rows_sorted = rs;
+  }
+  stage_event(c, 5);
+  if (!fused && (s = launch_fill(c, rows_sorted, rowpos, rows, pos, ST, m, n, M, row0, sense < 0))) return s;
+  stage_event(c, 6);
+  APPD_SYNC(c);
+  if (bad) {
+    u64 hb[3];
+    memcpy(hb, hbad, sizeof hb);
+    if ((s = report_validation(c, hb, n, points, d))) return s;
+  }
+  c->dend_pi = pi;
+  c->dend_h = ST;
+  c->dend_on_device = true;
+  c->dend_n = n;
+  c->have_dendrogram = true;
+  c->stats.rounds = 0;
+  c->stats.fill_bytes = rows * n * 4;
+  c->stats.kernel_launches = c->launches;
+  if (c->opt.timing) {
+    c->stats.ms_validate = ev_ms(c, 0, 1);
+    c->stats.ms_mst = ev_ms(c, 1, 2);
+    c->stats.ms_sort = ev_ms(c, 2, 3);
+    c->stats.ms_dendrogram = ev_ms(c, 3, 4);
+    c->stats.ms_prep = ev_ms(c, 4, 5);
+    c->stats.ms_fill = ev_ms(c, 5, 6);
+    c->stats.ms_total = ev_ms(c, 0, 6);
+  }
+  return APPD_OK;
+}
+
 // The whole pipeline.  X (points) or W (weights) is a device pointer.
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
@@ -405,6 +498,12 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (sa) return sa;
   }
   stage_event(c, 0);
+  if (n >= 2 && !f64 && want_prim(c, n, d, points, f64)) return solve_prim(c, W, X, n, d, M);
+  if (prim_requested(c) && n >= 2)
+    return fail(c, APPD_ERR_UNSUPPORTED,
+                "variant PRIM: n = %lld does not fit one CTA (weights n <= 300; points n <= 2048 and n * (d + 3) "
+                "words <= 56K), or the call needs the whole input (sharded weights, streamed output, fp64)",
+                (long long)n);
 
   // ---- a1: validation ----
   // Points mode with the tensor-core engine: the verdict is copied asynchronously and

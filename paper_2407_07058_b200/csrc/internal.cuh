@@ -370,10 +370,14 @@ appd_status launch_points_weights(appd_ctx* c, const float* X, int64_t n, int64_
                                   float* Wb);
 appd_status launch_gather_rowpos(appd_ctx* c, const int* pos, int64_t row0, int64_t rows, int* keys, int* vals);
 
-// Prim (single CTA)
-appd_status launch_prim_points(appd_ctx* c, const float* X, int64_t n, int64_t d, int* pi, float* h, void* scratch);
-appd_status launch_prim_weights(appd_ctx* c, const float* W, int64_t n, int sense, int* pi, float* h, void* scratch);
-int prim_max_n();
+// Prim variant (k_prim.cu): one persistent CTA; validation fused (bad != nullptr), then
+// pi, pos, rowpos = iota and the whole sparse table over h
+// (small n: M != nullptr also writes this rank's rows of the APPD in the same launch)
+bool prim_fits(int64_t n, int64_t d, bool points);
+bool prim_fuses_fill(int64_t n);
+appd_status launch_prim(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, int sense, int metric,
+                        u64* bad, int* pi, int* pos, int* rowpos, float* ST, int64_t stride, int levels, float* M,
+                        int64_t row0, int64_t rows);
 
 // sorting (CUB)
 appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count);

@@ -320,35 +320,47 @@ appd_status launch_fill_f64(appd_ctx* c, const int* rows_sorted, const int* rowp
   return APPD_OK;
 }
 
+template <int VEC, bool WIDEST>
+static void fill_rt(appd_ctx* c, int rt, dim3 g, const int* rows_sorted, const int* rowpos, int64_t nrows,
+                    const int* pos, const float* ST, int64_t stride, int64_t n, float* M, int64_t row0) {
+  switch (rt) {
+    case 128: k_fill<VEC, WIDEST, 0, 128><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0); break;
+    case 64: k_fill<VEC, WIDEST, 0, 64><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0); break;
+    case 32: k_fill<VEC, WIDEST, 0, 32><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0); break;
+    case 16: k_fill<VEC, WIDEST, 0, 16><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0); break;
+    default: k_fill<VEC, WIDEST, 0, 8><<<g, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0); break;
+  }
+}
+
+// Tile shape: VEC consecutive columns per thread (32-byte stores when n allows and every
+// thread still has columns), RT rows per tile.  Large outputs: 128-row tiles; smaller ones
+// shrink the tile (64, then down to 8 rows) until there are at least two waves of the 4
+// resident CTAs per SM -- a small fill is latency-bound, so it needs CTAs, not long tiles
+// (C1, n = 256: 60 us with four 64-row tiles of 32 busy threads each).
 appd_status launch_fill(appd_ctx* c, const int* rows_sorted, const int* rowpos, int64_t nrows, const int* pos,
                         const float* ST, int64_t stride, int64_t n, float* M, int64_t row0, int widest) {
   if (nrows <= 0) return APPD_OK;
   const bool vec8 = (n % 8) == 0 && ((uintptr_t)M % 32) == 0;
   const bool vec4 = (n % 4) == 0 && ((uintptr_t)M % 16) == 0;
-  const int cols_per_cta = FILL_THREADS * (vec8 ? 8 : vec4 ? 4 : 1);
-  dim3 grid((unsigned)((n + cols_per_cta - 1) / cols_per_cta), (unsigned)((nrows + FILL_R - 1) / FILL_R));
-  if (grid.y > 65535u) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
   // 32-byte stores by default (measured: fewer instructions per byte); APPD_FILL_VEC=4 picks 16-byte
   static const int want = dev_env("APPD_FILL_VEC") ? atoi(dev_env("APPD_FILL_VEC")) : 8;
-  // small matrices: 64-row tiles when 128-row tiles would leave fewer than ~6 waves of
-  // the 4 resident CTAs per SM (the last, partial wave dominates)
-  const bool small = (int64_t)grid.x * grid.y < (int64_t)c->sm_count * 4 * 6;
-  if (vec8 && want == 8 && small) {
-    dim3 g64(grid.x, (unsigned)((nrows + 63) / 64));
-    if (widest) k_fill<8, true, 0, 64><<<g64, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<8, false, 0, 64><<<g64, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-  } else if (vec8 && want == 8) {
-    if (widest) k_fill<8, true, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<8, false, 0><<<grid, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-  } else if (vec4) {
-    dim3 g4((unsigned)((n + FILL_THREADS * 4 - 1) / (FILL_THREADS * 4)), grid.y);
-    if (widest) k_fill<4, true, 0><<<g4, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<4, false, 0><<<g4, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-  } else {
-    dim3 g1((unsigned)((n + FILL_THREADS - 1) / FILL_THREADS), grid.y);
-    if (widest) k_fill<1, true><<<g1, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
-    else k_fill<1, false><<<g1, FILL_THREADS, 0, c->stream>>>(rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  const int vec = (vec8 && want == 8 && n >= FILL_THREADS * 8) ? 8 : (vec4 && n >= FILL_THREADS * 4) ? 4 : 1;
+  const int64_t gx = (n + FILL_THREADS * vec - 1) / (FILL_THREADS * vec);
+  auto ctas = [&](int rt) { return gx * ((nrows + rt - 1) / rt); };
+  const int64_t waves = (int64_t)c->sm_count * 4;
+  int rt = 128;
+  if (ctas(128) < 6 * waves) {
+    rt = 64;
+    while (rt > 8 && ctas(rt) < 2 * waves) rt /= 2;
   }
+  const dim3 g((unsigned)gx, (unsigned)((nrows + rt - 1) / rt));
+  if ((nrows + rt - 1) / rt > 65535) return fail(c, APPD_ERR_UNSUPPORTED, "fill grid too large");
+  if (vec == 8) widest ? fill_rt<8, true>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0)
+                       : fill_rt<8, false>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  else if (vec == 4) widest ? fill_rt<4, true>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0)
+                            : fill_rt<4, false>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
+  else widest ? fill_rt<1, true>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0)
+              : fill_rt<1, false>(c, rt, g, rows_sorted, rowpos, nrows, pos, ST, stride, n, M, row0);
   APPD_LAUNCHED(c);
   c->stats.fill_launches++;
   return APPD_OK;

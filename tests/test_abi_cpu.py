@@ -84,8 +84,14 @@ def test_options_defaults_and_create_without_gpu(lib):
     bad.struct_size = 3
     assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
     lib.appd_options_init(ctypes.byref(bad))
-    bad.variant = 1  # Prim: documented as not built
-    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 5
+    bad.variant = 3  # variants are 0 (AUTO), 1 (PRIM), 2 (BORUVKA)
+    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
+    lib.appd_options_init(ctypes.byref(bad))
+    bad.timeout_ms = -1
+    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
+    lib.appd_options_init(ctypes.byref(bad))
+    bad.world, bad.rank = 2, 0  # world > 1 needs an NCCL id or a host exchange callback
+    assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
     lib.appd_options_init(ctypes.byref(bad))
     bad.metric = 3  # metrics are 0, 1, 2
     assert lib.appd_create(ctypes.byref(h), ctypes.byref(bad)) == 1
@@ -123,3 +129,32 @@ def _load_fresh(path):
     finally:
         B._lib = saved
         importlib.invalidate_caches()
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of appd_options / appd_stats have the C header's size and field
+    offsets (gcc compiles a probe against include/appd.h)."""
+    import subprocess
+
+    import paper_2407_07058_b200.binding as B
+
+    probe = tmp_path / "probe.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "appd.h"', "int main(void) {"]
+    for struct, cls in (("appd_options", B.appd_options), ("appd_stats", B.appd_stats)):
+        lines.append(f'printf("{struct} size %zu\\n", sizeof({struct}));')
+        for name, _ in cls._fields_:
+            lines.append(f'printf("{struct} {name} %zu\\n", offsetof({struct}, {name}));')
+    lines += ["return 0; }"]
+    probe.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    got = {}
+    for line in out:
+        if line:
+            st, name, val = line.split()
+            got[(st, name)] = int(val)
+    for struct, cls in (("appd_options", B.appd_options), ("appd_stats", B.appd_stats)):
+        assert got[(struct, "size")] == ctypes.sizeof(cls), struct
+        for name, _ in cls._fields_:
+            assert got[(struct, name)] == getattr(cls, name).offset, (struct, name)

@@ -77,23 +77,33 @@ def test_c1(ctx):
     assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), "C1")
 
 
+@pytest.fixture(scope="module")
+def bctx(P):
+    """Boruvka forced (AUTO takes the Prim variant for the small sizes below)."""
+    c = P.Context(timing=True, variant=P.VARIANT_BORUVKA)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("variant", ["auto", "boruvka"])
 @pytest.mark.parametrize("kind", ["uniform", "ties", "ints255", "negative", "signed_zero", "huge"])
-def test_random_weights(ctx, kind):
+def test_random_weights(ctx, bctx, kind, variant):
+    c = ctx if variant == "auto" else bctx
     rs = np.random.default_rng(11)
     sizes = [1, 2, 3, 4, 5, 7, 8, 31, 33, 127, 128, 129, 255, 257, 300, 513, 1000, 1024, 1031]
     for t, n in enumerate(sizes):
         W = G.random_weights(n, 100 + t, kind)
-        assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), f"{kind} n={n}")
+        assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), f"{kind} n={n}")
     for t in range(40):
         n = int(rs.integers(2, 200))
         W = G.random_weights(n, 500 + t, kind)
-        assert_bit_equal(gpu_weights(ctx, W), oracle.appd_weights(W), f"{kind} n={n}")
+        assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), f"{kind} n={n}")
 
 
 @pytest.mark.parametrize("topk", [0, -1, 4, 32])
 def test_weights_cache_lengths(P, topk):
     """Weights mode with and without the round-0 candidate cache (several K), incl. ties."""
-    c = P.Context(timing=True, topk=topk)
+    c = P.Context(timing=True, topk=topk, variant=P.VARIANT_BORUVKA)
     try:
         for t, (n, kind) in enumerate([(300, "uniform"), (257, "ties"), (700, "ints255"), (129, "negative"),
                                        (1000, "ties")]):
@@ -103,8 +113,9 @@ def test_weights_cache_lengths(P, topk):
         c.close()
 
 
-def test_widest_sense(P):
-    with P.Context(sense=-1) as cw:
+@pytest.mark.parametrize("variant", [0, 2])
+def test_widest_sense(P, variant):
+    with P.Context(sense=-1, variant=variant) as cw:
         for t, n in enumerate([2, 3, 17, 64, 255, 600]):
             for kind in ("uniform", "ties", "negative"):
                 W = G.random_weights(n, t, kind)
@@ -190,13 +201,15 @@ def test_c2(ctx):
     assert_bit_equal(gpu_points(ctx, X), oracle.appd_points(X), "C2")
 
 
+@pytest.mark.parametrize("variant", ["auto", "boruvka"])
 @pytest.mark.parametrize("kind", ["uniform", "blobs", "dups", "grid", "wide"])
-def test_random_points(ctx, kind):
+def test_random_points(ctx, bctx, kind, variant):
+    c = ctx if variant == "auto" else bctx
     cases = [(1, 3), (2, 1), (3, 2), (5, 64), (64, 1), (127, 33), (128, 32), (129, 31), (300, 2), (513, 65),
              (1000, 16), (1031, 70), (2048, 3)]
     for t, (n, d) in enumerate(cases):
         X = G.random_points(n, d, 40 + t, kind)
-        assert_bit_equal(gpu_points(ctx, X), oracle.appd_points(X), f"{kind} n={n} d={d}")
+        assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), f"{kind} n={n} d={d}")
 
 
 # every points-mode engine configuration: the tensor-core filter with and
@@ -337,7 +350,7 @@ def test_points_too_large_for_the_filter(P):
     rs = np.random.default_rng(8)
     X = (rs.standard_normal((300, 6)) * 1e20).astype(np.float32)
     X[:150] *= np.float32(1e-20)  # half of the points at ordinary scale
-    with P.Context(timing=True) as c:
+    with P.Context(timing=True, variant=P.VARIANT_BORUVKA) as c:
         assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), "huge coordinates")
         assert c.stats()["points_engine"] == 1
         Xs = G.random_points(500, 8, 3, "blobs")  # the same context keeps working afterwards
@@ -412,16 +425,37 @@ def test_c4_full(ctx):
     torch.cuda.empty_cache()
 
 
+def hash_row_blocks(M, block_rows, workers=8):
+    """FNV-1a-64 of every block of block_rows rows of the device matrix M (host copies one
+    block at a time; the C hash runs in threads, ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    nb = (M.shape[0] + block_rows - 1) // block_rows
+
+    def one(b):
+        return f"{oracle.fnv1a64(M[b * block_rows:(b + 1) * block_rows].cpu().numpy()):016x}"
+
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(one, range(nb)))
+
+
 def test_c5_full_single_gpu(ctx):
+    """C5 (n = 131072, 64 GiB) on one GPU against the oracle: EVERY 1024-row block's
+    FNV-1a-64 equals tests/golden/C5.json (the oracle's R5 row windows: every
+    cell), plus the closed-form count of zero merge heights."""
     X = G.config("C5")
     Xt = torch.from_numpy(X).cuda()
     M = ctx.solve_points(Xt)
     pi, h = ctx.last_dendrogram(X.shape[0])
     assert (h == 0).sum() == 1311  # SURVEY §8(c) pin 5: exactly 1311 zero merge heights
     _properties(M, X, np.sort(h))
-    for name in ("C5_r0.json", "C5_r65536.json"):
-        if os.path.exists(os.path.join(GOLD, name)):
-            _check_golden(lambda r, c: M[r:r + c].cpu().numpy(), "C5", name)
+    path = os.path.join(GOLD, "C5.json")
+    g = json.load(open(path))
+    assert oracle.fnv1a64(X) == g["input_fnv1a64"], "input generator drifted"
+    assert g["rows"] == X.shape[0] and len(g["row_block_fnv1a64"]) == 128
+    got = hash_row_blocks(M, g["block_rows"])
+    bad = [b for b, (x, y) in enumerate(zip(got, g["row_block_fnv1a64"])) if x != y]
+    assert not bad, f"C5 row blocks differing from the oracle: {bad[:10]} ({len(bad)} of 128)"
     del M
     torch.cuda.empty_cache()
 
@@ -575,3 +609,87 @@ def test_f64_validation(ctx, P):
     assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (2, 50)
     with pytest.raises(TypeError):
         ctx.solve_weights_f64(torch.zeros((4, 4), dtype=torch.float32, device="cuda"))
+
+
+# --------------------------------------------------------------------------
+# the Prim variant: one CTA, (pi, h) directly
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", ["uniform", "ties", "ints255", "negative", "signed_zero", "huge"])
+def test_prim_variant_weights(P, kind):
+    with P.Context(variant=P.VARIANT_PRIM, timing=True) as c:
+        for t, n in enumerate([2, 3, 5, 31, 32, 33, 64, 127, 255, 256, 299, 300]):
+            W = G.random_weights(n, 700 + t, kind)
+            assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), f"prim {kind} n={n}")
+            st = c.stats()
+            assert st["variant"] == P.VARIANT_PRIM and st["rounds"] == 0
+    with P.Context(variant=P.VARIANT_PRIM, sense=-1) as c:
+        for t, n in enumerate([2, 17, 200, 300]):
+            W = G.random_weights(n, 720 + t, kind)
+            assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W, -1), f"prim widest {kind} n={n}")
+
+
+def test_prim_variant_c1_and_auto(P, ctx):
+    W = G.config("C1")
+    want = oracle.appd_weights(W)
+    with P.Context(variant=P.VARIANT_PRIM) as c:
+        assert_bit_equal(gpu_weights(c, W, c=c), want, "C1 prim")
+    assert_bit_equal(gpu_weights(ctx, W), want, "C1 auto")
+    assert ctx.stats()["variant"] == P.VARIANT_PRIM  # AUTO picks Prim at n = 256 (crossover table)
+    with P.Context(variant=P.VARIANT_BORUVKA) as c:
+        assert_bit_equal(gpu_weights(c, W, c=c), want, "C1 boruvka")
+        assert c.stats()["variant"] == P.VARIANT_BORUVKA
+
+
+@pytest.mark.parametrize("kind", ["uniform", "blobs", "dups", "grid", "clumps", "wide"])
+def test_prim_variant_points(P, kind):
+    with P.Context(variant=P.VARIANT_PRIM) as c:
+        for t, (n, d) in enumerate([(2, 1), (3, 2), (100, 3), (127, 2), (129, 4), (1023, 2), (1025, 5),
+                                    (2048, 2), (2000, 16), (700, 64)]):
+            X = G.random_points(n, d, 730 + t, kind)
+            assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), f"prim points {kind} n={n} d={d}")
+
+
+def test_prim_variant_c2_and_metrics(P):
+    X = G.config("C2", n=2048)  # the C2 recipe at the largest n the variant takes
+    want = oracle.appd_points(X)
+    with P.Context(variant=P.VARIANT_PRIM) as c:
+        assert_bit_equal(gpu_points(c, X), want, "C2 recipe n=2048 prim")
+    for metric in (1, 2):
+        Xm = G.random_points(1500, 6, 91 + metric, "blobs")
+        with P.Context(variant=P.VARIANT_PRIM, metric=metric) as c:
+            assert_bit_equal(gpu_points(c, Xm), oracle.appd_points(Xm, metric=metric), f"prim metric {metric}")
+
+
+def test_prim_variant_validation_and_limits(P):
+    with P.Context(variant=P.VARIANT_PRIM) as c:
+        W = G.random_weights(50, 3, "uniform")
+        W[7, 9] = np.float32(2.0)
+        with pytest.raises(P.AppdError) as e:
+            gpu_weights(c, W, c=c)
+        assert e.value.name == "APPD_ERR_NOT_SYMMETRIC" and e.value.index == (7, 9)
+        W = G.random_weights(50, 3, "uniform")
+        W[4, 4] = np.float32(1.0)
+        W[30, 2] = np.float32(np.nan)
+        W[2, 30] = np.float32(np.nan)
+        with pytest.raises(P.AppdError) as e:
+            gpu_weights(c, W, c=c)
+        assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (2, 30)
+        W = G.random_weights(50, 3, "uniform")
+        W[4, 4] = np.float32(1.0)
+        with pytest.raises(P.AppdError) as e:
+            gpu_weights(c, W, c=c)
+        assert e.value.name == "APPD_ERR_BAD_DIAGONAL" and e.value.index == (4, 4)
+        X = G.random_points(300, 3, 5, "uniform")
+        X[17, 1] = np.float32(np.inf)
+        with pytest.raises(P.AppdError) as e:
+            gpu_points(c, X)
+        assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index == (17, 1)
+        # too large for one CTA: explicit PRIM is refused, AUTO takes Boruvka
+        with pytest.raises(P.AppdError) as e:
+            gpu_weights(c, G.random_weights(301, 3, "uniform"), c=c)
+        assert e.value.name == "APPD_ERR_UNSUPPORTED"
+        with pytest.raises(P.AppdError) as e:
+            gpu_points(c, G.random_points(2049, 2, 3, "uniform"))
+        assert e.value.name == "APPD_ERR_UNSUPPORTED"
+        W = G.random_weights(50, 3, "ties")
+        assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), "after errors")

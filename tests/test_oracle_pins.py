@@ -521,3 +521,136 @@ def test_f64_equals_f32_on_representable_inputs(kind):
     M32 = oracle.appd_weights(W, 1)
     M64 = oracle.appd_weights_f64(W.astype(np.float64), 1)
     assert_f64_bit_equal(M64, M32.astype(np.float64))
+
+
+# --------------------------------------------------------------------------
+# round 2 pins: the L1 / L-inf chains on non-integer inputs (exact rational
+# arithmetic), and Prim (R2) against an independent Kruskal (no oracle code)
+# --------------------------------------------------------------------------
+def _metric_pair(xi, xj, metric):
+    X = np.stack([xi, xj]).astype(np.float32)
+    return oracle.points_weights(X, metric=metric)[0, 1]
+
+
+def l1_exact(xi, xj):
+    """S:L80 / DESIGN Q6 (metric 1): acc = +0; acc = fl32(acc + |fl32(x_k - y_k)|), k in order."""
+    acc = Fraction(0)
+    for a, b in zip(xi, xj):
+        t = abs(Fraction(float(round_f32(Fraction(float(a)) - Fraction(float(b))))))
+        acc = Fraction(float(round_f32(acc + t)))
+    return np.float32(float(acc))
+
+
+def linf_exact(xi, xj):
+    """metric 2: max over k of |fl32(x_k - y_k)| (a max of exactly rounded differences)."""
+    return np.float32(max(float(abs(Fraction(float(round_f32(Fraction(float(a)) - Fraction(float(b)))))))
+                          for a, b in zip(xi, xj)))
+
+
+def test_l1_matches_exact_rational_chain():
+    """300 random non-integer cases across magnitudes: every fp32 subtraction and every
+    partial sum rounds, so a double accumulator, a different summation order or an
+    unrounded difference changes some result bit."""
+    rs = np.random.default_rng(77)
+    for trial in range(300):
+        d = int(rs.integers(1, 17))
+        scale = 10.0 ** rs.integers(-5, 6)
+        xi = (rs.standard_normal(d) * scale).astype(np.float32)
+        xj = (rs.standard_normal(d) * scale * (10.0 ** rs.integers(-2, 3))).astype(np.float32)
+        assert bits(_metric_pair(xi, xj, 1)) == bits(l1_exact(xi, xj)), (trial, xi, xj)
+        assert bits(_metric_pair(xj, xi, 1)) == bits(l1_exact(xj, xi))
+
+
+def test_l1_order_sensitive_case():
+    """A case where the summation order decides the result: 1 + 2^-24 + 2^-24 is 1 in
+    k order (each add ties to even) but 1 + 2^-23 if the small terms were summed first."""
+    xi = np.array([1.0, 2.0 ** -24, 2.0 ** -24], np.float32)
+    xj = np.zeros(3, np.float32)
+    assert _metric_pair(xi, xj, 1) == np.float32(1.0)
+    assert bits(l1_exact(xi, xj)) == bits(np.float32(1.0))
+    xr = xi[::-1].copy()
+    assert _metric_pair(xr, xj, 1) == np.float32(1.0 + 2.0 ** -23)
+
+
+def test_linf_matches_exact_rational_max():
+    rs = np.random.default_rng(78)
+    for trial in range(300):
+        d = int(rs.integers(1, 17))
+        scale = 10.0 ** rs.integers(-5, 6)
+        xi = (rs.standard_normal(d) * scale).astype(np.float32)
+        xj = (rs.standard_normal(d) * scale * (10.0 ** rs.integers(-2, 3))).astype(np.float32)
+        assert bits(_metric_pair(xi, xj, 2)) == bits(linf_exact(xi, xj)), (trial, xi, xj)
+    # the rounded difference, not |x| - |y| or an fp64 difference: 1 - (-2^-30) rounds to 1
+    assert _metric_pair(np.array([1.0], np.float32), np.array([-(2.0 ** -30)], np.float32), 2) == np.float32(1.0)
+
+
+def kruskal_numpy(W):
+    """Kruskal's algorithm written here (not in oracle/): edges by (weight, i, j), union-find."""
+    n = W.shape[0]
+    iu, ju = np.triu_indices(n, 1)
+    order = np.lexsort((ju, iu, W[iu, ju].astype(np.float64)))
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    tree = []
+    for e in order:
+        a, b = find(int(iu[e])), find(int(ju[e]))
+        if a != b:
+            parent[a] = b
+            tree.append((int(iu[e]), int(ju[e]), W[iu[e], ju[e]]))
+    return tree
+
+
+def tree_path_appd(n, tree):
+    """APPD by the MST-path property: the largest weight on each tree path (numpy BFS)."""
+    adj = [[] for _ in range(n)]
+    for u, v, w in tree:
+        adj[u].append((v, w))
+        adj[v].append((u, w))
+    M = np.zeros((n, n), np.float32)
+    for s in range(n):
+        seen = np.zeros(n, bool)
+        seen[s] = True
+        stack = [(s, np.float32(-np.inf))]
+        while stack:
+            x, mx = stack.pop()
+            for y, w in adj[x]:
+                if not seen[y]:
+                    seen[y] = True
+                    m2 = max(mx, w)
+                    M[s, y] = m2
+                    stack.append((y, m2))
+    return M
+
+
+@pytest.mark.parametrize("kind", ["uniform", "ties", "ints255", "negative"])
+def test_prim_against_independent_kruskal(kind):
+    """R2 (Prim) pinned without going through oracle code twice: Prim's n-1 edges
+    form a spanning tree of W's own entries whose sorted weight multiset equals an
+    independent Kruskal's (all MSTs share it), and Algorithm 4 equals the path maxima of
+    the Kruskal tree -- so an error in prim() shared by the oracle's MST-path
+    checker cannot hide."""
+    for t, n in enumerate([2, 3, 5, 9, 17, 33, 64]):
+        W = G.random_weights(n, 900 + t, kind)
+        eu, ev, ew = oracle.prim_weights(W, 1)
+        assert len(ew) == n - 1
+        parent = list(range(n))
+
+        def find(x):
+            while parent[x] != x:
+                x = parent[x]
+            return x
+
+        for u, v, w in zip(eu, ev, ew):
+            assert u != v and bits(np.float32(w) + np.float32(0)) == bits(W[u, v] + np.float32(0))
+            a, b = find(int(u)), find(int(v))
+            assert a != b, "Prim closed a cycle"
+            parent[a] = b
+        kt = kruskal_numpy(W)
+        assert sorted(float(x) for x in ew) == sorted(float(w) for _, _, w in kt)
+        assert_bit_equal(oracle.appd_weights(W), tree_path_appd(n, kt) + np.float32(0))
