@@ -127,7 +127,10 @@ typedef struct {
                                     list, 0 = auto (32 n + 65536).  Rows whose candidates do not fit
                                     are answered exactly by a full-row scan, so a small value only
                                     slows the solve (used by the tests to force that path) */
-  int32_t reserved[4];
+  int32_t wide_keys;             /* points: 1 = the wide-key exact engine (two-step component reduction,
+                                    automatic above n = 131072) at any n -- the tests check it there
+                                    against the oracle; 0 (default) = automatic */
+  int32_t reserved[3];
 } appd_options;
 
 /* op argument of appd_options.host_allreduce */
@@ -179,7 +182,8 @@ appd_status appd_set_stream(appd_ctx* ctx, void* cuda_stream);
 appd_status appd_solve_weights(appd_ctx* ctx, const float* W, int64_t n, float* M);
 
 /* Points mode.  X: n x d (replicated on every rank); M: rows x n.  W is never
- * materialised; n <= 131072 (the packed 64-bit edge key). */
+ * materialised.  n <= 131072 packs (bits(d^2), pair index) into one 64-bit key (tensor-core
+ * engine); 131072 < n <= 2^20 uses wide keys on the exact engine (see appd_solve_points_sink). */
 appd_status appd_solve_points(appd_ctx* ctx, const float* X, int64_t n, int64_t d, float* M);
 
 /* The same with HOST buffers (pinned or pageable): copies X/W in and M out on
@@ -197,6 +201,18 @@ appd_status appd_solve_weights_host(appd_ctx* ctx, const float* W_host, int64_t 
  * 2 x block_rows x n floats. */
 appd_status appd_solve_points_stream(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, float* M_host,
                                      int64_t block_rows);
+
+/* NEXT-4, outputs beyond host memory too: as appd_solve_points_stream, but each block of
+ * block_rows rows (0: ~1 GiB) is handed to sink(user, row0, rows, block) in row order once
+ * its copy to a pinned staging buffer is complete -- block is rows x n fp32 row-major, valid
+ * only during the call -- while the GPU fills and copies the next block.  A non-zero return
+ * stops the solve with APPD_ERR_INVALID_ARGUMENT.  Points mode up to n = 2^20: above
+ * n = 131072 the 64-bit (weight, pair index) edge key does not fit, and the MST runs on
+ * the exact FP32 engine with a two-step component reduction (minimum weight, then minimum
+ * pair index among the ties; SURVEY §8(a) key note).  One rank only. */
+appd_status appd_solve_points_sink(appd_ctx* ctx, const float* X_host, int64_t n, int64_t d, int64_t block_rows,
+                                   int32_t (*sink)(void* user, int64_t row0, int64_t rows, const float* block),
+                                   void* user);
 
 /* NEXT-3 ("float64" weights): appd_solve_weights on an fp64 weight
  * matrix.  W: DEVICE n x n fp64 row-major; M: DEVICE n x n fp64, distinct from W.  The

@@ -36,6 +36,9 @@ HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POI
 # cudaStreamLegacy: the legacy default stream (torch's default stream has handle 0, which
 # appd_set_stream would read as "library-owned stream")
 CUDA_STREAM_LEGACY = 0x1
+# appd_solve_points_sink: int32 (*)(void* user, int64 row0, int64 rows, const float* block)
+BLOCK_SINK_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.POINTER(ctypes.c_float))
 
 
 class appd_options(ctypes.Structure):
@@ -59,7 +62,8 @@ class appd_options(ctypes.Structure):
         ("host_allreduce_user", ctypes.c_void_p),
         ("timeout_ms", ctypes.c_int32),
         ("list_cap", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 4),
+        ("wide_keys", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
 
@@ -108,7 +112,7 @@ class appd_stats(ctypes.Structure):
 
 EXPORTS = [
     "appd_options_init", "appd_create", "appd_set_stream", "appd_solve_weights", "appd_solve_points",
-    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_solve_points_stream", "appd_solve_weights_f64", "appd_destroy", "appd_row_range", "appd_row_range_of",
+    "appd_solve_points_host", "appd_solve_weights_host", "appd_floyd_weights", "appd_solve_points_stream", "appd_solve_points_sink", "appd_solve_weights_f64", "appd_destroy", "appd_row_range", "appd_row_range_of",
     "appd_points_weights", "appd_get_nccl_unique_id", "appd_get_stats", "appd_last_dendrogram",
     "appd_error_index", "appd_last_error", "appd_status_string", "appd_version",
 ]
@@ -138,6 +142,7 @@ def load(path: str | None = None):
     L.appd_floyd_weights.argtypes = [P, P, I64, P]
     L.appd_solve_weights_f64.argtypes = [P, P, I64, P]
     L.appd_solve_points_stream.argtypes = [P, P, I64, I64, P, I64]
+    L.appd_solve_points_sink.argtypes = [P, P, I64, I64, I64, BLOCK_SINK_FN, P]
     L.appd_destroy.restype = None
     L.appd_destroy.argtypes = [P]
     L.appd_row_range.argtypes = [P, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -213,7 +218,7 @@ class Context:
                  variant: int = VARIANT_AUTO, validate: bool = True, sense: int = 1, timing: bool = False,
                  dendrogram: int = 0, points_engine: int = 0, topk: int = 0,
                  finish_k: int = 0, metric: int = 0, host_allreduce=None, timeout_ms: int = 0,
-                 list_cap: int = 0):
+                 list_cap: int = 0, wide_keys: int = 0):
         """stream: a cudaStream_t handle (int) every call runs on; None (default) follows
         torch.cuda.current_stream(device) at each call, so the library's work is ordered
         with the torch kernels that produced its inputs and that read its outputs.
@@ -229,6 +234,7 @@ class Context:
         o.rank, o.world = rank, world
         o.timeout_ms = timeout_ms
         o.list_cap = list_cap
+        o.wide_keys = wide_keys
         self._xchg = None
         if host_allreduce is not None:
             import numpy as np
@@ -387,6 +393,34 @@ class Context:
         if s != APPD_OK:
             self._raise(s, "appd_solve_points_stream")
         return M
+
+    def solve_points_sink(self, X, sink, block_rows=0):
+        """appd_solve_points_sink (NEXT-4): X is a HOST float32 tensor; sink(row0, block) is
+        called in row order with each block as a numpy (rows x n) float32 view that is only
+        valid during the call (copy it to keep it).  Returns nothing; M is never held."""
+        import numpy as np
+
+        _check_tensor(X, "X")
+        if X.is_cuda:
+            raise ValueError("solve_points_sink takes a host X")
+        n, d = X.shape
+        err = []
+
+        def _cb(user, row0, rows, block, _n=n):
+            try:
+                sink(int(row0), np.ctypeslib.as_array(block, shape=(int(rows), _n)))
+                return 0
+            except Exception as e:  # noqa: BLE001 -- the library stops the solve
+                err.append(e)
+                return 1
+
+        cb = BLOCK_SINK_FN(_cb)
+        self._sync_stream()
+        s = self._L.appd_solve_points_sink(self._h, _ptr(X), n, d, int(block_rows), cb, None)
+        if err:
+            raise err[0]
+        if s != APPD_OK:
+            self._raise(s, "appd_solve_points_sink")
 
     def solve_points(self, X, M=None):
         """appd_solve_points: X is n x d (replicated on every rank)."""

@@ -139,7 +139,7 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   if (o.variant < 0 || o.variant > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.metric < 0 || o.metric > 2) return APPD_ERR_INVALID_ARGUMENT;
   if (o.world > 1 && !o.nccl_unique_id && !o.host_allreduce) return APPD_ERR_INVALID_ARGUMENT;
-  if (o.timeout_ms < 0 || o.list_cap < 0) return APPD_ERR_INVALID_ARGUMENT;
+  if (o.timeout_ms < 0 || o.list_cap < 0 || o.wide_keys < 0 || o.wide_keys > 1) return APPD_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -218,6 +218,7 @@ extern "C" void appd_destroy(appd_ctx* c) {
     for (int i = 0; i < 4; i++) cudaEventDestroy(c->sev[i]);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pinned_small) cudaFreeHost(c->pinned_small);
+  if (c->sink_host) cudaFreeHost(c->sink_host);
   cudaGetLastError();
   delete c;
 }
@@ -311,13 +312,14 @@ static appd_status agree(appd_ctx* c, const float* X, int64_t n, int64_t d, int 
   u64 v[NW];
   v[0] = (u64)n;
   v[1] = (u64)d;
-  v[2] = (u64)mode | (u64)(c->stream_out ? 1 : 0) << 8 | (u64)(uint32_t)c->opt.world << 32;
+  v[2] = (u64)mode | (u64)(c->stream_out ? 1 : 0) << 8 | (u64)(c->sink ? 1 : 0) << 9 |
+         (u64)(uint32_t)c->opt.world << 32;
   v[3] = (u64)(c->opt.sense + 1) | (u64)(c->opt.validate & 15) << 4 | (u64)(c->opt.metric & 15) << 8 |
          (u64)(c->opt.points_engine & 15) << 12 | (u64)(c->opt.dendrogram & 15) << 16 |
          (u64)(c->opt.variant & 15) << 20;
   v[4] = (u64)(uint32_t)c->opt.topk | (u64)(uint32_t)c->opt.finish_k << 32;
   v[5] = 0;
-  v[6] = (u64)(uint32_t)c->opt.list_cap;
+  v[6] = (u64)(uint32_t)c->opt.list_cap | (u64)(uint32_t)c->opt.wide_keys << 32;
   u64* dv = (u64*)ws(c, S_TMP, sizeof(u64) * 2 * NW);
   if (!dv) return fail(c, APPD_ERR_OUT_OF_MEMORY, "agreement buffer");
   if (X) {  // points mode: X is replicated, so its checksum must agree too
@@ -380,6 +382,11 @@ static void dev_check(appd_ctx* c, const char* what, const int32_t* d_eu, const 
 }
 #endif
 
+// points mode: up to kMaxPackedPoints the edge key packs bits(d2) (31) and the pair index
+// (33) into 64 bits; above it (NEXT-4, outputs beyond HBM) the wide-key path; the upper
+// bound keeps every index an int32 and the pair index below 2^40
+constexpr int64_t kMaxPackedPoints = 131072, kMaxPoints = 1 << 20;
+
 // ---------------------------------------------------------------------------
 // The Prim variant (k_prim.cu): one single-CTA launch validates the
 // input, runs Prim's n - 1 steps and writes (pi, h) with the fill's preparation; the fill
@@ -396,7 +403,7 @@ constexpr int64_t kPrimAutoMaxPoints = 1024, kPrimAutoMaxPointWork = 20480;  // 
 static bool prim_requested(const appd_ctx* c) { return c->opt.variant == APPD_VARIANT_PRIM; }
 
 static bool want_prim(const appd_ctx* c, int64_t n, int64_t d, bool points, bool f64) {
-  if (f64 || c->stream_out || n < 2) return false;
+  if (f64 || c->stream_out || c->sink || n < 2 || c->opt.wide_keys == 1) return false;
   if (!points && c->opt.world > 1) return false;
   if (!prim_fits(n, d, points)) return false;
   if (prim_requested(c)) return true;
@@ -512,7 +519,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine computes Euclidean distances only (metric = %d)",
                 c->opt.metric);
   const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 &&
-                                c->opt.metric == 0 && n >= 2;
+                                c->opt.metric == 0 && n >= 2 && n <= kMaxPackedPoints && c->opt.wide_keys != 1;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
   if (c->opt.validate) {
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
@@ -547,6 +554,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (c->stream_out) {
       APPD_SYNC(c);
       c->stream_out[0] = 0.0f;
+    } else if (c->sink) {
+      APPD_SYNC(c);
+      const float zero = 0.0f;
+      if (c->sink(c->sink_user, 0, 1, &zero) != 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "sink returned non-zero");
     } else if (rows > 0) {
       appd_status s = f64 ? launch_set_diag_zero_single_f64(c, c->f64_M) : launch_set_diag_zero_single(c, M);
       if (s) return s;
@@ -563,9 +574,12 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   }
 
   // ---- a2/a3: MST by Boruvka rounds ----
+  // wide keys (points, n > 131072): the pair index needs more than the 33 bits beside the
+  // weight; the exact engine with a two-step component reduction (k_boruvka.cu)
+  const bool wide = points && (n > kMaxPackedPoints || c->opt.wide_keys == 1);
   KeySpec ks;
   ks.points = points;
-  ks.shift = points ? 33 : 32;
+  ks.shift = wide ? 63 : points ? 33 : 32;
   ks.sense = sense;
   ks.metric = points ? c->opt.metric : 0;
   int* comp = (int*)ws(c, S_COMP, sizeof(int) * n);
@@ -586,7 +600,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // the dimension does not fit the shared-memory ring
   TcState tc;
   bool use_tc = false;
-  if (points && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
+  if (points && !wide && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
     host_mark("tcf_prepare queued");
     if (s == APPD_OK) {
@@ -752,6 +766,19 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         fprintf(stderr, "round %d: k=%lld mismatching components %d exact chunks %u fallback rows %u\n", rounds,
                 (long long)k, bad, tc.h_counters[2], tc.h_counters[0]);
       }
+    } else if (points && wide) {
+      // per-row winners, then compw (minimum weight bits) and compbest (minimum pair index
+      // among the winners of that weight), each reduced over the ranks
+      u64* rowbest = (u64*)ws(c, S_WIDE_ROW, sizeof(u64) * n);
+      u64* compw = (u64*)ws(c, S_WIDE_COMPW, sizeof(u64) * n);
+      if (!rowbest || !compw) return fail(c, APPD_ERR_OUT_OF_MEMORY, "wide-key round workspace");
+      if ((s = launch_fill_u64(c, rowbest, n, KEY_NONE))) return s;
+      if ((s = launch_fill_u64(c, compw, k, KEY_NONE))) return s;
+      if ((s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, rowbest, true))) return s;
+      if ((s = launch_wide_compw(c, rowbest, cmp, row0, row0 + rows, compw))) return s;
+      if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compw, k))) return s;
+      s = launch_wide_compbest(c, rowbest, cmp, row0, row0 + rows, compw, compbest);
+      c->stats.exact_rounds++;
     } else if (points) {
       s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, compbest);
       c->stats.exact_rounds++;
@@ -919,6 +946,10 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (!hw || !wk || !ix) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fp64 edge workspace");
     if ((s = launch_edges_f64(c, mstkeys, m, c->f64_W, n, sense, wk, wk + n, ix, ix + n, d_eu, d_ev, d_ew, hw)))
       return s;
+  } else if (wide) {
+    u64* key2s = (u64*)ws(c, S_WIDE_KEY2, sizeof(u64) * n);
+    if (!key2s) return fail(c, APPD_ERR_OUT_OF_MEMORY, "wide-key edge workspace");
+    if ((s = wide_edges(c, mstkeys, m, X, d, c->opt.metric, sorted, key2s, d_eu, d_ev, d_ew))) return s;
   } else if ((s = sort_keys_u64_bits64(c, mstkeys, sorted, n - 1, ks.shift, 64))) {
     return s;
   }
@@ -926,7 +957,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
 
   // ---- a5: dendrogram (v1: host union-find with list concatenation) ----
   // the GPU decodes the sorted keys to (u, v, w); pinned buffers keep the copies async
-  if (!f64 && (s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
+  if (!f64 && !wide && (s = launch_decode_edges(c, sorted, m, ks, d_eu, d_ev, d_ew))) return s;
   int levels = 1;
   while ((1ll << levels) <= m) levels++;
   const int64_t stride = m;
@@ -977,12 +1008,58 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   const int* rows_sorted = pi;
   int* rowpos = (int*)ws(c, S_ROWPOS, sizeof(int) * n);
   if (!rowpos) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
-  if (c->stream_out) {
+  if (c->stream_out || c->sink) {
     // ---- NEXT-4: M streamed to host memory in blocks of R original rows.  Per block the
     // rows' leaf positions are gathered and sorted (the multi-rank fill path), the fill
     // writes a device block buffer (two, alternating) and copy_stream moves it to the host
-    // while the next block is filled.
+    // while the next block is filled.  Sink mode: the host buffer is one of two pinned
+    // staging blocks, handed to the callback once its copy is complete (while the GPU
+    // fills and copies the next block).
     const int64_t R = std::min<int64_t>(c->stream_block, n);
+    float* hstage = nullptr;
+    if (c->sink) {
+      const size_t want = sizeof(float) * 2 * (size_t)R * n;
+      if (c->sink_bytes < want) {
+        if (c->sink_host) cudaFreeHost(c->sink_host);
+        c->sink_host = nullptr;
+        c->sink_bytes = 0;
+        if (cudaHostAlloc((void**)&c->sink_host, want, cudaHostAllocDefault) != cudaSuccess) {
+          cudaGetLastError();
+          return fail(c, APPD_ERR_OUT_OF_MEMORY, "pinned sink staging (%zu bytes)", want);
+        }
+        c->sink_bytes = want;
+      }
+      hstage = c->sink_host;
+    }
+    int64_t prev_b0 = -1, prev_rr = 0;
+    int prev_buf = 0;
+    auto drain_prev = [&]() -> appd_status {  // hand the previous block to the sink
+      if (!c->sink || prev_b0 < 0) return APPD_OK;
+      APPD_CUDA(c, cudaEventSynchronize(c->sev[2 + prev_buf]));
+      const int64_t b0 = prev_b0;
+      const int32_t r = c->sink(c->sink_user, b0, prev_rr, hstage + (size_t)prev_buf * R * n);
+      prev_b0 = -1;
+      if (r != 0) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamSynchronize(c->stream);
+        return fail(c, APPD_ERR_INVALID_ARGUMENT, "sink returned %d at rows [%lld, %lld)", (int)r, (long long)b0,
+                    (long long)(b0 + prev_rr));
+      }
+      return APPD_OK;
+    };
+    if (c->sink && cm_status_pending) {
+      // the callback must never see a block that is solved again: settle a component-matrix
+      // listing overflow (rare; the solve is repeated without it) before the first block
+      APPD_SYNC(c);
+      if (c->pinned_small[48] == 1) {
+        const int fk = c->opt.finish_k;
+        c->opt.finish_k = -1;
+        const appd_status s2 = solve(c, W, X, n, d, M);
+        c->opt.finish_k = fk;
+        c->stats.cm_retries++;
+        return s2;
+      }
+    }
     float* dblk = (float*)ws(c, S_HOST_OUT, sizeof(float) * 2 * R * n);
     int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (R + 1));
     int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (R + 1));
@@ -1007,10 +1084,15 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       if ((s = launch_fill(c, rs, rowpos, rr, pos, ST, stride, n, dst, b0, sense < 0))) return s;
       APPD_CUDA(c, cudaEventRecord(c->sev[buf], c->stream));
       APPD_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->sev[buf], 0));
-      APPD_CUDA(c, cudaMemcpyAsync(c->stream_out + (size_t)b0 * n, dst, sizeof(float) * rr * n,
-                                   cudaMemcpyDeviceToHost, c->copy_stream));
+      float* hdst = c->sink ? hstage + (size_t)buf * R * n : c->stream_out + (size_t)b0 * n;
+      APPD_CUDA(c, cudaMemcpyAsync(hdst, dst, sizeof(float) * rr * n, cudaMemcpyDeviceToHost, c->copy_stream));
       APPD_CUDA(c, cudaEventRecord(c->sev[2 + buf], c->copy_stream));
+      if ((s = drain_prev())) return s;
+      prev_b0 = b0;
+      prev_rr = rr;
+      prev_buf = buf;
     }
+    if ((s = drain_prev())) return s;
     APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)((blocks - 1) & 1)], 0));  // last copy done
     if (blocks >= 2) APPD_CUDA(c, cudaStreamWaitEvent(c->stream, c->sev[2 + (int)(blocks & 1)], 0));
     stage_event(c, 6);
@@ -1185,7 +1267,7 @@ extern "C" appd_status appd_solve_points(appd_ctx* c, const float* X, int64_t n,
   appd_status s = enter(c);
   if (s) return s;
   if (n < 1 || d < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld, d = %lld", (long long)n, (long long)d);
-  if (n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072 (33-bit pair index)");
+  if (n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
   if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
   if ((s = check_device_ptr(c, X, "X"))) return s;
   int64_t row0, rows;
@@ -1216,8 +1298,35 @@ static appd_status solve_host(appd_ctx* c, const float* Wh, const float* Xh, int
 }
 
 extern "C" appd_status appd_solve_points_host(appd_ctx* c, const float* X, int64_t n, int64_t d, float* M) {
-  if (c && n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072");
+  if (c && n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
+  if (c && d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
   return solve_host(c, nullptr, X, n, d, M);
+}
+
+// NEXT-4: points mode with each row block of M handed to a host callback (n beyond host
+// memory as well: 2^18 points make 256 GiB of output)
+extern "C" appd_status appd_solve_points_sink(appd_ctx* c, const float* X, int64_t n, int64_t d, int64_t block_rows,
+                                              int32_t (*sink)(void*, int64_t, int64_t, const float*), void* user) {
+  appd_status s = enter(c);
+  if (s) return s;
+  if (!X || !sink) return fail(c, APPD_ERR_INVALID_ARGUMENT, "NULL X or sink");
+  if (n < 1 || d < 1 || block_rows < 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n, d, block_rows");
+  if (n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
+  if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
+  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_sink runs on one rank");
+  const int64_t R = block_rows ? block_rows : std::max<int64_t>(128, ((int64_t)1 << 28) / n);
+  float* din = (float*)ws(c, S_HOST_IN, sizeof(float) * n * d);
+  if (!din) return fail(c, APPD_ERR_OUT_OF_MEMORY, "device copy of X");
+  APPD_CUDA(c, cudaMemcpyAsync(din, X, sizeof(float) * n * d, cudaMemcpyHostToDevice, c->stream));
+  c->sink = sink;
+  c->sink_user = user;
+  c->stream_block = R;
+  s = solve(c, nullptr, din, n, d, nullptr);
+  c->sink = nullptr;
+  c->sink_user = nullptr;
+  c->stream_block = 0;
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  return s;
 }
 
 // NEXT-4: points mode with M streamed to host memory in row blocks (n beyond HBM)
@@ -1227,7 +1336,8 @@ extern "C" appd_status appd_solve_points_stream(appd_ctx* c, const float* X, int
   if (s) return s;
   if (!X || !M) return fail(c, APPD_ERR_INVALID_ARGUMENT, "NULL host buffer");
   if (n < 1 || d < 1 || block_rows < 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n, d, block_rows");
-  if (n > 131072) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 131072");
+  if (n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
+  if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
   if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_stream runs on one rank");
   // default block: 1 GiB of rows per buffer (two buffers), at least 128 rows
   const int64_t R = block_rows ? block_rows : std::max<int64_t>(128, ((int64_t)1 << 28) / n);

@@ -124,6 +124,12 @@ struct appd_ctx {
   // blocks of stream_block rows, two device block buffers, copies on copy_stream
   float* stream_out = nullptr;
   int64_t stream_block = 0;
+  // NEXT-4 sink (appd_solve_points_sink): blocks go through two pinned staging buffers to a
+  // host callback instead of a host matrix (n beyond host memory too)
+  int32_t (*sink)(void*, int64_t, int64_t, const float*) = nullptr;
+  void* sink_user = nullptr;
+  float* sink_host = nullptr;
+  size_t sink_bytes = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t sev[4];  // filled[2], copied[2]
   bool sev_ready = false;
@@ -171,6 +177,7 @@ enum Slot {
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
   S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE, S_F64_A, S_F64_B, S_F64_HW,
+  S_WIDE_ROW, S_WIDE_COMPW, S_WIDE_KEY2,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
@@ -323,7 +330,14 @@ appd_status launch_scan_weights_list(appd_ctx* c, const float* W, int64_t n, int
 appd_status launch_transpose_points(appd_ctx* c, const float* X, int64_t n, int64_t d, float* XT, int64_t npad,
                                     int64_t dpad);
 appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
-                               int64_t rows, const int* comp, u64* compbest);
+                               int64_t rows, const int* comp, u64* compbest, bool wide = false);
+// wide keys (points, n > 131072): per-row winners -> two-step component reduction; the MST
+// edges' Kruskal order and (u, v, w) from the pair indices (k_boruvka.cu)
+appd_status launch_wide_compw(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1, u64* compw);
+appd_status launch_wide_compbest(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1,
+                                 const u64* compw, u64* compbest);
+appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, u64* key2,
+                       u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew);
 appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v);
 appd_status launch_iota(appd_ctx* c, int* p, int64_t count);
 appd_status launch_hook(appd_ctx* c, const u64* compbest, int64_t k, const int* comp, int shift, int* link);

@@ -420,7 +420,10 @@ __device__ __forceinline__ float metric_step(float a, float b, float acc) {
   return fmaxf(acc, fabsf(t));
 }
 
-template <bool ROUND0, int METRIC = 0>
+// WIDE (n > 131072, the pair index no longer fits beside the weight bits): each row's
+// (bits(d2) << 32 | j) minimum goes to compbest[row] instead (the per-row winners; the
+// component reduction runs in two steps, k_wide_compw / k_wide_compbest)
+template <bool ROUND0, int METRIC = 0, bool WIDE = false>
 __global__ void __launch_bounds__(256, 2)
     k_scan_points(const float* __restrict__ XT, int64_t n, int64_t npad, int dpad, int64_t row0, int64_t rows,
                   int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest) {
@@ -533,6 +536,10 @@ __global__ void __launch_bounds__(256, 2)
       u64 other = __shfl_xor_sync(0xffffffffu, key, o);
       key = other < key ? other : key;
     }
+    if (WIDE) {
+      if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) atomicMin(compbest + ri[a], key);
+      continue;
+    }
     if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) {
       int64_t j = (int64_t)(key & 0xFFFFFFFFull);
       u64 d2bits = (key >> 32) & 0x7FFFFFFFull;
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
-                               int64_t rows, const int* comp, u64* compbest) {
+                               int64_t rows, const int* comp, u64* compbest, bool wide) {
   const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4;
   if (rows <= 0) return APPD_OK;
   static std::atomic<unsigned long long> attr{0};
@@ -554,6 +561,12 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
     cudaFuncSetAttribute(k_scan_points<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_scan_points<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     setup_done(attr, c);
   }
   int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
@@ -568,8 +581,20 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
   dim3 grid((unsigned)row_blocks, (unsigned)splits);
 #define APPD_SCAN_POINTS(R0, MT) \
   k_scan_points<R0, MT><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp, compbest)
+#define APPD_SCAN_POINTS_W(R0, MT) \
+  k_scan_points<R0, MT, true><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp, compbest)
   const int mt = c->opt.metric;
-  if (comp == nullptr) {
+  if (wide) {
+    if (comp == nullptr) {
+      if (mt == 1) APPD_SCAN_POINTS_W(true, 1);
+      else if (mt == 2) APPD_SCAN_POINTS_W(true, 2);
+      else APPD_SCAN_POINTS_W(true, 0);
+    } else {
+      if (mt == 1) APPD_SCAN_POINTS_W(false, 1);
+      else if (mt == 2) APPD_SCAN_POINTS_W(false, 2);
+      else APPD_SCAN_POINTS_W(false, 0);
+    }
+  } else if (comp == nullptr) {
     if (mt == 1) APPD_SCAN_POINTS(true, 1);
     else if (mt == 2) APPD_SCAN_POINTS(true, 2);
     else APPD_SCAN_POINTS(true, 0);
@@ -579,6 +604,101 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
     else APPD_SCAN_POINTS(false, 0);
   }
 #undef APPD_SCAN_POINTS
+#undef APPD_SCAN_POINTS_W
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Wide keys (points, n > 131072: bits(d2) takes 31 bits and the pair index up to 40, more
+// than 64 together).  The strict edge order (weight, max(u,v), min(u,v)) is kept by a
+// two-step component reduction (SURVEY §8(a) packed-key note: "two-pass, min w first,
+// then min id among the winners"): compw[C] = the minimum weight bits over C's row
+// winners, then compbest[C] = the minimum pair index among the winners of that weight.
+// compbest then holds the pair index alone (the contraction decodes it with shift 63).
+// ---------------------------------------------------------------------------
+__global__ void k_wide_compw(const u64* __restrict__ rowbest, const int* __restrict__ comp, int64_t r0, int64_t r1,
+                             bool round0, u64* __restrict__ compw) {
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 rb = rowbest[i];
+    if (rb != KEY_NONE) atomicMin(compw + (round0 ? i : comp[i]), rb >> 32);
+  }
+}
+
+__global__ void k_wide_compbest(const u64* __restrict__ rowbest, const int* __restrict__ comp, int64_t r0,
+                                int64_t r1, bool round0, const u64* __restrict__ compw, u64* __restrict__ compbest) {
+  for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 rb = rowbest[i];
+    if (rb == KEY_NONE) continue;
+    const int ci = round0 ? (int)i : comp[i];
+    if ((rb >> 32) == compw[ci]) atomicMin(compbest + ci, tri_index(i, (int64_t)(rb & 0xFFFFFFFFull)));
+  }
+}
+
+appd_status launch_wide_compw(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1, u64* compw) {
+  if (r1 <= r0) return APPD_OK;
+  const int grid = (int)std::min<int64_t>((r1 - r0 + 255) / 256, (int64_t)c->sm_count * 8);
+  k_wide_compw<<<grid, 256, 0, c->stream>>>(rowbest, comp, r0, r1, comp == nullptr, compw);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+appd_status launch_wide_compbest(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1,
+                                 const u64* compw, u64* compbest) {
+  if (r1 <= r0) return APPD_OK;
+  const int grid = (int)std::min<int64_t>((r1 - r0 + 255) / 256, (int64_t)c->sm_count * 8);
+  k_wide_compbest<<<grid, 256, 0, c->stream>>>(rowbest, comp, r0, r1, comp == nullptr, compw, compbest);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
+// the MST edges of the wide keys (pair indices): key2[e] = bits(weight) << 32 | e with the
+// weight recomputed from X by the same chain as the scan (R1 d2, or the L1 / L-inf
+// distance), so that a radix sort over bits [32, 64) gives the Kruskal order (a4)
+template <int METRIC>
+__global__ void k_wide_edge_keys(const u64* __restrict__ tri, int64_t m, const float* __restrict__ X, int d,
+                                 u64* __restrict__ key2) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t u, v;
+    tri_decode(tri[e] & ((1ull << 63) - 1), &u, &v);
+    float acc = 0.0f;
+    for (int k = 0; k < d; k++) {
+      const float t = __fsub_rn(X[u * d + k], X[v * d + k]);
+      if (METRIC == 0) acc = __fmaf_rn(t, t, acc);
+      else if (METRIC == 1) acc = __fadd_rn(acc, fabsf(t));
+      else acc = fmaxf(acc, fabsf(t));
+    }
+    key2[e] = (u64)__float_as_uint(acc) << 32 | (u64)e;
+  }
+}
+
+template <int METRIC>
+__global__ void k_wide_decode(const u64* __restrict__ key2_sorted, const u64* __restrict__ tri, int64_t m,
+                              int32_t* __restrict__ eu, int32_t* __restrict__ ev, float* __restrict__ ew) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    const u64 k2 = key2_sorted[p];
+    int64_t u, v;
+    tri_decode(tri[k2 & 0xFFFFFFFFull] & ((1ull << 63) - 1), &u, &v);
+    const float w = __uint_as_float((uint32_t)(k2 >> 32));
+    eu[p] = (int32_t)u;
+    ev[p] = (int32_t)v;
+    ew[p] = METRIC == 0 ? __fsqrt_rn(w) : w;  // APPD(sqrtf o d2) = sqrtf o APPD(d2), App. A.4
+  }
+}
+
+appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, u64* key2,
+                       u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew) {
+  if (m <= 0) return APPD_OK;
+  const int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)c->sm_count * 8);
+  if (metric == 1) k_wide_edge_keys<1><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
+  else if (metric == 2) k_wide_edge_keys<2><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
+  else k_wide_edge_keys<0><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
+  APPD_LAUNCHED(c);
+  appd_status s = sort_keys_u64_bits64(c, key2, key2_sorted, m, 32, 64);
+  if (s) return s;
+  if (metric == 1) k_wide_decode<1><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
+  else if (metric == 2) k_wide_decode<2><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
+  else k_wide_decode<0><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

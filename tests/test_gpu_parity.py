@@ -693,3 +693,75 @@ def test_prim_variant_validation_and_limits(P):
         assert e.value.name == "APPD_ERR_UNSUPPORTED"
         W = G.random_weights(50, 3, "ties")
         assert_bit_equal(gpu_weights(c, W, c=c), oracle.appd_weights(W), "after errors")
+
+
+# --------------------------------------------------------------------------
+# NEXT-4 beyond n = 131072: wide edge keys (two-step component reduction) and the block sink
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", ["uniform", "dups", "grid", "clumps", "blobs"])
+def test_wide_keys_engine(P, kind):
+    """The wide-key path (automatic above n = 131072) forced at small n: bit-exact vs the
+    oracle, ties (grid), zero-weight edges (dups, clumps) and ragged sizes included."""
+    with P.Context(wide_keys=1, timing=True) as c:
+        for t, (n, d) in enumerate([(2, 3), (3, 1), (129, 4), (1000, 8), (2500, 3), (4100, 16)]):
+            X = G.random_points(n, d, 960 + t, kind)
+            assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), f"wide {kind} n={n} d={d}")
+            st = c.stats()
+            assert n < 2 or (st["points_engine"] == 1 and st["variant"] == P.VARIANT_BORUVKA)
+
+
+def test_wide_keys_metrics(P):
+    for metric in (1, 2):
+        X = G.random_points(1500, 5, 970 + metric, "blobs")
+        with P.Context(wide_keys=1, metric=metric) as c:
+            assert_bit_equal(gpu_points(c, X), oracle.appd_points(X, metric=metric), f"wide metric {metric}")
+
+
+def test_points_sink_blocks(P):
+    """appd_solve_points_sink: blocks arrive in row order, tile M exactly, equal the oracle."""
+    X = G.random_points(3000, 6, 975, "dups")
+    want = oracle.appd_points(X)
+    for block in (700, 0, 3000, 1):
+        got = np.full_like(want, np.nan)
+        seen = []
+        with P.Context() as c:
+            def sink(r0, blk):
+                seen.append((r0, blk.shape[0]))
+                got[r0:r0 + blk.shape[0]] = blk
+            c.solve_points_sink(torch.from_numpy(X), sink, block if block != 1 else 1)
+        assert [r for r, _ in seen] == sorted(r for r, _ in seen) and sum(k for _, k in seen) == 3000
+        assert_bit_equal(got, want, f"sink block={block}")
+    with P.Context() as c:  # a failing sink stops the solve
+        def bad(r0, blk):
+            raise RuntimeError("disk full")
+        with pytest.raises(RuntimeError):
+            c.solve_points_sink(torch.from_numpy(X), bad, 1000)
+        assert_bit_equal(gpu_points(c, X), want, "after a failed sink")
+
+
+def test_c5x_beyond_hbm_sink(P):
+    """NEXT-4: the C5 recipe at n = 2^18 -- 256 GiB of output, more than the GPU's
+    HBM and this host's RAM -- through the sink, on the wide-key path; the first, middle and
+    last 1024-row blocks hash to the oracle's R5 windows (tests/golden/C5x_windows.json)."""
+    path = os.path.join(GOLD, "C5x_windows.json")
+    if not os.path.exists(path):
+        pytest.skip("C5x_windows.json not generated")
+    g = json.load(open(path))
+    X = G.c5_points(g["n"], g["d"], 4)
+    assert oracle.fnv1a64(X) == g["input_fnv1a64"]
+    n, B = g["n"], g["block_rows"]
+    got, rows = {}, [0]
+
+    def sink(r0, blk):
+        assert r0 == rows[0]
+        rows[0] += blk.shape[0]
+        for b0 in range(r0, r0 + blk.shape[0], B):
+            if str(b0) in g["blocks"]:
+                got[str(b0)] = f"{oracle.fnv1a64(np.ascontiguousarray(blk[b0 - r0:b0 - r0 + B])):016x}"
+
+    with P.Context(timing=True) as c:
+        c.solve_points_sink(torch.from_numpy(X), sink, B)
+        st = c.stats()
+    assert rows[0] == n
+    assert got == g["blocks"], (got, g["blocks"])
+    assert st["points_engine"] == 1 and st["fill_bytes"] == n * n * 4

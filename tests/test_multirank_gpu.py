@@ -48,6 +48,7 @@ CASES = [
     ("points_manhattan_700", "points", ("blobs", 700, 5), {"metric": 1}),
     ("points_prim_replicated_900", "points", ("blobs", 900, 3), {"variant": 1}),
     ("points_prim_fused_300", "points", ("dups", 300, 4), {"variant": 1}),
+    ("points_wide_keys_1200", "points", ("dups", 1200, 6), {"wide_keys": 1}),
     ("c3_shape_4096_ties", "weights", ("C3", 4096), {}),
     ("weights_ties_1031", "weights", ("ties", 1031), {}),
     ("weights_negative_600_nocache", "weights", ("negative", 600), {"topk": -1}),
