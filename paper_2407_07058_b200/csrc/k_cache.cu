@@ -409,11 +409,18 @@ __global__ void k_chunk_runs(const unsigned* __restrict__ list, const unsigned* 
 }
 
 // counting sort of the list by chunk (no host-side count): histogram, scatter
+// the listing is emitted chunk-major (runs of one chunk), so the lanes of a warp mostly
+// share a chunk: one atomic per distinct chunk in the warp instead of one per entry
 __global__ void k_chunk_hist(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
                              unsigned* __restrict__ hist) {
   const unsigned total = min(*count, cap);
-  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x)
-    atomicAdd(hist + (list[e] >> LIST_SHIFT), 1u);
+  const int lane = threadIdx.x & 31;
+  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < total; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + lane;
+    const unsigned ch = e < total ? list[e] >> LIST_SHIFT : 0xFFFFFFFFu;
+    const unsigned peers = __match_any_sync(0xffffffffu, ch);
+    if (e < total && lane == __ffs(peers) - 1) atomicAdd(hist + ch, (unsigned)__popc(peers));
+  }
 }
 __global__ void k_chunk_scatter(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
                                 const unsigned* __restrict__ offs, unsigned* __restrict__ cursor,

@@ -285,11 +285,17 @@ __global__ void __launch_bounds__(FILL_THREADS)
         for (int q = 0; q < VEC; q++)
           if (jbase + q < n) __stcs(reinterpret_cast<double*>(dst) + q, o[q]);
       }
-    } else if (VEC == 8) {  // one 32-byte streaming store (st.global.cs.v8.f32, sm_100)
-      if (in_range)
-        asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
-                     "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-                     : "memory");
+    } else if (VEC == 8) {  // one 32-byte store (st.global[.cs].v8.f32, sm_100)
+      if (in_range) {
+        if (STORE == 0)
+          asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
+                       "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                       : "memory");
+        else
+          asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
+                       "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                       : "memory");
+      }
     } else if (VEC == 4) {
       if (in_range) fill_store4<STORE>(reinterpret_cast<float*>(dst), make_float4(v[0], v[1], v[2], v[3]));
     } else {
