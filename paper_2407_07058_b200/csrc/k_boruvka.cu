@@ -115,45 +115,50 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     const int64_t i = row0 + r;
     const float* Wr = W + r * n;
-    auto keyof = [&](float w, int64_t j) -> u64 {
+    auto keyof = [&](float w, int j) -> u64 {
       float m = SENSE > 0 ? w : -w;
       m = m + 0.0f;  // -0 -> +0 (reading Q5)
-      return ((u64)orderable(m) << 32) | (u64)j;
+      return ((u64)orderable(m) << 32) | (u64)(unsigned)j;
     };
     // one float compare per element (validated input: no NaN; -0 == +0 as in the key);
     // strict '<' (widest: '>') in increasing j keeps the smallest j among equal weights,
     // so (w, j) is the thread's minimum key
     auto better = [&](float a, float b) -> bool { return SENSE > 0 ? a < b : a > b; };
-    float bw = SENSE > 0 ? INFINITY : -INFINITY;
-    int64_t bj = -1;
+    const float NOPE = SENSE > 0 ? INFINITY : -INFINITY;  // the diagonal entry never competes
+    float bw = NOPE;
+    int bj = -1;
+    // 32-bit indices (weights mode: n <= 92682); the diagonal is not tested per element:
+    // the thread whose minimum lands on it (always, for non-negative weights) re-scans its
+    // own quads without it.  The full batches run without predicates.  (The scan was
+    // instruction-bound at 58 % issue with 64-bit j and a per-element j != i test.)
+    const int i32 = (int)i;
+    auto scan4 = [&](float4 v, int j, bool skip_diag) {
+      if (better(v.x, bw) && (!skip_diag || j != i32)) { bw = v.x; bj = j; }
+      if (better(v.y, bw) && (!skip_diag || j + 1 != i32)) { bw = v.y; bj = j + 1; }
+      if (better(v.z, bw) && (!skip_diag || j + 2 != i32)) { bw = v.z; bj = j + 2; }
+      if (better(v.w, bw) && (!skip_diag || j + 3 != i32)) { bw = v.w; bj = j + 3; }
+    };
     if (vec) {
-      // four 16-byte loads in flight per thread, then the four in order of j
       const float4* W4 = reinterpret_cast<const float4*>(Wr);
-      const int64_t n4 = n >> 2;
-      for (int64_t q0 = threadIdx.x; q0 < n4; q0 += 4 * 256) {
-        float4 w[4];
+      const int n4 = (int)(n >> 2);
+      int q0 = threadIdx.x;
+      for (; q0 + 7 * 256 < n4; q0 += 8 * 256) {  // eight 16-byte loads in flight, then in order of j
+        float4 w[8];
 #pragma unroll
-        for (int u = 0; u < 4; u++)
-          w[u] = q0 + u * 256 < n4 ? __ldcg(W4 + q0 + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 8; u++) w[u] = __ldcg(W4 + q0 + u * 256);
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int64_t q = q0 + u * 256;
-          if (q >= n4) break;
-          const float ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const int64_t j = 4 * q + e;
-            if (better(ws[e], bw) && j != i) {
-              bw = ws[e];
-              bj = j;
-            }
-          }
-        }
+        for (int u = 0; u < 8; u++) scan4(w[u], 4 * (q0 + u * 256), false);
+      }
+      for (; q0 < n4; q0 += 256) scan4(__ldcg(W4 + q0), 4 * q0, false);
+      if (bj == i32) {  // the diagonal won: this thread's quads again, without it
+        bw = NOPE;
+        bj = -1;
+        for (int q = threadIdx.x; q < n4; q += 256) scan4(__ldcg(W4 + q), 4 * q, true);
       }
     } else {
-      for (int64_t j = threadIdx.x; j < n; j += 256) {
+      for (int j = threadIdx.x; j < (int)n; j += 256) {
         const float w = __ldcg(Wr + j);
-        if (better(w, bw) && j != i) {
+        if (better(w, bw) && j != i32) {
           bw = w;
           bj = j;
         }
@@ -197,42 +202,37 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
     const float tau_f = tau == KEY_NONE ? (SENSE > 0 ? INFINITY : -INFINITY)
                                         : (SENSE > 0 ? from_orderable((uint32_t)(tau >> 32))
                                                      : -from_orderable((uint32_t)(tau >> 32)));
-    // pass 2: keys <= tau
-    if (vec) {
-      const float4* W4 = reinterpret_cast<const float4*>(Wr);
-      const int64_t n4 = n >> 2;
-      for (int64_t q0 = threadIdx.x; q0 < n4; q0 += 4 * 256) {
-        float4 wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-          wv[u] = q0 + u * 256 < n4 ? __ldcs(W4 + q0 + u * 256) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-        const int64_t q = q0 + u * 256;
-        if (q >= n4) break;
-        const float ws[4] = {wv[u].x, wv[u].y, wv[u].z, wv[u].w};
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const int64_t j = 4 * q + e;
-          if ((SENSE > 0 ? ws[e] <= tau_f : ws[e] >= tau_f) && j != i) {  // cheap float test first
-            const u64 kk = keyof(ws[e], j);
-            if (kk <= tau) {
-              const int slot = atomicAdd(&ncand, 1);
-              if (slot < CAP) cand[slot] = kk;
-            }
-          }
-        }
+    // pass 2: keys <= tau (a float test first; ties at tau's weight compare the full key;
+    // the diagonal is excluded on that rare path)
+    auto take = [&](float w, int j) {
+      if (SENSE > 0 ? w <= tau_f : w >= tau_f) {
+        const u64 kk = keyof(w, j);
+        if (kk <= tau && j != i32) {
+          const int slot = atomicAdd(&ncand, 1);
+          if (slot < CAP) cand[slot] = kk;
         }
       }
+    };
+    auto take4 = [&](float4 v, int j) {
+      take(v.x, j);
+      take(v.y, j + 1);
+      take(v.z, j + 2);
+      take(v.w, j + 3);
+    };
+    if (vec) {
+      const float4* W4 = reinterpret_cast<const float4*>(Wr);
+      const int n4 = (int)(n >> 2);
+      int q0 = threadIdx.x;
+      for (; q0 + 7 * 256 < n4; q0 += 8 * 256) {
+        float4 w[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) w[u] = __ldcs(W4 + q0 + u * 256);
+#pragma unroll
+        for (int u = 0; u < 8; u++) take4(w[u], 4 * (q0 + u * 256));
+      }
+      for (; q0 < n4; q0 += 256) take4(__ldcs(W4 + q0), 4 * q0);
     } else {
-      for (int64_t j = threadIdx.x; j < n; j += 256)
-        if (j != i) {
-          const u64 kk = keyof(__ldcs(Wr + j), j);
-          if (kk <= tau) {
-            const int slot = atomicAdd(&ncand, 1);
-            if (slot < CAP) cand[slot] = kk;
-          }
-        }
+      for (int j = threadIdx.x; j < (int)n; j += 256) take(__ldcs(Wr + j), j);
     }
     __syncthreads();
     if (warp == 0) {
