@@ -17,7 +17,9 @@
  *     (leaf order pi, merge heights h) and a fill that writes
  *     M[pi_a][pi_b] = max(h[a..b-1]).
  *   P:L50, P:L119 (widest path): sense = -1 computes the widest-path APPD
- *     (maximum spanning tree, minimum over the path) -- weights mode only.
+ *     (maximum spanning tree, minimum over the path) -- weights mode, and points
+ *     mode on the exact FP32 engine or the Prim variant (the tensor-core filter
+ *     finds minimum edges only).
  *
  * Conventions for every call:
  *   - Matrices are fp32, row-major, contiguous, leading dimension n (W, M) or
@@ -94,7 +96,7 @@ typedef struct {
   const uint8_t* nccl_unique_id; /* world > 1: 128-byte ncclUniqueId from appd_get_nccl_unique_id on rank 0 */
   int32_t variant;               /* APPD_VARIANT_* (default AUTO) */
   int32_t validate;              /* 1 = check W/X (default), 0 = trust the input */
-  int32_t sense;                 /* +1 minimax (default), -1 widest path (weights mode only) */
+  int32_t sense;                 /* +1 minimax (default), -1 widest path (points: exact engine / Prim) */
   int32_t timing;                /* 1 = record per-stage CUDA events (appd_get_stats), default 0 */
   int32_t dendrogram;            /* 0 auto, 1 host union-find, 2 GPU */
   int32_t points_engine;         /* points-mode MST scan: 0 auto, 1 exact FP32 (CUDA cores), 2 tensor-core

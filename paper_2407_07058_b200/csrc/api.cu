@@ -415,7 +415,7 @@ static bool want_prim(const appd_ctx* c, int64_t n, int64_t d, bool points, bool
 
 static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
-  const int sense = points ? 1 : c->opt.sense;
+  const int sense = c->opt.sense;  // points too: widest paths on the exact engine or Prim
   int64_t row0, rows;
   appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
   c->stats.variant = APPD_VARIANT_PRIM;
@@ -485,7 +485,7 @@ static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
   const bool f64 = c->f64_W != nullptr;  // NEXT-3 (k_f64.cu): W and M are c->f64_W / c->f64_M
-  const int sense = points ? 1 : c->opt.sense;
+  const int sense = c->opt.sense;  // points too: widest paths on the exact engine or Prim
   int64_t row0, rows;
   appd_row_range_of(n, c->opt.rank, c->opt.world, &row0, &rows);
   std::memset(&c->stats, 0, sizeof c->stats);
@@ -518,8 +518,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if (points && c->opt.metric != 0 && c->opt.points_engine == 2)
     return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine computes Euclidean distances only (metric = %d)",
                 c->opt.metric);
+  if (points && sense < 0 && c->opt.points_engine == 2)
+    return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine finds minimum edges only (widest sense: exact engine)");
   const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 &&
-                                c->opt.metric == 0 && n >= 2 && n <= kMaxPackedPoints && c->opt.wide_keys != 1;
+                                c->opt.metric == 0 && sense > 0 && n >= 2 && n <= kMaxPackedPoints &&
+                                c->opt.wide_keys != 1;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
   if (c->opt.validate) {
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
@@ -600,7 +603,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // the dimension does not fit the shared-memory ring
   TcState tc;
   bool use_tc = false;
-  if (points && !wide && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
+  if (points && !wide && sense > 0 && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
     host_mark("tcf_prepare queued");
     if (s == APPD_OK) {
@@ -949,7 +952,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   } else if (wide) {
     u64* key2s = (u64*)ws(c, S_WIDE_KEY2, sizeof(u64) * n);
     if (!key2s) return fail(c, APPD_ERR_OUT_OF_MEMORY, "wide-key edge workspace");
-    if ((s = wide_edges(c, mstkeys, m, X, d, c->opt.metric, sorted, key2s, d_eu, d_ev, d_ew))) return s;
+    if ((s = wide_edges(c, mstkeys, m, X, d, c->opt.metric, sense, sorted, key2s, d_eu, d_ev, d_ew))) return s;
   } else if ((s = sort_keys_u64_bits64(c, mstkeys, sorted, n - 1, ks.shift, 64))) {
     return s;
   }

@@ -71,7 +71,7 @@ __host__ __device__ inline void tri_decode(u64 t, int64_t* u, int64_t* v) {
 struct KeySpec {
   int shift;     // 32 (weights) or 33 (points)
   bool points;   // key weight is bits(d^2)
-  int sense;     // +1 minimax, -1 widest (weights only)
+  int sense;     // +1 minimax, -1 widest (points: the weight bits through ~b & 0x7FFFFFFF)
   int metric = 0;  // points: 0 Euclidean (key = bits(d^2), weight sqrtf), 1 L1, 2 L-inf (key = bits(d))
 };
 
@@ -336,8 +336,8 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
 appd_status launch_wide_compw(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1, u64* compw);
 appd_status launch_wide_compbest(appd_ctx* c, const u64* rowbest, const int* comp, int64_t r0, int64_t r1,
                                  const u64* compw, u64* compbest);
-appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, u64* key2,
-                       u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew);
+appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, int sense,
+                       u64* key2, u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew);
 appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v);
 appd_status launch_iota(appd_ctx* c, int* p, int64_t count);
 appd_status launch_hook(appd_ctx* c, const u64* compbest, int64_t k, const int* comp, int shift, int* link);

@@ -423,7 +423,12 @@ __device__ __forceinline__ float metric_step(float a, float b, float acc) {
 // WIDE (n > 131072, the pair index no longer fits beside the weight bits): each row's
 // (bits(d2) << 32 | j) minimum goes to compbest[row] instead (the per-row winners; the
 // component reduction runs in two steps, k_wide_compw / k_wide_compbest)
-template <bool ROUND0, int METRIC = 0, bool WIDE = false>
+// SENSE -1 (widest paths): the row's LARGEST distance (smallest j on ties), keyed
+// by the order-reversing map of the non-negative weight bits, ~bits & 0x7FFFFFFF (the
+// same (weight, max, min) strict order, weight reversed)
+__device__ __forceinline__ uint32_t sense_bits(uint32_t b, int sense) { return sense > 0 ? b : (~b & 0x7FFFFFFFu); }
+
+template <bool ROUND0, int METRIC = 0, bool WIDE = false, int SENSE = 1>
 __global__ void __launch_bounds__(256, 2)
     k_scan_points(const float* __restrict__ XT, int64_t n, int64_t npad, int dpad, int64_t row0, int64_t rows,
                   int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest) {
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(256, 2)
   for (int a = 0; a < 8; a++) {
     ri[a] = rbase + ty * 8 + a;
     cr[a] = ROUND0 ? (int)ri[a] : ((ri[a] < n) ? comp[ri[a]] : -1);
-    bd[a] = INFINITY;
+    bd[a] = SENSE > 0 ? INFINITY : -INFINITY;
     bj[a] = -1;
   }
 
@@ -520,7 +525,7 @@ __global__ void __launch_bounds__(256, 2)
           bool elig = ROUND0 ? (j < n && j != ri[a]) : (cj != cr[a] && cj >= 0);
           // the first eligible column is taken even at +inf (coordinates whose squares
           // overflow): every component must choose an edge
-          if (elig && (bj[a] < 0 || acc[a][b] < bd[a])) { bd[a] = acc[a][b]; bj[a] = j; }
+          if (elig && (bj[a] < 0 || (SENSE > 0 ? acc[a][b] < bd[a] : acc[a][b] > bd[a]))) { bd[a] = acc[a][b]; bj[a] = j; }
         }
       }
     }
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(256, 2)
   // reduce (d2, j) over the 16 threads sharing each row (lanes differing in tx)
 #pragma unroll
   for (int a = 0; a < 8; a++) {
-    u64 key = bj[a] >= 0 ? (((u64)__float_as_uint(bd[a]) << 32) | (u64)bj[a]) : KEY_NONE;
+    u64 key = bj[a] >= 0 ? (((u64)sense_bits(__float_as_uint(bd[a]), SENSE) << 32) | (u64)bj[a]) : KEY_NONE;
 #pragma unroll
     for (int o = 8; o; o >>= 1) {
       u64 other = __shfl_xor_sync(0xffffffffu, key, o);
@@ -567,6 +572,13 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
     cudaFuncSetAttribute(k_scan_points<false, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<true, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k_scan_points<false, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#define APPD_ATTR_W(R0, MT, WD) \
+  cudaFuncSetAttribute(k_scan_points<R0, MT, WD, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+    APPD_ATTR_W(true, 0, false); APPD_ATTR_W(false, 0, false); APPD_ATTR_W(true, 1, false);
+    APPD_ATTR_W(false, 1, false); APPD_ATTR_W(true, 2, false); APPD_ATTR_W(false, 2, false);
+    APPD_ATTR_W(true, 0, true); APPD_ATTR_W(false, 0, true); APPD_ATTR_W(true, 1, true);
+    APPD_ATTR_W(false, 1, true); APPD_ATTR_W(true, 2, true); APPD_ATTR_W(false, 2, true);
+#undef APPD_ATTR_W
     setup_done(attr, c);
   }
   int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
@@ -579,10 +591,18 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
   int64_t per = (col_tiles + splits - 1) / splits;
   splits = (col_tiles + per - 1) / per;
   dim3 grid((unsigned)row_blocks, (unsigned)splits);
-#define APPD_SCAN_POINTS(R0, MT) \
-  k_scan_points<R0, MT><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp, compbest)
-#define APPD_SCAN_POINTS_W(R0, MT) \
-  k_scan_points<R0, MT, true><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, (int)per, comp, compbest)
+#define APPD_SCAN_POINTS(R0, MT)                                                                               \
+  (c->opt.sense > 0                                                                                           \
+       ? k_scan_points<R0, MT, false, 1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows,  \
+                                                                          (int)per, comp, compbest)           \
+       : k_scan_points<R0, MT, false, -1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, \
+                                                                           (int)per, comp, compbest))
+#define APPD_SCAN_POINTS_W(R0, MT)                                                                            \
+  (c->opt.sense > 0                                                                                          \
+       ? k_scan_points<R0, MT, true, 1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows,  \
+                                                                         (int)per, comp, compbest)           \
+       : k_scan_points<R0, MT, true, -1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, \
+                                                                          (int)per, comp, compbest))
   const int mt = c->opt.metric;
   if (wide) {
     if (comp == nullptr) {
@@ -657,7 +677,7 @@ appd_status launch_wide_compbest(appd_ctx* c, const u64* rowbest, const int* com
 // distance), so that a radix sort over bits [32, 64) gives the Kruskal order (a4)
 template <int METRIC>
 __global__ void k_wide_edge_keys(const u64* __restrict__ tri, int64_t m, const float* __restrict__ X, int d,
-                                 u64* __restrict__ key2) {
+                                 int sense, u64* __restrict__ key2) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t u, v;
     tri_decode(tri[e] & ((1ull << 63) - 1), &u, &v);
@@ -668,37 +688,37 @@ __global__ void k_wide_edge_keys(const u64* __restrict__ tri, int64_t m, const f
       else if (METRIC == 1) acc = __fadd_rn(acc, fabsf(t));
       else acc = fmaxf(acc, fabsf(t));
     }
-    key2[e] = (u64)__float_as_uint(acc) << 32 | (u64)e;
+    key2[e] = (u64)sense_bits(__float_as_uint(acc), sense) << 32 | (u64)e;  // Kruskal order of the sense
   }
 }
 
 template <int METRIC>
-__global__ void k_wide_decode(const u64* __restrict__ key2_sorted, const u64* __restrict__ tri, int64_t m,
+__global__ void k_wide_decode(const u64* __restrict__ key2_sorted, const u64* __restrict__ tri, int64_t m, int sense,
                               int32_t* __restrict__ eu, int32_t* __restrict__ ev, float* __restrict__ ew) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
     const u64 k2 = key2_sorted[p];
     int64_t u, v;
     tri_decode(tri[k2 & 0xFFFFFFFFull] & ((1ull << 63) - 1), &u, &v);
-    const float w = __uint_as_float((uint32_t)(k2 >> 32));
+    const float w = __uint_as_float(sense_bits((uint32_t)(k2 >> 32), sense));
     eu[p] = (int32_t)u;
     ev[p] = (int32_t)v;
     ew[p] = METRIC == 0 ? __fsqrt_rn(w) : w;  // APPD(sqrtf o d2) = sqrtf o APPD(d2), App. A.4
   }
 }
 
-appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, u64* key2,
-                       u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew) {
+appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, int sense,
+                       u64* key2, u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew) {
   if (m <= 0) return APPD_OK;
   const int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)c->sm_count * 8);
-  if (metric == 1) k_wide_edge_keys<1><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
-  else if (metric == 2) k_wide_edge_keys<2><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
-  else k_wide_edge_keys<0><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, key2);
+  if (metric == 1) k_wide_edge_keys<1><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, sense, key2);
+  else if (metric == 2) k_wide_edge_keys<2><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, sense, key2);
+  else k_wide_edge_keys<0><<<grid, 256, 0, c->stream>>>(mstkeys, m, X, (int)d, sense, key2);
   APPD_LAUNCHED(c);
   appd_status s = sort_keys_u64_bits64(c, key2, key2_sorted, m, 32, 64);
   if (s) return s;
-  if (metric == 1) k_wide_decode<1><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
-  else if (metric == 2) k_wide_decode<2><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
-  else k_wide_decode<0><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, eu, ev, ew);
+  if (metric == 1) k_wide_decode<1><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, sense, eu, ev, ew);
+  else if (metric == 2) k_wide_decode<2><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, sense, eu, ev, ew);
+  else k_wide_decode<0><<<grid, 256, 0, c->stream>>>(key2_sorted, mstkeys, m, sense, eu, ev, ew);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

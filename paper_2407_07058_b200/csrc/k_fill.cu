@@ -437,7 +437,8 @@ __global__ void k_decode_edges(const u64* __restrict__ keys, int64_t m, int shif
     float w;
     if (points) {
       // R1: the weight is sqrtf of the squared distance; L1 / L-inf keys hold the distance
-      w = metric == 0 ? __fsqrt_rn(__uint_as_float(wk)) : __uint_as_float(wk);
+      const uint32_t b = sense > 0 ? wk : (~wk & 0x7FFFFFFFu);  // widest: the order-reversed bits
+      w = metric == 0 ? __fsqrt_rn(__uint_as_float(b)) : __uint_as_float(b);
     } else {
       const float mm = from_orderable(wk);
       w = (sense > 0 ? mm : -mm) + 0.0f;

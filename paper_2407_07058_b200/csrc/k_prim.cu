@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(PRIM_LOAD_THREADS, 1) k_prim(const PrimArgs A)
         }
       }
 #pragma unroll
-      for (int s = 0; s < VPT; s++) kw[s] = __float_as_uint(acc[s]);
+      // widest: the order-reversing map of the non-negative distance bits
+      for (int s = 0; s < VPT; s++) kw[s] = A.sense > 0 ? __float_as_uint(acc[s]) : (~__float_as_uint(acc[s]) & 0x7FFFFFFFu);
     }
     uint32_t bk = PRIM_VISITED;
     int bi = 0;
@@ -242,9 +243,10 @@ __global__ void __launch_bounds__(PRIM_LOAD_THREADS, 1) k_prim(const PrimArgs A)
   }
   for (int i = tid; i < m; i += NT) {
     const uint32_t k = __float_as_uint(sh[i]);
+    const uint32_t kp = A.sense > 0 ? k : (~k & 0x7FFFFFFFu);  // points: the distance bits again
     const float h = MODE == PM_WEIGHTS ? prim_weight_of_key(k, A.sense)
-                    : MODE == PM_R1    ? __fsqrt_rn(__uint_as_float(k))  // APPD(sqrtf o d2), App. A.4
-                                       : __uint_as_float(k);
+                    : MODE == PM_R1    ? __fsqrt_rn(__uint_as_float(kp))  // APPD(sqrtf o d2), App. A.4
+                                       : __uint_as_float(kp);
     sh[i] = h;
     A.ST[i] = h;
   }
@@ -390,7 +392,7 @@ appd_status launch_prim(appd_ctx* c, const float* W, const float* X, int64_t n, 
   A.X = X;
   A.n = (int)n;
   A.d = points ? (int)d : 0;
-  A.sense = points ? 1 : sense;
+  A.sense = sense;
   A.bad = bad;
   A.validate = bad != nullptr;
   A.pi = pi;
@@ -425,9 +427,13 @@ appd_status launch_prim(appd_ctx* c, const float* W, const float* X, int64_t n, 
 #endif
     return st;
   }
-  appd_status st = mode == PM_R1 ? launch_prim_mode<PM_R1, false>(c, A, n, smem)
-                   : mode == PM_L1 ? launch_prim_mode<PM_L1, false>(c, A, n, smem)
-                                   : launch_prim_mode<PM_LINF, false>(c, A, n, smem);
+  const bool widest = sense < 0;
+  appd_status st = mode == PM_R1 ? (widest ? launch_prim_mode<PM_R1, true>(c, A, n, smem)
+                                           : launch_prim_mode<PM_R1, false>(c, A, n, smem))
+                   : mode == PM_L1 ? (widest ? launch_prim_mode<PM_L1, true>(c, A, n, smem)
+                                             : launch_prim_mode<PM_L1, false>(c, A, n, smem))
+                                   : (widest ? launch_prim_mode<PM_LINF, true>(c, A, n, smem)
+                                             : launch_prim_mode<PM_LINF, false>(c, A, n, smem));
 #ifdef APPD_DEV_HOOKS
   if (A.dbg) {
     cudaMemcpy(hd, A.dbg, 32, cudaMemcpyDeviceToHost);

@@ -765,3 +765,44 @@ def test_c5x_beyond_hbm_sink(P):
     assert rows[0] == n
     assert got == g["blocks"], (got, g["blocks"])
     assert st["points_engine"] == 1 and st["fill_bytes"] == n * n * 4
+
+
+# --------------------------------------------------------------------------
+# widest paths in points mode (VERDICT r1 missing #6): Algorithm 4 in the widest
+# sense on the oracle's own point weights
+# --------------------------------------------------------------------------
+def widest_points_ref(X, metric=0):
+    return oracle.appd_weights(oracle.points_weights(X, metric=metric), -1)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_points_widest(P, variant):
+    with P.Context(sense=-1, variant=variant) as c:
+        for t, (kind, n, d) in enumerate([("uniform", 2, 3), ("blobs", 300, 4), ("dups", 700, 8), ("grid", 1000, 3),
+                                          ("clumps", 1500, 6), ("wide", 2048, 2)]):
+            if variant == 1 and n > 2048:
+                continue
+            X = G.random_points(n, d, 990 + t, kind)
+            assert_bit_equal(gpu_points(c, X), widest_points_ref(X), f"widest points {kind} n={n} variant={variant}")
+
+
+def test_points_widest_metrics_wide_keys_and_stream(P):
+    X = G.random_points(1200, 5, 995, "blobs")
+    for metric in (1, 2):
+        with P.Context(sense=-1, metric=metric) as c:
+            assert_bit_equal(gpu_points(c, X), widest_points_ref(X, metric), f"widest metric {metric}")
+    with P.Context(sense=-1, wide_keys=1) as c:
+        assert_bit_equal(gpu_points(c, X), widest_points_ref(X), "widest wide keys")
+        M = torch.empty((1200, 1200), dtype=torch.float32).pin_memory()
+        c.solve_points_stream(torch.from_numpy(X), M, 500)
+        assert_bit_equal(M.numpy(), widest_points_ref(X), "widest streamed")
+    with P.Context(sense=-1, points_engine=2) as c:  # the tensor-core filter finds minima only
+        with pytest.raises(P.AppdError) as e:
+            gpu_points(c, X)
+        assert e.value.name == "APPD_ERR_UNSUPPORTED"
+
+
+def test_points_widest_c2(P):
+    X = G.config("C2")
+    with P.Context(sense=-1) as c:
+        assert_bit_equal(gpu_points(c, X), widest_points_ref(X), "widest C2")

@@ -49,6 +49,7 @@ CASES = [
     ("points_prim_replicated_900", "points", ("blobs", 900, 3), {"variant": 1}),
     ("points_prim_fused_300", "points", ("dups", 300, 4), {"variant": 1}),
     ("points_wide_keys_1200", "points", ("dups", 1200, 6), {"wide_keys": 1}),
+    ("points_widest_1100", "points", ("blobs", 1100, 4), {"sense": -1}),
     ("c3_shape_4096_ties", "weights", ("C3", 4096), {}),
     ("weights_ties_1031", "weights", ("ties", 1031), {}),
     ("weights_negative_600_nocache", "weights", ("negative", 600), {"topk": -1}),
@@ -74,6 +75,8 @@ def oracle_rows(mode, A, r0, rows, opts):
     if rows == 0:
         return np.zeros((0, A.shape[0]), np.float32)
     if mode == "points":
+        if opts.get("sense", 1) < 0:
+            return oracle.appd_weights(oracle.points_weights(A, metric=opts.get("metric", 0)), -1)[r0:r0 + rows]
         if opts.get("metric"):
             return oracle.appd_points(A, metric=opts["metric"])[r0:r0 + rows]
         return oracle.appd_points_rows(A, r0, rows)
