@@ -264,7 +264,7 @@ def run_native(args):
                 "algorithmic_bytes_per_launch": fill_bytes, "avg_launch_ms": fill_ms,
                 "peak_source": pk["source"]}
     stage_ms = {k: statistics.mean(s[k] for s in stats) for k in
-                ("ms_validate", "ms_mst", "ms_sort", "ms_dendrogram", "ms_prep", "ms_fill", "ms_total", "ms_scan",
+                ("ms_validate", "ms_mst", "ms_sort", "ms_dendrogram", "ms_prep", "ms_fill", "ms_total",
                  "ms_tcscan")}
     roofline["write_only_peak_gbs"] = write_gbs
     roofline["frac_of_write_only_peak"] = fill_gbs / write_gbs

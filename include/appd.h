@@ -97,7 +97,9 @@ typedef struct {
   int32_t variant;               /* APPD_VARIANT_* (default AUTO) */
   int32_t validate;              /* 1 = check W/X (default), 0 = trust the input */
   int32_t sense;                 /* +1 minimax (default), -1 widest path (points: exact engine / Prim) */
-  int32_t timing;                /* 1 = record per-stage CUDA events (appd_get_stats), default 0 */
+  int32_t timing;                /* 1 = record per-stage CUDA events (appd_get_stats: ms_validate .. ms_total,
+                                    ms_tcscan), 2 = also per-round scan events (ms_scan; each event costs
+                                    a few us of stream time), default 0 */
   int32_t dendrogram;            /* 0 auto, 1 host union-find, 2 GPU */
   int32_t points_engine;         /* points-mode MST scan: 0 auto, 1 exact FP32 (CUDA cores), 2 tensor-core
                                     filter + exact recheck of the survivors (tcgen05) */

@@ -688,7 +688,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
       u64* WCM = (u64*)ws(c, S_TC_WCM, sizeof(u64) * k * k);
       if (!WCM) return fail(c, APPD_ERR_OUT_OF_MEMORY, "component matrix");
       bool ovf = false;
-      if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
+      if (c->opt.timing >= 2) cudaEventRecord(c->ev[8], c->stream);
       if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf, c->opt.world > 1))) return s;
       if (c->opt.world > 1) {  // every rank must take the same branch
         u64* flag = (u64*)ws(c, S_TMP, sizeof(u64));
@@ -713,7 +713,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 48, cm_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
                                      c->stream));
         cm_status_pending = true;
-        if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
+        if (c->opt.timing >= 2) cudaEventRecord(c->ev[9], c->stream);
         cm_timing_pending = c->opt.timing != 0;  // read after the final synchronisation
         c->stats.cm_k = (int)k;
         c->stats.tcscan_launches++;
@@ -736,7 +736,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
     if (!(use_tc && tc.lookup_pending) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
-    if (c->opt.timing) cudaEventRecord(c->ev[8], c->stream);
+    if (c->opt.timing >= 2) cudaEventRecord(c->ev[8], c->stream);  // per-round scan time (diagnostics)
     const int64_t l0 = c->launches;
     if (points && use_tc) {
       bool overflowed = false;
@@ -806,7 +806,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
     }
     if (s) return s;
     c->stats.scan_launches += c->launches - l0;
-    if (c->opt.timing) cudaEventRecord(c->ev[9], c->stream);
+    if (c->opt.timing >= 2) cudaEventRecord(c->ev[9], c->stream);
     host_mark("round scan queued");
     if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
     // the next round's cache lookup rides on this round's synchronisation (labels are
@@ -886,7 +886,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
         return s2;
       }
     }
-    if (c->opt.timing) c->stats.ms_scan += ev_ms(c, 8, 9);
+    if (c->opt.timing >= 2) c->stats.ms_scan += ev_ms(c, 8, 9);
     if (use_tc) {
       if (c->opt.timing && tc.scanned) {
         float ms = 0.0f;
@@ -1159,7 +1159,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if (*mst_count != n - 1)
     return fail(c, APPD_ERR_CUDA, "MST has %d edges, expected %lld", *mst_count, (long long)(n - 1));
   if (cm_timing_pending) {  // the component-matrix pass's events are complete only now
-    c->stats.ms_scan += ev_ms(c, 8, 9);
+    if (c->opt.timing >= 2) c->stats.ms_scan += ev_ms(c, 8, 9);
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]) == cudaSuccess) c->stats.ms_tcscan += ms;
     cudaGetLastError();

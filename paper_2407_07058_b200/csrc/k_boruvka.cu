@@ -431,16 +431,22 @@ __device__ __forceinline__ uint32_t sense_bits(uint32_t b, int sense) { return s
 template <bool ROUND0, int METRIC = 0, bool WIDE = false, int SENSE = 1>
 __global__ void __launch_bounds__(256, 2)
     k_scan_points(const float* __restrict__ XT, int64_t n, int64_t npad, int dpad, int64_t row0, int64_t rows,
-                  int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest) {
+                  int col_tiles_per_cta, const int* __restrict__ comp, u64* __restrict__ compbest, int sym) {
   extern __shared__ __align__(16) float smem[];
   float* As = smem;                           // [2][KC][BM]
   float* Bs = smem + 2 * PT_KC * PT_BM;       // [2][KC][BN]
   int* ccol = (int*)(Bs + 2 * PT_KC * PT_BN); // [BN] component labels of the current column tile
+  // sym: [16][BN] per-column best of each thread row (ty) of a tile, for the column epilogue
+  u64* colbest = reinterpret_cast<u64*>(ccol + PT_BN);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t rbase = row0 + (int64_t)blockIdx.x * PT_BM;
   const int64_t total_col_tiles = npad / PT_BN;
-  const int64_t ct0 = (int64_t)blockIdx.y * col_tiles_per_cta;
-  int64_t ct1 = ct0 + col_tiles_per_cta;
+  // sym (one rank, every row): only the column tiles ct >= this row block's own, split in
+  // gridDim.y parts; the pairs of an off-diagonal tile also update their COLUMNS' rows
+  const int64_t rb = blockIdx.x;
+  const int64_t span = sym ? (total_col_tiles - rb + gridDim.y - 1) / gridDim.y : col_tiles_per_cta;
+  const int64_t ct0 = sym ? rb + (int64_t)blockIdx.y * span : (int64_t)blockIdx.y * col_tiles_per_cta;
+  int64_t ct1 = ct0 + span;
   if (ct1 > total_col_tiles) ct1 = total_col_tiles;
   if (ct0 >= ct1) return;
   const int nk = dpad / PT_KC;
@@ -528,6 +534,42 @@ __global__ void __launch_bounds__(256, 2)
           if (elig && (bj[a] < 0 || (SENSE > 0 ? acc[a][b] < bd[a] : acc[a][b] > bd[a]))) { bd[a] = acc[a][b]; bj[a] = j; }
         }
       }
+      if (sym && ct != rb) {
+        // column epilogue: each column j's best row of this tile, (weight, i) smallest, over
+        // the thread's 8 rows, then over the 16 thread rows through shared memory
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+          const int64_t j = ct * PT_BN + tx * 8 + b;
+          const int cj = ROUND0 ? 0 : ccol[tx * 8 + b];
+          u64 best = KEY_NONE;
+#pragma unroll
+          for (int a = 0; a < 8; a++) {
+            const bool elig = ri[a] < n && j < n && (ROUND0 || (cj != cr[a] && cj >= 0));
+            const u64 key = ((u64)sense_bits(__float_as_uint(acc[a][b]), SENSE) << 32) | (u64)ri[a];
+            best = elig && key < best ? key : best;
+          }
+          colbest[ty * PT_BN + tx * 8 + b] = best;
+        }
+        __syncthreads();
+        if (threadIdx.x < PT_BN) {
+          u64 best = KEY_NONE;
+#pragma unroll
+          for (int t = 0; t < 16; t++) {
+            const u64 v = colbest[t * PT_BN + threadIdx.x];
+            best = v < best ? v : best;
+          }
+          const int64_t j = ct * PT_BN + threadIdx.x;
+          if (best != KEY_NONE) {
+            if (WIDE) {
+              atomicMin(compbest + j, best);  // row j's winner (w, i)
+            } else {
+              const int64_t i = (int64_t)(best & 0xFFFFFFFFull);
+              const u64 gkey = (((best >> 32) & 0x7FFFFFFFull) << 33) | tri_index(i, j);
+              atomicMin(compbest + (ROUND0 ? j : ccol[threadIdx.x]), gkey);
+            }
+          }
+        }
+      }
     }
     __syncthreads();
   }
@@ -556,8 +598,10 @@ __global__ void __launch_bounds__(256, 2)
 
 appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t npad, int64_t dpad, int64_t row0,
                                int64_t rows, const int* comp, u64* compbest, bool wide) {
-  const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4;
+  const size_t smem = (size_t)(2 * PT_KC * PT_BM + 2 * PT_KC * PT_BN) * 4 + PT_BN * 4 + 16 * PT_BN * 8;
   if (rows <= 0) return APPD_OK;
+  // one rank holding every row: the symmetric pass (each unordered pair once)
+  const int sym = (row0 == 0 && rows == n) ? 1 : 0;
   static std::atomic<unsigned long long> attr{0};
   if (needs_setup(attr, c)) {
     cudaFuncSetAttribute(k_scan_points<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -583,8 +627,9 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
   }
   int64_t row_blocks = (rows + PT_BM - 1) / PT_BM;
   int64_t col_tiles = npad / PT_BN;
-  // enough CTAs for ~4 waves of 2 CTAs/SM; split the column range accordingly
-  int64_t want = (int64_t)c->sm_count * 2 * 4;
+  // enough CTAs for ~4 waves of 2 CTAs/SM; split the column range accordingly (sym: the
+  // first row blocks hold the longest ranges and are scheduled first)
+  int64_t want = (int64_t)c->sm_count * 2 * 4 * (sym ? 2 : 1);
   int64_t splits = (want + row_blocks - 1) / row_blocks;
   if (splits > col_tiles) splits = col_tiles;
   if (splits < 1) splits = 1;
@@ -594,15 +639,15 @@ appd_status launch_scan_points(appd_ctx* c, const float* XT, int64_t n, int64_t 
 #define APPD_SCAN_POINTS(R0, MT)                                                                               \
   (c->opt.sense > 0                                                                                           \
        ? k_scan_points<R0, MT, false, 1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows,  \
-                                                                          (int)per, comp, compbest)           \
+                                                                          (int)per, comp, compbest, sym)      \
        : k_scan_points<R0, MT, false, -1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, \
-                                                                           (int)per, comp, compbest))
+                                                                           (int)per, comp, compbest, sym))
 #define APPD_SCAN_POINTS_W(R0, MT)                                                                            \
   (c->opt.sense > 0                                                                                          \
        ? k_scan_points<R0, MT, true, 1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows,  \
-                                                                         (int)per, comp, compbest)           \
+                                                                         (int)per, comp, compbest, sym)      \
        : k_scan_points<R0, MT, true, -1><<<grid, 256, smem, c->stream>>>(XT, n, npad, (int)dpad, row0, rows, \
-                                                                          (int)per, comp, compbest))
+                                                                          (int)per, comp, compbest, sym))
   const int mt = c->opt.metric;
   if (wide) {
     if (comp == nullptr) {
