@@ -386,6 +386,7 @@ static void dev_check(appd_ctx* c, const char* what, const int32_t* d_eu, const 
 // (33) into 64 bits; above it (NEXT-4, outputs beyond HBM) the wide-key path; the upper
 // bound keeps every index an int32 and the pair index below 2^40
 constexpr int64_t kMaxPackedPoints = 131072, kMaxPoints = 1 << 20;
+constexpr int64_t kExactEngineMaxN = 2048;  // AUTO: exact FP32 engine up to here (measured)
 
 // ---------------------------------------------------------------------------
 // The Prim variant (k_prim.cu): one single-CTA launch validates the
@@ -521,8 +522,8 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   if (points && sense < 0 && c->opt.points_engine == 2)
     return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine finds minimum edges only (widest sense: exact engine)");
   const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 &&
-                                c->opt.metric == 0 && sense > 0 && n >= 2 && n <= kMaxPackedPoints &&
-                                c->opt.wide_keys != 1;
+                                (c->opt.points_engine == 2 || n > kExactEngineMaxN) && c->opt.metric == 0 &&
+                                sense > 0 && n >= 2 && n <= kMaxPackedPoints && c->opt.wide_keys != 1;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
   if (c->opt.validate) {
     u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
@@ -603,7 +604,11 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   // the dimension does not fit the shared-memory ring
   TcState tc;
   bool use_tc = false;
-  if (points && !wide && sense > 0 && c->opt.points_engine != 1 && c->opt.metric == 0 && n >= 2) {
+  // AUTO engine: the tensor-core filter pays off above ~2048 points; below, the symmetric
+  // exact pass wins (measured, tools/engine_cmp.py: n = 2048, d = 2 / 64: 0.55 / 0.54 ms
+  // exact against 0.64 / 0.64 ms tensor core; n = 4096, d = 2: 0.96 against 0.87 ms)
+  const bool tc_wanted = c->opt.points_engine == 2 || (c->opt.points_engine == 0 && n > kExactEngineMaxN);
+  if (points && !wide && sense > 0 && tc_wanted && c->opt.metric == 0 && n >= 2) {
     s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
     host_mark("tcf_prepare queued");
     if (s == APPD_OK) {

@@ -348,12 +348,12 @@ def test_points_too_large_for_the_filter(P):
     first synchronisation and the solve is redone on the exact engine (same result as the
     oracle, infinite distances included)."""
     rs = np.random.default_rng(8)
-    X = (rs.standard_normal((300, 6)) * 1e20).astype(np.float32)
-    X[:150] *= np.float32(1e-20)  # half of the points at ordinary scale
+    X = (rs.standard_normal((2500, 6)) * 1e20).astype(np.float32)  # n > 2048: AUTO tries the filter
+    X[:1250] *= np.float32(1e-20)  # half of the points at ordinary scale
     with P.Context(timing=True, variant=P.VARIANT_BORUVKA) as c:
         assert_bit_equal(gpu_points(c, X), oracle.appd_points(X), "huge coordinates")
         assert c.stats()["points_engine"] == 1
-        Xs = G.random_points(500, 8, 3, "blobs")  # the same context keeps working afterwards
+        Xs = G.random_points(2500, 8, 3, "blobs")  # the same context keeps working afterwards
         assert_bit_equal(gpu_points(c, Xs), oracle.appd_points(Xs), "after fallback")
         assert c.stats()["points_engine"] == 2
 
