@@ -1019,11 +1019,12 @@ appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsign
     APPD_LAUNCHED(c);
   }
   const int grid = c->sm_count * (mode == 0 ? 5 : 4);  // 5 x 40 KB of shared memory fit an SM
-  static size_t attr_smem[2] = {0, 0};  // set once per size (attribute calls cost host time)
-  if (attr_smem[mode ? 1 : 0] < smem) {
-    if (mode == 0) cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else cudaFuncSetAttribute(k_list_exact<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_smem[mode ? 1 : 0] = smem;
+  // set once per device at the largest size any d needs (attribute calls cost host time)
+  static std::atomic<unsigned long long> attr{0};
+  if (needs_setup(attr, c)) {
+    cudaFuncSetAttribute(k_list_exact<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_list_exact<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    setup_done(attr, c);
   }
   if (mode == 0) k_list_exact<0><<<grid, 256, smem, c->stream>>>(L);
   else k_list_exact<1><<<grid, 256, smem, c->stream>>>(L);
