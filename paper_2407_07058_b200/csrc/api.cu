@@ -13,6 +13,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 using namespace appd;
@@ -268,8 +270,18 @@ static appd_status check_device_ptr(appd_ctx* c, const void* p, const char* name
   return APPD_OK;
 }
 
+// Stage boundaries: CUDA events (timing) and NVTX ranges "appd:<stage>" (header-only
+// NVTX3: no cost unless a profiler attaches; SURVEY §5 tracing)
+static const char* kStageNames[6] = {"appd:validate", "appd:mst", "appd:sort", "appd:dendrogram", "appd:prep",
+                                     "appd:fill"};
 static inline void stage_event(appd_ctx* c, int idx) {
   if (c->opt.timing) cudaEventRecord(c->ev[idx], c->stream);
+  if (c->nvtx_stage) nvtxRangeEnd(c->nvtx_stage);
+  c->nvtx_stage = idx < 6 ? nvtxRangeStartA(kStageNames[idx]) : 0;
+}
+static inline void nvtx_close(appd_ctx* c) {
+  if (c->nvtx_stage) nvtxRangeEnd(c->nvtx_stage);
+  c->nvtx_stage = 0;
 }
 
 
@@ -482,8 +494,19 @@ static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64
   return APPD_OK;
 }
 
-// The whole pipeline.  X (points) or W (weights) is a device pointer.
+static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M);
+
+// The whole pipeline (one NVTX range per call, one per stage inside)
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
+  nvtxRangePushA(X ? "appd_solve_points" : "appd_solve_weights");
+  const appd_status s = solve_impl(c, W, X, n, d, M);
+  nvtx_close(c);
+  nvtxRangePop();
+  return s;
+}
+
+// X (points) or W (weights) is a device pointer.
+static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   const bool points = X != nullptr;
   const bool f64 = c->f64_W != nullptr;  // NEXT-3 (k_f64.cu): W and M are c->f64_W / c->f64_M
   const int sense = c->opt.sense;  // points too: widest paths on the exact engine or Prim

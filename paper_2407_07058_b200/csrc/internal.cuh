@@ -114,6 +114,7 @@ struct appd_ctx {
   // events for stage timing
   cudaEvent_t ev[16];
   bool ev_ready = false;
+  uint64_t nvtx_stage = 0;  // the open NVTX stage range (nvtxRangeId_t)
   // pinned host staging for host-buffer calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;

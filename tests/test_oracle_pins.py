@@ -654,3 +654,65 @@ def test_prim_against_independent_kruskal(kind):
         kt = kruskal_numpy(W)
         assert sorted(float(x) for x in ew) == sorted(float(w) for _, _, w in kt)
         assert_bit_equal(oracle.appd_weights(W), tree_path_appd(n, kt) + np.float32(0))
+
+
+# --------------------------------------------------------------------------
+# fault injection: the checks that pin results must catch a corrupted APPD --
+# one entry changed to another MST weight, one merge height changed, two leaves swapped
+# in the leaf order -- so a GPU fault of that shape cannot pass as parity
+# --------------------------------------------------------------------------
+def _fill_from_dendrogram(pi, h, sense=1):
+    """M[pi_a][pi_b] = max (min for widest) of h[a..b-1] -- the fill's identity (App. A.2)."""
+    n = len(pi)
+    M = np.zeros((n, n), np.float32)
+    for a in range(n):
+        run = np.float32(-np.inf if sense > 0 else np.inf)
+        for b in range(a + 1, n):
+            run = max(run, h[b - 1]) if sense > 0 else min(run, h[b - 1])
+            M[pi[a], pi[b]] = M[pi[b], pi[a]] = run
+    return M
+
+
+def test_corruptions_are_caught():
+    W = G.random_weights(40, 77, "uniform")
+    M = oracle.appd_weights(W)
+    check_invariants(W, M)
+    # the leaf-order identity reproduces the oracle from a Prim order (App. A.3) ...
+    eu, ev, ew = oracle.prim_weights(W, 1)
+    order = [0] + [int(v) for v in ev]
+    pi = np.array(order, np.int32)
+    h = np.array(ew, np.float32)
+    assert (bits(_fill_from_dendrogram(pi, h)) == bits(M)).all()
+    # ... and each corruption below changes bits that parity compares, or breaks an invariant
+    bad = M.copy()
+    i, j = 3, 17
+    other = np.float32(ew[(np.searchsorted(np.sort(ew), M[i, j]) + 1) % len(ew)])
+    bad[i, j] = bad[j, i] = other  # another MST weight, still symmetric: parity sees it
+    assert (bits(bad) != bits(M)).any()
+    one_sided = M.copy()
+    one_sided[i, j] = other  # a one-sided write: the invariants see it without the oracle
+    with pytest.raises(AssertionError):
+        check_invariants(W, one_sided)
+    h2 = h.copy()
+    h2[10] = np.float32(h2[10] * 0.5)  # one merge height
+    assert (bits(_fill_from_dendrogram(pi, h2)) != bits(M)).any()
+    pi2 = pi.copy()
+    pi2[[5, 30]] = pi2[[30, 5]]  # two leaves swapped
+    assert (bits(_fill_from_dendrogram(pi2, h)) != bits(M)).any()
+
+
+def test_oracle_under_sanitizers(tmp_path):
+    """The oracle's C code under -fsanitize=address,undefined: Algorithm 4, the row windows,
+    Floyd, brute force and the points path on small inputs, checked against each other
+    (tests/oracle_san_main.c); any out-of-bounds access or UB aborts the run."""
+    import subprocess
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    exe = tmp_path / "oracle_san"
+    cmd = ["gcc", "-O1", "-g", "-std=c11", "-ffp-contract=off", "-mfma", "-fsanitize=address,undefined",
+           "-fno-sanitize-recover=all", os.path.join(here, "oracle_san_main.c"),
+           os.path.join(os.path.dirname(here), "oracle", "oracle.c"), "-lm", "-o", str(exe)]
+    subprocess.check_call(cmd)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ok" in out.stdout
