@@ -496,10 +496,67 @@ static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64
 
 static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M);
 
+#ifdef APPD_DEV_HOOKS
+namespace appd {
+namespace {
+struct TraceState {
+  bool on = dev_env("APPD_TRACE") != nullptr;
+  int depth = 0, used = 0;
+  cudaEvent_t ev[1024];
+  const char* site[1024];
+  double host_us[1024];
+  std::chrono::steady_clock::time_point t0;
+};
+TraceState& trace_state() {
+  static TraceState t;
+  return t;
+}
+}  // namespace
+void trace_begin(appd_ctx* c) {
+  TraceState& t = trace_state();
+  if (!t.on || t.depth++) return;
+  t.used = 0;
+  t.t0 = std::chrono::steady_clock::now();
+  trace_launch(c, "solve begin");
+}
+void trace_launch(appd_ctx* c, const char* site) {
+  TraceState& t = trace_state();
+  if (!t.on || t.used >= 1024) return;
+  if (!t.ev[t.used]) cudaEventCreate(&t.ev[t.used]);
+  cudaEventRecord(t.ev[t.used], c->stream);
+  t.site[t.used] = site;
+  t.host_us[t.used] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t.t0).count();
+  t.used++;
+}
+void trace_end(appd_ctx* c) {
+  TraceState& t = trace_state();
+  if (!t.on || --t.depth) return;
+  trace_launch(c, "solve end");
+  cudaStreamSynchronize(c->stream);
+  const char* base;
+  for (int i = 0; i < t.used; i++) {
+    float ms = 0.0f, ms0 = 0.0f;
+    if (i) cudaEventElapsedTime(&ms, t.ev[i - 1], t.ev[i]);
+    cudaEventElapsedTime(&ms0, t.ev[0], t.ev[i]);
+    base = strrchr(t.site[i], '/');
+    fprintf(stderr, "[trace] %3d host %8.1f us  gpu %8.1f us  +%7.1f us  %s\n", i, t.host_us[i], 1e3 * ms0, 1e3 * ms,
+            base ? base + 1 : t.site[i]);
+  }
+  cudaGetLastError();
+}
+}  // namespace appd
+#endif
+
 // The whole pipeline (one NVTX range per call, one per stage inside)
 static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n, int64_t d, float* M) {
   nvtxRangePushA(X ? "appd_solve_points" : "appd_solve_weights");
+#ifdef APPD_DEV_HOOKS
+  trace_begin(c);
+#endif
   const appd_status s = solve_impl(c, W, X, n, d, M);
+#ifdef APPD_DEV_HOOKS
+  trace_end(c);
+#endif
   nvtx_close(c);
   nvtxRangePop();
   return s;

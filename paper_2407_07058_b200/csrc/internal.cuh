@@ -280,8 +280,16 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
     if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
   } while (0)
 
+#ifdef APPD_DEV_HOOKS
+#define APPD_TRACE_SYNC(c) appd::trace_launch(c, "SYNC " __FILE__ ":" APPD_STR(__LINE__))
+#else
+#define APPD_TRACE_SYNC(c) \
+  do {                     \
+  } while (0)
+#endif
 #define APPD_SYNC(c)                                 \
   do {                                               \
+    APPD_TRACE_SYNC(c);                              \
     appd_status _s = appd::sync_stream(c);           \
     if (_s != APPD_OK) return _s;                    \
   } while (0)
@@ -289,6 +297,12 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
 #define APPD_STR2(x) #x
 #define APPD_STR(x) APPD_STR2(x)
 #ifdef APPD_DEV_HOOKS
+// development builds: APPD_TRACE=1 records an event after every launch and prints, per
+// solve, each launch site with its host issue time and the GPU time since the previous
+// event (kernel + gap), to find where the GPU idles
+void trace_launch(appd_ctx* c, const char* site);
+void trace_begin(appd_ctx* c);
+void trace_end(appd_ctx* c);
 // development builds: APPD_SYNC_EACH=1 synchronises after every launch, so an
 // asynchronous fault is reported at the kernel that caused it
 #define APPD_DEV_SYNC_EACH(c)                                                                    \
@@ -298,6 +312,7 @@ appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
       cudaError_t _e2 = cudaStreamSynchronize((c)->stream);                                     \
       if (_e2 != cudaSuccess) return appd::cuda_fail(c, _e2, "kernel " __FILE__ ":" APPD_STR(__LINE__)); \
     }                                                                                           \
+    appd::trace_launch(c, __FILE__ ":" APPD_STR(__LINE__));                                     \
   } while (0)
 #else
 #define APPD_DEV_SYNC_EACH(c) \
