@@ -174,10 +174,14 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   }
   for (int i = 0; i < 16; i++) cudaEventCreate(&c->ev[i]);
   c->ev_ready = true;
-  if (cudaHostAlloc((void**)&c->pinned_small, 64 * sizeof(unsigned), cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc((void**)&c->pinned_small, 64 * sizeof(unsigned), cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     appd_destroy(c);
     return APPD_ERR_OUT_OF_MEMORY;
+  }
+  if (cudaHostGetDevicePointer((void**)&c->pinned_small_dev, c->pinned_small, 0) != cudaSuccess) {
+    cudaGetLastError();
+    c->pinned_small_dev = nullptr;  // publish() falls back to copies
   }
   if (o.world > 1) {
     appd_status s = nccl_init(c, o.nccl_unique_id, o.rank, o.world);
@@ -454,7 +458,7 @@ static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64
   appd_status s = launch_prim(c, W, X, n, d, sense, points ? c->opt.metric : 0, bad, pi, pos, rowpos, ST, m, levels,
                               fused ? M : nullptr, row0, rows);
   if (s) return s;
-  if (bad) APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+  if (bad) APPD_PUBLISH(c, hbad, bad, 3 * sizeof(u64));
   for (int e = 2; e <= 4; e++) stage_event(c, e);
   const int* rows_sorted = pi;
   if (c->opt.world > 1 && !fused) {  // replicated Prim, this rank's rows in leaf order
@@ -554,6 +558,7 @@ static appd_status solve(appd_ctx* c, const float* W, const float* X, int64_t n,
   trace_begin(c);
 #endif
   const appd_status s = solve_impl(c, W, X, n, d, M);
+  if (s != APPD_OK) c->npub = 0;  // queued publications of a failed solve are dropped
 #ifdef APPD_DEV_HOOKS
   trace_end(c);
 #endif
@@ -605,15 +610,24 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
                                 (c->opt.points_engine == 2 || n > kExactEngineMaxN) && c->opt.metric == 0 &&
                                 sense > 0 && n >= 2 && n <= kMaxPackedPoints && c->opt.wide_keys != 1;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
+  u64* vbad = nullptr;
   if (c->opt.validate) {
-    u64* bad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
-    if (!bad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
-    APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
-    appd_status s = points ? launch_validate_points(c, X, n, d, bad)
-                    : f64  ? launch_validate_weights_f64(c, c->f64_W, n, bad)
-                           : launch_validate_weights(c, W, n, row0, rows, bad);
+    vbad = (u64*)ws(c, S_VALID, 3 * sizeof(u64));
+    if (!vbad) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
+  }
+  auto launch_validation = [&]() -> appd_status {
+    APPD_CUDA(c, cudaMemsetAsync(vbad, 0xFF, 3 * sizeof(u64), c->stream));
+    appd_status s = points ? launch_validate_points(c, X, n, d, vbad)
+                    : f64  ? launch_validate_weights_f64(c, c->f64_W, n, vbad)
+                           : launch_validate_weights(c, W, n, row0, rows, vbad);
     if (s) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+    APPD_PUBLISH(c, hbad, vbad, 3 * sizeof(u64));
+    return APPD_OK;
+  };
+  // deferred: the tensor-core preparation validates the points itself (one launch)
+  if (c->opt.validate && !defer_validation) {
+    appd_status s = launch_validation();
+    if (s) return s;
   }
   if (c->opt.validate && !defer_validation) {
     appd_status s;
@@ -689,12 +703,20 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
   // exact against 0.64 / 0.64 ms tensor core; n = 4096, d = 2: 0.96 against 0.87 ms)
   const bool tc_wanted = c->opt.points_engine == 2 || (c->opt.points_engine == 0 && n > kExactEngineMaxN);
   if (points && !wide && sense > 0 && tc_wanted && c->opt.metric == 0 && n >= 2) {
-    s = tcf_prepare(c, X, n, d, &tc);  // no synchronisation: scale and verdict are read later
+    // the round state's initialisation rides on the preparation's launch
+    InitList init;
+    init.add(comp, n, 0, 2);
+    init.add(counters, 16, 0, 0);
+    init.add(compbest, n, KEY_NONE, 1);
+    // no synchronisation: scale and verdict are read later
+    s = tcf_prepare(c, X, n, d, &tc, &init, defer_validation ? vbad : nullptr);
     host_mark("tcf_prepare queued");
     if (s == APPD_OK) {
       use_tc = true;
+      if (defer_validation) APPD_PUBLISH(c, hbad, vbad, 3 * sizeof(u64));
     } else {
       if (defer_validation) {  // the verdict decides before any fallback
+        if (appd_status sl = launch_validation()) return sl;
         APPD_SYNC(c);
         u64 hb[3];
         memcpy(hb, hbad, sizeof hb);
@@ -723,8 +745,10 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     return launch_transpose_points(c, X, n, d, XT, npad, dpad);
   };
   if (points && !use_tc && (s = ensure_xt())) return s;
-  if ((s = launch_iota(c, comp, n))) return s;
-  APPD_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(int) * 16, c->stream));
+  if (!use_tc) {  // (the tensor-core preparation initialised these)
+    if ((s = launch_iota(c, comp, n))) return s;
+    APPD_CUDA(c, cudaMemsetAsync(counters, 0, sizeof(int) * 16, c->stream));
+  }
   int64_t k = n;
   int rounds = 0;
   int* hostk = reinterpret_cast<int*>(c->pinned_small + 24);  // pinned: the copies stay asynchronous
@@ -759,7 +783,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     appd_status s2 = launch_cache_lookup(c, (int)row0, (int)(row0 + rows), wtopk, (int)n, w_ckey, w_cj, w_ccnt, comp,
                                          compbest, w_need, w_count, w_list);
     if (s2) return s2;
-    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, w_count, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    APPD_PUBLISH(c, c->pinned_small + 9, w_count, sizeof(unsigned));
     w_pending = true;
     return APPD_OK;
   };
@@ -795,8 +819,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
         if ((s = launch_cm_prim(c, WCM, (int)k, mstkeys, counters, tc.counters + 1, tc.list_entries_cap, tc.cstart,
                                 tc.perm, cm_status)))
           return s;
-        APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 48, cm_status, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                     c->stream));
+        APPD_PUBLISH(c, c->pinned_small + 48, cm_status, sizeof(unsigned));
         cm_status_pending = true;
         if (c->opt.timing >= 2) cudaEventRecord(c->ev[9], c->stream);
         cm_timing_pending = c->opt.timing != 0;  // read after the final synchronisation
@@ -819,7 +842,8 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     static const bool dbg = dev_env("APPD_DEBUG_ROUNDS") != nullptr;
     static const bool tc_verify = dev_env("APPD_TC_VERIFY") != nullptr;
     if (dbg) cudaEventRecord(c->ev[12], c->stream);
-    if (!(use_tc && tc.lookup_pending) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE))) return s;
+    if (!(use_tc && (tc.lookup_pending || rounds == 0)) && !w_pending && (s = launch_fill_u64(c, compbest, k, KEY_NONE)))
+      return s;
     const int* cmp = rounds == 0 ? nullptr : comp;
     if (c->opt.timing >= 2) cudaEventRecord(c->ev[8], c->stream);  // per-round scan time (diagnostics)
     const int64_t l0 = c->launches;
@@ -933,8 +957,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       fused_lookup = la.ckey != nullptr;
     }
     if (fused_lookup) {
-      APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, la.count, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                   c->stream));
+      APPD_PUBLISH(c, c->pinned_small + 9, la.count, sizeof(unsigned));
       if (use_tc && tc.topk) tc.lookup_pending = true;
       else w_pending = true;
     } else {
@@ -947,8 +970,8 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
         if ((s = w_lookup_async())) return s;
       }
     }
-    APPD_CUDA(c, cudaMemcpyAsync(&hostk[0], newid + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    APPD_CUDA(c, cudaMemcpyAsync(&hostk[1], flags + (k - 1), sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    APPD_PUBLISH(c, &hostk[0], newid + (k - 1), sizeof(int));
+    APPD_PUBLISH(c, &hostk[1], flags + (k - 1), sizeof(int));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
     host_mark("round queued, synchronising");
     APPD_SYNC(c);
@@ -1014,7 +1037,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
   // MST edge count: checked at the final synchronisation (an internal consistency check)
   int* mst_count = reinterpret_cast<int*>(c->pinned_small + 26);
   *mst_count = -1;
-  APPD_CUDA(c, cudaMemcpyAsync(mst_count, counters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  APPD_PUBLISH(c, mst_count, counters, sizeof(int));
   stage_event(c, 2);
 
   // ---- a4: sort the MST edge keys ascending (Kruskal order = P:L98's descending removal reversed) ----
@@ -1332,7 +1355,7 @@ extern "C" appd_status appd_floyd_weights(appd_ctx* c, const float* W, int64_t n
     u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);
     APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
     if ((s = launch_validate_weights(c, W, n, 0, n, bad))) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(hbad, bad, 3 * sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+    APPD_PUBLISH(c, hbad, bad, 3 * sizeof(u64));
     APPD_SYNC(c);
     u64 hb[3];
     memcpy(hb, hbad, sizeof hb);

@@ -119,6 +119,16 @@ struct appd_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
+  // the same words as the device sees them (mapped pinned memory): small device results are
+  // published there by one kernel per synchronisation instead of one copy each (publish())
+  unsigned* pinned_small_dev = nullptr;
+  struct PubEntry {
+    const void* src;
+    unsigned* dst;
+    int words;
+  };
+  PubEntry pub[16];
+  int npub = 0;
   std::vector<unsigned long long> host_xchg;  // host exchange backend staging (opt.host_allreduce)
   std::vector<int32_t> uf_scratch;   // host dendrogram work arrays
   // streamed output (NEXT-4, appd_solve_points_stream): M rows go to this host buffer in
@@ -178,7 +188,7 @@ enum Slot {
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
   S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE, S_F64_A, S_F64_B, S_F64_HW,
-  S_WIDE_ROW, S_WIDE_COMPW, S_WIDE_KEY2,
+  S_WIDE_ROW, S_WIDE_COMPW, S_WIDE_KEY2, S_LIST_CNT,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");
@@ -239,8 +249,25 @@ struct TcState {
   int64_t last_rescan_rows = 0, last_rescan_blocks = 0, invalid_rows = 0, last_list_entries = 0;
   bool scanned = false;  // this round launched the tensor-core scan (ev[10] -> ev[11] bracket it)
   bool lookup_pending = false;  // next round's cache lookup already queued (tcf_lookup_async)
+  bool r0_packed = false;       // the cooperative preparation also packed round 0 (identity order)
 };
-appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st);
+// device buffers to initialise before the first round, folded into one launch
+struct InitTask {
+  void* p;
+  int64_t count;
+  u64 value;
+  int kind;  // 0: fill 32-bit words with value, 1: fill 64-bit words, 2: iota (int32)
+};
+struct InitList {
+  InitTask t[16];
+  int count = 0;
+  void add(void* p, int64_t count_, u64 value, int kind) { t[this->count++] = {p, count_, value, kind}; }
+};
+// init: buffers the caller needs initialised (done inside the preparation when it runs
+// as one cooperative kernel, else by one separate launch); bad (validation, device
+// u64[3], may be null): non-finite coordinates are reported there (first element index)
+appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st,
+                        const InitList* init = nullptr, u64* bad = nullptr);
 appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp, int round, int64_t k,
                       u64* compbest, int64_t row_tile_begin, int64_t row_tile_end, bool* overflowed);
 
@@ -274,19 +301,24 @@ void* ws(appd_ctx* c, int slot, size_t bytes);  // grows; returns nullptr on OOM
 appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...);
 appd_status cuda_fail(appd_ctx* c, cudaError_t e, const char* where);
 
-#define APPD_CUDA(c, expr)                                   \
-  do {                                                       \
-    cudaError_t _e = (expr);                                 \
-    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
-  } while (0)
-
 #ifdef APPD_DEV_HOOKS
 #define APPD_TRACE_SYNC(c) appd::trace_launch(c, "SYNC " __FILE__ ":" APPD_STR(__LINE__))
+#define APPD_TRACE_OP(c) appd::trace_launch(c, "op " __FILE__ ":" APPD_STR(__LINE__))
 #else
 #define APPD_TRACE_SYNC(c) \
   do {                     \
   } while (0)
+#define APPD_TRACE_OP(c) \
+  do {                   \
+  } while (0)
 #endif
+#define APPD_CUDA(c, expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return appd::cuda_fail(c, _e, #expr); \
+    APPD_TRACE_OP(c);                                        \
+  } while (0)
+
 #define APPD_SYNC(c)                                 \
   do {                                               \
     APPD_TRACE_SYNC(c);                              \
@@ -354,6 +386,18 @@ appd_status launch_wide_compbest(appd_ctx* c, const u64* rowbest, const int* com
                                  const u64* compw, u64* compbest);
 appd_status wide_edges(appd_ctx* c, const u64* mstkeys, int64_t m, const float* X, int64_t d, int metric, int sense,
                        u64* key2, u64* key2_sorted, int32_t* eu, int32_t* ev, float* ew);
+// Small device -> host results: queue a copy of `bytes` (a multiple of 4) from device
+// memory into pinned_small; the queued copies run as ONE kernel writing the mapped host
+// words, launched by the next sync_stream (a 4-byte cudaMemcpyAsync costs ~5 us of stream
+// time each).  Invariant: the source must not change between publish() and that
+// synchronisation (every call site publishes a value its window no longer writes).
+appd_status publish(appd_ctx* c, void* host_dst, const void* dev_src, size_t bytes);
+appd_status publish_flush(appd_ctx* c);
+#define APPD_PUBLISH(c, dst, src, bytes)                        \
+  do {                                                          \
+    appd_status _p = appd::publish(c, dst, src, bytes);         \
+    if (_p != APPD_OK) return _p;                               \
+  } while (0)
 appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v);
 appd_status launch_iota(appd_ctx* c, int* p, int64_t count);
 appd_status launch_hook(appd_ctx* c, const u64* compbest, int64_t k, const int* comp, int shift, int* link);

@@ -784,6 +784,46 @@ appd_status launch_fill_u64(appd_ctx* c, u64* p, int64_t count, u64 v) {
   return APPD_OK;
 }
 
+// queued small results -> mapped pinned host words (one warp per entry)
+struct PubArgs {
+  const unsigned* src[16];
+  unsigned* dst[16];
+  int words[16];
+  int count;
+};
+__global__ void k_publish(const PubArgs a) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = w; e < a.count; e += blockDim.x >> 5)
+    for (int i = lane; i < a.words[e]; i += 32) a.dst[e][i] = a.src[e][i];
+}
+appd_status publish(appd_ctx* c, void* host_dst, const void* dev_src, size_t bytes) {
+  const int64_t off = (reinterpret_cast<unsigned*>(host_dst) - c->pinned_small);
+  if (!c->pinned_small_dev || off < 0 || off + (int64_t)(bytes / 4) > 64 || bytes % 4) {
+    APPD_CUDA(c, cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return APPD_OK;
+  }
+  if (c->npub == 16) {
+    appd_status s = publish_flush(c);
+    if (s) return s;
+  }
+  c->pub[c->npub++] = {dev_src, c->pinned_small_dev + off, (int)(bytes / 4)};
+  return APPD_OK;
+}
+appd_status publish_flush(appd_ctx* c) {
+  if (c->npub == 0) return APPD_OK;
+  PubArgs a;
+  for (int e = 0; e < c->npub; e++) {
+    a.src[e] = reinterpret_cast<const unsigned*>(c->pub[e].src);
+    a.dst[e] = c->pub[e].dst;
+    a.words[e] = c->pub[e].words;
+  }
+  a.count = c->npub;
+  c->npub = 0;
+  k_publish<<<1, 32 * 16, 0, c->stream>>>(a);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
+}
+
 __global__ void k_iota(int* p, int64_t count) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = (int)i;

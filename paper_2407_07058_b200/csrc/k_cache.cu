@@ -27,9 +27,14 @@
 //   k_rescan_select  a row with no eligible cached entry needs a re-scan only if its
 //                    K-th key is below its component's current best (else all of its
 //                    uncached edges are heavier than an edge the component already has).
+#include <vector>
+
+#include <cooperative_groups.h>
+
 #include "tc_common.cuh"
 
 namespace appd {
+namespace cg = cooperative_groups;
 
 // list entries: (32-column chunk << LIST_SHIFT) | row position (n <= 2^17, chunks < 2^12)
 constexpr int LIST_SHIFT = 17;
@@ -408,77 +413,234 @@ __global__ void k_chunk_runs(const unsigned* __restrict__ list, const unsigned* 
   }
 }
 
-// counting sort of the list by chunk (no host-side count): histogram, scatter
-// the listing is emitted chunk-major (runs of one chunk), so the lanes of a warp mostly
-// share a chunk: one atomic per distinct chunk in the warp instead of one per entry
-__global__ void k_chunk_hist(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
-                             unsigned* __restrict__ hist) {
-  const unsigned total = min(*count, cap);
-  const int lane = threadIdx.x & 31;
-  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < total; e0 += gridDim.x * blockDim.x) {
-    const unsigned e = e0 + lane;
-    const unsigned ch = e < total ? list[e] >> LIST_SHIFT : 0xFFFFFFFFu;
-    const unsigned peers = __match_any_sync(0xffffffffu, ch);
-    if (e < total && lane == __ffs(peers) - 1) atomicAdd(hist + ch, (unsigned)__popc(peers));
+// Counting sort of the list by chunk (no host-side count) in ONE cooperative launch (it
+// was seven kernels, scans and memsets: 60-100 us at C4): clear, histogram, a two-array
+// exclusive scan over chunk ranges per block (offsets and 128-row batch starts), item
+// table (item -> chunk, first entry, rows), scatter.  The listing is emitted chunk-major
+// (runs of one chunk), so the lanes of a warp mostly share a chunk: one atomic per
+// distinct chunk in the warp; the lanes of one chunk take consecutive slots in lane
+// order, so runs of rows listed together (one filter warp: consecutive rows, mostly one
+// component) stay together and in order.
+struct ListSortArgs {
+  const unsigned* list;
+  const unsigned* count;
+  unsigned cap;
+  int nch;
+  unsigned *hist, *offs, *cursor, *out, *run_lo, *run_nb, *item_start;
+  int4* items;
+  unsigned* blocksum;  // 2 per block
+  unsigned long long* marks;  // development builds (APPD_MARKS): %globaltimer per phase, CTA 0
+  int aggregate;              // the listing comes in chunk runs: warp-aggregated atomics
+  unsigned* cnt;              // (no runs) [nch][grid] per-CTA counts, then their offsets
+};
+__device__ __forceinline__ void ls_mark(const ListSortArgs& a, int i) {
+  if (a.marks && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.marks[i] = t;
   }
 }
-__global__ void k_chunk_scatter(const unsigned* __restrict__ list, const unsigned* __restrict__ count, unsigned cap,
-                                const unsigned* __restrict__ offs, unsigned* __restrict__ cursor,
-                                unsigned* __restrict__ out) {
-  // warp-aggregated per chunk: the lanes of one chunk take consecutive slots in lane
-  // order, so runs of rows listed together (one filter warp: consecutive rows, mostly one
-  // component) stay together and in order
-  const unsigned total = min(*count, cap);
-  const int lane = threadIdx.x & 31;
-  for (unsigned e0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < total; e0 += gridDim.x * blockDim.x) {
-    const unsigned e = e0 + lane;
-    const bool ok = e < total;
-    const unsigned v = ok ? list[e] : 0xFFFFFFFFu, ch = v >> LIST_SHIFT;
-    const unsigned peers = __match_any_sync(0xffffffffu, ch);
-    const int leader = __ffs(peers) - 1;
-    unsigned base = 0;
-    if (ok && lane == leader) base = atomicAdd(cursor + ch, (unsigned)__popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    if (ok) out[offs[ch] + base + __popc(peers & ((1u << lane) - 1u))] = v;
+__global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned total = min(*a.count, a.cap);
+  ls_mark(a, 0);
+  for (int64_t i = tid; i <= a.nch; i += nt) {
+    a.hist[i] = 0u;
+    a.cursor[i] = 0u;
   }
-}
-// runs from the histogram: run_lo = offsets, run_nb = 128-row batches
-__global__ void k_runs_from_hist(const unsigned* __restrict__ hist, const unsigned* __restrict__ offs, int nch,
-                                 unsigned* __restrict__ run_lo, unsigned* __restrict__ run_nb) {
-  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
-    run_lo[ch] = offs[ch];
-    run_nb[ch] = (hist[ch] + LE_RB - 1) / LE_RB;
+  grid.sync();
+  ls_mark(a, 1);
+  // no chunk runs (round 0: the listing is in row order, chunks at random): global atomics
+  // would serialise (~23 us for 640K entries), so every CTA counts its contiguous slice of
+  // the entries in shared memory and the [chunk][CTA] counts are scanned chunk-major
+  extern __shared__ unsigned sh[];  // [nch] (no-runs path)
+  const unsigned G = gridDim.x;
+  const unsigned e_lo = (unsigned)((uint64_t)total * blockIdx.x / G), e_hi = (unsigned)((uint64_t)total * (blockIdx.x + 1) / G);
+  if (a.aggregate) {
+    for (unsigned e0 = (unsigned)(tid & ~31ll); e0 < total; e0 += (unsigned)nt) {  // histogram
+      const unsigned e = e0 + lane;
+      const unsigned ch = e < total ? a.list[e] >> LIST_SHIFT : 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, ch);
+      if (e < total && lane == __ffs(peers) - 1) atomicAdd(a.hist + ch, (unsigned)__popc(peers));
+    }
+  } else {
+    for (int i = threadIdx.x; i < a.nch; i += blockDim.x) sh[i] = 0u;
+    __syncthreads();
+    for (unsigned e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) atomicAdd(sh + (a.list[e] >> LIST_SHIFT), 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.nch; i += blockDim.x) a.cnt[(int64_t)i * G + blockIdx.x] = sh[i];
   }
-}
-__global__ void k_item_table_h(const unsigned* __restrict__ run_lo, const unsigned* __restrict__ run_nb,
-                               const unsigned* __restrict__ item_start, const unsigned* __restrict__ hist, int nch,
-                               int4* __restrict__ table) {
-  for (int ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nch; ch += gridDim.x * blockDim.x) {
-    const unsigned lo = run_lo[ch], nb = run_nb[ch], base = item_start[ch], hi = lo + hist[ch];
-    for (unsigned b = 0; b < nb; b++) {
-      const unsigned b0 = lo + b * LE_RB;
-      table[base + b] = make_int4(ch, (int)b0, (int)min((unsigned)LE_RB, hi - b0), 0);
+  grid.sync();
+  ls_mark(a, 2);
+  if (!a.aggregate) {  // chunk totals, and each CTA's offset inside its chunk (a warp per chunk)
+    for (int i = (int)(tid >> 5); i < a.nch; i += (int)(nt >> 5)) {
+      unsigned carry = 0u, pre[8];  // the loads of up to 8 x 32 CTAs first, all in flight
+#pragma unroll
+      for (int u = 0; u < 8; u++) pre[u] = (u * 32u + lane < G) ? a.cnt[(int64_t)i * G + u * 32 + lane] : 0u;
+      auto step = [&](unsigned v, unsigned j) {  // exclusive offsets of 32 CTAs, running carry
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (j < G) a.cnt[(int64_t)i * G + j] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      };
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (u * 32u < G) step(pre[u], u * 32u + lane);
+      for (unsigned j0 = 256; j0 < G; j0 += 32) step(j0 + lane < G ? a.cnt[(int64_t)i * G + j0 + lane] : 0u, j0 + lane);
+      if (lane == 0) a.hist[i] = carry;
+    }
+    grid.sync();
+  }
+  // block b scans chunks [lo, hi): entries (offsets) and 128-row batches (item starts)
+  __shared__ unsigned ws1[32], ws2[32];
+  __shared__ unsigned carry1, carry2;
+  const int Sg = (a.nch + gridDim.x - 1) / gridDim.x;
+  const int lo = min(a.nch, (int)blockIdx.x * Sg), hi = min(a.nch, lo + Sg);
+  if (threadIdx.x == 0) carry1 = carry2 = 0u;
+  __syncthreads();
+  for (int base = lo; base < hi; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const unsigned f1 = i < hi ? a.hist[i] : 0u, f2 = (f1 + LE_RB - 1) / LE_RB;
+    unsigned x1 = f1, x2 = f2;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y1 = __shfl_up_sync(0xffffffffu, x1, o), y2 = __shfl_up_sync(0xffffffffu, x2, o);
+      if (lane >= o) { x1 += y1; x2 += y2; }
+    }
+    if (lane == 31) { ws1[warp] = x1; ws2[warp] = x2; }
+    __syncthreads();
+    if (warp == 0) {
+      unsigned w1 = lane < (int)(blockDim.x >> 5) ? ws1[lane] : 0u, w2 = lane < (int)(blockDim.x >> 5) ? ws2[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y1 = __shfl_up_sync(0xffffffffu, w1, o), y2 = __shfl_up_sync(0xffffffffu, w2, o);
+        if (lane >= o) { w1 += y1; w2 += y2; }
+      }
+      ws1[lane] = w1;
+      ws2[lane] = w2;
+    }
+    __syncthreads();
+    if (i < hi) {
+      a.offs[i] = carry1 + (warp ? ws1[warp - 1] : 0u) + x1 - f1;
+      a.item_start[i] = carry2 + (warp ? ws2[warp - 1] : 0u) + x2 - f2;
+      a.run_nb[i] = f2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry1 += ws1[(blockDim.x >> 5) - 1];
+      carry2 += ws2[(blockDim.x >> 5) - 1];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.blocksum[2 * blockIdx.x] = carry1;
+    a.blocksum[2 * blockIdx.x + 1] = carry2;
+  }
+  grid.sync();
+  ls_mark(a, 3);
+  // the sums of the earlier blocks' totals (a block-wide reduction, not a serial loop)
+  if (warp == 0) {
+    unsigned s1 = 0u, s2 = 0u;
+    for (int b = lane; b < (int)blockIdx.x; b += 32) {
+      s1 += a.blocksum[2 * b];
+      s2 += a.blocksum[2 * b + 1];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      ws1[0] = s1;
+      ws2[0] = s2;
     }
   }
+  __syncthreads();
+  const unsigned off1 = ws1[0], off2 = ws2[0];
+  for (int i = lo + warp; i < hi; i += blockDim.x >> 5) {  // a warp per chunk: its item table
+    const unsigned o1 = a.offs[i] + off1, o2 = a.item_start[i] + off2, h = a.hist[i], nb = a.run_nb[i];
+    __syncwarp();
+    if (lane == 0) {
+      a.offs[i] = o1;
+      a.item_start[i] = o2;
+      a.run_lo[i] = o1;
+    }
+    for (unsigned b = lane; b < nb; b += 32) {
+      const unsigned b0 = o1 + b * LE_RB;
+      a.items[o2 + b] = make_int4(i, (int)b0, (int)min((unsigned)LE_RB, o1 + h - b0), 0);
+    }
+  }
+  grid.sync();
+  ls_mark(a, 4);
+  if (a.aggregate) {
+    for (unsigned e0 = (unsigned)(tid & ~31ll); e0 < total; e0 += (unsigned)nt) {  // scatter
+      const unsigned e = e0 + lane;
+      const bool ok = e < total;
+      const unsigned v = ok ? a.list[e] : 0xFFFFFFFFu, ch = v >> LIST_SHIFT;
+      const unsigned peers = __match_any_sync(0xffffffffu, ch);
+      const int leader = __ffs(peers) - 1;
+      unsigned b = 0;
+      if (ok && lane == leader) b = atomicAdd(a.cursor + ch, (unsigned)__popc(peers));
+      b = __shfl_sync(peers, b, leader);
+      if (ok) a.out[a.offs[ch] + b + __popc(peers & ((1u << lane) - 1u))] = v;
+    }
+  } else {  // this CTA's slice again, cursors in shared memory from the scanned counts
+    for (int i = threadIdx.x; i < a.nch; i += blockDim.x) sh[i] = a.offs[i] + a.cnt[(int64_t)i * G + blockIdx.x];
+    __syncthreads();
+    for (unsigned e = e_lo + threadIdx.x; e < e_hi; e += blockDim.x) {
+      const unsigned v = a.list[e];
+      a.out[atomicAdd(sh + (v >> LIST_SHIFT), 1u)] = v;
+    }
+  }
+  ls_mark(a, 5);
 }
 
 appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsigned* count, unsigned cap, int nch,
                                  unsigned* hist, unsigned* offs, unsigned* cursor, unsigned* out, unsigned* run_lo,
-                                 unsigned* run_nb, unsigned* item_start, int4* items) {
-  const int g = c->sm_count * 8;
-  APPD_CUDA(c, cudaMemsetAsync(hist, 0, sizeof(unsigned) * (nch + 1), c->stream));
-  APPD_CUDA(c, cudaMemsetAsync(cursor, 0, sizeof(unsigned) * (nch + 1), c->stream));
-  k_chunk_hist<<<g, 256, 0, c->stream>>>(list, count, cap, hist);
+                                 unsigned* run_nb, unsigned* item_start, int4* items, bool aggregate) {
+  unsigned* blocksum = (unsigned*)ws(c, S_SCAN, sizeof(unsigned) * 2 * (c->sm_count + 1) + 64);
+  if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list sort workspace");
+  unsigned* cnt = nullptr;
+  if (!aggregate) {
+    cnt = (unsigned*)ws(c, S_LIST_CNT, sizeof(unsigned) * (size_t)nch * c->sm_count + 64);
+    if (!cnt) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list sort counts");
+  }
+  ListSortArgs a{list, count, cap, nch, hist, offs, cursor, out, run_lo, run_nb, item_start, items, blocksum, nullptr,
+                 aggregate ? 1 : 0, cnt};
+  const size_t smem = aggregate ? 0 : sizeof(unsigned) * nch;
+  if (smem > 64 * 1024) return fail(c, APPD_ERR_UNSUPPORTED, "list sort: %d chunks", nch);
+  static std::atomic<unsigned long long> attr{0};
+  if (needs_setup(attr, c)) {
+    cudaFuncSetAttribute(k_list_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    setup_done(attr, c);
+  }
+  static const bool marks = dev_env("APPD_MARKS") != nullptr;
+  if (marks) a.marks = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 64));
+  void* args[] = {&a};
+  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_list_sort, c->sm_count, 1024, args, smem, c->stream));
   APPD_LAUNCHED(c);
-  appd_status s = exclusive_scan_i32(c, (const int*)hist, (int*)offs, nch + 1);
-  if (s) return s;
-  k_chunk_scatter<<<g, 256, 0, c->stream>>>(list, count, cap, offs, cursor, out);
-  APPD_LAUNCHED(c);
-  k_runs_from_hist<<<(nch + 255) / 256, 256, 0, c->stream>>>(hist, offs, nch, run_lo, run_nb);
-  APPD_LAUNCHED(c);
-  if ((s = exclusive_scan_i32(c, (const int*)run_nb, (int*)item_start, nch))) return s;
-  k_item_table_h<<<(nch + 255) / 256, 256, 0, c->stream>>>(run_lo, run_nb, item_start, hist, nch, items);
-  APPD_LAUNCHED(c);
+  if (marks && a.marks) {
+    unsigned long long h[6];
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h, a.marks, sizeof h, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[list_sort] clear %.1f us, hist %.1f, scan %.1f, items %.1f, scatter %.1f\n", (h[1] - h[0]) * 1e-3,
+            (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3, (h[4] - h[3]) * 1e-3, (h[5] - h[4]) * 1e-3);
+    std::vector<unsigned> hh(nch);
+    cudaMemcpy(hh.data(), hist, sizeof(unsigned) * nch, cudaMemcpyDeviceToHost);
+    unsigned mx = 0, tot = 0, big = 0;
+    for (unsigned v : hh) {
+      mx = std::max(mx, v);
+      tot += v;
+      big += v > 4096;
+    }
+    fprintf(stderr, "[list_sort] entries %u, chunks %d, max per chunk %u, chunks over 4096: %u\n", tot, nch, mx, big);
+  }
   return APPD_OK;
 }
 
@@ -1257,10 +1419,12 @@ __device__ __forceinline__ void warp_argmin_u64(u64& key, int& idx) {
   idx = mi;
 }
 
-__global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
-                                                       unsigned* __restrict__ T) {
+// (1024 threads: the k x k staging is a few loads per thread, all in flight)
+__global__ void __launch_bounds__(1024) k_cm_thresholds(const unsigned* __restrict__ CUB, int k,
+                                                        unsigned* __restrict__ T) {
   extern __shared__ float symb[];   // [k][k] symmetric bounds, then [k][k] path maxima
   float* pm = symb + k * k;
+#pragma unroll 4
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
     const int a = e / k, b = e % k;
     symb[e] = fminf(__uint_as_float(CUB[(int64_t)a * k + b]), __uint_as_float(CUB[(int64_t)b * k + a]));
@@ -1331,12 +1495,13 @@ __global__ void __launch_bounds__(128) k_cm_thresholds(const unsigned* __restric
 // over component representatives (valid indices, largest key) so that every later
 // kernel stays in bounds, and status records why (1 overflow, 2 disconnected): the host
 // re-solves without the component matrix, or reports the inconsistency.
-__global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
-                                                 int* __restrict__ counters, const unsigned* __restrict__ list_count,
-                                                 unsigned list_cap, const int* __restrict__ cstart,
-                                                 const int* __restrict__ perm, unsigned* __restrict__ status) {
+__global__ void __launch_bounds__(1024) k_cm_prim(const u64* __restrict__ WCM, int k, u64* __restrict__ mstkeys,
+                                                  int* __restrict__ counters, const unsigned* __restrict__ list_count,
+                                                  unsigned list_cap, const int* __restrict__ cstart,
+                                                  const int* __restrict__ perm, unsigned* __restrict__ status) {
   extern __shared__ u64 wsym[];  // [k][k] symmetric minima
   const int lane = threadIdx.x & 31;
+#pragma unroll 4
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {  // all threads stage (latency)
     const int a = e / k, b = e % k;
     const u64 x = WCM[(int64_t)a * k + b], y = WCM[(int64_t)b * k + a];
@@ -1400,7 +1565,7 @@ __global__ void __launch_bounds__(256) k_cm_prim(const u64* __restrict__ WCM, in
 appd_status launch_cm_thresholds(appd_ctx* c, const unsigned* CUB, int k, unsigned* T) {
   const size_t smem = sizeof(float) * 2 * k * k;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_thresholds, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cm_thresholds<<<1, 128, smem, c->stream>>>(CUB, k, T);
+  k_cm_thresholds<<<1, 1024, smem, c->stream>>>(CUB, k, T);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -1409,7 +1574,7 @@ appd_status launch_cm_prim(appd_ctx* c, const u64* WCM, int k, u64* mstkeys, int
                            unsigned* status) {
   const size_t smem = sizeof(u64) * k * k;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_cm_prim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cm_prim<<<1, 256, smem, c->stream>>>(WCM, k, mstkeys, counters, list_count, list_cap, cstart, perm, status);
+  k_cm_prim<<<1, 1024, smem, c->stream>>>(WCM, k, mstkeys, counters, list_count, list_cap, cstart, perm, status);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

@@ -20,11 +20,15 @@
 // Eligibility (j in another component) is cheap because the points are sorted by
 // component every round: a row's ineligible columns form one contiguous range.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+
+#include <cooperative_groups.h>
 
 #include "tc_common.cuh"
 
 namespace appd {
+namespace cg = cooperative_groups;
 
 // per-row chunk buffer of the fused top-K scan (running threshold)
 
@@ -36,59 +40,79 @@ namespace appd {
 // column sums in fp64, deterministic order: block b sums rows [b R, (b+1) R); thread
 // slots (row lane l, dim k) with RL = 256 / d lanes (>= 1) sum rows l, l + RL, ..., then
 // the lanes are added in order
-__global__ void k_center_partial(const float* __restrict__ X, int64_t n, int d, int rows_per_block,
-                                 double* __restrict__ part) {
-  __shared__ double red[256];
+// (256 threads; block index b)
+__device__ __forceinline__ void center_partial_block(const float* __restrict__ X, int64_t n, int d, int rows_per_block,
+                                                     int64_t b, double* __restrict__ part, double* red) {
   const int RL = d >= 256 ? 1 : 256 / d;
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r0 = b * rows_per_block;
   const int64_t r1 = min(n, r0 + rows_per_block);
   for (int k0 = 0; k0 < d; k0 += 256) {  // d > 256: dims in slices of 256
     const int slot = threadIdx.x, l = slot / min(d, 256), k = k0 + slot % min(d, 256);
     double s = 0.0;
     if (l < RL && k < d)
+#pragma unroll 8
       for (int64_t r = r0 + l; r < r1; r += RL) s += (double)__ldg(X + r * d + k);
     red[threadIdx.x] = s;
     __syncthreads();
     if (threadIdx.x < min(d, 256) && k0 + (int)threadIdx.x < d) {
       double t = 0.0;
       for (int q = 0; q < RL; q++) t += red[q * min(d, 256) + threadIdx.x];
-      part[(int64_t)blockIdx.x * d + k0 + threadIdx.x] = t;
+      part[b * d + k0 + threadIdx.x] = t;
     }
     __syncthreads();
   }
 }
+__global__ void k_center_partial(const float* __restrict__ X, int64_t n, int d, int rows_per_block,
+                                 double* __restrict__ part) {
+  __shared__ double red[256];
+  center_partial_block(X, n, d, rows_per_block, blockIdx.x, part, red);
+}
 // one warp per dimension: lanes sum partials b = lane, lane + 32, ..., then a fixed tree
-__global__ void k_center_final(const double* __restrict__ part, int blocks, int64_t n, int d, float* __restrict__ c) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= d) return;
+__device__ __forceinline__ void center_final_dim(const double* __restrict__ part, int blocks, int64_t n, int d, int w,
+                                                 int lane, float* __restrict__ c) {
   double s = 0.0;
+#pragma unroll 8
   for (int b = lane; b < blocks; b += 32) s += part[(int64_t)b * d + w];
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) c[w] = (float)(s / (double)n);
 }
+__global__ void k_center_final(const double* __restrict__ part, int blocks, int64_t n, int d, float* __restrict__ c) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w < d) center_final_dim(part, blocks, n, d, w, lane, c);
+}
 // max |x_i - c| (fp32; sets the scale only): one thread per point, block maximum, one atomic
-__global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ c,
-                         unsigned* __restrict__ out) {
-  float best = 0.0f;
-  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.0f;
-    if (vec) {
-      const float4* x4 = reinterpret_cast<const float4*>(X + i * d);
-      for (int k = 0; k < d; k += 4) {
-        const float4 v = __ldg(x4 + k / 4);
-        const float t0 = v.x - c[k], t1 = v.y - c[k + 1], t2 = v.z - c[k + 2], t3 = v.w - c[k + 3];
-        s += t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
+// |x_i - c|^2 in fp32; bad: set to the element index of the first non-finite coordinate
+// when one is found (validation folded into the cooperative preparation)
+__device__ __forceinline__ float point_len2(const float* __restrict__ X, int64_t i, int d, const float* __restrict__ c,
+                                            bool vec, u64* bad = nullptr) {
+  float s = 0.0f;
+  if (vec) {
+    const float4* x4 = reinterpret_cast<const float4*>(X + i * d);
+#pragma unroll 4
+    for (int k = 0; k < d; k += 4) {
+      const float4 v = __ldg(x4 + k / 4);
+      if (bad && *bad == KEY_NONE) {
+        if (!isfinite(v.x)) *bad = (u64)(i * d + k);
+        else if (!isfinite(v.y)) *bad = (u64)(i * d + k + 1);
+        else if (!isfinite(v.z)) *bad = (u64)(i * d + k + 2);
+        else if (!isfinite(v.w)) *bad = (u64)(i * d + k + 3);
       }
-    } else {
-      for (int k = 0; k < d; k++) {
-        const float t = X[i * d + k] - c[k];
-        s += t * t;
-      }
+      const float t0 = v.x - c[k], t1 = v.y - c[k + 1], t2 = v.z - c[k + 2], t3 = v.w - c[k + 3];
+      s += t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
     }
-    best = fmaxf(best, s);
+  } else {
+    for (int k = 0; k < d; k++) {
+      const float x = X[i * d + k];
+      if (bad && *bad == KEY_NONE && !isfinite(x)) *bad = (u64)(i * d + k);
+      const float t = x - c[k];
+      s += t * t;
+    }
   }
+  return s;
+}
+// block maximum of best (non-negative) -> one atomicMax on the float bits of sqrt
+__device__ __forceinline__ void block_max_sqrt(float best, unsigned* __restrict__ out) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
   __shared__ float wb[32];
@@ -99,6 +123,15 @@ __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const fl
     for (int t = 0; t < (int)(blockDim.x >> 5); t++) m = fmaxf(m, wb[t]);
     atomicMax(out, __float_as_uint(sqrtf(m)));
   }
+  __syncthreads();
+}
+__global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const float* __restrict__ c,
+                         unsigned* __restrict__ out) {
+  float best = 0.0f;
+  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    best = fmaxf(best, point_len2(X, i, d, c, vec));
+  block_max_sqrt(best, out);
 }
 
 // pack point perm[p] into the row (YA) and column (YB) operand granules:
@@ -108,20 +141,21 @@ __global__ void k_maxlen(const float* __restrict__ X, int64_t n, int d, const fl
 // A: 1, 1, 0..; B: hi(-|y^|^2/2), lo(-|y^|^2/2), 0..].  Padding points: A = 0,
 // B augment = -65504 (never a maximum).  One thread per point, one 16-byte store per
 // 8 coordinates (lanes = consecutive points: 128-byte runs per core matrix).
-__global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, int K, const int* __restrict__ perm,
-                       const float* __restrict__ c, const TcScale* __restrict__ sc, int64_t npad, __half* __restrict__ YA,
-                       __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
-                       float* __restrict__ err, unsigned* __restrict__ maxerr) {
-  float emax = 0.0f;
-  const float scale = sc->scale;
-  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npad; p += (int64_t)gridDim.x * blockDim.x) {
+// one point (permuted position p; i = perm[p], or p without a permutation); xt != nullptr:
+// also the transposed fp32 copy xt[k][p] (consecutive threads: consecutive p, coalesced);
+// returns the point's error norm E_p
+__device__ __forceinline__ float pack_point(const float* __restrict__ X, int64_t n, int d, int dk, int K,
+                                            const int* __restrict__ perm, const float* __restrict__ c, float scale,
+                                            bool vec, int64_t npad, int64_t p, __half* __restrict__ YA,
+                                            __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
+                                            float* __restrict__ err, float* __restrict__ xt) {
+  {
     const int64_t gidx = p / 128;
     const int pl = (int)(p % 128), g = pl / 8, r = pl % 8;
     uint4* ga = reinterpret_cast<uint4*>(YA + gidx * 128 * K + (int64_t)g * (K / 8) * 64 + r * 8);
     uint4* gb = reinterpret_cast<uint4*>(YB + gidx * 128 * K + (int64_t)g * (K / 8) * 64 + r * 8);
     const bool real = p < n;
-    const int64_t i = real ? perm[p] : 0;
+    const int64_t i = real ? (perm ? perm[p] : p) : 0;
     const float* xi = X + i * d;
     float s = 0.0f;
     // E^2 = |y^ - s (x - c)|^2: per coordinate e = (y^ - y) - s dt with y = s fl(x - c) and
@@ -129,6 +163,7 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
     // Only a - s dt and the squares / sum round (relative (d + 4) 2^-24 over the sum,
     // covered by the margin applied below); round-up FMAs keep the sum an upper bound.
     float e2 = 0.0f;
+#pragma unroll 2
     for (int k8 = 0; k8 < dk; k8 += 8) {
       float xv[8];
       if (real && vec && k8 + 8 <= d) {
@@ -140,6 +175,10 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
 #pragma unroll
         for (int u = 0; u < 8; u++) xv[u] = (real && k8 + u < d) ? __ldg(xi + k8 + u) : 0.0f;
       }
+      if (xt)
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (k8 + u < d) xt[(int64_t)(k8 + u) * npad + p] = xv[u];
       __half hv[8];
 #pragma unroll
       for (int u = 0; u < 8; u++) {
@@ -189,8 +228,19 @@ __global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, in
     // rounded up, with a relative margin for the rounded subtraction and squares
     const float E = real ? __fsqrt_ru(__fmul_ru(e2, 1.0f + (float)(d + 8) * 0x1p-23f)) + 1e-30f : 0.0f;
     err[p] = E;
-    emax = fmaxf(emax, E);
+    return E;
   }
+}
+
+__global__ void k_pack(const float* __restrict__ X, int64_t n, int d, int dk, int K, const int* __restrict__ perm,
+                       const float* __restrict__ c, const TcScale* __restrict__ sc, int64_t npad, __half* __restrict__ YA,
+                       __half* __restrict__ YB, float* __restrict__ nrm, float* __restrict__ len,
+                       float* __restrict__ err, unsigned* __restrict__ maxerr) {
+  float emax = 0.0f;
+  const float scale = sc->scale;
+  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npad; p += (int64_t)gridDim.x * blockDim.x)
+    emax = fmaxf(emax, pack_point(X, n, d, dk, K, perm, c, scale, vec, npad, p, YA, YB, nrm, len, err, nullptr));
   // one atomic per block for the global maximum (a single address: atomics serialise)
 #pragma unroll
   for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
@@ -477,8 +527,8 @@ static ErrModel error_model(const TcState* st) {
 
 // scale = 2^e with scale * max|x - c| in [2^6.5, 2^7.5): |y^|^2 < 2^15, fp16 range safe;
 // fp16 rounding can lift |y^| by 2^-11 relative (plus subnormal slack): maxlen margin
-__global__ void k_tc_scale(const unsigned* __restrict__ maxlen_bits, TcScale* __restrict__ out) {
-  const float ml = __uint_as_float(*maxlen_bits);
+__device__ __forceinline__ TcScale tc_scale_of(unsigned maxlen_bits) {
+  const float ml = __uint_as_float(maxlen_bits);
   TcScale r;
   r.ok = ml < INFINITY ? 1 : 0;
   int e = 0;
@@ -490,38 +540,411 @@ __global__ void k_tc_scale(const unsigned* __restrict__ maxlen_bits, TcScale* __
   r.maxlen = r.ok ? (float)((double)ml * r.scale * (1.0 + ldexp(1.0, -10)) + 1e-6) : 0.0f;
   r.s2 = (double)r.scale * (double)r.scale;
   r.pad = 0;
-  *out = r;
+  return r;
+}
+__global__ void k_tc_scale(const unsigned* __restrict__ maxlen_bits, TcScale* __restrict__ out) {
+  *out = tc_scale_of(*maxlen_bits);
 }
 
-appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st) {
+// ---------------------------------------------------------------------------
+// The whole preparation of the first round in ONE cooperative launch (it was ten kernels
+// and memsets, ~100 us of a C4 solve): phase 1 per-block partial column sums (the fixed
+// 64-row partition of k_center_partial: the same centre bit for bit) and the caller's
+// buffer initialisations; phase 2 the centre; phase 3 max |x - c| (+ the input
+// validation); phase 4 the scale, the packed operands of round 0 (identity order), the
+// fp32 transpose for the exact kernels and the per-segment maxima.  Grid-wide barriers
+// separate the phases.
+// ---------------------------------------------------------------------------
+struct PrepArgs {
+  const float* X;
+  int64_t n, npad;
+  int d, dk, K, rpb, blocks;
+  double* part;
+  float* center;
+  unsigned* maxlen;
+  TcScale* dscale;
+  __half *YA, *YB;
+  float *nrm, *len, *err;
+  unsigned* maxerr;
+  float* xt;
+  unsigned *seg_maxlen, *seg_maxerr;
+  u64* bad;
+  unsigned long long* dbg;  // development builds: %globaltimer after each phase (CTA 0)
+  InitList init;
+};
+__device__ __forceinline__ void prep_mark(const PrepArgs& a, int i) {
+  if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[i] = t;
+  }
+}
+
+__device__ __forceinline__ void run_init(const InitList& L, int64_t tid, int64_t nt) {
+  for (int t = 0; t < L.count; t++) {
+    const InitTask& T = L.t[t];
+    if (T.kind == 0) {
+      unsigned* p = reinterpret_cast<unsigned*>(T.p);
+      for (int64_t i = tid; i < T.count; i += nt) p[i] = (unsigned)T.value;
+    } else if (T.kind == 1) {
+      u64* p = reinterpret_cast<u64*>(T.p);
+      for (int64_t i = tid; i < T.count; i += nt) p[i] = T.value;
+    } else {
+      int* p = reinterpret_cast<int*>(T.p);
+      for (int64_t i = tid; i < T.count; i += nt) p[i] = (int)i;
+    }
+  }
+}
+
+__global__ void k_init(const InitList L) {
+  run_init(L, blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
+// phase 4 body: one tile of 32 * sets points (identity order), GW warps per 32 points,
+// warp w covers the 8-coordinate groups g = w % GW, w % GW + GW, ... of point lane; the
+// per-group partial norms and error sums meet in shared memory (norm: fp32, any order is
+// inside the error model's d 2^-24 allowance; error sum: rounded up, so an upper bound)
+__device__ __forceinline__ float pack_tile(const PrepArgs& a, float scale, bool vec, int64_t p0, int G, int GW,
+                                           int sets, float (*s_part)[32], float (*e_part)[32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int set = w / GW, gw = w % GW;
+  const int64_t p = p0 + set * 32 + lane;
+  const bool act = set < sets;
+  const bool real = act && p < a.n;
+  const int K = a.K, d = a.d;
+  float s = 0.0f, e2 = 0.0f;
+  if (act) {
+    const int64_t gidx = p / 128;
+    const int pl = (int)(p % 128), g8 = pl / 8, r = pl % 8;
+    uint4* ga = reinterpret_cast<uint4*>(a.YA + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
+    uint4* gb = reinterpret_cast<uint4*>(a.YB + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
+    const float* xi = a.X + (real ? p : 0) * d;
+    for (int g = gw; g < G; g += GW) {
+      const int k8 = 8 * g;
+      float xv[8];
+      if (real && vec && k8 + 8 <= d) {
+        const float4 u0 = __ldg(reinterpret_cast<const float4*>(xi + k8));
+        const float4 u1 = __ldg(reinterpret_cast<const float4*>(xi + k8 + 4));
+        xv[0] = u0.x; xv[1] = u0.y; xv[2] = u0.z; xv[3] = u0.w;
+        xv[4] = u1.x; xv[5] = u1.y; xv[6] = u1.z; xv[7] = u1.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; u++) xv[u] = (real && k8 + u < d) ? __ldg(xi + k8 + u) : 0.0f;
+      }
+      if (a.xt)
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (k8 + u < d) a.xt[(int64_t)(k8 + u) * a.npad + p] = xv[u];
+      __half hv[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int k = k8 + u;
+        hv[u] = __float2half_rn(0.0f);
+        if (real && k < d) {  // as pack_point: TwoSum error of the centring, exact fp16 residual
+          const float xk = xv[u], ck = a.center[k];
+          const float t = __fsub_rn(xk, ck);
+          const float bb = __fsub_rn(t, xk);
+          const float dt = __fadd_rn(__fsub_rn(xk, __fsub_rn(t, bb)), __fsub_rn(-ck, bb));
+          const float y = scale * t;
+          hv[u] = __float2half_rn(y);
+          const float ek = __fsub_rn(__fsub_rn(__half2float(hv[u]), y), scale * dt);
+          e2 = __fmaf_ru(ek, ek, e2);
+        }
+        const float hf = __half2float(hv[u]);
+        s = fmaf(hf, hf, s);
+      }
+      uint4 pk;
+      pk.x = (uint32_t)__half_as_ushort(hv[0]) | ((uint32_t)__half_as_ushort(hv[1]) << 16);
+      pk.y = (uint32_t)__half_as_ushort(hv[2]) | ((uint32_t)__half_as_ushort(hv[3]) << 16);
+      pk.z = (uint32_t)__half_as_ushort(hv[4]) | ((uint32_t)__half_as_ushort(hv[5]) << 16);
+      pk.w = (uint32_t)__half_as_ushort(hv[6]) | ((uint32_t)__half_as_ushort(hv[7]) << 16);
+      ga[g * 8] = pk;
+      gb[g * 8] = pk;
+    }
+    s_part[w][lane] = s;
+    e_part[w][lane] = e2;
+  }
+  __syncthreads();
+  float E = 0.0f;
+  if (act && gw == 0) {  // the set's first warp: totals, augment columns, per-point outputs
+    s = 0.0f;
+    e2 = 0.0f;
+    for (int j = 0; j < GW; j++) {
+      s += s_part[set * GW + j][lane];
+      e2 = __fadd_ru(e2, e_part[set * GW + j][lane]);
+    }
+    const int64_t gidx = p / 128;
+    const int pl = (int)(p % 128), g8 = pl / 8, r = pl % 8;
+    uint4* ga = reinterpret_cast<uint4*>(a.YA + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
+    uint4* gb = reinterpret_cast<uint4*>(a.YB + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
+    for (int k8 = a.dk; k8 < K; k8 += 8) {
+      uint4 ua = make_uint4(0u, 0u, 0u, 0u), ub = make_uint4(0u, 0u, 0u, 0u);
+      if (k8 == a.dk) {
+        if (real) {
+          const uint32_t one = __half_as_ushort(__float2half_rn(1.0f));
+          ua.x = one | (one << 16);
+          const float hn = -0.5f * s;
+          const __half hi = __float2half_rn(hn);
+          const __half lo = __float2half_rn(hn - __half2float(hi));
+          ub.x = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+        } else {
+          ub.x = (uint32_t)__half_as_ushort(__float2half_rn(-65504.0f));
+        }
+      }
+      ga[(k8 / 8) * 8] = ua;
+      gb[(k8 / 8) * 8] = ub;
+    }
+    const float len = real ? sqrtf(s) : 0.0f;
+    a.nrm[p] = real ? s : 0.0f;
+    a.len[p] = len;
+    E = real ? __fsqrt_ru(__fmul_ru(e2, 1.0f + (float)(d + 8) * 0x1p-23f)) + 1e-30f : 0.0f;
+    a.err[p] = E;
+    float ml = len, me = E;  // the warp's 32 points lie in one TC_TMG segment
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ml = fmaxf(ml, __shfl_xor_sync(0xffffffffu, ml, o));
+      me = fmaxf(me, __shfl_xor_sync(0xffffffffu, me, o));
+    }
+    if (lane == 0) {
+      atomicMax(a.seg_maxlen + p / TC_TMG, __float_as_uint(ml));
+      atomicMax(a.seg_maxerr + p / TC_TMG, __float_as_uint(me));
+    }
+  }
+  __syncthreads();  // s_part / e_part are reused by the next tile
+  return E;
+}
+
+__global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[256];
+  __shared__ float s_part[8][32], e_part[8][32];
+  __shared__ float cs[1024];
+  const int64_t tid = blockIdx.x * 256ll + threadIdx.x, nt = gridDim.x * 256ll;
+  const int lane = threadIdx.x & 31;
+  const int d = a.d;
+  const bool vec = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  prep_mark(a, 0);
+  // phase 1: fp64 column sums of fixed 16-row blocks, one warp per block (lanes = columns)
+  for (int64_t b = tid >> 5; b < a.blocks; b += nt >> 5) {
+    const int64_t r0 = b * a.rpb, r1 = min(a.n, r0 + a.rpb);
+    for (int k0 = 0; k0 < d; k0 += 64) {
+      const int ka = k0 + lane, kb = k0 + 32 + lane;
+      double sa = 0.0, sb = 0.0;
+#pragma unroll 8
+      for (int64_t r = r0; r < r1; r++) {
+        if (ka < d) sa += (double)__ldg(a.X + r * d + ka);
+        if (kb < d) sb += (double)__ldg(a.X + r * d + kb);
+      }
+      if (ka < d) a.part[(int64_t)ka * a.blocks + b] = sa;  // column-major: phase 2 reads runs
+      if (kb < d) a.part[(int64_t)kb * a.blocks + b] = sb;
+    }
+  }
+  run_init(a.init, tid, nt);
+  if (tid == 0) {
+    *a.maxlen = 0u;
+    *a.maxerr = 0u;
+    if (a.bad) a.bad[0] = a.bad[1] = a.bad[2] = KEY_NONE;
+  }
+  prep_mark(a, 1);
+  grid.sync();
+  prep_mark(a, 2);
+  // phase 2: the centre, one CTA per column (a fixed tree: deterministic)
+  for (int k = blockIdx.x; k < d; k += gridDim.x) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int b = threadIdx.x; b < a.blocks; b += 256) s += a.part[(int64_t)k * a.blocks + b];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = 128; h; h >>= 1) {
+      if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.center[k] = (float)(red[0] / (double)a.n);
+    __syncthreads();
+  }
+  grid.sync();
+  prep_mark(a, 3);
+  const bool cs_ok = d <= 1024;  // the centre staged in shared memory
+  if (cs_ok) {
+    for (int k = threadIdx.x; k < d; k += 256) cs[k] = a.center[k];
+    __syncthreads();
+  }
+  const float* cen = cs_ok ? cs : a.center;
+  // phase 3: max |x - c| (fp32, sets the scale; the error model carries a 2^-10 margin)
+  // and the validation: four threads per point (float4 k-steps q, q + 4, ...)
+  {
+    float best = 0.0f;
+    u64 badi = KEY_NONE;
+    const int q = (int)(tid & 3);
+    for (int64_t i = tid >> 2; i < ((a.n + 7) & ~7ll); i += nt >> 2) {  // quads stay converged
+      float sum = 0.0f;
+      if (i < a.n) {
+        if (vec) {
+          const float4* x4 = reinterpret_cast<const float4*>(a.X + i * d);
+#pragma unroll 4
+          for (int k4 = q; k4 < d / 4; k4 += 4) {
+            const float4 v = __ldg(x4 + k4);
+            const int k = 4 * k4;
+            if (a.bad && badi == KEY_NONE) {
+              if (!isfinite(v.x)) badi = (u64)(i * d + k);
+              else if (!isfinite(v.y)) badi = (u64)(i * d + k + 1);
+              else if (!isfinite(v.z)) badi = (u64)(i * d + k + 2);
+              else if (!isfinite(v.w)) badi = (u64)(i * d + k + 3);
+            }
+            const float t0 = v.x - cen[k], t1 = v.y - cen[k + 1], t2 = v.z - cen[k + 2], t3 = v.w - cen[k + 3];
+            sum += t0 * t0 + t1 * t1 + t2 * t2 + t3 * t3;
+          }
+        } else {
+          for (int k = q; k < d; k += 4) {
+            const float x = a.X[i * d + k];
+            if (a.bad && badi == KEY_NONE && !isfinite(x)) badi = (u64)(i * d + k);
+            const float t = x - cen[k];
+            sum += t * t;
+          }
+        }
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      best = fmaxf(best, sum);
+    }
+    block_max_sqrt(best, a.maxlen);
+    if (badi != KEY_NONE) atomicMin(a.bad, badi);  // the smallest element index over all threads
+  }
+  grid.sync();
+  prep_mark(a, 4);
+  // phase 4: scale, packed operands, transpose, per-segment maxima
+  const TcScale sc = tc_scale_of(*reinterpret_cast<volatile unsigned*>(a.maxlen));
+  if (tid == 0) *a.dscale = sc;
+  const int G = a.dk / 8, GW = G < 8 ? G : 8, sets = 8 / GW, PT = 32 * sets;
+  float emax = 0.0f;
+  for (int64_t p0 = (int64_t)blockIdx.x * PT; p0 < a.npad; p0 += (int64_t)gridDim.x * PT)
+    emax = fmaxf(emax, pack_tile(a, sc.scale, vec, p0, G, GW, sets, s_part, e_part));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  __shared__ float wmax[8];
+  if (lane == 0) wmax[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int t = 0; t < 8; t++) m = fmaxf(m, wmax[t]);
+    if (m > 0.0f) atomicMax(a.maxerr, __float_as_uint(m));
+  }
+  prep_mark(a, 5);
+}
+
+// centre, scale (+ round 0's packing when cooperative), the caller's initialisations and
+// the validation verdict
+static appd_status launch_prepare(appd_ctx* c, const float* X, TcState* st, const InitList* init, u64* bad) {
+  const int64_t n = st->n, d = st->d;
+  const int rpb = 64;  // rows per partial sum (separate kernels)
+  const int blocks = (int)((n + rpb - 1) / rpb);
+  const int rpb_coop = 16;  // (cooperative: one warp per block)
+  const int blocks_coop = (int)((n + rpb_coop - 1) / rpb_coop);
+  double* part = (double*)ws(c, S_TC_PART, sizeof(double) * std::max(blocks, blocks_coop) * d);
+  if (!part) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc center");
+  unsigned* maxlen = (unsigned*)(st->center + d);
+  static std::atomic<unsigned long long> occ_set{0};
+  static int occ[64];
+  if (needs_setup(occ_set, c)) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_tc_prep, 256, 0) != cudaSuccess) o = 0;
+    cudaGetLastError();
+    occ[c->device & 63] = o;
+    setup_done(occ_set, c);
+  }
+  const int per_sm = std::min(occ[c->device & 63], 4);
+  InitList L;
+  if (init) L = *init;
+  if (per_sm >= 1 && st->topk && L.count + 8 <= 16) {
+    // round 0's own initialisations ride along
+    L.add(st->perm, n, 0, 2);
+    L.add(st->UB, st->npad, 0x7F7F7F7Fu, 0);
+    L.add(st->counters, 16, 0, 0);
+    L.add(st->rowflag, n, 0, 0);
+    L.add(st->cand_cnt, st->npad, 0, 0);
+    L.add(st->need, n, 0, 0);
+    L.add(st->seg_maxlen, st->npad / TC_TMG, 0, 0);
+    L.add(st->seg_maxerr, st->npad / TC_TMG, 0, 0);
+    PrepArgs a;
+    a.X = X;
+    a.n = n;
+    a.npad = st->npad;
+    a.d = (int)d;
+    a.dk = st->dk;
+    a.K = st->K;
+    a.rpb = rpb_coop;
+    a.blocks = blocks_coop;
+    a.part = part;
+    a.center = st->center;
+    a.maxlen = maxlen;
+    a.dscale = st->dscale;
+    a.YA = (__half*)st->YA;
+    a.YB = (__half*)st->YB;
+    a.nrm = st->nrm;
+    a.len = st->len;
+    a.err = st->err;
+    a.maxerr = st->maxerr;
+    a.xt = st->XT;
+    a.seg_maxlen = reinterpret_cast<unsigned*>(st->seg_maxlen);
+    a.seg_maxerr = reinterpret_cast<unsigned*>(st->seg_maxerr);
+    a.bad = bad;
+    a.dbg = nullptr;
+    a.init = L;
+    static const bool times = dev_env("APPD_PREP_TIMES") != nullptr;
+    if (times) a.dbg = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 64));
+    void* args[] = {&a};
+    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_tc_prep, c->sm_count * per_sm, 256, args, 0, c->stream));
+    APPD_LAUNCHED(c);
+    if (times && a.dbg) {
+      unsigned long long h[6];
+      cudaStreamSynchronize(c->stream);
+      cudaMemcpy(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[prep] grid %d: phase1 %.1f us, sync %.1f, centre %.1f, maxlen %.1f, pack %.1f\n",
+              c->sm_count * per_sm, (h[1] - h[0]) * 1e-3, (h[2] - h[1]) * 1e-3, (h[3] - h[2]) * 1e-3,
+              (h[4] - h[3]) * 1e-3, (h[5] - h[4]) * 1e-3);
+    }
+    st->r0_packed = true;
+  } else {
+    if (L.count) {
+      k_init<<<c->sm_count * 4, 256, 0, c->stream>>>(L);
+      APPD_LAUNCHED(c);
+    }
+    if (bad) {
+      APPD_CUDA(c, cudaMemsetAsync(bad, 0xFF, 3 * sizeof(u64), c->stream));
+      appd_status s = launch_validate_points(c, X, n, d, bad);
+      if (s) return s;
+    }
+    k_center_partial<<<blocks, 256, 0, c->stream>>>(X, n, (int)d, rpb, part);
+    APPD_LAUNCHED(c);
+    k_center_final<<<(unsigned)((d + 7) / 8), 256, 0, c->stream>>>(part, blocks, n, (int)d, st->center);
+    APPD_LAUNCHED(c);
+    APPD_CUDA(c, cudaMemsetAsync(maxlen, 0, sizeof(unsigned), c->stream));
+    k_maxlen<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8), 256, 0, c->stream>>>(
+        X, n, (int)d, st->center, maxlen);
+    APPD_LAUNCHED(c);
+    // the scale on the device (no host round trip)
+    k_tc_scale<<<1, 1, 0, c->stream>>>(maxlen, st->dscale);
+    APPD_LAUNCHED(c);
+  }
+  // its ok flag is read at the caller's next synchronisation (coordinates too large for
+  // the filter: the solve falls back to the exact engine)
+  APPD_PUBLISH(c, c->pinned_small + 50, &st->dscale->ok, sizeof(int));
+  return APPD_OK;
+}
+
+appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcState* st, const InitList* init,
+                        u64* bad) {
   st->n = n;
   st->d = d;
   st->npad = (n + TC_ROWS - 1) / TC_ROWS * TC_ROWS;
   st->dk = (int)((d + 15) / 16 * 16);
   st->K = st->dk + 16;
   st->stages = tcf_stages(st->K);
+  st->r0_packed = false;
   if (st->stages == 0) return APPD_ERR_UNSUPPORTED;
-  const int rpb = 64;  // rows per partial sum
-  const int blocks = (int)((n + rpb - 1) / rpb);
-  double* part = (double*)ws(c, S_TC_PART, sizeof(double) * blocks * d);
   st->center = (float*)ws(c, S_TC_CENTER, sizeof(float) * (d + 1) + 64);
-  if (!part || !st->center) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc center");
-  k_center_partial<<<blocks, 256, 0, c->stream>>>(X, n, (int)d, rpb, part);
-  APPD_LAUNCHED(c);
-  k_center_final<<<(unsigned)((d + 7) / 8), 256, 0, c->stream>>>(part, blocks, n, (int)d, st->center);
-  APPD_LAUNCHED(c);
-  unsigned* maxlen = (unsigned*)(st->center + d);
-  APPD_CUDA(c, cudaMemsetAsync(maxlen, 0, sizeof(unsigned), c->stream));
-  k_maxlen<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8), 256, 0, c->stream>>>(
-      X, n, (int)d, st->center, maxlen);
-  APPD_LAUNCHED(c);
-  // the scale on the device (no host round trip); its ok flag is read at the caller's next
-  // synchronisation (coordinates too large for the filter: the solve falls back)
   st->dscale = (TcScale*)ws(c, S_TC_SCALE, sizeof(TcScale));
-  if (!st->dscale) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc scale");
-  k_tc_scale<<<1, 1, 0, c->stream>>>(maxlen, st->dscale);
-  APPD_LAUNCHED(c);
-  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 50, &st->dscale->ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (!st->center || !st->dscale) return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc center");
   // Error model in scaled units (tc_common.cuh):
   //  delta: each fp16 coordinate is within 2^-11 (relative, normal range) or 2^-25
   //    (absolute, subnormal) of s*(x - c); centring x - c in fp32 adds 2^-24 relative;
@@ -610,7 +1033,7 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
       !st->perm || !st->sc || !st->keys || !st->cstart || !st->cend || !st->rs || !st->re || !st->UB ||
       !st->counters || !st->fallback || !st->rowflag || !st->TM || !st->list)
     return fail(c, APPD_ERR_OUT_OF_MEMORY, "tc workspace");
-  return APPD_OK;
+  return launch_prepare(c, X, st, init, bad);
 }
 
 // xt: the d x npad fp32 transpose of the packed order for the exact kernels (nullptr:
@@ -729,12 +1152,11 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   // counting sort by chunk on the device (no host round trip); the count is read at a
   // later synchronisation for the statistics (and the component-matrix overflow check)
   cnt = st->list_entries_cap;  // capacity bound; the kernels read the real count on the device
-  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 16, count_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                               c->stream));
+  APPD_PUBLISH(c, c->pinned_small + 16, count_dev, sizeof(unsigned));
   int4* items = (int4*)ws(c, S_TC_ITEMS, sizeof(int4) * ((size_t)cnt / 128 + nch + 8));
   if (!items) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list items");
   if ((s = launch_list_counting(c, st->lista, count_dev, cnt, nch, hist, offs, cursor, st->listb, run_lo, run_nb,
-                                item_start, items)))
+                                item_start, items, mode == 1)))
     return s;
   ListParams L;
   memset(&L, 0, sizeof L);
@@ -769,8 +1191,7 @@ appd_status tcf_lookup_async(appd_ctx* c, TcState* st, const int* comp, u64* com
   appd_status s = launch_cache_lookup(c, (int)st->cache_r0, (int)st->cache_r1, st->topk, (int)st->n, st->ckey, st->cj,
                                       st->ccnt, comp, compbest, st->need, st->counters + 3, st->rows_list);
   if (s) return s;
-  APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 9, st->counters + 3, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                               c->stream));
+  APPD_PUBLISH(c, c->pinned_small + 9, st->counters + 3, sizeof(unsigned));
   st->lookup_pending = true;
   return APPD_OK;
 }
@@ -808,8 +1229,10 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
       return launch_rows_exact(c, st->XT, st->npad, (int)n, (int)st->d, st->rows_list, st->counters + 3,
                                (int)rescan_rows, comp, compbest);
   }
+  const bool packed = round == 0 && st->r0_packed;  // done by the cooperative preparation
+  st->r0_packed = false;
   if (round == 0) {
-    if ((s = launch_iota(c, st->perm, n))) return s;
+    if (!packed && (s = launch_iota(c, st->perm, n))) return s;
   } else {
     k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
     APPD_LAUNCHED(c);
@@ -821,11 +1244,13 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   }
   // round 0 of the cache: the permutation is the identity, so the transpose is the
   // original-order one the exact row kernel reads
-  if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp))) return s;
-  host_mark("tcf_round: pack queued");
-  APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));  // ~3.4e38
-  APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
-  APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
+  if (!packed) {
+    if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp))) return s;
+    host_mark("tcf_round: pack queued");
+    APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));  // ~3.4e38
+    APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
+    APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
+  }
   TcParams P;
   fill_scan_params(st, &P);
   P.round0 = round == 0;
@@ -861,7 +1286,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     st->scanned = true;
     if (p_end > p_begin) {
       const int nch = (int)(st->npad / 32);
-      APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
+      if (!packed) APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
       if ((s = launch_topk_scan(c, st->topk, st->TM, nch, p_begin, p_end, st->nrm, st->len,
                                 st->dscale, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
                                 st->lista, st->counters + 6,
@@ -881,7 +1306,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     st->cache_r0 = p_begin;
     st->cache_r1 = p_end;
     // rows outside this rank's cache are never flagged (multi-rank: need[] is read for all rows)
-    APPD_CUDA(c, cudaMemsetAsync(st->need, 0, sizeof(int) * n, c->stream));
+    if (!packed) APPD_CUDA(c, cudaMemsetAsync(st->need, 0, sizeof(int) * n, c->stream));
   } else if (cache) {
     // ---- re-scan of the blocks holding flagged rows ----
     APPD_CUDA(c, cudaMemsetAsync(st->blockflag, 0, sizeof(int) * (2 * (T + 1) + 8), c->stream));
@@ -902,8 +1327,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     E.needp = st->needp;
     E.compUB = st->compUB;
     if ((s = exact_stage(c, E))) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_small + 8, st->rb_count, sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                 c->stream));
+    APPD_PUBLISH(c, c->pinned_small + 8, st->rb_count, sizeof(unsigned));
   } else {
     // ---- no cache: every row of this rank ----
     P.rb_begin = (int)rb_begin;
@@ -916,8 +1340,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if ((s = exact_stage(c, E))) return s;
   }
   // statistics land in pinned memory; read after the round's stream synchronisation
-  APPD_CUDA(c, cudaMemcpyAsync(st->h_counters, st->counters, 8 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                               c->stream));
+  APPD_PUBLISH(c, st->h_counters, st->counters, 8 * sizeof(unsigned));
   return APPD_OK;
 }
 

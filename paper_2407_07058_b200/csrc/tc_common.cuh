@@ -155,7 +155,7 @@ struct ListParams {
 };
 appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsigned* count, unsigned cap, int nch,
                                  unsigned* hist, unsigned* offs, unsigned* cursor, unsigned* out, unsigned* run_lo,
-                                 unsigned* run_nb, unsigned* item_start, int4* items);
+                                 unsigned* run_nb, unsigned* item_start, int4* items, bool aggregate);
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
 appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
