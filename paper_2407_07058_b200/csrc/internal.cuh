@@ -2,6 +2,7 @@
 // Nothing here is shared with oracle/ (the CPU oracle is independent).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <chrono>
 #include <cstdio>
@@ -221,7 +222,7 @@ struct TcState {
   unsigned* h_counters = nullptr;  // pinned host copy: [0] fallback rows, [2] exact chunks
   int* fallback = nullptr;
   int* rowflag = nullptr;
-  float* TM = nullptr;      // [col tile][row] eligible maxima of G' from the scan
+  void* TM = nullptr;       // stored maxima of the scans (fp32; the cache pass: fp16 encoded, tm_store)
   void* list = nullptr;     // uint2 (row, tile) pairs that need the exact check
   unsigned list_cap = 0;
   // round-0 candidate cache (k_cache.cu); topk == 0: no cache

@@ -62,7 +62,7 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
 // and keeping the running K largest BATCH maxima (one insertion per 32 chunks).  K
 // batches hold K distinct chunks, so the merged K-th largest batch maximum gK is a lower
 // bound of the row's K-th largest chunk maximum.  Every group whose maximum reaches
-// t = min(thr(gK), gK) is then read again (two 16-byte loads, TK_RG groups per lane in
+// t = min(thr(gK), gK) is then read again (one 16-byte load, TK_RG groups per lane in
 // flight): its chunks >= t are kept (shared memory) and enter the chunk-level top-K.
 // Every chunk of the row's K largest is >= gK >= t, so the merged chunk-level list is
 // the exact K largest, which give UBK and the listing threshold thrK >= t; the kept
@@ -70,7 +70,7 @@ __device__ __forceinline__ unsigned warp_alloc(unsigned* counter, unsigned cnt) 
 // its flagged groups once more; a row whose list entries do not fit is poisoned
 // (cand_cnt = 2^31: invalid cache, exact full-row minimum).
 constexpr int TK_PARTS = 4;
-constexpr int TK_BATCH = 32;  // chunk maxima per batch (8 x 128-bit loads)
+constexpr int TK_BATCH = 32;  // chunk maxima per batch (4 x 128-bit loads of fp16)
 constexpr int TK_SEL = 16;    // kept chunks per (row, quarter) in shared memory
 constexpr int TK_RG = 4;      // flagged groups re-read together
 constexpr int TK_STAGES = 4;  // cp.async ring depth (batches; 3 in flight while one is processed)
@@ -137,8 +137,20 @@ __device__ __forceinline__ void topk_merge(float (&top)[K], const float (*stop)[
   }
 }
 
+// 8 stored chunk values (fp16 distance estimates D', tm_store; one 16-byte piece of the
+// packed table) -> floats
+__device__ __forceinline__ void h8(const uint4 x, float (&f)[8]) {
+  const __half2* h = reinterpret_cast<const __half2*>(&x);
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const float2 t = __half22float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
 template <int K>
-__global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __restrict__ TM32, int nch, int p_begin,
+__global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __restrict__ TM32, int nch, int p_begin,
                                                              int p_end, const float* __restrict__ nrm,
                                                              const float* __restrict__ len, const TcScale* __restrict__ sc,
                                                              const float* __restrict__ err,
@@ -153,28 +165,28 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
   __shared__ int slost[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float maxlen = sc->maxlen;
-  constexpr int U4 = TK_BATCH / 4;
-  const int nch4 = (nch + 3) >> 2;
-  const int g0 = (int)((int64_t)w * nch4 / TK_PARTS), g1 = (int)((int64_t)(w + 1) * nch4 / TK_PARTS);
-  const int cb = 4 * g0, cend = min(nch, 4 * g1);  // this warp's chunk range
+  constexpr int U8 = TK_BATCH / 8;  // 16-byte pieces per batch
+  const int nch8 = (nch + 7) >> 3;
+  const int g0 = (int)((int64_t)w * nch8 / TK_PARTS), g1 = (int)((int64_t)(w + 1) * nch8 / TK_PARTS);
+  const int cb = 8 * g0, cend = min(nch, 8 * g1);  // this warp's chunk range (whole 8-chunk groups)
   const int nbat = (cend - cb + TK_BATCH - 1) / TK_BATCH;
   const int ng = (cend - cb + 7) / 8;               // 8-chunk groups of this quarter (<= ngq)
   float* gm = sgm + (size_t)w * ngq * 32 + lane;    // gm[g * 32]
-  // cp.async ring after the group maxima: [TK_PARTS][TK_STAGES][U4][32] float4
-  float4* ring = reinterpret_cast<float4*>(sgm + (size_t)TK_PARTS * ngq * 32) + (size_t)w * TK_STAGES * U4 * 32 + lane;
-  const float4 NEG = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+  // cp.async ring after the group maxima: [TK_PARTS][TK_STAGES][U8][32] uint4
+  uint4* ring = reinterpret_cast<uint4*>(sgm + (size_t)TK_PARTS * ngq * 32) + (size_t)w * TK_STAGES * U8 * 32 + lane;
   for (int p0 = p_begin + 32 * blockIdx.x; p0 < p_end; p0 += 32 * gridDim.x) {
     const int p = p0 + lane;
     const bool valid = p < p_end;
     if (w == 0) slost[lane] = 0;
-    const float4* row4 = reinterpret_cast<const float4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
-    // the 16-byte group of chunks c .. c+3 (c a multiple of 4; chunks past cend read as -inf)
-    auto load4 = [&](int c) -> float4 {
-      float4 x = (valid && c < cend) ? __ldcs(row4 + (int64_t)(c >> 2) * 512) : NEG;
-      if (c + 1 >= cend) x.y = -INFINITY;
-      if (c + 2 >= cend) x.z = -INFINITY;
-      if (c + 3 >= cend) x.w = -INFINITY;
-      return x;
+    const uint4* row8 = reinterpret_cast<const uint4*>(TM32 + tm32_index(0, valid ? p : p_begin, nch));
+    const float ni = valid ? nrm[p] : 0.0f;  // the encoding's |y^_p|^2 (tm_low / tm_up)
+    // the 8 chunks of group c .. c+7 (c a multiple of 8; chunks past cend read as +inf:
+    // no eligible column)
+    auto load8 = [&](int c, float (&f)[8]) {
+      if (valid && c < cend) h8(__ldcs(row8 + (int64_t)(c >> 3) * 512), f);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (!valid || c + u >= cend) f[u] = INFINITY;
     };
     // ---- scan: group maxima and the top-K of group maxima.  Batches are staged by
     // cp.async into a TK_STAGES ring (each lane copies and reads only its own row's 16-byte
@@ -185,10 +197,10 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     auto issue = [&](int b) {
       if (b < nbat) {
 #pragma unroll
-        for (int u = 0; u < U4; u++) {
-          const int c = cb + b * TK_BATCH + 4 * u;
+        for (int u = 0; u < U8; u++) {
+          const int c = cb + b * TK_BATCH + 8 * u;
           const bool ok = valid && c < cend;
-          cp_async16(&ring[((b % TK_STAGES) * U4 + u) * 32], row4 + (int64_t)((ok ? c : cb) >> 2) * 512, ok ? 16 : 0);
+          cp_async16(&ring[((b % TK_STAGES) * U8 + u) * 32], row8 + (int64_t)((ok ? c : cb) >> 3) * 512, ok ? 16 : 0);
         }
       }
       cp_async_commit();
@@ -198,30 +210,32 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     for (int b = 0; b < nbat; b++) {
       issue(b + TK_STAGES - 1);
       cp_async_wait<TK_STAGES - 1>();
-      float4 v[U4];
-#pragma unroll
-      for (int u = 0; u < U4; u++) v[u] = ring[((b % TK_STAGES) * U4 + u) * 32];
-      if (cb + (b + 1) * TK_BATCH > cend) {  // the quarter's ragged last batch (warp-uniform)
-#pragma unroll
-        for (int u = 0; u < U4; u++) {
-          const int c = cb + b * TK_BATCH + 4 * u;
-          if (c >= cend) v[u].x = -INFINITY;
-          if (c + 1 >= cend) v[u].y = -INFINITY;
-          if (c + 2 >= cend) v[u].z = -INFINITY;
-          if (c + 3 >= cend) v[u].w = -INFINITY;
-        }
-      }
       // (rows past p_end hold zero-filled data; nothing of theirs is written)
-      float bm = -INFINITY;
+      // the group minimum of D' (= maximum of G') in half2 arithmetic, then one decode
+      float bd = INFINITY;
 #pragma unroll
-      for (int q = 0; q < TK_BATCH / 8; q++) {
-        const float4 a = v[2 * q], c = v[2 * q + 1];
-        const float m = fmax3f(fmax3f(a.x, a.y, a.z), fmax3f(a.w, c.x, c.y), fmaxf(c.z, c.w));
+      for (int q = 0; q < U8; q++) {
+        const uint4 x = ring[((b % TK_STAGES) * U8 + q) * 32];
+        const int c = cb + b * TK_BATCH + 8 * q;
+        float m;
+        if (c + 8 > cend) {  // the quarter's ragged end (warp-uniform)
+          float f[8];
+          h8(x, f);
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+            if (c + u >= cend) f[u] = INFINITY;
+          m = fminf(fminf(fminf(f[0], f[1]), fminf(f[2], f[3])), fminf(fminf(f[4], f[5]), fminf(f[6], f[7])));
+        } else {
+          const __half2* hh = reinterpret_cast<const __half2*>(&x);
+          const __half2 t = __hmin2(__hmin2(hh[0], hh[1]), __hmin2(hh[2], hh[3]));
+          m = fminf(__low2float(t), __high2float(t));
+        }
         const int g = b * (TK_BATCH / 8) + q;
         if (g < ng) gm[g * 32] = m;
-        bm = fmaxf(bm, m);
+        bd = fminf(bd, m);
       }
-      // top-K of BATCH maxima: K batches hold K distinct chunks
+      // top-K of BATCH maxima (lower bounds): K batches hold K distinct chunks
+      const float bm = bd == INFINITY ? -INFINITY : tm_low(bd, ni);
       if (bm > top[K - 1]) topk_insert(top, bm);
     }
     cp_async_wait<0>();
@@ -230,18 +244,19 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     __syncthreads();
     topk_merge(top, stop, w, lane);
     const float gK = top[K - 1];
-    float ni = 0.0f, li = 0.0f, dl = 0.0f;
+    float li = 0.0f, dl = 0.0f;
     if (valid) {
-      ni = nrm[p];
       li = len[p];
       dl = em_delta2(err[p], *maxerr);
     }
-    // capture threshold t (fewer than K finite group maxima: every finite chunk)
+    // capture threshold t (fewer than K finite group maxima: every finite chunk).  The
+    // top-K is of lower bounds tm_low (gK, UBK stay valid); every test against a
+    // threshold takes the upper bound tm_up (the listing keeps every candidate)
     float tcap = valid ? -INFINITY : INFINITY;
     if (valid && gK > -INFINITY) tcap = fminf(gK, em_thr(em, em_upper(em, ni - 2.0f * gK, ni, li, maxlen, dl), ni, li, maxlen, dl));
     auto flagged = [&](int g) {
-      const float m = gm[g * 32];
-      return m >= tcap && m > -INFINITY;
+      const float dg = gm[g * 32];
+      return dg < INFINITY && tm_up(dg, ni) >= tcap;
     };
     // ---- re-read the flagged groups (bit masks, ng <= 128): keep chunks >= t,
     // chunk-level top-K
@@ -259,7 +274,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     unsigned kept = 0;
     for (int j = 0; j < jmax; j += TK_RG) {
       int gg[TK_RG];
-      float4 a[TK_RG], bq[TK_RG];
+      float vv[TK_RG][8];
 #pragma unroll
       for (int r = 0; r < TK_RG; r++) {
         if (fm0) {
@@ -271,22 +286,23 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
         } else {
           gg[r] = -1;
         }
-        const int c = cb + 8 * gg[r];
-        a[r] = gg[r] >= 0 ? load4(c) : NEG;
-        bq[r] = gg[r] >= 0 ? load4(c + 4) : NEG;
+        if (gg[r] >= 0) load8(cb + 8 * gg[r], vv[r]);
+        else
+#pragma unroll
+          for (int u = 0; u < 8; u++) vv[r][u] = INFINITY;
       }
 #pragma unroll
       for (int r = 0; r < TK_RG; r++) {
-        const float vv[8] = {a[r].x, a[r].y, a[r].z, a[r].w, bq[r].x, bq[r].y, bq[r].z, bq[r].w};
 #pragma unroll
         for (int u = 0; u < 8; u++)
-          if (vv[u] >= tcap && vv[u] > -INFINITY) {
+          if (vv[r][u] < INFINITY && tm_up(vv[r][u], ni) >= tcap) {
             if (kept < TK_SEL) {
-              sval[w][kept][lane] = vv[u];
+              sval[w][kept][lane] = vv[r][u];
               sidx[w][kept][lane] = (unsigned short)(cb + 8 * gg[r] + u);
             }
             kept++;
-            if (vv[u] > top[K - 1]) topk_insert(top, vv[u]);
+            const float lo = tm_low(vv[r][u], ni);
+            if (lo > top[K - 1]) topk_insert(top, lo);
           }
       }
     }
@@ -305,21 +321,21 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     // ---- list the kept chunks passing thrK: count, one warp allocation, write
     unsigned mine = 0;
     if (kept <= TK_SEL) {
-      for (unsigned t = 0; t < kept; t++) mine += sval[w][t][lane] >= thr;
+      for (unsigned t = 0; t < kept; t++) mine += tm_up(sval[w][t][lane], ni) >= thr;
     } else {
       for (int g = 0; g < ng; g++) {
         if (!flagged(g)) continue;
-        const float4 x0 = load4(cb + 8 * g), x1 = load4(cb + 8 * g + 4);
-        const float vv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        float vv[8];
+        load8(cb + 8 * g, vv);
 #pragma unroll
-        for (int u = 0; u < 8; u++) mine += vv[u] >= thr && vv[u] > -INFINITY;
+        for (int u = 0; u < 8; u++) mine += vv[u] < INFINITY && tm_up(vv[u], ni) >= thr;
       }
     }
     unsigned slot = warp_alloc(count, mine);
     bool lost = false;
     if (kept <= TK_SEL) {
       for (unsigned t = 0; t < kept; t++)
-        if (sval[w][t][lane] >= thr) {
+        if (tm_up(sval[w][t][lane], ni) >= thr) {
           if (slot < cap) list[slot] = ((unsigned)sidx[w][t][lane] << LIST_SHIFT) | (unsigned)p;
           else lost = true;
           slot++;
@@ -327,11 +343,11 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
     } else {  // more than TK_SEL kept chunks (rare): read the flagged groups again
       for (int g = 0; g < ng; g++) {
         if (!flagged(g)) continue;
-        const float4 x0 = load4(cb + 8 * g), x1 = load4(cb + 8 * g + 4);
-        const float vv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        float vv[8];
+        load8(cb + 8 * g, vv);
 #pragma unroll
         for (int u = 0; u < 8; u++)
-          if (vv[u] >= thr && vv[u] > -INFINITY) {
+          if (vv[u] < INFINITY && tm_up(vv[u], ni) >= thr) {
             if (slot < cap) list[slot] = ((unsigned)(cb + 8 * g + u) << LIST_SHIFT) | (unsigned)p;
             else lost = true;
             slot++;
@@ -344,17 +360,16 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const float* __rest
   }
 }
 
-appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
+appd_status launch_topk_scan(appd_ctx* c, int K, const __half* TM32, int nch, int p_begin, int p_end,
                              const float* nrm, const float* len, const TcScale* sc, const float* err,
                              const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
                              unsigned cap, unsigned* cand_cnt) {
   const int rows = p_end - p_begin;
   if (rows <= 0) return APPD_OK;
   const int grid = std::min(c->sm_count * 16, (rows + 31) / 32);
-  // groups per quarter: the largest quarter has ceil(ceil(nch/4)/TK_PARTS) 16-byte groups
-  const int q4 = ((nch + 3) / 4 + TK_PARTS - 1) / TK_PARTS;
-  const int ngq = (4 * q4 + 7) / 8;
-  const size_t smem = sizeof(float) * TK_PARTS * ngq * 32 + sizeof(float4) * TK_PARTS * TK_STAGES * (TK_BATCH / 4) * 32;
+  // 8-chunk groups per quarter: the largest quarter has ceil(ceil(nch/8)/TK_PARTS)
+  const int ngq = ((nch + 7) / 8 + TK_PARTS - 1) / TK_PARTS;
+  const size_t smem = sizeof(float) * TK_PARTS * ngq * 32 + sizeof(uint4) * TK_PARTS * TK_STAGES * (TK_BATCH / 8) * 32;
   if (ngq > 128) return fail(c, APPD_ERR_UNSUPPORTED, "top-K scan: %d chunks per row", nch);
 #define APPD_TOPK_SCAN(KK)                                                                                     \
   do {                                                                                                         \

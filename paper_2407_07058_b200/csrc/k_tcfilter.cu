@@ -992,7 +992,9 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
   if (st->topk != 0 && st->topk != 4 && st->topk != 8 && st->topk != 16 && st->topk != 32)
     return fail(c, APPD_ERR_INVALID_ARGUMENT, "topk = %d (0, -1, 4, 8, 16 or 32)", c->opt.topk);
   // TM holds 32-column maxima in the cache-building round (4x the 128-column layout)
-  st->TM = (float*)ws(c, S_TC_APPV, sizeof(float) * st->npad * (st->npad / (st->topk ? 32 : TC_TMG)));
+  // (the cache pass's fp16 32-column table and the later passes' fp32 64-column tables)
+  st->TM = ws(c, S_TC_APPV, std::max<int64_t>(st->topk ? sizeof(__half) * tm32_elems(st->npad) : 0,
+                                             sizeof(float) * st->npad * (st->npad / TC_TMG)));
   st->list_cap = (unsigned)std::min<int64_t>(16 * n + 65536, (int64_t)1 << 30);
   st->list = ws(c, S_TC_APPPC, sizeof(uint2) * st->list_cap);
   if (st->topk) {
@@ -1100,7 +1102,7 @@ static void exact_params(const TcState* st, const TcParams& P, const int* comp, 
   E->cs = st->rs;
   E->ce = st->re;
   E->UB = st->UB;
-  E->TM = st->TM;
+  E->TM = static_cast<const float*>(st->TM);
   E->nseg = (int)(st->npad / TC_TMG);
   E->p_begin = p_begin;
   E->p_end = p_end;
@@ -1287,7 +1289,7 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
     if (p_end > p_begin) {
       const int nch = (int)(st->npad / 32);
       if (!packed) APPD_CUDA(c, cudaMemsetAsync(st->cand_cnt, 0, sizeof(unsigned) * st->npad, c->stream));
-      if ((s = launch_topk_scan(c, st->topk, st->TM, nch, p_begin, p_end, st->nrm, st->len,
+      if ((s = launch_topk_scan(c, st->topk, static_cast<const __half*>(st->TM), nch, p_begin, p_end, st->nrm, st->len,
                                 st->dscale, st->err, reinterpret_cast<const float*>(st->maxerr), P.em, st->UBK,
                                 st->lista, st->counters + 6,
                                 st->list_entries_cap, st->cand_cnt)))
@@ -1381,7 +1383,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);
   CmParams C;
   memset(&C, 0, sizeof C);
-  C.TM = st->TM;
+  C.TM = static_cast<const float*>(st->TM);
   C.ld = st->npad;
   C.nseg = (int)(st->npad / TC_TMG);
   C.n = (int)n;

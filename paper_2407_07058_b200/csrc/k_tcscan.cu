@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
       // maximum so far and the running upper bound.  The cache-building pass (SEG32)
       // needs no bound.  Row p = rb * 512 + r * 128 + q * 32 + lane.
       int cs[TC_RT], ce[TC_RT];
-      float ub[TC_RT], gb[TC_RT];
+      float ub[TC_RT], gb[TC_RT], nr[TC_RT];  // nr: |y^_p|^2, the stored maxima's encoding (tm_store)
       const int pbase = rb * TC_ROWS + q * 32 + lane;
 #pragma unroll
       for (int r = 0; r < TC_RT; r++) {
@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
         const bool valid = p < P.n;
         cs[r] = valid ? (P.round0 ? p : P.cs[p]) : 0;
         ce[r] = valid ? (P.round0 ? p + 1 : P.ce[p]) : 0;
+        nr[r] = valid ? __ldg(P.nrm + p) : 0.0f;
         ub[r] = INFINITY;
         gb[r] = -INFINITY;
       }
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(tempty + b);  // accumulator consumed: free it early
           if (PASS == 4) {  // experiment: TMEM load only
-            if (v[0] == 12345.678f && valid) P.TM[p] = v[WCOLS - 1];
+            if (v[0] == 12345.678f && valid) static_cast<float*>(P.TM)[p] = v[WCOLS - 1];
             continue;
           }
           if (PASS == 2) {  // test hook: raw accumulators of the CTA's first item
@@ -318,7 +319,8 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
               cm[c] = chunk_max(w, valid, cs[r], ce[r], h0 + c * 32, fast, P.n);
             }
             if (valid)
-              *reinterpret_cast<float2*>(P.TM + tm32_index(h0 / 32, p, P.tm_nseg)) = make_float2(cm[0], cm[1]);
+              *reinterpret_cast<__half2*>(static_cast<__half*>(P.TM) + tm32_index(h0 / 32, p, P.tm_nseg)) =
+                  __halves2half2(tm_store(cm[0], nr[r]), tm_store(cm[1], nr[r]));
           } else {
             float m;
             if (fast) {
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(EpiCfg<SEG32>::threads, 1) k_tcf_scan(TcParams
             }
             // eligible maximum of G' over this (row, segment); a warp's rows are
             // consecutive, so the store is coalesced ([segment][row] layout)
-            if (valid) P.TM[tm_index(seg, p, P.col_tiles * (TC_N / TC_TMG))] = m;
+            if (valid) static_cast<float*>(P.TM)[tm_index(seg, p, P.col_tiles * (TC_N / TC_TMG))] = m;
             if (PASS == 0 && valid && m > gb[r]) {  // tighten the bound only when the best improves (rare)
               gb[r] = m;
               const float ni = __ldg(P.nrm + p), li = __ldg(P.len + p);

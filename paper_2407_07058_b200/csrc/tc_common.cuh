@@ -59,13 +59,34 @@ __host__ __device__ __forceinline__ int64_t tm_index(int s, int p, int nseg) {
   return (int64_t)(p >> 9) * nseg * 512 + (int64_t)s * 512 + (p & 511);
 }
 
-// The 32-column table additionally packs 4 consecutive chunks of a row together
-// (16 bytes), so a reader loads 4 chunk maxima per 128-bit access:
-//   (p / 512) * nch * 512 + (c / 4) * 2048 + (p % 512) * 4 + c % 4     (nch % 4 == 0)
+// The 32-column table additionally packs 8 consecutive chunks of a row together
+// (16 bytes of fp16), so a reader loads 8 chunk maxima per 128-bit access (nch rounded
+// up to a multiple of 8 per 512-row block):
+//   (p / 512) * nch8 * 512 + (c / 8) * 4096 + (p % 512) * 8 + c % 8
 __host__ __device__ __forceinline__ int64_t tm32_index(int c, int p, int nch) {
-  return (int64_t)(p >> 9) * nch * 512 + (int64_t)(c >> 2) * 2048 + (p & 511) * 4 + (c & 3);
+  const int nch8 = (nch + 7) & ~7;
+  return (int64_t)(p >> 9) * nch8 * 512 + (int64_t)(c >> 3) * 4096 + (p & 511) * 8 + (c & 7);
+}
+__host__ __device__ __forceinline__ int64_t tm32_elems(int64_t npad) {  // table size (halves)
+  return npad * (((npad / 32) + 7) & ~7ll);
 }
 
+// The 32-column maxima of the cache pass are stored in fp16 (half the traffic of fp32
+// for the writer and the top-K reader), as the squared-distance estimate D = |y^_i|^2 - 2 G' of the row rather than
+// G' itself: D is small exactly where precision matters (near neighbours; an fp16 ulp
+// of G' ~ 2^14 would be 8-16 scaled units, of D ~ 10^3 about one).  The writer rounds
+// up twice (D = ni - 2m in fp32, then to fp16), so for the row's ni = |y^_i|^2:
+//   tm_low(D', ni) <= m <= tm_up(D', ni)
+// -- every bound derived from tm_low stays valid, and every listing test made against
+// tm_up keeps every candidate.  An ineligible segment (m = -inf) is stored as +inf.
+__device__ __forceinline__ __half tm_store(float m, float ni) { return __float2half_ru(__fsub_ru(ni, 2.0f * m)); }
+__device__ __forceinline__ float tm_low(float D, float ni) { return 0.5f * __fsub_rd(ni, D); }
+__device__ __forceinline__ float tm_up(float D, float ni) {
+  // D' exceeds ni - 2m by less than one fp16 spacing (<= 2^-10 |D'|, or 2^-24) plus the
+  // fp32 rounding of the subtraction (<= 2^-23 |D|)
+  if (D == INFINITY) return -INFINITY;
+  return 0.5f * __fadd_ru(__fsub_ru(ni, D), fmaf(fabsf(D), 0x1.1p-10f, 0x1p-23f));
+}
 struct TcParams {
   const __half* YA;          // row operand granules (128 points x K, core-matrix layout)
   const __half* YB;          // column operand granules
@@ -77,7 +98,8 @@ struct TcParams {
   const int* cs;             // per permuted row: first position of its component
   const int* ce;             // per permuted row: one past the last position
   unsigned* UB;              // per permuted row: upper bound (float bits, >= 0)
-  float* TM;                 // [segment][row]: eligible maximum of G' over the TC_TMG columns
+  void* TM;                  // [segment][row]: eligible maximum of G' over the TC_TMG columns (fp32), or
+                             // the 32-column table of the cache pass (fp16 encoded, tm_store)
   int64_t tm_ld;             // leading dimension of TM (npad), [segment][row] layout (128-column tables)
   int tm_nseg;               // segments per row of the row-block-major 32-column table (npad / 32)
   int n;                     // points
@@ -158,7 +180,7 @@ appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsign
                                  unsigned* run_nb, unsigned* item_start, int4* items, bool aggregate);
 appd_status launch_list_exact(appd_ctx* c, int mode, const ListParams& L, unsigned* run_lo, unsigned* run_nb,
                               unsigned* item_start);
-appd_status launch_topk_scan(appd_ctx* c, int K, const float* TM32, int nch, int p_begin, int p_end,
+appd_status launch_topk_scan(appd_ctx* c, int K, const __half* TM32, int nch, int p_begin, int p_end,
                              const float* nrm, const float* len, const TcScale* sc, const float* err,
                              const float* maxerr, const ErrModel& em, float* UBK, unsigned* list, unsigned* count,
                              unsigned cap, unsigned* cand_cnt);
