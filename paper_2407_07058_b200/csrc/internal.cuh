@@ -360,6 +360,26 @@ void trace_end(appd_ctx* c);
     APPD_DEV_SYNC_EACH(c);                                                                      \
   } while (0)
 
+#ifdef __CUDACC__
+// sum of blocksum[0 .. blockIdx.x) for every thread of the block: warp 0 reduces with its
+// loads in flight (a serial loop over up to 147 earlier blocks was ~20 us of dependent
+// L2 latency in the last block of a cooperative scan)
+__device__ __forceinline__ int blocks_before(const int* blocksum) {
+  __shared__ int bb_sum;
+  if (threadIdx.x < 32) {
+    int s = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += 32) s += blocksum[b];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) bb_sum = s;
+  }
+  __syncthreads();
+  const int r = bb_sum;
+  __syncthreads();
+  return r;
+}
+#endif
+
 // ---- kernels (k_*.cu) ----
 // validation
 appd_status launch_validate_weights(appd_ctx* c, const float* W, int64_t n, int64_t row0, int64_t rows,

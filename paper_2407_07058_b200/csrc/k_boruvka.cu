@@ -1055,8 +1055,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
   grid.sync();
-  int off = 0;
-  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
+  const int off = blocks_before(blocksum);
   for (int i = lo + threadIdx.x; i < hi; i += kContractThreads) newid[i] += off;
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) newid[k] = off + carry_s;
   grid.sync();

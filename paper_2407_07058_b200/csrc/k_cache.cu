@@ -780,21 +780,31 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
         }
       // R1 ends with sqrtf; the MST runs on d^2 (monotone, App. A.4)
       if (MODE == 0) {
+        // s2 = scale^2 is a power of two, so s^2 r <= UBK  <=>  r <= UBK / s2 exactly: one
+        // fp32 compare per entry against lim = rd(UBK / s2); the few passing entries append
+        unsigned pass = 0;
+        int op4[4];
 #pragma unroll
         for (int a = 0; a < 4; a++) {
           const int p = rowp[4 * ty + a];
-          if (p < 0) continue;
-          const int op = L.perm ? L.perm[p] : p;
-          const double ubk = (double)L.UBK[p];
+          op4[a] = p < 0 ? -1 : (L.perm ? L.perm[p] : p);
+          const float lim = p < 0 ? -INFINITY : __double2float_rd((double)L.UBK[p] / s2);
 #pragma unroll
-          for (int b = 0; b < 4; b++) {
-            if (oq[b] >= 0 && oq[b] != op && (double)acc[a][b] * s2 <= ubk) {
-              const unsigned slot = atomicAdd(L.cnt + p, 1u);
-              if (slot < (unsigned)L.ccap)
-                L.cand[(int64_t)p * L.ccap + slot] =
-                    ((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(op, oq[b]);
-            }
-          }
+          for (int b = 0; b < 4; b++)
+            if (acc[a][b] <= lim && oq[b] >= 0 && oq[b] != op4[a]) pass |= 1u << (4 * a + b);
+        }
+        if (pass) {
+#pragma unroll
+          for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++)
+              if ((pass >> (4 * a + b)) & 1u) {
+                const int p = rowp[4 * ty + a];
+                const unsigned slot = atomicAdd(L.cnt + p, 1u);
+                if (slot < (unsigned)L.ccap)
+                  L.cand[(int64_t)p * L.ccap + slot] =
+                      ((u64)(__float_as_uint(acc[a][b]) & 0x7FFFFFFFu) << 33) | tri_index(op4[a], oq[b]);
+              }
         }
       } else {
         // component pair of each entry; the common case (one row component, one column

@@ -291,8 +291,7 @@ __device__ void grid_exclusive_scan(cg::grid_group& grid, const int* in, int* ou
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
   grid.sync();
-  int off = 0;
-  for (int b = 0; b < (int)blockIdx.x; b++) off += blocksum[b];
+  const int off = blocks_before(blocksum);
   for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) out[i] += off;
   grid.sync();
 }
