@@ -189,7 +189,7 @@ enum Slot {
   S_TC_XTP, S_TC_CML, S_TC_ROWFLAG, S_TC_APPPC, S_TC_APPV, S_EDGES,
   S_TC_CKEY, S_TC_CJ, S_TC_CCNT, S_TC_NEED, S_TC_NEEDP, S_TC_BLOCKFLAG, S_TC_RBLIST, S_TC_COMPUB, S_TC_UBK,
   S_TC_THRK, S_TC_CANDCNT, S_TC_CANDK, S_TC_WCM, S_TC_ROWLIST, S_TC_XTO, S_TC_LISTA, S_TC_LISTB, S_TC_RUNS, S_DENDRO, S_TC_SEGD, S_TC_ITEMS, S_TC_ERR, S_TC_SEGERR, S_SCAN, S_TC_SCALE, S_F64_A, S_F64_B, S_F64_HW,
-  S_WIDE_ROW, S_WIDE_COMPW, S_WIDE_KEY2, S_LIST_CNT,
+  S_WIDE_ROW, S_WIDE_COMPW, S_WIDE_KEY2, S_LIST_CNT, S_SORT,
   S_NSLOTS
 };
 static_assert(S_NSLOTS <= 96, "workspace slots");

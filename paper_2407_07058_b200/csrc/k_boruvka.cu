@@ -6,7 +6,6 @@
 // row finds its lightest edge leaving its component (a row-parallel, coalesced
 // component-filtered argmin), components take the minimum over their rows, and
 // the chosen edges merge components.  At most ceil(log2 n) rounds.
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <cooperative_groups.h>
@@ -913,59 +912,7 @@ appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent,
   return APPD_OK;
 }
 
-// ---------------------------------------------------------------------------
-// CUB wrappers
-// ---------------------------------------------------------------------------
-appd_status sort_keys_u64(appd_ctx* c, const u64* in, u64* out, int64_t count) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, (int)count, 0, 64, c->stream);
-  void* t = ws(c, S_KEYS_TMP, tmp + 16);
-  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
-  APPD_CUDA(c, cub::DeviceRadixSort::SortKeys(t, tmp, in, out, (int)count, 0, 64, c->stream));
-  c->launches += 4;
-  return APPD_OK;
-}
-
-appd_status sort_keys_u32_bits(appd_ctx* c, const unsigned* in, unsigned* out, int64_t count, int begin_bit, int end_bit) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, (int)count, begin_bit, end_bit, c->stream);
-  void* t = ws(c, S_KEYS_TMP, tmp + 16);
-  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
-  APPD_CUDA(c, cub::DeviceRadixSort::SortKeys(t, tmp, in, out, (int)count, begin_bit, end_bit, c->stream));
-  c->launches += 4;
-  return APPD_OK;
-}
-
-appd_status sort_keys_u64_bits64(appd_ctx* c, const u64* in, u64* out, int64_t count, int begin_bit, int end_bit) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, (int)count, begin_bit, end_bit, c->stream);
-  void* t = ws(c, S_KEYS_TMP, tmp + 16);
-  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
-  APPD_CUDA(c, cub::DeviceRadixSort::SortKeys(t, tmp, in, out, (int)count, begin_bit, end_bit, c->stream));
-  c->launches += 4;
-  return APPD_OK;
-}
-
-appd_status sort_pairs_i32_bits(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count,
-                                int end_bit) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)count, 0, end_bit, c->stream);
-  void* t = ws(c, S_KEYS_TMP, tmp + 16);
-  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
-  APPD_CUDA(c, cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)count, 0, end_bit, c->stream));
-  c->launches += 2;
-  return APPD_OK;
-}
-
-appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count) {
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)count, 0, 32, c->stream);
-  void* t = ws(c, S_KEYS_TMP, tmp + 16);
-  if (!t) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace");
-  APPD_CUDA(c, cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)count, 0, 32, c->stream));
-  c->launches += 4;
-  return APPD_OK;
-}
+// (the radix sorts of the path: k_sort.cu)
 
 // ---------------------------------------------------------------------------
 // One Boruvka contraction in a single cooperative launch (grid-wide barriers between the
