@@ -47,6 +47,49 @@ __global__ void __launch_bounds__(256) k_tiles(float* M, const int* rows, int n)
       __stcs(reinterpret_cast<float4*>(dst + c * 1024) + threadIdx.x, make_float4(1.f, 2.f, 3.f, (float)t));
   }
 }
+// TMA bulk stores: each row segment (W floats) is written to shared memory by the CTA and
+// stored by one thread with cp.async.bulk (NB segments in flight)
+template <int W, int NB>
+__global__ void __launch_bounds__(256) k_tiles_bulk(float* M, const int* rows, int n) {
+  __shared__ __align__(128) float buf[NB][W];
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  for (int t = 0; t < 128; t++) {
+    const int b = t % NB;
+    if (t >= NB) {
+      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1) : "memory");
+      __syncthreads();
+    }
+#pragma unroll
+    for (int c = 0; c < W / 1024; c++)
+      reinterpret_cast<float4*>(buf[b] + c * 1024)[threadIdx.x] = make_float4(1.f, 2.f, 3.f, (float)t);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float* dst = M + (int64_t)rows[t0 + t] * n + (int64_t)blockIdx.x * W;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                   "r"((uint32_t)__cvta_generic_to_shared(buf[b])), "r"(W * 4)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// persistent: grid = SMs x 4, tiles handed out in order
+template <int W>
+__global__ void __launch_bounds__(256) k_tiles_v8_persist(float* M, const int* rows, int n, int tiles_x, int tiles) {
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int bx = tile % tiles_x, by = tile / tiles_x;
+    const int64_t t0 = (int64_t)by * 128;
+    for (int t = 0; t < 128; t++) {
+      float* dst = M + (int64_t)rows[t0 + t] * n + (int64_t)bx * W + 8 * threadIdx.x;
+#pragma unroll
+      for (int c = 0; c < W / 2048; c++)
+        asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + c * 2048), "f"(1.f),
+                     "f"(2.f), "f"(3.f), "f"(4.f), "f"(5.f), "f"(6.f), "f"(7.f), "f"((float)t)
+                     : "memory");
+    }
+  }
+}
 int main() {
   const int n = 65536;
   const size_t bytes = (size_t)n * n * 4;
@@ -85,5 +128,10 @@ int main() {
   time([&] { k_linear_v8<<<148 * 16, 256>>>(M, bytes / 32); }, "linear v8 (32 B)");
   time([&] { k_tiles_v8<2048><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8 128 x 8 KB");
   time([&] { k_linear<<<148 * 64, 256>>>((float4*)M, bytes / 16); }, "linear (more CTAs)");
+  time([&] { k_tiles_bulk<2048, 4><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles bulk 8 KB x4");
+  time([&] { k_tiles_bulk<2048, 2><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles bulk 8 KB x2");
+  time([&] { k_tiles_bulk<4096, 2><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles bulk 16 KB x2");
+  time([&] { k_tiles_v8_persist<2048><<<148 * 4, 256>>>(M, rows, n, n / 2048, (n / 2048) * (n / 128)); }, "tiles v8 persistent");
+  time([&] { k_tiles_v8<4096><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles v8 128 x 16 KB");
   return 0;
 }
