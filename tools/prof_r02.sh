@@ -14,8 +14,9 @@ ncu --set full --clock-control none --import-source on -k regex:^k_fill$ -s 1 -c
 ncu --set full --clock-control none --import-source on -k regex:k_tcf_scan -s 2 -c 2 -o gpurun_out/r02/full_tcf $CMD > /dev/null 2>&1; echo "tcf $?"
 ncu --set full --clock-control none --import-source on -k regex:k_list_exact -s 2 -c 2 -o gpurun_out/r02/full_list $CMD > /dev/null 2>&1; echo "list $?"
 ncu --set full --clock-control none --import-source on -k regex:k_topk_scan -s 1 -c 1 -o gpurun_out/r02/full_topk $CMD > /dev/null 2>&1; echo "topk $?"
+ncu --set full --clock-control none --import-source on -k regex:"k_tc_prep|k_list_sort" -s 3 -c 3 -o gpurun_out/r02/full_prep $CMD > /dev/null 2>&1; echo "prep $?"
 python tools/cfg_times.py C1 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_prim -s 3 -c 2 -o gpurun_out/r02/full_prim python tools/cfg_times.py C1 > /dev/null 2>&1; echo "prim $?"
 ncu --set full --clock-control none --import-source on -k regex:"k_validate_square|k_scan_weights_topk|k_fill" -s 6 -c 3 -o gpurun_out/r02/full_c3 python tools/cfg_times.py C3 > /dev/null 2>&1; echo "c3 $?"
-for r in fill tcf list topk prim c3; do python tools/ncu_summary.py gpurun_out/r02/full_$r.ncu-rep > gpurun_out/r02/r02_$r.metrics.txt 2>&1; done
+for r in fill tcf list topk prep prim c3; do python tools/ncu_summary.py gpurun_out/r02/full_$r.ncu-rep > gpurun_out/r02/r02_$r.metrics.txt 2>&1; done
 ls -la gpurun_out/r02
