@@ -480,6 +480,11 @@ appd_status sort_keys_u32_bits(appd_ctx* c, const unsigned* in, unsigned* out, i
 appd_status sort_pairs_i32(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count);
 appd_status sort_pairs_i32_bits(appd_ctx* c, const int* kin, int* kout, const int* vin, int* vout, int64_t count,
                                 int end_bit);
+// component labels (< 2^bits, bits <= 8) -> sorted labels sc and positions perm (stable),
+// plus the label ranges cstart / cend and per position rs / re, in one cooperative launch
+// (APPD_ERR_UNSUPPORTED for wider labels)
+appd_status sort_components(appd_ctx* c, const int* comp, int64_t n, int bits, int* sc, int* perm, int* cstart,
+                            int* cend, int* rs, int* re);
 appd_status sort_keys_u64_bits64(appd_ctx* c, const u64* in, u64* out, int64_t count, int begin_bit, int end_bit);
 appd_status exclusive_scan_i32(appd_ctx* c, const int* in, int* out, int64_t count);
 

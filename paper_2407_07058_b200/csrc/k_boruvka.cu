@@ -953,6 +953,12 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     if (!(mutual && c > o)) mstkeys[atomicAdd(counters, 1)] = compbest[c];
   }
   grid.sync();
+  // (compbest is not read after the hook and mutual phases: the next round's lookup can
+  // start from KEY_NONE without a barrier of its own)
+  if (la.ckey) {
+    for (int i = tid; i < n; i += T) compbest[i] = KEY_NONE;
+    if (tid == 0) *la.count = 0u;
+  }
   // pointer jumping to the roots
   for (int c = tid; c < k; c += T) {
     int p = parent[c];
@@ -1011,21 +1017,26 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
   if (!la.ckey) return;
   // the next round's cache lookup (k_cache_lookup, k_rescan_select) on the final labels
   grid.sync();
-  for (int i = tid; i < n; i += T) compbest[i] = KEY_NONE;
-  if (tid == 0) *la.count = 0u;
-  grid.sync();
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     const int c = la.ccnt[i];
     const int ci = comp[i];
     int flag = 1;
     if (c > 0) {
-      for (int t = 0; t < c; t++) {
-        const int j = la.cj[(int64_t)i * la.K + t];
-        if (comp[j] != ci) {
-          atomicMin(compbest + ci, la.ckey[(int64_t)i * la.K + t]);
-          flag = 0;
-          break;
-        }
+      int t = 0;
+      if (la.K == 8 && c == 8) {  // the common case: all eight labels loaded at once
+        const int4* cj4 = reinterpret_cast<const int4*>(la.cj + (int64_t)i * 8);
+        const int4 a = cj4[0], b = cj4[1];
+        const int cc[8] = {comp[a.x], comp[a.y], comp[a.z], comp[a.w], comp[b.x], comp[b.y], comp[b.z], comp[b.w]};
+        t = 8;
+#pragma unroll
+        for (int u = 7; u >= 0; u--)
+          if (cc[u] != ci) t = u;  // the first cached entry in another component
+      } else {
+        while (t < c && comp[la.cj[(int64_t)i * la.K + t]] == ci) t++;
+      }
+      if (t < c) {
+        atomicMin(compbest + ci, la.ckey[(int64_t)i * la.K + t]);
+        flag = 0;
       }
       if (flag && c == n - 1) flag = 0;  // every other point cached, none eligible
     }

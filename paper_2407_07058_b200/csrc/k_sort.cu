@@ -40,6 +40,10 @@ struct CoopSortArgs {
   int n, begin_bit, passes, dbits;
   unsigned* cnt;   // [1 << dbits][G]
   unsigned* dtot;  // [1 << dbits]
+  int iota_vals;   // values = input index (vin ignored)
+  // optional epilogue for component labels (keys = labels, sorted): first / end position
+  // of every label, and per position the range of its own label
+  int *cstart, *cend, *rs, *re;
 };
 
 template <typename K>
@@ -133,7 +137,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
       if (valid) {
         key = src[i];
         d = digit(key);
-        if (vsrc) val = vsrc[i];
+        if (a.iota_vals && p == 0) val = i;
+        else if (vsrc) val = vsrc[i];
       }
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int leader = __ffs(peers) - 1;
@@ -148,18 +153,33 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
           }
           pos = __shfl_sync(peers, pos, leader) + rank;
           dst[pos] = key;
-          if (vsrc) vdst[pos] = val;
+          if (vsrc || a.iota_vals) vdst[pos] = val;
         }
         __syncthreads();
       }
     }
     grid.sync();
   }
+  if (a.cstart) {  // label ranges (k_comp_ranges, k_row_ranges)
+    const int64_t tid64 = (int64_t)b * kSortThreads + tid, nt = (int64_t)G * kSortThreads;
+    for (int64_t q = tid64; q < a.n; q += nt) {
+      const int cq = (int)a.kout[q];
+      if (q == 0 || (int)a.kout[q - 1] != cq) a.cstart[cq] = (int)q;
+      if (q == a.n - 1 || (int)a.kout[q + 1] != cq) a.cend[cq] = (int)q + 1;
+    }
+    grid.sync();
+    for (int64_t q = tid64; q < a.n; q += nt) {
+      const int cq = (int)a.kout[q];
+      a.rs[q] = a.cstart[cq];
+      a.re[q] = a.cend[cq];
+    }
+  }
 }
 
 template <typename K>
 appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* vout, int64_t count, int begin_bit,
-                      int end_bit) {
+                      int end_bit, bool iota_vals = false, int* cstart = nullptr, int* cend = nullptr,
+                      int* rs = nullptr, int* re = nullptr) {
   if (count <= 0) return APPD_OK;
   if (count > (int64_t)1 << 30) return fail(c, APPD_ERR_UNSUPPORTED, "sort of %lld keys", (long long)count);
   const int bits = std::max(1, end_bit - begin_bit);
@@ -167,7 +187,8 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   const int dbits = (bits + passes - 1) / passes;
   const int ND = 1 << dbits;
   const int G = c->sm_count;
-  const size_t kb = (sizeof(K) * (size_t)count + 255) & ~(size_t)255, vb = vin ? (sizeof(int) * (size_t)count + 255) & ~(size_t)255 : 0;
+  const bool vals = vin || iota_vals;
+  const size_t kb = (sizeof(K) * (size_t)count + 255) & ~(size_t)255, vb = vals ? (sizeof(int) * (size_t)count + 255) & ~(size_t)255 : 0;
   char* w = (char*)ws(c, S_SORT, kb + vb + sizeof(unsigned) * ((size_t)ND * G + ND) + 256);
   if (!w) return fail(c, APPD_ERR_OUT_OF_MEMORY, "sort workspace (%lld keys)", (long long)count);
   CoopSortArgs<K> a;
@@ -176,7 +197,12 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   a.kbuf = reinterpret_cast<K*>(w);
   a.vin = vin;
   a.vout = vout;
-  a.vbuf = vin ? reinterpret_cast<int*>(w + kb) : nullptr;
+  a.vbuf = vals ? reinterpret_cast<int*>(w + kb) : nullptr;
+  a.iota_vals = iota_vals ? 1 : 0;
+  a.cstart = cstart;
+  a.cend = cend;
+  a.rs = rs;
+  a.re = re;
   a.n = (int)count;
   a.begin_bit = begin_bit;
   a.passes = passes;
@@ -220,6 +246,13 @@ appd_status path_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
 }
 
 }  // namespace
+
+appd_status sort_components(appd_ctx* c, const int* comp, int64_t n, int bits, int* sc, int* perm, int* cstart,
+                            int* cend, int* rs, int* re) {
+  if (bits > kMaxDigitBits) return APPD_ERR_UNSUPPORTED;
+  return coop_sort<unsigned>(c, reinterpret_cast<const unsigned*>(comp), reinterpret_cast<unsigned*>(sc), nullptr, perm,
+                             n, 0, bits, true, cstart, cend, rs, re);
+}
 
 appd_status sort_keys_u64_bits64(appd_ctx* c, const u64* in, u64* out, int64_t count, int begin_bit, int end_bit) {
   return path_sort<u64>(c, in, out, nullptr, nullptr, count, begin_bit, end_bit);

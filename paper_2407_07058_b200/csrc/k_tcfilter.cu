@@ -570,6 +570,7 @@ struct PrepArgs {
   unsigned *seg_maxlen, *seg_maxerr;
   u64* bad;
   unsigned long long* dbg;  // development builds: %globaltimer after each phase (CTA 0)
+  const int* perm;          // pack_tile: point at position p (nullptr: identity)
   InitList init;
 };
 __device__ __forceinline__ void prep_mark(const PrepArgs& a, int i) {
@@ -618,7 +619,7 @@ __device__ __forceinline__ float pack_tile(const PrepArgs& a, float scale, bool 
     const int pl = (int)(p % 128), g8 = pl / 8, r = pl % 8;
     uint4* ga = reinterpret_cast<uint4*>(a.YA + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
     uint4* gb = reinterpret_cast<uint4*>(a.YB + gidx * 128 * K + (int64_t)g8 * (K / 8) * 64 + r * 8);
-    const float* xi = a.X + (real ? p : 0) * d;
+    const float* xi = a.X + (real ? (a.perm ? a.perm[p] : p) : 0) * d;
     for (int g = gw; g < G; g += GW) {
       const int k8 = 8 * g;
       float xv[8];
@@ -832,6 +833,30 @@ __global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
   prep_mark(a, 5);
 }
 
+// the packing of a later pass (points in component order): the same tiles as phase 4 of
+// k_tc_prep, the scale already on the device; seg_maxlen / seg_maxerr / maxerr zeroed
+// before (k_init)
+__global__ void __launch_bounds__(256, 3) k_pack_tiles(const PrepArgs a, const TcScale* __restrict__ sc) {
+  __shared__ float s_part[8][32], e_part[8][32];
+  const int lane = threadIdx.x & 31;
+  const bool vec = (a.d & 3) == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0;
+  const float scale = sc->scale;
+  const int G = a.dk / 8, GW = G < 8 ? G : 8, sets = 8 / GW, PT = 32 * sets;
+  float emax = 0.0f;
+  for (int64_t p0 = (int64_t)blockIdx.x * PT; p0 < a.npad; p0 += (int64_t)gridDim.x * PT)
+    emax = fmaxf(emax, pack_tile(a, scale, vec, p0, G, GW, sets, s_part, e_part));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+  __shared__ float wmax[8];
+  if (lane == 0) wmax[threadIdx.x >> 5] = emax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.0f;
+    for (int t = 0; t < 8; t++) m = fmaxf(m, wmax[t]);
+    if (m > 0.0f) atomicMax(a.maxerr, __float_as_uint(m));
+  }
+}
+
 // centre, scale (+ round 0's packing when cooperative), the caller's initialisations and
 // the validation verdict
 static appd_status launch_prepare(appd_ctx* c, const float* X, TcState* st, const InitList* init, u64* bad) {
@@ -889,6 +914,7 @@ static appd_status launch_prepare(appd_ctx* c, const float* X, TcState* st, cons
     a.seg_maxerr = reinterpret_cast<unsigned*>(st->seg_maxerr);
     a.bad = bad;
     a.dbg = nullptr;
+    a.perm = nullptr;
     a.init = L;
     static const bool times = dev_env("APPD_PREP_TIMES") != nullptr;
     if (times) a.dbg = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 64));
@@ -1039,21 +1065,35 @@ appd_status tcf_prepare(appd_ctx* c, const float* X, int64_t n, int64_t d, TcSta
 }
 
 // xt: the d x npad fp32 transpose of the packed order for the exact kernels (nullptr:
-// not needed)
-static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X, float* xt) {
-  const int64_t n = st->n;
-  APPD_CUDA(c, cudaMemsetAsync(st->maxerr, 0, sizeof(unsigned), c->stream));
-  k_pack<<<(unsigned)std::min<int64_t>((st->npad + 127) / 128, (int64_t)c->sm_count * 16), 128, 0, c->stream>>>(X, n, (int)st->d, st->dk, st->K, st->perm, st->center, st->dscale,
-                                                  st->npad, (__half*)st->YA, (__half*)st->YB, st->nrm, st->len,
-                                                  st->err, st->maxerr);
+// not needed); extra: the caller's initialisations, in the same launch as the pack's own
+static appd_status tcf_pack(appd_ctx* c, TcState* st, const float* X, float* xt, const InitList* extra = nullptr) {
+  InitList L;
+  if (extra) L = *extra;
+  L.add(st->maxerr, 1, 0, 0);
+  L.add(st->seg_maxlen, st->npad / TC_TMG, 0, 0);
+  L.add(st->seg_maxerr, st->npad / TC_TMG, 0, 0);
+  k_init<<<c->sm_count * 2, 256, 0, c->stream>>>(L);
   APPD_LAUNCHED(c);
-  if (xt) {
-    const dim3 tg((unsigned)(st->npad / 32), (unsigned)((st->d + 31) / 32));
-    k_transpose_perm<<<tg, dim3(32, 8), 0, c->stream>>>(X, n, (int)st->d, st->perm, st->npad, xt);
-    APPD_LAUNCHED(c);
-  }
-  k_seg_maxlen<<<(unsigned)std::min<int64_t>(c->sm_count * 8, (st->npad / TC_TMG + 7) / 8), 256, 0, c->stream>>>(
-      st->len, st->err, st->npad / TC_TMG, st->seg_maxlen, st->seg_maxerr);
+  PrepArgs a;
+  memset(&a, 0, sizeof a);
+  a.X = X;
+  a.n = st->n;
+  a.npad = st->npad;
+  a.d = (int)st->d;
+  a.dk = st->dk;
+  a.K = st->K;
+  a.center = st->center;
+  a.YA = (__half*)st->YA;
+  a.YB = (__half*)st->YB;
+  a.nrm = st->nrm;
+  a.len = st->len;
+  a.err = st->err;
+  a.maxerr = st->maxerr;
+  a.xt = xt;
+  a.seg_maxlen = reinterpret_cast<unsigned*>(st->seg_maxlen);
+  a.seg_maxerr = reinterpret_cast<unsigned*>(st->seg_maxerr);
+  a.perm = st->perm;
+  k_pack_tiles<<<c->sm_count * 3, 256, 0, c->stream>>>(a, st->dscale);
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -1138,6 +1178,24 @@ static int bits_for(int64_t v) {
   int b = 1;
   while ((int64_t)1 << b < v) b++;
   return b;
+}
+
+// points sorted by component (stable: by index inside a component), the permutation, and
+// the component ranges: one cooperative launch for k <= 256 components, else gather, the
+// library sort and two range kernels
+static appd_status sort_by_component(appd_ctx* c, TcState* st, const int* comp, int64_t k, int grid_n) {
+  const int64_t n = st->n;
+  const int bits = bits_for(k + 1);
+  appd_status s = sort_components(c, comp, n, bits, st->sc, st->perm, st->cstart, st->cend, st->rs, st->re);
+  if (s != APPD_ERR_UNSUPPORTED) return s;
+  k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
+  APPD_LAUNCHED(c);
+  if ((s = sort_pairs_i32_bits(c, st->keys, st->sc, st->keys + n + 1, st->perm, n, bits))) return s;
+  k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
+  APPD_LAUNCHED(c);
+  k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
+  APPD_LAUNCHED(c);
+  return APPD_OK;
 }
 
 // sort the listed (chunk << 32 | row) entries by chunk and re-check them exactly:
@@ -1236,22 +1294,17 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
   if (round == 0) {
     if (!packed && (s = launch_iota(c, st->perm, n))) return s;
   } else {
-    k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
-    APPD_LAUNCHED(c);
-    if ((s = sort_pairs_i32_bits(c, st->keys, st->sc, st->keys + n + 1, st->perm, n, bits_for(k + 1)))) return s;
-    k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
-    APPD_LAUNCHED(c);
-    k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
-    APPD_LAUNCHED(c);
+    if ((s = sort_by_component(c, st, comp, k, grid_n))) return s;
   }
   // round 0 of the cache: the permutation is the identity, so the transpose is the
   // original-order one the exact row kernel reads
   if (!packed) {
-    if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp))) return s;
+    InitList init;  // (UB ~3.4e38: permissive)
+    init.add(st->UB, st->npad, 0x7F7F7F7Fu, 0);
+    init.add(st->counters, 16, 0, 0);
+    init.add(st->rowflag, n, 0, 0);
+    if ((s = tcf_pack(c, st, X, (cache && round == 0) ? st->XT : st->XTp, &init))) return s;
     host_mark("tcf_round: pack queued");
-    APPD_CUDA(c, cudaMemsetAsync(st->UB, 0x7F, sizeof(unsigned) * st->npad, c->stream));  // ~3.4e38
-    APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
-    APPD_CUDA(c, cudaMemsetAsync(st->rowflag, 0, sizeof(int) * n, c->stream));
   }
   TcParams P;
   fill_scan_params(st, &P);
@@ -1359,18 +1412,15 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   const int grid_n = (int)std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 8);
   appd_status s;
   *listed_overflow = false;
-  k_gather_comp<<<grid_n, 256, 0, c->stream>>>(comp, n, st->keys, st->keys + n + 1);
-  APPD_LAUNCHED(c);
-  if ((s = sort_pairs_i32_bits(c, st->keys, st->sc, st->keys + n + 1, st->perm, n, bits_for(k + 1)))) return s;
-  k_comp_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend);
-  APPD_LAUNCHED(c);
-  k_row_ranges<<<grid_n, 256, 0, c->stream>>>(st->sc, n, st->cstart, st->cend, st->rs, st->re);
-  APPD_LAUNCHED(c);
-  if ((s = tcf_pack(c, st, X, nullptr))) return s;  // the component-matrix kernels read X
-  APPD_CUDA(c, cudaMemsetAsync(st->counters, 0, 64, c->stream));
+  if ((s = sort_by_component(c, st, comp, k, grid_n))) return s;
   unsigned* CUB = st->compUB;  // k x k <= 128 x 128 words (the buffer holds n >= k^2 words or more)
-  APPD_CUDA(c, cudaMemsetAsync(CUB, 0x7F, sizeof(unsigned) * k * k, c->stream));  // ~3.4e38: permissive
-  APPD_CUDA(c, cudaMemsetAsync(WCM, 0xFF, sizeof(u64) * k * k, c->stream));
+  {
+    InitList init;
+    init.add(st->counters, 16, 0, 0);
+    init.add(CUB, k * k, 0x7F7F7F7Fu, 0);  // ~3.4e38: permissive
+    init.add(WCM, k * k, KEY_NONE, 1);
+    if ((s = tcf_pack(c, st, X, nullptr, &init))) return s;  // the component-matrix kernels read X
+  }
   TcParams P;
   fill_scan_params(st, &P);
   P.round0 = 0;
