@@ -27,6 +27,7 @@
 //   k_rescan_select  a row with no eligible cached entry needs a re-scan only if its
 //                    K-th key is below its component's current best (else all of its
 //                    uncached edges are heavier than an edge the component already has).
+#include <cfloat>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -1292,6 +1293,19 @@ __global__ void k_seg_comp(const int* __restrict__ sc, int n, int nseg, int2* __
 // segments are sorted by component: stream each row's stored maxima in order (16 loads
 // in flight), keep the running maximum of the current component's full segments and
 // flush its bound when the component changes
+// U consecutive stored segments of one row (stride 512 floats, tm_index) from ptr; the
+// first `left` of them are real, the rest -inf.  A full batch (warp-uniform) is U loads
+// at immediate offsets; the lanes of invalid rows read a valid row and are masked later
+template <int U>
+__device__ __forceinline__ void load_segs(const float* __restrict__ ptr, int left, float (&v)[U]) {
+  if (left >= U) {
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = __ldcs(ptr + u * 512);
+  } else {
+#pragma unroll
+    for (int u = 0; u < U; u++) v[u] = u < left ? __ldcs(ptr + u * 512) : -INFINITY;
+  }
+}
 constexpr int CM_SPLIT = 4;  // warps per 32-row group, each over a quarter of the segments
 __global__ void k_cm_rowub(CmParams P) {
   const int lane = threadIdx.x & 31;
@@ -1305,6 +1319,9 @@ __global__ void k_cm_rowub(CmParams P) {
     const int part = (int)(task % CM_SPLIT);
     const int p = p0 + lane;
     const bool valid = p < P.p_end;
+    // this row's stored maxima: segment s at tm_row[s * 512] (tm_index; one base per row,
+    // immediate offsets per segment in the unrolled loads)
+    const float* tm_row = P.TM + tm_index(0, min(p, P.p_end - 1), P.nseg);
     const int C = valid ? P.sc[p] : -1;
     const bool uni = __all_sync(0xffffffffu, C == __shfl_sync(0xffffffffu, C, 0));
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
@@ -1337,8 +1354,7 @@ __global__ void k_cm_rowub(CmParams P) {
       float m = -INFINITY;
       for (int s0 = s; s0 < e; s0 += U) {
         float v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = (valid && s0 + u < e) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+        load_segs<U>(tm_row + (int64_t)s0 * 512, e - s0, v);
 #pragma unroll
         for (int u = 0; u < U; u++) m = fmaxf(m, v[u]);
       }
@@ -1363,6 +1379,7 @@ __global__ void k_cm_filter(CmParams P) {
     const int part = (int)(task % CM_SPLIT);
     const int p = p0 + lane;
     const bool valid = p < P.p_end;
+    const float* tm_row = P.TM + tm_index(0, min(p, P.p_end - 1), P.nseg);
     const int C = valid ? P.sc[p] : 0;
     const float ni = valid ? P.nrm[p] : 0.0f, li = valid ? P.len[p] : 0.0f;
     const float dl = em_delta2(valid ? P.err[p] : 0.0f, *P.maxerr);
@@ -1386,13 +1403,14 @@ __global__ void k_cm_filter(CmParams P) {
           if (D != C) ub = fmaxf(ub, __uint_as_float(P.CUB[(int64_t)C * P.k + D]));
         thr = em_thr(P.em, ub, ni, li, maxlen_, dl);
       }
+      const float thr_c = fmaxf(thr, -FLT_MAX);  // (-inf never passes: one compare per value)
       for (int s0 = s; s0 < e; s0 += U) {
         float v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = (valid && s0 + u < e) ? __ldcs(P.TM + tm_index(s0 + u, p, P.nseg)) : -INFINITY;
+        load_segs<U>(tm_row + (int64_t)s0 * 512, e - s0, v);
         unsigned mask = 0;
 #pragma unroll
-        for (int u = 0; u < U; u++) mask |= (v[u] >= thr && v[u] > -INFINITY) ? 1u << u : 0u;
+        for (int u = 0; u < U; u++) mask |= v[u] >= thr_c ? 1u << u : 0u;
+        if (!valid) mask = 0u;
         unsigned any = __reduce_or_sync(0xffffffffu, mask);
         // chunk-major emission: for each flagged segment and chunk, the warp's rows in
         // lane order (consecutive rows, mostly one component), so that the chunk runs of

@@ -371,6 +371,7 @@ __global__ void k_filter_tiles(ExactParams E) {
     if (valid && E.compUB) ub = fminf(ub, __uint_as_float(E.compUB[E.comp[E.perm[p]]]));
     const float ni = valid ? E.nrm[p] : 0.0f, li = valid ? E.len[p] : 0.0f;
     const float ei = valid ? E.err[p] : 0.0f, emax = *E.maxerr;
+    const float* tm_row = E.TM + tm_index(0, valid ? p : E.p_begin, E.nseg);  // segment s at tm_row[s * 512]
     const float thr_min = valid ? em_thr(E.em, ub, ni, li, E.tsc->maxlen, em_delta2(ei, emax)) : INFINITY;
     bool flagged = false;
     constexpr int U = 8;  // segments per batch: U independent coalesced loads in flight
@@ -378,7 +379,7 @@ __global__ void k_filter_tiles(ExactParams E) {
       float v[U];
 #pragma unroll
       for (int u = 0; u < U; u++)
-        v[u] = (valid && t0 + u < E.nseg) ? __ldcs(E.TM + tm_index(t0 + u, p, E.nseg)) : -INFINITY;
+        v[u] = (valid && t0 + u < E.nseg) ? __ldcs(tm_row + (int64_t)(t0 + u) * 512) : -INFINITY;
       bool any = false;
 #pragma unroll
       for (int u = 0; u < U; u++) any |= v[u] >= thr_min && v[u] > -INFINITY;
