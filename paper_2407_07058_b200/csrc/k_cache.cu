@@ -74,7 +74,7 @@ constexpr int TK_PARTS = 4;
 constexpr int TK_BATCH = 32;  // chunk maxima per batch (4 x 128-bit loads of fp16)
 constexpr int TK_SEL = 16;    // kept chunks per (row, quarter) in shared memory
 constexpr int TK_RG = 4;      // flagged groups re-read together
-constexpr int TK_STAGES = 4;  // cp.async ring depth (batches; 3 in flight while one is processed)
+constexpr int TK_STAGES = 3;  // cp.async ring depth (batches; 2 in flight while one is processed)
 
 // 16-byte asynchronous global -> shared copy (L2 only); src_bytes = 0 zero-fills
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -159,9 +159,9 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
                                                              float* __restrict__ UBK, unsigned* __restrict__ list,
                                                              unsigned* __restrict__ count, unsigned cap,
                                                              unsigned* __restrict__ cand_cnt, int ngq) {
-  extern __shared__ float sgm[];                  // [TK_PARTS][ngq][32] 8-chunk group maxima
+  extern __shared__ __align__(16) __half sgm[];   // [TK_PARTS][ngq][32] 8-chunk group minima of D' (fp16: exact)
   __shared__ float stop[TK_PARTS][K][32];         // per-quarter top-K lists for the merges
-  __shared__ float sval[TK_PARTS][TK_SEL][32];    // kept chunks: value
+  __shared__ __half sval[TK_PARTS][TK_SEL][32];   // kept chunks: stored D' (fp16: exact)
   __shared__ unsigned short sidx[TK_PARTS][TK_SEL][32];  //   and chunk index
   __shared__ int slost[32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -172,9 +172,10 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
   const int cb = 8 * g0, cend = min(nch, 8 * g1);  // this warp's chunk range (whole 8-chunk groups)
   const int nbat = (cend - cb + TK_BATCH - 1) / TK_BATCH;
   const int ng = (cend - cb + 7) / 8;               // 8-chunk groups of this quarter (<= ngq)
-  float* gm = sgm + (size_t)w * ngq * 32 + lane;    // gm[g * 32]
+  __half* gm = sgm + (size_t)w * ngq * 32 + lane;   // gm[g * 32]
   // cp.async ring after the group maxima: [TK_PARTS][TK_STAGES][U8][32] uint4
-  uint4* ring = reinterpret_cast<uint4*>(sgm + (size_t)TK_PARTS * ngq * 32) + (size_t)w * TK_STAGES * U8 * 32 + lane;
+  // (ngq * 32 halves per warp: a multiple of 16 bytes)
+  uint4* ring = reinterpret_cast<uint4*>(sgm + (size_t)TK_PARTS * ((ngq + 1) & ~1) * 32) + (size_t)w * TK_STAGES * U8 * 32 + lane;
   for (int p0 = p_begin + 32 * blockIdx.x; p0 < p_end; p0 += 32 * gridDim.x) {
     const int p = p0 + lane;
     const bool valid = p < p_end;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
           m = fminf(__low2float(t), __high2float(t));
         }
         const int g = b * (TK_BATCH / 8) + q;
-        if (g < ng) gm[g * 32] = m;
+        if (g < ng) gm[g * 32] = __float2half_rn(m);  // (m is an fp16 value or +inf: exact)
         bd = fminf(bd, m);
       }
       // top-K of BATCH maxima (lower bounds): K batches hold K distinct chunks
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
     float tcap = valid ? -INFINITY : INFINITY;
     if (valid && gK > -INFINITY) tcap = fminf(gK, em_thr(em, em_upper(em, ni - 2.0f * gK, ni, li, maxlen, dl), ni, li, maxlen, dl));
     auto flagged = [&](int g) {
-      const float dg = gm[g * 32];
+      const float dg = __half2float(gm[g * 32]);
       return dg < INFINITY && tm_up(dg, ni) >= tcap;
     };
     // ---- re-read the flagged groups (bit masks, ng <= 128): keep chunks >= t,
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
         for (int u = 0; u < 8; u++)
           if (vv[r][u] < INFINITY && tm_up(vv[r][u], ni) >= tcap) {
             if (kept < TK_SEL) {
-              sval[w][kept][lane] = vv[r][u];
+              sval[w][kept][lane] = __float2half_rn(vv[r][u]);
               sidx[w][kept][lane] = (unsigned short)(cb + 8 * gg[r] + u);
             }
             kept++;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
     // ---- list the kept chunks passing thrK: count, one warp allocation, write
     unsigned mine = 0;
     if (kept <= TK_SEL) {
-      for (unsigned t = 0; t < kept; t++) mine += tm_up(sval[w][t][lane], ni) >= thr;
+      for (unsigned t = 0; t < kept; t++) mine += tm_up(__half2float(sval[w][t][lane]), ni) >= thr;
     } else {
       for (int g = 0; g < ng; g++) {
         if (!flagged(g)) continue;
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(32 * TK_PARTS) k_topk_scan(const __half* __res
     bool lost = false;
     if (kept <= TK_SEL) {
       for (unsigned t = 0; t < kept; t++)
-        if (tm_up(sval[w][t][lane], ni) >= thr) {
+        if (tm_up(__half2float(sval[w][t][lane]), ni) >= thr) {
           if (slot < cap) list[slot] = ((unsigned)sidx[w][t][lane] << LIST_SHIFT) | (unsigned)p;
           else lost = true;
           slot++;
@@ -370,7 +371,7 @@ appd_status launch_topk_scan(appd_ctx* c, int K, const __half* TM32, int nch, in
   const int grid = std::min(c->sm_count * 16, (rows + 31) / 32);
   // 8-chunk groups per quarter: the largest quarter has ceil(ceil(nch/8)/TK_PARTS)
   const int ngq = ((nch + 7) / 8 + TK_PARTS - 1) / TK_PARTS;
-  const size_t smem = sizeof(float) * TK_PARTS * ngq * 32 + sizeof(uint4) * TK_PARTS * TK_STAGES * (TK_BATCH / 8) * 32;
+  const size_t smem = sizeof(__half) * TK_PARTS * ((ngq + 1) & ~1) * 32 + sizeof(uint4) * TK_PARTS * TK_STAGES * (TK_BATCH / 8) * 32;
   if (ngq > 128) return fail(c, APPD_ERR_UNSUPPORTED, "top-K scan: %d chunks per row", nch);
 #define APPD_TOPK_SCAN(KK)                                                                                     \
   do {                                                                                                         \
