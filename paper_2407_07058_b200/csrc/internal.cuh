@@ -437,6 +437,7 @@ struct LookupArgs {
   int* need = nullptr;
   unsigned* count = nullptr;
   int* list = nullptr;
+  unsigned long long* marks = nullptr;  // development builds: per-phase %globaltimer
 };
 // hook + mutual + jump + scan + relabel (+ the lookup) in one cooperative launch
 // (APPD_ERR_UNSUPPORTED if the device cannot co-schedule it: the caller then runs the

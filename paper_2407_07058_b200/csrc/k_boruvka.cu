@@ -920,6 +920,14 @@ appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent,
 // the same operations in the same order, one launch instead of six.  newid[k] = roots.
 // ---------------------------------------------------------------------------
 constexpr int kContractThreads = 1024;
+// development builds (APPD_MARKS): %globaltimer after each phase, CTA 0 (LookupArgs.marks)
+__device__ __forceinline__ void contract_mark(const LookupArgs& la, int i) {
+  if (la.marks && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    la.marks[i] = t;
+  }
+}
 __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__ compbest, int k,
                                                              int* __restrict__ comp, int n, int shift,
                                                              int* __restrict__ link, int* __restrict__ parent,
@@ -928,6 +936,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
                                                              int* __restrict__ blocksum, LookupArgs la) {
   cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
+  contract_mark(la, 0);
   // hook: the component at the other end of each component's lightest edge
   for (int c = tid; c < k; c += T) {
     const u64 key = compbest[c];
@@ -941,6 +950,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     link[c] = (cu == c) ? cv : cu;
   }
   grid.sync();
+  contract_mark(la, 1);
   // mutual pairs: the smaller id is the root, the shared edge is recorded once
   for (int c = tid; c < k; c += T) {
     const int o = link[c];
@@ -953,6 +963,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     if (!(mutual && c > o)) mstkeys[atomicAdd(counters, 1)] = compbest[c];
   }
   grid.sync();
+  contract_mark(la, 2);
   // (compbest is not read after the hook and mutual phases: the next round's lookup can
   // start from KEY_NONE without a barrier of its own)
   if (la.ckey) {
@@ -971,6 +982,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     flags[c] = p == c ? 1 : 0;
   }
   grid.sync();
+  contract_mark(la, 3);
   // exclusive scan of the flags: block b owns [b S, (b+1) S)
   __shared__ int wsum[kContractThreads / 32];
   __shared__ int carry_s;
@@ -1008,15 +1020,18 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
   grid.sync();
+  contract_mark(la, 4);
   const int off = blocks_before(blocksum);
   for (int i = lo + threadIdx.x; i < hi; i += kContractThreads) newid[i] += off;
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) newid[k] = off + carry_s;
   grid.sync();
+  contract_mark(la, 5);
   // relabel the points
   for (int i = tid; i < n; i += T) comp[i] = newid[parent[comp[i]]];
   if (!la.ckey) return;
   // the next round's cache lookup (k_cache_lookup, k_rescan_select) on the final labels
   grid.sync();
+  contract_mark(la, 6);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     const int c = la.ccnt[i];
     const int ci = comp[i];
@@ -1035,7 +1050,10 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
         while (t < c && comp[la.cj[(int64_t)i * la.K + t]] == ci) t++;
       }
       if (t < c) {
-        atomicMin(compbest + ci, la.ckey[(int64_t)i * la.K + t]);
+        // (most rows of a component lose: reading the current minimum first skips their
+        // atomics; in the last rounds 64K rows hit a few dozen components)
+        const u64 key = la.ckey[(int64_t)i * la.K + t];
+        if (key < __ldcg(compbest + ci)) atomicMin(compbest + ci, key);
         flag = 0;
       }
       if (flag && c == n - 1) flag = 0;  // every other point cached, none eligible
@@ -1043,6 +1061,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     la.need[i] = flag;
   }
   grid.sync();
+  contract_mark(la, 7);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     if (!la.need[i]) continue;
     const int c = la.ccnt[i];
@@ -1073,8 +1092,19 @@ appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, in
   LookupArgs la = look ? *look : LookupArgs{};
   void* args[] = {&compbest, &kk, &comp, &nn, &shift, &link, &parent, &mstkeys, &counters, &flags, &newid, &blocksum,
                   &la};
+  static const bool marks = dev_env("APPD_MARKS") != nullptr;
+  if (marks) la.marks = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 128));
   APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract, grid, kContractThreads, args, 0, c->stream));
   c->launches++;
+  if (marks && la.marks) {
+    unsigned long long h[10] = {};
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h, la.marks, sizeof h, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[contract] k %lld grid %d:", (long long)k, grid);
+    for (int i = 1; i < 9 && h[i]; i++) fprintf(stderr, " %.1f", (h[i] - h[i - 1]) * 1e-3);
+    fprintf(stderr, " us\n");
+    cudaMemset(la.marks, 0, 128);
+  }
   return APPD_OK;
 }
 
