@@ -361,6 +361,14 @@ void trace_end(appd_ctx* c);
   } while (0)
 
 #ifdef __CUDACC__
+// atomicMin that first reads the current value (L2): when many threads reduce onto few
+// addresses (component minima in the late rounds), most lose and skip the serialised atomic
+__device__ __forceinline__ void atomic_min_lt(unsigned long long* a, unsigned long long v) {
+  if (v < __ldcg(a)) atomicMin(a, v);
+}
+__device__ __forceinline__ void atomic_min_lt(unsigned* a, unsigned v) {
+  if (v < __ldcg(a)) atomicMin(a, v);
+}
 // sum of blocksum[0 .. blockIdx.x) for every thread of the block: warp 0 reduces with its
 // loads in flight (a serial loop over up to 147 earlier blocks was ~20 us of dependent
 // L2 latency in the last block of a cooperative scan)

@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(256) k_scan_weights(const float* __restrict__ 
       if (k != KEY_NONE) {
         int64_t j = (int64_t)(k & 0xFFFFFFFFull);
         u64 gkey = (k & 0xFFFFFFFF00000000ull) | tri_index(i, j);
-        atomicMin(compbest + ci, gkey);
+        atomic_min_lt(compbest + ci, gkey);
       }
     }
     __syncthreads();
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(256, 2)
             } else {
               const int64_t i = (int64_t)(best & 0xFFFFFFFFull);
               const u64 gkey = (((best >> 32) & 0x7FFFFFFFull) << 33) | tri_index(i, j);
-              atomicMin(compbest + (ROUND0 ? j : ccol[threadIdx.x]), gkey);
+              atomic_min_lt(compbest + (ROUND0 ? j : ccol[threadIdx.x]), gkey);
             }
           }
         }
@@ -583,14 +583,14 @@ __global__ void __launch_bounds__(256, 2)
       key = other < key ? other : key;
     }
     if (WIDE) {
-      if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) atomicMin(compbest + ri[a], key);
+      if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) atomic_min_lt(compbest + ri[a], key);
       continue;
     }
     if (tx == 0 && key != KEY_NONE && ri[a] < row0 + rows && ri[a] < n) {
       int64_t j = (int64_t)(key & 0xFFFFFFFFull);
       u64 d2bits = (key >> 32) & 0x7FFFFFFFull;
       u64 gkey = (d2bits << 33) | tri_index(ri[a], j);
-      atomicMin(compbest + cr[a], gkey);
+      atomic_min_lt(compbest + cr[a], gkey);
     }
   }
 }

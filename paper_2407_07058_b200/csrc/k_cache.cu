@@ -852,15 +852,15 @@ __global__ void __launch_bounds__(256, MODE == 0 ? 5 : 4) k_list_exact(ListParam
             const u64 other = __shfl_xor_sync(0xffffffffu, m, o);
             m = other < m ? other : m;
           }
-          if (lane == 0 && hb && m != KEY_NONE) atomicMin(L.WCM + (int64_t)wC * L.k + wD, m);
+          if (lane == 0 && hb && m != KEY_NONE) atomic_min_lt(L.WCM + (int64_t)wC * L.k + wD, m);
         } else if (has_pair) {
-          if (m != KEY_NONE) atomicMin(L.WCM + (int64_t)cC * L.k + cD, m);
+          if (m != KEY_NONE) atomic_min_lt(L.WCM + (int64_t)cC * L.k + cD, m);
         } else if (!uni) {
 #pragma unroll
           for (int a = 0; a < 4; a++)
 #pragma unroll
             for (int b = 0; b < 4; b++)
-              if (key[a][b] != KEY_NONE) atomicMin(L.WCM + (int64_t)Ca[a] * L.k + Dq[b], key[a][b]);
+              if (key[a][b] != KEY_NONE) atomic_min_lt(L.WCM + (int64_t)Ca[a] * L.k + Dq[b], key[a][b]);
         }
       }
       }  // 16 * warp < nb
@@ -997,7 +997,7 @@ __global__ void k_cache_lookup(int r0, int r1, int K, int n, const u64* __restri
       for (int t = 0; t < c; t++) {
         const int j = cj[(int64_t)i * K + t];
         if (comp[j] != ci) {
-          atomicMin(compbest + ci, ckey[(int64_t)i * K + t]);
+          atomic_min_lt(compbest + ci, ckey[(int64_t)i * K + t]);
           flag = 0;
           break;
         }
@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__
     if (threadIdx.x < RE_R && sri[threadIdx.x] >= 0) {
       u64 b = KEY_NONE;
       for (int w = 0; w < 8; w++) b = red[w][threadIdx.x] < b ? red[w][threadIdx.x] : b;
-      if (b != KEY_NONE) atomicMin(compbest + sci[threadIdx.x], b);
+      if (b != KEY_NONE) atomic_min_lt(compbest + sci[threadIdx.x], b);
     }
   };
   for (int item = i0; item < i1; item++) {
@@ -1334,9 +1334,9 @@ __global__ void k_cm_rowub(CmParams P) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) ub = fminf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
         if (lane == 0 && C >= 0 && ub < INFINITY)
-          atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
+          atomic_min_lt(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
       } else if (ub < INFINITY) {
-        atomicMin(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
+        atomic_min_lt(P.CUB + (int64_t)C * P.k + D, __float_as_uint(fmaxf(ub, 0.0f)));
       }
     };
     constexpr int U = 16;

@@ -453,7 +453,7 @@ __global__ void k_exact_tiles(ExactParams E) {
       const u64 other = __shfl_xor_sync(0xffffffffu, key, o);
       key = other < key ? other : key;
     }
-    if (lane == 0 && key != KEY_NONE) atomicMin(E.compbest + E.comp[oi], key);
+    if (lane == 0 && key != KEY_NONE) atomic_min_lt(E.compbest + E.comp[oi], key);
   }
   if (lane == 0 && done) atomicAdd(E.counters + 2, done);
 }
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256) k_exact_rows(ExactParams E) {
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int t = 0; t < (int)(blockDim.x >> 5); t++) best = red[t] < best ? red[t] : best;
-      if (best != KEY_NONE) atomicMin(E.compbest + E.comp[oi], best);
+      if (best != KEY_NONE) atomic_min_lt(E.compbest + E.comp[oi], best);
     }
     __syncthreads();
   }
