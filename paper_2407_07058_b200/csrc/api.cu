@@ -958,8 +958,11 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     }
     if (fused_lookup) {
       APPD_PUBLISH(c, c->pinned_small + 9, la.count, sizeof(unsigned));
-      if (use_tc && tc.topk) tc.lookup_pending = true;
-      else w_pending = true;
+      if (use_tc && tc.topk) {
+        tc.lookup_pending = true;
+      } else {
+        w_pending = true;
+      }
     } else {
       if (use_tc && tc.topk && c->opt.world == 1) {
         if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
@@ -974,7 +977,17 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     APPD_PUBLISH(c, &hostk[1], flags + (k - 1), sizeof(int));
     if (dbg) cudaEventRecord(c->ev[13], c->stream);
     host_mark("round queued, synchronising");
-    APPD_SYNC(c);
+    if (fused_lookup && use_tc && tc.topk) {
+      // the host waits for the round's results only; the next round's exact re-scan of the
+      // flagged rows (device list and count) runs meanwhile, so the GPU does not idle while
+      // the host wakes up and queues the rest of the next round
+      if ((s = publish_flush(c))) return s;
+      APPD_CUDA(c, cudaEventRecord(c->ev[7], c->stream));
+      if ((s = tcf_speculate_rows(c, &tc, comp, compbest))) return s;
+      APPD_CUDA(c, cudaEventSynchronize(c->ev[7]));
+    } else {
+      APPD_SYNC(c);
+    }
     host_mark("round synchronised");
     if (check_first_sync) {
       check_first_sync = false;

@@ -251,7 +251,9 @@ struct TcState {
   bool scanned = false;  // this round launched the tensor-core scan (ev[10] -> ev[11] bracket it)
   bool lookup_pending = false;  // next round's cache lookup already queued (tcf_lookup_async)
   bool r0_packed = false;       // the cooperative preparation also packed round 0 (identity order)
+  bool rows_spec = false;       // the next round's exact re-scan is already queued (tcf_speculate_rows)
 };
+appd_status tcf_speculate_rows(appd_ctx* c, TcState* st, const int* comp, u64* compbest);
 // device buffers to initialise before the first round, folded into one launch
 struct InitTask {
   void* p;

@@ -1076,11 +1076,13 @@ constexpr int RE_R = 16, RE_COLS = 256;
 template <bool FULL>  // FULL: d % 64 == 0 (no coordinate guards in the inner loop)
 __global__ void __launch_bounds__(256, 2) k_rows_exact(const float* __restrict__ XT, int64_t ldx, int n, int d,
                                                       const int* __restrict__ rows, const unsigned* __restrict__ nrows,
-                                                      const int* __restrict__ comp, u64* __restrict__ compbest) {
+                                                      const int* __restrict__ comp, u64* __restrict__ compbest,
+                                                      int max_rows) {
   extern __shared__ float xr[];  // [d][RE_R]
   __shared__ u64 red[8][RE_R];
   __shared__ int sri[RE_R], sci[RE_R];
   const int nr = (int)*nrows;
+  if (nr > max_rows) return;  // (a speculative launch whose rows need the tensor-core pass)
   const int ngroups = (nr + RE_R - 1) / RE_R;
   const int nblk = (n + RE_COLS - 1) / RE_COLS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1182,10 +1184,10 @@ appd_status launch_rows_exact(appd_ctx* c, const float* XT, int64_t ldx, int n, 
   const size_t smem = (size_t)d * RE_R * 4;
   if (d % 64 == 0) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_rows_exact<true><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
+    k_rows_exact<true><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest, max_rows);
   } else {
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_rows_exact<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_rows_exact<false><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest);
+    k_rows_exact<false><<<grid, 256, smem, c->stream>>>(XT, ldx, n, d, rows, nrows, comp, compbest, max_rows);
   }
   APPD_LAUNCHED(c);
   return APPD_OK;

@@ -1244,6 +1244,17 @@ static appd_status exact_list(appd_ctx* c, TcState* st, const float* X, int mode
   return launch_list_exact(c, mode, L, nullptr, run_nb, item_start);
 }
 
+// Queue the exact re-scan of the next round's flagged rows BEFORE the round's host
+// synchronisation (the lookup fused into the contraction left their list and count on the
+// device): the GPU works while the host wakes up.  The kernel does nothing if the rows
+// turn out to need the tensor-core pass (count > kSmallRescan); if the next step is the
+// component matrix its result is simply not used.
+appd_status tcf_speculate_rows(appd_ctx* c, TcState* st, const int* comp, u64* compbest) {
+  st->rows_spec = true;
+  return launch_rows_exact(c, st->XT, st->npad, (int)st->n, (int)st->d, st->rows_list, st->counters + 3, kSmallRescan,
+                           comp, compbest);
+}
+
 // Queue the cache lookup of the next round (compbest must hold KEY_NONE): per-row first
 // eligible cached key -> compbest, flagged rows -> rows_list; the count lands in
 // pinned_small[9] at the caller's next synchronisation.
@@ -1283,12 +1294,15 @@ appd_status tcf_round(appd_ctx* c, TcState* st, const float* X, const int* comp,
       APPD_SYNC(c);
     }
     st->lookup_pending = false;  // the caller synchronised after queueing it
+    const bool spec = st->rows_spec;
+    st->rows_spec = false;
     rescan_rows = c->pinned_small[9];
     st->last_rescan_rows = rescan_rows;
     if (rescan_rows == 0) return APPD_OK;  // every component decided by the cache
     if (rescan_rows <= (unsigned)kSmallRescan)  // a few rows: exact FP32 rows, no permutation / tensor pass
-      return launch_rows_exact(c, st->XT, st->npad, (int)n, (int)st->d, st->rows_list, st->counters + 3,
-                               (int)rescan_rows, comp, compbest);
+      return spec ? APPD_OK  // already queued before the synchronisation (tcf_speculate_rows)
+                  : launch_rows_exact(c, st->XT, st->npad, (int)n, (int)st->d, st->rows_list, st->counters + 3,
+                                      (int)rescan_rows, comp, compbest);
   }
   const bool packed = round == 0 && st->r0_packed;  // done by the cooperative preparation
   st->r0_packed = false;
