@@ -90,6 +90,60 @@ __global__ void __launch_bounds__(256) k_tiles_v8_persist(float* M, const int* r
     }
   }
 }
+template <int W>
+__global__ void __launch_bounds__(256) k_tiles_v8_smem(float* M, const int* rows, int n) {
+  extern __shared__ float dummy[];
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  if (threadIdx.x == 0) dummy[0] = 0.f;
+  for (int t = 0; t < 128; t++) {
+    float* dst = M + (int64_t)rows[t0 + t] * n + (int64_t)blockIdx.x * W + 8 * threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < W / 2048; c++)
+      asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + c * 2048), "f"(1.f),
+                   "f"(2.f), "f"(3.f), "f"(4.f), "f"(5.f), "f"(6.f), "f"(7.f), "f"((float)t)
+                   : "memory");
+  }
+}
+// the fill's shape with a setup of D dependent loads per CTA before its stores
+template <int W, int D>
+__global__ void __launch_bounds__(256) k_tiles_v8_setup(float* M, const int* rows, int n) {
+  __shared__ int srow[128];
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  int x = threadIdx.x + blockIdx.x * 97;
+#pragma unroll
+  for (int q = 0; q < D; q++) x = rows[(x * 31 + 7) & (n - 1)];
+  if (threadIdx.x < 128) srow[threadIdx.x] = rows[t0 + threadIdx.x] + (x == -5 ? 1 : 0);
+  __syncthreads();
+  for (int t = 0; t < 128; t++) {
+    float* dst = M + (int64_t)srow[t] * n + (int64_t)blockIdx.x * W + 8 * threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < W / 2048; c++)
+      asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + c * 2048), "f"(1.f),
+                   "f"(2.f), "f"(3.f), "f"(4.f), "f"(5.f), "f"(6.f), "f"(7.f), "f"((float)t)
+                   : "memory");
+  }
+}
+// the same stores with varying values (hash of the element index)
+template <int W>
+__global__ void __launch_bounds__(256) k_tiles_v8_rand(float* M, const int* rows, int n) {
+  const int64_t t0 = (int64_t)blockIdx.y * 128;
+  for (int t = 0; t < 128; t++) {
+    const int64_t r = rows[t0 + t];
+    float* dst = M + r * n + (int64_t)blockIdx.x * W + 8 * threadIdx.x;
+    unsigned h = (unsigned)(r * 2654435761u) ^ (unsigned)(blockIdx.x * W + 8 * threadIdx.x) * 40503u;
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      h = h * 1664525u + 1013904223u;
+      v[q] = __uint_as_float(0x3f800000u | (h >> 9));
+    }
+#pragma unroll
+    for (int c = 0; c < W / 2048; c++)
+      asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + c * 2048), "f"(v[0]),
+                   "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                   : "memory");
+  }
+}
 int main() {
   const int n = 65536;
   const size_t bytes = (size_t)n * n * 4;
@@ -133,5 +187,15 @@ int main() {
   time([&] { k_tiles_bulk<4096, 2><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles bulk 16 KB x2");
   time([&] { k_tiles_v8_persist<2048><<<148 * 4, 256>>>(M, rows, n, n / 2048, (n / 2048) * (n / 128)); }, "tiles v8 persistent");
   time([&] { k_tiles_v8<4096><<<dim3(n / 4096, n / 128), 256>>>(M, rows, n); }, "tiles v8 128 x 16 KB");
+  // occupancy limited by dynamic shared memory: 4 / 5 / 6 CTAs per SM
+  cudaFuncSetAttribute(k_tiles_v8_smem<2048>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  time([&] { k_tiles_v8_smem<2048><<<dim3(n / 2048, n / 128), 256, 52 * 1024>>>(M, rows, n); }, "tiles v8, 4 CTAs/SM");
+  time([&] { k_tiles_v8_smem<2048><<<dim3(n / 2048, n / 128), 256, 42 * 1024>>>(M, rows, n); }, "tiles v8, 5 CTAs/SM");
+  time([&] { k_tiles_v8_smem<2048><<<dim3(n / 2048, n / 128), 256, 35 * 1024>>>(M, rows, n); }, "tiles v8, 6 CTAs/SM");
+  time([&] { k_tiles_v8_smem<2048><<<dim3(n / 2048, n / 128), 256, 26 * 1024>>>(M, rows, n); }, "tiles v8, 8 CTAs/SM");
+  time([&] { k_tiles_v8_rand<2048><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8, random values");
+  time([&] { k_tiles_v8_setup<2048, 0><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8, setup 0 loads");
+  time([&] { k_tiles_v8_setup<2048, 3><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8, setup 3 loads");
+  time([&] { k_tiles_v8_setup<2048, 6><<<dim3(n / 2048, n / 128), 256>>>(M, rows, n); }, "tiles v8, setup 6 loads");
   return 0;
 }
