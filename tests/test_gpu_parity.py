@@ -263,6 +263,14 @@ def test_points_engine_paths_taken(P):
     st = c.stats()
     assert st["topk"] == 0 and st["cm_k"] == 0 and st["tcscan_launches"] == st["rounds"]
     c.close()
+    # rounds whose flagged rows exceed the exact-row limit (1024): the re-scan queued before
+    # the round's host wait must do nothing, the tensor-core re-scan then runs
+    Xu = G.random_points(8192, 4, 78, "uniform")  # (measured: 4793 flagged rows, 48 re-scanned blocks)
+    c = P.Context(timing=True, topk=4, finish_k=-1)
+    assert_bit_equal(gpu_points(c, Xu), oracle.appd_points(Xu), "uniform n=8192 d=4 K=4, Boruvka to the end")
+    st = c.stats()
+    assert st["rescan_blocks"] > 0 and st["rescan_rows"] > 1024, st
+    c.close()
     Xc = G.random_points(3000, 8, 77, "clumps")  # > 4K zero-distance columns per row: cache overflow
     c = P.Context(timing=True)
     assert_bit_equal(gpu_points(c, Xc), oracle.appd_points(Xc), "clumps")
