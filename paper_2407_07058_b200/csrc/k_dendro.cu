@@ -20,7 +20,9 @@
 //   C  list ranking (pointer jumping) -> tour positions; the earlier arc of an edge
 //      points downwards: parent and val of every vertex
 //   D  nearest heavier ancestor by binary lifting (2^j-th ancestor + max val on the way)
-//   E  children sorted by (record parent, val); Euler tour of the record tree, list
+//   E  children sorted by (record parent, val) -- the keys are laid out by val (edge
+//      rank), so a stable radix sort on the record-parent bits alone gives that order
+//      (2 digit passes at n = 65536 instead of 4); Euler tour of the record tree, list
 //      ranking, pre-order index = 1 + down arcs before the vertex's down arc
 //   F  pi[pre(v)] = v, h[a] = weight of the parent edge of pi[a+1]
 #include <cooperative_groups.h>
@@ -536,7 +538,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     }
     k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
     APPD_LAUNCHED(c);
-    if ((s = sort_keys_u64_bits64(c, key, S, m, 0, 2 * sh))) return s;
+    if ((s = sort_keys_u64_bits64(c, key, S, m, sh, 2 * sh))) return s;  // key[w] is in val order: a stable sort on rp
     {
       int mm = m, nn = n, shh = sh, rt = root, st = steps;
       void* args[] = {&S, &mm, &nn, &shh, &child_of, &first, &sidx, &rt, &bufA, &bufB, &rk, &flag, &downs, &blocksum,
@@ -579,7 +581,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
   APPD_LAUNCHED(c);
   // E: record tree, children ascending by val
-  if ((s = sort_keys_u64_bits64(c, key, S, m, 0, 2 * sh))) return s;
+  if ((s = sort_keys_u64_bits64(c, key, S, m, sh, 2 * sh))) return s;  // key[w] is in val order: a stable sort on rp
   APPD_CUDA(c, cudaMemsetAsync(first, 0xFF, sizeof(int) * n, c->stream));
   k_rt_index<<<gn, 256, 0, c->stream>>>(S, m, sh, child_of, first, sidx);
   APPD_LAUNCHED(c);
