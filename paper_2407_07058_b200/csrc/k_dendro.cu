@@ -225,6 +225,18 @@ __global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
   }
 }
 
+// Barrier of the fused tours: the whole cooperative grid (one CTA per SM), or -- for
+// small trees (n <= 16384) -- one thread-block cluster of kTourCluster CTAs, whose
+// hardware barrier (barrier.cluster.arrive.release / wait.acquire: the CTAs' global
+// writes before it are visible to the cluster after it) costs a fraction of a grid-wide
+// one.  The tours are chains of ~70 barrier-separated steps on arrays of a few hundred
+// KB, so at those sizes the barrier is the step.
+template <bool CL>
+__device__ __forceinline__ void all_sync() {
+  if constexpr (CL) cg::this_cluster().sync();
+  else cg::this_grid().sync();
+}
+
 // ---------------------------------------------------------------------------
 // Fused cooperative versions of the two tours (one launch each instead of 6-8):
 //   k_tour1: Euler successors of the MST (k_euler_succ), list ranking, orientation
@@ -233,9 +245,9 @@ __global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
 //            down flags, their exclusive scan and the outputs (k_emit).
 // The same operations in the same order, separated by grid-wide barriers.
 // ---------------------------------------------------------------------------
-template <int E>
-__device__ __forceinline__ void pj_steps(cg::grid_group& grid, int (&nx)[E], int (&rk)[E], int2* A, int2* B, int L,
-                                         int steps, int tid, int T) {
+template <int E, bool CL>
+__device__ __forceinline__ void pj_steps(int (&nx)[E], int (&rk)[E], int2* A, int2* B, int L, int steps, int tid,
+                                         int T) {
   for (int s = 0; s < steps; s++) {
     const int2* in = (s & 1) ? B : A;
     int2* out = (s & 1) ? A : B;
@@ -250,14 +262,15 @@ __device__ __forceinline__ void pj_steps(cg::grid_group& grid, int (&nx)[E], int
       }
       out[a] = make_int2(nx[e], rk[e]);
     }
-    grid.sync();
+    all_sync<CL>();
   }
 }
 
 // exclusive prefix sum of in[0..count) into out over the whole cooperative grid: block b
 // scans its contiguous segment, the block totals are added in order (grid barriers inside;
 // every thread of the grid must call it)
-__device__ void grid_exclusive_scan(cg::grid_group& grid, const int* in, int* out, int count, int* blocksum) {
+template <bool CL>
+__device__ void grid_exclusive_scan(const int* in, int* out, int count, int* blocksum) {
   __shared__ int wsum[32];
   __shared__ int carry_s;
   const int Sg = (count + gridDim.x - 1) / gridDim.x;
@@ -292,19 +305,18 @@ __device__ void grid_exclusive_scan(cg::grid_group& grid, const int* in, int* ou
     __syncthreads();
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
-  grid.sync();
+  all_sync<CL>();
   const int off = blocks_before(blocksum);
   for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) out[i] += off;
-  grid.sync();
+  all_sync<CL>();
 }
 
-template <int E>
+template <int E, bool CL>
 __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, const int32_t* __restrict__ ev, int m,
                                                 int n, int* sarc, int* start, int* end, int* posarc, int* deg,
                                                 int* cursor, int* blocksum, int root, int2* A, int2* B, int* rkout,
                                                 int* parent, int* val, int* child_of, int2* jm, int levels,
                                                 int steps) {
-  cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   // adjacency (CSR by source vertex; the order inside a list is irrelevant: the rooted
@@ -313,13 +325,13 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     deg[x] = 0;
     cursor[x] = 0;
   }
-  grid.sync();
+  all_sync<CL>();
   for (int ed = tid; ed < m; ed += T) {
     atomicAdd(deg + eu[ed], 1);
     atomicAdd(deg + ev[ed], 1);
   }
-  grid.sync();
-  grid_exclusive_scan(grid, deg, start, n, blocksum);
+  all_sync<CL>();
+  grid_exclusive_scan<CL>(deg, start, n, blocksum);
   for (int x = tid; x < n; x += T) end[x] = start[x] + deg[x];
   for (int a = tid; a < L; a += T) {
     const int src = (a & 1) ? ev[a >> 1] : eu[a >> 1];
@@ -327,7 +339,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     sarc[p] = a;
     posarc[a] = p;
   }
-  grid.sync();
+  all_sync<CL>();
   int nx[E], rk[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {  // Euler successors (k_euler_succ)
@@ -348,12 +360,12 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     val[root] = 0x7F7F7F7F;  // +inf: the root's parent edge
     parent[root] = root;
   }
-  grid.sync();
-  pj_steps<E>(grid, nx, rk, A, B, L, steps, tid, T);
+  all_sync<CL>();
+  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T);
 #pragma unroll
   for (int e = 0; e < E; e++)
     if (tid + e * T < L) rkout[tid + e * T] = rk[e];
-  grid.sync();
+  all_sync<CL>();
   for (int ed = tid; ed < m; ed += T) {  // orientation (k_orient): the earlier arc points down
     const bool down0 = rkout[2 * ed] > rkout[2 * ed + 1];
     const int ch = down0 ? ev[ed] : eu[ed], p = down0 ? eu[ed] : ev[ed];
@@ -361,7 +373,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     val[ch] = ed;
     child_of[ed] = ch;
   }
-  grid.sync();
+  all_sync<CL>();
   int2 cur[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {  // lifting level 0 (k_lift0)
@@ -373,7 +385,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
       jm[x] = cur[e];
     }
   }
-  grid.sync();
+  all_sync<CL>();
   for (int j = 1; j < levels; j++) {  // k_lift_coop
     const int2* in = jm + (size_t)(j - 1) * n;
     int2* out = jm + (size_t)j * n;
@@ -385,30 +397,29 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
       cur[e] = make_int2(q.x, max(cur[e].y, q.y));
       out[x] = cur[e];
     }
-    grid.sync();
+    all_sync<CL>();
   }
 }
 
-template <int E>
+template <int E, bool CL>
 __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __restrict__ S, int m, int n, int sh,
                                                 const int* __restrict__ child_of, int* first, int* sidx, int root,
                                                 int2* A, int2* B, int* rkout, int* flag, int* downs, int* blocksum,
                                                 const float* __restrict__ ew, int32_t* __restrict__ pi,
                                                 float* __restrict__ h, int steps) {
-  cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   const unsigned long long lo = (1ull << sh) - 1;
   for (int x = tid; x < n; x += T) first[x] = -1;
   for (int q = tid; q <= L; q += T) flag[q] = 0;
-  grid.sync();
+  all_sync<CL>();
   for (int i = tid; i < m; i += T) {  // k_rt_index
     const int rp = (int)(S[i] >> sh);
     const int v = child_of[(int)(S[i] & lo)];
     sidx[v] = i;
     if (i == 0 || (int)(S[i - 1] >> sh) != rp) first[rp] = i;
   }
-  grid.sync();
+  all_sync<CL>();
   for (int i = tid; i < m; i += T) {  // k_rt_succ
     const int rp = (int)(S[i] >> sh);
     const int v = child_of[(int)(S[i] & lo)];
@@ -420,7 +431,7 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
     A[2 * i] = make_int2(sd, 1);
     A[2 * i + 1] = make_int2(su, su < 0 ? 0 : 1);
   }
-  grid.sync();
+  all_sync<CL>();
   int nx[E], rk[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {
@@ -429,14 +440,14 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
     nx[e] = v.x;
     rk[e] = v.y;
   }
-  pj_steps<E>(grid, nx, rk, A, B, L, steps, tid, T);
+  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T);
 #pragma unroll
   for (int e = 0; e < E; e++)
     if (tid + e * T < L) rkout[tid + e * T] = rk[e];
-  grid.sync();
+  all_sync<CL>();
   for (int i = tid; i < m; i += T) flag[L - 1 - rkout[2 * i]] = 1;  // k_down_flags
-  grid.sync();
-  grid_exclusive_scan(grid, flag, downs, L, blocksum);
+  all_sync<CL>();
+  grid_exclusive_scan<CL>(flag, downs, L, blocksum);
   for (int i = tid; i < m; i += T) {  // k_emit
     const int e = (int)(S[i] & lo);
     const int v = child_of[e];
@@ -450,6 +461,30 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
 // one 1024-thread block per SM: the grid-wide barrier of every step is cheapest with
 // the fewest blocks, and 148 x 1024 threads cover the 2(n-1) arcs in a few strides
 constexpr int kCoopThreads = 1024;
+constexpr int kTourCluster = 8;  // portable cluster size
+
+// fused tour launch: cooperative (grid barrier) or one cluster of kTourCluster CTAs
+appd_status launch_tour(appd_ctx* c, const void* fn, bool cl, int grid, void** args) {
+  if (!cl) {
+    APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, grid, kCoopThreads, args, 0, c->stream));
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kTourCluster);
+    cfg.blockDim = dim3(kCoopThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kTourCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    APPD_CUDA(c, cudaLaunchKernelExC(&cfg, fn, args));
+  }
+  c->launches++;
+  return APPD_OK;
+}
 int coop_grid(appd_ctx* c, int items) {
   return std::max(1, std::min(c->sm_count, (items + kCoopThreads - 1) / kCoopThreads));
 }
@@ -521,7 +556,9 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   int steps = 0;
   while ((1 << steps) < L) steps++;
   steps++;
-  const int cgrid = coop_grid(c, L);
+  // one cluster when its threads cover the arcs in <= 4 strides, else the cooperative grid
+  const bool cl = L <= kTourCluster * kCoopThreads;  // (measured: at 4 strides the grid is faster)
+  const int cgrid = cl ? kTourCluster : coop_grid(c, L);
   const int cE = (L + cgrid * kCoopThreads - 1) / (cgrid * kCoopThreads);
   int* blocksum = (int*)ws(c, S_SCAN, sizeof(int) * (cgrid + 1) + 64);
   if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "dendrogram scan workspace");
@@ -532,9 +569,11 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
       int mm = m, nn = n, rt = root, lv = levels, st = steps;
       void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &src, &arc, &blocksum, &rt, &bufA, &bufB,
                       &rk, &parent, &val, &child_of, &jm, &lv, &st};
-      const void* fn = cE <= 1 ? (const void*)k_tour1<1> : cE <= 2 ? (const void*)k_tour1<2> : (const void*)k_tour1<4>;
-      APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, cgrid, kCoopThreads, args, 0, c->stream));
-      c->launches++;
+      const void* fn = cl ? (cE <= 1 ? (const void*)k_tour1<1, true> : cE <= 2 ? (const void*)k_tour1<2, true>
+                                                         : (const void*)k_tour1<4, true>)
+                          : (cE <= 1 ? (const void*)k_tour1<1, false> : cE <= 2 ? (const void*)k_tour1<2, false>
+                                                         : (const void*)k_tour1<4, false>);
+      if ((s = launch_tour(c, fn, cl, cgrid, args))) return s;
     }
     k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
     APPD_LAUNCHED(c);
@@ -543,9 +582,11 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
       int mm = m, nn = n, shh = sh, rt = root, st = steps;
       void* args[] = {&S, &mm, &nn, &shh, &child_of, &first, &sidx, &rt, &bufA, &bufB, &rk, &flag, &downs, &blocksum,
                       &ew, &pi, &h, &st};
-      const void* fn = cE <= 1 ? (const void*)k_tour2<1> : cE <= 2 ? (const void*)k_tour2<2> : (const void*)k_tour2<4>;
-      APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, cgrid, kCoopThreads, args, 0, c->stream));
-      c->launches++;
+      const void* fn = cl ? (cE <= 1 ? (const void*)k_tour2<1, true> : cE <= 2 ? (const void*)k_tour2<2, true>
+                                                         : (const void*)k_tour2<4, true>)
+                          : (cE <= 1 ? (const void*)k_tour2<1, false> : cE <= 2 ? (const void*)k_tour2<2, false>
+                                                         : (const void*)k_tour2<4, false>);
+      if ((s = launch_tour(c, fn, cl, cgrid, args))) return s;
     }
     return APPD_OK;
   }

@@ -28,6 +28,7 @@ namespace {
 
 constexpr int kSortThreads = 1024;
 constexpr int kMaxDigitBits = 8;
+constexpr int kSortCluster = 8;  // CTAs of the single-cluster sort (portable size)
 
 template <typename K>
 struct CoopSortArgs {
@@ -37,7 +38,7 @@ struct CoopSortArgs {
   const int* vin;  // nullptr: keys only
   int* vout;
   int* vbuf;
-  int n, begin_bit, passes, dbits;
+  int n, begin_bit, end_bit, passes, dbits;
   unsigned* cnt;   // [1 << dbits][G]
   unsigned* dtot;  // [1 << dbits]
   int iota_vals;   // values = input index (vin ignored)
@@ -46,9 +47,19 @@ struct CoopSortArgs {
   int *cstart, *cend, *rs, *re;
 };
 
-template <typename K>
+__device__ __forceinline__ unsigned end_bit_mask(int width, unsigned dmask) {
+  return width >= 32 ? dmask : (dmask & ((1u << width) - 1u));
+}
+
+// barrier of the persistent sort: the cooperative grid, or one cluster (small sorts)
+template <bool CL>
+__device__ __forceinline__ void sort_sync() {
+  if constexpr (CL) cg::this_cluster().sync();
+  else cg::this_grid().sync();
+}
+
+template <typename K, bool CL>
 __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArgs<K> a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned sm[];  // [ND] counts, then running scatter positions
   __shared__ unsigned part[kSortThreads / 32];
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -63,14 +74,16 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
     const K* src = p == 0 ? a.kin : (((a.passes - p) & 1) ? a.kbuf : a.kout);
     int* vdst = ((a.passes - 1 - p) & 1) ? a.vbuf : a.vout;
     const int* vsrc = p == 0 ? a.vin : (((a.passes - p) & 1) ? a.vbuf : a.vout);
-    auto digit = [&](K k) { return (unsigned)(k >> shift) & dmask; };
+    // (the last pass may be narrower: bits at and above end_bit never take part)
+    const unsigned pmask = end_bit_mask(a.end_bit - shift, dmask);
+    auto digit = [&](K k) { return (unsigned)(k >> shift) & pmask; };
     // ---- A: this CTA's digit counts
     for (int d = tid; d < ND; d += kSortThreads) sm[d] = 0u;
     __syncthreads();
     for (int i = lo + tid; i < hi; i += kSortThreads) atomicAdd(sm + digit(src[i]), 1u);
     __syncthreads();
     for (int d = tid; d < ND; d += kSortThreads) a.cnt[(int64_t)d * G + b] = sm[d];
-    grid.sync();
+    sort_sync<CL>();
     // ---- B: per digit, exclusive offsets of the CTAs and the digit total
     for (int d = gwarp; d < ND; d += nwarps) {
       unsigned carry = 0u;
@@ -88,7 +101,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
       }
       if (lane == 0) a.dtot[d] = carry;
     }
-    grid.sync();
+    sort_sync<CL>();
     // ---- C: digit bases (block scan of the totals, up to 4 per thread), then the
     // CTA's first position per digit
     {
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
         __syncthreads();
       }
     }
-    grid.sync();
+    sort_sync<CL>();
   }
   if (a.cstart) {  // label ranges (k_comp_ranges, k_row_ranges)
     const int64_t tid64 = (int64_t)b * kSortThreads + tid, nt = (int64_t)G * kSortThreads;
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
       if (q == 0 || (int)a.kout[q - 1] != cq) a.cstart[cq] = (int)q;
       if (q == a.n - 1 || (int)a.kout[q + 1] != cq) a.cend[cq] = (int)q + 1;
     }
-    grid.sync();
+    sort_sync<CL>();
     for (int64_t q = tid64; q < a.n; q += nt) {
       const int cq = (int)a.kout[q];
       a.rs[q] = a.cstart[cq];
@@ -186,7 +199,9 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   const int passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
   const int dbits = (bits + passes - 1) / passes;
   const int ND = 1 << dbits;
-  const int G = c->sm_count;
+  // small sorts (every CTA of one cluster holds <= 2 tiles of 1024 keys): one cluster
+  const bool cl = count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads * 2;
+  const int G = cl ? kSortCluster : c->sm_count;
   const bool vals = vin || iota_vals;
   const size_t kb = (sizeof(K) * (size_t)count + 255) & ~(size_t)255, vb = vals ? (sizeof(int) * (size_t)count + 255) & ~(size_t)255 : 0;
   char* w = (char*)ws(c, S_SORT, kb + vb + sizeof(unsigned) * ((size_t)ND * G + ND) + 256);
@@ -205,19 +220,38 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   a.re = re;
   a.n = (int)count;
   a.begin_bit = begin_bit;
+  a.end_bit = end_bit;
   a.passes = passes;
   a.dbits = dbits;
   a.cnt = reinterpret_cast<unsigned*>(w + kb + vb);
   a.dtot = a.cnt + (size_t)ND * G;
   static std::atomic<unsigned long long> attr{0};
   if (needs_setup(attr, c)) {
-    cudaFuncSetAttribute(k_coop_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_coop_sort<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(unsigned) << kMaxDigitBits));
+    cudaFuncSetAttribute(k_coop_sort<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(unsigned) << kMaxDigitBits));
     setup_done(attr, c);
   }
   void* args[] = {&a};
-  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_coop_sort<K>, G, kSortThreads, args,
-                                           sizeof(unsigned) * (size_t)ND, c->stream));
+  if (!cl) {
+    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_coop_sort<K, false>, G, kSortThreads, args,
+                                             sizeof(unsigned) * (size_t)ND, c->stream));
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kSortThreads);
+    cfg.dynamicSmemBytes = sizeof(unsigned) * (size_t)ND;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    APPD_CUDA(c, cudaLaunchKernelExC(&cfg, (const void*)k_coop_sort<K, true>, args));
+  }
   APPD_LAUNCHED(c);
   return APPD_OK;
 }
@@ -241,7 +275,10 @@ appd_status lib_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* vo
 template <typename K>
 appd_status path_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* vout, int64_t count, int begin_bit,
                       int end_bit) {
-  if (end_bit - begin_bit <= kMaxDigitBits) return coop_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
+  // one digit pass, or a small sort (one cluster, its barriers far cheaper than the
+  // library's per-pass launches): the cooperative sort; else the library's onesweep
+  if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads * 2))
+    return coop_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
   return lib_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
 }
 
