@@ -285,6 +285,115 @@ __global__ void __launch_bounds__(256) k_scan_weights_topk(const float* __restri
   }
 }
 
+// Single-pass variant (K <= 8): ONE WARP PER ROW and one read of W.  The warp keeps
+// the row's K smallest keys so far as a sorted list distributed over lanes 0..K-1, and
+// its K-th as a warp-uniform threshold.  A batch is 8 float4 per lane (1024 columns);
+// each lane tests its 32 values against the threshold with one float compare each
+// (candidates are rare once the list is warm), and the warp inserts the few candidates
+// one by one (shuffle shift of the list).  The first batch inserts the lanes' minima
+// first, so that the threshold is tight at once.  Keys are (orderable(m), j), m the
+// sense-adjusted weight -- the same cache as k_scan_weights_topk, whose second pass
+// re-read the row from L2 and whose CTA-wide merges idled the CTA's loads.
+template <int K, int SENSE>
+__global__ void __launch_bounds__(256, 3) k_scan_weights_topk_w(const float* __restrict__ W, int64_t n, int64_t row0,
+                                                           int64_t rows, u64* __restrict__ ckey, int* __restrict__ cj,
+                                                           int* __restrict__ ccnt, u64* __restrict__ compbest) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n4 = (int)(n >> 2);  // (launched only for n % 4 == 0 and an aligned W)
+  for (int64_t r = gw; r < rows; r += nw) {
+    const int64_t i = row0 + r;
+    const int i32 = (int)i;
+    const float4* W4 = reinterpret_cast<const float4*>(W + r * n);
+    u64 lk = KEY_NONE;  // lane t < K: the t-th smallest key so far
+    u64 thr = KEY_NONE;
+    auto insert = [&](u64 kc) {
+      u64 prev = __shfl_up_sync(0xffffffffu, lk, 1);
+      if (lane == 0) prev = 0ull;
+      const u64 nk = prev > kc ? prev : (lk > kc ? kc : lk);
+      lk = lane < K ? nk : KEY_NONE;
+      thr = __shfl_sync(0xffffffffu, lk, K - 1);
+    };
+    for (int b0 = 0; b0 < n4; b0 += 256) {
+      float m[32];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int q = b0 + u * 32 + lane;
+        float4 v = make_float4(NAN, NAN, NAN, NAN);  // past the row: never a candidate
+        if (q < n4) v = __ldcs(W4 + q);
+        m[4 * u + 0] = SENSE > 0 ? v.x : -v.x;
+        m[4 * u + 1] = SENSE > 0 ? v.y : -v.y;
+        m[4 * u + 2] = SENSE > 0 ? v.z : -v.z;
+        m[4 * u + 3] = SENSE > 0 ? v.w : -v.w;
+      }
+      if ((i32 >> 10) == (b0 >> 8)) {  // (warp-uniform) the batch with the diagonal: NaN
+        const int qd = i32 >> 2;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+#pragma unroll
+          for (int c = 0; c < 4; c++)
+            if (b0 + u * 32 + lane == qd && (i32 & 3) == c) m[4 * u + c] = NAN;
+      }
+      auto jof = [&](int e) { return 4 * (b0 + (e >> 2) * 32 + lane) + (e & 3); };
+      // (-0 -> +0 in the key, reading Q5; the compares treat them as equal anyway)
+      auto keyof = [&](int e) { return ((u64)orderable(m[e] + 0.0f) << 32) | (u64)(unsigned)jof(e); };
+      int own = -1;  // warm-up: this lane's minimum, inserted already
+      if (thr == KEY_NONE) {
+        float mn = NAN;
+#pragma unroll
+        for (int e = 0; e < 32; e++) mn = fminf(mn, m[e]);  // (fminf skips NaN)
+#pragma unroll
+        for (int e = 31; e >= 0; e--)
+          if (m[e] == mn) own = e;  // the smallest j among equal minima
+        u64 mk = KEY_NONE;
+#pragma unroll
+        for (int e = 0; e < 32; e++)
+          if (e == own) mk = keyof(e);
+        unsigned bal = __ballot_sync(0xffffffffu, own >= 0);
+        while (bal) {
+          const int l = __ffs(bal) - 1;
+          bal &= bal - 1;
+          insert(__shfl_sync(0xffffffffu, mk, l));
+        }
+      }
+      // candidates: m below the threshold's weight; a tie at that weight can only win if
+      // the threshold's column lies in this batch or later (columns of earlier batches
+      // are smaller), which is rare once the list is warm (warp-uniform test)
+      const float tw = thr == KEY_NONE ? INFINITY : from_orderable((uint32_t)(thr >> 32));
+      const bool tie_ok = thr == KEY_NONE || (int)(uint32_t)thr >= 4 * b0;
+      unsigned mask = 0;
+#pragma unroll
+      for (int e = 0; e < 32; e++)
+        if (m[e] < tw || (tie_ok && m[e] == tw)) mask |= 1u << e;
+      if (own >= 0) mask &= ~(1u << own);
+      if (__any_sync(0xffffffffu, mask != 0)) {
+#pragma unroll
+        for (int e = 0; e < 32; e++) {
+          unsigned bal = __ballot_sync(0xffffffffu, (mask >> e) & 1u);
+          const u64 ke = keyof(e);
+          while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const u64 kc = __shfl_sync(0xffffffffu, ke, l);
+            if (kc < thr) insert(kc);
+          }
+        }
+      }
+    }
+    // the list (ascending local keys (w, j)) -> global keys; lane t writes entry t
+    const unsigned valid = __ballot_sync(0xffffffffu, lk != KEY_NONE);
+    if (lane < K && lk != KEY_NONE) {
+      const int64_t j = (int64_t)(lk & 0xFFFFFFFFull);
+      const u64 g = (lk & 0xFFFFFFFF00000000ull) | tri_index(i, j);
+      ckey[i * K + lane] = g;
+      cj[i * K + lane] = (int)j;
+      if (lane == 0) compbest[i] = g;
+    }
+    if (lane == 0) ccnt[i] = __popc(valid);
+  }
+}
+
 // weights mode: exact scan of a list of rows (component-filtered argmin, re-scans)
 template <int SENSE>
 __global__ void __launch_bounds__(256) k_scan_weights_list(const float* __restrict__ W, int64_t n, int64_t row0,
@@ -330,14 +439,21 @@ appd_status launch_scan_weights_topk(appd_ctx* c, const float* W, int64_t n, int
 #define APPD_WTOPK(KK)                                                                                       \
   (sense > 0 ? (k_scan_weights_topk<KK, 1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)) \
              : (k_scan_weights_topk<KK, -1><<<grid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)))
+  // K <= 8: the single-pass warp-per-row kernel (8 warps per CTA)
+  const int wgrid = (int)std::min<int64_t>(std::max<int64_t>((rows + 7) / 8, 1), (int64_t)c->sm_count * 8);
+#define APPD_WTOPK_W(KK)                                                                                        \
+  (sense > 0 ? (k_scan_weights_topk_w<KK, 1><<<wgrid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)) \
+             : (k_scan_weights_topk_w<KK, -1><<<wgrid, 256, 0, c->stream>>>(W, n, row0, rows, ckey, cj, ccnt, compbest)))
+  const bool wv = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   switch (K) {
-    case 4: APPD_WTOPK(4); break;
-    case 8: APPD_WTOPK(8); break;
+    case 4: if (wv) APPD_WTOPK_W(4); else APPD_WTOPK(4); break;
+    case 8: if (wv) APPD_WTOPK_W(8); else APPD_WTOPK(8); break;
     case 16: APPD_WTOPK(16); break;
     case 32: APPD_WTOPK(32); break;
     default: return fail(c, APPD_ERR_INVALID_ARGUMENT, "cache length K = %d (4, 8, 16 or 32)", K);
   }
 #undef APPD_WTOPK
+#undef APPD_WTOPK_W
   APPD_LAUNCHED(c);
   return APPD_OK;
 }

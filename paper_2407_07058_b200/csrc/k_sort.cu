@@ -199,8 +199,9 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   const int passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
   const int dbits = (bits + passes - 1) / passes;
   const int ND = 1 << dbits;
-  // small sorts (every CTA of one cluster holds <= 2 tiles of 1024 keys): one cluster
-  const bool cl = count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads * 2;
+  // small sorts (every CTA of one cluster holds one tile of 1024 keys): one cluster (at
+  // two tiles per CTA the library sort measured faster)
+  const bool cl = count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads;
   const int G = cl ? kSortCluster : c->sm_count;
   const bool vals = vin || iota_vals;
   const size_t kb = (sizeof(K) * (size_t)count + 255) & ~(size_t)255, vb = vals ? (sizeof(int) * (size_t)count + 255) & ~(size_t)255 : 0;
@@ -277,7 +278,7 @@ appd_status path_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
                       int end_bit) {
   // one digit pass, or a small sort (one cluster, its barriers far cheaper than the
   // library's per-pass launches): the cooperative sort; else the library's onesweep
-  if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads * 2))
+  if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads))
     return coop_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
   return lib_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
 }
