@@ -113,6 +113,20 @@ def test_weights_cache_lengths(P, topk):
         c.close()
 
 
+@pytest.mark.parametrize("topk", [4, 8])
+def test_weights_cache_multi_batch(P, topk):
+    """The single-pass warp-per-row round-0 cache (n % 4 == 0: 1024-column batches) across
+    several batches with a ragged last one, the diagonal in a later batch, heavy ties and
+    signed zeros, both senses; n % 4 != 0 takes the two-pass kernel (same cache)."""
+    for sense in (1, -1):
+        with P.Context(timing=True, topk=topk, sense=sense, variant=P.VARIANT_BORUVKA) as c:
+            for t, (n, kind) in enumerate([(2052, "ints255"), (3000, "ties"), (4100, "signed_zero"),
+                                           (2050, "ints255"), (1028, "uniform")]):
+                W = G.random_weights(n, 900 + t, kind)
+                assert_bit_equal(gpu_weights(None, W, c=c), oracle.appd_weights(W, sense),
+                                 f"topk={topk} sense={sense} {kind} n={n}")
+
+
 @pytest.mark.parametrize("variant", [0, 2])
 def test_widest_sense(P, variant):
     with P.Context(sense=-1, variant=variant) as cw:
