@@ -1036,6 +1036,7 @@ appd_status launch_relabel(appd_ctx* c, int* comp, int64_t n, const int* parent,
 // the same operations in the same order, one launch instead of six.  newid[k] = roots.
 // ---------------------------------------------------------------------------
 constexpr int kContractThreads = 1024;
+constexpr int64_t kContractOneMax = 1024;  // one CTA (one item per thread): CTA barriers
 // development builds (APPD_MARKS): %globaltimer after each phase, CTA 0 (LookupArgs.marks)
 __device__ __forceinline__ void contract_mark(const LookupArgs& la, int i) {
   if (la.marks && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1044,13 +1045,22 @@ __device__ __forceinline__ void contract_mark(const LookupArgs& la, int i) {
     la.marks[i] = t;
   }
 }
+// ONE: a single CTA does it all (n, k <= kContractOneMax, where the cooperative grid would
+// be one CTA anyway): every grid-wide barrier becomes a CTA barrier (C1 with Boruvka forced:
+// MST 0.144 -> 0.102 ms).  At C2 (n = 4096) one CTA measured no faster than four: there the
+// pointer chasing and the cache lookups' dependent loads are the bound, not the barriers.
+template <bool ONE>
+__device__ __forceinline__ void contract_sync() {
+  if constexpr (ONE) __syncthreads();
+  else cg::this_grid().sync();
+}
+template <bool ONE>
 __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__ compbest, int k,
                                                              int* __restrict__ comp, int n, int shift,
                                                              int* __restrict__ link, int* __restrict__ parent,
                                                              u64* __restrict__ mstkeys, int* __restrict__ counters,
                                                              int* __restrict__ flags, int* __restrict__ newid,
                                                              int* __restrict__ blocksum, LookupArgs la) {
-  cg::grid_group grid = cg::this_grid();
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   contract_mark(la, 0);
   // hook: the component at the other end of each component's lightest edge
@@ -1065,7 +1075,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     const int cu = comp[u], cv = comp[v];
     link[c] = (cu == c) ? cv : cu;
   }
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 1);
   // mutual pairs: the smaller id is the root, the shared edge is recorded once
   for (int c = tid; c < k; c += T) {
@@ -1078,7 +1088,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     parent[c] = (mutual && c < o) ? c : o;
     if (!(mutual && c > o)) mstkeys[atomicAdd(counters, 1)] = compbest[c];
   }
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 2);
   // (compbest is not read after the hook and mutual phases: the next round's lookup can
   // start from KEY_NONE without a barrier of its own)
@@ -1097,7 +1107,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     parent[c] = p;
     flags[c] = p == c ? 1 : 0;
   }
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 3);
   // exclusive scan of the flags: block b owns [b S, (b+1) S)
   __shared__ int wsum[kContractThreads / 32];
@@ -1135,18 +1145,18 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 4);
   const int off = blocks_before(blocksum);
   for (int i = lo + threadIdx.x; i < hi; i += kContractThreads) newid[i] += off;
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) newid[k] = off + carry_s;
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 5);
   // relabel the points
   for (int i = tid; i < n; i += T) comp[i] = newid[parent[comp[i]]];
   if (!la.ckey) return;
   // the next round's cache lookup (k_cache_lookup, k_rescan_select) on the final labels
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 6);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     const int c = la.ccnt[i];
@@ -1176,7 +1186,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     }
     la.need[i] = flag;
   }
-  grid.sync();
+  contract_sync<ONE>();
   contract_mark(la, 7);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     if (!la.need[i]) continue;
@@ -1194,7 +1204,7 @@ appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, in
   static std::atomic<int> per_sm_plus1[64];  // 0: not yet measured on that device
   int per_sm = per_sm_plus1[c->device & 63].load() - 1;
   if (per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_contract, kContractThreads, 0) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_contract<false>, kContractThreads, 0) != cudaSuccess)
       per_sm = 0;
     cudaGetLastError();
     per_sm_plus1[c->device & 63].store(per_sm + 1);
@@ -1210,7 +1220,13 @@ appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, in
                   &la};
   static const bool marks = dev_env("APPD_MARKS") != nullptr;
   if (marks) la.marks = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 128));
-  APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract, grid, kContractThreads, args, 0, c->stream));
+  if (std::max(k, n) <= kContractOneMax) {
+    k_contract<true><<<1, kContractThreads, 0, c->stream>>>(compbest, kk, comp, nn, shift, link, parent, mstkeys,
+                                                             counters, flags, newid, blocksum, la);
+    APPD_CUDA(c, cudaGetLastError());
+  } else {
+    APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract<false>, grid, kContractThreads, args, 0, c->stream));
+  }
   c->launches++;
   if (marks && la.marks) {
     unsigned long long h[10] = {};
