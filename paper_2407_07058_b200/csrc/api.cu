@@ -209,11 +209,25 @@ extern "C" appd_status appd_set_stream(appd_ctx* c, void* stream) {
   return APPD_OK;
 }
 
+namespace appd {
+unsigned* grid_barrier_word(appd_ctx* c) {
+  if (!c->gridbar) {
+    if (cudaMalloc(&c->gridbar, 64) != cudaSuccess) {
+      c->gridbar = nullptr;
+      return nullptr;
+    }
+    if (cudaMemsetAsync(c->gridbar, 0, 64, c->stream) != cudaSuccess) return nullptr;
+  }
+  return c->gridbar;
+}
+}  // namespace appd
+
 extern "C" void appd_destroy(appd_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   nccl_destroy(c);
+  if (c->gridbar) cudaFree(c->gridbar);
   for (auto& b : c->buf)
     if (b.p) cudaFree(b.p);
   if (c->ev_ready)

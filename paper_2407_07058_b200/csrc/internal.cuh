@@ -130,6 +130,8 @@ struct appd_ctx {
   };
   PubEntry pub[16];
   int npub = 0;
+  // word of the cooperative kernels' grid barrier (coop_grid_sync), zeroed at first use
+  unsigned* gridbar = nullptr;
   std::vector<unsigned long long> host_xchg;  // host exchange backend staging (opt.host_allreduce)
   std::vector<int32_t> uf_scratch;   // host dendrogram work arrays
   // streamed output (NEXT-4, appd_solve_points_stream): M rows go to this host buffer in
@@ -374,6 +376,27 @@ __device__ __forceinline__ void atomic_min_lt(unsigned* a, unsigned v) {
 // sum of blocksum[0 .. blockIdx.x) for every thread of the block: warp 0 reduces with its
 // loads in flight (a serial loop over up to 147 earlier blocks was ~20 us of dependent
 // L2 latency in the last block of a cooperative scan)
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): thread 0 of each CTA
+// adds to the counter with release semantics -- CTA 0 adds 2^31 - (G - 1), the others 1, so
+// the counter's top bit flips exactly when the last CTA arrives and its low 31 bits return
+// to 0 (a zeroed word serves every launch and barrier) -- then spins with acquire loads on
+// the flip.  The same protocol as cooperative_groups' grid sync, without its full fences
+// before and after (the release add and the acquire load order the CTA's writes and reads).
+__device__ __forceinline__ void coop_grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned inc = blockIdx.x == 0 ? (0x80000000u - (gridDim.x - 1u)) : 1u;
+    unsigned old, cur;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(inc) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0u);
+  }
+  __syncthreads();
+}
+// the context's barrier word (allocated and zeroed on the context's stream at first use)
+unsigned* grid_barrier_word(appd_ctx* c);
+
 __device__ __forceinline__ int blocks_before(const int* blocksum) {
   __shared__ int bb_sum;
   if (threadIdx.x < 32) {

@@ -1050,9 +1050,9 @@ __device__ __forceinline__ void contract_mark(const LookupArgs& la, int i) {
 // MST 0.144 -> 0.102 ms).  At C2 (n = 4096) one CTA measured no faster than four: there the
 // pointer chasing and the cache lookups' dependent loads are the bound, not the barriers.
 template <bool ONE>
-__device__ __forceinline__ void contract_sync() {
+__device__ __forceinline__ void contract_sync(unsigned* bar) {
   if constexpr (ONE) __syncthreads();
-  else cg::this_grid().sync();
+  else coop_grid_sync(bar);
 }
 template <bool ONE>
 __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__ compbest, int k,
@@ -1060,7 +1060,8 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
                                                              int* __restrict__ link, int* __restrict__ parent,
                                                              u64* __restrict__ mstkeys, int* __restrict__ counters,
                                                              int* __restrict__ flags, int* __restrict__ newid,
-                                                             int* __restrict__ blocksum, LookupArgs la) {
+                                                             int* __restrict__ blocksum, LookupArgs la,
+                                                             unsigned* __restrict__ bar) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   contract_mark(la, 0);
   // hook: the component at the other end of each component's lightest edge
@@ -1075,7 +1076,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     const int cu = comp[u], cv = comp[v];
     link[c] = (cu == c) ? cv : cu;
   }
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 1);
   // mutual pairs: the smaller id is the root, the shared edge is recorded once
   for (int c = tid; c < k; c += T) {
@@ -1088,7 +1089,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     parent[c] = (mutual && c < o) ? c : o;
     if (!(mutual && c > o)) mstkeys[atomicAdd(counters, 1)] = compbest[c];
   }
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 2);
   // (compbest is not read after the hook and mutual phases: the next round's lookup can
   // start from KEY_NONE without a barrier of its own)
@@ -1107,7 +1108,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     parent[c] = p;
     flags[c] = p == c ? 1 : 0;
   }
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 3);
   // exclusive scan of the flags: block b owns [b S, (b+1) S)
   __shared__ int wsum[kContractThreads / 32];
@@ -1145,18 +1146,18 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 4);
   const int off = blocks_before(blocksum);
   for (int i = lo + threadIdx.x; i < hi; i += kContractThreads) newid[i] += off;
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) newid[k] = off + carry_s;
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 5);
   // relabel the points
   for (int i = tid; i < n; i += T) comp[i] = newid[parent[comp[i]]];
   if (!la.ckey) return;
   // the next round's cache lookup (k_cache_lookup, k_rescan_select) on the final labels
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 6);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     const int c = la.ccnt[i];
@@ -1186,7 +1187,7 @@ __global__ void __launch_bounds__(kContractThreads) k_contract(u64* __restrict__
     }
     la.need[i] = flag;
   }
-  contract_sync<ONE>();
+  contract_sync<ONE>(bar);
   contract_mark(la, 7);
   for (int i = la.r0 + tid; i < la.r1; i += T) {
     if (!la.need[i]) continue;
@@ -1216,13 +1217,15 @@ appd_status launch_contract(appd_ctx* c, u64* compbest, int64_t k, int* comp, in
   if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "contract workspace");
   int kk = (int)k, nn = (int)n;
   LookupArgs la = look ? *look : LookupArgs{};
+  unsigned* bar = grid_barrier_word(c);
+  if (!bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
   void* args[] = {&compbest, &kk, &comp, &nn, &shift, &link, &parent, &mstkeys, &counters, &flags, &newid, &blocksum,
-                  &la};
+                  &la, &bar};
   static const bool marks = dev_env("APPD_MARKS") != nullptr;
   if (marks) la.marks = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 128));
   if (std::max(k, n) <= kContractOneMax) {
     k_contract<true><<<1, kContractThreads, 0, c->stream>>>(compbest, kk, comp, nn, shift, link, parent, mstkeys,
-                                                             counters, flags, newid, blocksum, la);
+                                                             counters, flags, newid, blocksum, la, bar);
     APPD_CUDA(c, cudaGetLastError());
   } else {
     APPD_CUDA(c, cudaLaunchCooperativeKernel((const void*)k_contract<false>, grid, kContractThreads, args, 0, c->stream));

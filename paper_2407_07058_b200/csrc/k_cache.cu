@@ -449,6 +449,7 @@ struct ListSortArgs {
   unsigned long long* marks;  // development builds (APPD_MARKS): %globaltimer per phase, CTA 0
   int aggregate;              // the listing comes in chunk runs: warp-aggregated atomics
   unsigned* cnt;              // (no runs) [nch][grid] per-CTA counts, then their offsets
+  unsigned* bar;              // grid barrier word (coop_grid_sync)
 };
 __device__ __forceinline__ void ls_mark(const ListSortArgs& a, int i) {
   if (a.marks && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -458,7 +459,6 @@ __device__ __forceinline__ void ls_mark(const ListSortArgs& a, int i) {
   }
 }
 __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
-  cg::grid_group grid = cg::this_grid();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned total = min(*a.count, a.cap);
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
     a.hist[i] = 0u;
     a.cursor[i] = 0u;
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   ls_mark(a, 1);
   // no chunk runs (round 0: the listing is in row order, chunks at random): global atomics
   // would serialise (~23 us for 640K entries), so every CTA counts its contiguous slice of
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
     __syncthreads();
     for (int i = threadIdx.x; i < a.nch; i += blockDim.x) a.cnt[(int64_t)i * G + blockIdx.x] = sh[i];
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   ls_mark(a, 2);
   if (!a.aggregate) {  // chunk totals, and each CTA's offset inside its chunk (a warp per chunk)
     for (int i = (int)(tid >> 5); i < a.nch; i += (int)(nt >> 5)) {
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
       for (unsigned j0 = 256; j0 < G; j0 += 32) step(j0 + lane < G ? a.cnt[(int64_t)i * G + j0 + lane] : 0u, j0 + lane);
       if (lane == 0) a.hist[i] = carry;
     }
-    grid.sync();
+    coop_grid_sync(a.bar);
   }
   // block b scans chunks [lo, hi): entries (offsets) and 128-row batches (item starts)
   __shared__ unsigned ws1[32], ws2[32];
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
     a.blocksum[2 * blockIdx.x] = carry1;
     a.blocksum[2 * blockIdx.x + 1] = carry2;
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   ls_mark(a, 3);
   // the sums of the earlier blocks' totals (a block-wide reduction, not a serial loop)
   if (warp == 0) {
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(1024) k_list_sort(const ListSortArgs a) {
       a.items[o2 + b] = make_int4(i, (int)b0, (int)min((unsigned)LE_RB, o1 + h - b0), 0);
     }
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   ls_mark(a, 4);
   if (a.aggregate) {
     for (unsigned e0 = (unsigned)(tid & ~31ll); e0 < total; e0 += (unsigned)nt) {  // scatter
@@ -629,7 +629,8 @@ appd_status launch_list_counting(appd_ctx* c, const unsigned* list, const unsign
     if (!cnt) return fail(c, APPD_ERR_OUT_OF_MEMORY, "list sort counts");
   }
   ListSortArgs a{list, count, cap, nch, hist, offs, cursor, out, run_lo, run_nb, item_start, items, blocksum, nullptr,
-                 aggregate ? 1 : 0, cnt};
+                 aggregate ? 1 : 0, cnt, grid_barrier_word(c)};
+  if (!a.bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
   const size_t smem = aggregate ? 0 : sizeof(unsigned) * nch;
   if (smem > 64 * 1024) return fail(c, APPD_ERR_UNSUPPORTED, "list sort: %d chunks", nch);
   static std::atomic<unsigned long long> attr{0};

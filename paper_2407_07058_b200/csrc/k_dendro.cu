@@ -232,9 +232,9 @@ __global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
 // one.  The tours are chains of ~70 barrier-separated steps on arrays of a few hundred
 // KB, so at those sizes the barrier is the step.
 template <bool CL>
-__device__ __forceinline__ void all_sync() {
+__device__ __forceinline__ void all_sync(unsigned* bar) {
   if constexpr (CL) cg::this_cluster().sync();
-  else cg::this_grid().sync();
+  else coop_grid_sync(bar);
 }
 
 // ---------------------------------------------------------------------------
@@ -247,7 +247,7 @@ __device__ __forceinline__ void all_sync() {
 // ---------------------------------------------------------------------------
 template <int E, bool CL>
 __device__ __forceinline__ void pj_steps(int (&nx)[E], int (&rk)[E], int2* A, int2* B, int L, int steps, int tid,
-                                         int T) {
+                                         int T, unsigned* bar) {
   for (int s = 0; s < steps; s++) {
     const int2* in = (s & 1) ? B : A;
     int2* out = (s & 1) ? A : B;
@@ -262,7 +262,7 @@ __device__ __forceinline__ void pj_steps(int (&nx)[E], int (&rk)[E], int2* A, in
       }
       out[a] = make_int2(nx[e], rk[e]);
     }
-    all_sync<CL>();
+    all_sync<CL>(bar);
   }
 }
 
@@ -270,7 +270,7 @@ __device__ __forceinline__ void pj_steps(int (&nx)[E], int (&rk)[E], int2* A, in
 // scans its contiguous segment, the block totals are added in order (grid barriers inside;
 // every thread of the grid must call it)
 template <bool CL>
-__device__ void grid_exclusive_scan(const int* in, int* out, int count, int* blocksum) {
+__device__ void grid_exclusive_scan(const int* in, int* out, int count, int* blocksum, unsigned* bar) {
   __shared__ int wsum[32];
   __shared__ int carry_s;
   const int Sg = (count + gridDim.x - 1) / gridDim.x;
@@ -305,10 +305,10 @@ __device__ void grid_exclusive_scan(const int* in, int* out, int count, int* blo
     __syncthreads();
   }
   if (threadIdx.x == 0) blocksum[blockIdx.x] = carry_s;
-  all_sync<CL>();
+  all_sync<CL>(bar);
   const int off = blocks_before(blocksum);
   for (int i = lo_i + threadIdx.x; i < hi_i; i += blockDim.x) out[i] += off;
-  all_sync<CL>();
+  all_sync<CL>(bar);
 }
 
 template <int E, bool CL>
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
                                                 int n, int* sarc, int* start, int* end, int* posarc, int* deg,
                                                 int* cursor, int* blocksum, int root, int2* A, int2* B, int* rkout,
                                                 int* parent, int* val, int* child_of, int2* jm, int levels,
-                                                int steps) {
+                                                int steps, unsigned* bar) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   // adjacency (CSR by source vertex; the order inside a list is irrelevant: the rooted
@@ -325,13 +325,13 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     deg[x] = 0;
     cursor[x] = 0;
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int ed = tid; ed < m; ed += T) {
     atomicAdd(deg + eu[ed], 1);
     atomicAdd(deg + ev[ed], 1);
   }
-  all_sync<CL>();
-  grid_exclusive_scan<CL>(deg, start, n, blocksum);
+  all_sync<CL>(bar);
+  grid_exclusive_scan<CL>(deg, start, n, blocksum, bar);
   for (int x = tid; x < n; x += T) end[x] = start[x] + deg[x];
   for (int a = tid; a < L; a += T) {
     const int src = (a & 1) ? ev[a >> 1] : eu[a >> 1];
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     sarc[p] = a;
     posarc[a] = p;
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   int nx[E], rk[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {  // Euler successors (k_euler_succ)
@@ -360,12 +360,12 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     val[root] = 0x7F7F7F7F;  // +inf: the root's parent edge
     parent[root] = root;
   }
-  all_sync<CL>();
-  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T);
+  all_sync<CL>(bar);
+  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T, bar);
 #pragma unroll
   for (int e = 0; e < E; e++)
     if (tid + e * T < L) rkout[tid + e * T] = rk[e];
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int ed = tid; ed < m; ed += T) {  // orientation (k_orient): the earlier arc points down
     const bool down0 = rkout[2 * ed] > rkout[2 * ed + 1];
     const int ch = down0 ? ev[ed] : eu[ed], p = down0 ? eu[ed] : ev[ed];
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     val[ch] = ed;
     child_of[ed] = ch;
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   int2 cur[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {  // lifting level 0 (k_lift0)
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
       jm[x] = cur[e];
     }
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int j = 1; j < levels; j++) {  // k_lift_coop
     const int2* in = jm + (size_t)(j - 1) * n;
     int2* out = jm + (size_t)j * n;
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
       cur[e] = make_int2(q.x, max(cur[e].y, q.y));
       out[x] = cur[e];
     }
-    all_sync<CL>();
+    all_sync<CL>(bar);
   }
 }
 
@@ -406,20 +406,20 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
                                                 const int* __restrict__ child_of, int* first, int* sidx, int root,
                                                 int2* A, int2* B, int* rkout, int* flag, int* downs, int* blocksum,
                                                 const float* __restrict__ ew, int32_t* __restrict__ pi,
-                                                float* __restrict__ h, int steps) {
+                                                float* __restrict__ h, int steps, unsigned* bar) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   const unsigned long long lo = (1ull << sh) - 1;
   for (int x = tid; x < n; x += T) first[x] = -1;
   for (int q = tid; q <= L; q += T) flag[q] = 0;
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int i = tid; i < m; i += T) {  // k_rt_index
     const int rp = (int)(S[i] >> sh);
     const int v = child_of[(int)(S[i] & lo)];
     sidx[v] = i;
     if (i == 0 || (int)(S[i - 1] >> sh) != rp) first[rp] = i;
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int i = tid; i < m; i += T) {  // k_rt_succ
     const int rp = (int)(S[i] >> sh);
     const int v = child_of[(int)(S[i] & lo)];
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
     A[2 * i] = make_int2(sd, 1);
     A[2 * i + 1] = make_int2(su, su < 0 ? 0 : 1);
   }
-  all_sync<CL>();
+  all_sync<CL>(bar);
   int nx[E], rk[E];
 #pragma unroll
   for (int e = 0; e < E; e++) {
@@ -440,14 +440,14 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
     nx[e] = v.x;
     rk[e] = v.y;
   }
-  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T);
+  pj_steps<E, CL>(nx, rk, A, B, L, steps, tid, T, bar);
 #pragma unroll
   for (int e = 0; e < E; e++)
     if (tid + e * T < L) rkout[tid + e * T] = rk[e];
-  all_sync<CL>();
+  all_sync<CL>(bar);
   for (int i = tid; i < m; i += T) flag[L - 1 - rkout[2 * i]] = 1;  // k_down_flags
-  all_sync<CL>();
-  grid_exclusive_scan<CL>(flag, downs, L, blocksum);
+  all_sync<CL>(bar);
+  grid_exclusive_scan<CL>(flag, downs, L, blocksum, bar);
   for (int i = tid; i < m; i += T) {  // k_emit
     const int e = (int)(S[i] & lo);
     const int v = child_of[e];
@@ -562,13 +562,15 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
   const int cE = (L + cgrid * kCoopThreads - 1) / (cgrid * kCoopThreads);
   int* blocksum = (int*)ws(c, S_SCAN, sizeof(int) * (cgrid + 1) + 64);
   if (!blocksum) return fail(c, APPD_ERR_OUT_OF_MEMORY, "dendrogram scan workspace");
+  unsigned* gbar = grid_barrier_word(c);
+  if (!gbar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
   if (cE <= 4) {
     // fused cooperative tours (the separate kernels below are the fallback)
     {
       // the adjacency (CSR) is built inside the tour: src / arc serve as degree / cursor
       int mm = m, nn = n, rt = root, lv = levels, st = steps;
       void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &src, &arc, &blocksum, &rt, &bufA, &bufB,
-                      &rk, &parent, &val, &child_of, &jm, &lv, &st};
+                      &rk, &parent, &val, &child_of, &jm, &lv, &st, &gbar};
       const void* fn = cl ? (cE <= 1 ? (const void*)k_tour1<1, true> : cE <= 2 ? (const void*)k_tour1<2, true>
                                                          : (const void*)k_tour1<4, true>)
                           : (cE <= 1 ? (const void*)k_tour1<1, false> : cE <= 2 ? (const void*)k_tour1<2, false>
@@ -581,7 +583,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     {
       int mm = m, nn = n, shh = sh, rt = root, st = steps;
       void* args[] = {&S, &mm, &nn, &shh, &child_of, &first, &sidx, &rt, &bufA, &bufB, &rk, &flag, &downs, &blocksum,
-                      &ew, &pi, &h, &st};
+                      &ew, &pi, &h, &st, &gbar};
       const void* fn = cl ? (cE <= 1 ? (const void*)k_tour2<1, true> : cE <= 2 ? (const void*)k_tour2<2, true>
                                                          : (const void*)k_tour2<4, true>)
                           : (cE <= 1 ? (const void*)k_tour2<1, false> : cE <= 2 ? (const void*)k_tour2<2, false>

@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(256) k_st_levels_lo(float* ST, int64_t m, int6
 
 // levels k0 .. levels-1 in one cooperative launch (a grid-wide barrier between levels)
 template <bool WIDEST>
-__global__ void __launch_bounds__(1024) k_st_levels_hi(float* ST, int64_t m, int64_t stride, int k0, int levels) {
-  cg::grid_group grid = cg::this_grid();
+__global__ void __launch_bounds__(1024) k_st_levels_hi(float* ST, int64_t m, int64_t stride, int k0, int levels,
+                                                       unsigned* bar) {
   for (int k = k0; k < levels; k++) {
     const int64_t half = 1ll << (k - 1);
     const float* prev = ST + (int64_t)(k - 1) * stride;
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(1024) k_st_levels_hi(float* ST, int64_t m, int
     const int64_t cnt = m - (1ll << k) + 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
       cur[i] = WIDEST ? fminf(prev[i], prev[i + half]) : fmaxf(prev[i], prev[i + half]);
-    grid.sync();
+    coop_grid_sync(bar);
   }
 }
 
@@ -116,7 +116,9 @@ appd_status launch_sparse_table(appd_ctx* c, float* ST, int64_t m, int levels, i
     int k0 = kl + 1, lv = levels;
     int64_t mm = m, st = stride;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (m + 1023) / 1024));
-    void* args[] = {&ST, &mm, &st, &k0, &lv};
+    unsigned* bar = grid_barrier_word(c);
+    if (!bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
+    void* args[] = {&ST, &mm, &st, &k0, &lv, &bar};
     const cudaError_t e = cudaLaunchCooperativeKernel(widest ? (const void*)k_st_levels_hi<true>
                                                               : (const void*)k_st_levels_hi<false>,
                                                        grid, 1024, args, 0, c->stream);

@@ -45,6 +45,7 @@ struct CoopSortArgs {
   // optional epilogue for component labels (keys = labels, sorted): first / end position
   // of every label, and per position the range of its own label
   int *cstart, *cend, *rs, *re;
+  unsigned* bar;  // grid barrier word (coop_grid_sync)
 };
 
 __device__ __forceinline__ unsigned end_bit_mask(int width, unsigned dmask) {
@@ -53,9 +54,9 @@ __device__ __forceinline__ unsigned end_bit_mask(int width, unsigned dmask) {
 
 // barrier of the persistent sort: the cooperative grid, or one cluster (small sorts)
 template <bool CL>
-__device__ __forceinline__ void sort_sync() {
+__device__ __forceinline__ void sort_sync(unsigned* bar) {
   if constexpr (CL) cg::this_cluster().sync();
-  else cg::this_grid().sync();
+  else coop_grid_sync(bar);
 }
 
 template <typename K, bool CL>
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
     for (int i = lo + tid; i < hi; i += kSortThreads) atomicAdd(sm + digit(src[i]), 1u);
     __syncthreads();
     for (int d = tid; d < ND; d += kSortThreads) a.cnt[(int64_t)d * G + b] = sm[d];
-    sort_sync<CL>();
+    sort_sync<CL>(a.bar);
     // ---- B: per digit, exclusive offsets of the CTAs and the digit total
     for (int d = gwarp; d < ND; d += nwarps) {
       unsigned carry = 0u;
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
       }
       if (lane == 0) a.dtot[d] = carry;
     }
-    sort_sync<CL>();
+    sort_sync<CL>(a.bar);
     // ---- C: digit bases (block scan of the totals, up to 4 per thread), then the
     // CTA's first position per digit
     {
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
         __syncthreads();
       }
     }
-    sort_sync<CL>();
+    sort_sync<CL>(a.bar);
   }
   if (a.cstart) {  // label ranges (k_comp_ranges, k_row_ranges)
     const int64_t tid64 = (int64_t)b * kSortThreads + tid, nt = (int64_t)G * kSortThreads;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) k_coop_sort(const CoopSortArg
       if (q == 0 || (int)a.kout[q - 1] != cq) a.cstart[cq] = (int)q;
       if (q == a.n - 1 || (int)a.kout[q + 1] != cq) a.cend[cq] = (int)q + 1;
     }
-    sort_sync<CL>();
+    sort_sync<CL>(a.bar);
     for (int64_t q = tid64; q < a.n; q += nt) {
       const int cq = (int)a.kout[q];
       a.rs[q] = a.cstart[cq];
@@ -226,6 +227,8 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
   a.dbits = dbits;
   a.cnt = reinterpret_cast<unsigned*>(w + kb + vb);
   a.dtot = a.cnt + (size_t)ND * G;
+  a.bar = grid_barrier_word(c);
+  if (!a.bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
   static std::atomic<unsigned long long> attr{0};
   if (needs_setup(attr, c)) {
     cudaFuncSetAttribute(k_coop_sort<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

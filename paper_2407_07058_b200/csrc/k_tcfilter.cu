@@ -573,6 +573,7 @@ struct PrepArgs {
   unsigned long long* dbg;  // development builds: %globaltimer after each phase (CTA 0)
   const int* perm;          // pack_tile: point at position p (nullptr: identity)
   InitList init;
+  unsigned* bar;  // grid barrier word (coop_grid_sync)
 };
 __device__ __forceinline__ void prep_mark(const PrepArgs& a, int i) {
   if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -717,7 +718,6 @@ __device__ __forceinline__ float pack_tile(const PrepArgs& a, float scale, bool 
 }
 
 __global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ double red[256];
   __shared__ float s_part[8][32], e_part[8][32];
   __shared__ float cs[1024];
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
     if (a.bad) a.bad[0] = a.bad[1] = a.bad[2] = KEY_NONE;
   }
   prep_mark(a, 1);
-  grid.sync();
+  coop_grid_sync(a.bar);
   prep_mark(a, 2);
   // phase 2: the centre, one CTA per column (a fixed tree: deterministic)
   for (int k = blockIdx.x; k < d; k += gridDim.x) {
@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
     if (threadIdx.x == 0) a.center[k] = (float)(red[0] / (double)a.n);
     __syncthreads();
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   prep_mark(a, 3);
   const bool cs_ok = d <= 1024;  // the centre staged in shared memory
   if (cs_ok) {
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(256, 3) k_tc_prep(const PrepArgs a) {
     block_max_sqrt(best, a.maxlen);
     if (badi != KEY_NONE) atomicMin(a.bad, badi);  // the smallest element index over all threads
   }
-  grid.sync();
+  coop_grid_sync(a.bar);
   prep_mark(a, 4);
   // phase 4: scale, packed operands, transpose, per-segment maxima
   const TcScale sc = tc_scale_of(*reinterpret_cast<volatile unsigned*>(a.maxlen));
@@ -917,6 +917,8 @@ static appd_status launch_prepare(appd_ctx* c, const float* X, TcState* st, cons
     a.dbg = nullptr;
     a.perm = nullptr;
     a.init = L;
+    a.bar = grid_barrier_word(c);
+    if (!a.bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
     static const bool times = dev_env("APPD_PREP_TIMES") != nullptr;
     if (times) a.dbg = reinterpret_cast<unsigned long long*>(ws(c, S_TMP2, 64));
     void* args[] = {&a};
