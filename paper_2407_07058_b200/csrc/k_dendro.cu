@@ -163,8 +163,7 @@ __global__ void k_emit(const unsigned long long* __restrict__ S, int m, int sh, 
 // 8-byte load of the successor's pair from the previous step's buffer (ping-pong A/B).
 template <int E>
 __global__ void k_rank_coop(const int* __restrict__ succ0, const int* __restrict__ rank0, int2* __restrict__ A,
-                            int2* __restrict__ B, int* __restrict__ out_rank, int L, int steps) {
-  cg::grid_group grid = cg::this_grid();
+                            int2* __restrict__ B, int* __restrict__ out_rank, int L, int steps, unsigned* bar) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   int nx[E], rk[E];
 #pragma unroll
@@ -174,7 +173,7 @@ __global__ void k_rank_coop(const int* __restrict__ succ0, const int* __restrict
     rk[e] = a < L ? rank0[a] : 0;
     if (a < L) A[a] = make_int2(nx[e], rk[e]);
   }
-  grid.sync();
+  coop_grid_sync(bar);
   for (int s = 0; s < steps; s++) {
     const int2* in = (s & 1) ? B : A;
     int2* out = (s & 1) ? A : B;
@@ -189,7 +188,7 @@ __global__ void k_rank_coop(const int* __restrict__ succ0, const int* __restrict
       }
       out[a] = make_int2(nx[e], rk[e]);
     }
-    grid.sync();
+    coop_grid_sync(bar);
   }
 #pragma unroll
   for (int e = 0; e < E; e++) {
@@ -201,8 +200,7 @@ __global__ void k_rank_coop(const int* __restrict__ succ0, const int* __restrict
 // all binary-lifting levels in one cooperative launch: level j of x from level j-1 of
 // its 2^(j-1)-th ancestor (own pair in registers: one dependent 8-byte load per level)
 template <int E>
-__global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
-  cg::grid_group grid = cg::this_grid();
+__global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels, unsigned* bar) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   int2 cur[E];
 #pragma unroll
@@ -221,7 +219,7 @@ __global__ void k_lift_coop(int2* __restrict__ jm, int n, int levels) {
       cur[e] = make_int2(q.x, max(cur[e].y, q.y));
       out[x] = cur[e];
     }
-    grid.sync();
+    coop_grid_sync(bar);
   }
 }
 
@@ -495,7 +493,9 @@ appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int2* A, int2*
   steps++;
   const int grid = coop_grid(c, L);
   const int E = (L + grid * kCoopThreads - 1) / (grid * kCoopThreads);
-  void* args[] = {&succ0, &rank0, &A, &B, &out_rank, &L, &steps};
+  unsigned* bar = grid_barrier_word(c);
+  if (!bar) return fail(c, APPD_ERR_OUT_OF_MEMORY, "grid barrier word");
+  void* args[] = {&succ0, &rank0, &A, &B, &out_rank, &L, &steps, &bar};
   const void* fn = E <= 1 ? (const void*)k_rank_coop<1> : E <= 2 ? (const void*)k_rank_coop<2>
                  : E <= 4 ? (const void*)k_rank_coop<4> : E <= 8 ? (const void*)k_rank_coop<8> : nullptr;
   if (!fn) return fail(c, APPD_ERR_UNSUPPORTED, "GPU dendrogram: %d arcs", L);
@@ -617,7 +617,7 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     const void* fn = E <= 1 ? (const void*)k_lift_coop<1> : E <= 2 ? (const void*)k_lift_coop<2>
                    : E <= 4 ? (const void*)k_lift_coop<4> : E <= 8 ? (const void*)k_lift_coop<8> : nullptr;
     if (!fn) return fail(c, APPD_ERR_UNSUPPORTED, "GPU dendrogram: n = %d", n);
-    void* args[] = {&jm, &nn, &lv};
+    void* args[] = {&jm, &nn, &lv, &gbar};
     APPD_CUDA(c, cudaLaunchCooperativeKernel(fn, grid, kCoopThreads, args, 0, c->stream));
     c->launches++;
   }
