@@ -382,15 +382,20 @@ __device__ __forceinline__ void atomic_min_lt(unsigned* a, unsigned v) {
 // to 0 (a zeroed word serves every launch and barrier) -- then spins with acquire loads on
 // the flip.  The same protocol as cooperative_groups' grid sync, without its full fences
 // before and after (the release add and the acquire load order the CTA's writes and reads).
+// The arrival is a fire-and-forget red.add: the generation bit it must see flip is read
+// before it (this CTA has not arrived yet, so the flip cannot have happened), and that read
+// overlaps the CTA's own barrier.
 __device__ __forceinline__ void coop_grid_sync(unsigned* bar) {
+  unsigned gen = 0;
+  if (threadIdx.x == 0) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar) : "memory");
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned inc = blockIdx.x == 0 ? (0x80000000u - (gridDim.x - 1u)) : 1u;
-    unsigned old, cur;
-    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(inc) : "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(inc) : "memory");
+    unsigned cur;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
-    } while (((old ^ cur) & 0x80000000u) == 0u);
+    } while (((gen ^ cur) & 0x80000000u) == 0u);
   }
   __syncthreads();
 }
