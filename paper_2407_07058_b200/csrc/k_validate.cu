@@ -14,10 +14,9 @@ __device__ __forceinline__ uint32_t canon_bits(float w) { return __float_as_uint
 // are read with 16-byte loads (256-byte row segments), all issued before any shared-
 // memory store; the transposed compare goes through padded shared memory.
 constexpr int VT = 64;
-__global__ void __launch_bounds__(256) k_validate_square(const float* __restrict__ W, int64_t n, int64_t row0,
+__global__ void __launch_bounds__(256, 6) k_validate_square(const float* __restrict__ W, int64_t n, int64_t row0,
                                                          int64_t rows, int64_t tiles, u64* __restrict__ out3) {
-  __shared__ float a[VT][VT + 1];
-  __shared__ float b[VT][VT + 1];
+  __shared__ float b[VT][VT + 1];  // the (J, I) tile; (I, J) stays in registers
   // map blockIdx.x to (I, J) with I <= J over a T x T upper triangle
   const int64_t p = blockIdx.x, T = tiles;
   // pairs before row I: f(I) = I*T - I*(I-1)/2; largest I with f(I) <= p
@@ -55,10 +54,6 @@ __global__ void __launch_bounds__(256) k_validate_square(const float* __restrict
 #pragma unroll
   for (int s4 = 0; s4 < VT / 16; s4++) {
     const int r = r0 + 16 * s4;
-    a[r][4 * c4 + 0] = va[s4].x;
-    a[r][4 * c4 + 1] = va[s4].y;
-    a[r][4 * c4 + 2] = va[s4].z;
-    a[r][4 * c4 + 3] = va[s4].w;
     b[r][4 * c4 + 0] = vb[s4].x;
     b[r][4 * c4 + 1] = vb[s4].y;
     b[r][4 * c4 + 2] = vb[s4].z;
@@ -66,33 +61,48 @@ __global__ void __launch_bounds__(256) k_validate_square(const float* __restrict
   }
   __syncthreads();
   // fast path: 32-bit tests only (non-finite: exponent all ones; asymmetric: different bits
-  // unless both are zeros of either sign; bad diagonal: a non-zero on the diagonal); the
+  // unless both are zeros of either sign; bad diagonal: a non-zero on the diagonal); each
+  // thread tests its own (I, J) elements (registers) against the transposed (J, I) tile
+  // (shared memory, one 33 KB tile pair became one 17 KB tile: more CTAs in flight); the
   // exact first offenders are located only in a tile that has one
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
   const bool diag_tile = I == J;
   unsigned flag = 0;
-  for (int r = ty; r < VT; r += 4) {
-    const uint32_t bx = __float_as_uint(a[r][tx]), by = __float_as_uint(b[tx][r]);
-    flag |= ((bx & 0x7F800000u) == 0x7F800000u) | ((by & 0x7F800000u) == 0x7F800000u);
-    flag |= (bx != by) & (((bx | by) << 1) != 0u);
-    if (diag_tile) flag |= (r == tx) & ((bx << 1) != 0u);
+#pragma unroll
+  for (int s4 = 0; s4 < VT / 16; s4++) {
+    const int r = r0 + 16 * s4;
+    const float xs[4] = {va[s4].x, va[s4].y, va[s4].z, va[s4].w};
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int cc = 4 * c4 + e;
+      const uint32_t bx = __float_as_uint(xs[e]), by = __float_as_uint(b[cc][r]);
+      flag |= ((bx & 0x7F800000u) == 0x7F800000u) | ((by & 0x7F800000u) == 0x7F800000u);
+      flag |= (bx != by) & (((bx | by) << 1) != 0u);
+      if (diag_tile) flag |= (r == cc) & ((bx << 1) != 0u);
+    }
   }
   if (!__syncthreads_or(flag)) return;
+  // (rare: a tile pair with an offender) the (I, J) elements again from W (L2)
   u64 bad_nf = KEY_NONE, bad_diag = KEY_NONE, bad_sym = KEY_NONE;
-  for (int r = ty; r < VT; r += 4) {
-    const int64_t li = I * VT + r, lj = J * VT + tx;
-    if (li < rows && lj < rows) {
-      const int64_t gi = row0 + li, gj = row0 + lj;
-      const float x = a[r][tx];  // W[gi][gj]
-      const float y = b[tx][r];  // W[gj][gi]
-      const u64 idx = (u64)(gi * n + gj);
-      const u64 idxT = (u64)(gj * n + gi);
-      if (!isfinite(x)) bad_nf = min(bad_nf, idx);
-      if (!isfinite(y)) bad_nf = min(bad_nf, idxT);
-      if (gi == gj) {
-        if (x != 0.0f) bad_diag = min(bad_diag, idx);
-      } else if (canon_bits(x) != canon_bits(y)) {
-        bad_sym = min(bad_sym, gi < gj ? idx : idxT);
+#pragma unroll 1
+  for (int s4 = 0; s4 < VT / 16; s4++) {
+    const int r = r0 + 16 * s4;
+#pragma unroll 1
+    for (int e = 0; e < 4; e++) {
+      const int cc = 4 * c4 + e;
+      const int64_t li = I * VT + r, lj = J * VT + cc;
+      if (li < rows && lj < rows) {
+        const int64_t gi = row0 + li, gj = row0 + lj;
+        const float x = W[li * n + row0 + lj];  // W[gi][gj]
+        const float y = b[cc][r];  // W[gj][gi]
+        const u64 idx = (u64)(gi * n + gj);
+        const u64 idxT = (u64)(gj * n + gi);
+        if (!isfinite(x)) bad_nf = min(bad_nf, idx);
+        if (!isfinite(y)) bad_nf = min(bad_nf, idxT);
+        if (gi == gj) {
+          if (x != 0.0f) bad_diag = min(bad_diag, idx);
+        } else if (canon_bits(x) != canon_bits(y)) {
+          bad_sym = min(bad_sym, gi < gj ? idx : idxT);
+        }
       }
     }
   }
