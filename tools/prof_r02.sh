@@ -20,3 +20,8 @@ ncu --set full --clock-control none --import-source on -k regex:k_prim -s 3 -c 2
 ncu --set full --clock-control none --import-source on -k regex:"k_validate_square|k_scan_weights_topk|k_fill" -s 6 -c 3 -o gpurun_out/r02/full_c3 python tools/cfg_times.py C3 > /dev/null 2>&1; echo "c3 $?"
 for r in fill tcf list topk prep prim c3; do python tools/ncu_summary.py gpurun_out/r02/full_$r.ncu-rep > gpurun_out/r02/r02_$r.metrics.txt 2>&1; done
 ls -la gpurun_out/r02
+# late round 2: the cooperative kernels on the lighter grid barrier (tours, contraction)
+ncu --set full --clock-control none --import-source on -k regex:"k_tour1|k_tour2|k_contract" -s 3 -c 3 -o gpurun_out/r02/full_coop $CMD > /dev/null 2>&1; echo "coop $?"
+python tools/ncu_summary.py gpurun_out/r02/full_coop.ncu-rep > gpurun_out/r02/r02_coop.metrics.txt 2>&1
+# (the GPU suite runs separately)
+rm -f gpurun_out/r02/*.ncu-rep; du -sh gpurun_out
