@@ -27,7 +27,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kSortThreads = 1024;
-constexpr int kMaxDigitBits = 8;
+constexpr int kMaxDigitBits = 11;  // 2048 counters per CTA (8 KB of shared memory)
 constexpr int kSortCluster = 8;  // CTAs of the single-cluster sort (portable size)
 
 template <typename K>
@@ -196,13 +196,16 @@ appd_status coop_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
                       int* rs = nullptr, int* re = nullptr) {
   if (count <= 0) return APPD_OK;
   if (count > (int64_t)1 << 30) return fail(c, APPD_ERR_UNSUPPORTED, "sort of %lld keys", (long long)count);
-  const int bits = std::max(1, end_bit - begin_bit);
-  const int passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
-  const int dbits = (bits + passes - 1) / passes;
-  const int ND = 1 << dbits;
   // small sorts (every CTA of one cluster holds one tile of 1024 keys): one cluster (at
   // two tiles per CTA the library sort measured faster)
   const bool cl = count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads;
+  // digits: up to 11 bits (fewer passes) on the grid; 8 in the cluster, where a pass over
+  // a few thousand keys is dominated by its histogram of 2^bits counters
+  const int maxd = cl ? 8 : kMaxDigitBits;
+  const int bits = std::max(1, end_bit - begin_bit);
+  const int passes = (bits + maxd - 1) / maxd;
+  const int dbits = (bits + passes - 1) / passes;
+  const int ND = 1 << dbits;
   const int G = cl ? kSortCluster : c->sm_count;
   const bool vals = vin || iota_vals;
   const size_t kb = (sizeof(K) * (size_t)count + 255) & ~(size_t)255, vb = vals ? (sizeof(int) * (size_t)count + 255) & ~(size_t)255 : 0;
@@ -281,7 +284,10 @@ appd_status path_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
                       int end_bit) {
   // one digit pass, or a small sort (one cluster, its barriers far cheaper than the
   // library's per-pass launches): the cooperative sort; else the library's onesweep
-  if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads))
+  // Up to 2^17 keys the cooperative sort also takes multi-pass keys (11-bit digits: the MST
+  // edges' 31 weight bits in 3 passes instead of the library's 4 launches of 8 bits)
+  if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads) ||
+      (count <= (1 << 17) && end_bit - begin_bit <= 3 * kMaxDigitBits))
     return coop_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
   return lib_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
 }
