@@ -1104,12 +1104,17 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
   float* ST = (float*)ws(c, S_ST, sizeof(float) * stride * levels);
   if (!pi || !pos || !ST) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
   c->dend_n = n;
+  bool pos_fused = false, rowpos_fused = false;
   if (c->opt.dendrogram != 1) {
     // v2: Prim order of the MST on the GPU (k_dendro.cu); h lands in the sparse table's level 0
 #ifdef APPD_DEV_HOOKS
     dev_check(c, "edges", d_eu, d_ev, m, nullptr, n);
 #endif
-    if ((s = gpu_dendrogram(c, d_eu, d_ev, d_ew, n, pi, ST))) return s;
+    // the fused tours also write pos = pi^-1 and, for a one-rank in-HBM fill, the identity
+    // row positions (k_positions / k_iota folded in)
+    int* rp_out = (c->opt.world == 1 && !c->stream_out && !c->sink) ? (int*)ws(c, S_ROWPOS, sizeof(int) * n) : nullptr;
+    if ((s = gpu_dendrogram(c, d_eu, d_ev, d_ew, n, pi, ST, pos, rp_out, &pos_fused))) return s;
+    rowpos_fused = pos_fused && rp_out != nullptr;
 #ifdef APPD_DEV_HOOKS
     dev_check(c, "dendrogram", nullptr, nullptr, 0, pi, n);
 #endif
@@ -1139,7 +1144,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
   stage_event(c, 4);
 
   // ---- a6: fill prep ----
-  if ((s = launch_positions(c, pi, n, pos))) return s;
+  if (!pos_fused && (s = launch_positions(c, pi, n, pos))) return s;
   // fp64: ranks increase along the Kruskal order in either sense, so the max-combination
   const bool widest_fill = sense < 0 && !f64;
   if ((s = launch_sparse_table(c, ST, m, levels, stride, widest_fill))) return s;
@@ -1261,7 +1266,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     return APPD_OK;
   }
   if (c->opt.world == 1) {
-    if ((s = launch_iota(c, rowpos, n))) return s;
+    if (!rowpos_fused && (s = launch_iota(c, rowpos, n))) return s;
   } else {
     int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (rows + 1));
     int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (rows + 1));

@@ -532,7 +532,7 @@ void host_dendrogram(const u64* sorted_keys, int64_t n, const KeySpec& ks, int32
 void host_dendrogram_uvw(const int32_t* eu, const int32_t* ev, const float* ew, int64_t n, int32_t* pi, float* h,
                          int32_t* scratch /* 8 n */);
 appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, const float* ew, int64_t n,
-                           int32_t* pi, float* h);
+                           int32_t* pi, float* h, int* pos_out, int* rowpos_out, bool* fused_pos);
 appd_status launch_decode_edges(appd_ctx* c, const u64* keys, int64_t m, const KeySpec& ks, int32_t* eu,
                                 int32_t* ev, float* ew);
 void* pinned_host(appd_ctx* c, size_t bytes);  // grows ctx->pinned

@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
                                                 int n, int* sarc, int* start, int* end, int* posarc, int* deg,
                                                 int* cursor, int* blocksum, int root, int2* A, int2* B, int* rkout,
                                                 int* parent, int* val, int* child_of, int2* jm, int levels,
-                                                int steps, unsigned* bar) {
+                                                int steps, unsigned* bar, int sh,
+                                                unsigned long long* __restrict__ key) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   // adjacency (CSR by source vertex; the order inside a list is irrelevant: the rooted
@@ -397,6 +398,18 @@ __global__ void __launch_bounds__(1024) k_tour1(const int32_t* __restrict__ eu, 
     }
     all_sync<CL>(bar);
   }
+  // record parents (k_record_parent): nearest ancestor with a larger val, by the lifting
+  // levels just written; one key per edge rank
+  for (int v = tid; v < n; v += T) {
+    if (v == root) continue;
+    const int w = val[v];
+    int cur = v;
+    for (int j = levels - 1; j >= 0; j--) {
+      const int2 q = jm[(int64_t)j * n + cur];  // (2^j-th ancestor, max val on the way)
+      if (q.y < w) cur = q.x;
+    }
+    key[w] = ((unsigned long long)(unsigned)parent[cur] << sh) | (unsigned)w;
+  }
 }
 
 template <int E, bool CL>
@@ -404,7 +417,8 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
                                                 const int* __restrict__ child_of, int* first, int* sidx, int root,
                                                 int2* A, int2* B, int* rkout, int* flag, int* downs, int* blocksum,
                                                 const float* __restrict__ ew, int32_t* __restrict__ pi,
-                                                float* __restrict__ h, int steps, unsigned* bar) {
+                                                float* __restrict__ h, int steps, unsigned* bar,
+                                                int* __restrict__ pos, int* __restrict__ rowpos) {
   const int T = gridDim.x * blockDim.x, tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = 2 * m;
   const unsigned long long lo = (1ull << sh) - 1;
@@ -452,7 +466,13 @@ __global__ void __launch_bounds__(1024) k_tour2(const unsigned long long* __rest
     const int pre = 1 + downs[L - 1 - rkout[2 * i]];
     pi[pre] = v;
     h[pre - 1] = ew[e];
-    if (i == 0) pi[0] = root;
+    if (pos) pos[v] = pre;  // (k_positions: pos = pi^-1)
+    if (rowpos) rowpos[pre] = pre;
+    if (i == 0) {
+      pi[0] = root;
+      if (pos) pos[root] = 0;
+      if (rowpos) rowpos[0] = 0;
+    }
   }
 }
 
@@ -508,7 +528,8 @@ appd_status list_rank(appd_ctx* c, int L, int* succ0, int* rank0, int2* A, int2*
 
 // eu/ev/ew: MST edges in ascending key order (device); pi, h: device outputs
 appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, const float* ew, int64_t n64,
-                           int32_t* pi, float* h) {
+                           int32_t* pi, float* h, int* pos_out, int* rowpos_out, bool* fused_pos) {
+  if (fused_pos) *fused_pos = false;
   const int n = (int)n64, m = n - 1;
   if (n == 1) {
     APPD_CUDA(c, cudaMemsetAsync(pi, 0, sizeof(int32_t), c->stream));
@@ -568,28 +589,27 @@ appd_status gpu_dendrogram(appd_ctx* c, const int32_t* eu, const int32_t* ev, co
     // fused cooperative tours (the separate kernels below are the fallback)
     {
       // the adjacency (CSR) is built inside the tour: src / arc serve as degree / cursor
-      int mm = m, nn = n, rt = root, lv = levels, st = steps;
+      int mm = m, nn = n, rt = root, lv = levels, st = steps, shh1 = sh;
       void* args[] = {&eu, &ev, &mm, &nn, &sarc, &start, &end, &posarc, &src, &arc, &blocksum, &rt, &bufA, &bufB,
-                      &rk, &parent, &val, &child_of, &jm, &lv, &st, &gbar};
+                      &rk, &parent, &val, &child_of, &jm, &lv, &st, &gbar, &shh1, &key};
       const void* fn = cl ? (cE <= 1 ? (const void*)k_tour1<1, true> : cE <= 2 ? (const void*)k_tour1<2, true>
                                                          : (const void*)k_tour1<4, true>)
                           : (cE <= 1 ? (const void*)k_tour1<1, false> : cE <= 2 ? (const void*)k_tour1<2, false>
                                                          : (const void*)k_tour1<4, false>);
       if ((s = launch_tour(c, fn, cl, cgrid, args))) return s;
     }
-    k_record_parent<<<gn, 256, 0, c->stream>>>(jm, levels, n, parent, val, root, sh, key);
-    APPD_LAUNCHED(c);
     if ((s = sort_keys_u64_bits64(c, key, S, m, sh, 2 * sh))) return s;  // key[w] is in val order: a stable sort on rp
     {
       int mm = m, nn = n, shh = sh, rt = root, st = steps;
       void* args[] = {&S, &mm, &nn, &shh, &child_of, &first, &sidx, &rt, &bufA, &bufB, &rk, &flag, &downs, &blocksum,
-                      &ew, &pi, &h, &st, &gbar};
+                      &ew, &pi, &h, &st, &gbar, &pos_out, &rowpos_out};
       const void* fn = cl ? (cE <= 1 ? (const void*)k_tour2<1, true> : cE <= 2 ? (const void*)k_tour2<2, true>
                                                          : (const void*)k_tour2<4, true>)
                           : (cE <= 1 ? (const void*)k_tour2<1, false> : cE <= 2 ? (const void*)k_tour2<2, false>
                                                          : (const void*)k_tour2<4, false>);
       if ((s = launch_tour(c, fn, cl, cgrid, args))) return s;
     }
+    if (fused_pos) *fused_pos = true;
     return APPD_OK;
   }
   // A: adjacency
