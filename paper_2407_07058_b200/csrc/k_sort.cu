@@ -284,10 +284,11 @@ appd_status path_sort(appd_ctx* c, const K* kin, K* kout, const int* vin, int* v
                       int end_bit) {
   // one digit pass, or a small sort (one cluster, its barriers far cheaper than the
   // library's per-pass launches): the cooperative sort; else the library's onesweep
-  // Up to 2^17 keys the cooperative sort also takes multi-pass keys (11-bit digits: the MST
-  // edges' 31 weight bits in 3 passes instead of the library's 4 launches of 8 bits)
+  // From 8K to 2^17 keys the cooperative sort also takes multi-pass keys (11-bit digits: the
+  // MST edges' 31 weight bits in 3 passes instead of the library's 4 launches of 8 bits);
+  // below 2K keys the library's single-tile sort is the fastest
   if (end_bit - begin_bit <= kMaxDigitBits || (count >= 2048 && count <= (int64_t)kSortCluster * kSortThreads) ||
-      (count <= (1 << 17) && end_bit - begin_bit <= 3 * kMaxDigitBits))
+      (count > (int64_t)kSortCluster * kSortThreads && count <= (1 << 17) && end_bit - begin_bit <= 3 * kMaxDigitBits))
     return coop_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
   return lib_sort<K>(c, kin, kout, vin, vout, count, begin_bit, end_bit);
 }
