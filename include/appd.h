@@ -32,6 +32,12 @@
  *     APPD_ERR_INVALID_ARGUMENT.  The caller owns every buffer it passes.
  *   - Calls enqueue work on the context's stream and return after it has
  *     completed (so data-dependent validation errors can be reported).
+ *     Ordering against work on OTHER streams is the caller's: the
+ *     library-owned stream (cuda_stream NULL) is a cudaStreamNonBlocking
+ *     stream, unordered with the legacy default stream, so inputs produced
+ *     on another stream must be complete (or that stream passed through
+ *     appd_set_stream) before the call.  The Python binding passes the
+ *     caller's torch.cuda.current_stream(device) on every call.
  *   - Every call returns a status; nothing throws across the ABI.  After a
  *     CUDA or NCCL failure the context is poisoned: later calls return
  *     APPD_ERR_POISONED and only appd_destroy is valid.
