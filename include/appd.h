@@ -125,7 +125,10 @@ typedef struct {
    * callback, which must all-reduce `count` uint64 words in place over the `world` ranks
    * (op APPD_REDUCE_MIN or APPD_REDUCE_MAX, unsigned order) and return 0; any other value
    * makes the call fail with APPD_ERR_NCCL (context poisoned).  For MPI / gloo users and
-   * the multi-process tests; results are identical to the NCCL backend. */
+   * the multi-process tests; results are identical to the NCCL backend.
+   * world 1 with nccl_unique_id or host_allreduce set: the solve takes the same
+   * multi-rank path over a one-rank communicator (every exchange still issued), so the
+   * transport can be checked on one GPU; results equal the plain world-1 solve's. */
   int32_t (*host_allreduce)(void* user, uint64_t* words, int64_t count, int32_t op);
   void* host_allreduce_user;
   int32_t timeout_ms;            /* world > 1, NCCL backend: deadline of every wait on work that

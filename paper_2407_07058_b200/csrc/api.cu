@@ -151,6 +151,9 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   appd_ctx* c = new appd_ctx();
   c->opt = o;
   c->device = o.device;
+  // world 1 with an explicit communicator or host exchange runs the multi-rank path over
+  // one rank (the transport exercised on one GPU; results equal the world-1 path's)
+  c->coll = o.world > 1 || o.nccl_unique_id != nullptr || o.host_allreduce != nullptr;
   std::memset(&c->stats, 0, sizeof c->stats);
   c->stats.struct_size = sizeof(appd_stats);
   if (cudaSetDevice(c->device) != cudaSuccess) {
@@ -183,7 +186,7 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
     cudaGetLastError();
     c->pinned_small_dev = nullptr;  // publish() falls back to copies
   }
-  if (o.world > 1) {
+  if (c->coll) {
     appd_status s = nccl_init(c, o.nccl_unique_id, o.rank, o.world);
     if (s != APPD_OK) {
       appd_destroy(c);
@@ -435,7 +438,7 @@ static bool prim_requested(const appd_ctx* c) { return c->opt.variant == APPD_VA
 
 static bool want_prim(const appd_ctx* c, int64_t n, int64_t d, bool points, bool f64) {
   if (f64 || c->stream_out || c->sink || n < 2 || c->opt.wide_keys == 1) return false;
-  if (!points && c->opt.world > 1) return false;
+  if (!points && c->coll) return false;
   if (!prim_fits(n, d, points)) return false;
   if (prim_requested(c)) return true;
   if (c->opt.variant != APPD_VARIANT_AUTO) return false;
@@ -475,7 +478,7 @@ static appd_status solve_prim(appd_ctx* c, const float* W, const float* X, int64
   if (bad) APPD_PUBLISH(c, hbad, bad, 3 * sizeof(u64));
   for (int e = 2; e <= 4; e++) stage_event(c, e);
   const int* rows_sorted = pi;
-  if (c->opt.world > 1 && !fused) {  // replicated Prim, this rank's rows in leaf order
+  if (c->coll && !fused) {  // replicated Prim, this rank's rows in leaf order
     int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (rows + 1));
     int* rs = (int*)ws(c, S_ROWS_SORTED, sizeof(int) * (rows + 1));
     if (!keys || !rs) return fail(c, APPD_ERR_OUT_OF_MEMORY, "fill workspace");
@@ -600,7 +603,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
   c->err_i = c->err_j = -1;
   c->last_error.clear();
   host_mark("solve entry", true);
-  if (c->opt.world > 1) {
+  if (c->coll) {
     appd_status sa = agree(c, X, n, points ? d : 0, points ? 2 : (f64 ? 3 : 1));
     if (sa) return sa;
   }
@@ -620,7 +623,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
                 c->opt.metric);
   if (points && sense < 0 && c->opt.points_engine == 2)
     return fail(c, APPD_ERR_UNSUPPORTED, "the tensor-core engine finds minimum edges only (widest sense: exact engine)");
-  const bool defer_validation = points && c->opt.validate && c->opt.world == 1 && c->opt.points_engine != 1 &&
+  const bool defer_validation = points && c->opt.validate && !c->coll && c->opt.points_engine != 1 &&
                                 (c->opt.points_engine == 2 || n > kExactEngineMaxN) && c->opt.metric == 0 &&
                                 sense > 0 && n >= 2 && n <= kMaxPackedPoints && c->opt.wide_keys != 1;
   u64* hbad = reinterpret_cast<u64*>(c->pinned_small + 40);  // 3 words, pinned
@@ -648,7 +651,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     u64 hb[3];
     APPD_SYNC(c);
     memcpy(hb, hbad, sizeof hb);
-    if (c->opt.world > 1) {
+    if (c->coll) {
       // every rank must agree on the verdict (else the others would hang in the next collective)
       u64* agree = (u64*)ws(c, S_TMP, sizeof(u64) * 3);
       if (!agree) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
@@ -812,8 +815,8 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       if (!WCM) return fail(c, APPD_ERR_OUT_OF_MEMORY, "component matrix");
       bool ovf = false;
       if (c->opt.timing >= 2) cudaEventRecord(c->ev[8], c->stream);
-      if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf, c->opt.world > 1))) return s;
-      if (c->opt.world > 1) {  // every rank must take the same branch
+      if ((s = tcf_cm(c, &tc, X, comp, k, WCM, rt_begin, rt_end, &ovf, c->coll))) return s;
+      if (c->coll) {  // every rank must take the same branch
         u64* flag = (u64*)ws(c, S_TMP, sizeof(u64));
         if (!flag) return fail(c, APPD_ERR_OUT_OF_MEMORY, "flag");
         const u64 hf = ovf ? 1 : 0;
@@ -839,7 +842,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
         cm_timing_pending = c->opt.timing != 0;  // read after the final synchronisation
         c->stats.cm_k = (int)k;
         c->stats.tcscan_launches++;
-        if (c->opt.world == 1) {  // upper-triangle pass: row block rb against columns >= 512 rb
+        if (!c->coll) {  // upper-triangle pass: row block rb against columns >= 512 rb
           double pairs = 0.0;
           for (int64_t rb = 0; rb * 512 < n; rb++) pairs += (double)std::min<int64_t>(512, n - rb * 512) * (n - rb * 512);
           c->stats.tcscan_flops += 2.0 * pairs * d;
@@ -902,7 +905,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       if ((s = launch_fill_u64(c, compw, k, KEY_NONE))) return s;
       if ((s = launch_scan_points(c, XT, n, npad, dpad, row0, rows, cmp, rowbest, true))) return s;
       if ((s = launch_wide_compw(c, rowbest, cmp, row0, row0 + rows, compw))) return s;
-      if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compw, k))) return s;
+      if (c->coll && (s = nccl_allreduce_min_u64(c, compw, k))) return s;
       s = launch_wide_compbest(c, rowbest, cmp, row0, row0 + rows, compw, compbest);
       c->stats.exact_rounds++;
     } else if (points) {
@@ -931,12 +934,12 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     c->stats.scan_launches += c->launches - l0;
     if (c->opt.timing >= 2) cudaEventRecord(c->ev[9], c->stream);
     host_mark("round scan queued");
-    if (c->opt.world > 1 && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
+    if (c->coll && (s = nccl_allreduce_min_u64(c, compbest, k))) return s;
     // the next round's cache lookup rides on this round's synchronisation (labels are
     // final): one rank, fused into the cooperative contraction when it can run
     LookupArgs la;
     bool fused_lookup = false;
-    if (use_tc && tc.topk && c->opt.world == 1) {
+    if (use_tc && tc.topk && !c->coll) {
       la.r0 = (int)tc.cache_r0;
       la.r1 = (int)tc.cache_r1;
       la.K = tc.topk;
@@ -946,7 +949,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       la.need = tc.need;
       la.count = tc.counters + 3;
       la.list = tc.rows_list;
-    } else if (wtopk && c->opt.world == 1) {
+    } else if (wtopk && !c->coll) {
       la.r0 = (int)row0;
       la.r1 = (int)(row0 + rows);
       la.K = wtopk;
@@ -978,11 +981,11 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
         w_pending = true;
       }
     } else {
-      if (use_tc && tc.topk && c->opt.world == 1) {
+      if (use_tc && tc.topk && !c->coll) {
         if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
         if ((s = tcf_lookup_async(c, &tc, comp, compbest))) return s;
       }
-      if (wtopk && c->opt.world == 1) {
+      if (wtopk && !c->coll) {
         if ((s = launch_fill_u64(c, compbest, n, KEY_NONE))) return s;
         if ((s = w_lookup_async())) return s;
       }
@@ -1112,7 +1115,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
 #endif
     // the fused tours also write pos = pi^-1 and, for a one-rank in-HBM fill, the identity
     // row positions (k_positions / k_iota folded in)
-    int* rp_out = (c->opt.world == 1 && !c->stream_out && !c->sink) ? (int*)ws(c, S_ROWPOS, sizeof(int) * n) : nullptr;
+    int* rp_out = (!c->coll && !c->stream_out && !c->sink) ? (int*)ws(c, S_ROWPOS, sizeof(int) * n) : nullptr;
     if ((s = gpu_dendrogram(c, d_eu, d_ev, d_ew, n, pi, ST, pos, rp_out, &pos_fused))) return s;
     rowpos_fused = pos_fused && rp_out != nullptr;
 #ifdef APPD_DEV_HOOKS
@@ -1265,7 +1268,7 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
     }
     return APPD_OK;
   }
-  if (c->opt.world == 1) {
+  if (!c->coll) {
     if (!rowpos_fused && (s = launch_iota(c, rowpos, n))) return s;
   } else {
     int* keys = (int*)ws(c, S_TMP, sizeof(int) * 2 * (rows + 1));
@@ -1345,7 +1348,7 @@ extern "C" appd_status appd_solve_weights_f64(appd_ctx* c, const double* W, int6
   if (s) return s;
   if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
   if (n > 92682) return fail(c, APPD_ERR_UNSUPPORTED, "weights mode supports n <= 92682 (32-bit pair index)");
-  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_weights_f64 runs on one rank (world = %d)", c->opt.world);
+  if (c->coll) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_weights_f64 runs on one rank without collectives (world = %d)", c->opt.world);
   if ((s = check_device_ptr(c, W, "W"))) return s;
   if ((s = check_device_ptr(c, M, "M"))) return s;
   if ((const void*)W == (const void*)M) return fail(c, APPD_ERR_INVALID_ARGUMENT, "W and M must not alias");
@@ -1367,7 +1370,7 @@ extern "C" appd_status appd_floyd_weights(appd_ctx* c, const float* W, int64_t n
   appd_status s = enter(c);
   if (s) return s;
   if (n < 1) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n = %lld < 1", (long long)n);
-  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_floyd_weights runs on one rank (world = %d)", c->opt.world);
+  if (c->coll) return fail(c, APPD_ERR_UNSUPPORTED, "appd_floyd_weights runs on one rank without collectives (world = %d)", c->opt.world);
   if (n > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "appd_floyd_weights: n = %lld > 65536 (O(n^3))", (long long)n);
   if ((s = check_device_ptr(c, W, "W"))) return s;
   if ((s = check_device_ptr(c, M, "M"))) return s;
@@ -1456,7 +1459,7 @@ extern "C" appd_status appd_solve_points_sink(appd_ctx* c, const float* X, int64
   if (n < 1 || d < 1 || block_rows < 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n, d, block_rows");
   if (n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
   if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
-  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_sink runs on one rank");
+  if (c->coll) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_sink runs on one rank");
   const int64_t R = block_rows ? block_rows : std::max<int64_t>(128, ((int64_t)1 << 28) / n);
   float* din = (float*)ws(c, S_HOST_IN, sizeof(float) * n * d);
   if (!din) return fail(c, APPD_ERR_OUT_OF_MEMORY, "device copy of X");
@@ -1481,7 +1484,7 @@ extern "C" appd_status appd_solve_points_stream(appd_ctx* c, const float* X, int
   if (n < 1 || d < 1 || block_rows < 0) return fail(c, APPD_ERR_INVALID_ARGUMENT, "n, d, block_rows");
   if (n > kMaxPoints) return fail(c, APPD_ERR_UNSUPPORTED, "points mode supports n <= 2^20");
   if (d > 65536) return fail(c, APPD_ERR_UNSUPPORTED, "d > 65536");
-  if (c->opt.world != 1) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_stream runs on one rank");
+  if (c->coll) return fail(c, APPD_ERR_UNSUPPORTED, "appd_solve_points_stream runs on one rank");
   // default block: 1 GiB of rows per buffer (two buffers), at least 128 rows
   const int64_t R = block_rows ? block_rows : std::max<int64_t>(128, ((int64_t)1 << 28) / n);
   float* din = (float*)ws(c, S_HOST_IN, sizeof(float) * n * d);

@@ -102,6 +102,9 @@ struct appd_ctx {
   appd_stats stats;
   int64_t launches = 0;  // kernels launched in the current solve
   void* nccl_comm = nullptr;
+  // the solve takes the multi-rank path (every exchange a collective): world > 1, or world 1
+  // with an explicit communicator (nccl_unique_id) or host exchange (host_allreduce)
+  bool coll = false;
   int sm_count = 148;
   // workspace (grown on demand)
   appd::DevBuf buf[96];

@@ -1444,7 +1444,7 @@ appd_status tcf_cm(appd_ctx* c, TcState* st, const float* X, const int* comp, in
   P.rb_begin = (int)rb_begin;
   P.rb_end = (int)rb_end;
   // one rank: every unordered pair is needed from one side only -> upper-triangle pass
-  P.upper = c->opt.world == 1 && !dev_env("APPD_CM_FULL");
+  P.upper = !c->coll && !dev_env("APPD_CM_FULL");
   if (c->opt.timing) cudaEventRecord(c->ev[10], c->stream);
   if ((s = launch_tcf_scan(c, 7, P))) return s;
   if (c->opt.timing) cudaEventRecord(c->ev[11], c->stream);

@@ -104,7 +104,7 @@ static appd_status nccl_abort(appd_ctx* c, const char* why) {
 // diverged peer ends the call with APPD_ERR_NCCL instead of a hang.
 appd_status sync_stream(appd_ctx* c) {
   if (appd_status s = publish_flush(c)) return s;
-  if (c->opt.world == 1 || !c->nccl_comm) {
+  if (!c->coll || !c->nccl_comm) {
     cudaError_t e = cudaStreamSynchronize(c->stream);
     return e == cudaSuccess ? APPD_OK : cuda_fail(c, e, "cudaStreamSynchronize");
   }

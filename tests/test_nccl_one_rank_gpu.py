@@ -1,0 +1,122 @@
+"""The NCCL transport of the multi-rank path, executed on ONE GPU (
+DESIGN.md §7).
+
+A context created with world = 1 AND an explicit ncclUniqueId builds a one-rank NCCL
+communicator and runs the multi-rank code path over it: the solve-start agreement, the
+validation-verdict all-reduce, the row-sharded Boruvka scans with the per-round
+ncclAllReduce(min, uint64) of component keys, the component-matrix all-reduce, and the
+deadline-polled waits (cudaStreamQuery + ncclCommGetAsyncError) -- every collective issued
+through the real NCCL library on the B200, with one rank.  One process, one GPU: no rank
+waits on another.  The results must be bit-identical to the oracle's (Algorithm 4)
+and to the plain world-1 solve; the stats must show the collectives were issued.
+The same cases run with the host exchange backend at world 1 (identity callback).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from synth import generators as G
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")  # one-rank bootstrap on loopback
+    import paper_2407_07058_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def nccl_ctx(P):
+    c = P.Context(world=1, rank=0, nccl_id=P.appd_get_nccl_unique_id(), timing=True, timeout_ms=60000)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def host_ctx(P):
+    calls = []
+
+    def identity(words, op):  # one rank: the all-reduce of one contribution is itself
+        calls.append((len(words), op))
+        return words
+
+    c = P.Context(world=1, rank=0, host_allreduce=identity, timing=True)
+    c._calls = calls
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def plain_ctx(P):
+    c = P.Context(timing=True)
+    yield c
+    c.close()
+
+
+CASES = [
+    ("c2_4096", "points", lambda: G.config("C2", n=4096), {}),
+    ("c4_shape_8192", "points", lambda: G.config("C4", n=8192), {}),
+    ("c5_shape_6000_dups", "points", lambda: G.config("C5", n=6000), {}),
+    ("points_blobs_1500_d7", "points", lambda: G.random_points(1500, 7, 31, "blobs"), {}),
+    ("c3_shape_4096", "weights", lambda: G.config("C3", n=4096), {}),
+    ("weights_ties_1031", "weights", lambda: G.random_weights(1031, 23, "ties"), {}),
+]
+
+
+def _solve(ctx, mode, A):
+    t = torch.from_numpy(np.ascontiguousarray(A, np.float32)).cuda()
+    M = ctx.solve_points(t) if mode == "points" else ctx.solve_weights(t)
+    return M.cpu().numpy()
+
+
+def _oracle(mode, A):
+    return oracle.appd_points(A) if mode == "points" else oracle.appd_weights(A)
+
+
+@pytest.mark.parametrize("name,mode,make,opts", CASES, ids=[c[0] for c in CASES])
+def test_nccl_one_rank_matches_oracle_and_world1(nccl_ctx, plain_ctx, name, mode, make, opts):
+    A = make()
+    got = _solve(nccl_ctx, mode, A)
+    st = nccl_ctx.stats()
+    assert st["collectives"] >= 2, st  # agreement + at least one round exchange went through NCCL
+    want = _oracle(mode, A)
+    assert got.shape == want.shape
+    assert np.array_equal(_bits(got), _bits(want)), f"{name}: NCCL one-rank solve differs from the oracle"
+    ref = _solve(plain_ctx, mode, A)
+    assert plain_ctx.stats()["collectives"] == 0
+    assert np.array_equal(_bits(got), _bits(ref))
+
+
+@pytest.mark.parametrize("name,mode,make,opts", CASES[:2] + CASES[4:5], ids=[c[0] for c in CASES[:2] + CASES[4:5]])
+def test_host_exchange_one_rank_matches_oracle(host_ctx, name, mode, make, opts):
+    A = make()
+    host_ctx._calls.clear()
+    got = _solve(host_ctx, mode, A)
+    assert host_ctx.stats()["collectives"] == len(host_ctx._calls) >= 2
+    want = _oracle(mode, A)
+    assert np.array_equal(_bits(got), _bits(want)), f"{name}: host-exchange one-rank solve differs from the oracle"
+
+
+def test_nccl_one_rank_validation_error(P, nccl_ctx):
+    """The verdict all-reduce over NCCL: a non-finite input is reported with its first
+    offender (a complete graph with finite weights), and the context stays usable."""
+    W = G.random_weights(300, 5, "uniform")
+    W[7, 11] = W[11, 7] = np.nan
+    with pytest.raises(P.AppdError) as e:
+        _solve(nccl_ctx, "weights", W)
+    assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index in ((7, 11), (11, 7)), (e.value.name, e.value.index)
+    W2 = G.random_weights(300, 6, "uniform")
+    assert np.array_equal(_bits(_solve(nccl_ctx, "weights", W2)), _bits(oracle.appd_weights(W2)))
