@@ -59,6 +59,7 @@ def run(name):
     ref = None
     for label, extra in (("plain world 1", {}), ("one-rank NCCL", "nccl")):
         opts = {"nccl_id": P.appd_get_nccl_unique_id()} if extra == "nccl" else {}
+        M.fill_(float("nan"))  # same_M must come from this context's own writes
         with P.Context(stream=s.cuda_stream, timing=True, **opts) as c:
             med = timed(c, f, s, flush)
             st = c.stats()
