@@ -110,6 +110,33 @@ def test_host_exchange_one_rank_matches_oracle(host_ctx, name, mode, make, opts)
     assert np.array_equal(_bits(got), _bits(want)), f"{name}: host-exchange one-rank solve differs from the oracle"
 
 
+OPT_CASES = [
+    ("points_exact_engine_2500", "points", lambda: G.random_points(2500, 8, 41, "clumps"), {"points_engine": 1}),
+    ("points_prim_replicated_900", "points", lambda: G.random_points(900, 3, 43, "blobs"), {"variant": 1}),
+    ("points_wide_keys_1200", "points", lambda: G.random_points(1200, 6, 47, "dups"), {"wide_keys": 1}),
+    ("points_widest_1100", "points", lambda: G.random_points(1100, 4, 53, "blobs"), {"sense": -1}),
+    ("weights_widest_700", "weights", lambda: G.random_weights(700, 59, "ties"), {"sense": -1}),
+    ("weights_nocache_600", "weights", lambda: G.random_weights(600, 61, "negative"), {"topk": -1}),
+]
+
+
+@pytest.mark.parametrize("name,mode,make,opts", OPT_CASES, ids=[c[0] for c in OPT_CASES])
+def test_nccl_one_rank_options(P, name, mode, make, opts):
+    """Engine / variant / key / sense options on the NCCL multi-rank path (fresh communicator
+    per context), bit-exact against the oracle (widest: Algorithm 4 in the max-min sense)."""
+    A = make()
+    with P.Context(world=1, rank=0, nccl_id=P.appd_get_nccl_unique_id(), timing=True, timeout_ms=60000,
+                   **opts) as c:
+        got = _solve(c, mode, A)
+        assert c.stats()["collectives"] >= 1
+    sense = opts.get("sense", 1)
+    if mode == "points":
+        want = oracle.appd_weights(oracle.points_weights(A), sense) if sense < 0 else oracle.appd_points(A)
+    else:
+        want = oracle.appd_weights(A, sense)
+    assert np.array_equal(_bits(got), _bits(want)), f"{name}: differs from the oracle"
+
+
 def test_nccl_one_rank_validation_error(P, nccl_ctx):
     """The verdict all-reduce over NCCL: a non-finite input is reported with its first
     offender (a complete graph with finite weights), and the context stays usable."""
