@@ -147,3 +147,30 @@ def test_nccl_one_rank_validation_error(P, nccl_ctx):
     assert e.value.name == "APPD_ERR_NONFINITE" and e.value.index in ((7, 11), (11, 7)), (e.value.name, e.value.index)
     W2 = G.random_weights(300, 6, "uniform")
     assert np.array_equal(_bits(_solve(nccl_ctx, "weights", W2)), _bits(oracle.appd_weights(W2)))
+
+
+def test_failed_exchange_poisons_the_context(P):
+    """A failed exchange (the host_allreduce callback reports an error, as a dead peer's
+    transport would) ends the call with APPD_ERR_NCCL and poisons the context: every later
+    call returns APPD_ERR_POISONED instead of running on an inconsistent state (appd.h
+    error contract).  A fresh context on the same device works again."""
+    n_calls = []
+
+    def broken(words, op):
+        n_calls.append(op)
+        if len(n_calls) >= 2:  # the agreement passes, the next exchange fails
+            raise RuntimeError("peer lost")
+
+    X = G.random_points(700, 3, 67, "blobs")
+    c = P.Context(world=1, rank=0, host_allreduce=broken, variant=P.VARIANT_BORUVKA)
+    try:
+        with pytest.raises(P.AppdError) as e:
+            _solve(c, "points", X)
+        assert e.value.name == "APPD_ERR_NCCL", e.value.name
+        with pytest.raises(P.AppdError) as e2:
+            _solve(c, "points", X)
+        assert e2.value.name == "APPD_ERR_POISONED", e2.value.name
+    finally:
+        c.close()
+    with P.Context() as c2:
+        assert np.array_equal(_bits(_solve(c2, "points", X)), _bits(oracle.appd_points(X)))
