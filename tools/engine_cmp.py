@@ -5,6 +5,8 @@ import torch
 import paper_2407_07058_b200 as P
 from synth import generators as G
 cases = [("C2", None), ("C2", 2048), ("C4", 2048), ("C4", 8192), ("C4", 16384), ("C5", 8192), ("C5", 32768)]
+if len(sys.argv) > 1:  # e.g. C2:4096 C4:3072
+    cases = [(a.split(":")[0], int(a.split(":")[1]) if ":" in a else None) for a in sys.argv[1:]]
 for name, n in cases:
     X = torch.from_numpy(G.config(name, n=n)).cuda()
     nn = X.shape[0]
