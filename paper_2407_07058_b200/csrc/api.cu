@@ -177,6 +177,11 @@ extern "C" appd_status appd_create(appd_ctx** out, const appd_options* opt) {
   }
   for (int i = 0; i < 16; i++) cudaEventCreate(&c->ev[i]);
   c->ev_ready = true;
+  if (c->coll && cudaHostAlloc((void**)&c->pinned_xchg, 32 * sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    appd_destroy(c);
+    return APPD_ERR_OUT_OF_MEMORY;
+  }
   if (cudaHostAlloc((void**)&c->pinned_small, 64 * sizeof(unsigned), cudaHostAllocMapped) != cudaSuccess) {
     cudaGetLastError();
     appd_destroy(c);
@@ -241,6 +246,7 @@ extern "C" void appd_destroy(appd_ctx* c) {
     for (int i = 0; i < 4; i++) cudaEventDestroy(c->sev[i]);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->pinned_small) cudaFreeHost(c->pinned_small);
+  if (c->pinned_xchg) cudaFreeHost(c->pinned_xchg);
   if (c->sink_host) cudaFreeHost(c->sink_host);
   cudaGetLastError();
   delete c;
@@ -358,18 +364,19 @@ static appd_status agree(appd_ctx* c, const float* X, int64_t n, int64_t d, int 
   if (X) {  // points mode: X is replicated, so its checksum must agree too
     appd_status s = launch_checksum_words(c, X, n * d, dv);
     if (s) return s;
-    APPD_CUDA(c, cudaMemcpyAsync(&v[5], dv, sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
+    APPD_CUDA(c, cudaMemcpyAsync(c->pinned_xchg, dv, sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
     APPD_SYNC(c);
+    v[5] = c->pinned_xchg[0];
   }
-  u64 h[2 * NW];
+  u64* h = c->pinned_xchg;  // 2 NW <= 32 pinned words: the copies stay inside the polled waits
   for (int i = 0; i < NW; i++) {
     h[i] = v[i];
     h[NW + i] = ~v[i];
   }
-  APPD_CUDA(c, cudaMemcpyAsync(dv, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  APPD_CUDA(c, cudaMemcpyAsync(dv, h, sizeof(u64) * 2 * NW, cudaMemcpyHostToDevice, c->stream));
   appd_status s = nccl_allreduce_min_u64(c, dv, 2 * NW);
   if (s) return s;
-  APPD_CUDA(c, cudaMemcpyAsync(h, dv, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  APPD_CUDA(c, cudaMemcpyAsync(h, dv, sizeof(u64) * 2 * NW, cudaMemcpyDeviceToHost, c->stream));
   APPD_SYNC(c);
   static const char* what[NW] = {"n", "d", "entry point / world", "options (sense, validate, metric, engine, dendrogram, variant)",
                                  "options (topk, finish_k)", "the checksum of X", "options (list_cap)"};
@@ -655,10 +662,13 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       // every rank must agree on the verdict (else the others would hang in the next collective)
       u64* agree = (u64*)ws(c, S_TMP, sizeof(u64) * 3);
       if (!agree) return fail(c, APPD_ERR_OUT_OF_MEMORY, "validation buffer");
-      APPD_CUDA(c, cudaMemcpyAsync(agree, hb, sizeof hb, cudaMemcpyHostToDevice, c->stream));
+      u64* hx = c->pinned_xchg;
+      memcpy(hx, hb, sizeof hb);
+      APPD_CUDA(c, cudaMemcpyAsync(agree, hx, sizeof hb, cudaMemcpyHostToDevice, c->stream));
       if ((s = nccl_allreduce_min_u64(c, agree, 3))) return s;
-      APPD_CUDA(c, cudaMemcpyAsync(hb, agree, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
+      APPD_CUDA(c, cudaMemcpyAsync(hx, agree, sizeof hb, cudaMemcpyDeviceToHost, c->stream));
       APPD_SYNC(c);
+      memcpy(hb, hx, sizeof hb);
     }
     if ((s = report_validation(c, hb, n, points, d))) return s;
   }
@@ -819,13 +829,13 @@ static appd_status solve_impl(appd_ctx* c, const float* W, const float* X, int64
       if (c->coll) {  // every rank must take the same branch
         u64* flag = (u64*)ws(c, S_TMP, sizeof(u64));
         if (!flag) return fail(c, APPD_ERR_OUT_OF_MEMORY, "flag");
-        const u64 hf = ovf ? 1 : 0;
-        APPD_CUDA(c, cudaMemcpyAsync(flag, &hf, sizeof hf, cudaMemcpyHostToDevice, c->stream));
+        u64* hx = c->pinned_xchg;
+        hx[0] = ovf ? 1 : 0;
+        APPD_CUDA(c, cudaMemcpyAsync(flag, hx, sizeof(u64), cudaMemcpyHostToDevice, c->stream));
         if ((s = nccl_allreduce_max_u64(c, flag, 1))) return s;
-        u64 hf2 = 0;
-        APPD_CUDA(c, cudaMemcpyAsync(&hf2, flag, sizeof hf2, cudaMemcpyDeviceToHost, c->stream));
+        APPD_CUDA(c, cudaMemcpyAsync(hx, flag, sizeof(u64), cudaMemcpyDeviceToHost, c->stream));
         APPD_SYNC(c);
-        ovf = hf2 != 0;
+        ovf = hx[0] != 0;
         if (!ovf && (s = nccl_allreduce_min_u64(c, WCM, k * k))) return s;
       }
       if (!ovf) {

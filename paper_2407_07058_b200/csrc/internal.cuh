@@ -123,6 +123,9 @@ struct appd_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   unsigned* pinned_small = nullptr;  // 64 words of pinned host memory for small async reads
+  // 32 pinned words for the host side of the collectives' small exchanges (agreement, verdict,
+  // branch flag): a device->pageable copy would block outside the deadline-polled wait
+  unsigned long long* pinned_xchg = nullptr;
   // the same words as the device sees them (mapped pinned memory): small device results are
   // published there by one kernel per synchronisation instead of one copy each (publish())
   unsigned* pinned_small_dev = nullptr;

@@ -174,3 +174,34 @@ def test_failed_exchange_poisons_the_context(P):
         c.close()
     with P.Context() as c2:
         assert np.array_equal(_bits(_solve(c2, "points", X)), _bits(oracle.appd_points(X)))
+
+
+@pytest.mark.timeout(300)
+def test_nccl_deadline_aborts_and_poisons(P):
+    """The deadline of the NCCL backend's polled waits (appd_options.timeout_ms; SURVEY
+    §8(b): a dead or diverged peer must end the call, not hang it).  GPU work queued ahead
+    of the solve on the stream the library follows (a ~1.5 s spin kernel) stands in for a
+    peer that never arrives: the first polled wait passes timeout_ms = 100, the library
+    aborts the communicator (ncclCommAbort) and returns APPD_ERR_NCCL, and the context is
+    poisoned.  The process and the device stay usable."""
+    X = G.random_points(3000, 4, 71, "blobs")
+    t = torch.from_numpy(X).cuda()
+    torch.cuda.synchronize()
+    c = P.Context(world=1, rank=0, nccl_id=P.appd_get_nccl_unique_id(), timeout_ms=100,
+                  variant=P.VARIANT_BORUVKA)
+    M = torch.empty((X.shape[0], X.shape[0]), dtype=torch.float32, device="cuda")
+    try:
+        c.solve_points(t, M)  # workspace allocated now (a cudaFree would wait for the spin)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(int(3e9))  # ~1.5 s at 1.97 GHz on torch's current stream
+        with pytest.raises(P.AppdError) as e:
+            c.solve_points(t, M)
+        assert e.value.name == "APPD_ERR_NCCL" and "timeout_ms" in str(e.value), str(e.value)
+        with pytest.raises(P.AppdError) as e2:
+            c.solve_points(t, M)
+        assert e2.value.name == "APPD_ERR_POISONED", e2.value.name
+    finally:
+        torch.cuda.synchronize()
+        c.close()
+    with P.Context() as c2:
+        assert np.array_equal(_bits(_solve(c2, "points", X)), _bits(oracle.appd_points(X)))
