@@ -24,6 +24,9 @@ namespace appd {
 void* ws(appd_ctx* c, int slot, size_t bytes) {
   DevBuf& b = c->buf[slot];
   if (b.bytes >= bytes && b.p) return b.p;
+  // cudaFree waits for the whole device: with NCCL collectives queued, wait on the stream
+  // through the deadline-polled path first (a missing peer must not hang the free)
+  if (b.p && c->coll && c->nccl_comm && sync_stream(c) != APPD_OK) return nullptr;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.bytes = 0;
@@ -62,6 +65,9 @@ appd_status fail(appd_ctx* c, appd_status s, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(msg, sizeof msg, fmt, ap);
   va_end(ap);
+  // after an NCCL abort (deadline or asynchronous error) keep its status and message: a
+  // caller reporting the failed step (e.g. a workspace growth that waited) is secondary
+  if (c && c->nccl_aborted) return APPD_ERR_NCCL;
   if (c) c->last_error = msg;
   return s;
 }

@@ -105,6 +105,7 @@ struct appd_ctx {
   // the solve takes the multi-rank path (every exchange a collective): world > 1, or world 1
   // with an explicit communicator (nccl_unique_id) or host exchange (host_allreduce)
   bool coll = false;
+  bool nccl_aborted = false;  // set by the NCCL abort path (the context is poisoned too)
   int sm_count = 148;
   // workspace (grown on demand)
   appd::DevBuf buf[96];

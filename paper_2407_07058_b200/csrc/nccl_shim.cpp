@@ -95,7 +95,9 @@ static appd_status nccl_abort(appd_ctx* c, const char* why) {
   if (c->nccl_comm && g_nccl.commAbort) g_nccl.commAbort((ncclComm_t)c->nccl_comm);
   c->nccl_comm = nullptr;
   c->poisoned = true;
-  return fail(c, APPD_ERR_NCCL, "%s", why);
+  appd_status s = fail(c, APPD_ERR_NCCL, "%s", why);
+  c->nccl_aborted = true;
+  return s;
 }
 
 // Wait for the context stream.  One rank, or the host exchange backend (whose callback
